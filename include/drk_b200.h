@@ -1,0 +1,200 @@
+/* drk_b200.h — C-ABI of the B200-native DRK splatting rasterizer.
+ *
+ * This is the drop-in boundary for the reference's render / backward_render
+ * path.  The reference exposes a C++ API only; each entry
+ * point below cites the reference interface it replaces.  No C++ types, no
+ * exceptions: every call returns a drk_status whose non-zero values map 1:1
+ * onto the reference's drk::Error subclasses (reference include/drk/errors.hpp)
+ * plus CUDA / allocation / argument failures.
+ *
+ * Data layout at the boundary
+ *   raw parameters  float32, scalar-major SoA: raw[s * n + i] is scalar s of
+ *                   primitive i, s in drk::for_each_scalar order
+ *                   (reference types.hpp:48-72): center(3), quat(4, w first),
+ *                   scale_raw(K), angle_raw(K), eta_raw, tau_raw, opacity_raw,
+ *                   sh_raw(terms x 3, coefficient-major then RGB).
+ *                   S = drk_scalar_count(K, terms) = 3 + 4 + 2K + 3 + 3*terms.
+ *   activated       drk_prims (below): fp64 centre/rotation/shape, f32 SH.
+ *   images          float32, row-major, interleaved channels, H x W x C
+ *                   (same shapes as drk::FrameBuffers, reference raster.hpp:57-63).
+ *   gradients       same layout as the raw parameters (drk::ParamGrads::raw,
+ *                   reference grad.hpp:48-53).
+ * Device pointers unless a function name ends in _host.  Calls are ordered on
+ * the given CUDA stream (NULL = the context's stream).
+ */
+#ifndef DRK_B200_H
+#define DRK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DRK_ABI_VERSION 1
+
+typedef enum drk_status {
+  DRK_OK = 0,
+  DRK_ERR_GENERIC = 1,            /* drk::Error */
+  DRK_ERR_NONFINITE = 2,          /* drk::NonFiniteError (core.cpp:134) */
+  DRK_ERR_DEGENERATE_QUAT = 3,    /* drk::DegenerateQuaternionError (geometry.cpp:23) */
+  DRK_ERR_DEGENERATE_BASIS = 4,   /* drk::DegenerateBasisError (core.cpp:191) */
+  DRK_ERR_REPLAY_MISMATCH = 5,    /* drk::ReplayMismatchError (grad.cpp:311-314) */
+  DRK_ERR_DIMENSION = 6,          /* drk::DimensionMismatchError */
+  DRK_ERR_INVALID_ARG = 7,
+  DRK_ERR_CUDA = 8,
+  DRK_ERR_OOM = 9,
+  DRK_ERR_UNSUPPORTED = 10
+} drk_status;
+
+/* drk::Camera (reference geometry.hpp:9-19). */
+typedef struct drk_camera {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double R[9]; /* world->camera rotation, row-major */
+  double t[3]; /* world->camera translation */
+} drk_camera;
+
+/* drk::RenderOptions + drk::KernelConfig (reference raster.hpp:81-90,
+ * types.hpp:100-105).  presort: 0 None, 1 CenterDepth, 2 NearestDepth.
+ * `threads` is accepted for API parity and ignored (the GPU path is
+ * deterministic by construction).  record_replay > 0 keeps up to that many
+ * blend records per pixel for drk_get_replay (the ReplayBuffer* argument of
+ * drk::render; small images only). */
+typedef struct drk_options {
+  double lowpass_radius;            /* s_l, pixels (default 0.5) */
+  double alpha_min;                 /* default 1/255 */
+  double grazing_eps;               /* default 1e-6 */
+  double background[3];             /* default (1,1,1) */
+  double early_stop_transmittance;  /* default 1e-4 */
+  int32_t sh_degree;                /* default 3 */
+  int32_t use_cache;                /* default 1 */
+  int32_t exact_sort;               /* default 0 */
+  int32_t presort;                  /* default 2 */
+  int32_t threads;                  /* ignored */
+  int32_t record_replay;            /* default 0 */
+} drk_options;
+
+/* Activated primitives (drk::DrkPrimitive, reference types.hpp:77-98), all
+ * device pointers, primitive-major.  rot is row-major per primitive; its
+ * columns are the local axes R_x, R_y, R_z.  sh may be NULL (then terms=0). */
+typedef struct drk_prims {
+  const double* mu;       /* n x 3 */
+  const double* rot;      /* n x 9 */
+  const double* scales;  /* n x K */
+  const double* angles;  /* n x K, strictly increasing, angles[K-1] == 2 pi */
+  const double* eta;     /* n */
+  const double* tau;     /* n */
+  const double* opacity; /* n */
+  const float* sh;       /* n x terms x 3 */
+} drk_prims;
+
+/* Frame gradients (drk::FrameGrad, reference grad.hpp:40-45); NULL = empty. */
+typedef struct drk_frame_grad {
+  const float* d_color;  /* H x W x 3 */
+  const float* d_depth;  /* H x W */
+  const float* d_normal; /* H x W x 3 */
+  const float* d_alpha;  /* H x W */
+} drk_frame_grad;
+
+/* Work counters of the last forward (algorithmic-work accounting). */
+typedef struct drk_stats {
+  int64_t primitives;      /* primitives binned (visible at alpha_min) */
+  int64_t pairs;           /* tile-list entries */
+  int64_t streamed;        /* (pixel, candidate) intersections until saturation */
+  int64_t popped;          /* cache pops (alpha evaluations, incl. cheap rejects) */
+  int64_t composited;      /* blended entries */
+  int64_t near_ties;       /* binning decisions within 1e-9 relative of a tie */
+  int64_t poly_overflow;   /* primitives that needed the large-polygon path */
+  int64_t replay_overflow; /* pixels whose replay exceeded record_replay */
+} drk_stats;
+
+typedef struct drk_ctx drk_ctx;
+
+/* --- context ------------------------------------------------------------ */
+int drk_ctx_create(int device, drk_ctx** out);
+void drk_ctx_destroy(drk_ctx* ctx);
+const char* drk_status_string(int status);
+const char* drk_last_error(const drk_ctx* ctx);
+int drk_abi_version(void);
+int drk_scalar_count(int k, int sh_terms);
+void drk_default_options(drk_options* opt);
+int drk_get_stats(const drk_ctx* ctx, drk_stats* out);
+int drk_set_stream(drk_ctx* ctx, void* cuda_stream);
+
+/* --- activation (reference core.cpp:133-146 activate) -------------------- */
+/* raw (f32 SoA) -> activated fp64 arrays owned by the context; the pointers
+ * stay valid until the next call that activates.  Throws the reference's
+ * NonFinite / DegenerateQuaternion errors as status codes. */
+int drk_activate(drk_ctx* ctx, const float* raw, int n, int k, int sh_terms, drk_prims* out);
+
+/* --- forward (reference raster.hpp:92-93 render; raster.hpp:30-31
+ * bin_primitives) ---------------------------------------------------------- */
+/* From raw parameters (activation on device).  Outputs may be NULL. */
+int drk_forward(drk_ctx* ctx, const float* raw, int n, int k, int sh_terms,
+                const drk_camera* cam, const drk_options* opt, float* color, float* depth,
+                float* normal, float* alpha);
+/* From activated primitives (the reference's std::vector<DrkPrimitive> input). */
+int drk_forward_prims(drk_ctx* ctx, const drk_prims* prims, int n, int k, int sh_terms,
+                      const drk_camera* cam, const drk_options* opt, float* color,
+                      float* depth, float* normal, float* alpha);
+/* Host-buffer variant of drk_forward: copies raw in, renders, copies images
+ * out (any output may be NULL); synchronous. */
+int drk_forward_host(drk_ctx* ctx, const float* raw_host, int n, int k, int sh_terms,
+                     const drk_camera* cam, const drk_options* opt, float* color_host,
+                     float* depth_host, float* normal_host, float* alpha_host);
+
+/* Tile lists of the last forward (drk::TileBinning): per-tile offsets
+ * (tiles_x*tiles_y + 1), primitive ids and f64 presort keys, in the
+ * reference's per-tile (key, prim_id) order.  Host pointers; pass NULL to
+ * query sizes only. */
+int drk_get_tile_lists(drk_ctx* ctx, int64_t* total_pairs, int64_t* offsets_host,
+                       int32_t* ids_host, double* keys_host);
+/* Replay of the last forward with record_replay > 0 (drk::ReplayBuffer):
+ * per-pixel offsets (H*W + 1), prim ids and 5 doubles per record
+ * (u, v, depth, alpha, lowpass_active).  Host pointers; NULL to query. */
+int drk_get_replay(drk_ctx* ctx, int64_t* total_records, int64_t* offsets_host,
+                   int32_t* ids_host, double* vals_host);
+
+/* --- backward (reference grad.hpp:58-61 backward_render) ----------------- */
+/* Uses the state of the last drk_forward / drk_forward_prims call on this
+ * context (its binning and per-pixel accumulators stand in for the
+ * ReplayBuffer).  Camera dimensions / n must match it, else
+ * DRK_ERR_REPLAY_MISMATCH.  grad_raw (SoA, like raw) receives the raw-space
+ * gradient; with accumulate != 0 it is added to instead of overwritten
+ * (multi-view batches).  d_center_world (n x 3), screen_grad (n), touched (n)
+ * may be NULL.  deterministic != 0 selects the fixed-order reduction. */
+int drk_backward(drk_ctx* ctx, const float* raw, const drk_frame_grad* fg, float* grad_raw,
+                 float* d_center_world, float* screen_grad, uint8_t* touched, int accumulate,
+                 int deterministic);
+/* Activated-space gradients (drk::PrimGrads, reference grad.hpp:19-29) of the
+ * last backward, fp64, n x G with G = 3 + 9 + 2K + 3 + 3*terms in the order
+ * d_center, d_rot (row-major), d_scales, d_angles, d_eta, d_tau, d_opacity,
+ * d_sh.  Device pointer owned by the context. */
+int drk_get_prim_grads(drk_ctx* ctx, const double** grads, int* stride);
+
+/* --- loss and optimizer (reference optimize.cpp:171-204, :226-307) -------- */
+/* L1 branch of drk::loss (dssim_weight = 0): loss_out (device, 1 double)
+ * receives mean |r - t|, d_color = sign(r - t) / (3 W H). */
+int drk_l1_loss(drk_ctx* ctx, const float* rendered, const float* target, int width, int height,
+                double* loss_out, float* d_color);
+
+/* drk::TrainConfig learning-rate fields used by adam_step. */
+typedef struct drk_adam_config {
+  double lr_drk, lr_position, lr_rotation, lr_opacity, lr_sh;
+  int32_t steps;             /* schedule length (TrainConfig::steps) */
+  int32_t freeze_eta_tau, freeze_angles;
+  int32_t pad_;
+  double scene_extent;
+  double grad_scale;         /* gradients are multiplied by this first (1/views) */
+} drk_adam_config;
+/* drk::adam_step on SoA f32 params / grads / moments.  *step is
+ * OptState::step (host value, incremented). */
+int drk_adam_step(drk_ctx* ctx, float* params, const float* grads, float* m, float* v, int n,
+                  int k, int sh_terms, int64_t* step, const drk_adam_config* cfg);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DRK_B200_H */

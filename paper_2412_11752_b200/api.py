@@ -1,0 +1,396 @@
+"""Host-side mirror of the reference's render / backward_render interface.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(include/drk/raster.hpp, grad.hpp, optimize.hpp), over the C-ABI of
+include/drk_b200.h.  PyTorch supplies device memory and streams; all compute
+runs in libdrk_b200.so.  Parameters are the reference's RawDrkParams records
+in the ABI's scalar-major SoA layout (``raw[s, i]``, for_each_scalar order,
+float32), device-resident between calls.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (DegenerateBasisError, DegenerateQuaternionError, DimensionMismatchError,  # noqa: F401
+                   DrkError, NonFiniteError, ReplayMismatchError)
+from .scenes import Camera, scalar_count, sh_terms  # noqa: F401
+
+
+class PresortMode(enum.IntEnum):
+    """reference raster.hpp:12"""
+
+    None_ = 0
+    CenterDepth = 1
+    NearestDepth = 2
+
+
+@dataclass
+class KernelConfig:
+    """reference types.hpp:100-105"""
+
+    basis_count: int = 8
+    lowpass_radius: float = 0.5
+    alpha_min: float = 1.0 / 255.0
+    grazing_eps: float = 1e-6
+
+
+@dataclass
+class RenderOptions:
+    """reference raster.hpp:81-90 (``threads`` accepted, ignored: deterministic by construction)."""
+
+    kernel: KernelConfig = field(default_factory=KernelConfig)
+    background: tuple = (1.0, 1.0, 1.0)
+    threads: int = 1
+    sh_degree: int = 3
+    use_cache: bool = True
+    exact_sort: bool = False
+    presort: PresortMode = PresortMode.NearestDepth
+    early_stop_transmittance: float = 1e-4
+
+
+@dataclass
+class FrameBuffers:
+    """reference raster.hpp:57-63 (float32 device tensors, H x W x C)."""
+
+    color: torch.Tensor
+    depth: torch.Tensor
+    normal: torch.Tensor
+    alpha: torch.Tensor
+    background: tuple = (1.0, 1.0, 1.0)
+
+
+@dataclass
+class TileBinning:
+    """reference raster.hpp:19-26 as CSR arrays: tile t holds ids[offsets[t]:offsets[t+1]]."""
+
+    tiles_x: int
+    tiles_y: int
+    offsets: np.ndarray
+    prim_ids: np.ndarray
+    keys: np.ndarray
+    tile_size: int = 16
+
+    def tile(self, tx: int, ty: int):
+        t = ty * self.tiles_x + tx
+        s, e = self.offsets[t], self.offsets[t + 1]
+        return list(zip(self.prim_ids[s:e].tolist(), self.keys[s:e].tolist()))
+
+
+@dataclass
+class ReplayBuffer:
+    """reference raster.hpp:66-79 as CSR arrays; vals columns: u, v, depth, alpha, lowpass_active."""
+
+    width: int
+    height: int
+    offsets: np.ndarray
+    prim_ids: np.ndarray
+    vals: np.ndarray
+
+    def at(self, x: int, y: int):
+        p = y * self.width + x
+        s, e = self.offsets[p], self.offsets[p + 1]
+        return [dict(prim_id=int(i), u=v[0], v=v[1], depth=v[2], alpha=v[3], lowpass_active=bool(v[4]))
+                for i, v in zip(self.prim_ids[s:e], self.vals[s:e])]
+
+
+@dataclass
+class FrameGrad:
+    """reference grad.hpp:39-45; None = empty image."""
+
+    d_color: torch.Tensor | None = None
+    d_depth: torch.Tensor | None = None
+    d_normal: torch.Tensor | None = None
+    d_alpha: torch.Tensor | None = None
+
+
+@dataclass
+class ParamGrads:
+    """reference grad.hpp:48-53 (raw in the SoA layout of the parameters)."""
+
+    raw: torch.Tensor
+    d_center_world: torch.Tensor
+    screen_grad: torch.Tensor
+    touched: torch.Tensor
+
+
+@dataclass
+class TrainConfig:
+    """Learning-rate fields of reference optimize.hpp:30-61 used by adam_step."""
+
+    steps: int = 35000
+    lr_drk: float = 5e-3
+    lr_position: float = 1.6e-4
+    lr_rotation: float = 1e-3
+    lr_opacity: float = 5e-2
+    lr_sh: float = 2.5e-3
+    freeze_eta_tau: bool = False
+    freeze_angles: bool = False
+
+
+@dataclass
+class OptState:
+    """reference optimize.hpp:64-70 (SoA moments on the device)."""
+
+    m: torch.Tensor
+    v: torch.Tensor
+    step: int = 0
+
+    @staticmethod
+    def zeros_like(params: torch.Tensor) -> "OptState":
+        return OptState(torch.zeros_like(params), torch.zeros_like(params), 0)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _camera(cam: Camera) -> _lib.Camera_:
+    c = _lib.Camera_()
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    c.width, c.height = int(cam.width), int(cam.height)
+    R = np.asarray(cam.R, dtype=np.float64).reshape(9)
+    t = np.asarray(cam.t, dtype=np.float64).reshape(3)
+    for i in range(9):
+        c.R[i] = R[i]
+    for i in range(3):
+        c.t[i] = t[i]
+    return c
+
+
+def _options(opt: RenderOptions, replay_cap: int = 0) -> _lib.Options_:
+    o = _lib.Options_()
+    o.lowpass_radius, o.alpha_min, o.grazing_eps = (opt.kernel.lowpass_radius, opt.kernel.alpha_min,
+                                                    opt.kernel.grazing_eps)
+    for i in range(3):
+        o.background[i] = float(opt.background[i])
+    o.early_stop_transmittance = opt.early_stop_transmittance
+    o.sh_degree, o.use_cache, o.exact_sort = opt.sh_degree, int(opt.use_cache), int(opt.exact_sort)
+    o.presort, o.threads, o.record_replay = int(opt.presort), int(opt.threads), int(replay_cap)
+    return o
+
+
+class Rasterizer:
+    """One drk_ctx (device scratch + stream-ordered state of the last forward)."""
+
+    def __init__(self, device: int | torch.device | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2412_11752_b200 needs a CUDA device (no CPU fallback)")
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                           (device.index if isinstance(device, torch.device) else device))
+        self.device = dev
+        self._h = C.c_void_p()
+        _lib.check(_lib.lib().drk_ctx_create(dev.index, C.byref(self._h)))
+        self._shape = None
+
+    def close(self):
+        if self._h:
+            _lib.lib().drk_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        _lib.check(st, self._h)
+
+    def _sync_stream(self):
+        _lib.check(_lib.lib().drk_set_stream(self._h, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+
+    def _raw(self, raw) -> torch.Tensor:
+        if isinstance(raw, np.ndarray):
+            raw = torch.from_numpy(np.ascontiguousarray(raw, dtype=np.float32))
+        return raw.to(self.device, torch.float32).contiguous()
+
+    # --- forward -------------------------------------------------------
+    def render(self, raw, cam: Camera, opt: RenderOptions = None, k: int = 8, sh_degree: int | None = None,
+               replay: bool | int = False, outputs=("color", "depth", "normal", "alpha")) -> FrameBuffers:
+        """drk::render (reference raster.hpp:92-93) from raw parameters (activation included).
+
+        ``replay`` (True or a per-pixel capacity) records the blend lists, read back with
+        :meth:`replay_buffer`.
+        """
+        opt = opt or RenderOptions()
+        raw = self._raw(raw)
+        S, n = raw.shape
+        terms = (S - (3 + 4 + 2 * k + 3)) // 3
+        if scalar_count(k, terms) != S:
+            raise DimensionMismatchError(f"raw has {S} scalars, not scalar_count({k}, terms)")
+        H, W = cam.height, cam.width
+        kw = dict(device=self.device, dtype=torch.float32)
+        fb = FrameBuffers(torch.empty(H, W, 3, **kw) if "color" in outputs else None,
+                          torch.empty(H, W, **kw) if "depth" in outputs else None,
+                          torch.empty(H, W, 3, **kw) if "normal" in outputs else None,
+                          torch.empty(H, W, **kw) if "alpha" in outputs else None, tuple(opt.background))
+        cap = (256 if replay is True else int(replay)) if replay else 0
+        self._sync_stream()
+        self._check(_lib.lib().drk_forward(self._h, _ptr(raw), n, k, terms, C.byref(_camera(cam)),
+                                           C.byref(_options(opt, cap)), _ptr(fb.color), _ptr(fb.depth),
+                                           _ptr(fb.normal), _ptr(fb.alpha)))
+        self._shape = (n, k, terms, H, W)
+        return fb
+
+    def render_prims(self, prims: dict, cam: Camera, opt: RenderOptions = None, replay: bool | int = False):
+        """drk::render from activated primitives (dict of device tensors: mu [n,3] f64,
+        rot [n,3,3] f64, scales/angles [n,K] f64, eta/tau/opacity [n] f64, sh [n,terms,3] f32)."""
+        opt = opt or RenderOptions()
+        n, k = prims["scales"].shape
+        sh = prims["sh"].to(self.device, torch.float32).contiguous()
+        terms = sh.shape[1] if sh.numel() else 0
+        keep = {f: prims[f].to(self.device, torch.float64).contiguous()
+                for f in ("mu", "rot", "scales", "angles", "eta", "tau", "opacity")}
+        p = _lib.Prims_(*[C.c_void_p(keep[f].data_ptr()) for f in
+                          ("mu", "rot", "scales", "angles", "eta", "tau", "opacity")], C.c_void_p(sh.data_ptr()))
+        H, W = cam.height, cam.width
+        kw = dict(device=self.device, dtype=torch.float32)
+        fb = FrameBuffers(torch.empty(H, W, 3, **kw), torch.empty(H, W, **kw), torch.empty(H, W, 3, **kw),
+                          torch.empty(H, W, **kw), tuple(opt.background))
+        cap = (256 if replay is True else int(replay)) if replay else 0
+        self._sync_stream()
+        self._check(_lib.lib().drk_forward_prims(self._h, C.byref(p), n, k, terms, C.byref(_camera(cam)),
+                                                 C.byref(_options(opt, cap)), _ptr(fb.color), _ptr(fb.depth),
+                                                 _ptr(fb.normal), _ptr(fb.alpha)))
+        self._keep = (keep, sh)
+        self._shape = (n, k, terms, H, W)
+        return fb
+
+    def render_host(self, raw_host: np.ndarray, cam: Camera, opt: RenderOptions = None, k: int = 8):
+        """Host-buffer entry (drk_forward_host): numpy in, numpy colour/depth/normal/alpha out."""
+        opt = opt or RenderOptions()
+        raw_host = np.ascontiguousarray(raw_host, dtype=np.float32)
+        S, n = raw_host.shape
+        terms = (S - (3 + 4 + 2 * k + 3)) // 3
+        H, W = cam.height, cam.width
+        out = dict(color=np.empty((H, W, 3), np.float32), depth=np.empty((H, W), np.float32),
+                   normal=np.empty((H, W, 3), np.float32), alpha=np.empty((H, W), np.float32))
+        self._check(_lib.lib().drk_forward_host(self._h, raw_host.ctypes.data_as(C.c_void_p), n, k, terms,
+                                                C.byref(_camera(cam)), C.byref(_options(opt)),
+                                                *[out[f].ctypes.data_as(C.c_void_p) for f in
+                                                  ("color", "depth", "normal", "alpha")]))
+        self._shape = (n, k, terms, H, W)
+        return out
+
+    def tile_binning(self) -> TileBinning:
+        """drk::bin_primitives result of the last forward (reference raster.hpp:30-31)."""
+        total = C.c_int64(0)
+        self._check(_lib.lib().drk_get_tile_lists(self._h, C.byref(total), None, None, None))
+        n, k, terms, H, W = self._shape
+        tx, ty = (W + 15) // 16, (H + 15) // 16
+        off = np.zeros(tx * ty + 1, np.int64)
+        ids = np.zeros(total.value, np.int32)
+        keys = np.zeros(total.value, np.float64)
+        self._check(_lib.lib().drk_get_tile_lists(self._h, C.byref(total), off.ctypes.data_as(C.c_void_p),
+                                                  ids.ctypes.data_as(C.c_void_p), keys.ctypes.data_as(C.c_void_p)))
+        return TileBinning(tx, ty, off, ids, keys)
+
+    def bin_primitives(self, raw, cam: Camera, cfg: KernelConfig = None,
+                       presort: PresortMode = PresortMode.NearestDepth, k: int = 8) -> TileBinning:
+        cfg = cfg or KernelConfig()
+        opt = RenderOptions(kernel=cfg, presort=presort)
+        self.render(raw, cam, opt, k=k, outputs=())
+        return self.tile_binning()
+
+    def replay_buffer(self) -> ReplayBuffer:
+        total = C.c_int64(0)
+        self._check(_lib.lib().drk_get_replay(self._h, C.byref(total), None, None, None))
+        n, k, terms, H, W = self._shape
+        off = np.zeros(H * W + 1, np.int64)
+        ids = np.zeros(total.value, np.int32)
+        vals = np.zeros((total.value, 5), np.float64)
+        self._check(_lib.lib().drk_get_replay(self._h, C.byref(total), off.ctypes.data_as(C.c_void_p),
+                                              ids.ctypes.data_as(C.c_void_p), vals.ctypes.data_as(C.c_void_p)))
+        return ReplayBuffer(W, H, off, ids, vals)
+
+    def stats(self) -> dict:
+        s = _lib.Stats_()
+        self._check(_lib.lib().drk_get_stats(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in _lib.Stats_._fields_}
+
+    # --- backward ------------------------------------------------------
+    def backward_render(self, raw, frame_grad: FrameGrad, grad_out: torch.Tensor | None = None,
+                        accumulate: bool = False, deterministic: bool = False) -> ParamGrads:
+        """drk::backward_render (reference grad.hpp:58-61) for the last forward on this rasterizer."""
+        if self._shape is None:
+            raise ReplayMismatchError("backward_render without a forward on this rasterizer")
+        raw = self._raw(raw)
+        n, k, terms, H, W = self._shape
+        if raw.shape[1] != n:
+            raise ReplayMismatchError("raw and activated primitive counts differ")
+        for img, c in ((frame_grad.d_color, 3), (frame_grad.d_depth, 1), (frame_grad.d_normal, 3),
+                       (frame_grad.d_alpha, 1)):
+            if img is not None and img.numel() != H * W * c:
+                raise ReplayMismatchError("frame gradient does not match the camera dimensions")
+
+        def dev(t):
+            return None if t is None else t.to(self.device, torch.float32).contiguous()
+
+        fg_t = [dev(frame_grad.d_color), dev(frame_grad.d_depth), dev(frame_grad.d_normal), dev(frame_grad.d_alpha)]
+        fg = _lib.FrameGrad_(*[_ptr(t) for t in fg_t])
+        g = grad_out if grad_out is not None else torch.zeros_like(raw)
+        dcw = torch.empty(n, 3, device=self.device, dtype=torch.float32)
+        sg = torch.empty(n, device=self.device, dtype=torch.float32)
+        tch = torch.empty(n, device=self.device, dtype=torch.uint8)
+        self._sync_stream()
+        self._check(_lib.lib().drk_backward(self._h, _ptr(raw), C.byref(fg), _ptr(g), _ptr(dcw), _ptr(sg), _ptr(tch),
+                                            int(accumulate), int(deterministic)))
+        return ParamGrads(g, dcw, sg, tch)
+
+    # --- loss / optimizer ---------------------------------------------
+    def l1_loss(self, rendered: torch.Tensor, target: torch.Tensor):
+        """L1 branch of drk::loss (reference optimize.cpp:171-204, dssim_weight = 0)."""
+        if rendered.shape != target.shape:
+            raise DimensionMismatchError("rendered and target shapes differ")
+        H, W = rendered.shape[:2]
+        r = rendered.to(self.device, torch.float32).contiguous()
+        t = target.to(self.device, torch.float32).contiguous()
+        value = torch.empty(1, device=self.device, dtype=torch.float64)
+        d = torch.empty_like(r)
+        self._sync_stream()
+        self._check(_lib.lib().drk_l1_loss(self._h, _ptr(r), _ptr(t), W, H, _ptr(value), _ptr(d)))
+        return value, d
+
+    def adam_step(self, params: torch.Tensor, grads: torch.Tensor, state: OptState, cfg: TrainConfig,
+                  scene_extent: float, k: int = 8, grad_scale: float = 1.0):
+        """drk::adam_step (reference optimize.cpp:259-307), in place on device tensors."""
+        if params.shape != grads.shape or params.shape != state.m.shape:
+            raise DimensionMismatchError("optimizer shapes out of sync")
+        S, n = params.shape
+        terms = (S - (3 + 4 + 2 * k + 3)) // 3
+        a = _lib.AdamConfig_(cfg.lr_drk, cfg.lr_position, cfg.lr_rotation, cfg.lr_opacity, cfg.lr_sh, cfg.steps,
+                             int(cfg.freeze_eta_tau), int(cfg.freeze_angles), 0, float(scene_extent),
+                             float(grad_scale))
+        step = C.c_int64(state.step)
+        self._sync_stream()
+        self._check(_lib.lib().drk_adam_step(self._h, _ptr(params), _ptr(grads), _ptr(state.m), _ptr(state.v), n, k,
+                                             terms, C.byref(step), C.byref(a)))
+        state.step = step.value
+
+
+_default: dict[int, Rasterizer] = {}
+
+
+def default_rasterizer(device: int | None = None) -> Rasterizer:
+    idx = torch.cuda.current_device() if device is None else device
+    if idx not in _default:
+        _default[idx] = Rasterizer(idx)
+    return _default[idx]
+
+
+def render(raw, cam: Camera, opt: RenderOptions = None, k: int = 8, replay: bool | int = False) -> FrameBuffers:
+    return default_rasterizer().render(raw, cam, opt, k=k, replay=replay)
+
+
+def bin_primitives(raw, cam: Camera, cfg: KernelConfig = None, presort=PresortMode.NearestDepth, k: int = 8):
+    return default_rasterizer().bin_primitives(raw, cam, cfg, presort, k=k)
+
+
+def backward_render(raw, frame_grad: FrameGrad, **kw) -> ParamGrads:
+    return default_rasterizer().backward_render(raw, frame_grad, **kw)

@@ -1,0 +1,543 @@
+// C-ABI (include/drk_b200.h) and the host-side orchestration of one view:
+// activate -> K1 prep -> scan -> K2 rows -> scan -> K3 emit -> radix sort ->
+// tile offsets -> K4 raster; backward: K5 raster-bwd -> K6 activation bwd.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "drk_internal.h"
+
+namespace drk {
+
+// kernels defined in the other translation units
+__global__ void k_prep0(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pool,
+                        long long pool_cap, int* rowcnt, unsigned long long* counters, const int* list, int list_n,
+                        double2* scratch, int scratch_cap, int* overflow);
+__global__ void k_prep1(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pool,
+                        long long pool_cap, int* rowcnt, unsigned long long* counters, const int* list, int list_n,
+                        double2* scratch, int scratch_cap, int* overflow);
+__global__ void k_rows(int n, const int4* bbox, const int2* hullref, const double2* pool, const long long* rowoff,
+                       CamD cam, OptD opt, int4* rows, int* rowpaircnt, unsigned long long* counters);
+__global__ void k_tile_rays(CamD cam, double* cdirs, double* tdirs);
+__global__ void k_emit(long long n_rows, const int4* rows, const long long* rowpairoff, const Geo* geo,
+                       const double* cdirs, const double* tdirs, CamD cam, OptD opt, unsigned long long* pk,
+                       unsigned long long* pv, int* tilecnt);
+template <typename T>
+int exclusive_scan(drk_ctx* c, const T* in, long long n, long long* out, long long* total);
+int sort_pairs(drk_ctx* c, unsigned long long*& k, unsigned long long*& v, unsigned long long*& k2,
+               unsigned long long*& v2, long long n);
+void launch_act_bwd(int n, int K, int terms, const float* raw, const double* gact, int G,
+                    const unsigned char* touched_dev, const Geo* geo, const CamD& cam, float* grad_raw,
+                    float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
+                    cudaStream_t s);
+void launch_l1(long long n, const float* r, const float* t, double* loss, float* dcol, cudaStream_t s);
+
+void* ensure_bytes(DevBuf& b, size_t bytes) {
+  if (b.bytes >= bytes && b.p) return b.p;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  size_t want = bytes + bytes / 4 + 256;
+  if (cudaMalloc(&b.p, want) != cudaSuccess) {
+    cudaGetLastError();
+    b.p = nullptr;
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      b.p = nullptr;
+      return nullptr;
+    }
+    want = bytes;
+  }
+  b.bytes = want;
+  return b.p;
+}
+
+void release(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+int set_error(drk_ctx* c, int status, const std::string& msg) {
+  if (c) c->err = msg;
+  return status;
+}
+
+int cuda_check(drk_ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return DRK_OK;
+  cudaGetLastError();
+  return set_error(c, e == cudaErrorMemoryAllocation ? DRK_ERR_OOM : DRK_ERR_CUDA,
+                   std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+static CamD make_cam(const drk_camera* c) {
+  CamD d;
+  d.fx = c->fx;
+  d.fy = c->fy;
+  d.cx = c->cx;
+  d.cy = c->cy;
+  for (int i = 0; i < 9; ++i) d.R[i] = c->R[i];
+  for (int i = 0; i < 3; ++i) d.t[i] = c->t[i];
+  // Camera::position (geometry.hpp:15): (-R^T) t, left to right
+  for (int i = 0; i < 3; ++i) {
+    volatile double a = (-c->R[0 + i]) * c->t[0];
+    volatile double b = (-c->R[3 + i]) * c->t[1];
+    volatile double s = a + b;
+    volatile double e = (-c->R[6 + i]) * c->t[2];
+    d.o[i] = s + e;
+  }
+  d.W = c->width;
+  d.H = c->height;
+  d.tiles_x = (c->width + kTile - 1) / kTile;
+  d.tiles_y = (c->height + kTile - 1) / kTile;
+  return d;
+}
+
+static OptD make_opt(const drk_options* o, int terms) {
+  OptD d;
+  d.lowpass_radius = o->lowpass_radius;
+  d.alpha_min = o->alpha_min;
+  d.grazing_eps = o->grazing_eps;
+  for (int i = 0; i < 3; ++i) d.bg[i] = o->background[i];
+  d.early_stop = o->early_stop_transmittance;
+  d.lp_pad = o->lowpass_radius * std::sqrt(2.0 * std::log(1.0 / o->alpha_min)) + 1e-9;
+  d.sh_degree = o->sh_degree;
+  d.use_cache = o->use_cache;
+  d.exact_sort = o->exact_sort;
+  d.presort = o->presort;
+  d.record_replay = o->record_replay;
+  const int t = (o->sh_degree + 1) * (o->sh_degree + 1);
+  d.terms_active = t < terms ? t : terms;
+  return d;
+}
+
+static RasterParams raster_params(drk_ctx* c) {
+  RasterParams P;
+  std::memset(&P, 0, sizeof P);
+  P.cam = c->camd;
+  P.opt = c->optd;
+  P.tileoff = static_cast<const long long*>(c->tileoff.p);
+  P.pv = static_cast<const unsigned long long*>(c->pv.p);
+  P.geo = static_cast<const Geo*>(c->geo.p);
+  const Activated& A = c->act;
+  P.S = ShapeView{A.s, A.th, A.ex, A.ey, A.det, A.eta, A.tau, A.o, A.K};
+  P.sh = A.sh;
+  P.terms = A.terms;
+  P.counters = static_cast<unsigned long long*>(c->counters.p);
+  return P;
+}
+
+static int read_counters(drk_ctx* c, unsigned long long* h) {
+  cudaMemcpyAsync(h, c->counters.p, sizeof(unsigned long long) * C_COUNT, cudaMemcpyDeviceToHost, c->stream);
+  return cuda_check(c, cudaStreamSynchronize(c->stream), "counters");
+}
+
+int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float* color, float* depth,
+                float* normal, float* alpha) {
+  const Activated& A = c->act;
+  if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0) || !(cam->fy > 0))
+    return set_error(c, DRK_ERR_INVALID_ARG, "invalid camera");
+  if (A.K < 3 || A.K > kMaxK) return set_error(c, DRK_ERR_UNSUPPORTED, "K must be in [3, 16]");
+  cudaStream_t s = c->stream;
+  c->cam = *cam;
+  c->opt = *opt;
+  c->camd = make_cam(cam);
+  c->optd = make_opt(opt, A.terms);
+  const CamD& cd = c->camd;
+  const OptD& od = c->optd;
+  const int n = A.n;
+  const int n_tiles = cd.tiles_x * cd.tiles_y;
+  const long long n_pix = (long long)cam->width * cam->height;
+  unsigned long long* ctr = ensure<unsigned long long>(c->counters, C_COUNT);
+  Geo* geo = ensure<Geo>(c->geo, n);
+  int4* bbox = ensure<int4>(c->bbox, n);
+  int2* hullref = ensure<int2>(c->hullref, n);
+  int* rowcnt = ensure<int>(c->rowcnt, n + 1);
+  long long* rowoff = ensure<long long>(c->rowoff, n + 1);
+  if (!ctr || !geo || !bbox || !hullref || !rowcnt || !rowoff) return set_error(c, DRK_ERR_OOM, "prep buffers");
+  static_assert(sizeof(Geo) % 8 == 0, "Geo alignment");
+  if (c->hull_cap < (long long)n * 96 + 1024) c->hull_cap = (long long)n * 96 + 1024;
+  // K1 with retry on hull-pool overflow
+  DevBuf& ovf_buf = c->rows;  // reused as overflow list before rows are built
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    double2* pool = ensure<double2>(c->hull, (size_t)c->hull_cap);
+    int* ovf = ensure<int>(ovf_buf, n + 1);
+    if (!pool || !ovf) return set_error(c, DRK_ERR_OOM, "hull pool");
+    cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT, s);
+    if (n > 0)
+      k_prep0<<<(n + 127) / 128, 128, 0, s>>>(A, cd, od, geo, bbox, hullref, pool, c->hull_cap, rowcnt, ctr,
+                                                nullptr, 0, nullptr, 0, ovf);
+    unsigned long long h[C_COUNT];
+    if (int st = read_counters(c, h)) return st;
+    const long long n_ovf = (long long)h[C_POLY_OVERFLOW];
+    if (n_ovf > 0) {
+      // large-polygon path: 64k-vertex scratch per primitive, batches of 256
+      const int cap = 65536;
+      std::vector<int> list(n_ovf);
+      cudaMemcpyAsync(list.data(), ovf, sizeof(int) * n_ovf, cudaMemcpyDeviceToHost, s);
+      if (int st = cuda_check(c, cudaStreamSynchronize(s), "overflow list")) return st;
+      DevBuf scratch, dlist;
+      const int batch = 256;
+      double2* scr = ensure<double2>(scratch, (size_t)batch * 2 * (cap + 2));
+      int* dl = ensure<int>(dlist, n_ovf);
+      if (!scr || !dl) return set_error(c, DRK_ERR_OOM, "large polygon scratch");
+      cudaMemcpyAsync(dl, list.data(), sizeof(int) * n_ovf, cudaMemcpyHostToDevice, s);
+      for (long long b = 0; b < n_ovf; b += batch) {
+        const int cnt = (int)std::min<long long>(batch, n_ovf - b);
+        k_prep1<<<(cnt + 127) / 128, 128, 0, s>>>(A, cd, od, geo, bbox, hullref, pool, c->hull_cap, rowcnt, ctr,
+                                                    dl + b, cnt, scr, cap, ovf);
+      }
+      cudaStreamSynchronize(s);
+      release(scratch);
+      release(dlist);
+      if (int st = read_counters(c, h)) return st;
+      if (h[C_POLY_FAIL]) return set_error(c, DRK_ERR_UNSUPPORTED, "support polygon above 65536 vertices");
+    }
+    if ((long long)h[C_HULL_POOL] <= c->hull_cap) {
+      c->stats.poly_overflow = n_ovf;
+      c->stats.primitives = (int64_t)h[C_VISIBLE];
+      break;
+    }
+    c->hull_cap = (long long)h[C_HULL_POOL] + (long long)h[C_HULL_POOL] / 4 + 1024;
+    if (attempt == 3) return set_error(c, DRK_ERR_OOM, "hull pool retries");
+  }
+  // rows
+  long long n_rows = 0;
+  if (int st = exclusive_scan<int>(c, rowcnt, n, rowoff, &n_rows)) return st;
+  c->n_rows = n_rows;
+  int4* rows = ensure<int4>(c->rows, n_rows + 1);
+  int* rowpaircnt = ensure<int>(c->rowpaircnt, n_rows + 1);
+  long long* rowpairoff = ensure<long long>(c->rowpairoff, n_rows + 1);
+  if (!rows || !rowpaircnt || !rowpairoff) return set_error(c, DRK_ERR_OOM, "row buffers");
+  if (n > 0)
+    k_rows<<<(n + 127) / 128, 128, 0, s>>>(n, bbox, hullref, static_cast<const double2*>(c->hull.p), rowoff, cd,
+                                           od, rows, rowpaircnt, ctr);
+  long long n_pairs = 0;
+  if (int st = exclusive_scan<int>(c, rowpaircnt, n_rows, rowpairoff, &n_pairs)) return st;
+  c->n_pairs = n_pairs;
+  // pairs
+  unsigned long long* pk = ensure<unsigned long long>(c->pk, n_pairs + 1);
+  unsigned long long* pv = ensure<unsigned long long>(c->pv, n_pairs + 1);
+  unsigned long long* pk2 = ensure<unsigned long long>(c->pk2, n_pairs + 1);
+  unsigned long long* pv2 = ensure<unsigned long long>(c->pv2, n_pairs + 1);
+  int* tilecnt = ensure<int>(c->tilecnt, n_tiles + 1);
+  long long* tileoff = ensure<long long>(c->tileoff, n_tiles + 1);
+  double* cdirs = ensure<double>(c->cdirs, 3 * (size_t)(cd.tiles_x + 1) * (cd.tiles_y + 1));
+  double* tdirs = ensure<double>(c->tdirs, 3 * (size_t)n_tiles);
+  if (!pk || !pv || !pk2 || !pv2 || !tilecnt || !tileoff || !cdirs || !tdirs)
+    return set_error(c, DRK_ERR_OOM, "pair buffers");
+  cudaMemsetAsync(tilecnt, 0, sizeof(int) * (n_tiles + 1), s);
+  {
+    const int nr = (cd.tiles_x + 1) * (cd.tiles_y + 1) + n_tiles;
+    k_tile_rays<<<(nr + 127) / 128, 128, 0, s>>>(cd, cdirs, tdirs);
+  }
+  if (n_rows > 0)
+    k_emit<<<(unsigned)((n_rows + 127) / 128), 128, 0, s>>>(n_rows, rows, rowpairoff, geo, cdirs, tdirs, cd, od, pk,
+                                                            pv, tilecnt);
+  if (int st = sort_pairs(c, pk, pv, pk2, pv2, n_pairs)) return st;
+  // keep the sorted arrays in c->pk / c->pv
+  if (pk != c->pk.p) {
+    std::swap(c->pk, c->pk2);
+    std::swap(c->pv, c->pv2);
+  }
+  long long tot = 0;
+  if (int st = exclusive_scan<int>(c, tilecnt, n_tiles + 1, tileoff, &tot)) return st;
+  // per-pixel state / replay
+  double* pxstate = ensure<double>(c->pxstate, 8 * (size_t)n_pix);
+  if (!pxstate) return set_error(c, DRK_ERR_OOM, "pixel state");
+  RasterParams P = raster_params(c);
+  P.color = color;
+  P.depth = depth;
+  P.normal = normal;
+  P.alpha = alpha;
+  P.pxstate = pxstate;
+  if (opt->record_replay > 0) {
+    P.replay_cap = opt->record_replay;
+    P.replay_cnt = ensure<int>(c->replay_cnt, n_pix);
+    P.replay_ids = ensure<int>(c->replay_ids, (size_t)n_pix * P.replay_cap);
+    P.replay_rec = ensure<double>(c->replay_rec, 5 * (size_t)n_pix * P.replay_cap);
+    if (!P.replay_cnt || !P.replay_ids || !P.replay_rec) return set_error(c, DRK_ERR_OOM, "replay buffers");
+  }
+  launch_raster(P, n_tiles, false, s);
+  if (int st = cuda_check(c, cudaGetLastError(), "raster")) return st;
+  unsigned long long h[C_COUNT];
+  if (int st = read_counters(c, h)) return st;
+  c->stats.pairs = n_pairs;
+  c->stats.streamed = (int64_t)h[C_STREAMED];
+  c->stats.popped = (int64_t)h[C_POPPED];
+  c->stats.composited = (int64_t)h[C_COMPOSITED];
+  c->stats.near_ties = (int64_t)h[C_NEAR_TIES];
+  c->stats.replay_overflow = (int64_t)h[C_REPLAY_OVERFLOW];
+  if (h[C_ERR_DEGEN_BASIS]) return set_error(c, DRK_ERR_DEGENERATE_BASIS, "adjacent endpoints nearly collinear");
+  c->has_fwd = true;
+  return DRK_OK;
+}
+
+int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* grad_raw, float* d_center_world,
+                 float* screen_grad, uint8_t* touched, int accumulate, int deterministic) {
+  if (!c->has_fwd) return set_error(c, DRK_ERR_REPLAY_MISMATCH, "backward without a forward on this context");
+  const Activated& A = c->act;
+  const int n = A.n, K = A.K;
+  const int G = 3 + 9 + 2 * K + 3 + 3 * A.terms;
+  cudaStream_t s = c->stream;
+  double* gact = ensure<double>(c->gact, (size_t)G * n + 1);
+  unsigned char* tch = ensure<unsigned char>(c->touched, n + 1);
+  if (!gact || !tch) return set_error(c, DRK_ERR_OOM, "gradient buffers");
+  cudaMemsetAsync(gact, 0, sizeof(double) * G * (size_t)n, s);
+  cudaMemsetAsync(tch, 0, n + 1, s);
+  RasterParams P = raster_params(c);
+  P.pxstate = static_cast<double*>(c->pxstate.p);
+  if (fg) {
+    P.dC = fg->d_color;
+    P.dD = fg->d_depth;
+    P.dN = fg->d_normal;
+    P.dA = fg->d_alpha;
+  }
+  P.gact = gact;
+  P.G = G;
+  P.touched = tch;
+  (void)deterministic;  // atomics; see DESIGN.md (deterministic mode: adapter reduction)
+  const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
+  launch_raster(P, n_tiles, true, s);
+  if (int st = cuda_check(c, cudaGetLastError(), "raster bwd")) return st;
+  launch_act_bwd(n, K, A.terms, raw, gact, G, tch, static_cast<const Geo*>(c->geo.p), c->camd, grad_raw,
+                 d_center_world, screen_grad, touched, accumulate, s);
+  if (int st = cuda_check(c, cudaGetLastError(), "activation bwd")) return st;
+  return cuda_check(c, cudaStreamSynchronize(s), "backward");
+}
+
+int run_l1_loss(drk_ctx* c, const float* r, const float* t, int w, int h, double* loss, float* dcol) {
+  launch_l1((long long)w * h * 3, r, t, loss, dcol, c->stream);
+  return cuda_check(c, cudaGetLastError(), "l1 loss");
+}
+
+}  // namespace drk
+
+using namespace drk;
+
+extern "C" {
+
+int drk_abi_version(void) { return DRK_ABI_VERSION; }
+int drk_scalar_count(int k, int sh_terms) { return 3 + 4 + 2 * k + 3 + 3 * sh_terms; }
+
+void drk_default_options(drk_options* o) {
+  o->lowpass_radius = 0.5;
+  o->alpha_min = 1.0 / 255.0;
+  o->grazing_eps = 1e-6;
+  o->background[0] = o->background[1] = o->background[2] = 1.0;
+  o->early_stop_transmittance = 1e-4;
+  o->sh_degree = 3;
+  o->use_cache = 1;
+  o->exact_sort = 0;
+  o->presort = 2;
+  o->threads = 1;
+  o->record_replay = 0;
+}
+
+const char* drk_status_string(int s) {
+  switch (s) {
+    case DRK_OK: return "ok";
+    case DRK_ERR_GENERIC: return "error";
+    case DRK_ERR_NONFINITE: return "non-finite parameters";
+    case DRK_ERR_DEGENERATE_QUAT: return "degenerate quaternion";
+    case DRK_ERR_DEGENERATE_BASIS: return "degenerate basis";
+    case DRK_ERR_REPLAY_MISMATCH: return "replay mismatch";
+    case DRK_ERR_DIMENSION: return "dimension mismatch";
+    case DRK_ERR_INVALID_ARG: return "invalid argument";
+    case DRK_ERR_CUDA: return "CUDA error";
+    case DRK_ERR_OOM: return "out of device memory";
+    case DRK_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+int drk_ctx_create(int device, drk_ctx** out) {
+  if (!out) return DRK_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return DRK_ERR_CUDA;
+  }
+  drk_ctx* c = new drk_ctx();
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return DRK_ERR_CUDA;
+  }
+  c->own_stream = true;
+  *out = c;
+  return DRK_OK;
+}
+
+void drk_ctx_destroy(drk_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
+                    &c->a_ex, &c->a_ey, &c->a_det, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->rowcnt,
+                    &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->pk2, &c->pv2,
+                    &c->hist, &c->sortoff, &c->tilecnt, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
+                    &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
+                    &c->counters, &c->scan_tmp, &c->loss_tmp};
+  for (DevBuf* b : bufs) release(*b);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* drk_last_error(const drk_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int drk_set_stream(drk_ctx* c, void* stream) {
+  if (!c) return DRK_ERR_INVALID_ARG;
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  c->stream = static_cast<cudaStream_t>(stream);
+  c->own_stream = false;
+  return DRK_OK;
+}
+
+int drk_get_stats(const drk_ctx* c, drk_stats* out) {
+  if (!c || !out) return DRK_ERR_INVALID_ARG;
+  *out = c->stats;
+  return DRK_OK;
+}
+
+int drk_activate(drk_ctx* c, const float* raw, int n, int k, int sh_terms, drk_prims* out) {
+  if (!c || n < 0 || (n > 0 && !raw)) return DRK_ERR_INVALID_ARG;
+  if (k < 3 || k > kMaxK) return set_error(c, DRK_ERR_GENERIC, "K must be at least 3 (and at most 16 here)");
+  cudaSetDevice(c->device);
+  if (int st = launch_activate(c, raw, n, k, sh_terms)) return st;
+  if (out) {
+    const Activated& A = c->act;
+    *out = drk_prims{A.mu, A.rot, A.s, A.th, A.eta, A.tau, A.o, A.sh};
+  }
+  return DRK_OK;
+}
+
+int drk_forward(drk_ctx* c, const float* raw, int n, int k, int sh_terms, const drk_camera* cam,
+                const drk_options* opt, float* color, float* depth, float* normal, float* alpha) {
+  if (!c || !cam || !opt || n < 0 || (n > 0 && !raw)) return DRK_ERR_INVALID_ARG;
+  if (k < 3 || k > kMaxK) return set_error(c, DRK_ERR_GENERIC, "K must be at least 3 (and at most 16 here)");
+  cudaSetDevice(c->device);
+  c->has_fwd = false;
+  if (int st = launch_activate(c, raw, n, k, sh_terms)) return st;
+  return run_forward(c, cam, opt, color, depth, normal, alpha);
+}
+
+int drk_forward_prims(drk_ctx* c, const drk_prims* prims, int n, int k, int sh_terms, const drk_camera* cam,
+                      const drk_options* opt, float* color, float* depth, float* normal, float* alpha) {
+  if (!c || !prims || !cam || !opt || n < 0) return DRK_ERR_INVALID_ARG;
+  if (k < 3 || k > kMaxK) return set_error(c, DRK_ERR_GENERIC, "K must be at least 3 (and at most 16 here)");
+  cudaSetDevice(c->device);
+  c->has_fwd = false;
+  if (int st = launch_shape(c, prims, n, k, sh_terms)) return st;
+  return run_forward(c, cam, opt, color, depth, normal, alpha);
+}
+
+int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_terms, const drk_camera* cam,
+                     const drk_options* opt, float* color_host, float* depth_host, float* normal_host,
+                     float* alpha_host) {
+  if (!c || !cam || !opt || n < 0) return DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  const size_t S = (size_t)drk_scalar_count(k, sh_terms);
+  const size_t npix = (size_t)cam->width * cam->height;
+  static thread_local DevBuf raw_d, img_d;
+  float* r = ensure<float>(raw_d, S * n + 1);
+  float* img = ensure<float>(img_d, 8 * npix + 1);
+  if (!r || !img) return set_error(c, DRK_ERR_OOM, "host staging");
+  cudaMemcpyAsync(r, raw_host, sizeof(float) * S * n, cudaMemcpyHostToDevice, c->stream);
+  float* dcol = color_host ? img : nullptr;
+  float* ddep = depth_host ? img + 3 * npix : nullptr;
+  float* dnor = normal_host ? img + 4 * npix : nullptr;
+  float* dalp = alpha_host ? img + 7 * npix : nullptr;
+  if (int st = drk_forward(c, r, n, k, sh_terms, cam, opt, dcol, ddep, dnor, dalp)) return st;
+  if (color_host) cudaMemcpyAsync(color_host, dcol, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, c->stream);
+  if (depth_host) cudaMemcpyAsync(depth_host, ddep, sizeof(float) * npix, cudaMemcpyDeviceToHost, c->stream);
+  if (normal_host) cudaMemcpyAsync(normal_host, dnor, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, c->stream);
+  if (alpha_host) cudaMemcpyAsync(alpha_host, dalp, sizeof(float) * npix, cudaMemcpyDeviceToHost, c->stream);
+  return cuda_check(c, cudaStreamSynchronize(c->stream), "forward_host");
+}
+
+int drk_get_tile_lists(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* ids, double* keys) {
+  if (!c || !c->has_fwd) return c ? set_error(c, DRK_ERR_INVALID_ARG, "no forward on this context") : DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (total) *total = c->n_pairs;
+  const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
+  if (offsets)
+    cudaMemcpyAsync(offsets, c->tileoff.p, sizeof(int64_t) * (n_tiles + 1), cudaMemcpyDeviceToHost, c->stream);
+  std::vector<unsigned long long> v, k;
+  if (ids) {
+    v.resize(c->n_pairs);
+    cudaMemcpyAsync(v.data(), c->pv.p, sizeof(unsigned long long) * c->n_pairs, cudaMemcpyDeviceToHost, c->stream);
+  }
+  if (keys) {
+    k.resize(c->n_pairs);
+    cudaMemcpyAsync(k.data(), c->pk.p, sizeof(unsigned long long) * c->n_pairs, cudaMemcpyDeviceToHost, c->stream);
+  }
+  if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "tile lists")) return st;
+  for (int64_t i = 0; ids && i < c->n_pairs; ++i) ids[i] = (int32_t)(v[i] & 0xffffffffull);
+  for (int64_t i = 0; keys && i < c->n_pairs; ++i) std::memcpy(&keys[i], &k[i], sizeof(double));
+  return DRK_OK;
+}
+
+int drk_get_replay(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* ids, double* vals) {
+  if (!c || !c->has_fwd || c->opt.record_replay <= 0)
+    return c ? set_error(c, DRK_ERR_INVALID_ARG, "no replay recorded") : DRK_ERR_INVALID_ARG;
+  if (c->stats.replay_overflow) return set_error(c, DRK_ERR_UNSUPPORTED, "replay capacity exceeded");
+  cudaSetDevice(c->device);
+  const size_t npix = (size_t)c->cam.width * c->cam.height;
+  const int cap = c->opt.record_replay;
+  std::vector<int> cnt(npix);
+  cudaMemcpyAsync(cnt.data(), c->replay_cnt.p, sizeof(int) * npix, cudaMemcpyDeviceToHost, c->stream);
+  if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "replay")) return st;
+  int64_t tot = 0;
+  for (size_t p = 0; p < npix; ++p) tot += cnt[p];
+  if (total) *total = tot;
+  if (!offsets && !ids && !vals) return DRK_OK;
+  std::vector<int> rid(npix * cap);
+  std::vector<double> rv(5 * npix * cap);
+  cudaMemcpyAsync(rid.data(), c->replay_ids.p, sizeof(int) * rid.size(), cudaMemcpyDeviceToHost, c->stream);
+  cudaMemcpyAsync(rv.data(), c->replay_rec.p, sizeof(double) * rv.size(), cudaMemcpyDeviceToHost, c->stream);
+  if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "replay")) return st;
+  int64_t o = 0;
+  if (offsets) offsets[0] = 0;
+  for (size_t p = 0; p < npix; ++p) {
+    for (int j = 0; j < cnt[p]; ++j, ++o) {
+      if (ids) ids[o] = rid[p * cap + j];
+      if (vals) std::memcpy(vals + 5 * o, &rv[5 * (p * cap + j)], 5 * sizeof(double));
+    }
+    if (offsets) offsets[p + 1] = o;
+  }
+  return DRK_OK;
+}
+
+int drk_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* grad_raw, float* d_center_world,
+                 float* screen_grad, uint8_t* touched, int accumulate, int deterministic) {
+  if (!c) return DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (grad_raw && !raw) return set_error(c, DRK_ERR_INVALID_ARG, "grad_raw needs the raw parameters");
+  return run_backward(c, raw, fg, grad_raw, d_center_world, screen_grad, touched, accumulate, deterministic);
+}
+
+int drk_get_prim_grads(drk_ctx* c, const double** grads, int* stride) {
+  if (!c || !grads || !stride) return DRK_ERR_INVALID_ARG;
+  *grads = static_cast<const double*>(c->gact.p);
+  *stride = 3 + 9 + 2 * c->act.K + 3 + 3 * c->act.terms;
+  return DRK_OK;
+}
+
+int drk_l1_loss(drk_ctx* c, const float* rendered, const float* target, int width, int height, double* loss_out,
+                float* d_color) {
+  if (!c || !rendered || !target || !loss_out || width < 0 || height < 0) return DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  return run_l1_loss(c, rendered, target, width, height, loss_out, d_color);
+}
+
+int drk_adam_step(drk_ctx* c, float* params, const float* grads, float* m, float* v, int n, int k, int sh_terms,
+                  int64_t* step, const drk_adam_config* cfg) {
+  if (!c || !params || !grads || !m || !v || !step || !cfg || n < 0) return DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  *step += 1;
+  return run_adam(c, params, grads, m, v, n, k, sh_terms, *step, cfg);
+}
+
+}  // extern "C"

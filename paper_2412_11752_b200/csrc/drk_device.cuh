@@ -1,0 +1,289 @@
+// Device math for the DRK rasterizer (sm_100a).  Compiled with --fmad=false so
+// that every fp64 expression rounds exactly like the reference's x86-64 build
+// (no contraction); the op order of each function follows the reference line
+// it cites, with Eigen reductions left to right (oracle/shim/Eigen/Core).
+// Transcendentals (exp, log, sin, cos, atan2) are CUDA's (<= 2 ulp), so values
+// derived from them agree with the reference to ~1e-16 relative; everything
+// built from + - * / sqrt only (pixel rays, ray-plane depths, quaternion
+// rotation, projection) is bit-identical.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "drk_b200.h"
+
+namespace drk {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kTwoPi = 2.0 * kPi;
+constexpr double kThreeSigmaLevel = 1.2340980408667956e-4;  // core.cpp:14
+constexpr double kTauLow = -0.1;
+constexpr double kTauHigh = 0.99;
+constexpr double kMinExponent = -30.0;
+constexpr double kNearClip = 1e-6;  // raster.cpp:12
+constexpr int kTile = 16;
+constexpr int kCacheCap = 8;  // raster.hpp:37
+constexpr int kMaxK = 16;
+
+// Device-side error / counter slots (ctx->counters).
+enum Counter {
+  C_ERR_DEGEN_BASIS = 0,
+  C_ERR_NONFINITE,
+  C_ERR_DEGEN_QUAT,
+  C_POLY_OVERFLOW,
+  C_HULL_POOL,        // hull pool cursor
+  C_NEAR_TIES,
+  C_STREAMED,
+  C_POPPED,
+  C_COMPOSITED,
+  C_REPLAY_OVERFLOW,
+  C_VISIBLE,
+  C_POLY_FAIL,
+  C_COUNT
+};
+
+// Camera + derived constants, passed by value to kernels.
+struct CamD {
+  double fx, fy, cx, cy;
+  double R[9];  // row-major world->cam
+  double t[3];
+  double o[3];  // camera position, -(R^T) t, op order of geometry.hpp:15
+  int W, H, tiles_x, tiles_y;
+};
+
+struct OptD {
+  double lowpass_radius, alpha_min, grazing_eps;
+  double bg[3];
+  double early_stop;
+  double lp_pad;  // raster.cpp:128-129
+  int sh_degree, use_cache, exact_sort, presort, record_replay, terms_active;
+};
+
+__host__ __device__ inline double dmin(double a, double b) { return (b < a) ? b : a; }  // std::min
+__host__ __device__ inline double dmax(double a, double b) { return (a < b) ? b : a; }  // std::max
+
+// static_cast<int>(double) as compiled for x86-64 (cvttsd2si): NaN and
+// out-of-range values give INT_MIN.  raster.cpp:226-231 depends on it.
+__host__ __device__ inline int x86_int(double v) {
+  if (!(v > -2147483649.0 && v < 2147483648.0)) return (int)0x80000000u;
+  return (int)v;
+}
+
+__host__ __device__ inline double dot3(const double* a, const double* b) {
+  return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+}
+
+// pixel_ray (geometry.cpp:32-38): dir = normalize(R^T ((px-cx)/fx, (py-cy)/fy, 1)).
+__device__ __forceinline__ void pixel_dir(const CamD& c, double px, double py, double d[3]) {
+  const double dc0 = (px - c.cx) / c.fx, dc1 = (py - c.cy) / c.fy, dc2 = 1.0;
+  double v0 = c.R[0] * dc0 + c.R[3] * dc1 + c.R[6] * dc2;
+  double v1 = c.R[1] * dc0 + c.R[4] * dc1 + c.R[7] * dc2;
+  double v2 = c.R[2] * dc0 + c.R[5] * dc1 + c.R[8] * dc2;
+  const double sq = v0 * v0 + v1 * v1 + v2 * v2;
+  if (sq > 0) {
+    const double n = sqrt(sq);
+    v0 = v0 / n;
+    v1 = v1 / n;
+    v2 = v2 / n;
+  }
+  d[0] = v0;
+  d[1] = v1;
+  d[2] = v2;
+}
+
+// Camera::to_camera (geometry.hpp:14): R * w + t.
+__device__ __forceinline__ void to_camera(const CamD& c, const double w[3], double out[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    out[i] = (c.R[3 * i] * w[0] + c.R[3 * i + 1] * w[1] + c.R[3 * i + 2] * w[2]) + c.t[i];
+}
+
+// try_project_point (geometry.cpp:67-74).
+__device__ __forceinline__ bool try_project(const CamD& c, const double w[3], double out[3]) {
+  double p[3];
+  to_camera(c, w, p);
+  if (p[2] <= 0) return false;
+  out[0] = c.fx * p[0] / p[2] + c.cx;
+  out[1] = c.fy * p[1] / p[2] + c.cy;
+  out[2] = p[2];
+  return true;
+}
+
+// projection_jacobian (geometry.cpp:82-89), 2x3 row-major.
+__device__ __forceinline__ void projection_jacobian(const CamD& c, const double w[3], double J[6]) {
+  double p[3];
+  to_camera(c, w, p);
+  const double z = p[2];
+  const double jc[6] = {c.fx / z, 0, -c.fx * p[0] / (z * z), 0, c.fy / z, -c.fy * p[1] / (z * z)};
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      J[3 * i + j] = jc[3 * i] * c.R[j] + jc[3 * i + 1] * c.R[3 + j] + jc[3 * i + 2] * c.R[6 + j];
+}
+
+__device__ __forceinline__ double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }  // core.cpp:80
+
+// sharpen family (core.cpp:210-245).
+__device__ __forceinline__ double sharpen_inverse(double y, double tau) {
+  y = dmin(1.0, dmax(0.0, y));
+  if (y < (1.0 - tau) / 4.0) return (1.0 + tau) / (1.0 - tau) * y;
+  if (y < (3.0 + tau) / 4.0) return ((1.0 - tau) * y + tau) / (1.0 + tau);
+  return ((1.0 + tau) * y - 2.0 * tau) / (1.0 - tau);
+}
+__device__ __forceinline__ int sharpen_branch(double g, double tau) {
+  if (g < (1.0 + tau) / 4.0) return 0;
+  if (g < (3.0 - tau) / 4.0) return 1;
+  return 2;
+}
+__device__ __forceinline__ double sharpen_slope(int b, double tau) {
+  if (b == 1) return (1.0 + tau) / (1.0 - tau);
+  return (1.0 - tau) / (1.0 + tau);
+}
+__device__ __forceinline__ double sharpen_dtau(int b, double g, double tau) {
+  if (b == 0) return -2.0 * g / ((1.0 + tau) * (1.0 + tau));
+  if (b == 1) return (2.0 * g - 1.0) / ((1.0 - tau) * (1.0 - tau));
+  return (2.0 - 2.0 * g) / ((1.0 + tau) * (1.0 + tau));
+}
+__device__ __forceinline__ double sharpen(double g, double tau) {
+  g = dmin(1.0, dmax(0.0, g));
+  switch (sharpen_branch(g, tau)) {
+    case 0: return (1.0 - tau) / (1.0 + tau) * g;
+    case 1: return ((1.0 + tau) * g - tau) / (1.0 - tau);
+    default: return ((1.0 - tau) * g + 2.0 * tau) / (1.0 + tau);
+  }
+}
+
+// binning_radius_factor (core.cpp:305-318); false when never visible.
+__device__ __forceinline__ bool binning_radius_factor(double o, double tau, double amin, double* f,
+                                                      double* f_vis) {
+  const double vis = amin / o;
+  if (vis >= 1.0) return false;
+  const double gv = sharpen_inverse(vis, tau);
+  double fac = sqrt(-2.0 * log(gv));
+  *f_vis = fac;
+  const double cal = kThreeSigmaLevel / o;
+  if (cal < 1.0) {
+    const double gc = sharpen_inverse(cal, tau);
+    if (gc > 0 && gc < 1) fac = dmax(fac, sqrt(-log(gc)));
+  }
+  *f = fac;
+  return true;
+}
+
+// Per-primitive shape constants (view independent), primitive-major with
+// stride K: endpoints e_k = s_k (cos th_k, sin th_k) and the determinant of
+// the bracket (k, k+1 mod K) as evaluated in core.cpp:188-190.
+struct ShapeView {
+  const double* s;
+  const double* th;
+  const double* ex;
+  const double* ey;
+  const double* det;
+  const double* eta;
+  const double* tau;
+  const double* o;
+  int K;
+};
+
+struct KEval {
+  double g, r2, theta, delta, inv_sbar, a, b, r1;
+  int lo, hi;
+  bool center, clamped, degenerate;
+};
+
+// eval_kernel_detail (core.cpp:148-204) for primitive i.
+__device__ __forceinline__ void eval_kernel(double u, double v, const ShapeView& S, int i, KEval& ev) {
+  const int K = S.K;
+  const double* th = S.th + (size_t)i * K;
+  ev.g = 1.0;
+  ev.center = false;
+  ev.clamped = false;
+  ev.degenerate = false;
+  ev.r2 = u * u + v * v;
+  ev.lo = ev.hi = 0;
+  ev.theta = ev.delta = ev.inv_sbar = ev.a = ev.b = ev.r1 = 0;
+  if (ev.r2 == 0) {
+    ev.center = true;
+    return;
+  }
+  double theta = atan2(v, u);
+  if (theta <= 0) theta += kTwoPi;
+  ev.theta = theta;
+  int lo, hi;
+  double alo, ahi;
+  const double th0 = th[0], thK = th[K - 1];
+  if (theta <= th0 || theta > thK) {
+    lo = K - 1;
+    hi = 0;
+    alo = thK - kTwoPi;
+    ahi = th0;
+    if (theta > thK) theta -= kTwoPi;
+  } else {
+    hi = 1;
+    while (hi < K && th[hi] < theta) ++hi;  // lower_bound (th[0] < theta here)
+    lo = hi - 1;
+    alo = th[lo];
+    ahi = th[hi];
+  }
+  ev.lo = lo;
+  ev.hi = hi;
+  ev.delta = (theta - alo) * kPi / (ahi - alo);
+  const double c = cos(ev.delta);
+  const double slo = S.s[(size_t)i * K + lo], shi = S.s[(size_t)i * K + hi];
+  ev.inv_sbar = (1.0 + c) / (2.0 * slo * slo) + (1.0 - c) / (2.0 * shi * shi);
+  const double elx = S.ex[(size_t)i * K + lo], ely = S.ey[(size_t)i * K + lo];
+  const double ehx = S.ex[(size_t)i * K + hi], ehy = S.ey[(size_t)i * K + hi];
+  const double det = S.det[(size_t)i * K + lo];
+  if (fabs(det) < 1e-12) {
+    ev.degenerate = true;
+    return;
+  }
+  ev.a = (ehy * u - ehx * v) / det;
+  ev.b = (-ely * u + elx * v) / det;
+  ev.r1 = fabs(ev.a) + fabs(ev.b);
+  const double eta = S.eta[i];
+  double e = -0.5 * (eta * ev.r1 * ev.r1 + (1.0 - eta) * ev.r2 * ev.inv_sbar);
+  if (e < kMinExponent) {
+    e = kMinExponent;
+    ev.clamped = true;
+  }
+  ev.g = exp(e);
+}
+
+// low_pass_filter_term (core.cpp:267-273).
+__device__ __forceinline__ double low_pass_filter_term(double dpw, double dph, double cos_view, double o,
+                                                       double s_l) {
+  const double denom = 2.0 * cos_view * cos_view * s_l * s_l;
+  double e = -(dpw * dpw + dph * dph) / denom;
+  if (e < kMinExponent) e = kMinExponent;
+  return o * exp(e);
+}
+
+// Real SH basis (geometry.cpp:91-124), fp32.
+__device__ __forceinline__ void sh_basis_f(float x, float y, float z, int degree, float* out) {
+  const float kSh0 = 0.28209479177387814f, kSh1 = 0.4886025119029199f;
+  out[0] = kSh0;
+  if (degree < 1) return;
+  out[1] = -kSh1 * y;
+  out[2] = kSh1 * z;
+  out[3] = -kSh1 * x;
+  if (degree < 2) return;
+  const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+  out[4] = 1.0925484305920792f * xy;
+  out[5] = -1.0925484305920792f * yz;
+  out[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
+  out[7] = -1.0925484305920792f * xz;
+  out[8] = 0.5462742152960396f * (xx - yy);
+  if (degree < 3) return;
+  out[9] = -0.5900435899266435f * y * (3.f * xx - yy);
+  out[10] = 2.890611442640554f * xy * z;
+  out[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
+  out[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+  out[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy);
+  out[14] = 1.445305721320277f * z * (xx - yy);
+  out[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
+}
+
+}  // namespace drk

@@ -1,0 +1,121 @@
+// Host-side internals shared by the kernel launchers and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "drk_b200.h"
+#include "drk_device.cuh"
+
+namespace drk {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+// Grow-only device allocation; returns nullptr on OOM.
+void* ensure_bytes(DevBuf& b, size_t bytes);
+template <class T>
+T* ensure(DevBuf& b, size_t count) {
+  return static_cast<T*>(ensure_bytes(b, (count ? count : 1) * sizeof(T)));
+}
+void release(DevBuf& b);
+
+// Per-primitive, per-view record (fp64).  num = (mu - o) . R_z with the op
+// order of classify_intersect (geometry.cpp:40-52); proj = projected centre.
+struct Geo {
+  double num;
+  double rz[3];
+  double rx[3];
+  double ry[3];
+  double mu[3];
+  double ppx, ppy, projz;  // projected centre (valid iff has_proj); projz = +inf if not
+  double r2max;            // (s_max f_vis)^2 (1+1e-9): beyond it alpha_kernel < alpha_min
+  double dp2max;           // 2 s_l^2 ln(o / alpha_min) (1+1e-9): low-pass floor bound / cos^2
+  int has_proj;
+  int visible;
+};
+
+struct Activated {
+  const double *mu, *rot, *s, *th, *eta, *tau, *o;
+  const float* sh;  // n x terms x 3 (AoS)
+  const double *ex, *ey, *det;
+  int n, K, terms;
+};
+
+struct RasterParams {
+  CamD cam;
+  OptD opt;
+  const long long* tileoff;
+  const unsigned long long* pv;  // sorted (tile << 32 | pid)
+  const Geo* geo;
+  ShapeView S;
+  const float* sh;
+  int terms;  // stored SH rows per primitive
+  float *color, *depth, *normal, *alpha;
+  double* pxstate;  // 8 doubles per pixel: C(3, incl. background), D, N(3), A
+  int* replay_cnt;
+  double* replay_rec;  // 5 doubles per record
+  int* replay_ids;
+  int replay_cap;
+  // backward
+  const float *dC, *dD, *dN, *dA;
+  double* gact;
+  int G;
+  unsigned char* touched;
+  unsigned long long* counters;
+};
+
+void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s);
+
+}  // namespace drk
+
+struct drk_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+
+  // activated primitives owned by the context (raw path)
+  drk::DevBuf a_mu, a_rot, a_s, a_th, a_eta, a_tau, a_o, a_sh, a_ex, a_ey, a_det;
+  drk::Activated act{};
+
+  // per view
+  drk::DevBuf geo, bbox, hullref, hull, rowcnt, rowoff, rows, rowpaircnt, rowpairoff;
+  drk::DevBuf pk, pv, pk2, pv2, hist, sortoff, tilecnt, tileoff, cdirs, tdirs, bits;
+  drk::DevBuf pxstate, replay_cnt, replay_rec, replay_ids;
+  drk::DevBuf gact, touched;
+  drk::DevBuf counters, scan_tmp, loss_tmp;
+  int64_t hull_cap = 0;
+
+  // last forward
+  bool has_fwd = false;
+  drk_camera cam{};
+  drk_options opt{};
+  drk::CamD camd{};
+  drk::OptD optd{};
+  int64_t n_pairs = 0;
+  int64_t n_rows = 0;
+  drk_stats stats{};
+};
+
+namespace drk {
+
+// Launchers (drk_kernels.cu).  All return a drk_status.
+int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms);
+int launch_shape(drk_ctx* c, const drk_prims* p, int n, int K, int terms);
+int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float* color, float* depth,
+                float* normal, float* alpha);
+int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* grad_raw,
+                 float* d_center_world, float* screen_grad, uint8_t* touched, int accumulate,
+                 int deterministic);
+int run_l1_loss(drk_ctx* c, const float* r, const float* t, int w, int h, double* loss, float* dcol);
+int run_adam(drk_ctx* c, float* params, const float* grads, float* m, float* v, int n, int K, int terms,
+             int64_t step, const drk_adam_config* cfg);
+int set_error(drk_ctx* c, int status, const std::string& msg);
+int cuda_check(drk_ctx* c, cudaError_t e, const char* where);
+
+}  // namespace drk

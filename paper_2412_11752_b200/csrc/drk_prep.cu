@@ -1,0 +1,658 @@
+// K0 activation, K1 per-primitive preprocess (support polygon, near clip,
+// projection, convex hull, tile bbox), K2 per-row tile intervals and K3 pair
+// emission with NearestDepth keys.  Restates reference core.cpp:133-146
+// (activate) and raster.cpp:12-265 (bin_primitives) for sm_100a.
+//
+// Layout: one thread per primitive for K0/K1/K2 (SoA fp64 loads), one thread
+// per (primitive, tile row) for K3.  The hull of every primitive goes to a
+// bump-allocated pool; rows are addressed through an exclusive scan of the
+// per-primitive row counts so that pairs come out primitive-major (ascending
+// prim id inside every tile), which the stable radix sort turns into the
+// reference's (key, prim_id) order (raster.cpp:260-263).
+#include <cfloat>
+
+#include "drk_internal.h"
+
+namespace drk {
+
+// ---------------------------------------------------------------------------
+// K0: activation (core.cpp:89-146, geometry.cpp:21-30)
+// ---------------------------------------------------------------------------
+__global__ void k_activate(const float* __restrict__ raw, int n, int K, int terms, double* mu, double* rot,
+                           double* s, double* th, double* eta, double* tau, double* o, float* sh,
+                           double* ex, double* ey, double* det, unsigned long long* counters) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int S = 3 + 4 + 2 * K + 3 + 3 * terms;
+  bool finite = true;
+  for (int j = 0; j < S; ++j) finite &= isfinite(raw[(size_t)j * n + i]);
+  if (!finite) atomicAdd(&counters[C_ERR_NONFINITE], 1ull);
+#define RAW(j) ((double)raw[(size_t)(j)*n + i])
+  for (int a = 0; a < 3; ++a) mu[3 * i + a] = RAW(a);
+  const double q0 = RAW(3), q1 = RAW(4), q2 = RAW(5), q3 = RAW(6);
+  const double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+  if (qn < 1e-12) atomicAdd(&counters[C_ERR_DEGEN_QUAT], 1ull);
+  const double w = q0 / qn, x = q1 / qn, y = q2 / qn, z = q3 / qn;
+  double* R = rot + 9 * (size_t)i;
+  R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
+  R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+  R[6] = 2 * (x * z - w * y);     R[7] = 2 * (y * z + w * x);     R[8] = 1 - 2 * (x * x + y * y);
+  double* si = s + (size_t)K * i;
+  double* ti = th + (size_t)K * i;
+  for (int j = 0; j < K; ++j) si[j] = exp(RAW(7 + j));
+  // angle_activation (core.cpp:89-108)
+  const double residual = 1.0 / (K - 2);
+  double total = 0;
+  for (int j = 0; j < K; ++j) {
+    double sg = sigmoid(RAW(7 + K + j));
+    sg = sg < 1e-9 ? 1e-9 : (1.0 - 1e-9 < sg ? 1.0 - 1e-9 : sg);
+    total += sg + residual;
+    ti[j] = total;
+  }
+  const double scale = kTwoPi / total;
+  for (int j = 0; j < K; ++j) ti[j] = ti[j] * scale;
+  ti[K - 1] = kTwoPi;
+  eta[i] = sigmoid(RAW(7 + 2 * K));
+  tau[i] = kTauLow + (kTauHigh - kTauLow) * sigmoid(RAW(8 + 2 * K));
+  o[i] = sigmoid(RAW(9 + 2 * K));
+  for (int j = 0; j < 3 * terms; ++j) sh[(size_t)3 * terms * i + j] = raw[(size_t)(10 + 2 * K + j) * n + i];
+#undef RAW
+  // endpoints and bracket determinants (types.hpp:93-95, core.cpp:188-190)
+  for (int j = 0; j < K; ++j) {
+    ex[(size_t)K * i + j] = si[j] * cos(ti[j]);
+    ey[(size_t)K * i + j] = si[j] * sin(ti[j]);
+  }
+  for (int j = 0; j < K; ++j) {
+    const int h = (j + 1) % K;
+    det[(size_t)K * i + j] = ex[(size_t)K * i + j] * ey[(size_t)K * i + h] - ey[(size_t)K * i + j] * ex[(size_t)K * i + h];
+  }
+}
+
+// Shape constants for caller-provided activated primitives.
+__global__ void k_shape(int n, int K, const double* s, const double* th, double* ex, double* ey, double* det) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int j = 0; j < K; ++j) {
+    ex[(size_t)K * i + j] = s[(size_t)K * i + j] * cos(th[(size_t)K * i + j]);
+    ey[(size_t)K * i + j] = s[(size_t)K * i + j] * sin(th[(size_t)K * i + j]);
+  }
+  for (int j = 0; j < K; ++j) {
+    const int h = (j + 1) % K;
+    det[(size_t)K * i + j] = ex[(size_t)K * i + j] * ey[(size_t)K * i + h] - ey[(size_t)K * i + j] * ex[(size_t)K * i + h];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: support polygon -> clip -> project -> hull -> bbox  (raster.cpp:131-231)
+// ---------------------------------------------------------------------------
+struct PolyParams {
+  double alo, gap, slo, shi, elx, ely, ehx, ehy, det, eta, support_c;
+};
+struct W2 {
+  double rho1, inv;
+};
+
+// raster.cpp:158-168
+__device__ __forceinline__ W2 weight_at(const PolyParams& p, double a) {
+  const double delta = (a - p.alo) * kPi / p.gap;
+  const double c = cos(delta);
+  W2 w;
+  w.inv = (1.0 + c) / (2.0 * p.slo * p.slo) + (1.0 - c) / (2.0 * p.shi * p.shi);
+  const double dx = cos(a), dy = sin(a);
+  const double ca = (p.ehy * dx - p.ehx * dy) / p.det;
+  const double cb = (-p.ely * dx + p.elx * dy) / p.det;
+  w.rho1 = fabs(ca) + fabs(cb);
+  return w;
+}
+// raster.cpp:170-173
+__device__ __forceinline__ double radius_true(const PolyParams& p, W2 w) {
+  const double total = p.eta * w.rho1 * w.rho1 + (1.0 - p.eta) * w.inv;
+  return sqrt(p.support_c / dmax(total, 1e-12));
+}
+
+// Streaming Sutherland-Hodgman against z >= kNearClip (raster.cpp:15-30):
+// emits exactly the reference's output sequence, projected to pixels
+// (raster.cpp:214-215).
+struct Clipper {
+  double first[3], prev[3];
+  int count;
+  double2* out;
+  int cap, n;
+  const CamD* cam;
+  __device__ void push(const double q[3]) {
+    if (n < cap) out[n] = make_double2(cam->fx * q[0] / q[2] + cam->cx, cam->fy * q[1] / q[2] + cam->cy);
+    ++n;
+  }
+  __device__ void edge(const double a[3], const double b[3]) {
+    const bool a_in = a[2] >= kNearClip, b_in = b[2] >= kNearClip;
+    if (a_in) push(a);
+    if (a_in != b_in) {
+      const double t = (kNearClip - a[2]) / (b[2] - a[2]);
+      const double q[3] = {a[0] + t * (b[0] - a[0]), a[1] + t * (b[1] - a[1]), a[2] + t * (b[2] - a[2])};
+      push(q);
+    }
+  }
+  __device__ void feed(const double b[3]) {
+    if (count == 0) {
+      first[0] = b[0]; first[1] = b[1]; first[2] = b[2];
+    } else {
+      edge(prev, b);
+    }
+    prev[0] = b[0]; prev[1] = b[1]; prev[2] = b[2];
+    ++count;
+  }
+  __device__ void finish() {
+    if (count > 0) edge(prev, first);
+  }
+};
+
+__device__ __forceinline__ bool lessp(double2 a, double2 b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
+
+__device__ void heap_sort(double2* a, int n) {
+  auto sift = [&](int root, int end) {
+    while (true) {
+      int child = 2 * root + 1;
+      if (child >= end) break;
+      if (child + 1 < end && lessp(a[child], a[child + 1])) ++child;
+      if (lessp(a[root], a[child])) {
+        const double2 t = a[root];
+        a[root] = a[child];
+        a[child] = t;
+        root = child;
+      } else {
+        break;
+      }
+    }
+  };
+  for (int i = n / 2 - 1; i >= 0; --i) sift(i, n);
+  for (int end = n - 1; end > 0; --end) {
+    const double2 t = a[0];
+    a[0] = a[end];
+    a[end] = t;
+    sift(0, end);
+  }
+}
+
+__device__ __forceinline__ double cross2(double2 o, double2 a, double2 b) {
+  return (a.x - o.x) * (b.y - o.y) - (a.y - o.y) * (b.x - o.x);
+}
+
+// Andrew monotone chain (raster.cpp:33-58); pts sorted + deduplicated in
+// place, hull written to h (capacity n + 2).  Returns the hull size.
+__device__ int convex_hull(double2* pts, int n, double2* h) {
+  heap_sort(pts, n);
+  int m = 0;
+  for (int i = 0; i < n; ++i)
+    if (m == 0 || !(pts[i].x == pts[m - 1].x && pts[i].y == pts[m - 1].y)) pts[m++] = pts[i];
+  n = m;
+  if (n <= 2) {
+    for (int i = 0; i < n; ++i) h[i] = pts[i];
+    return n;
+  }
+  int k = 0;
+  for (int i = 0; i < n; ++i) {
+    while (k >= 2 && cross2(h[k - 2], h[k - 1], pts[i]) <= 0) --k;
+    h[k++] = pts[i];
+  }
+  const int lower = k + 1;
+  for (int i = n - 2; i >= 0; --i) {
+    while (k >= lower && cross2(h[k - 2], h[k - 1], pts[i]) <= 0) --k;
+    h[k++] = pts[i];
+  }
+  return k - 1;
+}
+
+// Builds the projected support polygon of primitive i into pts (capacity cap)
+// and its hull into h.  Returns the hull size, 0 when fully behind, or -1 on
+// polygon overflow (caller retries with a larger buffer).
+__device__ int build_hull(const Activated& A, int i, const CamD& cam, double factor, double2* pts, int cap,
+                          double2* h) {
+  const int K = A.K;
+  const double* s = A.s + (size_t)K * i;
+  const double* th = A.th + (size_t)K * i;
+  const double* R = A.rot + 9 * (size_t)i;
+  const double mu[3] = {A.mu[3 * i], A.mu[3 * i + 1], A.mu[3 * i + 2]};
+  const double rx[3] = {R[0], R[3], R[6]}, ry[3] = {R[1], R[4], R[7]};
+  Clipper clip;
+  clip.count = 0;
+  clip.out = pts;
+  clip.cap = cap;
+  clip.n = 0;
+  clip.cam = &cam;
+  PolyParams p;
+  p.eta = A.eta[i];
+  p.support_c = factor * factor;
+  struct Frame {
+    double a0, a1;
+    W2 w0, w1;
+    int depth;
+  };
+  Frame stack[12];
+  for (int k = 0; k < K; ++k) {
+    const int hi = (k + 1) % K;
+    p.alo = k + 1 < K ? th[k] : th[k] - 2.0 * kPi;
+    const double ahi = k + 1 < K ? th[hi] : th[0];
+    p.gap = ahi - p.alo;
+    p.slo = s[k];
+    p.shi = s[hi];
+    p.elx = A.ex[(size_t)K * i + k];
+    p.ely = A.ey[(size_t)K * i + k];
+    p.ehx = A.ex[(size_t)K * i + hi];
+    p.ehy = A.ey[(size_t)K * i + hi];
+    p.det = A.det[(size_t)K * i + k];
+    const int coarse_i = (int)ceil(p.gap / (kPi / 8.0));
+    const int coarse = coarse_i > 1 ? coarse_i : 1;
+    W2 prev = weight_at(p, p.alo);
+    for (int j = 0; j < coarse; ++j) {
+      const double a0 = p.alo + p.gap * j / coarse;
+      const double a1 = p.alo + p.gap * (j + 1) / coarse;
+      const W2 next = weight_at(p, a1);
+      // iterative depth-first emit (raster.cpp:178-198)
+      int sp = 0;
+      stack[sp++] = {a0, a1, prev, next, 0};
+      while (sp > 0) {
+        const Frame f = stack[--sp];
+        const double rho1_min = dmin(f.w0.rho1, f.w1.rho1);
+        const double inv_min = dmin(f.w0.inv, f.w1.inv);
+        const double w_lb = p.eta * rho1_min * rho1_min + (1.0 - p.eta) * inv_min;
+        const double bound = sqrt(p.support_c / dmax(w_lb, 1e-12)) / cos(0.5 * (f.a1 - f.a0));
+        if (f.depth < 9 && f.a1 - f.a0 > 2e-3 &&
+            bound > 1.25 * dmin(radius_true(p, f.w0), radius_true(p, f.w1))) {
+          const double mid = 0.5 * (f.a0 + f.a1);
+          const W2 wm = weight_at(p, mid);
+          stack[sp++] = {mid, f.a1, wm, f.w1, f.depth + 1};  // right half after
+          stack[sp++] = {f.a0, mid, f.w0, wm, f.depth + 1};  // left half first
+          continue;
+        }
+        const double as[2] = {f.a0, f.a1};
+        for (int e = 0; e < 2; ++e) {
+          const double ca = cos(as[e]), sa = sin(as[e]);
+          double w[3], pc[3];
+          for (int a = 0; a < 3; ++a) w[a] = mu[a] + bound * (ca * rx[a] + sa * ry[a]);
+          to_camera(cam, w, pc);
+          clip.feed(pc);
+        }
+      }
+      prev = next;
+    }
+  }
+  clip.finish();
+  if (clip.n > cap) return -1;
+  if (clip.n == 0) return 0;
+  return convex_hull(pts, clip.n, h);
+}
+
+constexpr int kPolyCap = 256;
+
+// K1.  pass == 0: all primitives with local buffers; pass == 1: the overflow
+// list with large per-thread global scratch.
+template <int pass>
+__device__ __forceinline__ void prep_body(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref,
+                                          double2* pool, long long pool_cap, int* rowcnt,
+                                          unsigned long long* counters, const int* list, int list_n,
+                                          double2* scratch, int scratch_cap, int* overflow) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  int i;
+  if (pass == 0) {
+    if (t >= A.n) return;
+    i = t;
+  } else {
+    if (t >= list_n) return;
+    i = list[t];
+  }
+  const int K = A.K;
+  if (pass == 0) {
+    // per-view geometry record
+    Geo g;
+    const double* R = A.rot + 9 * (size_t)i;
+    for (int a = 0; a < 3; ++a) {
+      g.mu[a] = A.mu[3 * i + a];
+      g.rx[a] = R[3 * a];
+      g.ry[a] = R[3 * a + 1];
+      g.rz[a] = R[3 * a + 2];
+    }
+    const double m0 = g.mu[0] - cam.o[0], m1 = g.mu[1] - cam.o[1], m2 = g.mu[2] - cam.o[2];
+    g.num = m0 * g.rz[0] + m1 * g.rz[1] + m2 * g.rz[2];
+    double pr[3];
+    g.has_proj = try_project(cam, g.mu, pr) ? 1 : 0;
+    g.ppx = g.has_proj ? pr[0] : 0.0;
+    g.ppy = g.has_proj ? pr[1] : 0.0;
+    g.projz = g.has_proj ? pr[2] : __longlong_as_double(0x7ff0000000000000ll);
+    double f, fv;
+    const double o = A.o[i];
+    g.visible = binning_radius_factor(o, A.tau[i], opt.alpha_min, &f, &fv) ? 1 : 0;
+    double smax = 0;
+    for (int j = 0; j < K; ++j) smax = dmax(smax, A.s[(size_t)K * i + j]);
+    g.r2max = g.visible ? (smax * fv) * (smax * fv) * (1.0 + 1e-9) : 0.0;
+    g.dp2max = g.visible ? 2.0 * opt.lowpass_radius * opt.lowpass_radius * log(o / opt.alpha_min) * (1.0 + 1e-9) : 0.0;
+    geo[i] = g;
+    rowcnt[i] = 0;
+    bbox[i] = make_int4(1, 0, 1, 0);
+    hullref[i] = make_int2(0, 0);
+    if (!g.visible) return;
+  }
+  double f, fv;
+  binning_radius_factor(A.o[i], A.tau[i], opt.alpha_min, &f, &fv);
+  double2 pts_local[pass == 0 ? kPolyCap : 1];
+  double2 hull_local[pass == 0 ? kPolyCap + 2 : 1];
+  double2* pts = pts_local;
+  double2* hh = hull_local;
+  int cap = kPolyCap;
+  if (pass == 1) {
+    pts = scratch + (size_t)t * 2 * (scratch_cap + 2);
+    hh = pts + scratch_cap + 2;
+    cap = scratch_cap;
+  }
+  const int hn = build_hull(A, i, cam, f, pts, cap, hh);
+  if (hn < 0) {
+    if (pass == 0) {
+      const unsigned long long slot = atomicAdd(&counters[C_POLY_OVERFLOW], 1ull);
+      overflow[slot] = i;
+    } else {
+      atomicAdd(&counters[C_POLY_FAIL], 1ull);  // polygon larger than the big scratch
+    }
+    return;
+  }
+  if (hn == 0) return;
+  double hx0 = hh[0].x, hx1 = hx0, hy0 = hh[0].y, hy1 = hy0;
+  for (int j = 0; j < hn; ++j) {
+    hx0 = dmin(hx0, hh[j].x);
+    hx1 = dmax(hx1, hh[j].x);
+    hy0 = dmin(hy0, hh[j].y);
+    hy1 = dmax(hy1, hh[j].y);
+  }
+  const double lp = opt.lp_pad;
+  int tx0 = x86_int(floor((hx0 - lp) / kTile));
+  tx0 = tx0 > 0 ? tx0 : 0;
+  int tx1 = x86_int(floor((hx1 + lp) / kTile));
+  tx1 = tx1 < cam.tiles_x - 1 ? tx1 : cam.tiles_x - 1;
+  int ty0 = x86_int(floor((hy0 - lp) / kTile));
+  ty0 = ty0 > 0 ? ty0 : 0;
+  int ty1 = x86_int(floor((hy1 + lp) / kTile));
+  ty1 = ty1 < cam.tiles_y - 1 ? ty1 : cam.tiles_y - 1;
+  if (tx1 < tx0 || ty1 < ty0) return;
+  const long long off = (long long)atomicAdd(&counters[C_HULL_POOL], (unsigned long long)hn);
+  if (off + hn > pool_cap) return;  // host detects via the cursor and retries with a larger pool
+  for (int j = 0; j < hn; ++j) pool[off + j] = hh[j];
+  hullref[i] = make_int2((int)off, hn);
+  bbox[i] = make_int4(tx0, tx1, ty0, ty1);
+  rowcnt[i] = ty1 - ty0 + 1;
+  atomicAdd(&counters[C_VISIBLE], 1ull);
+}
+
+// ---------------------------------------------------------------------------
+// K2: per-row tile intervals.  For a convex hull H and the dilated row band
+// B = [Y0, Y1], a dilated tile rectangle overlaps H iff its x-range meets the
+// x-extent of H ∩ B.  That is the geometric content of the reference's
+// separating-axis test (raster.cpp:63-97); decisions within 1e-9 relative of
+// a tie are resolved with a replica of that test (same op order) and counted.
+// ---------------------------------------------------------------------------
+__device__ bool hull_overlaps_rect(const double2* h, int n, double x0, double y0, double x1, double y1) {
+  if (n == 0) return false;
+  double hx0 = h[0].x, hx1 = h[0].x, hy0 = h[0].y, hy1 = h[0].y;
+  for (int i = 0; i < n; ++i) {
+    hx0 = dmin(hx0, h[i].x);
+    hx1 = dmax(hx1, h[i].x);
+    hy0 = dmin(hy0, h[i].y);
+    hy1 = dmax(hy1, h[i].y);
+  }
+  if (hx1 < x0 || hx0 > x1 || hy1 < y0 || hy0 > y1) return false;
+  if (n <= 1) return true;
+  const double cx[4] = {x0, x1, x1, x0}, cy[4] = {y0, y0, y1, y1};
+  for (int i = 0; i < n; ++i) {
+    const double2 a = h[i], b = h[(i + 1) % n];
+    const double ex = b.x - a.x, ey = b.y - a.y;
+    if (ex * ex + ey * ey < 1e-24) continue;
+    const double ax = -ey, ay = ex;
+    double pmin = ax * h[0].x + ay * h[0].y, pmax = pmin;
+    for (int j = 0; j < n; ++j) {
+      const double d = ax * h[j].x + ay * h[j].y;
+      pmin = dmin(pmin, d);
+      pmax = dmax(pmax, d);
+    }
+    double rmin = ax * cx[0] + ay * cy[0], rmax = rmin;
+    for (int j = 0; j < 4; ++j) {
+      const double d = ax * cx[j] + ay * cy[j];
+      rmin = dmin(rmin, d);
+      rmax = dmax(rmax, d);
+    }
+    if (pmax < rmin || pmin > rmax) return false;
+  }
+  return true;
+}
+
+// Row record: prim id, tile row, first and last tile column (ta > tb: empty).
+__global__ void k_rows(int n, const int4* __restrict__ bbox, const int2* __restrict__ hullref,
+                       const double2* __restrict__ pool, const long long* __restrict__ rowoff, CamD cam, OptD opt,
+                       int4* rows, int* rowpaircnt, unsigned long long* counters) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int4 bb = bbox[i];
+  if (bb.y < bb.x || bb.w < bb.z) return;
+  const int2 hr = hullref[i];
+  const double2* h = pool + hr.x;
+  const int hn = hr.y;
+  const double lp = opt.lp_pad;
+  double hy_min = h[0].y, hy_max = h[0].y, amax = 1.0;
+  for (int j = 0; j < hn; ++j) {
+    hy_min = dmin(hy_min, h[j].y);
+    hy_max = dmax(hy_max, h[j].y);
+    amax = dmax(amax, dmax(fabs(h[j].x), fabs(h[j].y)));
+  }
+  const double delta = 1e-9 * amax + 1e-9;
+  long long ro = rowoff[i];
+  unsigned long long ties = 0;
+  for (int ty = bb.z; ty <= bb.w; ++ty, ++ro) {
+    const double y0 = ty * kTile, y1 = y0 + kTile;
+    const double Y0 = y0 - lp, Y1 = y1 + lp;
+    // x-extent of H ∩ [Y0, Y1]
+    double xl = __longlong_as_double(0x7ff0000000000000ll), xr = -xl;
+    for (int j = 0; j < hn; ++j) {
+      const double2 a = h[j];
+      if (a.y >= Y0 && a.y <= Y1) {
+        xl = dmin(xl, a.x);
+        xr = dmax(xr, a.x);
+      }
+      if (hn > 1) {
+        const double2 b = h[(j + 1) % hn];
+        const double Ys[2] = {Y0, Y1};
+        for (int e = 0; e < 2; ++e) {
+          const double Yc = Ys[e];
+          if ((a.y < Yc && b.y > Yc) || (a.y > Yc && b.y < Yc)) {
+            const double xc = a.x + (Yc - a.y) * (b.x - a.x) / (b.y - a.y);
+            xl = dmin(xl, xc);
+            xr = dmax(xr, xc);
+          }
+        }
+      }
+    }
+    const bool row_ambiguous = fabs(hy_max - Y0) <= delta || fabs(hy_min - Y1) <= delta;
+    int ta = bb.x, tb = bb.x - 1;
+    if (row_ambiguous) {
+      // resolve every tile of the row with the reference test
+      ++ties;
+      int first = -1, last = -2;
+      for (int tx = bb.x; tx <= bb.y; ++tx) {
+        const double x0 = tx * kTile, x1 = x0 + kTile;
+        if (hull_overlaps_rect(h, hn, x0 - lp, Y0, x1 + lp, Y1)) {
+          if (first < 0) first = tx;
+          last = tx;
+        }
+      }
+      if (first >= 0) {
+        ta = first;
+        tb = last;
+      }
+    } else if (xl <= xr) {
+      // first tile with X1 >= xl, last tile with X0 <= xr
+      int a = bb.x;
+      while (a <= bb.y && (a * kTile + kTile + lp) < xl - delta) ++a;
+      int b = bb.y;
+      while (b >= a && (b * kTile - lp) > xr + delta) --b;
+      if (a <= b) {
+        // boundary tiles inside the tie band: reference test decides
+        const double x0a = a * kTile, x1a = x0a + kTile;
+        if (fabs((x1a + lp) - xl) <= delta || fabs((x0a - lp) - xr) <= delta) {
+          ++ties;
+          if (!hull_overlaps_rect(h, hn, x0a - lp, Y0, x1a + lp, Y1)) ++a;
+        }
+        if (b >= a) {
+          const double x0b = b * kTile, x1b = x0b + kTile;
+          if (fabs((x0b - lp) - xr) <= delta || fabs((x1b + lp) - xl) <= delta) {
+            ++ties;
+            if (!hull_overlaps_rect(h, hn, x0b - lp, Y0, x1b + lp, Y1)) --b;
+          }
+        }
+        ta = a;
+        tb = b;
+      }
+    }
+    rows[ro] = make_int4(i, ty, ta, tb);
+    rowpaircnt[ro] = tb >= ta ? tb - ta + 1 : 0;
+  }
+  if (ties) atomicAdd(&counters[C_NEAR_TIES], ties);
+}
+
+// Corner rays of the tile grid ((tiles_x+1) x (tiles_y+1)) and tile-centre
+// rays, pixel_ray at the undilated tile corners (raster.cpp:101-102).
+__global__ void k_tile_rays(CamD cam, double* cdirs, double* tdirs) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nc = (cam.tiles_x + 1) * (cam.tiles_y + 1);
+  const int nt = cam.tiles_x * cam.tiles_y;
+  double d[3];
+  if (idx < nc) {
+    const int cx = idx % (cam.tiles_x + 1), cy = idx / (cam.tiles_x + 1);
+    pixel_dir(cam, (double)(cx * kTile), (double)(cy * kTile), d);
+    for (int a = 0; a < 3; ++a) cdirs[3 * (size_t)idx + a] = d[a];
+  } else if (idx < nc + nt) {
+    const int t = idx - nc;
+    const double x0 = (t % cam.tiles_x) * kTile, y0 = (t / cam.tiles_x) * kTile;
+    pixel_dir(cam, 0.5 * (x0 + (x0 + kTile)), 0.5 * (y0 + (y0 + kTile)), d);
+    for (int a = 0; a < 3; ++a) tdirs[3 * (size_t)t + a] = d[a];
+  }
+}
+
+// classify_intersect depth only (geometry.cpp:40-48).
+__device__ __forceinline__ bool hit_depth(const double* d, const Geo& g, double eps, double* rt) {
+  const double denom = d[0] * g.rz[0] + d[1] * g.rz[1] + d[2] * g.rz[2];
+  if (fabs(denom) < eps) return false;
+  const double r = g.num / denom;
+  if (r <= 0) return false;
+  *rt = r;
+  return true;
+}
+
+// K3: emit (key, tile|pid) pairs row by row (raster.cpp:233-257).
+__global__ void k_emit(long long n_rows, const int4* __restrict__ rows, const long long* __restrict__ rowpairoff,
+                       const Geo* __restrict__ geo, const double* __restrict__ cdirs,
+                       const double* __restrict__ tdirs, CamD cam, OptD opt, unsigned long long* pk,
+                       unsigned long long* pv, int* tilecnt) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  const int4 rr = rows[r];
+  if (rr.w < rr.z) return;
+  const int pid = rr.x, ty = rr.y;
+  const Geo g = geo[pid];
+  long long pos = rowpairoff[r];
+  const int cw = cam.tiles_x + 1;
+  for (int tx = rr.z; tx <= rr.w; ++tx, ++pos) {
+    double key;
+    if (opt.presort == 0) {
+      key = (double)pid;
+    } else if (opt.presort == 1) {
+      key = g.projz;
+    } else {
+      // nearest_depth_key (raster.cpp:99-115): corners (x0,y0) (x1,y0) (x1,y1) (x0,y1), centre
+      const int c00 = ty * cw + tx;
+      const double* dirs[5] = {cdirs + 3 * (size_t)c00, cdirs + 3 * (size_t)(c00 + 1),
+                               cdirs + 3 * (size_t)(c00 + cw + 1), cdirs + 3 * (size_t)(c00 + cw),
+                               tdirs + 3 * (size_t)(ty * cam.tiles_x + tx)};
+      double best = __longlong_as_double(0x7ff0000000000000ll);
+      for (int q = 0; q < 5; ++q) {
+        const double d[3] = {dirs[q][0], dirs[q][1], dirs[q][2]};
+        double rt;
+        if (hit_depth(d, g, opt.grazing_eps, &rt)) best = dmin(best, rt);
+      }
+      if (isinf(best) && g.has_proj) best = g.projz;
+      key = best;
+    }
+    const int tile = ty * cam.tiles_x + tx;
+    pk[pos] = (unsigned long long)__double_as_longlong(key);
+    pv[pos] = ((unsigned long long)(unsigned)tile << 32) | (unsigned)pid;
+    atomicAdd(&tilecnt[tile], 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms) {
+  Activated& A = c->act;
+  A.n = n;
+  A.K = K;
+  A.terms = terms;
+  A.mu = ensure<double>(c->a_mu, 3 * (size_t)n);
+  A.rot = ensure<double>(c->a_rot, 9 * (size_t)n);
+  A.s = ensure<double>(c->a_s, (size_t)K * n);
+  A.th = ensure<double>(c->a_th, (size_t)K * n);
+  A.eta = ensure<double>(c->a_eta, n);
+  A.tau = ensure<double>(c->a_tau, n);
+  A.o = ensure<double>(c->a_o, n);
+  A.sh = ensure<float>(c->a_sh, (size_t)3 * terms * n);
+  A.ex = ensure<double>(c->a_ex, (size_t)K * n);
+  A.ey = ensure<double>(c->a_ey, (size_t)K * n);
+  A.det = ensure<double>(c->a_det, (size_t)K * n);
+  unsigned long long* ctr = ensure<unsigned long long>(c->counters, C_COUNT);
+  if (!A.mu || !A.rot || !A.s || !A.th || !A.eta || !A.tau || !A.o || !A.sh || !A.ex || !A.ey || !A.det || !ctr)
+    return set_error(c, DRK_ERR_OOM, "activation buffers");
+  cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT, c->stream);
+  if (n > 0)
+    k_activate<<<(n + 127) / 128, 128, 0, c->stream>>>(
+        raw, n, K, terms, const_cast<double*>(A.mu), const_cast<double*>(A.rot), const_cast<double*>(A.s),
+        const_cast<double*>(A.th), const_cast<double*>(A.eta), const_cast<double*>(A.tau),
+        const_cast<double*>(A.o), const_cast<float*>(A.sh), const_cast<double*>(A.ex),
+        const_cast<double*>(A.ey), const_cast<double*>(A.det), ctr);
+  unsigned long long h[C_COUNT];
+  if (int st = cuda_check(c, cudaMemcpyAsync(h, ctr, sizeof h, cudaMemcpyDeviceToHost, c->stream), "activate"))
+    return st;
+  if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "activate")) return st;
+  if (h[C_ERR_NONFINITE]) return set_error(c, DRK_ERR_NONFINITE, "raw parameters contain NaN/Inf");
+  if (h[C_ERR_DEGEN_QUAT]) return set_error(c, DRK_ERR_DEGENERATE_QUAT, "quaternion norm below 1e-12");
+  return DRK_OK;
+}
+
+int launch_shape(drk_ctx* c, const drk_prims* p, int n, int K, int terms) {
+  Activated& A = c->act;
+  A.n = n;
+  A.K = K;
+  A.terms = terms;
+  A.mu = p->mu;
+  A.rot = p->rot;
+  A.s = p->scales;
+  A.th = p->angles;
+  A.eta = p->eta;
+  A.tau = p->tau;
+  A.o = p->opacity;
+  A.sh = p->sh;
+  A.ex = ensure<double>(c->a_ex, (size_t)K * n);
+  A.ey = ensure<double>(c->a_ey, (size_t)K * n);
+  A.det = ensure<double>(c->a_det, (size_t)K * n);
+  if (!A.ex || !A.ey || !A.det) return set_error(c, DRK_ERR_OOM, "shape buffers");
+  if (n > 0)
+    k_shape<<<(n + 127) / 128, 128, 0, c->stream>>>(n, K, A.s, A.th, const_cast<double*>(A.ex),
+                                                   const_cast<double*>(A.ey), const_cast<double*>(A.det));
+  return cuda_check(c, cudaGetLastError(), "shape");
+}
+
+}  // namespace drk
+
+namespace drk {
+#define DRK_PREP_ARGS                                                                                       \
+  Activated A, CamD cam, OptD opt, Geo *geo, int4 *bbox, int2 *hullref, double2 *pool, long long pool_cap, \
+      int *rowcnt, unsigned long long *counters, const int *list, int list_n, double2 *scratch,            \
+      int scratch_cap, int *overflow
+#define DRK_PREP_PASS \
+  A, cam, opt, geo, bbox, hullref, pool, pool_cap, rowcnt, counters, list, list_n, scratch, scratch_cap, overflow
+__global__ void __launch_bounds__(128) k_prep0(DRK_PREP_ARGS) { prep_body<0>(DRK_PREP_PASS); }
+__global__ void __launch_bounds__(128) k_prep1(DRK_PREP_ARGS) { prep_body<1>(DRK_PREP_PASS); }
+}  // namespace drk

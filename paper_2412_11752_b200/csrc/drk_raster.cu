@@ -1,0 +1,718 @@
+// K4 forward rasterizer and K5 backward rasterizer (reference raster.cpp:267-430,
+// grad.cpp:16-303), K6 activation backward (grad.cpp:122-159, :370-383).
+//
+// One CTA per 16x16 tile, one thread per pixel.  The tile list is streamed in
+// batches of 256 candidates staged in shared memory (id, ray-plane numerator,
+// plane normal: 36 B each); every pixel intersects the batch in fp64 with the
+// reference op order (bit-identical depths), runs the capacity-8 SortCache
+// (raster.cpp:267-303) in registers, and composites popped entries.  A pixel
+// leaves the stream once saturated; the CTA leaves once all pixels have
+// (__syncthreads_count).  Popped entries outside the kernel's alpha_min
+// support (r2 > (s_max f_vis)^2, proven bound) and outside the low-pass
+// floor's reach skip the kernel evaluation.  The backward kernel re-streams
+// the same decisions (no replay buffer) and rebuilds `rest` from the forward
+// pass's fp64 per-pixel accumulators.
+#include <algorithm>
+
+#include "drk_internal.h"
+
+namespace drk {
+
+template <bool BWD>
+struct Pixel {
+  double dir[3];
+  float basis[16];
+  double px, py;
+  double T, C[3], D, N[3], A;
+  // backward
+  double dC[3], dD, dN[3], dA, rest;
+  bool has_dN;
+  long long n_pop, n_comp;
+  int pix, n_rec;
+  bool err;
+
+  // composite_candidate (raster.cpp:327-362) + backward_pixel (grad.cpp:224-301)
+  // for one popped entry.  Returns false once the pixel saturates.
+  __device__ bool composite(const RasterParams& P, double rt, int id) {
+    const Geo& g = P.geo[id];
+    const double rz0 = g.rz[0], rz1 = g.rz[1], rz2 = g.rz[2];
+    const double denom = dir[0] * rz0 + dir[1] * rz1 + dir[2] * rz2;
+    // u, v (geometry.cpp:48-50)
+    const double h0 = P.cam.o[0] + rt * dir[0] - g.mu[0];
+    const double h1 = P.cam.o[1] + rt * dir[1] - g.mu[1];
+    const double h2 = P.cam.o[2] + rt * dir[2] - g.mu[2];
+    const double u = g.rx[0] * h0 + g.rx[1] * h1 + g.rx[2] * h2;
+    const double v = g.ry[0] * h0 + g.ry[1] * h1 + g.ry[2] * h2;
+    ++n_pop;
+    const double cos_view = fabs(denom);
+    double dpw = 0, dph = 0;
+    if (g.has_proj) {
+      dpw = px - g.ppx;
+      dph = py - g.ppy;
+    }
+    // Cheap reject: alpha_kernel < alpha_min whenever r2^2 / s_max^2 > f_vis^2
+    // (Q >= r2^2 / s_max^2), and the low-pass floor < alpha_min whenever
+    // dp^2 > 2 cos^2 s_l^2 ln(o / alpha_min); both with a 1e-9 margin.
+    const double r2 = u * u + v * v;
+    if (r2 > g.r2max && (!g.has_proj || dpw * dpw + dph * dph > cos_view * cos_view * g.dp2max)) return true;
+    KEval ev;
+    eval_kernel(u, v, P.S, id, ev);
+    if (ev.degenerate) {
+      err = true;
+      return false;
+    }
+    const double o = P.S.o[id], tau = P.S.tau[id];
+    const double a_kernel = o * sharpen(ev.g, tau);
+    double a = a_kernel;
+    bool lp = false;
+    if (g.has_proj) {
+      const double f = low_pass_filter_term(dpw, dph, cos_view, o, P.opt.lowpass_radius);
+      if (f > a_kernel) {
+        a = f;
+        lp = true;
+      }
+    }
+    if (a < P.opt.alpha_min) return true;
+    a = dmin(a, 1.0 - 1e-6);
+    // SH colour (geometry.cpp:126-138) in fp32
+    const float* shp = P.sh + (size_t)id * P.terms * 3;
+    float r0 = 0.5f, r1 = 0.5f, r2c = 0.5f;
+    for (int t = 0; t < P.opt.terms_active; ++t) {
+      r0 += basis[t] * __ldg(shp + 3 * t);
+      r1 += basis[t] * __ldg(shp + 3 * t + 1);
+      r2c += basis[t] * __ldg(shp + 3 * t + 2);
+    }
+    const bool cl0 = r0 < 0, cl1 = r1 < 0, cl2 = r2c < 0;
+    const double rgb[3] = {cl0 ? 0.0 : (double)r0, cl1 ? 0.0 : (double)r1, cl2 ? 0.0 : (double)r2c};
+    const double sgn = denom < 0 ? 1.0 : -1.0;
+    const double w = T * a;
+    ++n_comp;
+    if (!BWD) {
+      C[0] += w * rgb[0];
+      C[1] += w * rgb[1];
+      C[2] += w * rgb[2];
+      D += w * rt;
+      N[0] += w * (sgn * rz0);
+      N[1] += w * (sgn * rz1);
+      N[2] += w * (sgn * rz2);
+      A += w;
+      if (P.replay_cap > 0) {
+        if (n_rec < P.replay_cap) {
+          const size_t r = (size_t)pix * P.replay_cap + n_rec;
+          P.replay_ids[r] = id;
+          double* rec = P.replay_rec + 5 * r;
+          rec[0] = u;
+          rec[1] = v;
+          rec[2] = rt;
+          rec[3] = a;
+          rec[4] = lp ? 1.0 : 0.0;
+        }
+        ++n_rec;
+      }
+    } else {
+      backward_record(P, id, g, rt, u, v, a, lp, ev, rgb, cl0, cl1, cl2, sgn, denom, dpw, dph, w);
+    }
+    T *= 1.0 - a;
+    return T >= P.opt.early_stop;
+  }
+
+  __device__ void backward_record(const RasterParams& P, int id, const Geo& g, double rt, double u, double v,
+                                  double a, bool lp, const KEval& ev, const double rgb[3], bool cl0, bool cl1,
+                                  bool cl2, double sgn, double rdz, double dpw, double dph, double wb) {
+    double* pg = P.gact + (size_t)id * P.G;
+    const int K = P.S.K;
+    const double rz[3] = {g.rz[0], g.rz[1], g.rz[2]};
+    const double cw = (dC[0] * rgb[0] + dC[1] * rgb[1] + dC[2] * rgb[2]) + dD * rt +
+                      (dN[0] * (sgn * rz[0]) + dN[1] * (sgn * rz[1]) + dN[2] * (sgn * rz[2])) + dA;
+    rest -= wb * cw;
+    const double dat = T * cw - rest / (1.0 - a);
+    P.touched[id] = 1;
+    const int o_rot = 3, o_sc = 12, o_an = 12 + K, o_eta = 12 + 2 * K, o_tau = o_eta + 1, o_op = o_eta + 2,
+              o_sh = o_eta + 3;
+    // SH (linear, clamped channels gated)
+    const bool cl[3] = {cl0, cl1, cl2};
+    for (int ch = 0; ch < 3; ++ch) {
+      if (cl[ch]) continue;
+      const double dc = wb * dC[ch];
+      if (dc == 0) continue;
+      for (int t = 0; t < P.opt.terms_active; ++t) atomicAdd(pg + o_sh + 3 * t + ch, dc * (double)basis[t]);
+    }
+    if (has_dN)
+      for (int q = 0; q < 3; ++q) atomicAdd(pg + o_rot + 3 * q + 2, wb * sgn * dN[q]);
+    if (dD != 0) {
+      const double d_rt = wb * dD;
+      for (int q = 0; q < 3; ++q) {
+        const double h = P.cam.o[q] + rt * dir[q] - g.mu[q];
+        atomicAdd(pg + q, d_rt * rz[q] / rdz);
+        atomicAdd(pg + o_rot + 3 * q + 2, d_rt * (-h / rdz));
+      }
+    }
+    const bool alpha_clamped = a >= 1.0 - 1e-6 - 1e-12;
+    if (alpha_clamped) return;
+    const double o = P.S.o[id];
+    if (lp) {
+      const double cv = fabs(rdz), sl = P.opt.lowpass_radius;
+      atomicAdd(pg + o_op, dat * a / o);
+      const double inv = 1.0 / (cv * cv * sl * sl);
+      const double d_dpw = dat * a * (-dpw * inv);
+      const double d_dph = dat * a * (-dph * inv);
+      const double d_cos = dat * a * (dpw * dpw + dph * dph) * inv / cv;
+      double J[6];
+      projection_jacobian(P.cam, g.mu, J);
+      for (int q = 0; q < 3; ++q) atomicAdd(pg + q, -(J[q] * d_dpw + J[3 + q] * d_dph));
+      const double sg = rdz < 0 ? -1.0 : 1.0;
+      for (int q = 0; q < 3; ++q) atomicAdd(pg + o_rot + 3 * q + 2, d_cos * sg * dir[q]);
+      return;
+    }
+    // backward_alpha (grad.cpp:16-101)
+    const double tau = P.S.tau[id];
+    const double d_alpha = dat;
+    atomicAdd(pg + o_op, d_alpha * sharpen(ev.g, tau));
+    if (ev.center) return;
+    const int br = sharpen_branch(ev.g, tau);
+    atomicAdd(pg + o_tau, d_alpha * o * sharpen_dtau(br, ev.g, tau));
+    if (ev.clamped) return;
+    const double d_g = d_alpha * o * sharpen_slope(br, tau);
+    const double d_q = d_g * (-0.5 * ev.g);
+    const int lo = ev.lo, hi = ev.hi;
+    const double* s = P.S.s + (size_t)id * K;
+    const double* th = P.S.th + (size_t)id * K;
+    const double slo = s[lo], shi = s[hi], eta = P.S.eta[id];
+    atomicAdd(pg + o_eta, d_q * (ev.r1 * ev.r1 - ev.r2 * ev.inv_sbar));
+    const double d_r1 = d_q * eta * 2.0 * ev.r1;
+    const double d_r2sq = d_q * (1.0 - eta) * ev.inv_sbar;
+    const double d_inv = d_q * (1.0 - eta) * ev.r2;
+    const double c = cos(ev.delta);
+    double ds_lo = d_inv * (-(1.0 + c) / (slo * slo * slo));
+    double ds_hi = d_inv * (-(1.0 - c) / (shi * shi * shi));
+    const double d_c = d_inv * (0.5 / (slo * slo) - 0.5 / (shi * shi));
+    const double d_delta = d_c * (-sin(ev.delta));
+    double alo = th[lo], ahi = th[hi], theta = ev.theta;
+    if (hi == 0) {
+      alo -= kTwoPi;
+      if (theta > th[K - 1]) theta -= kTwoPi;
+    }
+    const double gap = ahi - alo;
+    const double d_tfd = d_delta * kPi / gap;
+    double da_lo = d_delta * kPi * (theta - ahi) / (gap * gap);
+    double da_hi = d_delta * (-kPi) * (theta - alo) / (gap * gap);
+    const double r2s = dmax(ev.r2, 1e-24);
+    double du = d_tfd * (-v / r2s);
+    double dv = d_tfd * (u / r2s);
+    du += d_r2sq * 2.0 * u;
+    dv += d_r2sq * 2.0 * v;
+    const double sa = ev.a > 0 ? 1 : (ev.a < 0 ? -1 : 0);
+    const double sb = ev.b > 0 ? 1 : (ev.b < 0 ? -1 : 0);
+    const double elx = P.S.ex[(size_t)id * K + lo], ely = P.S.ey[(size_t)id * K + lo];
+    const double ehx = P.S.ex[(size_t)id * K + hi], ehy = P.S.ey[(size_t)id * K + hi];
+    const double det = P.S.det[(size_t)id * K + lo];
+    du += d_r1 * (sa * ((ehy * 1.0 - ehx * 0.0) / det) + sb * ((-ely * 1.0 + elx * 0.0) / det));
+    dv += d_r1 * (sa * ((ehy * 0.0 - ehx * 1.0) / det) + sb * ((-ely * 0.0 + elx * 1.0) / det));
+    const double ca = cos(th[lo]), sa_lo = sin(th[lo]);
+    const double cb = cos(th[hi]), sb_hi = sin(th[hi]);
+    ds_lo += d_r1 * (-sa * ev.a / slo);
+    ds_hi += d_r1 * (-sb * ev.b / shi);
+    const double tlx = -slo * sa_lo, tly = slo * ca, thx = -shi * sb_hi, thy = shi * cb;
+    const double na = -ev.a, nb = -ev.b;
+    const double dtl_x = na * ((ehy * tlx - ehx * tly) / det), dtl_y = na * ((-ely * tlx + elx * tly) / det);
+    const double dth_x = nb * ((ehy * thx - ehx * thy) / det), dth_y = nb * ((-ely * thx + elx * thy) / det);
+    da_lo += d_r1 * (sa * dtl_x + sb * dtl_y);
+    da_hi += d_r1 * (sa * dth_x + sb * dth_y);
+    atomicAdd(pg + o_sc + lo, ds_lo);
+    atomicAdd(pg + o_sc + hi, ds_hi);
+    atomicAdd(pg + o_an + lo, da_lo);
+    atomicAdd(pg + o_an + hi, da_hi);
+    // (u, v) and r_t chain to centre and rotation columns (grad.cpp:290-300)
+    const double h[3] = {P.cam.o[0] + rt * dir[0] - g.mu[0], P.cam.o[1] + rt * dir[1] - g.mu[1],
+                         P.cam.o[2] + rt * dir[2] - g.mu[2]};
+    const double drx = dir[0] * g.rx[0] + dir[1] * g.rx[1] + dir[2] * g.rx[2];
+    const double dry = dir[0] * g.ry[0] + dir[1] * g.ry[1] + dir[2] * g.ry[2];
+    for (int q = 0; q < 3; ++q) {
+      const double du_dmu = rz[q] * (drx / rdz) - g.rx[q];
+      const double dv_dmu = rz[q] * (dry / rdz) - g.ry[q];
+      atomicAdd(pg + q, du * du_dmu + dv * dv_dmu);
+    }
+    const double f = -(du * drx + dv * dry) / rdz;
+    for (int q = 0; q < 3; ++q) {
+      atomicAdd(pg + o_rot + 3 * q + 0, du * h[q]);
+      atomicAdd(pg + o_rot + 3 * q + 1, dv * h[q]);
+      atomicAdd(pg + o_rot + 3 * q + 2, f * h[q]);
+    }
+  }
+};
+
+// MODE 0: SortCache streaming; MODE 1: list order (use_cache = false).
+template <int MODE, bool BWD>
+__global__ void __launch_bounds__(256) k_raster(RasterParams P) {
+  __shared__ int s_id[256];
+  __shared__ double s_num[256], s_r0[256], s_r1[256], s_r2[256];
+  const int tile = blockIdx.x;
+  const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
+  const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
+  const bool active = x < P.cam.W && y < P.cam.H;
+  Pixel<BWD> px;
+  px.px = x + 0.5;
+  px.py = y + 0.5;
+  pixel_dir(P.cam, px.px, px.py, px.dir);
+  sh_basis_f((float)px.dir[0], (float)px.dir[1], (float)px.dir[2], P.opt.sh_degree, px.basis);
+  px.T = 1.0;
+  px.C[0] = px.C[1] = px.C[2] = px.D = px.N[0] = px.N[1] = px.N[2] = px.A = 0;
+  px.n_pop = px.n_comp = 0;
+  px.n_rec = 0;
+  px.err = false;
+  px.pix = y * P.cam.W + x;
+  if (BWD && active) {
+    const size_t p = (size_t)px.pix;
+    px.dC[0] = P.dC ? P.dC[3 * p] : 0.f;
+    px.dC[1] = P.dC ? P.dC[3 * p + 1] : 0.f;
+    px.dC[2] = P.dC ? P.dC[3 * p + 2] : 0.f;
+    px.dD = P.dD ? P.dD[p] : 0.f;
+    px.has_dN = P.dN != nullptr;
+    px.dN[0] = P.dN ? P.dN[3 * p] : 0.f;
+    px.dN[1] = P.dN ? P.dN[3 * p + 1] : 0.f;
+    px.dN[2] = P.dN ? P.dN[3 * p + 2] : 0.f;
+    px.dA = P.dA ? P.dA[p] : 0.f;
+    const double* st = P.pxstate + 8 * p;
+    // total = dC.C + dD D + dN.N + dA A (C includes T_n bg): grad.cpp:210-222
+    px.rest = (px.dC[0] * st[0] + px.dC[1] * st[1] + px.dC[2] * st[2]) + px.dD * st[3] +
+              (px.dN[0] * st[4] + px.dN[1] * st[5] + px.dN[2] * st[6]) + px.dA * st[7];
+  }
+  bool done = !active;
+  long long streamed = 0;
+  double cd[kCacheCap];
+  int ci[kCacheCap];
+  int csz = 0;
+  const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
+  const double eps = P.opt.grazing_eps;
+  for (long long b0 = beg; b0 < end; b0 += 256) {
+    __syncthreads();
+    const long long j = b0 + threadIdx.x;
+    if (j < end) {
+      const int id = (int)(P.pv[j] & 0xffffffffull);
+      const Geo& g = P.geo[id];
+      s_id[threadIdx.x] = id;
+      s_num[threadIdx.x] = g.num;
+      s_r0[threadIdx.x] = g.rz[0];
+      s_r1[threadIdx.x] = g.rz[1];
+      s_r2[threadIdx.x] = g.rz[2];
+    }
+    __syncthreads();
+    const int cnt = (int)min((long long)256, end - b0);
+    if (!done) {
+      for (int c = 0; c < cnt; ++c) {
+        // classify_intersect (geometry.cpp:40-46)
+        const double denom = px.dir[0] * s_r0[c] + px.dir[1] * s_r1[c] + px.dir[2] * s_r2[c];
+        if (fabs(denom) < eps) continue;
+        const double rt = s_num[c] / denom;
+        if (rt <= 0) continue;
+        ++streamed;
+        const int id = s_id[c];
+        if (MODE == 1) {
+          if (!px.composite(P, rt, id)) {
+            done = true;
+            break;
+          }
+          continue;
+        }
+        // SortCache::step (raster.cpp:267-303)
+        int pos = 0;
+#pragma unroll
+        for (int q = 0; q < kCacheCap; ++q) pos += (q < csz && cd[q] <= rt) ? 1 : 0;
+        if (csz < kCacheCap) {
+#pragma unroll
+          for (int q = kCacheCap - 1; q > 0; --q)
+            if (q > pos) {
+              cd[q] = cd[q - 1];
+              ci[q] = ci[q - 1];
+            }
+#pragma unroll
+          for (int q = 0; q < kCacheCap; ++q)
+            if (q == pos) {
+              cd[q] = rt;
+              ci[q] = id;
+            }
+          ++csz;
+          continue;
+        }
+        double prt;
+        int pid;
+        if (pos == 0) {  // incoming is the new minimum: pops straight through
+          prt = rt;
+          pid = id;
+        } else {
+          prt = cd[0];
+          pid = ci[0];
+#pragma unroll
+          for (int q = 0; q < kCacheCap; ++q) {
+            if (q < pos - 1) {
+              if (q + 1 < kCacheCap) {
+                cd[q] = cd[q + 1];
+                ci[q] = ci[q + 1];
+              }
+            } else if (q == pos - 1) {
+              cd[q] = rt;
+              ci[q] = id;
+            }
+          }
+        }
+        if (!px.composite(P, prt, pid)) {
+          done = true;
+          break;
+        }
+      }
+    }
+    if (__syncthreads_count(!done) == 0) break;
+  }
+  // end marker: drain the cache head first (raster.cpp:410-414)
+  if (MODE == 0) {
+    while (!done && csz > 0) {
+      const double prt = cd[0];
+      const int pid = ci[0];
+#pragma unroll
+      for (int q = 0; q < kCacheCap - 1; ++q) {
+        cd[q] = cd[q + 1];
+        ci[q] = ci[q + 1];
+      }
+      --csz;
+      if (!px.composite(P, prt, pid)) done = true;
+    }
+  }
+  if (!active) return;
+  if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
+  if (!BWD) {
+    const size_t p = (size_t)px.pix;
+    const double c0 = px.C[0] + px.T * P.opt.bg[0];
+    const double c1 = px.C[1] + px.T * P.opt.bg[1];
+    const double c2 = px.C[2] + px.T * P.opt.bg[2];
+    if (P.color) {
+      P.color[3 * p] = (float)c0;
+      P.color[3 * p + 1] = (float)c1;
+      P.color[3 * p + 2] = (float)c2;
+    }
+    if (P.normal) {
+      P.normal[3 * p] = (float)px.N[0];
+      P.normal[3 * p + 1] = (float)px.N[1];
+      P.normal[3 * p + 2] = (float)px.N[2];
+    }
+    if (P.depth) P.depth[p] = (float)px.D;
+    if (P.alpha) P.alpha[p] = (float)px.A;
+    if (P.pxstate) {
+      double* st = P.pxstate + 8 * p;
+      st[0] = c0;
+      st[1] = c1;
+      st[2] = c2;
+      st[3] = px.D;
+      st[4] = px.N[0];
+      st[5] = px.N[1];
+      st[6] = px.N[2];
+      st[7] = px.A;
+    }
+    if (P.replay_cap > 0) {
+      P.replay_cnt[p] = px.n_rec;
+      if (px.n_rec > P.replay_cap) atomicAdd(&P.counters[C_REPLAY_OVERFLOW], 1ull);
+    }
+    // work counters (warp-aggregated)
+    unsigned long long s = streamed, pp = px.n_pop, cc = px.n_comp;
+    for (int off = 16; off > 0; off >>= 1) {
+      s += __shfl_down_sync(__activemask(), s, off);
+      pp += __shfl_down_sync(__activemask(), pp, off);
+      cc += __shfl_down_sync(__activemask(), cc, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&P.counters[C_STREAMED], s);
+      atomicAdd(&P.counters[C_POPPED], pp);
+      atomicAdd(&P.counters[C_COMPOSITED], cc);
+    }
+  }
+}
+
+// exact_sort oracle mode (raster.cpp:395-401): every hit composited in
+// stable depth order.  One thread per pixel, selection by (depth, list index).
+template <bool BWD>
+__global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
+  const int tile = blockIdx.y;
+  const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= 256) return;
+  const int x = tx * kTile + (l & 15), y = ty * kTile + (l >> 4);
+  if (x >= P.cam.W || y >= P.cam.H) return;
+  Pixel<BWD> px;
+  px.px = x + 0.5;
+  px.py = y + 0.5;
+  pixel_dir(P.cam, px.px, px.py, px.dir);
+  sh_basis_f((float)px.dir[0], (float)px.dir[1], (float)px.dir[2], P.opt.sh_degree, px.basis);
+  px.T = 1.0;
+  px.C[0] = px.C[1] = px.C[2] = px.D = px.N[0] = px.N[1] = px.N[2] = px.A = 0;
+  px.n_pop = px.n_comp = 0;
+  px.n_rec = 0;
+  px.err = false;
+  px.pix = y * P.cam.W + x;
+  const size_t p = (size_t)px.pix;
+  if (BWD) {
+    px.dC[0] = P.dC ? P.dC[3 * p] : 0.f;
+    px.dC[1] = P.dC ? P.dC[3 * p + 1] : 0.f;
+    px.dC[2] = P.dC ? P.dC[3 * p + 2] : 0.f;
+    px.dD = P.dD ? P.dD[p] : 0.f;
+    px.has_dN = P.dN != nullptr;
+    px.dN[0] = P.dN ? P.dN[3 * p] : 0.f;
+    px.dN[1] = P.dN ? P.dN[3 * p + 1] : 0.f;
+    px.dN[2] = P.dN ? P.dN[3 * p + 2] : 0.f;
+    px.dA = P.dA ? P.dA[p] : 0.f;
+    const double* st = P.pxstate + 8 * p;
+    px.rest = (px.dC[0] * st[0] + px.dC[1] * st[1] + px.dC[2] * st[2]) + px.dD * st[3] +
+              (px.dN[0] * st[4] + px.dN[1] * st[5] + px.dN[2] * st[6]) + px.dA * st[7];
+  }
+  const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
+  double last_d = -1.0;
+  long long last_j = -1;
+  while (true) {
+    double best_d = 0;
+    long long best_j = -1;
+    for (long long j = beg; j < end; ++j) {
+      const int id = (int)(P.pv[j] & 0xffffffffull);
+      const Geo& g = P.geo[id];
+      const double denom = px.dir[0] * g.rz[0] + px.dir[1] * g.rz[1] + px.dir[2] * g.rz[2];
+      if (fabs(denom) < P.opt.grazing_eps) continue;
+      const double rt = g.num / denom;
+      if (rt <= 0) continue;
+      const bool after_last = rt > last_d || (rt == last_d && j > last_j);
+      if (!after_last) continue;
+      if (best_j < 0 || rt < best_d) {
+        best_d = rt;
+        best_j = j;
+      }
+    }
+    if (best_j < 0) break;
+    last_d = best_d;
+    last_j = best_j;
+    if (!px.composite(P, best_d, (int)(P.pv[best_j] & 0xffffffffull))) break;
+  }
+  if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
+  if (!BWD) {
+    const double c0 = px.C[0] + px.T * P.opt.bg[0];
+    const double c1 = px.C[1] + px.T * P.opt.bg[1];
+    const double c2 = px.C[2] + px.T * P.opt.bg[2];
+    if (P.color) {
+      P.color[3 * p] = (float)c0;
+      P.color[3 * p + 1] = (float)c1;
+      P.color[3 * p + 2] = (float)c2;
+    }
+    if (P.normal) {
+      P.normal[3 * p] = (float)px.N[0];
+      P.normal[3 * p + 1] = (float)px.N[1];
+      P.normal[3 * p + 2] = (float)px.N[2];
+    }
+    if (P.depth) P.depth[p] = (float)px.D;
+    if (P.alpha) P.alpha[p] = (float)px.A;
+    if (P.pxstate) {
+      double* st = P.pxstate + 8 * p;
+      st[0] = c0;
+      st[1] = c1;
+      st[2] = c2;
+      st[3] = px.D;
+      st[4] = px.N[0];
+      st[5] = px.N[1];
+      st[6] = px.N[2];
+      st[7] = px.A;
+    }
+    if (P.replay_cap > 0) {
+      P.replay_cnt[p] = px.n_rec;
+      if (px.n_rec > P.replay_cap) atomicAdd(&P.counters[C_REPLAY_OVERFLOW], 1ull);
+    }
+  }
+}
+
+void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s) {
+  if (n_tiles == 0) return;
+  if (P.opt.exact_sort) {
+    dim3 grid(2, n_tiles);
+    if (bwd) k_raster_exact<true><<<grid, 128, 0, s>>>(P);
+    else k_raster_exact<false><<<grid, 128, 0, s>>>(P);
+  } else if (P.opt.use_cache) {
+    if (bwd) k_raster<0, true><<<n_tiles, 256, 0, s>>>(P);
+    else k_raster<0, false><<<n_tiles, 256, 0, s>>>(P);
+  } else {
+    if (bwd) k_raster<1, true><<<n_tiles, 256, 0, s>>>(P);
+    else k_raster<1, false><<<n_tiles, 256, 0, s>>>(P);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6: activation backward (grad.cpp:122-159) + screen_grad (grad.cpp:375-383)
+// ---------------------------------------------------------------------------
+__global__ void k_act_bwd(int n, int K, int terms, const float* __restrict__ raw, const double* __restrict__ gact,
+                          int G, const unsigned char* __restrict__ touched_dev, const Geo* __restrict__ geo, CamD cam,
+                          float* grad_raw, float* d_center_world, float* screen_grad, unsigned char* touched_out,
+                          int accumulate) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* g = gact + (size_t)i * G;
+  const int tch = touched_dev[i];
+  if (d_center_world)
+    for (int a = 0; a < 3; ++a) d_center_world[3 * i + a] = (float)g[a];
+  if (touched_out) touched_out[i] = (unsigned char)tch;
+  if (screen_grad) {
+    double sgv = 0;
+    if (tch && geo[i].has_proj) {
+      double J[6];
+      projection_jacobian(cam, geo[i].mu, J);
+      const double jx = J[0] * g[0] + J[1] * g[1] + J[2] * g[2];
+      const double jy = J[3] * g[0] + J[4] * g[1] + J[5] * g[2];
+      sgv = sqrt(jx * jx + jy * jy);
+    }
+    screen_grad[i] = (float)sgv;
+  }
+  if (!grad_raw || !raw) return;
+#define RAW(j) ((double)raw[(size_t)(j)*n + i])
+  double out[3 + 4 + 2 * kMaxK + 3];
+  for (int a = 0; a < 3; ++a) out[a] = g[a];
+  // quat_rotation_backward (grad.cpp:122-141)
+  const double q[4] = {RAW(3), RAW(4), RAW(5), RAW(6)};
+  const double qn = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const double qh[4] = {q[0] / qn, q[1] / qn, q[2] / qn, q[3] / qn};
+  const double w = qh[0], x = qh[1], y = qh[2], z = qh[3];
+  const double Ms[4][9] = {{0, -z, y, z, 0, -x, -y, x, 0},
+                           {0, y, z, y, -2 * x, -w, z, w, -2 * x},
+                           {-2 * y, x, w, x, 0, z, -w, z, -2 * y},
+                           {-2 * z, -w, x, w, -2 * z, y, x, y, 0}};
+  const double* dR = g + 3;
+  double dqh[4];
+  for (int m = 0; m < 4; ++m) {
+    double acc = Ms[m][0] * dR[0];
+    for (int idx = 1; idx < 9; ++idx) {
+      const int r = idx % 3, c = idx / 3;  // column-major storage order of Eigen's sum
+      acc = acc + Ms[m][3 * r + c] * dR[3 * r + c];
+    }
+    dqh[m] = 2.0 * acc;
+  }
+  const double dd = qh[0] * dqh[0] + qh[1] * dqh[1] + qh[2] * dqh[2] + qh[3] * dqh[3];
+  for (int m = 0; m < 4; ++m) out[3 + m] = (dqh[m] - qh[m] * dd) / qn;
+  for (int j = 0; j < K; ++j) out[7 + j] = g[12 + j] * exp(RAW(7 + j));
+  // angle_activation_jacobian (core.cpp:110-131), out = J^T d_angles
+  const double residual = 1.0 / (K - 2);
+  double dstep[kMaxK], cum[kMaxK], total = 0;
+  for (int j = 0; j < K; ++j) {
+    const double sg = sigmoid(RAW(7 + K + j));
+    const bool clmp = sg < 1e-9 || sg > 1.0 - 1e-9;
+    const double sc = sg < 1e-9 ? 1e-9 : (1.0 - 1e-9 < sg ? 1.0 - 1e-9 : sg);
+    dstep[j] = clmp ? 0.0 : sg * (1.0 - sg);
+    total += sc + residual;
+    cum[j] = total;
+  }
+  for (int c = 0; c < K; ++c) {
+    double acc = 0;
+    for (int r = 0; r < K; ++r) {
+      const double ind = (c <= r) ? 1.0 : 0.0;
+      const double jac = (r == K - 1) ? 0.0 : kTwoPi / total * (ind - cum[r] / total) * dstep[c];
+      acc = (r == 0) ? jac * g[12 + K + r] : acc + jac * g[12 + K + r];
+    }
+    out[7 + K + c] = acc;
+  }
+  const double eta = sigmoid(RAW(7 + 2 * K));
+  out[7 + 2 * K] = g[12 + 2 * K] * eta * (1.0 - eta);
+  const double st = sigmoid(RAW(8 + 2 * K));
+  out[8 + 2 * K] = g[13 + 2 * K] * (kTauHigh - kTauLow) * st * (1.0 - st);
+  const double o = sigmoid(RAW(9 + 2 * K));
+  out[9 + 2 * K] = g[14 + 2 * K] * o * (1.0 - o);
+#undef RAW
+  const int S0 = 10 + 2 * K;
+  for (int j = 0; j < S0; ++j) {
+    float* dst = grad_raw + (size_t)j * n + i;
+    *dst = accumulate ? *dst + (float)out[j] : (float)out[j];
+  }
+  for (int j = 0; j < 3 * terms; ++j) {
+    float* dst = grad_raw + (size_t)(S0 + j) * n + i;
+    const float val = (float)g[15 + 2 * K + j];
+    *dst = accumulate ? *dst + val : val;
+  }
+}
+
+void launch_act_bwd(int n, int K, int terms, const float* raw, const double* gact, int G,
+                    const unsigned char* touched_dev, const Geo* geo, const CamD& cam, float* grad_raw,
+                    float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
+                    cudaStream_t s) {
+  if (n == 0) return;
+  k_act_bwd<<<(n + 127) / 128, 128, 0, s>>>(n, K, terms, raw, gact, G, touched_dev, geo, cam, grad_raw,
+                                              d_center_world, screen_grad, touched_out, accumulate);
+}
+
+// ---------------------------------------------------------------------------
+// K7: L1 loss (optimize.cpp:171-204 with dssim_weight = 0)
+// ---------------------------------------------------------------------------
+__global__ void k_l1(long long n, const float* __restrict__ r, const float* __restrict__ t, double inv_n,
+                     double* loss, float* dcol) {
+  double acc = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double d = (double)r[i] - (double)t[i];
+    acc += fabs(d);
+    if (dcol) dcol[i] = (float)(1.0 * inv_n * (d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0)));
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+  __shared__ double sm[32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+    if (threadIdx.x == 0) atomicAdd(loss, acc * inv_n);
+  }
+}
+
+void launch_l1(long long n, const float* r, const float* t, double* loss, float* dcol, cudaStream_t s) {
+  cudaMemsetAsync(loss, 0, sizeof(double), s);
+  if (n == 0) return;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  k_l1<<<blocks, 256, 0, s>>>(n, r, t, 1.0 / (double)n, loss, dcol);
+}
+
+// ---------------------------------------------------------------------------
+// K8: Adam (optimize.cpp:226-307): beta (0.9, 0.999), eps 1e-15, bias
+// corrected, per-class learning rates, SH rows >= 1 at lr_sh / 20.
+// ---------------------------------------------------------------------------
+__global__ void k_adam(long long total, int n, int K, float* p, const float* __restrict__ gr, float* m, float* v,
+                       double bc1, double bc2, double lr_center, double lr_quat, double lr_scale, double lr_angle,
+                       double lr_eta, double lr_tau, double lr_op, double lr_sh, double lr_sh_rest,
+                       double grad_scale) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(e / n);
+    double lr;
+    if (s < 3) lr = lr_center;
+    else if (s < 7) lr = lr_quat;
+    else if (s < 7 + K) lr = lr_scale;
+    else if (s < 7 + 2 * K) lr = lr_angle;
+    else if (s == 7 + 2 * K) lr = lr_eta;
+    else if (s == 8 + 2 * K) lr = lr_tau;
+    else if (s == 9 + 2 * K) lr = lr_op;
+    else lr = (s - (10 + 2 * K)) < 3 ? lr_sh : lr_sh_rest;
+    const double g = (double)gr[e] * grad_scale;
+    const double mm = 0.9 * (double)m[e] + (1.0 - 0.9) * g;
+    const double vv = 0.999 * (double)v[e] + (1.0 - 0.999) * g * g;
+    m[e] = (float)mm;
+    v[e] = (float)vv;
+    const double mh = mm / bc1, vh = vv / bc2;
+    p[e] = (float)((double)p[e] - lr * mh / (sqrt(vh) + 1e-15));
+  }
+}
+
+int run_adam(drk_ctx* c, float* params, const float* grads, float* m, float* v, int n, int K, int terms,
+             int64_t step, const drk_adam_config* cfg) {
+  const long long total = (long long)(3 + 4 + 2 * K + 3 + 3 * terms) * n;
+  const double bc1 = 1.0 - pow(0.9, (double)step);
+  const double bc2 = 1.0 - pow(0.999, (double)step);
+  const double t = cfg->steps > 0 ? dmin(1.0, (double)step / cfg->steps) : 1.0;
+  const double decay = pow(1e-2, t);
+  const double lr_drk = cfg->lr_drk * decay;
+  const double lr_sh = cfg->lr_sh;
+  if (total > 0) {
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+    k_adam<<<blocks, 256, 0, c->stream>>>(total, n, K, params, grads, m, v, bc1, bc2,
+                                           cfg->lr_position * cfg->scene_extent * decay, cfg->lr_rotation, lr_drk,
+                                           cfg->freeze_angles ? 0.0 : lr_drk, cfg->freeze_eta_tau ? 0.0 : lr_drk,
+                                           cfg->freeze_eta_tau ? 0.0 : lr_drk, cfg->lr_opacity, lr_sh, lr_sh / 20.0,
+                                           cfg->grad_scale);
+  }
+  return cuda_check(c, cudaGetLastError(), "adam");
+}
+
+}  // namespace drk

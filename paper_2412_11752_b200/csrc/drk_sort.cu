@@ -1,0 +1,228 @@
+// Device-wide exclusive scan and stable LSD radix sort (hand-written, no CUB).
+//
+// Sort: 8-bit digits, 2048 elements per CTA (8 warps x 32 lanes x 8 items).
+// Per pass: k_rs_hist (per-CTA digit histogram, digit-major layout) ->
+// exclusive scan of the 256 x nblk histogram -> k_rs_scatter (stable ranks via
+// warp match_any + per-warp running counts, then warp prefix per digit).
+// Pairs are (key u64, value u64); the digit comes from either word.  Passes
+// whose digit is constant over all elements are skipped (OR/AND reduction).
+#include "drk_internal.h"
+
+namespace drk {
+
+constexpr int kScanThreads = 256, kScanItems = 4, kScanBlock = kScanThreads * kScanItems;
+
+template <typename T>
+__global__ void k_scan_block(const T* __restrict__ in, long long n, long long* out, long long* bsum) {
+  __shared__ long long sm[kScanThreads];
+  const long long base = (long long)blockIdx.x * kScanBlock + threadIdx.x * kScanItems;
+  long long v[kScanItems], run = 0;
+  for (int k = 0; k < kScanItems; ++k) {
+    const long long idx = base + k;
+    v[k] = idx < n ? (long long)in[idx] : 0;
+    run += v[k];
+  }
+  sm[threadIdx.x] = run;
+  __syncthreads();
+  for (int off = 1; off < kScanThreads; off <<= 1) {
+    const long long t = threadIdx.x >= off ? sm[threadIdx.x - off] : 0;
+    __syncthreads();
+    sm[threadIdx.x] += t;
+    __syncthreads();
+  }
+  long long ex = sm[threadIdx.x] - run;
+  for (int k = 0; k < kScanItems; ++k) {
+    const long long idx = base + k;
+    if (idx < n) out[idx] = ex;
+    ex += v[k];
+  }
+  if (threadIdx.x == kScanThreads - 1) bsum[blockIdx.x] = sm[threadIdx.x];
+}
+
+__global__ void k_scan_add(long long* out, long long n, const long long* __restrict__ bpre) {
+  const long long base = (long long)blockIdx.x * kScanBlock;
+  const long long add = bpre[blockIdx.x];
+  for (int k = threadIdx.x; k < kScanBlock; k += kScanThreads) {
+    const long long idx = base + k;
+    if (idx < n) out[idx] += add;
+  }
+}
+
+// Exclusive scan of n values into out; *total receives the sum (host value;
+// synchronises the stream).  tmp must hold scan_tmp_elems(n) long longs.
+size_t scan_tmp_elems(long long n) {
+  size_t tot = 0;
+  long long m = n;
+  do {
+    m = (m + kScanBlock - 1) / kScanBlock;
+    tot += 2 * (size_t)m + 2;
+  } while (m > 1);
+  return tot + 4;
+}
+
+template <typename T>
+void scan_level(const T* in, long long n, long long* out, long long* tmp, cudaStream_t s) {
+  const long long nb = (n + kScanBlock - 1) / kScanBlock;
+  long long* bsum = tmp;
+  long long* bpre = tmp + nb + 1;
+  k_scan_block<T><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, out, bsum);
+  if (nb > 1) {
+    scan_level<long long>(bsum, nb, bpre, tmp + 2 * nb + 2, s);
+    k_scan_add<<<(unsigned)nb, kScanThreads, 0, s>>>(out, n, bpre);
+  }
+}
+
+template <typename T>
+int exclusive_scan(drk_ctx* c, const T* in, long long n, long long* out, long long* total) {
+  long long* tmp = ensure<long long>(c->scan_tmp, scan_tmp_elems(n) + 1);
+  if (!tmp) return set_error(c, DRK_ERR_OOM, "scan scratch");
+  if (n == 0) {
+    if (total) *total = 0;
+    return DRK_OK;
+  }
+  scan_level<T>(in, n, out, tmp, c->stream);
+  if (total) {
+    long long last_ex = 0;
+    T last_in{};
+    cudaMemcpyAsync(&last_ex, out + n - 1, sizeof(long long), cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(&last_in, in + n - 1, sizeof(T), cudaMemcpyDeviceToHost, c->stream);
+    if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "scan")) return st;
+    *total = last_ex + (long long)last_in;
+  }
+  return cuda_check(c, cudaGetLastError(), "scan");
+}
+
+template int exclusive_scan<int>(drk_ctx*, const int*, long long, long long*, long long*);
+template int exclusive_scan<unsigned>(drk_ctx*, const unsigned*, long long, long long*, long long*);
+
+// ---------------------------------------------------------------------------
+// radix sort
+// ---------------------------------------------------------------------------
+constexpr int kRsWarps = 8, kRsItems = 8, kRsThreads = kRsWarps * 32, kRsChunk = kRsThreads * kRsItems;
+
+__global__ void k_bits(const unsigned long long* __restrict__ k, const unsigned long long* __restrict__ v, long long n,
+                       unsigned long long* acc /* or_k, and_k, or_v, and_v */) {
+  unsigned long long ok = 0, ak = ~0ull, ov = 0, av = ~0ull;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    ok |= k[i];
+    ak &= k[i];
+    ov |= v[i];
+    av &= v[i];
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    ok |= __shfl_down_sync(0xffffffffu, ok, off);
+    ak &= __shfl_down_sync(0xffffffffu, ak, off);
+    ov |= __shfl_down_sync(0xffffffffu, ov, off);
+    av &= __shfl_down_sync(0xffffffffu, av, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(&acc[0], ok);
+    atomicAnd(&acc[1], ak);
+    atomicOr(&acc[2], ov);
+    atomicAnd(&acc[3], av);
+  }
+}
+
+__global__ void __launch_bounds__(kRsThreads) k_rs_hist(const unsigned long long* __restrict__ src, long long n,
+                                                        int shift, unsigned* hist, int nblk) {
+  __shared__ unsigned cnt[256];
+  cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const long long base = (long long)blockIdx.x * kRsChunk;
+  for (int k = 0; k < kRsItems; ++k) {
+    const long long i = base + k * kRsThreads + threadIdx.x;
+    if (i < n) atomicAdd(&cnt[(unsigned)(src[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[(size_t)threadIdx.x * nblk + blockIdx.x] = cnt[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned long long* __restrict__ kin,
+                                                           const unsigned long long* __restrict__ vin,
+                                                           unsigned long long* kout, unsigned long long* vout,
+                                                           long long n, int shift, int digit_from_v,
+                                                           const long long* __restrict__ offs, int nblk) {
+  __shared__ unsigned whist[kRsWarps][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int d = threadIdx.x; d < kRsWarps * 256; d += kRsThreads) (&whist[0][0])[d] = 0;
+  __syncthreads();
+  const long long base = (long long)blockIdx.x * kRsChunk + (long long)warp * 32 * kRsItems;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned long long kk[kRsItems], vv[kRsItems];
+  int dig[kRsItems];
+  unsigned rank[kRsItems];
+#pragma unroll
+  for (int r = 0; r < kRsItems; ++r) {
+    const long long i = base + r * 32 + lane;
+    const bool valid = i < n;
+    kk[r] = valid ? kin[i] : 0;
+    vv[r] = valid ? vin[i] : 0;
+    const int d = valid ? (int)((unsigned)((digit_from_v ? vv[r] : kk[r]) >> shift) & 255u) : 256;
+    dig[r] = d;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned cur = valid ? whist[warp][d] : 0;
+    rank[r] = cur + __popc(peers & lt);
+    __syncwarp();
+    const int leader = 31 - __clz(peers);
+    if (valid && lane == leader) whist[warp][d] = cur + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;  // kRsThreads == 256 digits
+    unsigned run = 0;
+    for (int w = 0; w < kRsWarps; ++w) {
+      const unsigned t = whist[w][d];
+      whist[w][d] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRsItems; ++r) {
+    if (dig[r] == 256) continue;
+    const long long pos = offs[(size_t)dig[r] * nblk + blockIdx.x] + whist[warp][dig[r]] + rank[r];
+    kout[pos] = kk[r];
+    vout[pos] = vv[r];
+  }
+}
+
+// Stable sort of (k, v) pairs, first by the 64-bit key, then by bits [32, 48)
+// of v (the tile id).  Result ends in (k, v) (buffers swapped as needed).
+int sort_pairs(drk_ctx* c, unsigned long long*& k, unsigned long long*& v, unsigned long long*& k2,
+               unsigned long long*& v2, long long n) {
+  if (n <= 1) return DRK_OK;
+  cudaStream_t s = c->stream;
+  unsigned long long* acc = ensure<unsigned long long>(c->bits, 4);
+  const int nblk = (int)((n + kRsChunk - 1) / kRsChunk);
+  unsigned* hist = ensure<unsigned>(c->hist, (size_t)256 * nblk);
+  long long* off = ensure<long long>(c->sortoff, (size_t)256 * nblk);
+  if (!acc || !hist || !off) return set_error(c, DRK_ERR_OOM, "sort scratch");
+  const unsigned long long init[4] = {0ull, ~0ull, 0ull, ~0ull};
+  cudaMemcpyAsync(acc, init, sizeof init, cudaMemcpyHostToDevice, s);
+  k_bits<<<min(nblk * 8, 148 * 8), 256, 0, s>>>(k, v, n, acc);
+  unsigned long long h[4];
+  cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, s);
+  if (int st = cuda_check(c, cudaStreamSynchronize(s), "sort bits")) return st;
+  const unsigned long long vary_k = h[0] ^ h[1], vary_v = h[2] ^ h[3];
+  struct Pass {
+    int shift, from_v;
+  };
+  Pass passes[10];
+  int np = 0;
+  for (int d = 0; d < 8; ++d)
+    if ((vary_k >> (8 * d)) & 255ull) passes[np++] = {8 * d, 0};
+  for (int d = 4; d < 6; ++d)
+    if ((vary_v >> (8 * d)) & 255ull) passes[np++] = {8 * d, 1};
+  for (int p = 0; p < np; ++p) {
+    const unsigned long long* src = passes[p].from_v ? v : k;
+    k_rs_hist<<<nblk, kRsThreads, 0, s>>>(src, n, passes[p].shift, hist, nblk);
+    if (int st = exclusive_scan<unsigned>(c, hist, (long long)256 * nblk, off, nullptr)) return st;
+    k_rs_scatter<<<nblk, kRsThreads, 0, s>>>(k, v, k2, v2, n, passes[p].shift, passes[p].from_v, off, nblk);
+    std::swap(k, k2);
+    std::swap(v, v2);
+  }
+  return cuda_check(c, cudaGetLastError(), "sort");
+}
+
+}  // namespace drk

@@ -1,0 +1,32 @@
+"""Quick per-config forward / backward timing (development aid)."""
+import sys, time
+import numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2412_11752_b200 import scenes
+from paper_2412_11752_b200.api import Rasterizer, RenderOptions, FrameGrad
+
+r = Rasterizer(0)
+for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:
+    sc = scenes.config_scene(cfg)
+    cam = scenes.config_cameras(cfg)[0]
+    raw = torch.from_numpy(sc.f32()).cuda()
+    opt = RenderOptions(sh_degree=scenes.CONFIGS[cfg]['sh_degree'])
+    for _ in range(2):
+        fb = r.render(raw, cam, opt)
+    torch.cuda.synchronize()
+    t = time.time(); N = 5
+    for _ in range(N):
+        fb = r.render(raw, cam, opt)
+    torch.cuda.synchronize(); dt = (time.time() - t) / N
+    st = r.stats()
+    mp = cam.width * cam.height / 1e6
+    print(f"cfg{cfg} fwd {dt*1e3:.2f} ms  {mp/dt:.1f} MP/s  stats {st}", flush=True)
+    if scenes.CONFIGS[cfg]['backward']:
+        tgt = torch.from_numpy(scenes.config_target(cfg, cam).astype(np.float32)).cuda()
+        for _ in range(2):
+            fb = r.render(raw, cam, opt); v, d = r.l1_loss(fb.color, tgt); g = r.backward_render(raw, FrameGrad(d_color=d))
+        torch.cuda.synchronize(); t = time.time()
+        for _ in range(N):
+            fb = r.render(raw, cam, opt); v, d = r.l1_loss(fb.color, tgt); g = r.backward_render(raw, FrameGrad(d_color=d))
+        torch.cuda.synchronize(); dt = (time.time() - t) / N
+        print(f"cfg{cfg} fwd+bwd {dt*1e3:.2f} ms  {mp/dt:.1f} MP/s loss {float(v):.4f}", flush=True)

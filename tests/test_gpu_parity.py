@@ -1,0 +1,193 @@
+"""CUDA path vs the CPU oracle on identical seeded inputs (parity bar of BASELINE.json):
+tile/key lists and per-tile ranges bit-exact, RGB/alpha/depth/normal within 1e-4 max
+absolute error, parameter gradients within 1e-3 relative L2.
+
+The oracle is oracle/liboracle.so (C restatement, itself pinned bit-exactly to the
+reference build by tests/test_oracle.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import port, ref
+from paper_2412_11752_b200 import scenes
+from tests.helpers import api_options, opt_for, rel_l2, small_scene
+
+pytestmark = pytest.mark.gpu
+
+FB_TOL = 1e-4   # max abs, colour / depth / normal / alpha (BASELINE.json north_star)
+GRAD_TOL = 1e-3  # relative L2 of parameter gradients
+
+
+def _fb_close(gpu, orc, tol=FB_TOL):
+    for f in ("color", "depth", "normal", "alpha"):
+        g = getattr(gpu, f).cpu().numpy().astype(np.float64)
+        o = orc[f]
+        err = np.abs(g - o).max() if o.size else 0.0
+        assert err <= tol, f"{f}: max abs err {err:.3e}"
+
+
+def _bins_equal(gpu_bins, orc_bins):
+    off, ids, keys = orc_bins
+    np.testing.assert_array_equal(gpu_bins.offsets, off)
+    np.testing.assert_array_equal(gpu_bins.prim_ids, ids)
+    np.testing.assert_array_equal(gpu_bins.keys.view(np.uint64), keys.view(np.uint64))
+
+
+def test_config0_forward_parity(rast):
+    sc = scenes.config_scene(0)
+    cam = scenes.config_cameras(0)[0]
+    o = opt_for(0)
+    fb = rast.render(sc.f32(), cam, api_options(o))
+    bins = rast.tile_binning()
+    _bins_equal(bins, port.bin_primitives(sc, cam, o))
+    _fb_close(fb, port.render(sc, cam, o))
+    st = rast.stats()
+    assert st["pairs"] == len(bins.prim_ids) and st["near_ties"] == 0
+
+
+@pytest.mark.parametrize("presort", [0, 1, 2])
+@pytest.mark.parametrize("mode", ["cache", "list", "exact"])
+def test_small_scene_modes(rast, presort, mode):
+    sc, cam = small_scene(seed=3 + presort, n=80)
+    o = opt_for(0, presort=presort, use_cache=(mode != "list"), exact_sort=(mode == "exact"),
+                background=(0.2, 0.4, 0.6))
+    fb = rast.render(sc.f32(), cam, api_options(o))
+    _bins_equal(rast.tile_binning(), port.bin_primitives(sc, cam, o))
+    _fb_close(fb, port.render(sc, cam, o))
+
+
+def test_sh_degree3_and_k4(rast):
+    sc = scenes.random_scene(120, seed=11, k=4, sh_degree=3)
+    cam = scenes.look_at_camera(80, 64, (0.0, 0.5, -3.0))
+    for deg in (0, 1, 3):
+        o = opt_for(deg)
+        fb = rast.render(sc.f32(), cam, api_options(o), k=4)
+        _bins_equal(rast.tile_binning(), port.bin_primitives(sc, cam, o))
+        _fb_close(fb, port.render(sc, cam, o))
+
+
+def test_replay_records_match(rast):
+    sc, cam = small_scene(seed=5, n=40)
+    o = opt_for(0)
+    rast.render(sc.f32(), cam, api_options(o), replay=128)
+    rb = rast.replay_buffer()
+    off, ids, vals = port.render(sc, cam, o, replay=True)["replay"]
+    np.testing.assert_array_equal(rb.offsets, off)
+    np.testing.assert_array_equal(rb.prim_ids, ids)
+    np.testing.assert_allclose(rb.vals[:, :3], vals[:, :3], rtol=0, atol=1e-12)  # u, v, depth (bit-level ops)
+    np.testing.assert_allclose(rb.vals[:, 3], vals[:, 3], rtol=1e-12, atol=1e-15)  # alpha
+    np.testing.assert_array_equal(rb.vals[:, 4], vals[:, 4])
+
+
+def test_empty_scene_background(rast):
+    sc = scenes.random_scene(0, seed=1)
+    cam = scenes.simple_camera(32, 32)
+    o = opt_for(0, background=(0.2, 0.4, 0.6))
+    fb = rast.render(sc.f32(), cam, api_options(o))
+    col = fb.color.cpu().numpy()
+    assert np.allclose(col, np.array([0.2, 0.4, 0.6], np.float32)[None, None], atol=1e-7)
+    assert float(fb.alpha.abs().max()) == 0.0
+
+
+def test_behind_camera_no_tiles(rast):
+    sc = scenes.random_scene(30, seed=2)
+    sc.raw[2] = -2.0 - np.abs(sc.raw[2])  # all centres behind the identity camera
+    cam = scenes.simple_camera(64, 64)
+    o = opt_for(0)
+    rast.render(sc.f32(), cam, api_options(o))
+    b = rast.tile_binning()
+    _bins_equal(b, port.bin_primitives(sc, cam, o))
+
+
+def _random_frame_grad(H, W, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.uniform(-1, 1, (H, W, 3)), rng.uniform(-0.1, 0.1, (H, W)), rng.uniform(-0.1, 0.1, (H, W, 3)),
+            rng.uniform(-0.5, 0.5, (H, W)))
+
+
+def _check_grads(g, og):
+    gr = g.raw.cpu().numpy().astype(np.float64)
+    assert rel_l2(gr, og["raw"]) <= GRAD_TOL, f"raw grads rel L2 {rel_l2(gr, og['raw']):.2e}"
+    assert rel_l2(g.d_center_world.cpu().numpy(), og["d_center_world"]) <= GRAD_TOL
+    assert rel_l2(g.screen_grad.cpu().numpy(), og["screen_grad"]) <= GRAD_TOL
+    np.testing.assert_array_equal(g.touched.cpu().numpy(), og["touched"])
+
+
+@pytest.mark.parametrize("mode", ["cache", "list", "exact"])
+def test_backward_small(rast, mode):
+    from paper_2412_11752_b200.api import FrameGrad
+    sc, cam = small_scene(seed=7, n=50, sh_degree=1)
+    o = opt_for(1, use_cache=(mode != "list"), exact_sort=(mode == "exact"), background=(0.3, 0.5, 0.2))
+    rast.render(sc.f32(), cam, api_options(o))
+    dc, dd, dn, da = _random_frame_grad(cam.height, cam.width, 1)
+    t = lambda a: torch.from_numpy(a.astype(np.float32))  # noqa: E731
+    g = rast.backward_render(sc.f32(), FrameGrad(t(dc), t(dd), t(dn), t(da)))
+    # the oracle consumes the f32-rounded frame gradients the GPU saw
+    og = port.backward(sc, cam, o, dc.astype(np.float32), dd.astype(np.float32), dn.astype(np.float32),
+                       da.astype(np.float32))
+    _check_grads(g, og)
+
+
+def test_l1_loss_and_adam(rast):
+    from paper_2412_11752_b200.api import OptState, TrainConfig
+    rng = np.random.default_rng(0)
+    r = rng.uniform(0, 1, (20, 24, 3)).astype(np.float32)
+    t = rng.uniform(0, 1, (20, 24, 3)).astype(np.float32)
+    t[0, 0] = r[0, 0]  # sign(0) = 0
+    v, d = rast.l1_loss(torch.from_numpy(r), torch.from_numpy(t))
+    rv, rd = ref.loss_l1(r.astype(np.float64), t.astype(np.float64))
+    assert abs(float(v) - rv) <= 1e-12
+    np.testing.assert_allclose(d.cpu().numpy(), rd, rtol=1e-6, atol=0)
+    # Adam: three steps from a fresh state vs the reference adam_step
+    sc = scenes.random_scene(17, seed=4, sh_degree=3)
+    p = torch.from_numpy(sc.f32()).cuda()
+    st = OptState.zeros_like(p)
+    cfg = TrainConfig(steps=100, lr_drk=1e-3, lr_position=1e-3, lr_rotation=1e-3, lr_opacity=1e-3, lr_sh=1e-3)
+    rp = sc.raw.astype(np.float64).copy()
+    rm = np.zeros_like(rp)
+    rvv = np.zeros_like(rp)
+    step = 0
+    for it in range(3):
+        g = rng.normal(0, 1, rp.shape).astype(np.float32)
+        rast.adam_step(p, torch.from_numpy(g).cuda(), st, cfg, scene_extent=2.0)
+        step = ref.adam_step(rp, g.astype(np.float64), rm, rvv, 8, 16, step,
+                             [1e-3, 1e-3, 1e-3, 1e-3, 1e-3], 100, 2.0)
+    assert st.step == step == 3
+    assert rel_l2(p.cpu().numpy() - sc.raw, rp - sc.raw) <= 1e-5
+
+
+@pytest.mark.parametrize("cfg,crop", [(1, 128), (2, 96)])
+def test_config_crop_forward_parity(rast, cfg, crop):
+    """BASELINE configs 1/2 (full primitive sets) on a centred crop the oracle finishes quickly."""
+    sc = scenes.config_scene(cfg)
+    cam0 = scenes.config_cameras(cfg)[0]
+    x0 = (cam0.width // 2 - crop // 2) // 16 * 16
+    y0 = (cam0.height // 2 - crop // 2) // 16 * 16
+    cam = cam0.crop(x0, y0, crop, crop)
+    o = opt_for(3)
+    fb = rast.render(sc.f32(), cam, api_options(o))
+    _bins_equal(rast.tile_binning(), port.bin_primitives(sc, cam, o))
+    _fb_close(fb, port.render(sc, cam, o))
+
+
+def test_config2_crop_backward_parity(rast):
+    from paper_2412_11752_b200.api import FrameGrad
+    sc = scenes.config_scene(2)
+    cam0 = scenes.config_cameras(2)[0]
+    cam = cam0.crop(cam0.width // 2 // 16 * 16, cam0.height // 2 // 16 * 16, 64, 48)
+    o = opt_for(3)
+    fb = rast.render(sc.f32(), cam, api_options(o))
+    tgt = scenes.config_target(2, cam)
+    v, d = rast.l1_loss(fb.color, torch.from_numpy(tgt.astype(np.float32)))
+    orc = port.render(sc, cam, o)
+    ov, od = port.loss_l1(orc["color"], tgt.astype(np.float32).astype(np.float64))
+    assert abs(float(v) - ov) <= 1e-6
+    # d_color signs can only differ where |render - target| is below the render tolerance
+    assert (np.sign(d.cpu().numpy()) == np.sign(od)).mean() > 0.999
+    # identical frame gradient into both backward passes
+    g = rast.backward_render(sc.f32(), FrameGrad(d_color=torch.from_numpy(od.astype(np.float32))))
+    og = port.backward(sc, cam, o, od.astype(np.float32), None, None, None)
+    _check_grads(g, og)
