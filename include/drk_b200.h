@@ -108,6 +108,7 @@ typedef struct drk_stats {
   int64_t near_ties;       /* binning decisions within 1e-9 relative of a tie */
   int64_t poly_overflow;   /* primitives that needed the large-polygon path */
   int64_t replay_overflow; /* pixels whose replay exceeded record_replay */
+  int64_t fp64_pixels;     /* pixels re-rendered in fp64 (termination within the fp32 error bound) */
 } drk_stats;
 
 typedef struct drk_ctx drk_ctx;
@@ -193,6 +194,13 @@ typedef struct drk_adam_config {
  * OptState::step (host value, incremented). */
 int drk_adam_step(drk_ctx* ctx, float* params, const float* grads, float* m, float* v, int n,
                   int k, int sh_terms, int64_t* step, const drk_adam_config* cfg);
+
+/* --- validation hook ----------------------------------------------------- */
+/* Samples the fp32 alpha fast path against the fp64 path on the activated
+ * primitives of this context: max |a32 - a64| / (bound * a32) and
+ * max |a32 - a64|.  Used by the parity tests to check the error bound that
+ * gates the fp64 fallback. */
+int drk_debug_alpha_bound(drk_ctx* ctx, int64_t samples, uint64_t seed, double* max_ratio, double* max_abs);
 
 #ifdef __cplusplus
 }

@@ -64,7 +64,7 @@ class FrameGrad_(C.Structure):
 
 class Stats_(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("primitives", "pairs", "streamed", "popped", "composited", "near_ties",
-                                          "poly_overflow", "replay_overflow")]
+                                          "poly_overflow", "replay_overflow", "fp64_pixels")]
 
 
 class AdamConfig_(C.Structure):
@@ -98,6 +98,7 @@ SIGNATURES = {
     "drk_backward": (C.c_int, [_P, _P, C.POINTER(FrameGrad_), _P, _P, _P, _P, C.c_int, C.c_int]),
     "drk_get_prim_grads": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int)]),
     "drk_l1_loss": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, _P]),
+    "drk_debug_alpha_bound": (C.c_int, [_P, C.c_int64, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "drk_adam_step": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                 C.POINTER(AdamConfig_)]),
 }

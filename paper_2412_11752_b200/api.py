@@ -309,6 +309,12 @@ class Rasterizer:
                                               ids.ctypes.data_as(C.c_void_p), vals.ctypes.data_as(C.c_void_p)))
         return ReplayBuffer(W, H, off, ids, vals)
 
+    def alpha_bound_check(self, samples: int = 1 << 22, seed: int = 1):
+        """(max error / bound, max abs error) of the fp32 alpha path on the last activated set."""
+        r, a = C.c_double(0), C.c_double(0)
+        self._check(_lib.lib().drk_debug_alpha_bound(self._h, samples, seed, C.byref(r), C.byref(a)))
+        return r.value, a.value
+
     def stats(self) -> dict:
         s = _lib.Stats_()
         self._check(_lib.lib().drk_get_stats(self._h, C.byref(s)))

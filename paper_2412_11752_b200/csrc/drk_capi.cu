@@ -31,6 +31,8 @@ void launch_act_bwd(int n, int K, int terms, const float* raw, const double* gac
                     float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
                     cudaStream_t s);
 void launch_l1(long long n, const float* r, const float* t, double* loss, float* dcol, cudaStream_t s);
+void launch_alpha_bound(const ShapeView& S, int n, long long samples, unsigned long long seed,
+                        unsigned long long* out, cudaStream_t s);
 
 void* ensure_bytes(DevBuf& b, size_t bytes) {
   if (b.bytes >= bytes && b.p) return b.p;
@@ -120,7 +122,7 @@ static RasterParams raster_params(drk_ctx* c) {
   P.pv = static_cast<const unsigned long long*>(c->pv.p);
   P.geo = static_cast<const Geo*>(c->geo.p);
   const Activated& A = c->act;
-  P.S = ShapeView{A.s, A.th, A.ex, A.ey, A.det, A.eta, A.tau, A.o, A.K};
+  P.S = ShapeView{A.s, A.th, A.ex, A.ey, A.det, A.eta, A.tau, A.o, A.thf, A.invdetf, A.piogf, A.hf, A.K};
   P.sh = A.sh;
   P.terms = A.terms;
   P.counters = static_cast<unsigned long long*>(c->counters.p);
@@ -244,8 +246,10 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   if (int st = exclusive_scan<int>(c, tilecnt, n_tiles + 1, tileoff, &tot)) return st;
   // per-pixel state / replay
   double* pxstate = ensure<double>(c->pxstate, 8 * (size_t)n_pix);
-  if (!pxstate) return set_error(c, DRK_ERR_OOM, "pixel state");
+  unsigned char* pxflag = ensure<unsigned char>(c->pxflag, (size_t)n_pix);
+  if (!pxstate || !pxflag) return set_error(c, DRK_ERR_OOM, "pixel state");
   RasterParams P = raster_params(c);
+  P.pxflag = pxflag;
   P.color = color;
   P.depth = depth;
   P.normal = normal;
@@ -268,6 +272,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   c->stats.composited = (int64_t)h[C_COMPOSITED];
   c->stats.near_ties = (int64_t)h[C_NEAR_TIES];
   c->stats.replay_overflow = (int64_t)h[C_REPLAY_OVERFLOW];
+  c->stats.fp64_pixels = (int64_t)h[C_REDO_PIXELS];
   if (h[C_ERR_DEGEN_BASIS]) return set_error(c, DRK_ERR_DEGENERATE_BASIS, "adjacent endpoints nearly collinear");
   c->has_fwd = true;
   return DRK_OK;
@@ -287,6 +292,7 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   cudaMemsetAsync(tch, 0, n + 1, s);
   RasterParams P = raster_params(c);
   P.pxstate = static_cast<double*>(c->pxstate.p);
+  P.pxflag = static_cast<unsigned char*>(c->pxflag.p);
   if (fg) {
     P.dC = fg->d_color;
     P.dD = fg->d_depth;
@@ -375,7 +381,8 @@ void drk_ctx_destroy(drk_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
-                    &c->a_ex, &c->a_ey, &c->a_det, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->rowcnt,
+                    &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
+                    &c->pxflag, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->rowcnt,
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->pk2, &c->pv2,
                     &c->hist, &c->sortoff, &c->tilecnt, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
@@ -522,6 +529,21 @@ int drk_get_prim_grads(drk_ctx* c, const double** grads, int* stride) {
   if (!c || !grads || !stride) return DRK_ERR_INVALID_ARG;
   *grads = static_cast<const double*>(c->gact.p);
   *stride = 3 + 9 + 2 * c->act.K + 3 + 3 * c->act.terms;
+  return DRK_OK;
+}
+
+int drk_debug_alpha_bound(drk_ctx* c, int64_t samples, uint64_t seed, double* max_ratio, double* max_abs) {
+  if (!c || !max_ratio || !max_abs || c->act.n <= 0) return DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  unsigned long long* out = ensure<unsigned long long>(c->bits, 4);
+  if (!out) return set_error(c, DRK_ERR_OOM, "alpha bound");
+  RasterParams P = raster_params(c);
+  launch_alpha_bound(P.S, c->act.n, samples, seed, out, c->stream);
+  unsigned long long h[2];
+  cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, c->stream);
+  if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "alpha bound")) return st;
+  std::memcpy(max_ratio, &h[0], sizeof(double));
+  std::memcpy(max_abs, &h[1], sizeof(double));
   return DRK_OK;
 }
 

@@ -40,6 +40,7 @@ enum Counter {
   C_REPLAY_OVERFLOW,
   C_VISIBLE,
   C_POLY_FAIL,
+  C_REDO_PIXELS,  // pixels re-rendered by the fp64 pass
   C_COUNT
 };
 
@@ -74,15 +75,25 @@ __host__ __device__ inline double dot3(const double* a, const double* b) {
   return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
 }
 
+// Explicitly rounded fp64 ops: never contracted into FMA, whatever --fmad
+// says.  Used for every value that must be bit-identical to the reference
+// (ray directions, ray-plane depths, tangent coordinates).
+__device__ __forceinline__ double xm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xa(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xs(double a, double b) { return __dadd_rn(a, -b); }
+__device__ __forceinline__ double xdot3(double a0, double a1, double a2, double b0, double b1, double b2) {
+  return xa(xa(xm(a0, b0), xm(a1, b1)), xm(a2, b2));
+}
+
 // pixel_ray (geometry.cpp:32-38): dir = normalize(R^T ((px-cx)/fx, (py-cy)/fy, 1)).
 __device__ __forceinline__ void pixel_dir(const CamD& c, double px, double py, double d[3]) {
-  const double dc0 = (px - c.cx) / c.fx, dc1 = (py - c.cy) / c.fy, dc2 = 1.0;
-  double v0 = c.R[0] * dc0 + c.R[3] * dc1 + c.R[6] * dc2;
-  double v1 = c.R[1] * dc0 + c.R[4] * dc1 + c.R[7] * dc2;
-  double v2 = c.R[2] * dc0 + c.R[5] * dc1 + c.R[8] * dc2;
-  const double sq = v0 * v0 + v1 * v1 + v2 * v2;
+  const double dc0 = xs(px, c.cx) / c.fx, dc1 = xs(py, c.cy) / c.fy, dc2 = 1.0;
+  double v0 = xdot3(c.R[0], c.R[3], c.R[6], dc0, dc1, dc2);
+  double v1 = xdot3(c.R[1], c.R[4], c.R[7], dc0, dc1, dc2);
+  double v2 = xdot3(c.R[2], c.R[5], c.R[8], dc0, dc1, dc2);
+  const double sq = xdot3(v0, v1, v2, v0, v1, v2);
   if (sq > 0) {
-    const double n = sqrt(sq);
+    const double n = __dsqrt_rn(sq);
     v0 = v0 / n;
     v1 = v1 / n;
     v2 = v2 / n;
@@ -184,6 +195,12 @@ struct ShapeView {
   const double* eta;
   const double* tau;
   const double* o;
+  // fp32 fast-path constants, stride K: theta_k, 1/det_k, pi/gap_k (bracket
+  // k, k+1 mod K), 1/s_k^2
+  const float* thf;
+  const float* invdetf;
+  const float* piogf;
+  const float* hf;
   int K;
 };
 
@@ -250,6 +267,63 @@ __device__ __forceinline__ void eval_kernel(double u, double v, const ShapeView&
     ev.clamped = true;
   }
   ev.g = exp(e);
+}
+
+__device__ __forceinline__ float sharpen_f(float g, float tau) {
+  g = fminf(1.0f, fmaxf(0.0f, g));
+  if (g < (1.0f + tau) * 0.25f) return (1.0f - tau) / (1.0f + tau) * g;
+  if (g < (3.0f - tau) * 0.25f) return ((1.0f + tau) * g - tau) / (1.0f - tau);
+  return ((1.0f - tau) * g + 2.0f * tau) / (1.0f + tau);
+}
+
+// fp32 fast path of alpha = o * Psi(g(u, v)) (core.cpp:148-204, :229-237,
+// :263-265).  Cancellation-prone quantities are formed in fp64 and rounded
+// once: the endpoint-basis numerators (a, b) and the angle from the lower
+// bracket endpoint (so delta keeps relative precision), with the cosine
+// blend written as cos^2(delta/2)/s_lo^2 + sin^2(delta/2)/s_hi^2.  Returns
+// alpha and a relative error bound *rel (validated against the fp64 path by
+// tests/test_gpu_alpha_bound.py); r2 == 0 gives the exact centre value.
+__device__ __forceinline__ float alpha_f32(double u, double v, double r2, const ShapeView& S, int i, float o,
+                                           float tau, float eta, float* rel, bool* degenerate) {
+  *degenerate = false;
+  if (r2 == 0) {
+    *rel = 1e-7f;
+    return o * sharpen_f(1.0f, tau);
+  }
+  const int K = S.K;
+  const float* thf = S.thf + (size_t)i * K;
+  const float uf = (float)u, vf = (float)v;
+  float th = atan2f(vf, uf);
+  if (th <= 0.0f) th += 6.28318530717958647692f;
+  int lo, hi;
+  if (th <= thf[0] || th > thf[K - 1]) {
+    lo = K - 1;
+    hi = 0;
+  } else {
+    hi = 1;
+    while (hi < K && thf[hi] < th) ++hi;
+    lo = hi - 1;
+  }
+  const size_t bl = (size_t)i * K + lo, bh = (size_t)i * K + hi;
+  if (fabs(S.det[bl]) < 1e-12) {
+    *degenerate = true;
+    return 0.0f;
+  }
+  const double elx = S.ex[bl], ely = S.ey[bl], ehx = S.ex[bh], ehy = S.ey[bh];
+  const float invd = S.invdetf[bl];
+  const float a = (float)(ehy * u - ehx * v) * invd;
+  const float b = (float)(-ely * u + elx * v) * invd;
+  const float r1 = fabsf(a) + fabsf(b);
+  const float dth = atan2f((float)(elx * v - ely * u), (float)(elx * u + ely * v));
+  const float delta = dth * S.piogf[bl];
+  float sh, ch;
+  sincosf(0.5f * delta, &sh, &ch);
+  const float inv = ch * ch * S.hf[bl] + sh * sh * S.hf[bh];
+  const float Q = eta * r1 * r1 + (1.0f - eta) * (float)r2 * inv;
+  const float e = fmaxf(-0.5f * Q, -30.0f);
+  const float g = expf(e);
+  *rel = 2e-6f * (1.0f + fminf(Q, 60.0f));
+  return o * sharpen_f(g, tau);
 }
 
 // low_pass_filter_term (core.cpp:267-273).

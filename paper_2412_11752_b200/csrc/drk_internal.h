@@ -43,6 +43,7 @@ struct Activated {
   const double *mu, *rot, *s, *th, *eta, *tau, *o;
   const float* sh;  // n x terms x 3 (AoS)
   const double *ex, *ey, *det;
+  const float *thf, *invdetf, *piogf, *hf;
   int n, K, terms;
 };
 
@@ -67,6 +68,7 @@ struct RasterParams {
   int G;
   unsigned char* touched;
   unsigned long long* counters;
+  unsigned char* pxflag;  // 1 = pixel needs the fp64 re-render (uncertain termination)
 };
 
 void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s);
@@ -81,6 +83,7 @@ struct drk_ctx {
 
   // activated primitives owned by the context (raw path)
   drk::DevBuf a_mu, a_rot, a_s, a_th, a_eta, a_tau, a_o, a_sh, a_ex, a_ey, a_det;
+  drk::DevBuf a_thf, a_invdetf, a_piogf, a_hf, pxflag;
   drk::Activated act{};
 
   // per view

@@ -20,7 +20,7 @@ namespace drk {
 // ---------------------------------------------------------------------------
 __global__ void k_activate(const float* __restrict__ raw, int n, int K, int terms, double* mu, double* rot,
                            double* s, double* th, double* eta, double* tau, double* o, float* sh,
-                           double* ex, double* ey, double* det, unsigned long long* counters) {
+                           unsigned long long* counters) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int S = 3 + 4 + 2 * K + 3 + 3 * terms;
@@ -57,28 +57,27 @@ __global__ void k_activate(const float* __restrict__ raw, int n, int K, int term
   o[i] = sigmoid(RAW(9 + 2 * K));
   for (int j = 0; j < 3 * terms; ++j) sh[(size_t)3 * terms * i + j] = raw[(size_t)(10 + 2 * K + j) * n + i];
 #undef RAW
-  // endpoints and bracket determinants (types.hpp:93-95, core.cpp:188-190)
-  for (int j = 0; j < K; ++j) {
-    ex[(size_t)K * i + j] = si[j] * cos(ti[j]);
-    ey[(size_t)K * i + j] = si[j] * sin(ti[j]);
-  }
-  for (int j = 0; j < K; ++j) {
-    const int h = (j + 1) % K;
-    det[(size_t)K * i + j] = ex[(size_t)K * i + j] * ey[(size_t)K * i + h] - ey[(size_t)K * i + j] * ex[(size_t)K * i + h];
-  }
 }
 
-// Shape constants for caller-provided activated primitives.
-__global__ void k_shape(int n, int K, const double* s, const double* th, double* ex, double* ey, double* det) {
+// Endpoints and bracket determinants (types.hpp:93-95, core.cpp:188-190) and
+// the fp32 fast-path constants of ShapeView.
+__global__ void k_shape(int n, int K, const double* s, const double* th, double* ex, double* ey, double* det,
+                        float* thf, float* invdetf, float* piogf, float* hf) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const size_t b = (size_t)K * i;
   for (int j = 0; j < K; ++j) {
-    ex[(size_t)K * i + j] = s[(size_t)K * i + j] * cos(th[(size_t)K * i + j]);
-    ey[(size_t)K * i + j] = s[(size_t)K * i + j] * sin(th[(size_t)K * i + j]);
+    ex[b + j] = s[b + j] * cos(th[b + j]);
+    ey[b + j] = s[b + j] * sin(th[b + j]);
   }
   for (int j = 0; j < K; ++j) {
     const int h = (j + 1) % K;
-    det[(size_t)K * i + j] = ex[(size_t)K * i + j] * ey[(size_t)K * i + h] - ey[(size_t)K * i + j] * ex[(size_t)K * i + h];
+    det[b + j] = ex[b + j] * ey[b + h] - ey[b + j] * ex[b + h];
+    const double gap = j + 1 < K ? th[b + h] - th[b + j] : th[b] - (th[b + K - 1] - kTwoPi);
+    thf[b + j] = (float)th[b + j];
+    invdetf[b + j] = (float)(1.0 / det[b + j]);
+    piogf[b + j] = (float)(kPi / gap);
+    hf[b + j] = (float)(1.0 / (s[b + j] * s[b + j]));
   }
 }
 
@@ -586,6 +585,25 @@ __global__ void k_emit(long long n_rows, const int4* __restrict__ rows, const lo
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+static int launch_shape_consts(drk_ctx* c, int n, int K) {
+  Activated& A = c->act;
+  A.ex = ensure<double>(c->a_ex, (size_t)K * n);
+  A.ey = ensure<double>(c->a_ey, (size_t)K * n);
+  A.det = ensure<double>(c->a_det, (size_t)K * n);
+  A.thf = ensure<float>(c->a_thf, (size_t)K * n);
+  A.invdetf = ensure<float>(c->a_invdetf, (size_t)K * n);
+  A.piogf = ensure<float>(c->a_piogf, (size_t)K * n);
+  A.hf = ensure<float>(c->a_hf, (size_t)K * n);
+  if (!A.ex || !A.ey || !A.det || !A.thf || !A.invdetf || !A.piogf || !A.hf)
+    return set_error(c, DRK_ERR_OOM, "shape buffers");
+  if (n > 0)
+    k_shape<<<(n + 127) / 128, 128, 0, c->stream>>>(n, K, A.s, A.th, const_cast<double*>(A.ex),
+                                                   const_cast<double*>(A.ey), const_cast<double*>(A.det),
+                                                   const_cast<float*>(A.thf), const_cast<float*>(A.invdetf),
+                                                   const_cast<float*>(A.piogf), const_cast<float*>(A.hf));
+  return cuda_check(c, cudaGetLastError(), "shape");
+}
+
 int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms) {
   Activated& A = c->act;
   A.n = n;
@@ -599,19 +617,16 @@ int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms) {
   A.tau = ensure<double>(c->a_tau, n);
   A.o = ensure<double>(c->a_o, n);
   A.sh = ensure<float>(c->a_sh, (size_t)3 * terms * n);
-  A.ex = ensure<double>(c->a_ex, (size_t)K * n);
-  A.ey = ensure<double>(c->a_ey, (size_t)K * n);
-  A.det = ensure<double>(c->a_det, (size_t)K * n);
   unsigned long long* ctr = ensure<unsigned long long>(c->counters, C_COUNT);
-  if (!A.mu || !A.rot || !A.s || !A.th || !A.eta || !A.tau || !A.o || !A.sh || !A.ex || !A.ey || !A.det || !ctr)
+  if (!A.mu || !A.rot || !A.s || !A.th || !A.eta || !A.tau || !A.o || !A.sh || !ctr)
     return set_error(c, DRK_ERR_OOM, "activation buffers");
   cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT, c->stream);
   if (n > 0)
     k_activate<<<(n + 127) / 128, 128, 0, c->stream>>>(
         raw, n, K, terms, const_cast<double*>(A.mu), const_cast<double*>(A.rot), const_cast<double*>(A.s),
         const_cast<double*>(A.th), const_cast<double*>(A.eta), const_cast<double*>(A.tau),
-        const_cast<double*>(A.o), const_cast<float*>(A.sh), const_cast<double*>(A.ex),
-        const_cast<double*>(A.ey), const_cast<double*>(A.det), ctr);
+        const_cast<double*>(A.o), const_cast<float*>(A.sh), ctr);
+  if (int st = launch_shape_consts(c, n, K)) return st;
   unsigned long long h[C_COUNT];
   if (int st = cuda_check(c, cudaMemcpyAsync(h, ctr, sizeof h, cudaMemcpyDeviceToHost, c->stream), "activate"))
     return st;
@@ -634,14 +649,7 @@ int launch_shape(drk_ctx* c, const drk_prims* p, int n, int K, int terms) {
   A.tau = p->tau;
   A.o = p->opacity;
   A.sh = p->sh;
-  A.ex = ensure<double>(c->a_ex, (size_t)K * n);
-  A.ey = ensure<double>(c->a_ey, (size_t)K * n);
-  A.det = ensure<double>(c->a_det, (size_t)K * n);
-  if (!A.ex || !A.ey || !A.det) return set_error(c, DRK_ERR_OOM, "shape buffers");
-  if (n > 0)
-    k_shape<<<(n + 127) / 128, 128, 0, c->stream>>>(n, K, A.s, A.th, const_cast<double*>(A.ex),
-                                                   const_cast<double*>(A.ey), const_cast<double*>(A.det));
-  return cuda_check(c, cudaGetLastError(), "shape");
+  return launch_shape_consts(c, n, K);
 }
 
 }  // namespace drk

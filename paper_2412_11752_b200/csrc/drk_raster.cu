@@ -1,29 +1,41 @@
 // K4 forward rasterizer and K5 backward rasterizer (reference raster.cpp:267-430,
-// grad.cpp:16-303), K6 activation backward (grad.cpp:122-159, :370-383).
+// grad.cpp:16-303), K6 activation backward (grad.cpp:122-159, :370-383),
+// K7 L1 loss, K8 Adam.
 //
 // One CTA per 16x16 tile, one thread per pixel.  The tile list is streamed in
 // batches of 256 candidates staged in shared memory (id, ray-plane numerator,
-// plane normal: 36 B each); every pixel intersects the batch in fp64 with the
-// reference op order (bit-identical depths), runs the capacity-8 SortCache
-// (raster.cpp:267-303) in registers, and composites popped entries.  A pixel
-// leaves the stream once saturated; the CTA leaves once all pixels have
-// (__syncthreads_count).  Popped entries outside the kernel's alpha_min
-// support (r2 > (s_max f_vis)^2, proven bound) and outside the low-pass
-// floor's reach skip the kernel evaluation.  The backward kernel re-streams
-// the same decisions (no replay buffer) and rebuilds `rest` from the forward
-// pass's fp64 per-pixel accumulators.
+// plane normal: 36 B each); every pixel intersects the batch in fp64 with
+// explicitly rounded ops in the reference order (bit-identical depths), runs
+// the capacity-8 SortCache (raster.cpp:267-303) in registers, and composites
+// popped entries.  A pixel leaves the stream once saturated; the CTA leaves
+// once all pixels have (__syncthreads_count).
+//
+// Alpha of a popped entry is evaluated in fp32 (alpha_f32) with a relative
+// error bound.  Decisions that fall inside the bound (alpha_min skip, low-pass
+// floor vs kernel, the 1-1e-6 clamp) are re-evaluated in fp64 on the spot; a
+// pixel whose transmittance comes within its accumulated error bound of the
+// early-stop threshold is flagged and re-rendered entirely in fp64 by a
+// second launch (F64 = true).  Composited values are accumulated in fp64.
+//
+// The backward kernel re-streams the same decisions (no replay buffer) and
+// rebuilds `rest` from the forward pass's fp64 per-pixel accumulators.
+//
+// This translation unit is compiled with --fmad=true: every fp64 value that
+// must match the reference bit for bit uses __dmul_rn / __dadd_rn.
 #include <algorithm>
 
 #include "drk_internal.h"
 
 namespace drk {
 
-template <bool BWD>
+template <bool BWD, bool F64>
 struct Pixel {
   double dir[3];
   float basis[16];
   double px, py;
   double T, C[3], D, N[3], A;
+  float E;  // relative error bound of T (fp32 alphas)
+  bool uncertain;
   // backward
   double dC[3], dD, dN[3], dA, rest;
   bool has_dN;
@@ -31,46 +43,114 @@ struct Pixel {
   int pix, n_rec;
   bool err;
 
+  __device__ void init(const RasterParams& P, int x, int y) {
+    px = x + 0.5;
+    py = y + 0.5;
+    pixel_dir(P.cam, px, py, dir);
+    sh_basis_f((float)dir[0], (float)dir[1], (float)dir[2], P.opt.sh_degree, basis);
+    T = 1.0;
+    C[0] = C[1] = C[2] = D = N[0] = N[1] = N[2] = A = 0;
+    E = 0.f;
+    uncertain = false;
+    n_pop = n_comp = 0;
+    n_rec = 0;
+    err = false;
+    pix = y * P.cam.W + x;
+  }
+
+  __device__ void init_bwd(const RasterParams& P) {
+    const size_t p = (size_t)pix;
+    dC[0] = P.dC ? P.dC[3 * p] : 0.f;
+    dC[1] = P.dC ? P.dC[3 * p + 1] : 0.f;
+    dC[2] = P.dC ? P.dC[3 * p + 2] : 0.f;
+    dD = P.dD ? P.dD[p] : 0.f;
+    has_dN = P.dN != nullptr;
+    dN[0] = P.dN ? P.dN[3 * p] : 0.f;
+    dN[1] = P.dN ? P.dN[3 * p + 1] : 0.f;
+    dN[2] = P.dN ? P.dN[3 * p + 2] : 0.f;
+    dA = P.dA ? P.dA[p] : 0.f;
+    const double* st = P.pxstate + 8 * p;
+    // total = dC.C + dD D + dN.N + dA A (C includes T_n bg): grad.cpp:210-222
+    rest = (dC[0] * st[0] + dC[1] * st[1] + dC[2] * st[2]) + dD * st[3] +
+           (dN[0] * st[4] + dN[1] * st[5] + dN[2] * st[6]) + dA * st[7];
+  }
+
   // composite_candidate (raster.cpp:327-362) + backward_pixel (grad.cpp:224-301)
   // for one popped entry.  Returns false once the pixel saturates.
   __device__ bool composite(const RasterParams& P, double rt, int id) {
     const Geo& g = P.geo[id];
     const double rz0 = g.rz[0], rz1 = g.rz[1], rz2 = g.rz[2];
-    const double denom = dir[0] * rz0 + dir[1] * rz1 + dir[2] * rz2;
+    const double denom = xdot3(dir[0], dir[1], dir[2], rz0, rz1, rz2);
     // u, v (geometry.cpp:48-50)
-    const double h0 = P.cam.o[0] + rt * dir[0] - g.mu[0];
-    const double h1 = P.cam.o[1] + rt * dir[1] - g.mu[1];
-    const double h2 = P.cam.o[2] + rt * dir[2] - g.mu[2];
-    const double u = g.rx[0] * h0 + g.rx[1] * h1 + g.rx[2] * h2;
-    const double v = g.ry[0] * h0 + g.ry[1] * h1 + g.ry[2] * h2;
+    const double h0 = xs(xa(P.cam.o[0], xm(rt, dir[0])), g.mu[0]);
+    const double h1 = xs(xa(P.cam.o[1], xm(rt, dir[1])), g.mu[1]);
+    const double h2 = xs(xa(P.cam.o[2], xm(rt, dir[2])), g.mu[2]);
+    const double u = xdot3(g.rx[0], g.rx[1], g.rx[2], h0, h1, h2);
+    const double v = xdot3(g.ry[0], g.ry[1], g.ry[2], h0, h1, h2);
     ++n_pop;
     const double cos_view = fabs(denom);
     double dpw = 0, dph = 0;
     if (g.has_proj) {
-      dpw = px - g.ppx;
-      dph = py - g.ppy;
+      dpw = xs(px, g.ppx);
+      dph = xs(py, g.ppy);
     }
     // Cheap reject: alpha_kernel < alpha_min whenever r2^2 / s_max^2 > f_vis^2
     // (Q >= r2^2 / s_max^2), and the low-pass floor < alpha_min whenever
     // dp^2 > 2 cos^2 s_l^2 ln(o / alpha_min); both with a 1e-9 margin.
-    const double r2 = u * u + v * v;
+    const double r2 = xa(xm(u, u), xm(v, v));
     if (r2 > g.r2max && (!g.has_proj || dpw * dpw + dph * dph > cos_view * cos_view * g.dp2max)) return true;
-    KEval ev;
-    eval_kernel(u, v, P.S, id, ev);
-    if (ev.degenerate) {
-      err = true;
-      return false;
-    }
     const double o = P.S.o[id], tau = P.S.tau[id];
-    const double a_kernel = o * sharpen(ev.g, tau);
-    double a = a_kernel;
+    double a;
     bool lp = false;
-    if (g.has_proj) {
-      const double f = low_pass_filter_term(dpw, dph, cos_view, o, P.opt.lowpass_radius);
-      if (f > a_kernel) {
-        a = f;
-        lp = true;
+    float rel = 0.f;
+    bool use64 = F64;
+    KEval ev;
+    ev.center = false;
+    ev.clamped = false;
+    if (!F64) {
+      bool degen;
+      float relk;
+      const float ak = alpha_f32(u, v, r2, P.S, id, (float)o, (float)tau, (float)P.S.eta[id], &relk, &degen);
+      if (degen) {
+        err = true;
+        return false;
       }
+      float at = ak, relt = relk;
+      if (g.has_proj) {
+        const float sl = (float)P.opt.lowpass_radius, cv = (float)cos_view;
+        const float ex = fmaxf(-((float)(dpw * dpw + dph * dph)) / (2.0f * cv * cv * sl * sl), -30.0f);
+        const float f = (float)o * expf(ex);
+        const float relf = 4e-7f * (1.0f - ex);
+        if (fabsf(f - ak) <= relk * ak + relf * f) use64 = true;
+        if (f > ak) {
+          at = f;
+          relt = relf;
+          lp = true;
+        }
+      }
+      const float amin = (float)P.opt.alpha_min;
+      if (fabsf(at - amin) <= relt * at + 1e-12f) use64 = true;
+      if (at >= 0.99f && fabs((double)at - (1.0 - 1e-6)) <= (double)relt * at + 1e-12) use64 = true;
+      a = (double)at;
+      rel = relt;
+    }
+    if (use64) {
+      eval_kernel(u, v, P.S, id, ev);
+      if (ev.degenerate) {
+        err = true;
+        return false;
+      }
+      const double a_kernel = o * sharpen(ev.g, tau);
+      a = a_kernel;
+      lp = false;
+      if (g.has_proj) {
+        const double f = low_pass_filter_term(dpw, dph, cos_view, o, P.opt.lowpass_radius);
+        if (f > a_kernel) {
+          a = f;
+          lp = true;
+        }
+      }
+      rel = 0.f;
     }
     if (a < P.opt.alpha_min) return true;
     a = dmin(a, 1.0 - 1e-6);
@@ -110,9 +190,17 @@ struct Pixel {
         ++n_rec;
       }
     } else {
+      const bool alpha_clamped = a >= 1.0 - 1e-6 - 1e-12;
+      if (!use64 && !lp && !alpha_clamped) {
+        eval_kernel(u, v, P.S, id, ev);  // fp64 partials for backward_alpha
+      }
       backward_record(P, id, g, rt, u, v, a, lp, ev, rgb, cl0, cl1, cl2, sgn, denom, dpw, dph, w);
     }
-    T *= 1.0 - a;
+    T = xm(T, xs(1.0, a));
+    if (!F64) {
+      E += rel * (float)(a / (1.0 - a)) + 1e-15f;
+      if (fabs(T - P.opt.early_stop) <= T * (double)E) uncertain = true;
+    }
     return T >= P.opt.early_stop;
   }
 
@@ -206,8 +294,8 @@ struct Pixel {
     const double elx = P.S.ex[(size_t)id * K + lo], ely = P.S.ey[(size_t)id * K + lo];
     const double ehx = P.S.ex[(size_t)id * K + hi], ehy = P.S.ey[(size_t)id * K + hi];
     const double det = P.S.det[(size_t)id * K + lo];
-    du += d_r1 * (sa * ((ehy * 1.0 - ehx * 0.0) / det) + sb * ((-ely * 1.0 + elx * 0.0) / det));
-    dv += d_r1 * (sa * ((ehy * 0.0 - ehx * 1.0) / det) + sb * ((-ely * 0.0 + elx * 1.0) / det));
+    du += d_r1 * (sa * (ehy / det) + sb * (-ely / det));
+    dv += d_r1 * (sa * (-ehx / det) + sb * (elx / det));
     const double ca = cos(th[lo]), sa_lo = sin(th[lo]);
     const double cb = cos(th[hi]), sb_hi = sin(th[hi]);
     ds_lo += d_r1 * (-sa * ev.a / slo);
@@ -239,44 +327,61 @@ struct Pixel {
       atomicAdd(pg + o_rot + 3 * q + 2, f * h[q]);
     }
   }
+
+  __device__ void finish_forward(const RasterParams& P) {
+    const size_t p = (size_t)pix;
+    const double c0 = C[0] + T * P.opt.bg[0];
+    const double c1 = C[1] + T * P.opt.bg[1];
+    const double c2 = C[2] + T * P.opt.bg[2];
+    if (P.color) {
+      P.color[3 * p] = (float)c0;
+      P.color[3 * p + 1] = (float)c1;
+      P.color[3 * p + 2] = (float)c2;
+    }
+    if (P.normal) {
+      P.normal[3 * p] = (float)N[0];
+      P.normal[3 * p + 1] = (float)N[1];
+      P.normal[3 * p + 2] = (float)N[2];
+    }
+    if (P.depth) P.depth[p] = (float)D;
+    if (P.alpha) P.alpha[p] = (float)A;
+    if (P.pxstate) {
+      double* st = P.pxstate + 8 * p;
+      st[0] = c0;
+      st[1] = c1;
+      st[2] = c2;
+      st[3] = D;
+      st[4] = N[0];
+      st[5] = N[1];
+      st[6] = N[2];
+      st[7] = A;
+    }
+    if (P.replay_cap > 0) {
+      P.replay_cnt[p] = n_rec;
+      if (n_rec > P.replay_cap) atomicAdd(&P.counters[C_REPLAY_OVERFLOW], 1ull);
+    }
+    if (!F64 && P.pxflag) P.pxflag[p] = uncertain ? 1 : 0;
+  }
 };
 
 // MODE 0: SortCache streaming; MODE 1: list order (use_cache = false).
-template <int MODE, bool BWD>
+// F64: re-render of the pixels flagged by the fp32 pass.
+template <int MODE, bool BWD, bool F64>
 __global__ void __launch_bounds__(256) k_raster(RasterParams P) {
   __shared__ int s_id[256];
   __shared__ double s_num[256], s_r0[256], s_r1[256], s_r2[256];
   const int tile = blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
-  const bool active = x < P.cam.W && y < P.cam.H;
-  Pixel<BWD> px;
-  px.px = x + 0.5;
-  px.py = y + 0.5;
-  pixel_dir(P.cam, px.px, px.py, px.dir);
-  sh_basis_f((float)px.dir[0], (float)px.dir[1], (float)px.dir[2], P.opt.sh_degree, px.basis);
-  px.T = 1.0;
-  px.C[0] = px.C[1] = px.C[2] = px.D = px.N[0] = px.N[1] = px.N[2] = px.A = 0;
-  px.n_pop = px.n_comp = 0;
-  px.n_rec = 0;
-  px.err = false;
-  px.pix = y * P.cam.W + x;
-  if (BWD && active) {
-    const size_t p = (size_t)px.pix;
-    px.dC[0] = P.dC ? P.dC[3 * p] : 0.f;
-    px.dC[1] = P.dC ? P.dC[3 * p + 1] : 0.f;
-    px.dC[2] = P.dC ? P.dC[3 * p + 2] : 0.f;
-    px.dD = P.dD ? P.dD[p] : 0.f;
-    px.has_dN = P.dN != nullptr;
-    px.dN[0] = P.dN ? P.dN[3 * p] : 0.f;
-    px.dN[1] = P.dN ? P.dN[3 * p + 1] : 0.f;
-    px.dN[2] = P.dN ? P.dN[3 * p + 2] : 0.f;
-    px.dA = P.dA ? P.dA[p] : 0.f;
-    const double* st = P.pxstate + 8 * p;
-    // total = dC.C + dD D + dN.N + dA A (C includes T_n bg): grad.cpp:210-222
-    px.rest = (px.dC[0] * st[0] + px.dC[1] * st[1] + px.dC[2] * st[2]) + px.dD * st[3] +
-              (px.dN[0] * st[4] + px.dN[1] * st[5] + px.dN[2] * st[6]) + px.dA * st[7];
+  bool active = x < P.cam.W && y < P.cam.H;
+  if (P.pxflag && (F64 || BWD) && active) {
+    const bool flagged = P.pxflag[(size_t)y * P.cam.W + x] != 0;
+    active = F64 ? flagged : !flagged;  // the fp64 launch owns the flagged pixels
   }
+  if (F64 && __syncthreads_count(active) == 0) return;
+  Pixel<BWD, F64> px;
+  px.init(P, x, y);
+  if (BWD && active) px.init_bwd(P);
   bool done = !active;
   long long streamed = 0;
   double cd[kCacheCap];
@@ -301,7 +406,7 @@ __global__ void __launch_bounds__(256) k_raster(RasterParams P) {
     if (!done) {
       for (int c = 0; c < cnt; ++c) {
         // classify_intersect (geometry.cpp:40-46)
-        const double denom = px.dir[0] * s_r0[c] + px.dir[1] * s_r1[c] + px.dir[2] * s_r2[c];
+        const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], s_r0[c], s_r1[c], s_r2[c]);
         if (fabs(denom) < eps) continue;
         const double rt = s_num[c] / denom;
         if (rt <= 0) continue;
@@ -380,45 +485,11 @@ __global__ void __launch_bounds__(256) k_raster(RasterParams P) {
   if (!active) return;
   if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
   if (!BWD) {
-    const size_t p = (size_t)px.pix;
-    const double c0 = px.C[0] + px.T * P.opt.bg[0];
-    const double c1 = px.C[1] + px.T * P.opt.bg[1];
-    const double c2 = px.C[2] + px.T * P.opt.bg[2];
-    if (P.color) {
-      P.color[3 * p] = (float)c0;
-      P.color[3 * p + 1] = (float)c1;
-      P.color[3 * p + 2] = (float)c2;
-    }
-    if (P.normal) {
-      P.normal[3 * p] = (float)px.N[0];
-      P.normal[3 * p + 1] = (float)px.N[1];
-      P.normal[3 * p + 2] = (float)px.N[2];
-    }
-    if (P.depth) P.depth[p] = (float)px.D;
-    if (P.alpha) P.alpha[p] = (float)px.A;
-    if (P.pxstate) {
-      double* st = P.pxstate + 8 * p;
-      st[0] = c0;
-      st[1] = c1;
-      st[2] = c2;
-      st[3] = px.D;
-      st[4] = px.N[0];
-      st[5] = px.N[1];
-      st[6] = px.N[2];
-      st[7] = px.A;
-    }
-    if (P.replay_cap > 0) {
-      P.replay_cnt[p] = px.n_rec;
-      if (px.n_rec > P.replay_cap) atomicAdd(&P.counters[C_REPLAY_OVERFLOW], 1ull);
-    }
-    // work counters (warp-aggregated)
+    px.finish_forward(P);
     unsigned long long s = streamed, pp = px.n_pop, cc = px.n_comp;
-    for (int off = 16; off > 0; off >>= 1) {
-      s += __shfl_down_sync(__activemask(), s, off);
-      pp += __shfl_down_sync(__activemask(), pp, off);
-      cc += __shfl_down_sync(__activemask(), cc, off);
-    }
-    if ((threadIdx.x & 31) == 0) {
+    if (F64) {
+      atomicAdd(&P.counters[C_REDO_PIXELS], 1ull);
+    } else {
       atomicAdd(&P.counters[C_STREAMED], s);
       atomicAdd(&P.counters[C_POPPED], pp);
       atomicAdd(&P.counters[C_COMPOSITED], cc);
@@ -427,7 +498,8 @@ __global__ void __launch_bounds__(256) k_raster(RasterParams P) {
 }
 
 // exact_sort oracle mode (raster.cpp:395-401): every hit composited in
-// stable depth order.  One thread per pixel, selection by (depth, list index).
+// stable depth order (fp64 alpha).  One thread per pixel, selection by
+// (depth, list index).
 template <bool BWD>
 __global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
   const int tile = blockIdx.y;
@@ -436,32 +508,9 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
   if (l >= 256) return;
   const int x = tx * kTile + (l & 15), y = ty * kTile + (l >> 4);
   if (x >= P.cam.W || y >= P.cam.H) return;
-  Pixel<BWD> px;
-  px.px = x + 0.5;
-  px.py = y + 0.5;
-  pixel_dir(P.cam, px.px, px.py, px.dir);
-  sh_basis_f((float)px.dir[0], (float)px.dir[1], (float)px.dir[2], P.opt.sh_degree, px.basis);
-  px.T = 1.0;
-  px.C[0] = px.C[1] = px.C[2] = px.D = px.N[0] = px.N[1] = px.N[2] = px.A = 0;
-  px.n_pop = px.n_comp = 0;
-  px.n_rec = 0;
-  px.err = false;
-  px.pix = y * P.cam.W + x;
-  const size_t p = (size_t)px.pix;
-  if (BWD) {
-    px.dC[0] = P.dC ? P.dC[3 * p] : 0.f;
-    px.dC[1] = P.dC ? P.dC[3 * p + 1] : 0.f;
-    px.dC[2] = P.dC ? P.dC[3 * p + 2] : 0.f;
-    px.dD = P.dD ? P.dD[p] : 0.f;
-    px.has_dN = P.dN != nullptr;
-    px.dN[0] = P.dN ? P.dN[3 * p] : 0.f;
-    px.dN[1] = P.dN ? P.dN[3 * p + 1] : 0.f;
-    px.dN[2] = P.dN ? P.dN[3 * p + 2] : 0.f;
-    px.dA = P.dA ? P.dA[p] : 0.f;
-    const double* st = P.pxstate + 8 * p;
-    px.rest = (px.dC[0] * st[0] + px.dC[1] * st[1] + px.dC[2] * st[2]) + px.dD * st[3] +
-              (px.dN[0] * st[4] + px.dN[1] * st[5] + px.dN[2] * st[6]) + px.dA * st[7];
-  }
+  Pixel<BWD, true> px;
+  px.init(P, x, y);
+  if (BWD) px.init_bwd(P);
   const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
   double last_d = -1.0;
   long long last_j = -1;
@@ -471,7 +520,7 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
     for (long long j = beg; j < end; ++j) {
       const int id = (int)(P.pv[j] & 0xffffffffull);
       const Geo& g = P.geo[id];
-      const double denom = px.dir[0] * g.rz[0] + px.dir[1] * g.rz[1] + px.dir[2] * g.rz[2];
+      const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.rz[0], g.rz[1], g.rz[2]);
       if (fabs(denom) < P.opt.grazing_eps) continue;
       const double rt = g.num / denom;
       if (rt <= 0) continue;
@@ -488,53 +537,80 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
     if (!px.composite(P, best_d, (int)(P.pv[best_j] & 0xffffffffull))) break;
   }
   if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
-  if (!BWD) {
-    const double c0 = px.C[0] + px.T * P.opt.bg[0];
-    const double c1 = px.C[1] + px.T * P.opt.bg[1];
-    const double c2 = px.C[2] + px.T * P.opt.bg[2];
-    if (P.color) {
-      P.color[3 * p] = (float)c0;
-      P.color[3 * p + 1] = (float)c1;
-      P.color[3 * p + 2] = (float)c2;
-    }
-    if (P.normal) {
-      P.normal[3 * p] = (float)px.N[0];
-      P.normal[3 * p + 1] = (float)px.N[1];
-      P.normal[3 * p + 2] = (float)px.N[2];
-    }
-    if (P.depth) P.depth[p] = (float)px.D;
-    if (P.alpha) P.alpha[p] = (float)px.A;
-    if (P.pxstate) {
-      double* st = P.pxstate + 8 * p;
-      st[0] = c0;
-      st[1] = c1;
-      st[2] = c2;
-      st[3] = px.D;
-      st[4] = px.N[0];
-      st[5] = px.N[1];
-      st[6] = px.N[2];
-      st[7] = px.A;
-    }
-    if (P.replay_cap > 0) {
-      P.replay_cnt[p] = px.n_rec;
-      if (px.n_rec > P.replay_cap) atomicAdd(&P.counters[C_REPLAY_OVERFLOW], 1ull);
-    }
-  }
+  if (!BWD) px.finish_forward(P);
 }
 
 void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s) {
   if (n_tiles == 0) return;
   if (P.opt.exact_sort) {
+    RasterParams Q = P;
+    Q.pxflag = nullptr;
     dim3 grid(2, n_tiles);
-    if (bwd) k_raster_exact<true><<<grid, 128, 0, s>>>(P);
-    else k_raster_exact<false><<<grid, 128, 0, s>>>(P);
-  } else if (P.opt.use_cache) {
-    if (bwd) k_raster<0, true><<<n_tiles, 256, 0, s>>>(P);
-    else k_raster<0, false><<<n_tiles, 256, 0, s>>>(P);
-  } else {
-    if (bwd) k_raster<1, true><<<n_tiles, 256, 0, s>>>(P);
-    else k_raster<1, false><<<n_tiles, 256, 0, s>>>(P);
+    if (bwd) k_raster_exact<true><<<grid, 128, 0, s>>>(Q);
+    else k_raster_exact<false><<<grid, 128, 0, s>>>(Q);
+    return;
   }
+  // fp32 pass (all pixels; flags uncertain ones), then the fp64 pass over the
+  // flagged pixels (CTAs without flagged pixels exit immediately).
+  if (P.opt.use_cache) {
+    if (bwd) {
+      k_raster<0, true, false><<<n_tiles, 256, 0, s>>>(P);
+      k_raster<0, true, true><<<n_tiles, 256, 0, s>>>(P);
+    } else {
+      k_raster<0, false, false><<<n_tiles, 256, 0, s>>>(P);
+      k_raster<0, false, true><<<n_tiles, 256, 0, s>>>(P);
+    }
+  } else {
+    if (bwd) {
+      k_raster<1, true, false><<<n_tiles, 256, 0, s>>>(P);
+      k_raster<1, true, true><<<n_tiles, 256, 0, s>>>(P);
+    } else {
+      k_raster<1, false, false><<<n_tiles, 256, 0, s>>>(P);
+      k_raster<1, false, true><<<n_tiles, 256, 0, s>>>(P);
+    }
+  }
+}
+
+// Validation of alpha_f32's error bound against the fp64 path: random
+// (primitive, u, v) samples over each primitive's support; reports
+// max |a32 - a64| / (rel * a32 + 1e-30) and max |a32 - a64|.
+__global__ void k_alpha_bound(ShapeView S, int n, long long samples, unsigned long long seed,
+                              unsigned long long* max_ratio_bits, unsigned long long* max_abs_bits) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= samples || n == 0) return;
+  unsigned long long x = seed ^ (0x9E3779B97F4A7C15ull * (unsigned long long)(t + 1));
+  auto next = [&]() {
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    return (double)((x * 2685821657736338717ull) >> 11) * (1.0 / 9007199254740992.0);
+  };
+  const int i = (int)(next() * n) % n;
+  double smax = 0;
+  for (int k = 0; k < S.K; ++k) smax = dmax(smax, S.s[(size_t)i * S.K + k]);
+  const double r = 3.5 * smax * sqrt(next());
+  const double ang = kTwoPi * next();
+  const double u = r * cos(ang), v = r * sin(ang);
+  const double r2 = xa(xm(u, u), xm(v, v));
+  KEval ev;
+  eval_kernel(u, v, S, i, ev);
+  if (ev.degenerate) return;
+  const double a64 = S.o[i] * sharpen(ev.g, S.tau[i]);
+  float rel;
+  bool degen;
+  const float a32 = alpha_f32(u, v, r2, S, i, (float)S.o[i], (float)S.tau[i], (float)S.eta[i], &rel, &degen);
+  if (degen) return;
+  const double diff = fabs((double)a32 - a64);
+  const double ratio = diff / ((double)rel * a32 + 1e-30);
+  atomicMax(max_ratio_bits, (unsigned long long)__double_as_longlong(ratio));
+  atomicMax(max_abs_bits, (unsigned long long)__double_as_longlong(diff));
+}
+
+void launch_alpha_bound(const ShapeView& S, int n, long long samples, unsigned long long seed,
+                        unsigned long long* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), s);
+  if (samples > 0)
+    k_alpha_bound<<<(unsigned)((samples + 255) / 256), 256, 0, s>>>(S, n, samples, seed, out, out + 1);
 }
 
 // ---------------------------------------------------------------------------
