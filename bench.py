@@ -1,0 +1,348 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 DRK rasterizer (metric of BASELINE.json: megapixels/s).
+
+Workload (BASELINE.json configs[1], the metric's headline): forward render of
+100,000 DRKs, K=8, SH degree 3, 1920x1080, one view per GPU per step
+("scaling": "weak": views are independent; primitives replicated; no
+data-path collective).  A step goes from raw parameters resident in HBM to the
+four framebuffers (colour, depth, normal, alpha) in HBM: activation,
+preprocess, tile binning, radix sort, rasterization.  Inputs are seeded
+synthetic (paper_2412_11752_b200/scenes.py); L2 is flushed (256 MiB write)
+between timed steps and the flush is outside the timed events.
+
+The same line carries:
+  e2e          same metric through the C-ABI host-buffer entry (drk_forward_host):
+               pinned host params -> H2D -> render -> D2H of all four planes
+  fwd_bwd      config 2 (300k DRKs, 1280x720): forward + L1 loss + backward, MP/s
+  roofline     dominant kernel (fp32-pass rasterizer): algorithmic FP32 flops
+               (SURVEY.md §8(d) counts) / CUDA-event kernel time vs measured FFMA peak
+  cpu_baseline the reference CPU renderer (oracle/_ref, unmodified sources) on
+               a bounded crop of the same workload, all host threads
+`--impl reference` times that reference CPU renderer alone (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# SURVEY.md §8(d) algorithmic FP32 flops (FMA = 2): per pixel, per streamed
+# candidate (intersection), per popped candidate (alpha), per composited entry.
+F_PIXEL = {0: 34, 3: 82}
+F_ISECT = 22
+F_ALPHA = 37
+F_BLEND = {0: 30, 3: 120}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-crop", default="960x544", help="crop of the CPU baseline sample (tile aligned)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fwd-bwd", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.lines, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def reference_cpu_sample(crop: str, steps: int = 1):
+    """Reference CPU forward (activate + render, all host threads) on a centred crop of config 1."""
+    from oracle import ref
+    from paper_2412_11752_b200 import scenes
+    w, h = (int(x) for x in crop.split("x"))
+    sc = scenes.config_scene(1)
+    cam0 = scenes.config_cameras(1)[0]
+    x0 = (cam0.width // 2 - w // 2) // 16 * 16
+    y0 = (cam0.height // 2 - h // 2) // 16 * 16
+    cam = cam0.crop(x0, y0, w, h)
+    threads = ref.hardware_threads()
+    opt = ref.Options(sh_degree=3, threads=0)
+    secs = []
+    for _ in range(steps):
+        secs.append(ref.render(sc, cam, opt)["seconds"])
+    t = float(np.mean(secs))
+    return dict(value=w * h / t / 1e6, unit="megapixels/s", cores=threads, kind="reference",
+                sample=f"config 1 (100k DRK, SH3) centred {w}x{h} crop of the 1920x1080 view; reference activate+render "
+                       f"(oracle/_ref, unmodified sources, -O3) with RenderOptions::threads=0 ({threads} threads); "
+                       f"bin_primitives (single-threaded by design) still processes all primitives; "
+                       f"{steps} run(s), {t:.2f} s each"), t
+
+
+def run_reference(args):
+    """Reference CPU arm: rank 0 alone times the unmodified reference (oracle/_ref); W warm-up
+    steps are skipped (the CPU has no warm-up effects worth the minutes), K bounded steps timed."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    vals, cpu = [], None
+    for _ in range(max(1, args.steps)):
+        cpu, _ = reference_cpu_sample(args.cpu_crop, 1)
+        vals.append(cpu["value"])
+    v = float(np.mean(vals))
+    cpu["value"] = v
+    w, h = (int(x) for x in args.cpu_crop.split("x"))
+    line = {"impl": "reference", "metric": "megapixels/sec rendered (forward; fwd+bwd in fwd_bwd)", "value": v,
+            "unit": "megapixels/s", "n_gpus": world, "steps": args.steps, "warmup": 0,
+            "ms_per_step": 1e3 * (w * h) / (v * 1e6), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scenes.py generator)",
+            "config": {"workload": f"config1 forward (100k DRK, K=8, SH3, 1920x1080 view), {args.cpu_crop} centred "
+                                   "crop per step as the bounded CPU sample", "primitives": 100000, "K": 8,
+                       "sh_degree": 3},
+            "cpu_baseline": cpu,
+            "e2e": {"value": v, "unit": "megapixels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_11752_b200 import scenes
+    from paper_2412_11752_b200.api import FrameGrad, Rasterizer, RenderOptions
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    r = Rasterizer(local)
+    r.set_timing(True)
+    cfg = 1
+    sc = scenes.config_scene(cfg)
+    cam = scenes.config_cameras(cfg)[0]
+    opt = RenderOptions(sh_degree=3)
+    raw = torch.from_numpy(sc.f32()).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        r.render(raw, cam, opt)
+    torch.cuda.synchronize(dev)
+    stats0 = r.stats()
+
+    # ---- device-resident timed region ----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    raster_ms, launches, stage_acc = [], 0, {}
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            r.render(raw, cam, opt)
+            evs[i][1].record(stream)
+            st = r.stats()
+            raster_ms.append(st["stage_ms"]["raster"])
+            launches += st["launches"]
+            for k, v in st["stage_ms"].items():
+                stage_acc[k] = stage_acc.get(k, 0.0) + v
+        torch.cuda.synchronize(dev)
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    px = cam.width * cam.height
+    value = world * px / (ms_per_step * 1e-3) / 1e6
+    st = r.stats()
+
+    # ---- roofline of the dominant kernel (fp32-pass rasterizer) ----
+    flops = (px * F_PIXEL[3] + st["streamed"] * F_ISECT + st["popped"] * F_ALPHA + st["composited"] * F_BLEND[3])
+    rast_ms = float(np.mean(raster_ms))
+    peak = r.fp32_peak_tflops()
+    achieved = flops / (rast_ms * 1e-3) / 1e12
+    stage_ms = {k: v / args.steps for k, v in stage_acc.items() if k in ("activate", "preprocess", "rows_emit", "sort",
+                                                                         "raster", "raster_fp64")}
+    roofline = {"kernel": "k_raster<0,false,false> (fp32-alpha pass)", "bound": "fp32", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": "FFMA microbenchmark (drk_measure_fp32_peak) in this run; MEASURED_PEAKS.json has no "
+                               "FP32 CUDA-core figure",
+                "algorithmic_flops_per_launch": flops, "kernel_ms": rast_ms,
+                "counts": {"pixels": px, "streamed": st["streamed"], "popped": st["popped"],
+                           "composited": st["composited"]},
+                "share_of_step": rast_ms / ms_per_step}
+    # sort (HBM-bound): 10 passes max of 16 B/pair read + 16 B/pair write + 8 B/pair digit read
+    sort_ms = stage_ms.get("sort", 0.0)
+
+    # ---- e2e through the C-ABI host-buffer entry ----
+    e2e = None
+    host_raw = torch.from_numpy(sc.f32()).pin_memory()
+    outs = {"color": torch.empty(cam.height, cam.width, 3, pin_memory=True),
+            "depth": torch.empty(cam.height, cam.width, pin_memory=True),
+            "normal": torch.empty(cam.height, cam.width, 3, pin_memory=True),
+            "alpha": torch.empty(cam.height, cam.width, pin_memory=True)}
+    for _ in range(max(1, args.warmup)):
+        r.render_host_ptrs(host_raw, outs, cam, opt)
+    torch.cuda.synchronize(dev)
+    barrier()
+    e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        r.render_host_ptrs(host_raw, outs, cam, opt)
+        b.record(stream)
+        b.synchronize()
+        e_ms.append(a.elapsed_time(b))
+    e_tot = float(np.sum(e_ms))
+    if world > 1:
+        t = torch.tensor([e_tot], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_tot = float(t.item())
+    e2e = {"value": world * px / (e_tot / args.steps * 1e-3) / 1e6, "unit": "megapixels/s",
+           "h2d_bytes_per_step": int(host_raw.numel() * 4), "d2h_bytes_per_step": int(px * 8 * 4),
+           "path": "drk_forward_host (C-ABI): pinned host raw params -> device -> 4 framebuffers -> pinned host"}
+
+    # ---- forward + backward (config 2) ----
+    fwd_bwd = None
+    if not args.no_fwd_bwd:
+        sc2 = scenes.config_scene(2)
+        cam2 = scenes.config_cameras(2)[0]
+        raw2 = torch.from_numpy(sc2.f32()).to(dev)
+        tgt2 = torch.from_numpy(scenes.config_target(2, cam2).astype(np.float32)).to(dev)
+        opt2 = RenderOptions(sh_degree=3)
+        grad2 = torch.zeros_like(raw2)
+
+        def train_step():
+            fb = r.render(raw2, cam2, opt2)
+            _, dcol = r.l1_loss(fb.color, tgt2)
+            r.backward_render(raw2, FrameGrad(d_color=dcol), grad_out=grad2)
+
+        for _ in range(max(1, min(args.warmup, 2))):
+            train_step()
+        torch.cuda.synchronize(dev)
+        nfb = max(2, args.steps // 2)
+        fb_ms = []
+        bst = {}
+        for _ in range(nfb):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            train_step()
+            b.record(stream)
+            b.synchronize()
+            fb_ms.append(a.elapsed_time(b))
+            s2 = r.stats()["stage_ms"]
+            for k, v in s2.items():
+                bst[k] = bst.get(k, 0.0) + v / nfb
+        fb_tot = float(np.mean(fb_ms))
+        if world > 1:
+            t = torch.tensor([fb_tot], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            fb_tot = float(t.item())
+        px2 = cam2.width * cam2.height
+        fwd_bwd = {"value": world * px2 / (fb_tot * 1e-3) / 1e6, "unit": "megapixels/s", "ms_per_step": fb_tot,
+                   "steps": nfb, "workload": "config2: 300k DRK, K=8, SH3, 1280x720, forward + L1 loss + backward "
+                                             "(raw-parameter gradients), one view per GPU",
+                   "stage_ms": bst}
+
+    # ---- CPU baseline (rank 0, N = 1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu, _ = reference_cpu_sample(args.cpu_crop, 1)
+        except Exception as e:  # the oracle build is missing: report, do not fail the bench
+            cpu = {"value": None, "unit": "megapixels/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {"metric": "megapixels/sec rendered (forward; fwd+bwd in fwd_bwd)", "value": value,
+                "unit": "megapixels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32 (fp64 ray-plane depths, sort keys and accumulators; fp32 alpha with fp64 fallback)",
+                "data": "synthetic (seeded scenes.py generator; BASELINE.json config 1 distributions)",
+                "config": {"workload": "config1 forward: 100k DRK, K=8, SH degree 3, 1920x1080, 1 view per GPU per step",
+                           "primitives": 100000, "K": 8, "sh_degree": 3, "width": 1920, "height": 1080,
+                           "views_per_gpu": 1, "parallelism": f"views x{world} (replicated primitives)",
+                           "l2": "flushed between timed steps (256 MiB write, outside the timed events)"},
+                "stage_ms": stage_ms, "pairs": st["pairs"], "fp64_pixels": st["fp64_pixels"],
+                "roofline": roofline, "e2e": e2e, "fwd_bwd": fwd_bwd, "cpu_baseline": cpu,
+                "clocks": clk.summary(), "gpu_launches": int(launches)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -109,6 +109,11 @@ typedef struct drk_stats {
   int64_t poly_overflow;   /* primitives that needed the large-polygon path */
   int64_t replay_overflow; /* pixels whose replay exceeded record_replay */
   int64_t fp64_pixels;     /* pixels re-rendered in fp64 (termination within the fp32 error bound) */
+  int64_t launches;        /* kernels launched by the last forward + backward */
+  /* CUDA-event stage times of the last forward / backward, ms (when
+   * drk_set_timing(ctx, 1)): activate, preprocess, rows+emit, sort, raster,
+   * raster_fp64, backward_raster, activation_backward */
+  double stage_ms[8];
 } drk_stats;
 
 typedef struct drk_ctx drk_ctx;
@@ -123,6 +128,10 @@ int drk_scalar_count(int k, int sh_terms);
 void drk_default_options(drk_options* opt);
 int drk_get_stats(const drk_ctx* ctx, drk_stats* out);
 int drk_set_stream(drk_ctx* ctx, void* cuda_stream);
+/* Enables per-stage CUDA-event timing (drk_stats.stage_ms). */
+int drk_set_timing(drk_ctx* ctx, int enabled);
+/* Measured FP32 FFMA throughput of this device (TFLOP/s), for rooflines. */
+int drk_measure_fp32_peak(drk_ctx* ctx, double* tflops);
 
 /* --- activation (reference core.cpp:133-146 activate) -------------------- */
 /* raw (f32 SoA) -> activated fp64 arrays owned by the context; the pointers

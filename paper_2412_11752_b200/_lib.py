@@ -62,9 +62,14 @@ class FrameGrad_(C.Structure):
     _fields_ = [(f, C.c_void_p) for f in ("d_color", "d_depth", "d_normal", "d_alpha")]
 
 
+STAGES = ("activate", "preprocess", "rows_emit", "sort", "raster", "raster_fp64", "backward_raster",
+          "activation_backward")
+
+
 class Stats_(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("primitives", "pairs", "streamed", "popped", "composited", "near_ties",
-                                          "poly_overflow", "replay_overflow", "fp64_pixels")]
+                                          "poly_overflow", "replay_overflow", "fp64_pixels", "launches")] + \
+        [("stage_ms", C.c_double * 8)]
 
 
 class AdamConfig_(C.Structure):
@@ -86,6 +91,8 @@ SIGNATURES = {
     "drk_default_options": (None, [C.POINTER(Options_)]),
     "drk_get_stats": (C.c_int, [_P, C.POINTER(Stats_)]),
     "drk_set_stream": (C.c_int, [_P, _P]),
+    "drk_set_timing": (C.c_int, [_P, C.c_int]),
+    "drk_measure_fp32_peak": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "drk_activate": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(Prims_)]),
     "drk_forward": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(Camera_), C.POINTER(Options_),
                               _P, _P, _P, _P]),

@@ -278,6 +278,19 @@ class Rasterizer:
         self._shape = (n, k, terms, H, W)
         return out
 
+    def render_host_ptrs(self, raw_host: torch.Tensor, outs: dict, cam: Camera, opt: RenderOptions = None,
+                         k: int = 8):
+        """drk_forward_host with caller-owned (pinned) host tensors: raw [S, n] f32 in,
+        outs['color'|'depth'|'normal'|'alpha'] f32 out; ordered on the current torch stream."""
+        opt = opt or RenderOptions()
+        S, n = raw_host.shape
+        terms = (S - (3 + 4 + 2 * k + 3)) // 3
+        self._sync_stream()
+        self._check(_lib.lib().drk_forward_host(self._h, C.c_void_p(raw_host.data_ptr()), n, k, terms,
+                                                C.byref(_camera(cam)), C.byref(_options(opt)),
+                                                *[_ptr(outs.get(f)) for f in ("color", "depth", "normal", "alpha")]))
+        self._shape = (n, k, terms, cam.height, cam.width)
+
     def tile_binning(self) -> TileBinning:
         """drk::bin_primitives result of the last forward (reference raster.hpp:30-31)."""
         total = C.c_int64(0)
@@ -318,7 +331,17 @@ class Rasterizer:
     def stats(self) -> dict:
         s = _lib.Stats_()
         self._check(_lib.lib().drk_get_stats(self._h, C.byref(s)))
-        return {f: getattr(s, f) for f, _ in _lib.Stats_._fields_}
+        out = {f: getattr(s, f) for f, _ in _lib.Stats_._fields_ if f != "stage_ms"}
+        out["stage_ms"] = dict(zip(_lib.STAGES, list(s.stage_ms)))
+        return out
+
+    def set_timing(self, enabled: bool = True):
+        self._check(_lib.lib().drk_set_timing(self._h, int(enabled)))
+
+    def fp32_peak_tflops(self) -> float:
+        v = C.c_double(0)
+        self._check(_lib.lib().drk_measure_fp32_peak(self._h, C.byref(v)))
+        return v.value
 
     # --- backward ------------------------------------------------------
     def backward_render(self, raw, frame_grad: FrameGrad, grad_out: torch.Tensor | None = None,

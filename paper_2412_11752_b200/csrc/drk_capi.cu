@@ -134,6 +134,19 @@ static int read_counters(drk_ctx* c, unsigned long long* h) {
   return cuda_check(c, cudaStreamSynchronize(c->stream), "counters");
 }
 
+static void mark(drk_ctx* c, int i) {
+  if (c->timing) cudaEventRecord(c->ev[i], c->stream);
+}
+
+static float elapsed(drk_ctx* c, int a, int b) {
+  float ms = 0;
+  if (cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.f;
+  }
+  return ms;
+}
+
 int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float* color, float* depth,
                 float* normal, float* alpha) {
   const Activated& A = c->act;
@@ -141,6 +154,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     return set_error(c, DRK_ERR_INVALID_ARG, "invalid camera");
   if (A.K < 3 || A.K > kMaxK) return set_error(c, DRK_ERR_UNSUPPORTED, "K must be in [3, 16]");
   cudaStream_t s = c->stream;
+  mark(c, 1);
   c->cam = *cam;
   c->opt = *opt;
   c->camd = make_cam(cam);
@@ -169,6 +183,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     if (n > 0)
       k_prep0<<<(n + 127) / 128, 128, 0, s>>>(A, cd, od, geo, bbox, hullref, pool, c->hull_cap, rowcnt, ctr,
                                                 nullptr, 0, nullptr, 0, ovf);
+    DRK_COUNT_LAUNCH();
     unsigned long long h[C_COUNT];
     if (int st = read_counters(c, h)) return st;
     const long long n_ovf = (long long)h[C_POLY_OVERFLOW];
@@ -203,6 +218,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     c->hull_cap = (long long)h[C_HULL_POOL] + (long long)h[C_HULL_POOL] / 4 + 1024;
     if (attempt == 3) return set_error(c, DRK_ERR_OOM, "hull pool retries");
   }
+  mark(c, 2);
   // rows
   long long n_rows = 0;
   if (int st = exclusive_scan<int>(c, rowcnt, n, rowoff, &n_rows)) return st;
@@ -236,6 +252,8 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   if (n_rows > 0)
     k_emit<<<(unsigned)((n_rows + 127) / 128), 128, 0, s>>>(n_rows, rows, rowpairoff, geo, cdirs, tdirs, cd, od, pk,
                                                             pv, tilecnt);
+  launch_counter() += 3;
+  mark(c, 3);
   if (int st = sort_pairs(c, pk, pv, pk2, pv2, n_pairs)) return st;
   // keep the sorted arrays in c->pk / c->pv
   if (pk != c->pk.p) {
@@ -244,6 +262,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   }
   long long tot = 0;
   if (int st = exclusive_scan<int>(c, tilecnt, n_tiles + 1, tileoff, &tot)) return st;
+  mark(c, 4);
   // per-pixel state / replay
   double* pxstate = ensure<double>(c->pxstate, 8 * (size_t)n_pix);
   unsigned char* pxflag = ensure<unsigned char>(c->pxflag, (size_t)n_pix);
@@ -262,10 +281,14 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     P.replay_rec = ensure<double>(c->replay_rec, 5 * (size_t)n_pix * P.replay_cap);
     if (!P.replay_cnt || !P.replay_ids || !P.replay_rec) return set_error(c, DRK_ERR_OOM, "replay buffers");
   }
-  launch_raster(P, n_tiles, false, s);
+  launch_raster(P, n_tiles, false, s, c->timing ? c->ev[5] : nullptr);
+  mark(c, 6);
   if (int st = cuda_check(c, cudaGetLastError(), "raster")) return st;
   unsigned long long h[C_COUNT];
   if (int st = read_counters(c, h)) return st;
+  if (c->timing)
+    for (int i = 0; i < 6; ++i) c->stats.stage_ms[i] = elapsed(c, i, i + 1);
+  c->stats.launches = launch_counter() - c->launch_base;
   c->stats.pairs = n_pairs;
   c->stats.streamed = (int64_t)h[C_STREAMED];
   c->stats.popped = (int64_t)h[C_POPPED];
@@ -304,12 +327,22 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   P.touched = tch;
   (void)deterministic;  // atomics; see DESIGN.md (deterministic mode: adapter reduction)
   const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
+  mark(c, 7);
   launch_raster(P, n_tiles, true, s);
+  mark(c, 8);
   if (int st = cuda_check(c, cudaGetLastError(), "raster bwd")) return st;
   launch_act_bwd(n, K, A.terms, raw, gact, G, tch, static_cast<const Geo*>(c->geo.p), c->camd, grad_raw,
                  d_center_world, screen_grad, touched, accumulate, s);
+  DRK_COUNT_LAUNCH();
+  mark(c, 9);
   if (int st = cuda_check(c, cudaGetLastError(), "activation bwd")) return st;
-  return cuda_check(c, cudaStreamSynchronize(s), "backward");
+  if (int st = cuda_check(c, cudaStreamSynchronize(s), "backward")) return st;
+  if (c->timing) {
+    c->stats.stage_ms[6] = elapsed(c, 7, 8);
+    c->stats.stage_ms[7] = elapsed(c, 8, 9);
+  }
+  c->stats.launches = launch_counter() - c->launch_base;
+  return DRK_OK;
 }
 
 int run_l1_loss(drk_ctx* c, const float* r, const float* t, int w, int h, double* loss, float* dcol) {
@@ -372,8 +405,22 @@ int drk_ctx_create(int device, drk_ctx** out) {
     return DRK_ERR_CUDA;
   }
   c->own_stream = true;
+  for (cudaEvent_t& e : c->ev) cudaEventCreate(&e);
   *out = c;
   return DRK_OK;
+}
+
+int drk_set_timing(drk_ctx* c, int enabled) {
+  if (!c) return DRK_ERR_INVALID_ARG;
+  c->timing = enabled != 0;
+  return DRK_OK;
+}
+
+int drk_measure_fp32_peak(drk_ctx* c, double* tflops) {
+  if (!c || !tflops) return DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  *tflops = measure_fp32_peak(c->stream);
+  return cuda_check(c, cudaGetLastError(), "fp32 peak");
 }
 
 void drk_ctx_destroy(drk_ctx* c) {
@@ -388,6 +435,8 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
                     &c->counters, &c->scan_tmp, &c->loss_tmp};
   for (DevBuf* b : bufs) release(*b);
+  for (cudaEvent_t e : c->ev)
+    if (e) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -426,6 +475,8 @@ int drk_forward(drk_ctx* c, const float* raw, int n, int k, int sh_terms, const 
   if (k < 3 || k > kMaxK) return set_error(c, DRK_ERR_GENERIC, "K must be at least 3 (and at most 16 here)");
   cudaSetDevice(c->device);
   c->has_fwd = false;
+  c->launch_base = launch_counter();
+  mark(c, 0);
   if (int st = launch_activate(c, raw, n, k, sh_terms)) return st;
   return run_forward(c, cam, opt, color, depth, normal, alpha);
 }
@@ -436,6 +487,8 @@ int drk_forward_prims(drk_ctx* c, const drk_prims* prims, int n, int k, int sh_t
   if (k < 3 || k > kMaxK) return set_error(c, DRK_ERR_GENERIC, "K must be at least 3 (and at most 16 here)");
   cudaSetDevice(c->device);
   c->has_fwd = false;
+  c->launch_base = launch_counter();
+  mark(c, 0);
   if (int st = launch_shape(c, prims, n, k, sh_terms)) return st;
   return run_forward(c, cam, opt, color, depth, normal, alpha);
 }

@@ -16,6 +16,13 @@ struct DevBuf {
   size_t bytes = 0;
 };
 
+// Process-wide count of kernels this library has launched (drk_stats.launches).
+inline long long& launch_counter() {
+  static long long n = 0;
+  return n;
+}
+#define DRK_COUNT_LAUNCH() (++::drk::launch_counter())
+
 // Grow-only device allocation; returns nullptr on OOM.
 void* ensure_bytes(DevBuf& b, size_t bytes);
 template <class T>
@@ -71,7 +78,8 @@ struct RasterParams {
   unsigned char* pxflag;  // 1 = pixel needs the fp64 re-render (uncertain termination)
 };
 
-void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s);
+void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s, cudaEvent_t mid = nullptr);
+double measure_fp32_peak(cudaStream_t s);
 
 }  // namespace drk
 
@@ -93,6 +101,11 @@ struct drk_ctx {
   drk::DevBuf gact, touched;
   drk::DevBuf counters, scan_tmp, loss_tmp;
   int64_t hull_cap = 0;
+
+  // stage timing
+  bool timing = false;
+  cudaEvent_t ev[10] = {};
+  long long launch_base = 0;
 
   // last forward
   bool has_fwd = false;

@@ -596,11 +596,13 @@ static int launch_shape_consts(drk_ctx* c, int n, int K) {
   A.hf = ensure<float>(c->a_hf, (size_t)K * n);
   if (!A.ex || !A.ey || !A.det || !A.thf || !A.invdetf || !A.piogf || !A.hf)
     return set_error(c, DRK_ERR_OOM, "shape buffers");
-  if (n > 0)
+  if (n > 0) {
     k_shape<<<(n + 127) / 128, 128, 0, c->stream>>>(n, K, A.s, A.th, const_cast<double*>(A.ex),
                                                    const_cast<double*>(A.ey), const_cast<double*>(A.det),
                                                    const_cast<float*>(A.thf), const_cast<float*>(A.invdetf),
                                                    const_cast<float*>(A.piogf), const_cast<float*>(A.hf));
+    DRK_COUNT_LAUNCH();
+  }
   return cuda_check(c, cudaGetLastError(), "shape");
 }
 
@@ -626,6 +628,7 @@ int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms) {
         raw, n, K, terms, const_cast<double*>(A.mu), const_cast<double*>(A.rot), const_cast<double*>(A.s),
         const_cast<double*>(A.th), const_cast<double*>(A.eta), const_cast<double*>(A.tau),
         const_cast<double*>(A.o), const_cast<float*>(A.sh), ctr);
+  if (n > 0) DRK_COUNT_LAUNCH();
   if (int st = launch_shape_consts(c, n, K)) return st;
   unsigned long long h[C_COUNT];
   if (int st = cuda_check(c, cudaMemcpyAsync(h, ctr, sizeof h, cudaMemcpyDeviceToHost, c->stream), "activate"))

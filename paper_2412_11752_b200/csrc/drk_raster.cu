@@ -540,8 +540,9 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
   if (!BWD) px.finish_forward(P);
 }
 
-void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s) {
+void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s, cudaEvent_t mid) {
   if (n_tiles == 0) return;
+  launch_counter() += P.opt.exact_sort ? 1 : 2;
   if (P.opt.exact_sort) {
     RasterParams Q = P;
     Q.pxflag = nullptr;
@@ -553,22 +554,55 @@ void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s)
   // fp32 pass (all pixels; flags uncertain ones), then the fp64 pass over the
   // flagged pixels (CTAs without flagged pixels exit immediately).
   if (P.opt.use_cache) {
-    if (bwd) {
-      k_raster<0, true, false><<<n_tiles, 256, 0, s>>>(P);
-      k_raster<0, true, true><<<n_tiles, 256, 0, s>>>(P);
-    } else {
-      k_raster<0, false, false><<<n_tiles, 256, 0, s>>>(P);
-      k_raster<0, false, true><<<n_tiles, 256, 0, s>>>(P);
-    }
+    if (bwd) k_raster<0, true, false><<<n_tiles, 256, 0, s>>>(P);
+    else k_raster<0, false, false><<<n_tiles, 256, 0, s>>>(P);
+    if (mid) cudaEventRecord(mid, s);
+    if (bwd) k_raster<0, true, true><<<n_tiles, 256, 0, s>>>(P);
+    else k_raster<0, false, true><<<n_tiles, 256, 0, s>>>(P);
   } else {
-    if (bwd) {
-      k_raster<1, true, false><<<n_tiles, 256, 0, s>>>(P);
-      k_raster<1, true, true><<<n_tiles, 256, 0, s>>>(P);
-    } else {
-      k_raster<1, false, false><<<n_tiles, 256, 0, s>>>(P);
-      k_raster<1, false, true><<<n_tiles, 256, 0, s>>>(P);
-    }
+    if (bwd) k_raster<1, true, false><<<n_tiles, 256, 0, s>>>(P);
+    else k_raster<1, false, false><<<n_tiles, 256, 0, s>>>(P);
+    if (mid) cudaEventRecord(mid, s);
+    if (bwd) k_raster<1, true, true><<<n_tiles, 256, 0, s>>>(P);
+    else k_raster<1, false, true><<<n_tiles, 256, 0, s>>>(P);
   }
+}
+
+// FFMA throughput probe (8 independent chains per thread, 148 x 8 CTAs).
+__global__ void __launch_bounds__(256) k_ffma(float* out, int iters) {
+  float a[8];
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3f + k;
+  const float b = 0.9999f, c = 1e-4f;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], b, c);
+  float s = 0;
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678f) out[0] = s;
+}
+
+double measure_fp32_peak(cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float* out = nullptr;
+  cudaMalloc(&out, sizeof(float));
+  const int iters = 1 << 16, blocks = sms * 8;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_ffma<<<blocks, 256, 0, s>>>(out, iters / 16);  // warm-up
+  cudaEventRecord(e0, s);
+  k_ffma<<<blocks, 256, 0, s>>>(out, iters);
+  cudaEventRecord(e1, s);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double flops = 2.0 * 8.0 * iters * (double)blocks * 256;
+  return flops / (ms * 1e-3) / 1e12;
 }
 
 // Validation of alpha_f32's error bound against the fp64 path: random

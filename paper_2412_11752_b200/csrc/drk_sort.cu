@@ -66,6 +66,7 @@ void scan_level(const T* in, long long n, long long* out, long long* tmp, cudaSt
   long long* bsum = tmp;
   long long* bpre = tmp + nb + 1;
   k_scan_block<T><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, out, bsum);
+  launch_counter() += nb > 1 ? 2 : 1;
   if (nb > 1) {
     scan_level<long long>(bsum, nb, bpre, tmp + 2 * nb + 2, s);
     k_scan_add<<<(unsigned)nb, kScanThreads, 0, s>>>(out, n, bpre);
@@ -201,6 +202,7 @@ int sort_pairs(drk_ctx* c, unsigned long long*& k, unsigned long long*& v, unsig
   const unsigned long long init[4] = {0ull, ~0ull, 0ull, ~0ull};
   cudaMemcpyAsync(acc, init, sizeof init, cudaMemcpyHostToDevice, s);
   k_bits<<<min(nblk * 8, 148 * 8), 256, 0, s>>>(k, v, n, acc);
+  DRK_COUNT_LAUNCH();
   unsigned long long h[4];
   cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, s);
   if (int st = cuda_check(c, cudaStreamSynchronize(s), "sort bits")) return st;
@@ -219,6 +221,7 @@ int sort_pairs(drk_ctx* c, unsigned long long*& k, unsigned long long*& v, unsig
     k_rs_hist<<<nblk, kRsThreads, 0, s>>>(src, n, passes[p].shift, hist, nblk);
     if (int st = exclusive_scan<unsigned>(c, hist, (long long)256 * nblk, off, nullptr)) return st;
     k_rs_scatter<<<nblk, kRsThreads, 0, s>>>(k, v, k2, v2, n, passes[p].shift, passes[p].from_v, off, nblk);
+    launch_counter() += 2;
     std::swap(k, k2);
     std::swap(v, v2);
   }
