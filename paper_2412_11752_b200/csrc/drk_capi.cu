@@ -126,6 +126,9 @@ static RasterParams raster_params(drk_ctx* c) {
   P.sh = A.sh;
   P.terms = A.terms;
   P.counters = static_cast<unsigned long long*>(c->counters.p);
+  // pixels flagged for the fp64 re-render (list written by the fp32 pass)
+  P.redo_list = static_cast<int*>(c->redo.p);
+  P.redo_count = reinterpret_cast<unsigned int*>(ensure<unsigned long long>(c->redo_cnt, 1));
   return P;
 }
 
@@ -266,7 +269,8 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   // per-pixel state / replay
   double* pxstate = ensure<double>(c->pxstate, 8 * (size_t)n_pix);
   unsigned char* pxflag = ensure<unsigned char>(c->pxflag, (size_t)n_pix);
-  if (!pxstate || !pxflag) return set_error(c, DRK_ERR_OOM, "pixel state");
+  int* redo = ensure<int>(c->redo, (size_t)n_pix + 1);
+  if (!pxstate || !pxflag || !redo) return set_error(c, DRK_ERR_OOM, "pixel state");
   RasterParams P = raster_params(c);
   P.pxflag = pxflag;
   P.color = color;
@@ -429,7 +433,7 @@ void drk_ctx_destroy(drk_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
                     &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
-                    &c->pxflag, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->rowcnt,
+                    &c->pxflag, &c->redo, &c->redo_cnt, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->rowcnt,
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->pk2, &c->pv2,
                     &c->hist, &c->sortoff, &c->tilecnt, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,

@@ -76,6 +76,8 @@ struct RasterParams {
   unsigned char* touched;
   unsigned long long* counters;
   unsigned char* pxflag;  // 1 = pixel needs the fp64 re-render (uncertain termination)
+  int* redo_list;         // flagged pixel indices (forward fp32 pass appends)
+  unsigned int* redo_count;
 };
 
 void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s, cudaEvent_t mid = nullptr);
@@ -91,7 +93,7 @@ struct drk_ctx {
 
   // activated primitives owned by the context (raw path)
   drk::DevBuf a_mu, a_rot, a_s, a_th, a_eta, a_tau, a_o, a_sh, a_ex, a_ey, a_det;
-  drk::DevBuf a_thf, a_invdetf, a_piogf, a_hf, pxflag;
+  drk::DevBuf a_thf, a_invdetf, a_piogf, a_hf, pxflag, redo, redo_cnt;
   drk::Activated act{};
 
   // per view

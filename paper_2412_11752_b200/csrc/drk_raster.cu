@@ -154,14 +154,8 @@ struct Pixel {
     }
     if (a < P.opt.alpha_min) return true;
     a = dmin(a, 1.0 - 1e-6);
-    // SH colour (geometry.cpp:126-138) in fp32
-    const float* shp = P.sh + (size_t)id * P.terms * 3;
-    float r0 = 0.5f, r1 = 0.5f, r2c = 0.5f;
-    for (int t = 0; t < P.opt.terms_active; ++t) {
-      r0 += basis[t] * __ldg(shp + 3 * t);
-      r1 += basis[t] * __ldg(shp + 3 * t + 1);
-      r2c += basis[t] * __ldg(shp + 3 * t + 2);
-    }
+    float r0, r1, r2c;
+    sh_rgb(P, id, r0, r1, r2c);
     const bool cl0 = r0 < 0, cl1 = r1 < 0, cl2 = r2c < 0;
     const double rgb[3] = {cl0 ? 0.0 : (double)r0, cl1 ? 0.0 : (double)r1, cl2 ? 0.0 : (double)r2c};
     const double sgn = denom < 0 ? 1.0 : -1.0;
@@ -328,6 +322,271 @@ struct Pixel {
     }
   }
 
+  // ---- warp-cooperative backward (k_raster_bwd) -------------------------
+  // Called by all 32 lanes of a warp together.  `want` lanes replay the
+  // forward decision for their popped entry; composited records compute
+  // their activated-space gradient, and each of the G components is reduced
+  // over the lanes whose record hits the same primitive as the first
+  // composited lane (butterfly shuffles), then added to HBM with one fp64
+  // atomic; lanes of other primitives add their own values directly.
+  // Returns false once this lane's pixel saturates.
+  __device__ bool composite_warp(const RasterParams& P, bool want, double rt, int id) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    bool rec = false, cont = true, lp = false, use64 = F64;
+    double a = 0, u = 0, v = 0, denom = 0, dpw = 0, dph = 0, rz[3] = {0, 0, 0};
+    float rgbf[3] = {0, 0, 0};
+    bool cl[3] = {false, false, false};
+    KEval ev;
+    ev.center = ev.clamped = ev.degenerate = false;
+    ev.g = 1.0;
+    ev.lo = ev.hi = 0;
+    const Geo* gp = nullptr;
+    float rel = 0.f;
+    if (want) {
+      const Geo& g = P.geo[id];
+      gp = &g;
+      rz[0] = g.rz[0];
+      rz[1] = g.rz[1];
+      rz[2] = g.rz[2];
+      denom = xdot3(dir[0], dir[1], dir[2], rz[0], rz[1], rz[2]);
+      const double h0 = xs(xa(P.cam.o[0], xm(rt, dir[0])), g.mu[0]);
+      const double h1 = xs(xa(P.cam.o[1], xm(rt, dir[1])), g.mu[1]);
+      const double h2 = xs(xa(P.cam.o[2], xm(rt, dir[2])), g.mu[2]);
+      u = xdot3(g.rx[0], g.rx[1], g.rx[2], h0, h1, h2);
+      v = xdot3(g.ry[0], g.ry[1], g.ry[2], h0, h1, h2);
+      const double cos_view = fabs(denom);
+      if (g.has_proj) {
+        dpw = xs(px, g.ppx);
+        dph = xs(py, g.ppy);
+      }
+      const double r2 = xa(xm(u, u), xm(v, v));
+      const bool reject =
+          r2 > g.r2max && (!g.has_proj || dpw * dpw + dph * dph > cos_view * cos_view * g.dp2max);
+      if (!reject) {
+        const double o = P.S.o[id], tau = P.S.tau[id];
+        if (!F64) {
+          bool degen;
+          float relk;
+          const float ak = alpha_f32(u, v, r2, P.S, id, (float)o, (float)tau, (float)P.S.eta[id], &relk, &degen);
+          if (degen) {
+            err = true;
+            cont = false;
+          }
+          float at = ak, relt = relk;
+          if (g.has_proj) {
+            const float sl = (float)P.opt.lowpass_radius, cv = (float)cos_view;
+            const float ex = fmaxf(-((float)(dpw * dpw + dph * dph)) / (2.0f * cv * cv * sl * sl), -30.0f);
+            const float f = (float)o * expf(ex);
+            const float relf = 4e-7f * (1.0f - ex);
+            if (fabsf(f - ak) <= relk * ak + relf * f) use64 = true;
+            if (f > ak) {
+              at = f;
+              relt = relf;
+              lp = true;
+            }
+          }
+          const float amin = (float)P.opt.alpha_min;
+          if (fabsf(at - amin) <= relt * at + 1e-12f) use64 = true;
+          if (at >= 0.99f && fabs((double)at - (1.0 - 1e-6)) <= (double)relt * at + 1e-12) use64 = true;
+          a = (double)at;
+          rel = relt;
+        }
+        if (cont && use64) {
+          eval_kernel(u, v, P.S, id, ev);
+          if (ev.degenerate) {
+            err = true;
+            cont = false;
+          } else {
+            const double a_kernel = o * sharpen(ev.g, tau);
+            a = a_kernel;
+            lp = false;
+            if (g.has_proj) {
+              const double f = low_pass_filter_term(dpw, dph, cos_view, o, P.opt.lowpass_radius);
+              if (f > a_kernel) {
+                a = f;
+                lp = true;
+              }
+            }
+            rel = 0.f;
+          }
+        }
+        if (cont && a >= P.opt.alpha_min) {
+          a = dmin(a, 1.0 - 1e-6);
+          rec = true;
+          float r0, r1, r2c;
+          sh_rgb(P, id, r0, r1, r2c);
+          cl[0] = r0 < 0;
+          cl[1] = r1 < 0;
+          cl[2] = r2c < 0;
+          rgbf[0] = cl[0] ? 0.f : r0;
+          rgbf[1] = cl[1] ? 0.f : r1;
+          rgbf[2] = cl[2] ? 0.f : r2c;
+          if (!use64 && !lp && !(a >= 1.0 - 1e-6 - 1e-12)) eval_kernel(u, v, P.S, id, ev);
+        }
+      }
+    }
+    // upstream scalars (grad.cpp:224-233)
+    double wb = 0, dat = 0, sgn = 0;
+    if (rec) {
+      sgn = denom < 0 ? 1.0 : -1.0;
+      wb = T * a;
+      const double cw = (dC[0] * rgbf[0] + dC[1] * rgbf[1] + dC[2] * rgbf[2]) + dD * rt +
+                        (dN[0] * (sgn * rz[0]) + dN[1] * (sgn * rz[1]) + dN[2] * (sgn * rz[2])) + dA;
+      rest -= wb * cw;
+      dat = T * cw - rest / (1.0 - a);
+      P.touched[id] = 1;
+      ++n_comp;
+    }
+    // per-record activated-space gradient (grad.cpp:237-301, :16-101)
+    const int K = P.S.K;
+    double dcen[3] = {0, 0, 0}, drot[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double deta = 0, dtau = 0, dop = 0, ds_lo = 0, ds_hi = 0, da_lo = 0, da_hi = 0;
+    int lo = 0, hi = 0;
+    if (rec) {
+      const Geo& g = *gp;
+      if (has_dN)
+        for (int q = 0; q < 3; ++q) drot[3 * q + 2] += wb * sgn * dN[q];
+      if (dD != 0) {
+        const double d_rt = wb * dD;
+        for (int q = 0; q < 3; ++q) {
+          const double h = P.cam.o[q] + rt * dir[q] - g.mu[q];
+          dcen[q] += d_rt * rz[q] / denom;
+          drot[3 * q + 2] += d_rt * (-h / denom);
+        }
+      }
+      const bool alpha_clamped = a >= 1.0 - 1e-6 - 1e-12;
+      const double o = P.S.o[id];
+      if (!alpha_clamped && lp) {
+        const double cv = fabs(denom), sl = P.opt.lowpass_radius;
+        dop += dat * a / o;
+        const double inv = 1.0 / (cv * cv * sl * sl);
+        const double d_dpw = dat * a * (-dpw * inv);
+        const double d_dph = dat * a * (-dph * inv);
+        const double d_cos = dat * a * (dpw * dpw + dph * dph) * inv / cv;
+        double J[6];
+        projection_jacobian(P.cam, g.mu, J);
+        for (int q = 0; q < 3; ++q) dcen[q] += -(J[q] * d_dpw + J[3 + q] * d_dph);
+        const double sg = denom < 0 ? -1.0 : 1.0;
+        for (int q = 0; q < 3; ++q) drot[3 * q + 2] += d_cos * sg * dir[q];
+      } else if (!alpha_clamped) {
+        const double tau = P.S.tau[id];
+        dop += dat * sharpen(ev.g, tau);
+        if (!ev.center) {
+          const int br = sharpen_branch(ev.g, tau);
+          dtau += dat * o * sharpen_dtau(br, ev.g, tau);
+          if (!ev.clamped) {
+            const double d_g = dat * o * sharpen_slope(br, tau);
+            const double d_q = d_g * (-0.5 * ev.g);
+            lo = ev.lo;
+            hi = ev.hi;
+            const double* s = P.S.s + (size_t)id * K;
+            const double* th = P.S.th + (size_t)id * K;
+            const double slo = s[lo], shi = s[hi], eta = P.S.eta[id];
+            deta += d_q * (ev.r1 * ev.r1 - ev.r2 * ev.inv_sbar);
+            const double d_r1 = d_q * eta * 2.0 * ev.r1;
+            const double d_r2sq = d_q * (1.0 - eta) * ev.inv_sbar;
+            const double d_inv = d_q * (1.0 - eta) * ev.r2;
+            const double c = cos(ev.delta);
+            ds_lo = d_inv * (-(1.0 + c) / (slo * slo * slo));
+            ds_hi = d_inv * (-(1.0 - c) / (shi * shi * shi));
+            const double d_c = d_inv * (0.5 / (slo * slo) - 0.5 / (shi * shi));
+            const double d_delta = d_c * (-sin(ev.delta));
+            double alo = th[lo], ahi = th[hi], theta = ev.theta;
+            if (hi == 0) {
+              alo -= kTwoPi;
+              if (theta > th[K - 1]) theta -= kTwoPi;
+            }
+            const double gap = ahi - alo;
+            const double d_tfd = d_delta * kPi / gap;
+            da_lo = d_delta * kPi * (theta - ahi) / (gap * gap);
+            da_hi = d_delta * (-kPi) * (theta - alo) / (gap * gap);
+            const double r2s = dmax(ev.r2, 1e-24);
+            double du = d_tfd * (-v / r2s);
+            double dv = d_tfd * (u / r2s);
+            du += d_r2sq * 2.0 * u;
+            dv += d_r2sq * 2.0 * v;
+            const double sa = ev.a > 0 ? 1 : (ev.a < 0 ? -1 : 0);
+            const double sb = ev.b > 0 ? 1 : (ev.b < 0 ? -1 : 0);
+            const double elx = P.S.ex[(size_t)id * K + lo], ely = P.S.ey[(size_t)id * K + lo];
+            const double ehx = P.S.ex[(size_t)id * K + hi], ehy = P.S.ey[(size_t)id * K + hi];
+            const double det = P.S.det[(size_t)id * K + lo];
+            du += d_r1 * (sa * (ehy / det) + sb * (-ely / det));
+            dv += d_r1 * (sa * (-ehx / det) + sb * (elx / det));
+            const double ca = cos(th[lo]), sa_lo = sin(th[lo]);
+            const double cb = cos(th[hi]), sb_hi = sin(th[hi]);
+            ds_lo += d_r1 * (-sa * ev.a / slo);
+            ds_hi += d_r1 * (-sb * ev.b / shi);
+            const double tlx = -slo * sa_lo, tly = slo * ca, thx = -shi * sb_hi, thy = shi * cb;
+            const double na = -ev.a, nb = -ev.b;
+            da_lo += d_r1 * (sa * (na * ((ehy * tlx - ehx * tly) / det)) + sb * (na * ((-ely * tlx + elx * tly) / det)));
+            da_hi += d_r1 * (sa * (nb * ((ehy * thx - ehx * thy) / det)) + sb * (nb * ((-ely * thx + elx * thy) / det)));
+            const double hh[3] = {P.cam.o[0] + rt * dir[0] - g.mu[0], P.cam.o[1] + rt * dir[1] - g.mu[1],
+                                  P.cam.o[2] + rt * dir[2] - g.mu[2]};
+            const double drx = dir[0] * g.rx[0] + dir[1] * g.rx[1] + dir[2] * g.rx[2];
+            const double dry = dir[0] * g.ry[0] + dir[1] * g.ry[1] + dir[2] * g.ry[2];
+            const double f = -(du * drx + dv * dry) / denom;
+            for (int q = 0; q < 3; ++q) {
+              dcen[q] += du * (rz[q] * (drx / denom) - g.rx[q]) + dv * (rz[q] * (dry / denom) - g.ry[q]);
+              drot[3 * q + 0] += du * hh[q];
+              drot[3 * q + 1] += dv * hh[q];
+              drot[3 * q + 2] += f * hh[q];
+            }
+          }
+        }
+      }
+    }
+    // warp-cooperative accumulation
+    const unsigned recmask = __ballot_sync(FULL, rec);
+    if (recmask) {
+      const int lead = __ffs(recmask) - 1;
+      const int lead_id = __shfl_sync(FULL, id, lead);
+      const bool in_lead = rec && id == lead_id;
+      const bool solo = __all_sync(FULL, !rec || in_lead);
+      double* pgl = P.gact + (size_t)lead_id * P.G;
+      double* pgo = rec ? P.gact + (size_t)id * P.G : nullptr;
+      auto emit = [&](int off, float val) {
+        float s = in_lead ? val : 0.f;
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(FULL, s, m);
+        if (lane == lead && s != 0.f) atomicAdd(pgl + off, (double)s);
+        if (!solo && rec && !in_lead && val != 0.f) atomicAdd(pgo + off, (double)val);
+      };
+      const int o_sc = 12, o_an = 12 + K, o_eta = 12 + 2 * K, o_sh = o_eta + 3;
+      for (int t = 0; t < P.opt.terms_active; ++t)
+        for (int ch = 0; ch < 3; ++ch)
+          emit(o_sh + 3 * t + ch, (rec && !cl[ch]) ? (float)(wb * dC[ch]) * basis[t] : 0.f);
+      for (int q = 0; q < 3; ++q) emit(q, (float)dcen[q]);
+      for (int q = 0; q < 9; ++q) emit(3 + q, (float)drot[q]);
+      for (int k = 0; k < K; ++k) {
+        emit(o_sc + k, (float)((k == lo ? ds_lo : 0.0) + (k == hi ? ds_hi : 0.0)));
+        emit(o_an + k, (float)((k == lo ? da_lo : 0.0) + (k == hi ? da_hi : 0.0)));
+      }
+      emit(o_eta, (float)deta);
+      emit(o_eta + 1, (float)dtau);
+      emit(o_eta + 2, (float)dop);
+    }
+    if (rec) {
+      T = xm(T, xs(1.0, a));
+      cont = T >= P.opt.early_stop;
+    }
+    (void)rel;
+    return cont;
+  }
+
+  // SH colour (geometry.cpp:126-138) in fp32, before the clamp at zero.
+  __device__ __forceinline__ void sh_rgb(const RasterParams& P, int id, float& r0, float& r1, float& r2) const {
+    const float* shp = P.sh + (size_t)id * P.terms * 3;
+    r0 = 0.5f;
+    r1 = 0.5f;
+    r2 = 0.5f;
+    for (int t = 0; t < P.opt.terms_active; ++t) {
+      r0 += basis[t] * __ldg(shp + 3 * t);
+      r1 += basis[t] * __ldg(shp + 3 * t + 1);
+      r2 += basis[t] * __ldg(shp + 3 * t + 2);
+    }
+  }
+
   __device__ void finish_forward(const RasterParams& P) {
     const size_t p = (size_t)pix;
     const double c0 = C[0] + T * P.opt.bg[0];
@@ -360,7 +619,10 @@ struct Pixel {
       P.replay_cnt[p] = n_rec;
       if (n_rec > P.replay_cap) atomicAdd(&P.counters[C_REPLAY_OVERFLOW], 1ull);
     }
-    if (!F64 && P.pxflag) P.pxflag[p] = uncertain ? 1 : 0;
+    if (!F64 && P.pxflag) {
+      P.pxflag[p] = uncertain ? 1 : 0;
+      if (uncertain) P.redo_list[atomicAdd(P.redo_count, 1u)] = pix;
+    }
   }
 };
 
@@ -497,6 +759,238 @@ __global__ void __launch_bounds__(256) k_raster(RasterParams P) {
   }
 }
 
+// Backward rasterizer: re-streams the forward decisions with warp-uniform
+// control flow so that gradient components can be reduced across lanes
+// (Pixel::composite_warp).  MODE / F64 as in k_raster.
+template <int MODE, bool F64>
+__global__ void __launch_bounds__(256) k_raster_bwd(RasterParams P) {
+  __shared__ int s_id[256];
+  __shared__ double s_num[256], s_r0[256], s_r1[256], s_r2[256];
+  const unsigned FULL = 0xffffffffu;
+  const int tile = blockIdx.x;
+  const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
+  const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
+  bool active = x < P.cam.W && y < P.cam.H;
+  if (P.pxflag && active) {
+    const bool flagged = P.pxflag[(size_t)y * P.cam.W + x] != 0;
+    active = F64 ? flagged : !flagged;
+  }
+  if (__syncthreads_count(active) == 0) return;
+  Pixel<true, F64> px;
+  px.init(P, x, y);
+  px.dC[0] = px.dC[1] = px.dC[2] = px.dD = px.dN[0] = px.dN[1] = px.dN[2] = px.dA = px.rest = 0;
+  px.has_dN = P.dN != nullptr;
+  if (active) px.init_bwd(P);
+  bool done = !active;
+  double cd[kCacheCap];
+  int ci[kCacheCap];
+  int csz = 0;
+  const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
+  const double eps = P.opt.grazing_eps;
+  for (long long b0 = beg; b0 < end; b0 += 256) {
+    __syncthreads();
+    const long long j = b0 + threadIdx.x;
+    if (j < end) {
+      const int id = (int)(P.pv[j] & 0xffffffffull);
+      const Geo& g = P.geo[id];
+      s_id[threadIdx.x] = id;
+      s_num[threadIdx.x] = g.num;
+      s_r0[threadIdx.x] = g.rz[0];
+      s_r1[threadIdx.x] = g.rz[1];
+      s_r2[threadIdx.x] = g.rz[2];
+    }
+    __syncthreads();
+    const int cnt = (int)min((long long)256, end - b0);
+    if (__any_sync(FULL, !done)) {
+      for (int c = 0; c < cnt; ++c) {
+        bool want = false;
+        double prt = 0;
+        int pid = -1;
+        if (!done) {
+          const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], s_r0[c], s_r1[c], s_r2[c]);
+          if (fabs(denom) >= eps) {
+            const double rt = s_num[c] / denom;
+            if (rt > 0) {
+              const int id = s_id[c];
+              if (MODE == 1) {
+                want = true;
+                prt = rt;
+                pid = id;
+              } else {
+                int pos = 0;
+#pragma unroll
+                for (int q = 0; q < kCacheCap; ++q) pos += (q < csz && cd[q] <= rt) ? 1 : 0;
+                if (csz < kCacheCap) {
+#pragma unroll
+                  for (int q = kCacheCap - 1; q > 0; --q)
+                    if (q > pos) {
+                      cd[q] = cd[q - 1];
+                      ci[q] = ci[q - 1];
+                    }
+#pragma unroll
+                  for (int q = 0; q < kCacheCap; ++q)
+                    if (q == pos) {
+                      cd[q] = rt;
+                      ci[q] = id;
+                    }
+                  ++csz;
+                } else {
+                  want = true;
+                  if (pos == 0) {
+                    prt = rt;
+                    pid = id;
+                  } else {
+                    prt = cd[0];
+                    pid = ci[0];
+#pragma unroll
+                    for (int q = 0; q < kCacheCap; ++q) {
+                      if (q < pos - 1) {
+                        if (q + 1 < kCacheCap) {
+                          cd[q] = cd[q + 1];
+                          ci[q] = ci[q + 1];
+                        }
+                      } else if (q == pos - 1) {
+                        cd[q] = rt;
+                        ci[q] = id;
+                      }
+                    }
+                  }
+                }
+              }
+            }
+          }
+        }
+        if (__any_sync(FULL, want)) {
+          const bool cont = px.composite_warp(P, want, prt, pid);
+          if (want && !cont) done = true;
+        }
+      }
+    }
+    if (__syncthreads_count(!done) == 0) break;
+  }
+  if (MODE == 0) {
+    while (true) {
+      const bool want = !done && csz > 0;
+      if (!__any_sync(FULL, want)) break;
+      double prt = 0;
+      int pid = -1;
+      if (want) {
+        prt = cd[0];
+        pid = ci[0];
+#pragma unroll
+        for (int q = 0; q < kCacheCap - 1; ++q) {
+          cd[q] = cd[q + 1];
+          ci[q] = ci[q + 1];
+        }
+        --csz;
+      }
+      const bool cont = px.composite_warp(P, want, prt, pid);
+      if (want && !cont) done = true;
+    }
+  }
+  if (active && px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
+}
+
+// SortCache::step (raster.cpp:267-303) on a register cache; returns true and
+// the popped entry when the step pops.
+__device__ __forceinline__ bool cache_step(double (&cd)[kCacheCap], int (&ci)[kCacheCap], int& csz, double rt, int id,
+                                           double& prt, int& pid) {
+  int pos = 0;
+#pragma unroll
+  for (int q = 0; q < kCacheCap; ++q) pos += (q < csz && cd[q] <= rt) ? 1 : 0;
+  if (csz < kCacheCap) {
+#pragma unroll
+    for (int q = kCacheCap - 1; q > 0; --q)
+      if (q > pos) {
+        cd[q] = cd[q - 1];
+        ci[q] = ci[q - 1];
+      }
+#pragma unroll
+    for (int q = 0; q < kCacheCap; ++q)
+      if (q == pos) {
+        cd[q] = rt;
+        ci[q] = id;
+      }
+    ++csz;
+    return false;
+  }
+  if (pos == 0) {
+    prt = rt;
+    pid = id;
+    return true;
+  }
+  prt = cd[0];
+  pid = ci[0];
+#pragma unroll
+  for (int q = 0; q < kCacheCap; ++q) {
+    if (q < pos - 1) {
+      if (q + 1 < kCacheCap) {
+        cd[q] = cd[q + 1];
+        ci[q] = ci[q + 1];
+      }
+    } else if (q == pos - 1) {
+      cd[q] = rt;
+      ci[q] = id;
+    }
+  }
+  return true;
+}
+
+// fp64 re-render of the pixels flagged by the fp32 pass (uncertain
+// early-stop decision): one thread per listed pixel streams its tile list
+// straight from L2 with fp64 alpha (forward: outputs overwritten; backward:
+// per-record atomics).
+template <int MODE, bool BWD>
+__global__ void __launch_bounds__(128) k_raster_pixels(RasterParams P) {
+  const unsigned total = *P.redo_count;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int pix = P.redo_list[t];
+    const int x = pix % P.cam.W, y = pix / P.cam.W;
+    const int tile = (y / kTile) * P.cam.tiles_x + (x / kTile);
+    Pixel<BWD, true> px;
+    px.init(P, x, y);
+    if (BWD) px.init_bwd(P);
+    double cd[kCacheCap];
+    int ci[kCacheCap];
+    int csz = 0;
+    bool done = false;
+    const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
+    for (long long j = beg; j < end && !done; ++j) {
+      const int id = (int)(P.pv[j] & 0xffffffffull);
+      const Geo& g = P.geo[id];
+      const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.rz[0], g.rz[1], g.rz[2]);
+      if (fabs(denom) < P.opt.grazing_eps) continue;
+      const double rt = g.num / denom;
+      if (rt <= 0) continue;
+      if (MODE == 1) {
+        done = !px.composite(P, rt, id);
+        continue;
+      }
+      double prt;
+      int pid;
+      if (cache_step(cd, ci, csz, rt, id, prt, pid)) done = !px.composite(P, prt, pid);
+    }
+    if (MODE == 0) {
+      while (!done && csz > 0) {
+        const double prt = cd[0];
+        const int pid = ci[0];
+#pragma unroll
+        for (int q = 0; q < kCacheCap - 1; ++q) {
+          cd[q] = cd[q + 1];
+          ci[q] = ci[q + 1];
+        }
+        --csz;
+        done = !px.composite(P, prt, pid);
+      }
+    }
+    if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
+    if (!BWD) {
+      px.finish_forward(P);
+      atomicAdd(&P.counters[C_REDO_PIXELS], 1ull);
+    }
+  }
+}
+
 // exact_sort oracle mode (raster.cpp:395-401): every hit composited in
 // stable depth order (fp64 alpha).  One thread per pixel, selection by
 // (depth, list index).
@@ -553,18 +1047,20 @@ void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s,
   }
   // fp32 pass (all pixels; flags uncertain ones), then the fp64 pass over the
   // flagged pixels (CTAs without flagged pixels exit immediately).
+  const int redo_blocks = 148 * 2;
+  if (!bwd) cudaMemsetAsync(P.redo_count, 0, sizeof(unsigned), s);
   if (P.opt.use_cache) {
-    if (bwd) k_raster<0, true, false><<<n_tiles, 256, 0, s>>>(P);
+    if (bwd) k_raster_bwd<0, false><<<n_tiles, 256, 0, s>>>(P);
     else k_raster<0, false, false><<<n_tiles, 256, 0, s>>>(P);
     if (mid) cudaEventRecord(mid, s);
-    if (bwd) k_raster<0, true, true><<<n_tiles, 256, 0, s>>>(P);
-    else k_raster<0, false, true><<<n_tiles, 256, 0, s>>>(P);
+    if (bwd) k_raster_pixels<0, true><<<redo_blocks, 128, 0, s>>>(P);
+    else k_raster_pixels<0, false><<<redo_blocks, 128, 0, s>>>(P);
   } else {
-    if (bwd) k_raster<1, true, false><<<n_tiles, 256, 0, s>>>(P);
+    if (bwd) k_raster_bwd<1, false><<<n_tiles, 256, 0, s>>>(P);
     else k_raster<1, false, false><<<n_tiles, 256, 0, s>>>(P);
     if (mid) cudaEventRecord(mid, s);
-    if (bwd) k_raster<1, true, true><<<n_tiles, 256, 0, s>>>(P);
-    else k_raster<1, false, true><<<n_tiles, 256, 0, s>>>(P);
+    if (bwd) k_raster_pixels<1, true><<<redo_blocks, 128, 0, s>>>(P);
+    else k_raster_pixels<1, false><<<redo_blocks, 128, 0, s>>>(P);
   }
 }
 

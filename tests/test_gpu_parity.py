@@ -78,7 +78,8 @@ def test_replay_records_match(rast):
     np.testing.assert_array_equal(rb.offsets, off)
     np.testing.assert_array_equal(rb.prim_ids, ids)
     np.testing.assert_allclose(rb.vals[:, :3], vals[:, :3], rtol=0, atol=1e-12)  # u, v, depth (bit-level ops)
-    np.testing.assert_allclose(rb.vals[:, 3], vals[:, 3], rtol=1e-12, atol=1e-15)  # alpha
+    # alpha: fp32 fast path, within its validated error bound (<= 2e-6 (1 + Q) relative)
+    np.testing.assert_allclose(rb.vals[:, 3], vals[:, 3], rtol=1e-4, atol=1e-12)
     np.testing.assert_array_equal(rb.vals[:, 4], vals[:, 4])
 
 
