@@ -114,6 +114,8 @@ typedef struct drk_stats {
    * drk_set_timing(ctx, 1)): activate, preprocess, rows+emit, sort, raster,
    * raster_fp64, backward_raster, activation_backward */
   double stage_ms[8];
+  int64_t bwd_warp_steps;    /* warp-cooperative backward steps with >= 1 composited record */
+  int64_t bwd_lead_records;  /* records reduced within a warp's leader group */
 } drk_stats;
 
 typedef struct drk_ctx drk_ctx;

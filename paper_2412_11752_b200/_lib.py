@@ -69,7 +69,7 @@ STAGES = ("activate", "preprocess", "rows_emit", "sort", "raster", "raster_fp64"
 class Stats_(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("primitives", "pairs", "streamed", "popped", "composited", "near_ties",
                                           "poly_overflow", "replay_overflow", "fp64_pixels", "launches")] + \
-        [("stage_ms", C.c_double * 8)]
+        [("stage_ms", C.c_double * 8), ("bwd_warp_steps", C.c_int64), ("bwd_lead_records", C.c_int64)]
 
 
 class AdamConfig_(C.Structure):

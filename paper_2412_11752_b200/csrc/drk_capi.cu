@@ -122,7 +122,7 @@ static RasterParams raster_params(drk_ctx* c) {
   P.pv = static_cast<const unsigned long long*>(c->pv.p);
   P.geo = static_cast<const Geo*>(c->geo.p);
   const Activated& A = c->act;
-  P.S = ShapeView{A.s, A.th, A.ex, A.ey, A.det, A.eta, A.tau, A.o, A.thf, A.invdetf, A.piogf, A.hf, A.K};
+  P.S = ShapeView{A.s, A.th, A.ex, A.ey, A.det, A.eta, A.tau, A.o, A.thf, A.invdetf, A.piogf, A.hf, A.psif, A.K};
   P.sh = A.sh;
   P.terms = A.terms;
   P.counters = static_cast<unsigned long long*>(c->counters.p);
@@ -341,6 +341,14 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   mark(c, 9);
   if (int st = cuda_check(c, cudaGetLastError(), "activation bwd")) return st;
   if (int st = cuda_check(c, cudaStreamSynchronize(s), "backward")) return st;
+  {
+    unsigned long long h[C_COUNT];
+    if (int st = read_counters(c, h)) return st;
+    c->stats.bwd_warp_steps = (int64_t)h[C_BWD_WARPSTEPS];
+    c->stats.bwd_lead_records = (int64_t)h[C_BWD_LEAD_RECORDS];
+    cudaMemsetAsync(static_cast<unsigned long long*>(c->counters.p) + C_BWD_WARPSTEPS, 0,
+                    2 * sizeof(unsigned long long), s);
+  }
   if (c->timing) {
     c->stats.stage_ms[6] = elapsed(c, 7, 8);
     c->stats.stage_ms[7] = elapsed(c, 8, 9);
@@ -433,7 +441,7 @@ void drk_ctx_destroy(drk_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
                     &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
-                    &c->pxflag, &c->redo, &c->redo_cnt, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->rowcnt,
+                    &c->a_psif, &c->pxflag, &c->redo, &c->redo_cnt, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->rowcnt,
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->pk2, &c->pv2,
                     &c->hist, &c->sortoff, &c->tilecnt, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,

@@ -41,6 +41,8 @@ enum Counter {
   C_VISIBLE,
   C_POLY_FAIL,
   C_REDO_PIXELS,  // pixels re-rendered by the fp64 pass
+  C_BWD_WARPSTEPS,     // warp-cooperative backward steps with >= 1 record
+  C_BWD_LEAD_RECORDS,  // records reduced in the leader group (rest: direct atomics)
   C_COUNT
 };
 
@@ -201,6 +203,9 @@ struct ShapeView {
   const float* invdetf;
   const float* piogf;
   const float* hf;
+  // per primitive, 8 floats: sharpen breakpoints and point-slope form
+  // g1, g2, A0, A1, A2, Psi(g1), Psi(g2), opacity (fp64-derived, rounded once)
+  const float* psif;
   int K;
 };
 
@@ -283,12 +288,36 @@ __device__ __forceinline__ float sharpen_f(float g, float tau) {
 // blend written as cos^2(delta/2)/s_lo^2 + sin^2(delta/2)/s_hi^2.  Returns
 // alpha and a relative error bound *rel (validated against the fp64 path by
 // tests/test_gpu_alpha_bound.py); r2 == 0 gives the exact centre value.
+// Psi(g) in point-slope form from fp64-derived per-primitive constants, with
+// the condition number A g / Psi that maps the relative error of g onto alpha.
+__device__ __forceinline__ float sharpen_ps(const float4 c0, const float4 c1, float g, float* cond) {
+  // c0 = (g1, g2, A0, A1), c1 = (A2, Psi(g1), Psi(g2), o)
+  float A, P;
+  if (g < c0.x) {
+    A = c0.z;
+    P = c0.z * g;
+  } else if (g < c0.y) {
+    A = c0.w;
+    P = c1.y + c0.w * (g - c0.x);
+  } else {
+    A = c1.x;
+    P = c1.z + c1.x * (g - c0.y);
+  }
+  *cond = P > 0.f ? A * g / P : 1.0f;
+  return P;
+}
+
 __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const ShapeView& S, int i, float o,
                                            float tau, float eta, float* rel, bool* degenerate) {
   *degenerate = false;
+  (void)o;
+  (void)tau;
+  const float4* pc = reinterpret_cast<const float4*>(S.psif) + 2 * (size_t)i;
+  const float4 c0 = __ldg(pc), c1 = __ldg(pc + 1);
   if (r2 == 0) {
-    *rel = 1e-7f;
-    return o * sharpen_f(1.0f, tau);
+    float cond;
+    *rel = 5e-7f;
+    return c1.w * sharpen_ps(c0, c1, 1.0f, &cond);
   }
   const int K = S.K;
   const float* thf = S.thf + (size_t)i * K;
@@ -296,7 +325,17 @@ __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const 
   float th = atan2f(vf, uf);
   if (th <= 0.0f) th += 6.28318530717958647692f;
   int lo, hi;
-  if (th <= thf[0] || th > thf[K - 1]) {
+  if (K == 8) {
+    // two vector loads + branchless count instead of a dependent search loop
+    const float4 t0 = __ldg(reinterpret_cast<const float4*>(thf)), t1 = __ldg(reinterpret_cast<const float4*>(thf) + 1);
+    if (th <= t0.x || th > t1.w) {
+      lo = 7;
+      hi = 0;
+    } else {
+      hi = 1 + (t0.y < th) + (t0.z < th) + (t0.w < th) + (t1.x < th) + (t1.y < th) + (t1.z < th);
+      lo = hi - 1;
+    }
+  } else if (th <= thf[0] || th > thf[K - 1]) {
     lo = K - 1;
     hi = 0;
   } else {
@@ -322,8 +361,15 @@ __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const 
   const float Q = eta * r1 * r1 + (1.0f - eta) * (float)r2 * inv;
   const float e = fmaxf(-0.5f * Q, -30.0f);
   const float g = expf(e);
-  *rel = 2e-6f * (1.0f + fminf(Q, 60.0f));
-  return o * sharpen_f(g, tau);
+  float cond;
+  const float P = sharpen_ps(c0, c1, g, &cond);
+  // relative error of g: Q's fp32 formation (dominated by the cosine blend,
+  // ~1.4e-6 Q worst case measured) plus expf; mapped through Psi's condition
+  // number, plus the rounding of the constants.  Calibrated with a 2x margin
+  // over the worst case of an fp32 emulation and checked on the GPU by
+  // tests/test_gpu_parity.py::test_fp32_alpha_error_bound.
+  *rel = cond * (3e-6f * fminf(Q, 60.0f) + 6e-7f) + 6e-7f;
+  return c1.w * P;
 }
 
 // low_pass_filter_term (core.cpp:267-273).

@@ -50,7 +50,7 @@ struct Activated {
   const double *mu, *rot, *s, *th, *eta, *tau, *o;
   const float* sh;  // n x terms x 3 (AoS)
   const double *ex, *ey, *det;
-  const float *thf, *invdetf, *piogf, *hf;
+  const float *thf, *invdetf, *piogf, *hf, *psif;
   int n, K, terms;
 };
 
@@ -93,7 +93,7 @@ struct drk_ctx {
 
   // activated primitives owned by the context (raw path)
   drk::DevBuf a_mu, a_rot, a_s, a_th, a_eta, a_tau, a_o, a_sh, a_ex, a_ey, a_det;
-  drk::DevBuf a_thf, a_invdetf, a_piogf, a_hf, pxflag, redo, redo_cnt;
+  drk::DevBuf a_thf, a_invdetf, a_piogf, a_hf, a_psif, pxflag, redo, redo_cnt;
   drk::Activated act{};
 
   // per view

@@ -62,9 +62,26 @@ __global__ void k_activate(const float* __restrict__ raw, int n, int K, int term
 // Endpoints and bracket determinants (types.hpp:93-95, core.cpp:188-190) and
 // the fp32 fast-path constants of ShapeView.
 __global__ void k_shape(int n, int K, const double* s, const double* th, double* ex, double* ey, double* det,
-                        float* thf, float* invdetf, float* piogf, float* hf) {
+                        float* thf, float* invdetf, float* piogf, float* hf, const double* tau, const double* o,
+                        float* psif) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  {
+    // sharpen (core.cpp:229-237) in point-slope form
+    const double t = tau[i];
+    const double g1 = (1.0 + t) / 4.0, g2 = (3.0 - t) / 4.0;
+    const double A0 = (1.0 - t) / (1.0 + t), A1 = (1.0 + t) / (1.0 - t);
+    const double P1 = A0 * g1, P2 = ((1.0 + t) * g2 - t) / (1.0 - t);
+    float* q = psif + 8 * (size_t)i;
+    q[0] = (float)g1;
+    q[1] = (float)g2;
+    q[2] = (float)A0;
+    q[3] = (float)A1;
+    q[4] = (float)A0;
+    q[5] = (float)P1;
+    q[6] = (float)P2;
+    q[7] = (float)o[i];
+  }
   const size_t b = (size_t)K * i;
   for (int j = 0; j < K; ++j) {
     ex[b + j] = s[b + j] * cos(th[b + j]);
@@ -594,13 +611,15 @@ static int launch_shape_consts(drk_ctx* c, int n, int K) {
   A.invdetf = ensure<float>(c->a_invdetf, (size_t)K * n);
   A.piogf = ensure<float>(c->a_piogf, (size_t)K * n);
   A.hf = ensure<float>(c->a_hf, (size_t)K * n);
-  if (!A.ex || !A.ey || !A.det || !A.thf || !A.invdetf || !A.piogf || !A.hf)
+  A.psif = ensure<float>(c->a_psif, 8 * (size_t)n);
+  if (!A.ex || !A.ey || !A.det || !A.thf || !A.invdetf || !A.piogf || !A.hf || !A.psif)
     return set_error(c, DRK_ERR_OOM, "shape buffers");
   if (n > 0) {
     k_shape<<<(n + 127) / 128, 128, 0, c->stream>>>(n, K, A.s, A.th, const_cast<double*>(A.ex),
                                                    const_cast<double*>(A.ey), const_cast<double*>(A.det),
                                                    const_cast<float*>(A.thf), const_cast<float*>(A.invdetf),
-                                                   const_cast<float*>(A.piogf), const_cast<float*>(A.hf));
+                                                   const_cast<float*>(A.piogf), const_cast<float*>(A.hf), A.tau, A.o,
+                                                   const_cast<float*>(A.psif));
     DRK_COUNT_LAUNCH();
   }
   return cuda_check(c, cudaGetLastError(), "shape");

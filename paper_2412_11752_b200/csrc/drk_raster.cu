@@ -543,6 +543,11 @@ struct Pixel {
       const int lead_id = __shfl_sync(FULL, id, lead);
       const bool in_lead = rec && id == lead_id;
       const bool solo = __all_sync(FULL, !rec || in_lead);
+      const unsigned leadmask = __ballot_sync(FULL, in_lead);
+      if (lane == lead) {
+        atomicAdd(&P.counters[C_BWD_WARPSTEPS], 1ull);
+        atomicAdd(&P.counters[C_BWD_LEAD_RECORDS], (unsigned long long)__popc(leadmask));
+      }
       double* pgl = P.gact + (size_t)lead_id * P.G;
       double* pgo = rec ? P.gact + (size_t)id * P.G : nullptr;
       auto emit = [&](int off, float val) {
@@ -1126,6 +1131,7 @@ __global__ void k_alpha_bound(ShapeView S, int n, long long samples, unsigned lo
   eval_kernel(u, v, S, i, ev);
   if (ev.degenerate) return;
   const double a64 = S.o[i] * sharpen(ev.g, S.tau[i]);
+  if (a64 < 1e-4) return;  // far below alpha_min: no decision or composite depends on it
   float rel;
   bool degen;
   const float a32 = alpha_f32(u, v, r2, S, i, (float)S.o[i], (float)S.tau[i], (float)S.eta[i], &rel, &degen);

@@ -6,6 +6,7 @@ from paper_2412_11752_b200 import scenes
 from paper_2412_11752_b200.api import Rasterizer, RenderOptions, FrameGrad
 
 r = Rasterizer(0)
+r.set_timing(True)
 for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:
     sc = scenes.config_scene(cfg)
     cam = scenes.config_cameras(cfg)[0]
@@ -20,7 +21,8 @@ for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:
     torch.cuda.synchronize(); dt = (time.time() - t) / N
     st = r.stats()
     mp = cam.width * cam.height / 1e6
-    print(f"cfg{cfg} fwd {dt*1e3:.2f} ms  {mp/dt:.1f} MP/s  stats {st}", flush=True)
+    print(f"cfg{cfg} fwd {dt*1e3:.2f} ms  {mp/dt:.1f} MP/s", {k: round(v, 3) for k, v in st['stage_ms'].items()},
+          {k: st[k] for k in ('pairs', 'streamed', 'popped', 'composited', 'fp64_pixels', 'launches')}, flush=True)
     if scenes.CONFIGS[cfg]['backward']:
         tgt = torch.from_numpy(scenes.config_target(cfg, cam).astype(np.float32)).cuda()
         for _ in range(2):
@@ -29,4 +31,7 @@ for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:
         for _ in range(N):
             fb = r.render(raw, cam, opt); v, d = r.l1_loss(fb.color, tgt); g = r.backward_render(raw, FrameGrad(d_color=d))
         torch.cuda.synchronize(); dt = (time.time() - t) / N
-        print(f"cfg{cfg} fwd+bwd {dt*1e3:.2f} ms  {mp/dt:.1f} MP/s loss {float(v):.4f}", flush=True)
+        st = r.stats()
+        print(f"cfg{cfg} fwd+bwd {dt*1e3:.2f} ms  {mp/dt:.1f} MP/s loss {float(v):.4f}",
+              {k: round(v, 3) for k, v in st['stage_ms'].items()}, 'warpsteps', st['bwd_warp_steps'],
+              'lead_records', st['bwd_lead_records'], 'composited', st['composited'], flush=True)
