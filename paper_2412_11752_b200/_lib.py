@@ -69,7 +69,8 @@ STAGES = ("activate", "preprocess", "rows_emit", "sort", "raster", "raster_fp64"
 class Stats_(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("primitives", "pairs", "streamed", "popped", "composited", "near_ties",
                                           "poly_overflow", "replay_overflow", "fp64_pixels", "launches")] + \
-        [("stage_ms", C.c_double * 8), ("bwd_warp_steps", C.c_int64), ("bwd_lead_records", C.c_int64)]
+        [("stage_ms", C.c_double * 8), ("bwd_warp_steps", C.c_int64), ("bwd_lead_records", C.c_int64),
+         ("reject_radius", C.c_int64), ("reject_bracket", C.c_int64), ("fp64_evals", C.c_int64)]
 
 
 class AdamConfig_(C.Structure):

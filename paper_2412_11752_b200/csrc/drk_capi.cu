@@ -300,6 +300,9 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   c->stats.near_ties = (int64_t)h[C_NEAR_TIES];
   c->stats.replay_overflow = (int64_t)h[C_REPLAY_OVERFLOW];
   c->stats.fp64_pixels = (int64_t)h[C_REDO_PIXELS];
+  c->stats.reject_radius = (int64_t)h[C_REJECT_RADIUS];
+  c->stats.reject_bracket = (int64_t)h[C_REJECT_BRACKET];
+  c->stats.fp64_evals = (int64_t)h[C_FP64_EVALS];
   if (h[C_ERR_DEGEN_BASIS]) return set_error(c, DRK_ERR_DEGENERATE_BASIS, "adjacent endpoints nearly collinear");
   c->has_fwd = true;
   return DRK_OK;

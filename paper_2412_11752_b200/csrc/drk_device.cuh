@@ -43,6 +43,9 @@ enum Counter {
   C_REDO_PIXELS,  // pixels re-rendered by the fp64 pass
   C_BWD_WARPSTEPS,     // warp-cooperative backward steps with >= 1 record
   C_BWD_LEAD_RECORDS,  // records reduced in the leader group (rest: direct atomics)
+  C_REJECT_RADIUS,     // pops rejected by the isotropic support radius
+  C_REJECT_BRACKET,    // pops rejected by the in-bracket Q lower bound
+  C_FP64_EVALS,        // pops re-evaluated in fp64 (decision within the fp32 bound)
   C_COUNT
 };
 
@@ -203,8 +206,9 @@ struct ShapeView {
   const float* invdetf;
   const float* piogf;
   const float* hf;
-  // per primitive, 8 floats: sharpen breakpoints and point-slope form
-  // g1, g2, A0, A1, A2, Psi(g1), Psi(g2), opacity (fp64-derived, rounded once)
+  // per primitive, 12 floats: sharpen breakpoints and point-slope form
+  // g1, g2, A0, A1, A2, Psi(g1), Psi(g2), opacity, f_vis^2, 0, 0, 0
+  // (fp64-derived, rounded once)
   const float* psif;
   int K;
 };
@@ -307,12 +311,17 @@ __device__ __forceinline__ float sharpen_ps(const float4 c0, const float4 c1, fl
   return P;
 }
 
+// With reject_ok, returns -1 as soon as a lower bound of Q shows
+// alpha_kernel < alpha_min with margin: within the bracket, r1 and the
+// cosine blend give Q >= eta r1^2 + (1-eta) r2^2 min(1/s_lo^2, 1/s_hi^2), and
+// alpha < alpha_min <=> Q > f_vis^2 (core.cpp:305-318 with Psi monotone).
 __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const ShapeView& S, int i, float o,
-                                           float tau, float eta, float* rel, bool* degenerate) {
+                                           float tau, float eta, float* rel, bool* degenerate,
+                                           bool reject_ok = false) {
   *degenerate = false;
   (void)o;
   (void)tau;
-  const float4* pc = reinterpret_cast<const float4*>(S.psif) + 2 * (size_t)i;
+  const float4* pc = reinterpret_cast<const float4*>(S.psif) + 3 * (size_t)i;
   const float4 c0 = __ldg(pc), c1 = __ldg(pc + 1);
   if (r2 == 0) {
     float cond;
@@ -353,6 +362,11 @@ __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const 
   const float a = (float)(ehy * u - ehx * v) * invd;
   const float b = (float)(-ely * u + elx * v) * invd;
   const float r1 = fabsf(a) + fabsf(b);
+  if (reject_ok) {
+    const float fvis2 = __ldg(S.psif + 12 * (size_t)i + 8);
+    const float q_lb = eta * r1 * r1 + (1.0f - eta) * (float)r2 * fminf(S.hf[bl], S.hf[bh]);
+    if (q_lb > fvis2 * 1.00002f) return -1.0f;
+  }
   const float dth = atan2f((float)(elx * v - ely * u), (float)(elx * u + ely * v));
   const float delta = dth * S.piogf[bl];
   float sh, ch;

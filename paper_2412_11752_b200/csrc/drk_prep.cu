@@ -72,7 +72,7 @@ __global__ void k_shape(int n, int K, const double* s, const double* th, double*
     const double g1 = (1.0 + t) / 4.0, g2 = (3.0 - t) / 4.0;
     const double A0 = (1.0 - t) / (1.0 + t), A1 = (1.0 + t) / (1.0 - t);
     const double P1 = A0 * g1, P2 = ((1.0 + t) * g2 - t) / (1.0 - t);
-    float* q = psif + 8 * (size_t)i;
+    float* q = psif + 12 * (size_t)i;
     q[0] = (float)g1;
     q[1] = (float)g2;
     q[2] = (float)A0;
@@ -81,6 +81,10 @@ __global__ void k_shape(int n, int K, const double* s, const double* th, double*
     q[5] = (float)P1;
     q[6] = (float)P2;
     q[7] = (float)o[i];
+    // q[8] = f_vis^2 = -2 ln Psi^-1(alpha_min / o) (core.cpp:309-310) depends on the
+    // render options: written per view by K1 (prep_body)
+    q[8] = 0.f;
+    q[9] = q[10] = q[11] = 0.f;
   }
   const size_t b = (size_t)K * i;
   for (int j = 0; j < K; ++j) {
@@ -340,6 +344,7 @@ __device__ __forceinline__ void prep_body(Activated A, CamD cam, OptD opt, Geo* 
     double smax = 0;
     for (int j = 0; j < K; ++j) smax = dmax(smax, A.s[(size_t)K * i + j]);
     g.r2max = g.visible ? (smax * fv) * (smax * fv) * (1.0 + 1e-9) : 0.0;
+    const_cast<float*>(A.psif)[12 * (size_t)i + 8] = g.visible ? (float)(fv * fv) : __int_as_float(0x7f800000);
     g.dp2max = g.visible ? 2.0 * opt.lowpass_radius * opt.lowpass_radius * log(o / opt.alpha_min) * (1.0 + 1e-9) : 0.0;
     geo[i] = g;
     rowcnt[i] = 0;
@@ -611,7 +616,7 @@ static int launch_shape_consts(drk_ctx* c, int n, int K) {
   A.invdetf = ensure<float>(c->a_invdetf, (size_t)K * n);
   A.piogf = ensure<float>(c->a_piogf, (size_t)K * n);
   A.hf = ensure<float>(c->a_hf, (size_t)K * n);
-  A.psif = ensure<float>(c->a_psif, 8 * (size_t)n);
+  A.psif = ensure<float>(c->a_psif, 12 * (size_t)n);
   if (!A.ex || !A.ey || !A.det || !A.thf || !A.invdetf || !A.piogf || !A.hf || !A.psif)
     return set_error(c, DRK_ERR_OOM, "shape buffers");
   if (n > 0) {

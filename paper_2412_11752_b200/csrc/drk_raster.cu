@@ -40,10 +40,12 @@ struct Pixel {
   double dC[3], dD, dN[3], dA, rest;
   bool has_dN;
   long long n_pop, n_comp;
+  unsigned n_rej1, n_rej2, n_f64;
   int pix, n_rec;
   bool err;
 
   __device__ void init(const RasterParams& P, int x, int y) {
+    n_rej1 = n_rej2 = n_f64 = 0;
     px = x + 0.5;
     py = y + 0.5;
     pixel_dir(P.cam, px, py, dir);
@@ -98,7 +100,11 @@ struct Pixel {
     // (Q >= r2^2 / s_max^2), and the low-pass floor < alpha_min whenever
     // dp^2 > 2 cos^2 s_l^2 ln(o / alpha_min); both with a 1e-9 margin.
     const double r2 = xa(xm(u, u), xm(v, v));
-    if (r2 > g.r2max && (!g.has_proj || dpw * dpw + dph * dph > cos_view * cos_view * g.dp2max)) return true;
+    const bool lp_possible = g.has_proj && dpw * dpw + dph * dph <= cos_view * cos_view * g.dp2max;
+    if (r2 > g.r2max && !lp_possible) {
+      ++n_rej1;
+      return true;
+    }
     const double o = P.S.o[id], tau = P.S.tau[id];
     double a;
     bool lp = false;
@@ -110,10 +116,15 @@ struct Pixel {
     if (!F64) {
       bool degen;
       float relk;
-      const float ak = alpha_f32(u, v, r2, P.S, id, (float)o, (float)tau, (float)P.S.eta[id], &relk, &degen);
+      const float ak = alpha_f32(u, v, r2, P.S, id, (float)o, (float)tau, (float)P.S.eta[id], &relk, &degen,
+                                 !lp_possible);
       if (degen) {
         err = true;
         return false;
+      }
+      if (ak < 0.f) {  // kernel below alpha_min in its bracket, floor out of reach
+        ++n_rej2;
+        return true;
       }
       float at = ak, relt = relk;
       if (g.has_proj) {
@@ -135,6 +146,7 @@ struct Pixel {
       rel = relt;
     }
     if (use64) {
+      ++n_f64;
       eval_kernel(u, v, P.S, id, ev);
       if (ev.degenerate) {
         err = true;
@@ -361,18 +373,21 @@ struct Pixel {
         dph = xs(py, g.ppy);
       }
       const double r2 = xa(xm(u, u), xm(v, v));
-      const bool reject =
-          r2 > g.r2max && (!g.has_proj || dpw * dpw + dph * dph > cos_view * cos_view * g.dp2max);
+      const bool lp_possible = g.has_proj && dpw * dpw + dph * dph <= cos_view * cos_view * g.dp2max;
+      const bool reject = r2 > g.r2max && !lp_possible;
       if (!reject) {
         const double o = P.S.o[id], tau = P.S.tau[id];
+        bool skip = false;
         if (!F64) {
           bool degen;
           float relk;
-          const float ak = alpha_f32(u, v, r2, P.S, id, (float)o, (float)tau, (float)P.S.eta[id], &relk, &degen);
+          const float ak = alpha_f32(u, v, r2, P.S, id, (float)o, (float)tau, (float)P.S.eta[id], &relk, &degen,
+                                     !lp_possible);
           if (degen) {
             err = true;
             cont = false;
           }
+          skip = ak < 0.f;
           float at = ak, relt = relk;
           if (g.has_proj) {
             const float sl = (float)P.opt.lowpass_radius, cv = (float)cos_view;
@@ -392,7 +407,9 @@ struct Pixel {
           a = (double)at;
           rel = relt;
         }
-        if (cont && use64) {
+        if (skip) {
+          a = 0;  // alpha < alpha_min: not composited
+        } else if (cont && use64) {
           eval_kernel(u, v, P.S, id, ev);
           if (ev.degenerate) {
             err = true;
@@ -411,7 +428,7 @@ struct Pixel {
             rel = 0.f;
           }
         }
-        if (cont && a >= P.opt.alpha_min) {
+        if (cont && !skip && a >= P.opt.alpha_min) {
           a = dmin(a, 1.0 - 1e-6);
           rec = true;
           float r0, r1, r2c;
@@ -760,6 +777,9 @@ __global__ void __launch_bounds__(256) k_raster(RasterParams P) {
       atomicAdd(&P.counters[C_STREAMED], s);
       atomicAdd(&P.counters[C_POPPED], pp);
       atomicAdd(&P.counters[C_COMPOSITED], cc);
+      atomicAdd(&P.counters[C_REJECT_RADIUS], (unsigned long long)px.n_rej1);
+      atomicAdd(&P.counters[C_REJECT_BRACKET], (unsigned long long)px.n_rej2);
+      atomicAdd(&P.counters[C_FP64_EVALS], (unsigned long long)px.n_f64);
     }
   }
 }

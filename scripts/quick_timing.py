@@ -22,7 +22,7 @@ for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:
     st = r.stats()
     mp = cam.width * cam.height / 1e6
     print(f"cfg{cfg} fwd {dt*1e3:.2f} ms  {mp/dt:.1f} MP/s", {k: round(v, 3) for k, v in st['stage_ms'].items()},
-          {k: st[k] for k in ('pairs', 'streamed', 'popped', 'composited', 'fp64_pixels', 'launches')}, flush=True)
+          {k: st[k] for k in ('pairs', 'streamed', 'popped', 'composited', 'reject_radius', 'reject_bracket', 'fp64_evals', 'fp64_pixels', 'launches')}, flush=True)
     if scenes.CONFIGS[cfg]['backward']:
         tgt = torch.from_numpy(scenes.config_target(cfg, cam).astype(np.float32)).cuda()
         for _ in range(2):
