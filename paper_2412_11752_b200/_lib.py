@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdrk_b200.so")
+LIB_PATH = os.environ.get("DRK_LIB_PATH") or os.path.join(HERE, "libdrk_b200.so")
 
 
 class DrkError(RuntimeError):

@@ -26,6 +26,10 @@
 
 #include "drk_internal.h"
 
+#ifndef DRK_RASTER_MIN_BLOCKS
+#define DRK_RASTER_MIN_BLOCKS 2
+#endif
+
 namespace drk {
 
 template <bool BWD, bool F64>
@@ -105,7 +109,6 @@ struct Pixel {
       ++n_rej1;
       return true;
     }
-    const double o = P.S.o[id], tau = P.S.tau[id];
     double a;
     bool lp = false;
     float rel = 0.f;
@@ -116,8 +119,7 @@ struct Pixel {
     if (!F64) {
       bool degen;
       float relk;
-      const float ak = alpha_f32(u, v, r2, P.S, id, (float)o, (float)tau, (float)P.S.eta[id], &relk, &degen,
-                                 !lp_possible);
+      const float ak = alpha_f32(u, v, r2, P.S, id, 0.f, 0.f, (float)P.S.eta[id], &relk, &degen, !lp_possible);
       if (degen) {
         err = true;
         return false;
@@ -127,10 +129,12 @@ struct Pixel {
         return true;
       }
       float at = ak, relt = relk;
-      if (g.has_proj) {
+      // The low-pass floor only matters where it can reach alpha_min
+      // (otherwise max(alpha, floor) >= alpha_min <=> alpha >= alpha_min).
+      if (lp_possible) {
         const float sl = (float)P.opt.lowpass_radius, cv = (float)cos_view;
         const float ex = fmaxf(-((float)(dpw * dpw + dph * dph)) / (2.0f * cv * cv * sl * sl), -30.0f);
-        const float f = (float)o * expf(ex);
+        const float f = (float)P.S.o[id] * expf(ex);
         const float relf = 4e-7f * (1.0f - ex);
         if (fabsf(f - ak) <= relk * ak + relf * f) use64 = true;
         if (f > ak) {
@@ -145,8 +149,10 @@ struct Pixel {
       a = (double)at;
       rel = relt;
     }
+    const double o = P.S.o[id];
     if (use64) {
       ++n_f64;
+      const double tau = P.S.tau[id];
       eval_kernel(u, v, P.S, id, ev);
       if (ev.degenerate) {
         err = true;
@@ -204,7 +210,8 @@ struct Pixel {
     }
     T = xm(T, xs(1.0, a));
     if (!F64) {
-      E += rel * (float)(a / (1.0 - a)) + 1e-15f;
+      const float af = (float)a;
+      E += rel * __fdividef(af, 1.0f - af) + 1e-15f;
       if (fabs(T - P.opt.early_stop) <= T * (double)E) uncertain = true;
     }
     return T >= P.opt.early_stop;
@@ -389,7 +396,7 @@ struct Pixel {
           }
           skip = ak < 0.f;
           float at = ak, relt = relk;
-          if (g.has_proj) {
+          if (lp_possible) {
             const float sl = (float)P.opt.lowpass_radius, cv = (float)cos_view;
             const float ex = fmaxf(-((float)(dpw * dpw + dph * dph)) / (2.0f * cv * cv * sl * sl), -30.0f);
             const float f = (float)o * expf(ex);
@@ -597,15 +604,45 @@ struct Pixel {
   }
 
   // SH colour (geometry.cpp:126-138) in fp32, before the clamp at zero.
+  // Coefficients are AoS (terms x RGB); groups of 4 terms (12 floats) are
+  // read as 3 x float4 when the layout allows it.
   __device__ __forceinline__ void sh_rgb(const RasterParams& P, int id, float& r0, float& r1, float& r2) const {
     const float* shp = P.sh + (size_t)id * P.terms * 3;
     r0 = 0.5f;
     r1 = 0.5f;
     r2 = 0.5f;
-    for (int t = 0; t < P.opt.terms_active; ++t) {
-      r0 += basis[t] * __ldg(shp + 3 * t);
-      r1 += basis[t] * __ldg(shp + 3 * t + 1);
-      r2 += basis[t] * __ldg(shp + 3 * t + 2);
+    // Loops are fully unrolled over the 16 possible terms (guarded) so that
+    // basis[] stays in registers.
+    const int ta = P.opt.terms_active;
+    if ((P.terms & 3) == 0 && (ta & 3) == 0) {
+      const float4* q = reinterpret_cast<const float4*>(shp);
+#pragma unroll
+      for (int t = 0; t < 16; t += 4) {
+        if (t < ta) {
+          const float4 a = __ldg(q + 3 * (t / 4)), b = __ldg(q + 3 * (t / 4) + 1), c = __ldg(q + 3 * (t / 4) + 2);
+          r0 += basis[t] * a.x;
+          r1 += basis[t] * a.y;
+          r2 += basis[t] * a.z;
+          r0 += basis[t + 1] * a.w;
+          r1 += basis[t + 1] * b.x;
+          r2 += basis[t + 1] * b.y;
+          r0 += basis[t + 2] * b.z;
+          r1 += basis[t + 2] * b.w;
+          r2 += basis[t + 2] * c.x;
+          r0 += basis[t + 3] * c.y;
+          r1 += basis[t + 3] * c.z;
+          r2 += basis[t + 3] * c.w;
+        }
+      }
+      return;
+    }
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      if (t < ta) {
+        r0 += basis[t] * __ldg(shp + 3 * t);
+        r1 += basis[t] * __ldg(shp + 3 * t + 1);
+        r2 += basis[t] * __ldg(shp + 3 * t + 2);
+      }
     }
   }
 
@@ -651,7 +688,7 @@ struct Pixel {
 // MODE 0: SortCache streaming; MODE 1: list order (use_cache = false).
 // F64: re-render of the pixels flagged by the fp32 pass.
 template <int MODE, bool BWD, bool F64>
-__global__ void __launch_bounds__(256) k_raster(RasterParams P) {
+__global__ void __launch_bounds__(256, DRK_RASTER_MIN_BLOCKS) k_raster(RasterParams P) {
   __shared__ int s_id[256];
   __shared__ double s_num[256], s_r0[256], s_r1[256], s_r2[256];
   const int tile = blockIdx.x;
