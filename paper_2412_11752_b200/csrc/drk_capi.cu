@@ -332,10 +332,10 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   P.gact = gact;
   P.G = G;
   P.touched = tch;
-  (void)deterministic;  // atomics; see DESIGN.md (deterministic mode: adapter reduction)
   const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
   mark(c, 7);
-  launch_raster(P, n_tiles, true, s);
+  if (deterministic) launch_backward_serial(P, s);  // fixed accumulation order, small images
+  else launch_raster(P, n_tiles, true, s);
   mark(c, 8);
   if (int st = cuda_check(c, cudaGetLastError(), "raster bwd")) return st;
   launch_act_bwd(n, K, A.terms, raw, gact, G, tch, static_cast<const Geo*>(c->geo.p), c->camd, grad_raw,

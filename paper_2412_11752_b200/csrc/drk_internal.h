@@ -82,6 +82,7 @@ struct RasterParams {
 
 void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s, cudaEvent_t mid = nullptr);
 double measure_fp32_peak(cudaStream_t s);
+void launch_backward_serial(const RasterParams& P, cudaStream_t s);
 
 }  // namespace drk
 

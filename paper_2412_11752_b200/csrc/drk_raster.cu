@@ -1002,21 +1002,44 @@ __device__ __forceinline__ bool cache_step(double (&cd)[kCacheCap], int (&ci)[kC
 // early-stop decision): one thread per listed pixel streams its tile list
 // straight from L2 with fp64 alpha (forward: outputs overwritten; backward:
 // per-record atomics).
+// One pixel, fp64 alpha, sequential over its tile list.  MODE 0: SortCache,
+// 1: list order, 2: exact sort by (depth, list index).
 template <int MODE, bool BWD>
-__global__ void __launch_bounds__(128) k_raster_pixels(RasterParams P) {
-  const unsigned total = *P.redo_count;
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const int pix = P.redo_list[t];
-    const int x = pix % P.cam.W, y = pix / P.cam.W;
-    const int tile = (y / kTile) * P.cam.tiles_x + (x / kTile);
-    Pixel<BWD, true> px;
-    px.init(P, x, y);
-    if (BWD) px.init_bwd(P);
-    double cd[kCacheCap];
-    int ci[kCacheCap];
-    int csz = 0;
-    bool done = false;
-    const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
+__device__ void process_pixel(const RasterParams& P, int pix) {
+  const int x = pix % P.cam.W, y = pix / P.cam.W;
+  const int tile = (y / kTile) * P.cam.tiles_x + (x / kTile);
+  Pixel<BWD, true> px;
+  px.init(P, x, y);
+  if (BWD) px.init_bwd(P);
+  double cd[kCacheCap];
+  int ci[kCacheCap];
+  int csz = 0;
+  bool done = false;
+  const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
+  if (MODE == 2) {
+    double last_d = -1.0;
+    long long last_j = -1;
+    while (!done) {
+      double best_d = 0;
+      long long best_j = -1;
+      for (long long j = beg; j < end; ++j) {
+        const Geo& g = P.geo[(int)(P.pv[j] & 0xffffffffull)];
+        const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.rz[0], g.rz[1], g.rz[2]);
+        if (fabs(denom) < P.opt.grazing_eps) continue;
+        const double rt = g.num / denom;
+        if (rt <= 0) continue;
+        if (!(rt > last_d || (rt == last_d && j > last_j))) continue;
+        if (best_j < 0 || rt < best_d) {
+          best_d = rt;
+          best_j = j;
+        }
+      }
+      if (best_j < 0) break;
+      last_d = best_d;
+      last_j = best_j;
+      done = !px.composite(P, best_d, (int)(P.pv[best_j] & 0xffffffffull));
+    }
+  } else {
     for (long long j = beg; j < end && !done; ++j) {
       const int id = (int)(P.pv[j] & 0xffffffffull);
       const Geo& g = P.geo[id];
@@ -1045,12 +1068,40 @@ __global__ void __launch_bounds__(128) k_raster_pixels(RasterParams P) {
         done = !px.composite(P, prt, pid);
       }
     }
-    if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
-    if (!BWD) {
-      px.finish_forward(P);
-      atomicAdd(&P.counters[C_REDO_PIXELS], 1ull);
-    }
   }
+  if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
+  if (!BWD) px.finish_forward(P);
+}
+
+template <int MODE, bool BWD>
+__global__ void __launch_bounds__(128) k_raster_pixels(RasterParams P) {
+  const unsigned total = *P.redo_count;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    process_pixel<MODE, BWD>(P, P.redo_list[t]);
+    if (!BWD) atomicAdd(&P.counters[C_REDO_PIXELS], 1ull);
+  }
+}
+
+// Deterministic backward (drk_backward(..., deterministic = 1)): one thread
+// walks tiles in index order and pixels row-major inside each tile — the
+// reference's accumulation order (grad.cpp:327-368) — so every fp64 atomic
+// lands in a fixed order and the gradients are bitwise reproducible.
+// Meant for the small images of the drop-in test suites.
+template <int MODE>
+__global__ void k_backward_serial(RasterParams P) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int t = 0; t < P.cam.tiles_x * P.cam.tiles_y; ++t) {
+    const int tx = t % P.cam.tiles_x, ty = t / P.cam.tiles_x;
+    for (int y = ty * kTile; y < min(P.cam.H, (ty + 1) * kTile); ++y)
+      for (int x = tx * kTile; x < min(P.cam.W, (tx + 1) * kTile); ++x) process_pixel<MODE, true>(P, y * P.cam.W + x);
+  }
+}
+
+void launch_backward_serial(const RasterParams& P, cudaStream_t s) {
+  launch_counter() += 1;
+  if (P.opt.exact_sort) k_backward_serial<2><<<1, 1, 0, s>>>(P);
+  else if (P.opt.use_cache) k_backward_serial<0><<<1, 1, 0, s>>>(P);
+  else k_backward_serial<1><<<1, 1, 0, s>>>(P);
 }
 
 // exact_sort oracle mode (raster.cpp:395-401): every hit composited in
