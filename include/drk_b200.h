@@ -74,6 +74,9 @@ typedef struct drk_options {
   int32_t presort;                  /* default 2 */
   int32_t threads;                  /* ignored */
   int32_t record_replay;            /* default 0 */
+  int32_t fp64_alpha;               /* default 0; 1 = every alpha in fp64 (reference-precision mode:
+                                       identical arithmetic across cache / list / exact-sort modes) */
+  int32_t reserved_;
 } drk_options;
 
 /* Activated primitives (drk::DrkPrimitive, reference types.hpp:77-98), all
@@ -166,6 +169,12 @@ int drk_forward_host(drk_ctx* ctx, const float* raw_host, int n, int k, int sh_t
  * query sizes only. */
 int drk_get_tile_lists(drk_ctx* ctx, int64_t* total_pairs, int64_t* offsets_host,
                        int32_t* ids_host, double* keys_host);
+/* fp64 framebuffers of the last forward (the rasterizer's per-pixel fp64
+ * accumulators; colour includes the background term), host pointers, any may
+ * be NULL.  drk::FrameBuffers holds doubles; the drop-in adapter returns
+ * these. */
+int drk_get_framebuffers_f64(drk_ctx* ctx, double* color_host, double* depth_host, double* normal_host,
+                             double* alpha_host);
 /* Replay of the last forward with record_replay > 0 (drk::ReplayBuffer):
  * per-pixel offsets (H*W + 1), prim ids and 5 doubles per record
  * (u, v, depth, alpha, lowpass_active).  Host pointers; NULL to query. */

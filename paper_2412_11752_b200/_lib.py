@@ -51,7 +51,8 @@ class Options_(C.Structure):
     _fields_ = [("lowpass_radius", C.c_double), ("alpha_min", C.c_double), ("grazing_eps", C.c_double),
                 ("background", C.c_double * 3), ("early_stop_transmittance", C.c_double),
                 ("sh_degree", C.c_int32), ("use_cache", C.c_int32), ("exact_sort", C.c_int32),
-                ("presort", C.c_int32), ("threads", C.c_int32), ("record_replay", C.c_int32)]
+                ("presort", C.c_int32), ("threads", C.c_int32), ("record_replay", C.c_int32),
+                ("fp64_alpha", C.c_int32), ("reserved_", C.c_int32)]
 
 
 class Prims_(C.Structure):
@@ -103,6 +104,7 @@ SIGNATURES = {
                                    _P, _P, _P, _P]),
     "drk_get_tile_lists": (C.c_int, [_P, C.POINTER(C.c_int64), _P, _P, _P]),
     "drk_get_replay": (C.c_int, [_P, C.POINTER(C.c_int64), _P, _P, _P]),
+    "drk_get_framebuffers_f64": (C.c_int, [_P, _P, _P, _P, _P]),
     "drk_backward": (C.c_int, [_P, _P, C.POINTER(FrameGrad_), _P, _P, _P, _P, C.c_int, C.c_int]),
     "drk_get_prim_grads": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int)]),
     "drk_l1_loss": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, _P]),

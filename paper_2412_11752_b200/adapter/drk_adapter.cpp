@@ -1,0 +1,293 @@
+// Drop-in adapter: the reference's C++ API (include/drk/raster.hpp,
+// include/drk/grad.hpp) implemented on top of the C-ABI of include/drk_b200.h.
+//
+// A maintainer of the reference replaces three functions by linking this
+// translation unit:
+//   drk::bin_primitives   (reference raster.hpp:30-31, raster.cpp:119-265)
+//   drk::render           (reference raster.hpp:92-93, raster.cpp:440-485)
+//   drk::backward_render  (reference grad.hpp:58-61, grad.cpp:307-384)
+// Everything else (SortCache, eval_sorting, backward_alpha,
+// finite_diff_check, ...) stays the reference's and calls into these.
+//
+// Conversions: std::vector<DrkPrimitive> -> activated SoA on the device
+// (fp64 centre / rotation / shape, f32 SH); Image (double) <- f32 planes;
+// ReplayBuffer <- drk_get_replay; ParamGrads <- f32 SoA gradients.  Status
+// codes become the matching drk::Error subclasses.  The adapter asks the GPU
+// path for its reference-precision mode (fp64 alpha everywhere) and the
+// deterministic backward, the contract of the reference's own tests
+// (bitwise equality across cache / exact-sort modes and thread counts).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "drk/errors.hpp"
+#include "drk/grad.hpp"
+#include "drk/raster.hpp"
+#include "drk_b200.h"
+
+namespace {
+
+struct Context {
+  drk_ctx* c = nullptr;
+  Context() {
+    if (drk_ctx_create(0, &c) != DRK_OK) throw drk::Error("drk_b200: no CUDA device");
+  }
+  ~Context() { drk_ctx_destroy(c); }
+};
+
+drk_ctx* ctx() {
+  static Context g;
+  return g.c;
+}
+
+[[noreturn]] void raise(int st) {
+  const std::string m = std::string(drk_status_string(st)) + ": " + drk_last_error(ctx());
+  switch (st) {
+    case DRK_ERR_NONFINITE: throw drk::NonFiniteError(m);
+    case DRK_ERR_DEGENERATE_QUAT: throw drk::DegenerateQuaternionError(m);
+    case DRK_ERR_DEGENERATE_BASIS: throw drk::DegenerateBasisError(m);
+    case DRK_ERR_REPLAY_MISMATCH: throw drk::ReplayMismatchError(m);
+    case DRK_ERR_DIMENSION: throw drk::DimensionMismatchError(m);
+    default: throw drk::Error(m);
+  }
+}
+
+void check(int st) {
+  if (st != DRK_OK) raise(st);
+}
+
+template <class T>
+struct Dev {
+  T* p = nullptr;
+  size_t n = 0;
+  explicit Dev(size_t count) : n(count) {
+    if (cudaMalloc(&p, sizeof(T) * (count ? count : 1)) != cudaSuccess) throw drk::Error("drk_b200: cudaMalloc");
+  }
+  Dev(const std::vector<T>& h) : Dev(h.size()) {
+    if (!h.empty()) cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice);
+  }
+  ~Dev() { cudaFree(p); }
+  std::vector<T> get() const {
+    std::vector<T> h(n);
+    if (n) cudaMemcpy(h.data(), p, sizeof(T) * n, cudaMemcpyDeviceToHost);
+    return h;
+  }
+};
+
+// Activated primitives on the device (drk_prims).
+struct DevPrims {
+  int n, k, terms;
+  Dev<double> mu, rot, s, th, eta, tau, o;
+  Dev<float> sh;
+  drk_prims view;
+  static std::vector<double> field(const std::vector<drk::DrkPrimitive>& P, int per, int which) {
+    std::vector<double> v;
+    v.reserve(P.size() * per);
+    for (const auto& p : P) {
+      switch (which) {
+        case 0: for (int a = 0; a < 3; ++a) v.push_back(p.center[a]); break;
+        case 1: for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) v.push_back(p.rot(r, c)); break;
+        case 2: for (int j = 0; j < per; ++j) v.push_back(p.scales[j]); break;
+        case 3: for (int j = 0; j < per; ++j) v.push_back(p.angles[j]); break;
+        case 4: v.push_back(p.eta); break;
+        case 5: v.push_back(p.tau); break;
+        default: v.push_back(p.opacity); break;
+      }
+    }
+    return v;
+  }
+  static std::vector<float> shf(const std::vector<drk::DrkPrimitive>& P, int terms) {
+    std::vector<float> v;
+    v.reserve(P.size() * terms * 3);
+    for (const auto& p : P)
+      for (int t = 0; t < terms; ++t)
+        for (int c = 0; c < 3; ++c) v.push_back(t < p.sh.rows() ? (float)p.sh(t, c) : 0.f);
+    return v;
+  }
+  DevPrims(const std::vector<drk::DrkPrimitive>& P, int k_default)
+      : n((int)P.size()),
+        k(P.empty() ? k_default : P[0].basis_count()),
+        terms([&] {
+          int t = 0;
+          for (const auto& p : P) t = std::max<int>(t, (int)p.sh.rows());
+          return t;
+        }()),
+        mu(field(P, 3, 0)),
+        rot(field(P, 9, 1)),
+        s(field(P, k, 2)),
+        th(field(P, k, 3)),
+        eta(field(P, 1, 4)),
+        tau(field(P, 1, 5)),
+        o(field(P, 1, 6)),
+        sh(shf(P, terms)) {
+    for (const auto& p : P)
+      if (p.basis_count() != k) throw drk::DimensionMismatchError("drk_b200 adapter: mixed basis counts");
+    view = drk_prims{mu.p, rot.p, s.p, th.p, eta.p, tau.p, o.p, sh.p};
+  }
+};
+
+drk_camera to_cam(const drk::Camera& c) {
+  drk_camera d;
+  d.fx = c.fx;
+  d.fy = c.fy;
+  d.cx = c.cx;
+  d.cy = c.cy;
+  d.width = c.width;
+  d.height = c.height;
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) d.R[3 * r + k] = c.world_to_cam_rot(r, k);
+  for (int r = 0; r < 3; ++r) d.t[r] = c.world_to_cam_trans[r];
+  return d;
+}
+
+drk_options to_opt(const drk::RenderOptions& o, int replay_cap) {
+  drk_options d;
+  drk_default_options(&d);
+  d.lowpass_radius = o.kernel.lowpass_radius;
+  d.alpha_min = o.kernel.alpha_min;
+  d.grazing_eps = o.kernel.grazing_eps;
+  for (int i = 0; i < 3; ++i) d.background[i] = o.background[i];
+  d.early_stop_transmittance = o.early_stop_transmittance;
+  d.sh_degree = o.sh_degree;
+  d.use_cache = o.use_cache ? 1 : 0;
+  d.exact_sort = o.exact_sort ? 1 : 0;
+  d.presort = static_cast<int>(o.presort);
+  d.threads = o.threads;
+  d.record_replay = replay_cap;
+  d.fp64_alpha = 1;
+  return d;
+}
+
+void forward(const std::vector<drk::DrkPrimitive>& prims, const drk::Camera& cam, const drk::RenderOptions& opt,
+             int replay_cap, float* color, float* depth, float* normal, float* alpha, DevPrims& dp) {
+  const drk_camera c = to_cam(cam);
+  const drk_options o = to_opt(opt, replay_cap);
+  check(drk_forward_prims(ctx(), &dp.view, dp.n, dp.k, dp.terms, &c, &o, color, depth, normal, alpha));
+}
+
+}  // namespace
+
+namespace drk {
+
+TileBinning bin_primitives(const std::vector<DrkPrimitive>& prims, const Camera& cam, const KernelConfig& cfg,
+                           PresortMode presort) {
+  DevPrims dp(prims, cfg.basis_count);
+  RenderOptions opt;
+  opt.kernel = cfg;
+  opt.presort = presort;
+  forward(prims, cam, opt, 0, nullptr, nullptr, nullptr, nullptr, dp);
+  TileBinning b;
+  b.tiles_x = (cam.width + b.tile_size - 1) / b.tile_size;
+  b.tiles_y = (cam.height + b.tile_size - 1) / b.tile_size;
+  b.tiles.assign((size_t)b.tiles_x * b.tiles_y, {});
+  int64_t total = 0;
+  check(drk_get_tile_lists(ctx(), &total, nullptr, nullptr, nullptr));
+  std::vector<int64_t> off(b.tiles.size() + 1);
+  std::vector<int32_t> ids(total);
+  std::vector<double> keys(total);
+  check(drk_get_tile_lists(ctx(), &total, off.data(), ids.data(), keys.data()));
+  for (size_t t = 0; t < b.tiles.size(); ++t)
+    for (int64_t j = off[t]; j < off[t + 1]; ++j) b.tiles[t].push_back({ids[j], keys[j]});
+  return b;
+}
+
+FrameBuffers render(const std::vector<DrkPrimitive>& prims, const Camera& cam, const RenderOptions& opt,
+                    ReplayBuffer* replay) {
+  DevPrims dp(prims, opt.kernel.basis_count);
+  const size_t npx = (size_t)cam.width * cam.height;
+  Dev<float> color(3 * npx), depth(npx), normal(3 * npx), alpha(npx);
+  forward(prims, cam, opt, replay ? 1024 : 0, color.p, depth.p, normal.p, alpha.p, dp);
+  FrameBuffers fb;
+  fb.color = Image(cam.width, cam.height, 3);
+  fb.depth = Image(cam.width, cam.height, 1);
+  fb.normal = Image(cam.width, cam.height, 3);
+  fb.alpha = Image(cam.width, cam.height, 1);
+  // the rasterizer's fp64 accumulators (the f32 planes above are their rounding)
+  check(drk_get_framebuffers_f64(ctx(), fb.color.data.data(), fb.depth.data.data(), fb.normal.data.data(),
+                                 fb.alpha.data.data()));
+  fb.background = opt.background;
+  if (replay) {
+    replay->width = cam.width;
+    replay->height = cam.height;
+    replay->pixels.assign(npx, {});
+    int64_t total = 0;
+    check(drk_get_replay(ctx(), &total, nullptr, nullptr, nullptr));
+    std::vector<int64_t> off(npx + 1);
+    std::vector<int32_t> ids(total);
+    std::vector<double> vals(5 * total);
+    check(drk_get_replay(ctx(), &total, off.data(), ids.data(), vals.data()));
+    for (size_t p = 0; p < npx; ++p)
+      for (int64_t j = off[p]; j < off[p + 1]; ++j) {
+        BlendRecord r;
+        r.prim_id = ids[j];
+        r.u = vals[5 * j];
+        r.v = vals[5 * j + 1];
+        r.depth = vals[5 * j + 2];
+        r.alpha = vals[5 * j + 3];
+        r.lowpass_active = vals[5 * j + 4] != 0.0;
+        replay->pixels[p].push_back(r);
+      }
+  }
+  return fb;
+}
+
+ParamGrads backward_render(const std::vector<RawDrkParams>& raws, const std::vector<DrkPrimitive>& prims,
+                           const Camera& cam, const RenderOptions& opt, const ReplayBuffer& replay,
+                           const FrameGrad& frame_grad) {
+  if (replay.width != cam.width || replay.height != cam.height)
+    throw ReplayMismatchError("replay buffer does not match the camera dimensions");
+  if (raws.size() != prims.size()) throw ReplayMismatchError("raw and activated primitive counts differ");
+  DevPrims dp(prims, opt.kernel.basis_count);
+  // the device keeps the decisions of this forward in place of the ReplayBuffer
+  forward(prims, cam, opt, 0, nullptr, nullptr, nullptr, nullptr, dp);
+  const int n = dp.n, k = dp.k, terms = dp.terms;
+  const int S = drk_scalar_count(k, terms);
+  std::vector<float> raw_soa((size_t)S * n, 0.f);
+  for (int i = 0; i < n; ++i) {
+    int s = 0;
+    for_each_scalar(raws[i], [&](const double& x, ParamClass) {
+      if (s < S) raw_soa[(size_t)s * n + i] = (float)x;
+      ++s;
+    });
+  }
+  Dev<float> raw_d(raw_soa);
+  auto img = [&](const Image& im, int ch) -> std::vector<float> {
+    if (im.empty()) return {};
+    if (im.width != cam.width || im.height != cam.height || im.channels != ch)
+      throw DimensionMismatchError("frame gradient shape");
+    return std::vector<float>(im.data.begin(), im.data.end());
+  };
+  const std::vector<float> hc = img(frame_grad.d_color, 3), hd = img(frame_grad.d_depth, 1),
+                           hn = img(frame_grad.d_normal, 3), ha = img(frame_grad.d_alpha, 1);
+  Dev<float> dc(hc), dd(hd), dn(hn), da(ha);
+  drk_frame_grad fg{hc.empty() ? nullptr : dc.p, hd.empty() ? nullptr : dd.p, hn.empty() ? nullptr : dn.p,
+                    ha.empty() ? nullptr : da.p};
+  Dev<float> g((size_t)S * n), dcw(3 * (size_t)n), sg(n);
+  Dev<uint8_t> tch(n);
+  check(drk_backward(ctx(), raw_d.p, &fg, g.p, dcw.p, sg.p, tch.p, 0, /*deterministic=*/1));
+  const std::vector<float> gh = g.get(), dcwh = dcw.get(), sgh = sg.get();
+  const std::vector<uint8_t> th = tch.get();
+  ParamGrads out;
+  out.raw.resize(n);
+  out.d_center_world.resize(n);
+  out.screen_grad.assign(n, 0.0);
+  out.touched.assign(n, 0);
+  for (int i = 0; i < n; ++i) {
+    RawDrkParams r = RawDrkParams::zeros_like(raws[i]);
+    int s = 0;
+    for_each_scalar(r, [&](double& x, ParamClass) {
+      if (s < S) x = gh[(size_t)s * n + i];
+      ++s;
+    });
+    out.raw[i] = r;
+    out.d_center_world[i] = Vec3(dcwh[3 * i], dcwh[3 * i + 1], dcwh[3 * i + 2]);
+    out.screen_grad[i] = sgh[i];
+    out.touched[i] = (char)th[i];
+  }
+  return out;
+}
+
+}  // namespace drk

@@ -108,6 +108,7 @@ static OptD make_opt(const drk_options* o, int terms) {
   d.exact_sort = o->exact_sort;
   d.presort = o->presort;
   d.record_replay = o->record_replay;
+  d.fp64_alpha = o->fp64_alpha;
   const int t = (o->sh_degree + 1) * (o->sh_degree + 1);
   d.terms_active = t < terms ? t : terms;
   return d;
@@ -386,6 +387,8 @@ void drk_default_options(drk_options* o) {
   o->presort = 2;
   o->threads = 1;
   o->record_replay = 0;
+  o->fp64_alpha = 0;
+  o->reserved_ = 0;
 }
 
 const char* drk_status_string(int s) {
@@ -551,6 +554,25 @@ int drk_get_tile_lists(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* id
   if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "tile lists")) return st;
   for (int64_t i = 0; ids && i < c->n_pairs; ++i) ids[i] = (int32_t)(v[i] & 0xffffffffull);
   for (int64_t i = 0; keys && i < c->n_pairs; ++i) std::memcpy(&keys[i], &k[i], sizeof(double));
+  return DRK_OK;
+}
+
+int drk_get_framebuffers_f64(drk_ctx* c, double* color, double* depth, double* normal, double* alpha) {
+  if (!c || !c->has_fwd) return c ? set_error(c, DRK_ERR_INVALID_ARG, "no forward on this context") : DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  const size_t npix = (size_t)c->cam.width * c->cam.height;
+  std::vector<double> st(8 * npix);
+  cudaMemcpyAsync(st.data(), c->pxstate.p, sizeof(double) * st.size(), cudaMemcpyDeviceToHost, c->stream);
+  if (int s = cuda_check(c, cudaStreamSynchronize(c->stream), "framebuffers")) return s;
+  for (size_t p = 0; p < npix; ++p) {
+    const double* q = st.data() + 8 * p;
+    if (color)
+      for (int k = 0; k < 3; ++k) color[3 * p + k] = q[k];
+    if (depth) depth[p] = q[3];
+    if (normal)
+      for (int k = 0; k < 3; ++k) normal[3 * p + k] = q[4 + k];
+    if (alpha) alpha[p] = q[7];
+  }
   return DRK_OK;
 }
 

@@ -63,7 +63,7 @@ struct OptD {
   double bg[3];
   double early_stop;
   double lp_pad;  // raster.cpp:128-129
-  int sh_degree, use_cache, exact_sort, presort, record_replay, terms_active;
+  int sh_degree, use_cache, exact_sort, presort, record_replay, terms_active, fp64_alpha;
 };
 
 __host__ __device__ inline double dmin(double a, double b) { return (b < a) ? b : a; }  // std::min

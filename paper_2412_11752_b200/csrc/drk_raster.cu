@@ -1147,6 +1147,12 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
   if (!BWD) px.finish_forward(P);
 }
 
+__global__ void k_fill_pixels(int* list, unsigned* count, unsigned n) {
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) list[i] = (int)i;
+  if (i == 0) *count = n;
+}
+
 void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s, cudaEvent_t mid) {
   if (n_tiles == 0) return;
   launch_counter() += P.opt.exact_sort ? 1 : 2;
@@ -1161,6 +1167,21 @@ void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s,
   // fp32 pass (all pixels; flags uncertain ones), then the fp64 pass over the
   // flagged pixels (CTAs without flagged pixels exit immediately).
   const int redo_blocks = 148 * 2;
+  if (P.opt.fp64_alpha) {
+    // reference-precision mode: every pixel through the fp64 per-pixel path
+    const unsigned npx = (unsigned)P.cam.W * P.cam.H;
+    if (!bwd) k_fill_pixels<<<(npx + 255) / 256, 256, 0, s>>>(P.redo_list, P.redo_count, npx);
+    const int blocks = (int)std::min<unsigned>((npx + 127) / 128, 148 * 8);
+    if (P.opt.use_cache) {
+      if (bwd) k_raster_pixels<0, true><<<blocks, 128, 0, s>>>(P);
+      else k_raster_pixels<0, false><<<blocks, 128, 0, s>>>(P);
+    } else {
+      if (bwd) k_raster_pixels<1, true><<<blocks, 128, 0, s>>>(P);
+      else k_raster_pixels<1, false><<<blocks, 128, 0, s>>>(P);
+    }
+    if (mid) cudaEventRecord(mid, s);
+    return;
+  }
   if (!bwd) cudaMemsetAsync(P.redo_count, 0, sizeof(unsigned), s);
   if (P.opt.use_cache) {
     if (bwd) k_raster_bwd<0, false><<<n_tiles, 256, 0, s>>>(P);
