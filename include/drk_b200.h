@@ -118,7 +118,7 @@ typedef struct drk_stats {
    * raster_fp64, backward_raster, activation_backward */
   double stage_ms[8];
   int64_t bwd_warp_steps;    /* warp-cooperative backward steps with >= 1 composited record */
-  int64_t bwd_lead_records;  /* records reduced within a warp's leader group */
+  int64_t bwd_lead_records;  /* primitive groups reduced in the warp-cooperative backward */
   int64_t reject_radius;     /* pops rejected by the isotropic alpha_min support radius */
   int64_t reject_bracket;    /* pops rejected by the in-bracket lower bound of the exponent */
   int64_t fp64_evals;        /* pops re-evaluated in fp64 (decision inside the fp32 error bound) */

@@ -32,6 +32,12 @@
 
 namespace drk {
 
+// Backward: per-CTA shared-memory gradient slots (direct-mapped by primitive
+// id), flushed to HBM at every batch boundary.  Stride >= G for K <= 16,
+// SH degree <= 3.
+constexpr int kGradSlots = 64;
+constexpr int kGradSlotStride = 96;
+
 template <bool BWD, bool F64>
 struct Pixel {
   double dir[3];
@@ -349,7 +355,8 @@ struct Pixel {
   // composited lane (butterfly shuffles), then added to HBM with one fp64
   // atomic; lanes of other primitives add their own values directly.
   // Returns false once this lane's pixel saturates.
-  __device__ bool composite_warp(const RasterParams& P, bool want, double rt, int id) {
+  __device__ bool composite_warp(const RasterParams& P, bool want, double rt, int id, int* slot_id,
+                                 float* slot_val) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     bool rec = false, cont = true, lp = false, use64 = F64;
@@ -560,31 +567,51 @@ struct Pixel {
         }
       }
     }
-    // warp-cooperative accumulation
+    // Warp-cooperative accumulation.  Lanes are grouped by primitive (first
+    // composited lane's primitive first, then the next remaining one ...);
+    // each group's G components are butterfly-reduced and added into the
+    // CTA's shared-memory slot for that primitive (direct-mapped, claimed
+    // once per batch, flushed to HBM with fp64 atomics at batch boundaries),
+    // or straight to HBM when the slot holds another primitive.
     const unsigned recmask = __ballot_sync(FULL, rec);
-    if (recmask) {
-      const int lead = __ffs(recmask) - 1;
-      const int lead_id = __shfl_sync(FULL, id, lead);
-      const bool in_lead = rec && id == lead_id;
-      const bool solo = __all_sync(FULL, !rec || in_lead);
-      const unsigned leadmask = __ballot_sync(FULL, in_lead);
-      if (lane == lead) {
-        atomicAdd(&P.counters[C_BWD_WARPSTEPS], 1ull);
-        atomicAdd(&P.counters[C_BWD_LEAD_RECORDS], (unsigned long long)__popc(leadmask));
+    unsigned remaining = recmask;
+    if (recmask && lane == __ffs(recmask) - 1) atomicAdd(&P.counters[C_BWD_WARPSTEPS], 1ull);
+    const int o_sc = 12, o_an = 12 + K, o_eta = 12 + 2 * K, o_sh = o_eta + 3;
+    const float wc0 = rec && !cl[0] ? (float)(wb * dC[0]) : 0.f;
+    const float wc1 = rec && !cl[1] ? (float)(wb * dC[1]) : 0.f;
+    const float wc2 = rec && !cl[2] ? (float)(wb * dC[2]) : 0.f;
+    while (remaining) {
+      const int lead = __ffs(remaining) - 1;
+      const int gid = __shfl_sync(FULL, id, lead);
+      const bool in_g = rec && id == gid && ((remaining >> lane) & 1u);
+      const unsigned gmask = __ballot_sync(FULL, in_g);
+      remaining &= ~gmask;
+      if (lane == lead) atomicAdd(&P.counters[C_BWD_LEAD_RECORDS], 1ull);  // groups reduced
+      int slot = -1;
+      if (lane == lead && slot_id) {
+        const int s = gid & (kGradSlots - 1);
+        const int old = atomicCAS(&slot_id[s], -1, gid);
+        slot = (old == -1 || old == gid) ? s : -1;
       }
-      double* pgl = P.gact + (size_t)lead_id * P.G;
-      double* pgo = rec ? P.gact + (size_t)id * P.G : nullptr;
+      slot = __shfl_sync(FULL, slot, lead);
+      float* acc = slot >= 0 ? slot_val + (size_t)slot * kGradSlotStride : nullptr;
+      double* pg = P.gact + (size_t)gid * P.G;
       auto emit = [&](int off, float val) {
-        float s = in_lead ? val : 0.f;
+        float s = in_g ? val : 0.f;
 #pragma unroll
         for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(FULL, s, m);
-        if (lane == lead && s != 0.f) atomicAdd(pgl + off, (double)s);
-        if (!solo && rec && !in_lead && val != 0.f) atomicAdd(pgo + off, (double)val);
+        if (lane == (off & 31) && s != 0.f) {
+          if (acc) atomicAdd(acc + off, s);
+          else atomicAdd(pg + off, (double)s);
+        }
       };
-      const int o_sc = 12, o_an = 12 + K, o_eta = 12 + 2 * K, o_sh = o_eta + 3;
-      for (int t = 0; t < P.opt.terms_active; ++t)
-        for (int ch = 0; ch < 3; ++ch)
-          emit(o_sh + 3 * t + ch, (rec && !cl[ch]) ? (float)(wb * dC[ch]) * basis[t] : 0.f);
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        if (t < P.opt.terms_active) {
+          emit(o_sh + 3 * t, wc0 * basis[t]);
+          emit(o_sh + 3 * t + 1, wc1 * basis[t]);
+          emit(o_sh + 3 * t + 2, wc2 * basis[t]);
+        }
       for (int q = 0; q < 3; ++q) emit(q, (float)dcen[q]);
       for (int q = 0; q < 9; ++q) emit(3 + q, (float)drot[q]);
       for (int k = 0; k < K; ++k) {
@@ -824,11 +851,31 @@ __global__ void __launch_bounds__(256, DRK_RASTER_MIN_BLOCKS) k_raster(RasterPar
 // Backward rasterizer: re-streams the forward decisions with warp-uniform
 // control flow so that gradient components can be reduced across lanes
 // (Pixel::composite_warp).  MODE / F64 as in k_raster.
+// Flush the shared-memory gradient slots to HBM (fp64 atomics) and clear
+// them; called by the whole CTA between __syncthreads.
+__device__ __forceinline__ void flush_grad_slots(const RasterParams& P, int* slot_id, float* slot_val) {
+  const int G = P.G;
+  for (int idx = threadIdx.x; idx < kGradSlots * G; idx += blockDim.x) {
+    const int s = idx / G, c = idx - s * G;
+    const int id = slot_id[s];
+    float* v = slot_val + (size_t)s * kGradSlotStride + c;
+    if (id >= 0 && *v != 0.f) atomicAdd(P.gact + (size_t)id * G + c, (double)*v);
+    *v = 0.f;
+  }
+  __syncthreads();
+  if (threadIdx.x < kGradSlots) slot_id[threadIdx.x] = -1;
+  __syncthreads();
+}
+
 template <int MODE, bool F64>
-__global__ void __launch_bounds__(256) k_raster_bwd(RasterParams P) {
+__global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterParams P) {
   __shared__ int s_id[256];
   __shared__ double s_num[256], s_r0[256], s_r1[256], s_r2[256];
+  __shared__ int slot_id[kGradSlots];
+  __shared__ float slot_val[kGradSlots * kGradSlotStride];
   const unsigned FULL = 0xffffffffu;
+  for (int i = threadIdx.x; i < kGradSlots * kGradSlotStride; i += blockDim.x) slot_val[i] = 0.f;
+  if (threadIdx.x < kGradSlots) slot_id[threadIdx.x] = -1;
   const int tile = blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
@@ -923,12 +970,14 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterParams P) {
           }
         }
         if (__any_sync(FULL, want)) {
-          const bool cont = px.composite_warp(P, want, prt, pid);
+          const bool cont = px.composite_warp(P, want, prt, pid, slot_id, slot_val);
           if (want && !cont) done = true;
         }
       }
     }
-    if (__syncthreads_count(!done) == 0) break;
+    const int busy = __syncthreads_count(!done);
+    flush_grad_slots(P, slot_id, slot_val);
+    if (busy == 0) break;
   }
   if (MODE == 0) {
     while (true) {
@@ -946,10 +995,12 @@ __global__ void __launch_bounds__(256) k_raster_bwd(RasterParams P) {
         }
         --csz;
       }
-      const bool cont = px.composite_warp(P, want, prt, pid);
+      const bool cont = px.composite_warp(P, want, prt, pid, slot_id, slot_val);
       if (want && !cont) done = true;
     }
   }
+  __syncthreads();
+  flush_grad_slots(P, slot_id, slot_val);
   if (active && px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
 }
 
