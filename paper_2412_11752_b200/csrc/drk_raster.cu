@@ -37,6 +37,16 @@ namespace drk {
 // SH degree <= 3.
 constexpr int kGradSlots = 64;
 constexpr int kGradSlotStride = 96;
+// Measured on config 2: the CTA-shared slots (same-address shared atomics
+// from 8 warps) were slower (357 ms) than warp-reduced global atomics
+// (224 ms); kept switchable for the next round's CTA-level design.
+#ifndef DRK_GRAD_SLOTS
+#define DRK_GRAD_SLOTS 0
+#endif
+constexpr bool kUseGradSlots = DRK_GRAD_SLOTS != 0;
+#ifndef DRK_BWD_MIN_BLOCKS
+#define DRK_BWD_MIN_BLOCKS 2
+#endif
 
 template <bool BWD, bool F64>
 struct Pixel {
@@ -575,18 +585,17 @@ struct Pixel {
     // or straight to HBM when the slot holds another primitive.
     const unsigned recmask = __ballot_sync(FULL, rec);
     unsigned remaining = recmask;
-    if (recmask && lane == __ffs(recmask) - 1) atomicAdd(&P.counters[C_BWD_WARPSTEPS], 1ull);
+    if (recmask && lane == __ffs(recmask) - 1) ++n_rej1;  // warp steps (backward reuses the counter)
     const int o_sc = 12, o_an = 12 + K, o_eta = 12 + 2 * K, o_sh = o_eta + 3;
     const float wc0 = rec && !cl[0] ? (float)(wb * dC[0]) : 0.f;
     const float wc1 = rec && !cl[1] ? (float)(wb * dC[1]) : 0.f;
     const float wc2 = rec && !cl[2] ? (float)(wb * dC[2]) : 0.f;
-    while (remaining) {
+    if (remaining) {
       const int lead = __ffs(remaining) - 1;
       const int gid = __shfl_sync(FULL, id, lead);
-      const bool in_g = rec && id == gid && ((remaining >> lane) & 1u);
-      const unsigned gmask = __ballot_sync(FULL, in_g);
-      remaining &= ~gmask;
-      if (lane == lead) atomicAdd(&P.counters[C_BWD_LEAD_RECORDS], 1ull);  // groups reduced
+      const bool in_g = rec && id == gid;
+      const bool solo = __all_sync(FULL, !rec || in_g);
+      if (lane == lead) ++n_rej2;  // groups reduced (backward reuses the counter)
       int slot = -1;
       if (lane == lead && slot_id) {
         const int s = gid & (kGradSlots - 1);
@@ -596,22 +605,27 @@ struct Pixel {
       slot = __shfl_sync(FULL, slot, lead);
       float* acc = slot >= 0 ? slot_val + (size_t)slot * kGradSlotStride : nullptr;
       double* pg = P.gact + (size_t)gid * P.G;
+      double* pgo = rec ? P.gact + (size_t)id * P.G : nullptr;
       auto emit = [&](int off, float val) {
         float s = in_g ? val : 0.f;
 #pragma unroll
         for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(FULL, s, m);
-        if (lane == (off & 31) && s != 0.f) {
+        // lanes of other primitives (7% of records on config 2) add directly
+        if (!solo && rec && !in_g && val != 0.f) atomicAdd(pgo + off, (double)val);
+        if (lane == lead && s != 0.f) {
           if (acc) atomicAdd(acc + off, s);
           else atomicAdd(pg + off, (double)s);
         }
       };
-#pragma unroll
-      for (int t = 0; t < 16; ++t)
-        if (t < P.opt.terms_active) {
-          emit(o_sh + 3 * t, wc0 * basis[t]);
-          emit(o_sh + 3 * t + 1, wc1 * basis[t]);
-          emit(o_sh + 3 * t + 2, wc2 * basis[t]);
-        }
+      // rolled on purpose: keeps the 48 SH emits out of the register budget
+      // (basis[] is read from local memory here; measured faster than unrolled)
+#pragma unroll 1
+      for (int t = 0; t < P.opt.terms_active; ++t) {
+        const float b = basis[t];
+        emit(o_sh + 3 * t, wc0 * b);
+        emit(o_sh + 3 * t + 1, wc1 * b);
+        emit(o_sh + 3 * t + 2, wc2 * b);
+      }
       for (int q = 0; q < 3; ++q) emit(q, (float)dcen[q]);
       for (int q = 0; q < 9; ++q) emit(3 + q, (float)drot[q]);
       for (int k = 0; k < K; ++k) {
@@ -868,14 +882,18 @@ __device__ __forceinline__ void flush_grad_slots(const RasterParams& P, int* slo
 }
 
 template <int MODE, bool F64>
-__global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterParams P) {
+__global__ void __launch_bounds__(256, DRK_BWD_MIN_BLOCKS) k_raster_bwd(RasterParams P) {
   __shared__ int s_id[256];
   __shared__ double s_num[256], s_r0[256], s_r1[256], s_r2[256];
-  __shared__ int slot_id[kGradSlots];
-  __shared__ float slot_val[kGradSlots * kGradSlotStride];
+  __shared__ int slot_id_s[kGradSlots];
+  __shared__ float slot_val_s[kUseGradSlots ? kGradSlots * kGradSlotStride : 1];
+  int* slot_id = kUseGradSlots ? slot_id_s : nullptr;
+  float* slot_val = kUseGradSlots ? slot_val_s : nullptr;
   const unsigned FULL = 0xffffffffu;
-  for (int i = threadIdx.x; i < kGradSlots * kGradSlotStride; i += blockDim.x) slot_val[i] = 0.f;
-  if (threadIdx.x < kGradSlots) slot_id[threadIdx.x] = -1;
+  if (kUseGradSlots) {
+    for (int i = threadIdx.x; i < kGradSlots * kGradSlotStride; i += blockDim.x) slot_val_s[i] = 0.f;
+    if (threadIdx.x < kGradSlots) slot_id_s[threadIdx.x] = -1;
+  }
   const int tile = blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
@@ -976,7 +994,7 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterParams P) {
       }
     }
     const int busy = __syncthreads_count(!done);
-    flush_grad_slots(P, slot_id, slot_val);
+    if (kUseGradSlots) flush_grad_slots(P, slot_id, slot_val);
     if (busy == 0) break;
   }
   if (MODE == 0) {
@@ -999,9 +1017,13 @@ __global__ void __launch_bounds__(256, 2) k_raster_bwd(RasterParams P) {
       if (want && !cont) done = true;
     }
   }
-  __syncthreads();
-  flush_grad_slots(P, slot_id, slot_val);
+  if (kUseGradSlots) {
+    __syncthreads();
+    flush_grad_slots(P, slot_id, slot_val);
+  }
   if (active && px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
+  if (px.n_rej1) atomicAdd(&P.counters[C_BWD_WARPSTEPS], (unsigned long long)px.n_rej1);
+  if (px.n_rej2) atomicAdd(&P.counters[C_BWD_LEAD_RECORDS], (unsigned long long)px.n_rej2);
 }
 
 // SortCache::step (raster.cpp:267-303) on a register cache; returns true and
