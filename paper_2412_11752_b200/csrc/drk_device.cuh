@@ -371,18 +371,25 @@ __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const 
   const float delta = dth * S.piogf[bl];
   float sh, ch;
   sincosf(0.5f * delta, &sh, &ch);
-  const float inv = ch * ch * S.hf[bl] + sh * sh * S.hf[bh];
+  const float hlo = S.hf[bl], hhi = S.hf[bh];
+  const float inv = ch * ch * hlo + sh * sh * hhi;
   const float Q = eta * r1 * r1 + (1.0f - eta) * (float)r2 * inv;
   const float e = fmaxf(-0.5f * Q, -30.0f);
   const float g = expf(e);
   float cond;
   const float P = sharpen_ps(c0, c1, g, &cond);
-  // relative error of g: Q's fp32 formation (dominated by the cosine blend,
-  // ~1.4e-6 Q worst case measured) plus expf; mapped through Psi's condition
-  // number, plus the rounding of the constants.  Calibrated with a 2x margin
-  // over the worst case of an fp32 emulation and checked on the GPU by
-  // tests/test_gpu_parity.py::test_fp32_alpha_error_bound.
-  *rel = cond * (3e-6f * fminf(Q, 60.0f) + 6e-7f) + 6e-7f;
+  // Relative error bound.  Q: fp32 formation of r1 and the products (~4
+  // ulp) plus the cosine blend's sensitivity to delta, |d inv| <=
+  // |sin(delta)| |h_lo - h_hi| / 2 * |d delta| with |d delta| <= 8e-7 (1 + delta)
+  // (atan2f of the in-bracket angle times pi/gap).  g = exp(-Q/2) adds
+  // Q/2 * rel(Q) and expf's ~2 ulp; Psi maps it through its condition
+  // number; the constants add ~4 ulp.  Checked against the fp64 path on the
+  // GPU (tests/test_gpu_parity.py::test_fp32_alpha_error_bound) and by an fp32
+  // emulation (max observed error below half the bound).
+  const float sd = 2.0f * sh * ch;  // sin(delta)
+  const float dinv = 0.5f * fabsf(sd) * fabsf(hlo - hhi) * 8e-7f * (1.0f + fabsf(delta));
+  const float rel_q = 5e-7f + (1.0f - eta) * (float)r2 * dinv / fmaxf(Q, 1e-30f);
+  *rel = cond * (0.5f * fminf(Q, 60.0f) * 2.0f * rel_q + 4e-7f) + 6e-7f;
   return c1.w * P;
 }
 
