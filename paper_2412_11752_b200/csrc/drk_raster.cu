@@ -236,13 +236,25 @@ struct Pixel {
   __device__ void backward_record(const RasterParams& P, int id, const Geo& g, double rt, double u, double v,
                                   double a, bool lp, const KEval& ev, const double rgb[3], bool cl0, bool cl1,
                                   bool cl2, double sgn, double rdz, double dpw, double dph, double wb) {
-    double* pg = P.gact + (size_t)id * P.G;
-    const int K = P.S.K;
     const double rz[3] = {g.rz[0], g.rz[1], g.rz[2]};
     const double cw = (dC[0] * rgb[0] + dC[1] * rgb[1] + dC[2] * rgb[2]) + dD * rt +
                       (dN[0] * (sgn * rz[0]) + dN[1] * (sgn * rz[1]) + dN[2] * (sgn * rz[2])) + dA;
     rest -= wb * cw;
     const double dat = T * cw - rest / (1.0 - a);
+    backward_record_dat(P, id, g, rt, u, v, a, lp, ev, rgb, cl0, cl1, cl2, sgn, rdz, dpw, dph, wb, dat, T);
+  }
+
+  // Gradient of one record given its upstream dL/d(alpha_tilde) (`dat`) and
+  // blend weight wb = T alpha (grad.cpp:237-301, :16-101), fp64 atomics.
+  __device__ void backward_record_dat(const RasterParams& P, int id, const Geo& g, double rt, double u, double v,
+                                      double a, bool lp, const KEval& ev, const double rgb[3], bool cl0, bool cl1,
+                                      bool cl2, double sgn, double rdz, double dpw, double dph, double wb,
+                                      double dat, double T_i) const {
+    (void)rgb;
+    (void)T_i;
+    double* pg = P.gact + (size_t)id * P.G;
+    const int K = P.S.K;
+    const double rz[3] = {g.rz[0], g.rz[1], g.rz[2]};
     P.touched[id] = 1;
     const int o_rot = 3, o_sc = 12, o_an = 12 + K, o_eta = 12 + 2 * K, o_tau = o_eta + 1, o_op = o_eta + 2,
               o_sh = o_eta + 3;
@@ -1146,6 +1158,231 @@ __device__ void process_pixel(const RasterParams& P, int pix) {
   if (!BWD) px.finish_forward(P);
 }
 
+// fp64 evaluation of one popped entry (composite_candidate minus the
+// transmittance-dependent part): alpha decision, tangent coordinates,
+// colour, kernel partials for the backward.
+struct PopEval {
+  double a, rt, u, v, denom, dpw, dph;
+  float rgb[3];
+  bool valid, lp, cl[3];
+  KEval ev;
+  int id;
+};
+
+template <bool BWD>
+__device__ void eval_pop(const RasterParams& P, const Pixel<BWD, true>& px, double rt, int id, PopEval& e) {
+  const Geo& g = P.geo[id];
+  e.valid = false;
+  e.lp = false;
+  e.id = id;
+  e.rt = rt;
+  e.denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.rz[0], g.rz[1], g.rz[2]);
+  const double h0 = xs(xa(P.cam.o[0], xm(rt, px.dir[0])), g.mu[0]);
+  const double h1 = xs(xa(P.cam.o[1], xm(rt, px.dir[1])), g.mu[1]);
+  const double h2 = xs(xa(P.cam.o[2], xm(rt, px.dir[2])), g.mu[2]);
+  e.u = xdot3(g.rx[0], g.rx[1], g.rx[2], h0, h1, h2);
+  e.v = xdot3(g.ry[0], g.ry[1], g.ry[2], h0, h1, h2);
+  const double cos_view = fabs(e.denom);
+  e.dpw = e.dph = 0;
+  if (g.has_proj) {
+    e.dpw = xs(px.px, g.ppx);
+    e.dph = xs(px.py, g.ppy);
+  }
+  const double r2 = xa(xm(e.u, e.u), xm(e.v, e.v));
+  const bool lp_possible = g.has_proj && e.dpw * e.dpw + e.dph * e.dph <= cos_view * cos_view * g.dp2max;
+  e.ev.center = e.ev.clamped = e.ev.degenerate = false;
+  if (r2 > g.r2max && !lp_possible) return;
+  eval_kernel(e.u, e.v, P.S, id, e.ev);
+  if (e.ev.degenerate) return;
+  const double o = P.S.o[id];
+  const double a_kernel = o * sharpen(e.ev.g, P.S.tau[id]);
+  double a = a_kernel;
+  if (g.has_proj) {
+    const double f = low_pass_filter_term(e.dpw, e.dph, cos_view, o, P.opt.lowpass_radius);
+    if (f > a_kernel) {
+      a = f;
+      e.lp = true;
+    }
+  }
+  if (a < P.opt.alpha_min) return;
+  e.a = dmin(a, 1.0 - 1e-6);
+  float r0, r1, r2c;
+  px.sh_rgb(P, id, r0, r1, r2c);
+  e.cl[0] = r0 < 0;
+  e.cl[1] = r1 < 0;
+  e.cl[2] = r2c < 0;
+  e.rgb[0] = e.cl[0] ? 0.f : r0;
+  e.rgb[1] = e.cl[1] ? 0.f : r1;
+  e.rgb[2] = e.cl[2] ? 0.f : r2c;
+  e.valid = true;
+}
+
+// fp64 re-render, one WARP per flagged pixel: lanes intersect 32 list
+// entries at once, lane 0 runs the SortCache over them (in order), lanes
+// evaluate the popped entries' alpha in parallel, and lane 0 composites
+// them in order until saturation (backward: lanes then compute their
+// record's gradient with the transmittance / rest lane 0 produced).
+template <int MODE, bool BWD>
+__global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned total = *P.redo_count;
+  const unsigned nwarps = gridDim.x * (blockDim.x / 32);
+  for (unsigned t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); t < total; t += nwarps) {
+    const int pix = P.redo_list[t];
+    const int x = pix % P.cam.W, y = pix / P.cam.W;
+    const int tile = (y / kTile) * P.cam.tiles_x + (x / kTile);
+    Pixel<BWD, true> px;
+    px.init(P, x, y);
+    if (BWD) px.init_bwd(P);
+    double cd[kCacheCap];
+    int ci[kCacheCap];
+    int csz = 0;
+    bool done = false;
+    const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
+    long long j = beg;
+    while (!done) {
+      // 1) up to 32 pops: parallel intersections, in-order SortCache on lane 0
+      double my_rt = 0;
+      int my_id = -1, npop = 0;
+      bool list_end = j >= end;
+      if (!list_end) {
+        const long long jj = j + lane;
+        double rt = 0;
+        int id = -1;
+        bool hit = false;
+        if (jj < end) {
+          id = (int)(P.pv[jj] & 0xffffffffull);
+          const Geo& g = P.geo[id];
+          const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.rz[0], g.rz[1], g.rz[2]);
+          if (fabs(denom) >= P.opt.grazing_eps) {
+            rt = g.num / denom;
+            hit = rt > 0;
+          }
+        }
+        const unsigned hits = __ballot_sync(FULL, hit);
+        for (int k = 0; k < 32; ++k) {
+          const double rk = __shfl_sync(FULL, rt, k);
+          const int ik = __shfl_sync(FULL, id, k);
+          if (!((hits >> k) & 1u)) continue;
+          bool pop = false;
+          double prt = rk;
+          int pid = ik;
+          if (MODE == 1) pop = true;
+          else pop = cache_step(cd, ci, csz, rk, ik, prt, pid);  // replicated on all lanes
+          if (pop) {
+            if (lane == npop) {
+              my_rt = prt;
+              my_id = pid;
+            }
+            ++npop;
+          }
+        }
+        j += 32;
+      } else if (MODE == 0) {
+        // end marker: drain the head (up to 8 pops)
+        while (csz > 0 && npop < 32) {
+          if (lane == npop) {
+            my_rt = cd[0];
+            my_id = ci[0];
+          }
+#pragma unroll
+          for (int q = 0; q < kCacheCap - 1; ++q) {
+            cd[q] = cd[q + 1];
+            ci[q] = ci[q + 1];
+          }
+          --csz;
+          ++npop;
+        }
+      }
+      if (npop == 0) {
+        if (list_end) break;
+        continue;
+      }
+      // 2) parallel fp64 evaluation of the pops
+      PopEval e;
+      e.valid = false;
+      if (lane < npop) eval_pop<BWD>(P, px, my_rt, my_id, e);
+      if (lane < npop && e.ev.degenerate) px.err = true;
+      // 3) in-order compositing (all lanes replicate the scalar state)
+      double wb_mine = 0, dat_mine = 0, T_mine = 1;
+      int last_k = npop - 1;
+      for (int k = 0; k < npop && !done; ++k) {
+        last_k = k;
+        const bool valid = __shfl_sync(FULL, e.valid, k);
+        if (!valid) continue;
+        const double a = __shfl_sync(FULL, e.a, k);
+        const double rt = __shfl_sync(FULL, e.rt, k);
+        const float r0 = __shfl_sync(FULL, e.rgb[0], k), r1 = __shfl_sync(FULL, e.rgb[1], k),
+                    r2 = __shfl_sync(FULL, e.rgb[2], k);
+        const double denom = __shfl_sync(FULL, e.denom, k);
+        const int id = __shfl_sync(FULL, e.id, k);
+        const Geo& g = P.geo[id];
+        const double sgn = denom < 0 ? 1.0 : -1.0;
+        const double w = px.T * a;
+        ++px.n_comp;
+        if (!BWD) {
+          px.C[0] += w * r0;
+          px.C[1] += w * r1;
+          px.C[2] += w * r2;
+          px.D += w * rt;
+          px.N[0] += w * (sgn * g.rz[0]);
+          px.N[1] += w * (sgn * g.rz[1]);
+          px.N[2] += w * (sgn * g.rz[2]);
+          px.A += w;
+        } else {
+          const double cw = (px.dC[0] * r0 + px.dC[1] * r1 + px.dC[2] * r2) + px.dD * rt +
+                            (px.dN[0] * (sgn * g.rz[0]) + px.dN[1] * (sgn * g.rz[1]) + px.dN[2] * (sgn * g.rz[2])) +
+                            px.dA;
+          px.rest -= w * cw;
+          if (lane == k) {
+            wb_mine = w;
+            T_mine = px.T;
+            dat_mine = px.T * cw - px.rest / (1.0 - a);
+          }
+        }
+        px.T = xm(px.T, xs(1.0, a));
+        if (px.T < P.opt.early_stop) done = true;
+      }
+      if (!BWD && P.replay_cap > 0) {
+        // replay records in order (lane k writes its own entry)
+        int rec_idx = px.n_rec;
+        for (int k = 0; k <= last_k; ++k) {
+          const bool valid = __shfl_sync(FULL, e.valid, k);
+          if (!valid) continue;
+          if (lane == k && rec_idx < P.replay_cap) {
+            const size_t r = (size_t)px.pix * P.replay_cap + rec_idx;
+            P.replay_ids[r] = e.id;
+            double* rec = P.replay_rec + 5 * r;
+            rec[0] = e.u;
+            rec[1] = e.v;
+            rec[2] = e.rt;
+            rec[3] = e.a;
+            rec[4] = e.lp ? 1.0 : 0.0;
+          }
+          ++rec_idx;
+        }
+        px.n_rec = rec_idx;
+      }
+      if (BWD && lane < npop && e.valid && wb_mine != 0) {
+        // this lane's record: gradients with the sequential T / rest
+        const Geo& g = P.geo[e.id];
+        const double rgb[3] = {(double)e.rgb[0], (double)e.rgb[1], (double)e.rgb[2]};
+        const double sgn = e.denom < 0 ? 1.0 : -1.0;
+        px.backward_record_dat(P, e.id, g, e.rt, e.u, e.v, e.a, e.lp, e.ev, rgb, e.cl[0], e.cl[1], e.cl[2], sgn,
+                               e.denom, e.dpw, e.dph, wb_mine, dat_mine, T_mine);
+      }
+    }
+    if (lane == 0) {
+      if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
+      if (!BWD) {
+        px.finish_forward(P);
+        atomicAdd(&P.counters[C_REDO_PIXELS], 1ull);
+      }
+    }
+  }
+}
+
 template <int MODE, bool BWD>
 __global__ void __launch_bounds__(128) k_raster_pixels(RasterParams P) {
   const unsigned total = *P.redo_count;
@@ -1239,18 +1476,18 @@ void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s,
   }
   // fp32 pass (all pixels; flags uncertain ones), then the fp64 pass over the
   // flagged pixels (CTAs without flagged pixels exit immediately).
-  const int redo_blocks = 148 * 2;
+  // warp per pixel: 148 SMs x 8 CTAs x 4 warps, grid-stride over the list
+  const int redo_blocks = 148 * 8;
   if (P.opt.fp64_alpha) {
     // reference-precision mode: every pixel through the fp64 per-pixel path
     const unsigned npx = (unsigned)P.cam.W * P.cam.H;
     if (!bwd) k_fill_pixels<<<(npx + 255) / 256, 256, 0, s>>>(P.redo_list, P.redo_count, npx);
-    const int blocks = (int)std::min<unsigned>((npx + 127) / 128, 148 * 8);
     if (P.opt.use_cache) {
-      if (bwd) k_raster_pixels<0, true><<<blocks, 128, 0, s>>>(P);
-      else k_raster_pixels<0, false><<<blocks, 128, 0, s>>>(P);
+      if (bwd) k_raster_pixels_warp<0, true><<<redo_blocks, 128, 0, s>>>(P);
+      else k_raster_pixels_warp<0, false><<<redo_blocks, 128, 0, s>>>(P);
     } else {
-      if (bwd) k_raster_pixels<1, true><<<blocks, 128, 0, s>>>(P);
-      else k_raster_pixels<1, false><<<blocks, 128, 0, s>>>(P);
+      if (bwd) k_raster_pixels_warp<1, true><<<redo_blocks, 128, 0, s>>>(P);
+      else k_raster_pixels_warp<1, false><<<redo_blocks, 128, 0, s>>>(P);
     }
     if (mid) cudaEventRecord(mid, s);
     return;
@@ -1260,14 +1497,14 @@ void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s,
     if (bwd) k_raster_bwd<0, false><<<n_tiles, 256, 0, s>>>(P);
     else k_raster<0, false, false><<<n_tiles, 256, 0, s>>>(P);
     if (mid) cudaEventRecord(mid, s);
-    if (bwd) k_raster_pixels<0, true><<<redo_blocks, 128, 0, s>>>(P);
-    else k_raster_pixels<0, false><<<redo_blocks, 128, 0, s>>>(P);
+    if (bwd) k_raster_pixels_warp<0, true><<<redo_blocks, 128, 0, s>>>(P);
+    else k_raster_pixels_warp<0, false><<<redo_blocks, 128, 0, s>>>(P);
   } else {
     if (bwd) k_raster_bwd<1, false><<<n_tiles, 256, 0, s>>>(P);
     else k_raster<1, false, false><<<n_tiles, 256, 0, s>>>(P);
     if (mid) cudaEventRecord(mid, s);
-    if (bwd) k_raster_pixels<1, true><<<redo_blocks, 128, 0, s>>>(P);
-    else k_raster_pixels<1, false><<<redo_blocks, 128, 0, s>>>(P);
+    if (bwd) k_raster_pixels_warp<1, true><<<redo_blocks, 128, 0, s>>>(P);
+    else k_raster_pixels_warp<1, false><<<redo_blocks, 128, 0, s>>>(P);
   }
 }
 
