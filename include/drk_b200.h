@@ -193,10 +193,11 @@ int drk_backward(drk_ctx* ctx, const float* raw, const drk_frame_grad* fg, float
                  float* d_center_world, float* screen_grad, uint8_t* touched, int accumulate,
                  int deterministic);
 /* Activated-space gradients (drk::PrimGrads, reference grad.hpp:19-29) of the
- * last backward, fp64, n x G with G = 3 + 9 + 2K + 3 + 3*terms in the order
- * d_center, d_rot (row-major), d_scales, d_angles, d_eta, d_tau, d_opacity,
- * d_sh.  Device pointer owned by the context. */
-int drk_get_prim_grads(drk_ctx* ctx, const double** grads, int* stride);
+ * last backward, fp32, n rows of *stride floats (3 + 9 + 2K + 3 + 3*terms
+ * components padded to a multiple of 4) in the order d_center, d_rot
+ * (row-major), d_scales, d_angles, d_eta, d_tau, d_opacity, d_sh.  Device
+ * pointer owned by the context. */
+int drk_get_prim_grads(drk_ctx* ctx, const float** grads, int* stride);
 
 /* --- loss and optimizer (reference optimize.cpp:171-204, :226-307) -------- */
 /* L1 branch of drk::loss (dssim_weight = 0): loss_out (device, 1 double)

@@ -26,7 +26,7 @@ template <typename T>
 int exclusive_scan(drk_ctx* c, const T* in, long long n, long long* out, long long* total);
 int sort_pairs(drk_ctx* c, unsigned long long*& k, unsigned long long*& v, unsigned long long*& k2,
                unsigned long long*& v2, long long n);
-void launch_act_bwd(int n, int K, int terms, const float* raw, const double* gact, int G,
+void launch_act_bwd(int n, int K, int terms, const float* raw, const float* gact, int G,
                     const unsigned char* touched_dev, const Geo* geo, const CamD& cam, float* grad_raw,
                     float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
                     cudaStream_t s);
@@ -314,12 +314,14 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   if (!c->has_fwd) return set_error(c, DRK_ERR_REPLAY_MISMATCH, "backward without a forward on this context");
   const Activated& A = c->act;
   const int n = A.n, K = A.K;
-  const int G = 3 + 9 + 2 * K + 3 + 3 * A.terms;
+  // activated-space gradient rows, padded to a multiple of 4 floats so that
+  // the warp-reduced sums go out as 16-byte vector atomics
+  const int G = (3 + 9 + 2 * K + 3 + 3 * A.terms + 3) & ~3;
   cudaStream_t s = c->stream;
-  double* gact = ensure<double>(c->gact, (size_t)G * n + 1);
+  float* gact = ensure<float>(c->gact, (size_t)G * n + 4);
   unsigned char* tch = ensure<unsigned char>(c->touched, n + 1);
   if (!gact || !tch) return set_error(c, DRK_ERR_OOM, "gradient buffers");
-  cudaMemsetAsync(gact, 0, sizeof(double) * G * (size_t)n, s);
+  cudaMemsetAsync(gact, 0, sizeof(float) * G * (size_t)n, s);
   cudaMemsetAsync(tch, 0, n + 1, s);
   RasterParams P = raster_params(c);
   P.pxstate = static_cast<double*>(c->pxstate.p);
@@ -615,10 +617,10 @@ int drk_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   return run_backward(c, raw, fg, grad_raw, d_center_world, screen_grad, touched, accumulate, deterministic);
 }
 
-int drk_get_prim_grads(drk_ctx* c, const double** grads, int* stride) {
+int drk_get_prim_grads(drk_ctx* c, const float** grads, int* stride) {
   if (!c || !grads || !stride) return DRK_ERR_INVALID_ARG;
-  *grads = static_cast<const double*>(c->gact.p);
-  *stride = 3 + 9 + 2 * c->act.K + 3 + 3 * c->act.terms;
+  *grads = static_cast<const float*>(c->gact.p);
+  *stride = (3 + 9 + 2 * c->act.K + 3 + 3 * c->act.terms + 3) & ~3;
   return DRK_OK;
 }
 

@@ -71,7 +71,7 @@ struct RasterParams {
   int replay_cap;
   // backward
   const float *dC, *dD, *dN, *dA;
-  double* gact;
+  float* gact;  // activated-space gradients, fp32, row stride G (multiple of 4)
   int G;
   unsigned char* touched;
   unsigned long long* counters;

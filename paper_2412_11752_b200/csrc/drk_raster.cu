@@ -252,7 +252,7 @@ struct Pixel {
                                       double dat, double T_i) const {
     (void)rgb;
     (void)T_i;
-    double* pg = P.gact + (size_t)id * P.G;
+    float* pg = P.gact + (size_t)id * P.G;
     const int K = P.S.K;
     const double rz[3] = {g.rz[0], g.rz[1], g.rz[2]};
     P.touched[id] = 1;
@@ -602,7 +602,76 @@ struct Pixel {
     const float wc0 = rec && !cl[0] ? (float)(wb * dC[0]) : 0.f;
     const float wc1 = rec && !cl[1] ? (float)(wb * dC[1]) : 0.f;
     const float wc2 = rec && !cl[2] ? (float)(wb * dC[2]) : 0.f;
-    if (remaining) {
+    if (remaining && !kUseGradSlots) {
+      // Transpose-reduce: the lane's G components go to a local array; per
+      // chunk of 32 components, 5 halving steps (16+8+4+2+1 = 31 shuffles)
+      // leave lane l with the group sum of component (chunk + l), which it
+      // adds to HBM — 31 shuffles and one atomic instruction per 32
+      // components instead of 160 shuffles and 32 single-lane atomics.
+      float comps[kGradSlotStride];
+#pragma unroll
+      for (int c = 0; c < kGradSlotStride; ++c) comps[c] = 0.f;
+      if (rec) {
+        comps[0] = (float)dcen[0];
+        comps[1] = (float)dcen[1];
+        comps[2] = (float)dcen[2];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) comps[3 + q] = (float)drot[q];
+        comps[o_sc + lo] += (float)ds_lo;
+        comps[o_sc + hi] += (float)ds_hi;
+        comps[o_an + lo] += (float)da_lo;
+        comps[o_an + hi] += (float)da_hi;
+        comps[o_eta] = (float)deta;
+        comps[o_eta + 1] = (float)dtau;
+        comps[o_eta + 2] = (float)dop;
+        for (int t = 0; t < P.opt.terms_active; ++t) {
+          const float b = basis[t];
+          comps[o_sh + 3 * t] = wc0 * b;
+          comps[o_sh + 3 * t + 1] = wc1 * b;
+          comps[o_sh + 3 * t + 2] = wc2 * b;
+        }
+      }
+      const int G = P.G;
+      for (int pass = 0; pass < 2 && remaining; ++pass) {
+        const int lead = __ffs(remaining) - 1;
+        const int gid = __shfl_sync(FULL, id, lead);
+        const bool in_g = rec && id == gid && ((remaining >> lane) & 1u);
+        remaining &= ~__ballot_sync(FULL, in_g);
+        if (lane == lead) ++n_rej2;  // groups reduced (backward reuses the counter)
+        float* pg = P.gact + (size_t)gid * G;
+#pragma unroll
+        for (int base = 0; base < kGradSlotStride; base += 32) {
+          if (base >= G) break;
+          float x[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = in_g ? comps[base + i] : 0.f;
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) {
+            const bool up = (lane & off) != 0;
+#pragma unroll
+            for (int i = 0; i < off; ++i) {
+              const float send = up ? x[i] : x[i + off];
+              const float keep = up ? x[i + off] : x[i];
+              x[i] = keep + __shfl_xor_sync(FULL, send, off);
+            }
+          }
+          // lane 4m gathers components 4m..4m+3 and issues one 16-byte vector atomic
+          const float x1 = __shfl_down_sync(FULL, x[0], 1), x2 = __shfl_down_sync(FULL, x[0], 2),
+                      x3 = __shfl_down_sync(FULL, x[0], 3);
+          const int c = base + lane;
+          if ((lane & 3) == 0 && c < G && (x[0] != 0.f || x1 != 0.f || x2 != 0.f || x3 != 0.f))
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(pg + c), "f"(x[0]), "f"(x1),
+                         "f"(x2), "f"(x3)
+                         : "memory");
+        }
+      }
+      // third and later primitive groups of this step: direct atomics
+      if (rec && ((remaining >> lane) & 1u)) {
+        float* po = P.gact + (size_t)id * G;
+        for (int c = 0; c < G; ++c)
+          if (comps[c] != 0.f) atomicAdd(po + c, comps[c]);
+      }
+    } else if (remaining) {
       const int lead = __ffs(remaining) - 1;
       const int gid = __shfl_sync(FULL, id, lead);
       const bool in_g = rec && id == gid;
@@ -616,21 +685,19 @@ struct Pixel {
       }
       slot = __shfl_sync(FULL, slot, lead);
       float* acc = slot >= 0 ? slot_val + (size_t)slot * kGradSlotStride : nullptr;
-      double* pg = P.gact + (size_t)gid * P.G;
-      double* pgo = rec ? P.gact + (size_t)id * P.G : nullptr;
+      float* pg = P.gact + (size_t)gid * P.G;
+      float* pgo = rec ? P.gact + (size_t)id * P.G : nullptr;
       auto emit = [&](int off, float val) {
         float s = in_g ? val : 0.f;
 #pragma unroll
         for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(FULL, s, m);
-        // lanes of other primitives (7% of records on config 2) add directly
-        if (!solo && rec && !in_g && val != 0.f) atomicAdd(pgo + off, (double)val);
+        // lanes of other primitives add directly
+        if (!solo && rec && !in_g && val != 0.f) atomicAdd(pgo + off, val);
         if (lane == lead && s != 0.f) {
           if (acc) atomicAdd(acc + off, s);
-          else atomicAdd(pg + off, (double)s);
+          else atomicAdd(pg + off, s);
         }
       };
-      // rolled on purpose: keeps the 48 SH emits out of the register budget
-      // (basis[] is read from local memory here; measured faster than unrolled)
 #pragma unroll 1
       for (int t = 0; t < P.opt.terms_active; ++t) {
         const float b = basis[t];
@@ -885,7 +952,7 @@ __device__ __forceinline__ void flush_grad_slots(const RasterParams& P, int* slo
     const int s = idx / G, c = idx - s * G;
     const int id = slot_id[s];
     float* v = slot_val + (size_t)s * kGradSlotStride + c;
-    if (id >= 0 && *v != 0.f) atomicAdd(P.gact + (size_t)id * G + c, (double)*v);
+    if (id >= 0 && *v != 0.f) atomicAdd(P.gact + (size_t)id * G + c, *v);
     *v = 0.f;
   }
   __syncthreads();
@@ -1591,13 +1658,14 @@ void launch_alpha_bound(const ShapeView& S, int n, long long samples, unsigned l
 // ---------------------------------------------------------------------------
 // K6: activation backward (grad.cpp:122-159) + screen_grad (grad.cpp:375-383)
 // ---------------------------------------------------------------------------
-__global__ void k_act_bwd(int n, int K, int terms, const float* __restrict__ raw, const double* __restrict__ gact,
+__global__ void k_act_bwd(int n, int K, int terms, const float* __restrict__ raw, const float* __restrict__ gact,
                           int G, const unsigned char* __restrict__ touched_dev, const Geo* __restrict__ geo, CamD cam,
                           float* grad_raw, float* d_center_world, float* screen_grad, unsigned char* touched_out,
                           int accumulate) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double* g = gact + (size_t)i * G;
+  double g[kGradSlotStride];
+  for (int c = 0; c < kGradSlotStride; ++c) g[c] = c < G ? (double)gact[(size_t)i * G + c] : 0.0;
   const int tch = touched_dev[i];
   if (d_center_world)
     for (int a = 0; a < 3; ++a) d_center_world[3 * i + a] = (float)g[a];
@@ -1678,7 +1746,7 @@ __global__ void k_act_bwd(int n, int K, int terms, const float* __restrict__ raw
   }
 }
 
-void launch_act_bwd(int n, int K, int terms, const float* raw, const double* gact, int G,
+void launch_act_bwd(int n, int K, int terms, const float* raw, const float* gact, int G,
                     const unsigned char* touched_dev, const Geo* geo, const CamD& cam, float* grad_raw,
                     float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
                     cudaStream_t s) {

@@ -99,7 +99,10 @@ template int exclusive_scan<unsigned>(drk_ctx*, const unsigned*, long long, long
 // ---------------------------------------------------------------------------
 // radix sort
 // ---------------------------------------------------------------------------
-constexpr int kRsWarps = 8, kRsItems = 8, kRsThreads = kRsWarps * 32, kRsChunk = kRsThreads * kRsItems;
+#ifndef DRK_RS_ITEMS
+#define DRK_RS_ITEMS 8
+#endif
+constexpr int kRsWarps = 8, kRsItems = DRK_RS_ITEMS, kRsThreads = kRsWarps * 32, kRsChunk = kRsThreads * kRsItems;
 
 __global__ void k_bits(const unsigned long long* __restrict__ k, const unsigned long long* __restrict__ v, long long n,
                        unsigned long long* acc /* or_k, and_k, or_v, and_v */) {
