@@ -193,10 +193,11 @@ int drk_backward(drk_ctx* ctx, const float* raw, const drk_frame_grad* fg, float
                  float* d_center_world, float* screen_grad, uint8_t* touched, int accumulate,
                  int deterministic);
 /* Activated-space gradients (drk::PrimGrads, reference grad.hpp:19-29) of the
- * last backward, fp32, n rows of *stride floats (3 + 9 + 2K + 3 + 3*terms
- * components padded to a multiple of 4) in the order d_center, d_rot
- * (row-major), d_scales, d_angles, d_eta, d_tau, d_opacity, d_sh.  Device
- * pointer owned by the context. */
+ * last backward, fp32, n rows of *stride floats in a K-independent layout:
+ * d_center [0,3), d_rot [3,12) (row-major), d_scales [12,28), d_angles
+ * [28,44) (first K used), d_eta 44, d_tau 45, d_opacity 46, d_sh from 47
+ * (RGB per term); rows padded to a multiple of 4.  Device pointer owned by
+ * the context. */
 int drk_get_prim_grads(drk_ctx* ctx, const float** grads, int* stride);
 
 /* --- loss and optimizer (reference optimize.cpp:171-204, :226-307) -------- */

@@ -316,7 +316,7 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   const int n = A.n, K = A.K;
   // activated-space gradient rows, padded to a multiple of 4 floats so that
   // the warp-reduced sums go out as 16-byte vector atomics
-  const int G = (3 + 9 + 2 * K + 3 + 3 * A.terms + 3) & ~3;
+  const int G = grad_row_stride(A.terms);
   cudaStream_t s = c->stream;
   float* gact = ensure<float>(c->gact, (size_t)G * n + 4);
   unsigned char* tch = ensure<unsigned char>(c->touched, n + 1);

@@ -26,6 +26,15 @@ constexpr int kTile = 16;
 constexpr int kCacheCap = 8;  // raster.hpp:37
 constexpr int kMaxK = 16;
 
+// Row layout of the activated-space gradient buffer (drk::PrimGrads,
+// grad.hpp:19-29), fixed for every K so that the backward's component indices
+// are compile-time constants: d_center 0..2, d_rot 3..11 (row-major),
+// d_scales [12, 12+kMaxK), d_angles, d_eta, d_tau, d_opacity, d_sh (RGB per
+// term).  Rows are padded to a multiple of 4 floats (16-byte vector atomics).
+constexpr int kGOffSc = 12, kGOffAn = kGOffSc + kMaxK, kGOffEta = kGOffAn + kMaxK, kGOffTau = kGOffEta + 1,
+              kGOffOp = kGOffEta + 2, kGOffSh = kGOffEta + 3;
+__host__ __device__ inline int grad_row_stride(int terms) { return (kGOffSh + 3 * terms + 3) & ~3; }
+
 // Device-side error / counter slots (ctx->counters).
 enum Counter {
   C_ERR_DEGEN_BASIS = 0,
@@ -294,22 +303,40 @@ __device__ __forceinline__ float sharpen_f(float g, float tau) {
 // tests/test_gpu_alpha_bound.py); r2 == 0 gives the exact centre value.
 // Psi(g) in point-slope form from fp64-derived per-primitive constants, with
 // the condition number A g / Psi that maps the relative error of g onto alpha.
-__device__ __forceinline__ float sharpen_ps(const float4 c0, const float4 c1, float g, float* cond) {
+__device__ __forceinline__ float sharpen_ps(const float4 c0, const float4 c1, float g, float* cond,
+                                            float* slope = nullptr, int* branch = nullptr) {
   // c0 = (g1, g2, A0, A1), c1 = (A2, Psi(g1), Psi(g2), o)
   float A, P;
+  int br;
   if (g < c0.x) {
     A = c0.z;
     P = c0.z * g;
+    br = 0;
   } else if (g < c0.y) {
     A = c0.w;
     P = c1.y + c0.w * (g - c0.x);
+    br = 1;
   } else {
     A = c1.x;
     P = c1.z + c1.x * (g - c0.y);
+    br = 2;
   }
   *cond = P > 0.f ? A * g / P : 1.0f;
+  if (slope) *slope = A;
+  if (branch) *branch = br;
   return P;
 }
+
+// Intermediates of the fp32 kernel evaluation, kept for the fp32 backward
+// (grad.cpp:16-101 restated on the fp32 quantities).
+struct KEvalF {
+  float g, P, A;          // g(u, v), Psi(g), dPsi/dg
+  float a, b, r1;         // endpoint-basis coordinates, r1 = |a| + |b|
+  float delta, sh, ch;    // bracket angle and sin/cos(delta / 2)
+  float inv;              // 1 / s_bar^2
+  int lo, hi, br;         // bracket, sharpen branch
+  bool center, clamped;
+};
 
 // With reject_ok, returns -1 as soon as a lower bound of Q shows
 // alpha_kernel < alpha_min with margin: within the bracket, r1 and the
@@ -317,7 +344,7 @@ __device__ __forceinline__ float sharpen_ps(const float4 c0, const float4 c1, fl
 // alpha < alpha_min <=> Q > f_vis^2 (core.cpp:305-318 with Psi monotone).
 __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const ShapeView& S, int i, float o,
                                            float tau, float eta, float* rel, bool* degenerate,
-                                           bool reject_ok = false) {
+                                           bool reject_ok = false, KEvalF* kf = nullptr) {
   *degenerate = false;
   (void)o;
   (void)tau;
@@ -326,6 +353,13 @@ __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const 
   if (r2 == 0) {
     float cond;
     *rel = 5e-7f;
+    if (kf) {
+      kf->center = true;
+      kf->clamped = false;
+      kf->g = 1.0f;
+      kf->P = sharpen_ps(c0, c1, 1.0f, &cond, &kf->A, &kf->br);
+      return c1.w * kf->P;
+    }
     return c1.w * sharpen_ps(c0, c1, 1.0f, &cond);
   }
   const int K = S.K;
@@ -377,7 +411,22 @@ __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const 
   const float e = fmaxf(-0.5f * Q, -30.0f);
   const float g = expf(e);
   float cond;
-  const float P = sharpen_ps(c0, c1, g, &cond);
+  const float P = kf ? sharpen_ps(c0, c1, g, &cond, &kf->A, &kf->br) : sharpen_ps(c0, c1, g, &cond);
+  if (kf) {
+    kf->center = false;
+    kf->clamped = -0.5f * Q < -30.0f;
+    kf->g = g;
+    kf->P = P;
+    kf->a = a;
+    kf->b = b;
+    kf->r1 = r1;
+    kf->delta = delta;
+    kf->sh = sh;
+    kf->ch = ch;
+    kf->inv = inv;
+    kf->lo = lo;
+    kf->hi = hi;
+  }
   // Relative error bound.  Q: fp32 formation of r1 and the products (~4
   // ulp) plus the cosine blend's sensitivity to delta, |d inv| <=
   // |sin(delta)| |h_lo - h_hi| / 2 * |d delta| with |d delta| <= 8e-7 (1 + delta)

@@ -32,18 +32,9 @@
 
 namespace drk {
 
-// Backward: per-CTA shared-memory gradient slots (direct-mapped by primitive
-// id), flushed to HBM at every batch boundary.  Stride >= G for K <= 16,
-// SH degree <= 3.
-constexpr int kGradSlots = 64;
+// Row stride bound of the activated-gradient buffer (grad_row_stride(16)).
 constexpr int kGradSlotStride = 96;
-// Measured on config 2: the CTA-shared slots (same-address shared atomics
-// from 8 warps) were slower (357 ms) than warp-reduced global atomics
-// (224 ms); kept switchable for the next round's CTA-level design.
-#ifndef DRK_GRAD_SLOTS
-#define DRK_GRAD_SLOTS 0
-#endif
-constexpr bool kUseGradSlots = DRK_GRAD_SLOTS != 0;
+static_assert(kGOffSh + 48 <= kGradSlotStride, "gradient row layout");
 #ifndef DRK_BWD_MIN_BLOCKS
 #define DRK_BWD_MIN_BLOCKS 2
 #endif
@@ -69,6 +60,8 @@ struct Pixel {
     px = x + 0.5;
     py = y + 0.5;
     pixel_dir(P.cam, px, py, dir);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) basis[t] = 0.f;
     sh_basis_f((float)dir[0], (float)dir[1], (float)dir[2], P.opt.sh_degree, basis);
     T = 1.0;
     C[0] = C[1] = C[2] = D = N[0] = N[1] = N[2] = A = 0;
@@ -256,8 +249,8 @@ struct Pixel {
     const int K = P.S.K;
     const double rz[3] = {g.rz[0], g.rz[1], g.rz[2]};
     P.touched[id] = 1;
-    const int o_rot = 3, o_sc = 12, o_an = 12 + K, o_eta = 12 + 2 * K, o_tau = o_eta + 1, o_op = o_eta + 2,
-              o_sh = o_eta + 3;
+    const int o_rot = 3, o_sc = kGOffSc, o_an = kGOffAn, o_eta = kGOffEta, o_tau = kGOffTau, o_op = kGOffOp,
+              o_sh = kGOffSh;
     // SH (linear, clamped channels gated)
     const bool cl[3] = {cl0, cl1, cl2};
     for (int ch = 0; ch < 3; ++ch) {
@@ -372,25 +365,26 @@ struct Pixel {
   // ---- warp-cooperative backward (k_raster_bwd) -------------------------
   // Called by all 32 lanes of a warp together.  `want` lanes replay the
   // forward decision for their popped entry; composited records compute
-  // their activated-space gradient, and each of the G components is reduced
-  // over the lanes whose record hits the same primitive as the first
-  // composited lane (butterfly shuffles), then added to HBM with one fp64
-  // atomic; lanes of other primitives add their own values directly.
-  // Returns false once this lane's pixel saturates.
-  __device__ bool composite_warp(const RasterParams& P, bool want, double rt, int id, int* slot_id,
-                                 float* slot_val) {
+  // their activated-space gradient (fp32 from the fp32 kernel evaluation, or
+  // fp64 in the F64 kernels), and the components are reduced over the lanes
+  // whose record hits the same primitive (transpose-reduce, below) and added
+  // to HBM with 16-byte vector reductions.  Returns false once this lane's
+  // pixel saturates.
+  __device__ bool composite_warp(const RasterParams& P, bool want, double rt, int id) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     bool rec = false, cont = true, lp = false, use64 = F64;
-    double a = 0, u = 0, v = 0, denom = 0, dpw = 0, dph = 0, rz[3] = {0, 0, 0};
+    double a = 0, u = 0, v = 0, r2 = 0, denom = 0, dpw = 0, dph = 0, rz[3] = {0, 0, 0};
     float rgbf[3] = {0, 0, 0};
     bool cl[3] = {false, false, false};
-    KEval ev;
+    KEval ev;  // fp64 evaluation (F64 kernels; fp32 decisions inside their bound)
     ev.center = ev.clamped = ev.degenerate = false;
     ev.g = 1.0;
     ev.lo = ev.hi = 0;
+    KEvalF kf;  // fp32 evaluation, differentiated by the fp32 backward
+    kf.center = true;
+    kf.clamped = false;
     const Geo* gp = nullptr;
-    float rel = 0.f;
     if (want) {
       const Geo& g = P.geo[id];
       gp = &g;
@@ -408,7 +402,7 @@ struct Pixel {
         dpw = xs(px, g.ppx);
         dph = xs(py, g.ppy);
       }
-      const double r2 = xa(xm(u, u), xm(v, v));
+      r2 = xa(xm(u, u), xm(v, v));
       const bool lp_possible = g.has_proj && dpw * dpw + dph * dph <= cos_view * cos_view * g.dp2max;
       const bool reject = r2 > g.r2max && !lp_possible;
       if (!reject) {
@@ -418,7 +412,7 @@ struct Pixel {
           bool degen;
           float relk;
           const float ak = alpha_f32(u, v, r2, P.S, id, (float)o, (float)tau, (float)P.S.eta[id], &relk, &degen,
-                                     !lp_possible);
+                                     !lp_possible, &kf);
           if (degen) {
             err = true;
             cont = false;
@@ -441,7 +435,6 @@ struct Pixel {
           if (fabsf(at - amin) <= relt * at + 1e-12f) use64 = true;
           if (at >= 0.99f && fabs((double)at - (1.0 - 1e-6)) <= (double)relt * at + 1e-12) use64 = true;
           a = (double)at;
-          rel = relt;
         }
         if (skip) {
           a = 0;  // alpha < alpha_min: not composited
@@ -461,7 +454,6 @@ struct Pixel {
                 lp = true;
               }
             }
-            rel = 0.f;
           }
         }
         if (cont && !skip && a >= P.opt.alpha_min) {
@@ -475,7 +467,6 @@ struct Pixel {
           rgbf[0] = cl[0] ? 0.f : r0;
           rgbf[1] = cl[1] ? 0.f : r1;
           rgbf[2] = cl[2] ? 0.f : r2c;
-          if (!use64 && !lp && !(a >= 1.0 - 1e-6 - 1e-12)) eval_kernel(u, v, P.S, id, ev);
         }
       }
     }
@@ -492,235 +483,318 @@ struct Pixel {
       ++n_comp;
     }
     // per-record activated-space gradient (grad.cpp:237-301, :16-101)
-    const int K = P.S.K;
-    double dcen[3] = {0, 0, 0}, drot[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    double deta = 0, dtau = 0, dop = 0, ds_lo = 0, ds_hi = 0, da_lo = 0, da_hi = 0;
+    float dcen[3] = {0, 0, 0}, drot[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    float deta = 0, dtau = 0, dop = 0, ds_lo = 0, ds_hi = 0, da_lo = 0, da_hi = 0;
     int lo = 0, hi = 0;
     if (rec) {
-      const Geo& g = *gp;
-      if (has_dN)
-        for (int q = 0; q < 3; ++q) drot[3 * q + 2] += wb * sgn * dN[q];
-      if (dD != 0) {
-        const double d_rt = wb * dD;
-        for (int q = 0; q < 3; ++q) {
-          const double h = P.cam.o[q] + rt * dir[q] - g.mu[q];
-          dcen[q] += d_rt * rz[q] / denom;
-          drot[3 * q + 2] += d_rt * (-h / denom);
-        }
-      }
-      const bool alpha_clamped = a >= 1.0 - 1e-6 - 1e-12;
-      const double o = P.S.o[id];
-      if (!alpha_clamped && lp) {
-        const double cv = fabs(denom), sl = P.opt.lowpass_radius;
-        dop += dat * a / o;
-        const double inv = 1.0 / (cv * cv * sl * sl);
-        const double d_dpw = dat * a * (-dpw * inv);
-        const double d_dph = dat * a * (-dph * inv);
-        const double d_cos = dat * a * (dpw * dpw + dph * dph) * inv / cv;
-        double J[6];
-        projection_jacobian(P.cam, g.mu, J);
-        for (int q = 0; q < 3; ++q) dcen[q] += -(J[q] * d_dpw + J[3 + q] * d_dph);
-        const double sg = denom < 0 ? -1.0 : 1.0;
-        for (int q = 0; q < 3; ++q) drot[3 * q + 2] += d_cos * sg * dir[q];
-      } else if (!alpha_clamped) {
-        const double tau = P.S.tau[id];
-        dop += dat * sharpen(ev.g, tau);
-        if (!ev.center) {
-          const int br = sharpen_branch(ev.g, tau);
-          dtau += dat * o * sharpen_dtau(br, ev.g, tau);
-          if (!ev.clamped) {
-            const double d_g = dat * o * sharpen_slope(br, tau);
-            const double d_q = d_g * (-0.5 * ev.g);
-            lo = ev.lo;
-            hi = ev.hi;
-            const double* s = P.S.s + (size_t)id * K;
-            const double* th = P.S.th + (size_t)id * K;
-            const double slo = s[lo], shi = s[hi], eta = P.S.eta[id];
-            deta += d_q * (ev.r1 * ev.r1 - ev.r2 * ev.inv_sbar);
-            const double d_r1 = d_q * eta * 2.0 * ev.r1;
-            const double d_r2sq = d_q * (1.0 - eta) * ev.inv_sbar;
-            const double d_inv = d_q * (1.0 - eta) * ev.r2;
-            const double c = cos(ev.delta);
-            ds_lo = d_inv * (-(1.0 + c) / (slo * slo * slo));
-            ds_hi = d_inv * (-(1.0 - c) / (shi * shi * shi));
-            const double d_c = d_inv * (0.5 / (slo * slo) - 0.5 / (shi * shi));
-            const double d_delta = d_c * (-sin(ev.delta));
-            double alo = th[lo], ahi = th[hi], theta = ev.theta;
-            if (hi == 0) {
-              alo -= kTwoPi;
-              if (theta > th[K - 1]) theta -= kTwoPi;
-            }
-            const double gap = ahi - alo;
-            const double d_tfd = d_delta * kPi / gap;
-            da_lo = d_delta * kPi * (theta - ahi) / (gap * gap);
-            da_hi = d_delta * (-kPi) * (theta - alo) / (gap * gap);
-            const double r2s = dmax(ev.r2, 1e-24);
-            double du = d_tfd * (-v / r2s);
-            double dv = d_tfd * (u / r2s);
-            du += d_r2sq * 2.0 * u;
-            dv += d_r2sq * 2.0 * v;
-            const double sa = ev.a > 0 ? 1 : (ev.a < 0 ? -1 : 0);
-            const double sb = ev.b > 0 ? 1 : (ev.b < 0 ? -1 : 0);
-            const double elx = P.S.ex[(size_t)id * K + lo], ely = P.S.ey[(size_t)id * K + lo];
-            const double ehx = P.S.ex[(size_t)id * K + hi], ehy = P.S.ey[(size_t)id * K + hi];
-            const double det = P.S.det[(size_t)id * K + lo];
-            du += d_r1 * (sa * (ehy / det) + sb * (-ely / det));
-            dv += d_r1 * (sa * (-ehx / det) + sb * (elx / det));
-            const double ca = cos(th[lo]), sa_lo = sin(th[lo]);
-            const double cb = cos(th[hi]), sb_hi = sin(th[hi]);
-            ds_lo += d_r1 * (-sa * ev.a / slo);
-            ds_hi += d_r1 * (-sb * ev.b / shi);
-            const double tlx = -slo * sa_lo, tly = slo * ca, thx = -shi * sb_hi, thy = shi * cb;
-            const double na = -ev.a, nb = -ev.b;
-            da_lo += d_r1 * (sa * (na * ((ehy * tlx - ehx * tly) / det)) + sb * (na * ((-ely * tlx + elx * tly) / det)));
-            da_hi += d_r1 * (sa * (nb * ((ehy * thx - ehx * thy) / det)) + sb * (nb * ((-ely * thx + elx * thy) / det)));
-            const double hh[3] = {P.cam.o[0] + rt * dir[0] - g.mu[0], P.cam.o[1] + rt * dir[1] - g.mu[1],
-                                  P.cam.o[2] + rt * dir[2] - g.mu[2]};
-            const double drx = dir[0] * g.rx[0] + dir[1] * g.rx[1] + dir[2] * g.rx[2];
-            const double dry = dir[0] * g.ry[0] + dir[1] * g.ry[1] + dir[2] * g.ry[2];
-            const double f = -(du * drx + dv * dry) / denom;
-            for (int q = 0; q < 3; ++q) {
-              dcen[q] += du * (rz[q] * (drx / denom) - g.rx[q]) + dv * (rz[q] * (dry / denom) - g.ry[q]);
-              drot[3 * q + 0] += du * hh[q];
-              drot[3 * q + 1] += dv * hh[q];
-              drot[3 * q + 2] += f * hh[q];
-            }
-          }
-        }
-      }
+      if (F64)
+        record_grad_f64(P, id, *gp, rt, u, v, a, lp, ev, denom, dpw, dph, wb, dat, sgn, dcen, drot, deta, dtau, dop,
+                        ds_lo, ds_hi, da_lo, da_hi, lo, hi);
+      else
+        record_grad_f32(P, id, *gp, rt, u, v, r2, a, lp, kf, denom, dpw, dph, wb, dat, sgn, dcen, drot, deta, dtau,
+                        dop, ds_lo, ds_hi, da_lo, da_hi, lo, hi);
     }
-    // Warp-cooperative accumulation.  Lanes are grouped by primitive (first
-    // composited lane's primitive first, then the next remaining one ...);
-    // each group's G components are butterfly-reduced and added into the
-    // CTA's shared-memory slot for that primitive (direct-mapped, claimed
-    // once per batch, flushed to HBM with fp64 atomics at batch boundaries),
-    // or straight to HBM when the slot holds another primitive.
-    const unsigned recmask = __ballot_sync(FULL, rec);
-    unsigned remaining = recmask;
-    if (recmask && lane == __ffs(recmask) - 1) ++n_rej1;  // warp steps (backward reuses the counter)
-    const int o_sc = 12, o_an = 12 + K, o_eta = 12 + 2 * K, o_sh = o_eta + 3;
     const float wc0 = rec && !cl[0] ? (float)(wb * dC[0]) : 0.f;
     const float wc1 = rec && !cl[1] ? (float)(wb * dC[1]) : 0.f;
     const float wc2 = rec && !cl[2] ? (float)(wb * dC[2]) : 0.f;
-    if (remaining && !kUseGradSlots) {
-      // Transpose-reduce: the lane's G components go to a local array; per
-      // chunk of 32 components, 5 halving steps (16+8+4+2+1 = 31 shuffles)
-      // leave lane l with the group sum of component (chunk + l), which it
-      // adds to HBM — 31 shuffles and one atomic instruction per 32
-      // components instead of 160 shuffles and 32 single-lane atomics.
-      float comps[kGradSlotStride];
-#pragma unroll
-      for (int c = 0; c < kGradSlotStride; ++c) comps[c] = 0.f;
-      if (rec) {
-        comps[0] = (float)dcen[0];
-        comps[1] = (float)dcen[1];
-        comps[2] = (float)dcen[2];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) comps[3 + q] = (float)drot[q];
-        comps[o_sc + lo] += (float)ds_lo;
-        comps[o_sc + hi] += (float)ds_hi;
-        comps[o_an + lo] += (float)da_lo;
-        comps[o_an + hi] += (float)da_hi;
-        comps[o_eta] = (float)deta;
-        comps[o_eta + 1] = (float)dtau;
-        comps[o_eta + 2] = (float)dop;
-        for (int t = 0; t < P.opt.terms_active; ++t) {
-          const float b = basis[t];
-          comps[o_sh + 3 * t] = wc0 * b;
-          comps[o_sh + 3 * t + 1] = wc1 * b;
-          comps[o_sh + 3 * t + 2] = wc2 * b;
-        }
-      }
-      const int G = P.G;
-      for (int pass = 0; pass < 2 && remaining; ++pass) {
-        const int lead = __ffs(remaining) - 1;
-        const int gid = __shfl_sync(FULL, id, lead);
-        const bool in_g = rec && id == gid && ((remaining >> lane) & 1u);
-        remaining &= ~__ballot_sync(FULL, in_g);
-        if (lane == lead) ++n_rej2;  // groups reduced (backward reuses the counter)
-        float* pg = P.gact + (size_t)gid * G;
-#pragma unroll
-        for (int base = 0; base < kGradSlotStride; base += 32) {
-          if (base >= G) break;
-          float x[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) x[i] = in_g ? comps[base + i] : 0.f;
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) {
-            const bool up = (lane & off) != 0;
-#pragma unroll
-            for (int i = 0; i < off; ++i) {
-              const float send = up ? x[i] : x[i + off];
-              const float keep = up ? x[i + off] : x[i];
-              x[i] = keep + __shfl_xor_sync(FULL, send, off);
-            }
-          }
-          // lane 4m gathers components 4m..4m+3 and issues one 16-byte vector atomic
-          const float x1 = __shfl_down_sync(FULL, x[0], 1), x2 = __shfl_down_sync(FULL, x[0], 2),
-                      x3 = __shfl_down_sync(FULL, x[0], 3);
-          const int c = base + lane;
-          if ((lane & 3) == 0 && c < G && (x[0] != 0.f || x1 != 0.f || x2 != 0.f || x3 != 0.f))
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(pg + c), "f"(x[0]), "f"(x1),
-                         "f"(x2), "f"(x3)
-                         : "memory");
-        }
-      }
-      // third and later primitive groups of this step: direct atomics
-      if (rec && ((remaining >> lane) & 1u)) {
-        float* po = P.gact + (size_t)id * G;
-        for (int c = 0; c < G; ++c)
-          if (comps[c] != 0.f) atomicAdd(po + c, comps[c]);
-      }
-    } else if (remaining) {
+    // Component c of this lane's gradient row (layout kGOff*); c is a
+    // compile-time constant at every call site, so nothing is indexed.
+    auto comp = [&](const int c) -> float {
+      if (c < 3) return dcen[c];
+      if (c < kGOffSc) return drot[c - 3];
+      if (c < kGOffAn) return (c - kGOffSc == lo ? ds_lo : 0.f) + (c - kGOffSc == hi ? ds_hi : 0.f);
+      if (c < kGOffEta) return (c - kGOffAn == lo ? da_lo : 0.f) + (c - kGOffAn == hi ? da_hi : 0.f);
+      if (c == kGOffEta) return deta;
+      if (c == kGOffTau) return dtau;
+      if (c == kGOffOp) return dop;
+      const int t = (c - kGOffSh) / 3, ch = (c - kGOffSh) % 3;
+      if (t >= 16) return 0.f;
+      return (ch == 0 ? wc0 : (ch == 1 ? wc1 : wc2)) * basis[t];
+    };
+    // Transpose-reduce: lanes are grouped by primitive (the first remaining
+    // record's primitive, twice per step); per chunk of 32 components, 5
+    // halving steps (16+8+4+2+1 = 31 shuffles) leave lane l with the group sum
+    // of component (chunk + l); lanes 4m gather four and issue one
+    // red.global.add.v4.f32.  Records of a third or later primitive in the
+    // same step add their own components directly.
+    const unsigned recmask = __ballot_sync(FULL, rec);
+    unsigned remaining = recmask;
+    if (recmask && lane == __ffs(recmask) - 1) ++n_rej1;  // warp steps (backward reuses the counter)
+    const int G = P.G;
+    for (int pass = 0; pass < 2 && remaining; ++pass) {
       const int lead = __ffs(remaining) - 1;
       const int gid = __shfl_sync(FULL, id, lead);
-      const bool in_g = rec && id == gid;
-      const bool solo = __all_sync(FULL, !rec || in_g);
+      const bool in_g = rec && id == gid && ((remaining >> lane) & 1u);
+      remaining &= ~__ballot_sync(FULL, in_g);
       if (lane == lead) ++n_rej2;  // groups reduced (backward reuses the counter)
-      int slot = -1;
-      if (lane == lead && slot_id) {
-        const int s = gid & (kGradSlots - 1);
-        const int old = atomicCAS(&slot_id[s], -1, gid);
-        slot = (old == -1 || old == gid) ? s : -1;
-      }
-      slot = __shfl_sync(FULL, slot, lead);
-      float* acc = slot >= 0 ? slot_val + (size_t)slot * kGradSlotStride : nullptr;
-      float* pg = P.gact + (size_t)gid * P.G;
-      float* pgo = rec ? P.gact + (size_t)id * P.G : nullptr;
-      auto emit = [&](int off, float val) {
-        float s = in_g ? val : 0.f;
+      float* pg = P.gact + (size_t)gid * G;
 #pragma unroll
-        for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(FULL, s, m);
-        // lanes of other primitives add directly
-        if (!solo && rec && !in_g && val != 0.f) atomicAdd(pgo + off, val);
-        if (lane == lead && s != 0.f) {
-          if (acc) atomicAdd(acc + off, s);
-          else atomicAdd(pg + off, s);
+      for (int base = 0; base < kGradSlotStride; base += 32) {
+        if (base >= G) break;
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = in_g ? comp(base + i) : 0.f;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+          const bool up = (lane & off) != 0;
+#pragma unroll
+          for (int i = 0; i < off; ++i) {
+            const float send = up ? x[i] : x[i + off];
+            const float keep = up ? x[i + off] : x[i];
+            x[i] = keep + __shfl_xor_sync(FULL, send, off);
+          }
         }
-      };
-#pragma unroll 1
-      for (int t = 0; t < P.opt.terms_active; ++t) {
-        const float b = basis[t];
-        emit(o_sh + 3 * t, wc0 * b);
-        emit(o_sh + 3 * t + 1, wc1 * b);
-        emit(o_sh + 3 * t + 2, wc2 * b);
+        const float x1 = __shfl_down_sync(FULL, x[0], 1), x2 = __shfl_down_sync(FULL, x[0], 2),
+                    x3 = __shfl_down_sync(FULL, x[0], 3);
+        const int c = base + lane;
+        if ((lane & 3) == 0 && c < G && (x[0] != 0.f || x1 != 0.f || x2 != 0.f || x3 != 0.f))
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(pg + c), "f"(x[0]), "f"(x1), "f"(x2),
+                       "f"(x3)
+                       : "memory");
       }
-      for (int q = 0; q < 3; ++q) emit(q, (float)dcen[q]);
-      for (int q = 0; q < 9; ++q) emit(3 + q, (float)drot[q]);
-      for (int k = 0; k < K; ++k) {
-        emit(o_sc + k, (float)((k == lo ? ds_lo : 0.0) + (k == hi ? ds_hi : 0.0)));
-        emit(o_an + k, (float)((k == lo ? da_lo : 0.0) + (k == hi ? da_hi : 0.0)));
+    }
+    if (rec && ((remaining >> lane) & 1u)) {
+      float* po = P.gact + (size_t)id * G;
+#pragma unroll
+      for (int c = 0; c < kGOffSc; ++c)
+        if (comp(c) != 0.f) atomicAdd(po + c, comp(c));
+      if (ds_lo != 0.f) atomicAdd(po + kGOffSc + lo, ds_lo);
+      if (ds_hi != 0.f) atomicAdd(po + kGOffSc + hi, ds_hi);
+      if (da_lo != 0.f) atomicAdd(po + kGOffAn + lo, da_lo);
+      if (da_hi != 0.f) atomicAdd(po + kGOffAn + hi, da_hi);
+      if (deta != 0.f) atomicAdd(po + kGOffEta, deta);
+      if (dtau != 0.f) atomicAdd(po + kGOffTau, dtau);
+      if (dop != 0.f) atomicAdd(po + kGOffOp, dop);
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        if (t < P.opt.terms_active) {
+          if (wc0 != 0.f) atomicAdd(po + kGOffSh + 3 * t, wc0 * basis[t]);
+          if (wc1 != 0.f) atomicAdd(po + kGOffSh + 3 * t + 1, wc1 * basis[t]);
+          if (wc2 != 0.f) atomicAdd(po + kGOffSh + 3 * t + 2, wc2 * basis[t]);
+        }
       }
-      emit(o_eta, (float)deta);
-      emit(o_eta + 1, (float)dtau);
-      emit(o_eta + 2, (float)dop);
     }
     if (rec) {
       T = xm(T, xs(1.0, a));
       cont = T >= P.opt.early_stop;
     }
-    (void)rel;
     return cont;
+  }
+
+  // fp32 gradient of one record (grad.cpp:237-301 and backward_alpha
+  // grad.cpp:16-101) differentiating the fp32 evaluation kf: the bracket
+  // angle terms use delta (theta - a_lo = delta gap / pi), the endpoint
+  // tangents are (-e_y, e_x), and cos/sin(delta) come from the half angle.
+  __device__ __forceinline__ void record_grad_f32(const RasterParams& P, int id, const Geo& g, double rt, double u,
+                                                  double v, double r2, double a, bool lp, const KEvalF& k,
+                                                  double denom, double dpw, double dph, double wb, double dat,
+                                                  double sgn, float (&dcen)[3], float (&drot)[9], float& deta,
+                                                  float& dtau, float& dop, float& ds_lo, float& ds_hi, float& da_lo,
+                                                  float& da_hi, int& lo, int& hi) const {
+    const float wbf = (float)wb, denf = (float)denom, datf = (float)dat, af = (float)a;
+    const float df[3] = {(float)dir[0], (float)dir[1], (float)dir[2]};
+    const float rzf[3] = {(float)g.rz[0], (float)g.rz[1], (float)g.rz[2]};
+    float hv[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) hv[q] = (float)(P.cam.o[q] + rt * dir[q] - g.mu[q]);
+    if (has_dN)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) drot[3 * q + 2] += wbf * (float)(sgn * dN[q]);
+    if (dD != 0) {
+      const float d_rt = wbf * (float)dD;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        dcen[q] += d_rt * rzf[q] / denf;
+        drot[3 * q + 2] += d_rt * (-hv[q] / denf);
+      }
+    }
+    if (a >= 1.0 - 1e-6 - 1e-12) return;  // alpha clamped
+    const float o = (float)P.S.o[id];
+    if (lp) {
+      const float cv = fabsf(denf), sl = (float)P.opt.lowpass_radius;
+      const float dpwf = (float)dpw, dphf = (float)dph;
+      dop += datf * af / o;
+      const float inv = 1.0f / (cv * cv * sl * sl);
+      const float d_dpw = datf * af * (-dpwf * inv), d_dph = datf * af * (-dphf * inv);
+      const float d_cos = datf * af * (dpwf * dpwf + dphf * dphf) * inv / cv;
+      double J[6];
+      projection_jacobian(P.cam, g.mu, J);
+      const float sg = denf < 0 ? -1.0f : 1.0f;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        dcen[q] += -((float)J[q] * d_dpw + (float)J[3 + q] * d_dph);
+        drot[3 * q + 2] += d_cos * sg * df[q];
+      }
+      return;
+    }
+    const float tau = (float)P.S.tau[id];
+    dop += datf * k.P;
+    if (k.center) return;
+    dtau += datf * o *
+            (k.br == 0 ? -2.0f * k.g / ((1.0f + tau) * (1.0f + tau))
+                       : (k.br == 1 ? (2.0f * k.g - 1.0f) / ((1.0f - tau) * (1.0f - tau))
+                                    : (2.0f - 2.0f * k.g) / ((1.0f + tau) * (1.0f + tau))));
+    if (k.clamped) return;
+    const int K = P.S.K;
+    lo = k.lo;
+    hi = k.hi;
+    const size_t bl = (size_t)id * K + lo, bh = (size_t)id * K + hi;
+    const float eta = (float)P.S.eta[id], r2f = (float)r2;
+    const float d_q = datf * o * k.A * (-0.5f * k.g);
+    const float hlo = P.S.hf[bl], hhi = P.S.hf[bh];
+    const float slo = (float)P.S.s[bl], shi = (float)P.S.s[bh];
+    deta += d_q * (k.r1 * k.r1 - r2f * k.inv);
+    const float d_r1 = d_q * eta * 2.0f * k.r1;
+    const float d_r2sq = d_q * (1.0f - eta) * k.inv;
+    const float d_inv = d_q * (1.0f - eta) * r2f;
+    ds_lo = d_inv * (-2.0f * k.ch * k.ch * hlo / slo);
+    ds_hi = d_inv * (-2.0f * k.sh * k.sh * hhi / shi);
+    const float d_delta = -(d_inv * 0.5f * (hlo - hhi)) * (2.0f * k.sh * k.ch);
+    const float d_tfd = d_delta * P.S.piogf[bl];
+    const float dl = k.delta * (float)(1.0 / kPi);
+    da_lo = d_tfd * (dl - 1.0f);
+    da_hi = -d_tfd * dl;
+    const float uf = (float)u, vf = (float)v, r2s = fmaxf(r2f, 1e-24f);
+    const float sa = k.a > 0.f ? 1.f : (k.a < 0.f ? -1.f : 0.f);
+    const float sb = k.b > 0.f ? 1.f : (k.b < 0.f ? -1.f : 0.f);
+    const float elx = (float)P.S.ex[bl], ely = (float)P.S.ey[bl];
+    const float ehx = (float)P.S.ex[bh], ehy = (float)P.S.ey[bh];
+    const float invd = P.S.invdetf[bl];
+    const float du = d_tfd * (-vf / r2s) + 2.0f * d_r2sq * uf + d_r1 * (sa * ehy - sb * ely) * invd;
+    const float dv = d_tfd * (uf / r2s) + 2.0f * d_r2sq * vf + d_r1 * (sb * elx - sa * ehx) * invd;
+    ds_lo += d_r1 * (-sa * k.a / slo);
+    ds_hi += d_r1 * (-sb * k.b / shi);
+    const float cross = ehy * ely + ehx * elx;
+    da_lo += d_r1 * invd * (sa * k.a * cross - sb * k.a * slo * slo);
+    da_hi += d_r1 * invd * (sa * k.b * shi * shi - sb * k.b * cross);
+    // (u, v) and r_t chain to centre and rotation columns (grad.cpp:290-300)
+    const float rxf[3] = {(float)g.rx[0], (float)g.rx[1], (float)g.rx[2]};
+    const float ryf[3] = {(float)g.ry[0], (float)g.ry[1], (float)g.ry[2]};
+    const float drx = df[0] * rxf[0] + df[1] * rxf[1] + df[2] * rxf[2];
+    const float dry = df[0] * ryf[0] + df[1] * ryf[1] + df[2] * ryf[2];
+    const float f = -(du * drx + dv * dry) / denf;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      dcen[q] += du * (rzf[q] * (drx / denf) - rxf[q]) + dv * (rzf[q] * (dry / denf) - ryf[q]);
+      drot[3 * q + 0] += du * hv[q];
+      drot[3 * q + 1] += dv * hv[q];
+      drot[3 * q + 2] += f * hv[q];
+    }
+  }
+
+  // fp64 gradient of one record (grad.cpp:237-301, :16-101) from the fp64
+  // evaluation ev, in the reference's formulation (F64 kernels).
+  __device__ void record_grad_f64(const RasterParams& P, int id, const Geo& g, double rt, double u, double v,
+                                  double a, bool lp, const KEval& ev, double denom, double dpw, double dph, double wb,
+                                  double dat, double sgn, float (&dcen_o)[3], float (&drot_o)[9], float& deta_o,
+                                  float& dtau_o, float& dop_o, float& ds_lo_o, float& ds_hi_o, float& da_lo_o,
+                                  float& da_hi_o, int& lo_o, int& hi_o) const {
+    const int K = P.S.K;
+    const double rz[3] = {g.rz[0], g.rz[1], g.rz[2]};
+    double dcen[3] = {0, 0, 0}, drot[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double deta = 0, dtau = 0, dop = 0, ds_lo = 0, ds_hi = 0, da_lo = 0, da_hi = 0;
+    int lo = 0, hi = 0;
+    if (has_dN)
+      for (int q = 0; q < 3; ++q) drot[3 * q + 2] += wb * sgn * dN[q];
+    if (dD != 0) {
+      const double d_rt = wb * dD;
+      for (int q = 0; q < 3; ++q) {
+        const double h = P.cam.o[q] + rt * dir[q] - g.mu[q];
+        dcen[q] += d_rt * rz[q] / denom;
+        drot[3 * q + 2] += d_rt * (-h / denom);
+      }
+    }
+    const bool alpha_clamped = a >= 1.0 - 1e-6 - 1e-12;
+    const double o = P.S.o[id];
+    if (!alpha_clamped && lp) {
+      const double cv = fabs(denom), sl = P.opt.lowpass_radius;
+      dop += dat * a / o;
+      const double inv = 1.0 / (cv * cv * sl * sl);
+      const double d_dpw = dat * a * (-dpw * inv);
+      const double d_dph = dat * a * (-dph * inv);
+      const double d_cos = dat * a * (dpw * dpw + dph * dph) * inv / cv;
+      double J[6];
+      projection_jacobian(P.cam, g.mu, J);
+      for (int q = 0; q < 3; ++q) dcen[q] += -(J[q] * d_dpw + J[3 + q] * d_dph);
+      const double sg = denom < 0 ? -1.0 : 1.0;
+      for (int q = 0; q < 3; ++q) drot[3 * q + 2] += d_cos * sg * dir[q];
+    } else if (!alpha_clamped) {
+      const double tau = P.S.tau[id];
+      dop += dat * sharpen(ev.g, tau);
+      if (!ev.center) {
+        const int br = sharpen_branch(ev.g, tau);
+        dtau += dat * o * sharpen_dtau(br, ev.g, tau);
+        if (!ev.clamped) {
+          const double d_g = dat * o * sharpen_slope(br, tau);
+          const double d_q = d_g * (-0.5 * ev.g);
+          lo = ev.lo;
+          hi = ev.hi;
+          const double* s = P.S.s + (size_t)id * K;
+          const double* th = P.S.th + (size_t)id * K;
+          const double slo = s[lo], shi = s[hi], eta = P.S.eta[id];
+          deta += d_q * (ev.r1 * ev.r1 - ev.r2 * ev.inv_sbar);
+          const double d_r1 = d_q * eta * 2.0 * ev.r1;
+          const double d_r2sq = d_q * (1.0 - eta) * ev.inv_sbar;
+          const double d_inv = d_q * (1.0 - eta) * ev.r2;
+          const double c = cos(ev.delta);
+          ds_lo = d_inv * (-(1.0 + c) / (slo * slo * slo));
+          ds_hi = d_inv * (-(1.0 - c) / (shi * shi * shi));
+          const double d_c = d_inv * (0.5 / (slo * slo) - 0.5 / (shi * shi));
+          const double d_delta = d_c * (-sin(ev.delta));
+          double alo = th[lo], ahi = th[hi], theta = ev.theta;
+          if (hi == 0) {
+            alo -= kTwoPi;
+            if (theta > th[K - 1]) theta -= kTwoPi;
+          }
+          const double gap = ahi - alo;
+          const double d_tfd = d_delta * kPi / gap;
+          da_lo = d_delta * kPi * (theta - ahi) / (gap * gap);
+          da_hi = d_delta * (-kPi) * (theta - alo) / (gap * gap);
+          const double r2s = dmax(ev.r2, 1e-24);
+          double du = d_tfd * (-v / r2s);
+          double dv = d_tfd * (u / r2s);
+          du += d_r2sq * 2.0 * u;
+          dv += d_r2sq * 2.0 * v;
+          const double sa = ev.a > 0 ? 1 : (ev.a < 0 ? -1 : 0);
+          const double sb = ev.b > 0 ? 1 : (ev.b < 0 ? -1 : 0);
+          const double elx = P.S.ex[(size_t)id * K + lo], ely = P.S.ey[(size_t)id * K + lo];
+          const double ehx = P.S.ex[(size_t)id * K + hi], ehy = P.S.ey[(size_t)id * K + hi];
+          const double det = P.S.det[(size_t)id * K + lo];
+          du += d_r1 * (sa * (ehy / det) + sb * (-ely / det));
+          dv += d_r1 * (sa * (-ehx / det) + sb * (elx / det));
+          const double ca = cos(th[lo]), sa_lo = sin(th[lo]);
+          const double cb = cos(th[hi]), sb_hi = sin(th[hi]);
+          ds_lo += d_r1 * (-sa * ev.a / slo);
+          ds_hi += d_r1 * (-sb * ev.b / shi);
+          const double tlx = -slo * sa_lo, tly = slo * ca, thx = -shi * sb_hi, thy = shi * cb;
+          const double na = -ev.a, nb = -ev.b;
+          da_lo += d_r1 * (sa * (na * ((ehy * tlx - ehx * tly) / det)) + sb * (na * ((-ely * tlx + elx * tly) / det)));
+          da_hi += d_r1 * (sa * (nb * ((ehy * thx - ehx * thy) / det)) + sb * (nb * ((-ely * thx + elx * thy) / det)));
+          const double hh[3] = {P.cam.o[0] + rt * dir[0] - g.mu[0], P.cam.o[1] + rt * dir[1] - g.mu[1],
+                                P.cam.o[2] + rt * dir[2] - g.mu[2]};
+          const double drx = dir[0] * g.rx[0] + dir[1] * g.rx[1] + dir[2] * g.rx[2];
+          const double dry = dir[0] * g.ry[0] + dir[1] * g.ry[1] + dir[2] * g.ry[2];
+          const double f = -(du * drx + dv * dry) / denom;
+          for (int q = 0; q < 3; ++q) {
+            dcen[q] += du * (rz[q] * (drx / denom) - g.rx[q]) + dv * (rz[q] * (dry / denom) - g.ry[q]);
+            drot[3 * q + 0] += du * hh[q];
+            drot[3 * q + 1] += dv * hh[q];
+            drot[3 * q + 2] += f * hh[q];
+          }
+        }
+      }
+    }
+    for (int q = 0; q < 3; ++q) dcen_o[q] = (float)dcen[q];
+    for (int q = 0; q < 9; ++q) drot_o[q] = (float)drot[q];
+    deta_o = (float)deta;
+    dtau_o = (float)dtau;
+    dop_o = (float)dop;
+    ds_lo_o = (float)ds_lo;
+    ds_hi_o = (float)ds_hi;
+    da_lo_o = (float)da_lo;
+    da_hi_o = (float)da_hi;
+    lo_o = lo;
+    hi_o = hi;
   }
 
   // SH colour (geometry.cpp:126-138) in fp32, before the clamp at zero.
@@ -944,35 +1018,11 @@ __global__ void __launch_bounds__(256, DRK_RASTER_MIN_BLOCKS) k_raster(RasterPar
 // Backward rasterizer: re-streams the forward decisions with warp-uniform
 // control flow so that gradient components can be reduced across lanes
 // (Pixel::composite_warp).  MODE / F64 as in k_raster.
-// Flush the shared-memory gradient slots to HBM (fp64 atomics) and clear
-// them; called by the whole CTA between __syncthreads.
-__device__ __forceinline__ void flush_grad_slots(const RasterParams& P, int* slot_id, float* slot_val) {
-  const int G = P.G;
-  for (int idx = threadIdx.x; idx < kGradSlots * G; idx += blockDim.x) {
-    const int s = idx / G, c = idx - s * G;
-    const int id = slot_id[s];
-    float* v = slot_val + (size_t)s * kGradSlotStride + c;
-    if (id >= 0 && *v != 0.f) atomicAdd(P.gact + (size_t)id * G + c, *v);
-    *v = 0.f;
-  }
-  __syncthreads();
-  if (threadIdx.x < kGradSlots) slot_id[threadIdx.x] = -1;
-  __syncthreads();
-}
-
 template <int MODE, bool F64>
 __global__ void __launch_bounds__(256, DRK_BWD_MIN_BLOCKS) k_raster_bwd(RasterParams P) {
   __shared__ int s_id[256];
   __shared__ double s_num[256], s_r0[256], s_r1[256], s_r2[256];
-  __shared__ int slot_id_s[kGradSlots];
-  __shared__ float slot_val_s[kUseGradSlots ? kGradSlots * kGradSlotStride : 1];
-  int* slot_id = kUseGradSlots ? slot_id_s : nullptr;
-  float* slot_val = kUseGradSlots ? slot_val_s : nullptr;
   const unsigned FULL = 0xffffffffu;
-  if (kUseGradSlots) {
-    for (int i = threadIdx.x; i < kGradSlots * kGradSlotStride; i += blockDim.x) slot_val_s[i] = 0.f;
-    if (threadIdx.x < kGradSlots) slot_id_s[threadIdx.x] = -1;
-  }
   const int tile = blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
@@ -993,26 +1043,48 @@ __global__ void __launch_bounds__(256, DRK_BWD_MIN_BLOCKS) k_raster_bwd(RasterPa
   int csz = 0;
   const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
   const double eps = P.opt.grazing_eps;
-  for (long long b0 = beg; b0 < end; b0 += 256) {
-    __syncthreads();
-    const long long j = b0 + threadIdx.x;
-    if (j < end) {
-      const int id = (int)(P.pv[j] & 0xffffffffull);
-      const Geo& g = P.geo[id];
-      s_id[threadIdx.x] = id;
-      s_num[threadIdx.x] = g.num;
-      s_r0[threadIdx.x] = g.rz[0];
-      s_r1[threadIdx.x] = g.rz[1];
-      s_r2[threadIdx.x] = g.rz[2];
+  // Batches of 256 candidates, then (MODE 0) one drain pass over the cache
+  // (raster.cpp:410-414) through the same call site, so composite_warp is
+  // instantiated once.
+  const long long nb = (end - beg + 255) / 256;
+  for (long long bi = 0; bi <= nb; ++bi) {
+    const bool drain = bi == nb;
+    if (drain && MODE != 0) break;
+    const long long b0 = beg + bi * 256;
+    int cnt = kCacheCap;
+    if (!drain) {
+      __syncthreads();
+      const long long j = b0 + threadIdx.x;
+      if (j < end) {
+        const int id = (int)(P.pv[j] & 0xffffffffull);
+        const Geo& g = P.geo[id];
+        s_id[threadIdx.x] = id;
+        s_num[threadIdx.x] = g.num;
+        s_r0[threadIdx.x] = g.rz[0];
+        s_r1[threadIdx.x] = g.rz[1];
+        s_r2[threadIdx.x] = g.rz[2];
+      }
+      __syncthreads();
+      cnt = (int)min((long long)256, end - b0);
     }
-    __syncthreads();
-    const int cnt = (int)min((long long)256, end - b0);
     if (__any_sync(FULL, !done)) {
       for (int c = 0; c < cnt; ++c) {
         bool want = false;
         double prt = 0;
         int pid = -1;
-        if (!done) {
+        if (drain) {
+          if (!done && csz > 0) {
+            want = true;
+            prt = cd[0];
+            pid = ci[0];
+#pragma unroll
+            for (int q = 0; q < kCacheCap - 1; ++q) {
+              cd[q] = cd[q + 1];
+              ci[q] = ci[q + 1];
+            }
+            --csz;
+          }
+        } else if (!done) {
           const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], s_r0[c], s_r1[c], s_r2[c]);
           if (fabs(denom) >= eps) {
             const double rt = s_num[c] / denom;
@@ -1067,38 +1139,12 @@ __global__ void __launch_bounds__(256, DRK_BWD_MIN_BLOCKS) k_raster_bwd(RasterPa
           }
         }
         if (__any_sync(FULL, want)) {
-          const bool cont = px.composite_warp(P, want, prt, pid, slot_id, slot_val);
+          const bool cont = px.composite_warp(P, want, prt, pid);
           if (want && !cont) done = true;
         }
       }
     }
-    const int busy = __syncthreads_count(!done);
-    if (kUseGradSlots) flush_grad_slots(P, slot_id, slot_val);
-    if (busy == 0) break;
-  }
-  if (MODE == 0) {
-    while (true) {
-      const bool want = !done && csz > 0;
-      if (!__any_sync(FULL, want)) break;
-      double prt = 0;
-      int pid = -1;
-      if (want) {
-        prt = cd[0];
-        pid = ci[0];
-#pragma unroll
-        for (int q = 0; q < kCacheCap - 1; ++q) {
-          cd[q] = cd[q + 1];
-          ci[q] = ci[q + 1];
-        }
-        --csz;
-      }
-      const bool cont = px.composite_warp(P, want, prt, pid, slot_id, slot_val);
-      if (want && !cont) done = true;
-    }
-  }
-  if (kUseGradSlots) {
-    __syncthreads();
-    flush_grad_slots(P, slot_id, slot_val);
+    if (drain || __syncthreads_count(!done) == 0) break;
   }
   if (active && px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
   if (px.n_rej1) atomicAdd(&P.counters[C_BWD_WARPSTEPS], (unsigned long long)px.n_rej1);
@@ -1706,7 +1752,7 @@ __global__ void k_act_bwd(int n, int K, int terms, const float* __restrict__ raw
   }
   const double dd = qh[0] * dqh[0] + qh[1] * dqh[1] + qh[2] * dqh[2] + qh[3] * dqh[3];
   for (int m = 0; m < 4; ++m) out[3 + m] = (dqh[m] - qh[m] * dd) / qn;
-  for (int j = 0; j < K; ++j) out[7 + j] = g[12 + j] * exp(RAW(7 + j));
+  for (int j = 0; j < K; ++j) out[7 + j] = g[kGOffSc + j] * exp(RAW(7 + j));
   // angle_activation_jacobian (core.cpp:110-131), out = J^T d_angles
   const double residual = 1.0 / (K - 2);
   double dstep[kMaxK], cum[kMaxK], total = 0;
@@ -1723,16 +1769,16 @@ __global__ void k_act_bwd(int n, int K, int terms, const float* __restrict__ raw
     for (int r = 0; r < K; ++r) {
       const double ind = (c <= r) ? 1.0 : 0.0;
       const double jac = (r == K - 1) ? 0.0 : kTwoPi / total * (ind - cum[r] / total) * dstep[c];
-      acc = (r == 0) ? jac * g[12 + K + r] : acc + jac * g[12 + K + r];
+      acc = (r == 0) ? jac * g[kGOffAn + r] : acc + jac * g[kGOffAn + r];
     }
     out[7 + K + c] = acc;
   }
   const double eta = sigmoid(RAW(7 + 2 * K));
-  out[7 + 2 * K] = g[12 + 2 * K] * eta * (1.0 - eta);
+  out[7 + 2 * K] = g[kGOffEta] * eta * (1.0 - eta);
   const double st = sigmoid(RAW(8 + 2 * K));
-  out[8 + 2 * K] = g[13 + 2 * K] * (kTauHigh - kTauLow) * st * (1.0 - st);
+  out[8 + 2 * K] = g[kGOffTau] * (kTauHigh - kTauLow) * st * (1.0 - st);
   const double o = sigmoid(RAW(9 + 2 * K));
-  out[9 + 2 * K] = g[14 + 2 * K] * o * (1.0 - o);
+  out[9 + 2 * K] = g[kGOffOp] * o * (1.0 - o);
 #undef RAW
   const int S0 = 10 + 2 * K;
   for (int j = 0; j < S0; ++j) {
@@ -1741,7 +1787,7 @@ __global__ void k_act_bwd(int n, int K, int terms, const float* __restrict__ raw
   }
   for (int j = 0; j < 3 * terms; ++j) {
     float* dst = grad_raw + (size_t)(S0 + j) * n + i;
-    const float val = (float)g[15 + 2 * K + j];
+    const float val = (float)g[kGOffSh + j];
     *dst = accumulate ? *dst + val : val;
   }
 }
