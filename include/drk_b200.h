@@ -76,7 +76,7 @@ typedef struct drk_options {
   int32_t record_replay;            /* default 0 */
   int32_t fp64_alpha;               /* default 0; 1 = every alpha in fp64 (reference-precision mode:
                                        identical arithmetic across cache / list / exact-sort modes) */
-  int32_t reserved_;
+  int32_t raster_kernel;            /* 0 = auto (fp32 interval kernel where eligible), 1 = legacy fp64-depth kernel */
 } drk_options;
 
 /* Activated primitives (drk::DrkPrimitive, reference types.hpp:77-98), all
@@ -122,6 +122,8 @@ typedef struct drk_stats {
   int64_t reject_radius;     /* pops rejected by the isotropic alpha_min support radius */
   int64_t reject_bracket;    /* pops rejected by the in-bracket lower bound of the exponent */
   int64_t fp64_evals;        /* pops re-evaluated in fp64 (decision inside the fp32 error bound) */
+  int64_t ambiguous;         /* cache steps whose fp32 depth intervals overlapped (resolved in fp64) */
+  int64_t ring_miss;         /* pops of entries older than the shared-memory ring (re-staged from HBM) */
 } drk_stats;
 
 typedef struct drk_ctx drk_ctx;
@@ -138,6 +140,11 @@ int drk_get_stats(const drk_ctx* ctx, drk_stats* out);
 int drk_set_stream(drk_ctx* ctx, void* cuda_stream);
 /* Enables per-stage CUDA-event timing (drk_stats.stage_ms). */
 int drk_set_timing(drk_ctx* ctx, int enabled);
+/* Validation of the fast forward kernel: while enabled, every fp32 alpha is
+ * also evaluated in fp64; drk_get_validation returns max |a32 - a64| / bound
+ * (must stay below 1) and max |a32 - a64| since validation was enabled. */
+int drk_set_validation(drk_ctx* ctx, int enabled);
+int drk_get_validation(drk_ctx* ctx, double* out2);
 /* Measured FP32 FFMA throughput of this device (TFLOP/s), for rooflines. */
 int drk_measure_fp32_peak(drk_ctx* ctx, double* tflops);
 

@@ -52,7 +52,7 @@ class Options_(C.Structure):
                 ("background", C.c_double * 3), ("early_stop_transmittance", C.c_double),
                 ("sh_degree", C.c_int32), ("use_cache", C.c_int32), ("exact_sort", C.c_int32),
                 ("presort", C.c_int32), ("threads", C.c_int32), ("record_replay", C.c_int32),
-                ("fp64_alpha", C.c_int32), ("reserved_", C.c_int32)]
+                ("fp64_alpha", C.c_int32), ("raster_kernel", C.c_int32)]
 
 
 class Prims_(C.Structure):
@@ -71,7 +71,8 @@ class Stats_(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("primitives", "pairs", "streamed", "popped", "composited", "near_ties",
                                           "poly_overflow", "replay_overflow", "fp64_pixels", "launches")] + \
         [("stage_ms", C.c_double * 8), ("bwd_warp_steps", C.c_int64), ("bwd_lead_records", C.c_int64),
-         ("reject_radius", C.c_int64), ("reject_bracket", C.c_int64), ("fp64_evals", C.c_int64)]
+         ("reject_radius", C.c_int64), ("reject_bracket", C.c_int64), ("fp64_evals", C.c_int64),
+         ("ambiguous", C.c_int64), ("ring_miss", C.c_int64)]
 
 
 class AdamConfig_(C.Structure):
@@ -95,6 +96,8 @@ SIGNATURES = {
     "drk_set_stream": (C.c_int, [_P, _P]),
     "drk_set_timing": (C.c_int, [_P, C.c_int]),
     "drk_measure_fp32_peak": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "drk_set_validation": (C.c_int, [_P, C.c_int]),
+    "drk_get_validation": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "drk_activate": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(Prims_)]),
     "drk_forward": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(Camera_), C.POINTER(Options_),
                               _P, _P, _P, _P]),

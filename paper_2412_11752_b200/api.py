@@ -52,6 +52,9 @@ class RenderOptions:
     exact_sort: bool = False
     presort: PresortMode = PresortMode.NearestDepth
     early_stop_transmittance: float = 1e-4
+    # B200 extension (not in the reference): 0 = fp32 interval kernel where
+    # eligible (SortCache mode, K = 8), 1 = legacy fp64-depth kernel
+    raster_kernel: int = 0
 
 
 @dataclass
@@ -172,6 +175,7 @@ def _options(opt: RenderOptions, replay_cap: int = 0) -> _lib.Options_:
     o.early_stop_transmittance = opt.early_stop_transmittance
     o.sh_degree, o.use_cache, o.exact_sort = opt.sh_degree, int(opt.use_cache), int(opt.exact_sort)
     o.presort, o.threads, o.record_replay = int(opt.presort), int(opt.threads), int(replay_cap)
+    o.raster_kernel = int(opt.raster_kernel)
     return o
 
 
@@ -337,6 +341,16 @@ class Rasterizer:
 
     def set_timing(self, enabled: bool = True):
         self._check(_lib.lib().drk_set_timing(self._h, int(enabled)))
+
+    def set_validation(self, enabled: bool = True):
+        """Fast forward kernel: check every fp32 alpha against its fp64 value (slow; tests only)."""
+        self._check(_lib.lib().drk_set_validation(self._h, int(enabled)))
+
+    def validation(self) -> tuple[float, float]:
+        """(max |a32 - a64| / error bound, max |a32 - a64|) since set_validation(True)."""
+        v = (C.c_double * 2)()
+        self._check(_lib.lib().drk_get_validation(self._h, v))
+        return float(v[0]), float(v[1])
 
     def fp32_peak_tflops(self) -> float:
         v = C.c_double(0)

@@ -109,6 +109,7 @@ static OptD make_opt(const drk_options* o, int terms) {
   d.presort = o->presort;
   d.record_replay = o->record_replay;
   d.fp64_alpha = o->fp64_alpha;
+  d.raster_kernel = o->raster_kernel;
   const int t = (o->sh_degree + 1) * (o->sh_degree + 1);
   d.terms_active = t < terms ? t : terms;
   return d;
@@ -130,6 +131,7 @@ static RasterParams raster_params(drk_ctx* c) {
   // pixels flagged for the fp64 re-render (list written by the fp32 pass)
   P.redo_list = static_cast<int*>(c->redo.p);
   P.redo_count = reinterpret_cast<unsigned int*>(ensure<unsigned long long>(c->redo_cnt, 1));
+  P.shrec = A.rec;
   return P;
 }
 
@@ -270,10 +272,16 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   // per-pixel state / replay
   double* pxstate = ensure<double>(c->pxstate, 8 * (size_t)n_pix);
   unsigned char* pxflag = ensure<unsigned char>(c->pxflag, (size_t)n_pix);
+  int* pxstop = ensure<int>(c->pxstop, (size_t)n_pix);
   int* redo = ensure<int>(c->redo, (size_t)n_pix + 1);
-  if (!pxstate || !pxflag || !redo) return set_error(c, DRK_ERR_OOM, "pixel state");
+  if (!pxstate || !pxflag || !redo || !pxstop) return set_error(c, DRK_ERR_OOM, "pixel state");
   RasterParams P = raster_params(c);
   P.pxflag = pxflag;
+  P.pxstop = pxstop;
+  if (c->validate_fast) {
+    P.vstat = ensure<unsigned long long>(c->vstat, 2);
+    if (!P.vstat) return set_error(c, DRK_ERR_OOM, "validation buffer");
+  }
   P.color = color;
   P.depth = depth;
   P.normal = normal;
@@ -304,6 +312,8 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   c->stats.reject_radius = (int64_t)h[C_REJECT_RADIUS];
   c->stats.reject_bracket = (int64_t)h[C_REJECT_BRACKET];
   c->stats.fp64_evals = (int64_t)h[C_FP64_EVALS];
+  c->stats.ambiguous = (int64_t)h[C_AMBIGUOUS];
+  c->stats.ring_miss = (int64_t)h[C_RING_MISS];
   if (h[C_ERR_DEGEN_BASIS]) return set_error(c, DRK_ERR_DEGENERATE_BASIS, "adjacent endpoints nearly collinear");
   c->has_fwd = true;
   return DRK_OK;
@@ -326,6 +336,7 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   RasterParams P = raster_params(c);
   P.pxstate = static_cast<double*>(c->pxstate.p);
   P.pxflag = static_cast<unsigned char*>(c->pxflag.p);
+  P.pxstop = static_cast<int*>(c->pxstop.p);
   if (fg) {
     P.dC = fg->d_color;
     P.dD = fg->d_depth;
@@ -390,7 +401,7 @@ void drk_default_options(drk_options* o) {
   o->threads = 1;
   o->record_replay = 0;
   o->fp64_alpha = 0;
-  o->reserved_ = 0;
+  o->raster_kernel = 0;
 }
 
 const char* drk_status_string(int s) {
@@ -436,6 +447,30 @@ int drk_set_timing(drk_ctx* c, int enabled) {
   return DRK_OK;
 }
 
+int drk_set_validation(drk_ctx* c, int enabled) {
+  if (!c) return DRK_ERR_INVALID_ARG;
+  c->validate_fast = enabled != 0;
+  if (c->validate_fast) {
+    cudaSetDevice(c->device);
+    unsigned long long* v = ensure<unsigned long long>(c->vstat, 2);
+    if (!v) return set_error(c, DRK_ERR_OOM, "validation buffer");
+    cudaMemsetAsync(v, 0, 2 * sizeof(unsigned long long), c->stream);
+  }
+  return cuda_check(c, cudaGetLastError(), "validation");
+}
+
+int drk_get_validation(drk_ctx* c, double* out) {
+  if (!c || !out) return DRK_ERR_INVALID_ARG;
+  out[0] = out[1] = 0;
+  if (!c->vstat.p) return DRK_OK;
+  unsigned long long h[2];
+  cudaMemcpyAsync(h, c->vstat.p, sizeof h, cudaMemcpyDeviceToHost, c->stream);
+  if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "validation")) return st;
+  std::memcpy(&out[0], &h[0], 8);
+  std::memcpy(&out[1], &h[1], 8);
+  return DRK_OK;
+}
+
 int drk_measure_fp32_peak(drk_ctx* c, double* tflops) {
   if (!c || !tflops) return DRK_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
@@ -449,7 +484,7 @@ void drk_ctx_destroy(drk_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
                     &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
-                    &c->a_psif, &c->pxflag, &c->redo, &c->redo_cnt, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->rowcnt,
+                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->rowcnt,
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->pk2, &c->pv2,
                     &c->hist, &c->sortoff, &c->tilecnt, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,

@@ -55,6 +55,8 @@ enum Counter {
   C_REJECT_RADIUS,     // pops rejected by the isotropic support radius
   C_REJECT_BRACKET,    // pops rejected by the in-bracket Q lower bound
   C_FP64_EVALS,        // pops re-evaluated in fp64 (decision within the fp32 bound)
+  C_AMBIGUOUS,         // fast kernel: cache steps with overlapping depth intervals
+  C_RING_MISS,         // fast kernel: pops re-staged from HBM (older than the ring)
   C_COUNT
 };
 
@@ -72,7 +74,7 @@ struct OptD {
   double bg[3];
   double early_stop;
   double lp_pad;  // raster.cpp:128-129
-  int sh_degree, use_cache, exact_sort, presort, record_replay, terms_active, fp64_alpha;
+  int sh_degree, use_cache, exact_sort, presort, record_replay, terms_active, fp64_alpha, raster_kernel;
 };
 
 __host__ __device__ inline double dmin(double a, double b) { return (b < a) ? b : a; }  // std::min

@@ -51,6 +51,7 @@ struct Activated {
   const float* sh;  // n x terms x 3 (AoS)
   const double *ex, *ey, *det;
   const float *thf, *invdetf, *piogf, *hf, *psif;
+  const float* rec;  // fast-kernel shape records (K == 8), else nullptr
   int n, K, terms;
 };
 
@@ -78,9 +79,15 @@ struct RasterParams {
   unsigned char* pxflag;  // 1 = pixel needs the fp64 re-render (uncertain termination)
   int* redo_list;         // flagged pixel indices (forward fp32 pass appends)
   unsigned int* redo_count;
+  const float* shrec;     // fast kernel: per-primitive fp32 shape records (K == 8)
+  int* pxstop;            // composites until saturation per pixel (INT_MAX: never), written by the forward
+  unsigned long long* vstat;  // fast kernel validation: max |a32 - a64| / bound, max |a32 - a64| (double bits)
 };
 
 void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s, cudaEvent_t mid = nullptr);
+bool raster_fast_eligible(const RasterParams& P);
+void launch_raster_fast(const RasterParams& P, int n_tiles, bool validate, cudaStream_t s);
+void launch_shape_rec(const ShapeView& S, int n, float* rec, cudaStream_t s);
 double measure_fp32_peak(cudaStream_t s);
 void launch_backward_serial(const RasterParams& P, cudaStream_t s);
 
@@ -94,7 +101,7 @@ struct drk_ctx {
 
   // activated primitives owned by the context (raw path)
   drk::DevBuf a_mu, a_rot, a_s, a_th, a_eta, a_tau, a_o, a_sh, a_ex, a_ey, a_det;
-  drk::DevBuf a_thf, a_invdetf, a_piogf, a_hf, a_psif, pxflag, redo, redo_cnt;
+  drk::DevBuf a_thf, a_invdetf, a_piogf, a_hf, a_psif, a_rec, pxflag, pxstop, redo, redo_cnt, vstat;
   drk::Activated act{};
 
   // per view
@@ -107,6 +114,7 @@ struct drk_ctx {
 
   // stage timing
   bool timing = false;
+  bool validate_fast = false;  // fast kernel: check every fp32 alpha against fp64 (drk_validate_fast)
   cudaEvent_t ev[10] = {};
   long long launch_base = 0;
 

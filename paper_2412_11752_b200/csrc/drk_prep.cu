@@ -627,6 +627,14 @@ static int launch_shape_consts(drk_ctx* c, int n, int K) {
                                                    const_cast<float*>(A.psif));
     DRK_COUNT_LAUNCH();
   }
+  A.rec = nullptr;
+  if (K == 8) {
+    // AoS fp32 records of the fast forward kernel (drk_raster_fast.cu)
+    A.rec = ensure<float>(c->a_rec, (size_t)88 * n);
+    if (!A.rec) return set_error(c, DRK_ERR_OOM, "shape records");
+    const ShapeView S{A.s, A.th, A.ex, A.ey, A.det, A.eta, A.tau, A.o, A.thf, A.invdetf, A.piogf, A.hf, A.psif, K};
+    launch_shape_rec(S, n, const_cast<float*>(A.rec), c->stream);
+  }
   return cuda_check(c, cudaGetLastError(), "shape");
 }
 

@@ -52,7 +52,7 @@ struct Pixel {
   bool has_dN;
   long long n_pop, n_comp;
   unsigned n_rej1, n_rej2, n_f64;
-  int pix, n_rec;
+  int pix, n_rec, stop;
   bool err;
 
   __device__ void init(const RasterParams& P, int x, int y) {
@@ -69,6 +69,7 @@ struct Pixel {
     uncertain = false;
     n_pop = n_comp = 0;
     n_rec = 0;
+    stop = 0x7fffffff;
     err = false;
     pix = y * P.cam.W + x;
   }
@@ -223,7 +224,9 @@ struct Pixel {
       E += rel * __fdividef(af, 1.0f - af) + 1e-15f;
       if (fabs(T - P.opt.early_stop) <= T * (double)E) uncertain = true;
     }
-    return T >= P.opt.early_stop;
+    if (T >= P.opt.early_stop) return true;
+    stop = (int)n_comp;
+    return false;
   }
 
   __device__ void backward_record(const RasterParams& P, int id, const Geo& g, double rt, double u, double v,
@@ -576,7 +579,9 @@ struct Pixel {
     }
     if (rec) {
       T = xm(T, xs(1.0, a));
-      cont = T >= P.opt.early_stop;
+      // the fp32 forward's termination (its count is exact for unflagged
+      // pixels); fp64 kernels decide on their own exact T
+      cont = (!F64 && P.pxstop) ? n_comp < P.pxstop[pix] : T >= P.opt.early_stop;
     }
     return cont;
   }
@@ -857,6 +862,7 @@ struct Pixel {
     }
     if (P.depth) P.depth[p] = (float)D;
     if (P.alpha) P.alpha[p] = (float)A;
+    if (!F64 && P.pxstop) P.pxstop[p] = stop;
     if (P.pxstate) {
       double* st = P.pxstate + 8 * p;
       st[0] = c0;
@@ -1608,6 +1614,7 @@ void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s,
   if (!bwd) cudaMemsetAsync(P.redo_count, 0, sizeof(unsigned), s);
   if (P.opt.use_cache) {
     if (bwd) k_raster_bwd<0, false><<<n_tiles, 256, 0, s>>>(P);
+    else if (P.opt.raster_kernel == 0 && raster_fast_eligible(P)) launch_raster_fast(P, n_tiles, P.vstat != nullptr, s);
     else k_raster<0, false, false><<<n_tiles, 256, 0, s>>>(P);
     if (mid) cudaEventRecord(mid, s);
     if (bwd) k_raster_pixels_warp<0, true><<<redo_blocks, 128, 0, s>>>(P);

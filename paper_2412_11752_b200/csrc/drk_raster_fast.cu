@@ -1,0 +1,724 @@
+// K4 fast path: forward rasterizer for the SortCache mode (reference
+// raster.cpp:267-430) with every per-candidate quantity in fp32 and exact
+// fp64 fallbacks wherever a discrete decision falls inside its error bound.
+//
+// One CTA per 16x16 tile, one thread per pixel.  Tile-list entries are staged
+// 256 at a time into a 512-entry shared-memory ring (the current and the
+// previous batch) as an 84-byte fp32 record computed once per (entry, tile)
+// in fp64 (stage_record):
+//
+//   r0 = (R_z, R_z . d0)                     ray-plane denominator at the tile ray d0
+//   r1 = (G_u, N_u(d0)), r2 = (G_v, N_v(d0)) tangent-coordinate numerators
+//   r3 = (num, e_z, e_N, r2max)              r_t numerator and error scales
+//   r4 = (projected centre - tile origin, dp2max, f_vis^2)
+//
+// With a = o - mu and the primitive frame (R_x, R_y, R_z), the reference's
+// r_t = num / (d . R_z) and (u, v) = R_{x,y} . (a + r_t d) (geometry.cpp:40-52)
+// are u = N_u(d) / (d . R_z), v = N_v(d) / (d . R_z) with
+// N_u(d) = (R_x . a)(R_z . d) - (R_z . a)(R_x . d) linear in d.  Expanding
+// around the tile ray d0 (d = d0 + dd, |dd| <= ~8 px / f) leaves the
+// cancellation in the fp64 staging and gives u, v, r_t with ~1e-7 relative
+// error from 9 FMAs and one reciprocal per (pixel, candidate).
+//
+// The SortCache holds fp32 depth intervals [lo, hi] that contain the exact
+// fp64 r_t; a comparison whose intervals overlap is resolved exactly
+// (exact_rt: the reference's op order in fp64), so the pop sequence is the
+// reference's.  The grazing / behind tests are exact the same way.  Alpha
+// (core.cpp:148-265) is evaluated in fp32 with a relative error bound that
+// includes the tangent-coordinate error; alpha_min / low-pass / clamp
+// decisions inside the bound are re-evaluated in fp64 (pop_f64), and pixels
+// whose early-stop decision falls inside the accumulated transmittance bound
+// are flagged for the fp64 re-render (k_raster_pixels_warp), as in k_raster.
+//
+// This translation unit is compiled with --fmad=true; the exact fp64 paths use
+// explicitly rounded intrinsics (__dmul_rn / __dadd_rn).
+#include <climits>
+
+#include "drk_internal.h"
+
+namespace drk {
+
+constexpr int kRing = 512;
+constexpr int kBatch = 256;
+constexpr int kRecHdr = 24;
+constexpr int kRecStride = kRecHdr + 8 * 8;  // K == 8
+
+// ---------------------------------------------------------------------------
+// Per-primitive fp32 shape record (view independent, K == 8), AoS:
+//   [0, 8)   theta_k
+//   [8, 12)  sharpen point-slope constants (g1, g2, A0, A1)
+//   [12, 16) (A2, Psi(g1), Psi(g2), opacity)
+//   [16]     eta
+//   [24 + 8k, 32 + 8k) bracket (k, k+1 mod K): e_lo (x, y), e_hi (x, y),
+//            1/det (NaN when |det| < 1e-12, core.cpp:191), pi/gap, 1/s_lo^2, 1/s_hi^2
+// ---------------------------------------------------------------------------
+__global__ void k_shape_rec(int n, ShapeView S, float* __restrict__ rec) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int K = 8;
+  float* r = rec + (size_t)kRecStride * i;
+  const size_t b = (size_t)K * i;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = (float)S.th[b + k];
+  const float* q = S.psif + 12 * (size_t)i;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[8 + k] = q[k];
+  r[16] = (float)S.eta[i];
+#pragma unroll
+  for (int k = 17; k < kRecHdr; ++k) r[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int h = (k + 1) & 7;
+    float* br = r + kRecHdr + 8 * k;
+    br[0] = (float)S.ex[b + k];
+    br[1] = (float)S.ey[b + k];
+    br[2] = (float)S.ex[b + h];
+    br[3] = (float)S.ey[b + h];
+    const double det = S.det[b + k];
+    br[4] = fabs(det) < 1e-12 ? __int_as_float(0x7fc00000) : (float)(1.0 / det);
+    br[5] = S.piogf[b + k];
+    br[6] = S.hf[b + k];
+    br[7] = S.hf[b + h];
+  }
+}
+
+void launch_shape_rec(const ShapeView& S, int n, float* rec, cudaStream_t s) {
+  if (n > 0 && S.K == 8) {
+    k_shape_rec<<<(n + 127) / 128, 128, 0, s>>>(n, S, rec);
+    DRK_COUNT_LAUNCH();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp32 helpers with known error
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// atan2 in (-pi, pi]; |error| <= 2.5e-7 |result| + 1.5e-7 (minimax polynomial
+// for atan on [0, 1]: relative error 8.8e-8 measured in fp32 Horner form).
+__device__ __forceinline__ float atan2_fast(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  const float t = mx > 0.f ? __fdividef(mn, mx) : 0.f;
+  const float s = t * t;
+  float r = 2.920356113e-03f;
+  r = fmaf(r, s, -1.636656933e-02f);
+  r = fmaf(r, s, 4.320959747e-02f);
+  r = fmaf(r, s, -7.552013546e-02f);
+  r = fmaf(r, s, 1.066590250e-01f);
+  r = fmaf(r, s, -1.421102583e-01f);
+  r = fmaf(r, s, 1.999376863e-01f);
+  r = fmaf(r, s, -3.333315253e-01f);
+  r = r * s;
+  r = fmaf(r, t, t);
+  if (ay > ax) r = 1.57079637f - r;
+  if (x < 0.f) r = 3.14159274f - r;
+  return copysignf(r, y);
+}
+
+// ---------------------------------------------------------------------------
+// Staging (fp64, once per (entry, tile))
+// ---------------------------------------------------------------------------
+struct Rec {
+  float4 r0, r1, r2, r3, r4;
+};
+
+// Per-tile constants shared by the CTA: reference ray d0 (tile centre), tile
+// origin, bound of |dd| over the tile's pixels.
+struct TileConst {
+  double d0[3];
+  double tx0, ty0;
+  float ddmax;
+};
+
+__device__ __forceinline__ void stage_record(const RasterParams& P, int id, const TileConst& tc, Rec& R) {
+  const Geo& g = P.geo[id];
+  const double d00 = tc.d0[0], d01 = tc.d0[1], d02 = tc.d0[2], tx0 = tc.tx0, ty0 = tc.ty0;
+  const double ddmax = tc.ddmax;
+  const double a0 = P.cam.o[0] - g.mu[0], a1 = P.cam.o[1] - g.mu[1], a2 = P.cam.o[2] - g.mu[2];
+  const double au = g.rx[0] * a0 + g.rx[1] * a1 + g.rx[2] * a2;
+  const double av = g.ry[0] * a0 + g.ry[1] * a1 + g.ry[2] * a2;
+  const double az = -g.num;  // R_z . (o - mu) = -num exactly (same op order, negated operands)
+  const double dz0 = g.rz[0] * d00 + g.rz[1] * d01 + g.rz[2] * d02;
+  const double dx0 = g.rx[0] * d00 + g.rx[1] * d01 + g.rx[2] * d02;
+  const double dy0 = g.ry[0] * d00 + g.ry[1] * d01 + g.ry[2] * d02;
+  const double nu0 = au * dz0 - az * dx0, nv0 = av * dz0 - az * dy0;
+  double gu[3], gv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    gu[k] = au * g.rz[k] - az * g.rx[k];
+    gv[k] = av * g.rz[k] - az * g.ry[k];
+  }
+  const double rz1 = fabs(g.rz[0]) + fabs(g.rz[1]) + fabs(g.rz[2]);
+  const double gu1 = fabs(gu[0]) + fabs(gu[1]) + fabs(gu[2]);
+  const double gv1 = fabs(gv[0]) + fabs(gv[1]) + fabs(gv[2]);
+  // absolute error bounds of the per-pixel fp32 evaluations (3-FMA chains
+  // from fp32-rounded operands; see the header)
+  const double ez = 4e-7 * (fabs(dz0) + rz1 * ddmax) + 1e-12;
+  const double eN = 2.5e-7 * fmax(fabs(nu0), fabs(nv0)) + 3.2e-7 * fmax(gu1, gv1) * ddmax + 1e-30;
+  R.r0 = make_float4((float)g.rz[0], (float)g.rz[1], (float)g.rz[2], (float)dz0);
+  R.r1 = make_float4((float)gu[0], (float)gu[1], (float)gu[2], (float)nu0);
+  R.r2 = make_float4((float)gv[0], (float)gv[1], (float)gv[2], (float)nv0);
+  R.r3 = make_float4((float)g.num, (float)ez, (float)eN, (float)g.r2max);
+  const float fvis2 = P.S.psif[12 * (size_t)id + 8];
+  R.r4 = g.has_proj ? make_float4((float)(g.ppx - tx0), (float)(g.ppy - ty0), (float)g.dp2max, fvis2)
+                    : make_float4(0.f, 0.f, -1.f, fvis2);
+}
+
+// Exact r_t of primitive id on the ray of pixel (x, y) (geometry.cpp:40-47,
+// reference op order); returns false for grazing / behind.
+__device__ __noinline__ bool exact_rt(const RasterParams& P, int id, int x, int y, double* rt) {
+  double dir[3];
+  pixel_dir(P.cam, x + 0.5, y + 0.5, dir);
+  const Geo& g = P.geo[id];
+  const double denom = xdot3(dir[0], dir[1], dir[2], g.rz[0], g.rz[1], g.rz[2]);
+  if (fabs(denom) < P.opt.grazing_eps) return false;
+  const double r = g.num / denom;
+  *rt = r;
+  return r > 0;
+}
+
+// fp64 composite_candidate values (raster.cpp:327-350) for one popped entry:
+// alpha (before the skip test / clamp), low-pass flag, r_t and the normal sign.
+struct Pop64 {
+  double a, rt;
+  float sgn;
+  bool lp, degen;
+};
+__device__ __noinline__ void pop_f64(const RasterParams& P, int id, int x, int y, Pop64& o) {
+  double dir[3];
+  const double px = x + 0.5, py = y + 0.5;
+  pixel_dir(P.cam, px, py, dir);
+  const Geo& g = P.geo[id];
+  const double denom = xdot3(dir[0], dir[1], dir[2], g.rz[0], g.rz[1], g.rz[2]);
+  const double rt = g.num / denom;
+  const double h0 = xs(xa(P.cam.o[0], xm(rt, dir[0])), g.mu[0]);
+  const double h1 = xs(xa(P.cam.o[1], xm(rt, dir[1])), g.mu[1]);
+  const double h2 = xs(xa(P.cam.o[2], xm(rt, dir[2])), g.mu[2]);
+  const double u = xdot3(g.rx[0], g.rx[1], g.rx[2], h0, h1, h2);
+  const double v = xdot3(g.ry[0], g.ry[1], g.ry[2], h0, h1, h2);
+  KEval ev;
+  eval_kernel(u, v, P.S, id, ev);
+  o.degen = ev.degenerate;
+  o.rt = rt;
+  o.sgn = denom < 0 ? 1.f : -1.f;
+  o.lp = false;
+  if (ev.degenerate) {
+    o.a = 0;
+    return;
+  }
+  const double ak = P.S.o[id] * sharpen(ev.g, P.S.tau[id]);
+  o.a = ak;
+  if (g.has_proj) {
+    const double f = low_pass_filter_term(xs(px, g.ppx), xs(py, g.ppy), fabs(denom), P.S.o[id], P.opt.lowpass_radius);
+    if (f > ak) {
+      o.a = f;
+      o.lp = true;
+    }
+  }
+}
+
+__device__ __forceinline__ int entry_id(const RasterParams& P, const int* s_id, long long beg, int jr, int ring_lo) {
+  return jr >= ring_lo ? s_id[jr & (kRing - 1)] : (int)(P.pv[beg + jr] & 0xffffffffull);
+}
+
+// ---------------------------------------------------------------------------
+// The kernel
+// ---------------------------------------------------------------------------
+struct FastPixel {
+  double T;
+  float C0, C1, C2, D, N0, N1, N2, A, E;
+  float ddx, ddy, ddz, pxr, pyr;
+  int ncomp, stop;
+  unsigned n_pop, n_rej1, n_rej2, n_f64, n_miss;
+  bool uncertain, err;
+};
+
+template <bool VALIDATE>
+__device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, const float* s_basis, const Rec* ring,
+                                         const int* s_id, const TileConst& tc, long long beg, int ring_lo, int jr,
+                                         int x, int y) {
+  ++px.n_pop;
+  Rec R;
+  int id;
+  if (jr >= ring_lo) {
+    const int slot = jr & (kRing - 1);
+    R = ring[slot];
+    id = s_id[slot];
+  } else {
+    id = (int)(P.pv[beg + jr] & 0xffffffffull);
+    stage_record(P, id, tc, R);
+    ++px.n_miss;
+  }
+  const float dz = fmaf(R.r0.x, px.ddx, fmaf(R.r0.y, px.ddy, fmaf(R.r0.z, px.ddz, R.r0.w)));
+  const float nu = fmaf(R.r1.x, px.ddx, fmaf(R.r1.y, px.ddy, fmaf(R.r1.z, px.ddz, R.r1.w)));
+  const float nv = fmaf(R.r2.x, px.ddx, fmaf(R.r2.y, px.ddy, fmaf(R.r2.z, px.ddz, R.r2.w)));
+  const float inv = rcp_approx(dz);
+  const float ainv = fabsf(inv);
+  const float rel_z = R.r3.y * ainv;
+  const float u = nu * inv, v = nv * inv;
+  float rt = R.r3.x * inv;
+  float sgn = dz < 0.f ? 1.f : -1.f;
+  const float amin = (float)P.opt.alpha_min;
+  float at = 0.f, relt = 0.f;
+  bool use64 = rel_z > 1e-3f;
+  double a64 = 0;
+  if (!use64) {
+    // absolute error bound of u and v
+    const float du = ainv * R.r3.z + fabsf(u) * (rel_z + 3e-7f);
+    const float dv = ainv * R.r3.z + fabsf(v) * (rel_z + 3e-7f);
+    const float dp = fmaxf(du, dv);
+    const float r2 = fmaf(u, u, v * v);
+    const float au_ = fabsf(u), av_ = fabsf(v);
+    const float dr2 = 2.f * (au_ + av_) * dp + 2.f * dp * dp + 2.5e-7f * r2;
+    // low-pass reach: dp^2 <= cos^2 dp2max (raster.cpp:337, core.cpp:267-273)
+    bool lp_possible = false;
+    float dpx = 0.f, dpy = 0.f, dpp2 = 0.f;
+    if (R.r4.z >= 0.f) {
+      dpx = px.pxr - R.r4.x;
+      dpy = px.pyr - R.r4.y;
+      dpp2 = fmaf(dpx, dpx, dpy * dpy);
+      lp_possible = dpp2 <= dz * dz * R.r4.z * (1.0001f + 4.f * rel_z) + 1e-6f;
+    }
+    if (r2 - dr2 > R.r3.w * 1.000001f && !lp_possible) {
+      ++px.n_rej1;
+      return true;
+    }
+    // ---- alpha = o Psi(g(u, v)) (core.cpp:148-265) ----
+    const float* hd = P.shrec + (size_t)kRecStride * id;
+    const float4 t0 = __ldg(reinterpret_cast<const float4*>(hd)), t1 = __ldg(reinterpret_cast<const float4*>(hd) + 1);
+    float th = atan2_fast(v, u);
+    if (th <= 0.f) th += 6.28318530717958647692f;
+    int lo;
+    if (th <= t0.x || th > t1.w) {
+      lo = 7;
+    } else {
+      lo = (t0.y < th) + (t0.z < th) + (t0.w < th) + (t1.x < th) + (t1.y < th) + (t1.z < th);
+    }
+    const float4* bp = reinterpret_cast<const float4*>(hd + kRecHdr + 8 * lo);
+    const float4 e = __ldg(bp), f = __ldg(bp + 1);  // (elx, ely, ehx, ehy), (1/det, pi/gap, h_lo, h_hi)
+    if (isnan(f.x)) {
+      px.err = true;
+      return false;
+    }
+    const float eta = __ldg(hd + 16);
+    const float ka = (e.w * u - e.z * v) * f.x;
+    const float kb = (e.x * v - e.y * u) * f.x;
+    const float r1 = fabsf(ka) + fabsf(kb);
+    const float L1 = fabsf(f.x) * (fabsf(e.x) + fabsf(e.y) + fabsf(e.z) + fabsf(e.w));
+    const float dr1 = L1 * (dp + 3.6e-7f * fmaxf(au_, av_));
+    const float hmin = fminf(f.z, f.w);
+    const float fvis2 = R.r4.w;
+    {
+      // in-bracket lower bound of Q: alpha_kernel < alpha_min once it exceeds f_vis^2
+      const float r1l = fmaxf(r1 - dr1, 0.f);
+      const float qlb = eta * r1l * r1l + (1.f - eta) * fmaxf(r2 - dr2, 0.f) * hmin;
+      if (qlb > fvis2 * 1.00002f && !lp_possible) {
+        ++px.n_rej2;
+        return true;
+      }
+    }
+    const float4 c0 = __ldg(reinterpret_cast<const float4*>(hd) + 2), c1 = __ldg(reinterpret_cast<const float4*>(hd) + 3);
+    float ak, relk;
+    if (r2 == 0.f) {
+      float cond;
+      ak = c1.w * sharpen_ps(c0, c1, 1.0f, &cond);
+      relk = 6e-7f + cond * 1e-6f;
+    } else {
+      // angle from e_lo inside the bracket, delta = that * pi / gap
+      const float cr = e.x * v - e.y * u, dt = e.x * u + e.y * v;
+      const float dth = atan2_fast(cr, dt);
+      const float delta = fmaxf(dth, 0.f) * f.y;
+      const float cd = __cosf(delta);
+      const float hs = 0.5f * (f.z + f.w), hdiff = 0.5f * (f.z - f.w);
+      const float inv_s = fmaf(hdiff, cd, hs);
+      const float Q = fmaf(eta * r1, r1, (1.f - eta) * r2 * inv_s);
+      // error of Q: r1 and r2 from the tangent coordinates, the bracket angle
+      // (atan2 + coordinate error) through the cosine blend, __cosf (<= 5e-7
+      // absolute), rounding
+      const float pabs = sqrtf(r2);
+      const float dth_err = 2.5e-7f * dth + 2.5e-7f + 1.5f * dp / pabs;
+      const float dinv = fabsf(hdiff) * (dth_err * f.y + 2.4e-7f * delta + 6e-7f) + 2e-7f * (hs + fabsf(hdiff));
+      const float dQ = eta * (2.f * r1 * dr1 + dr1 * dr1) + (1.f - eta) * (r2 * dinv + inv_s * dr2) + 6e-7f * Q;
+      const float ex = fmaxf(-0.5f * Q, -30.0f);
+      const float g = __expf(ex);
+      float cond;
+      const float Pv = sharpen_ps(c0, c1, g, &cond);
+      ak = c1.w * Pv;
+      relk = cond * (0.5f * dQ + 2.5e-7f + 1.2e-7f * fabsf(ex)) + 6e-7f;
+    }
+    at = ak;
+    relt = relk;
+    if (lp_possible) {
+      const float sl = (float)P.opt.lowpass_radius;
+      const float den = 2.0f * dz * dz * sl * sl;
+      const float exl = fmaxf(-dpp2 / den, -30.0f);
+      const float fl = c1.w * __expf(exl);
+      const float ddp = 6e-8f * (fabsf(R.r4.x) + fabsf(R.r4.y) + 32.f);
+      const float relf = 4e-7f + 1.2e-7f * fabsf(exl) + fabsf(exl) * (2.f * rel_z + 1e-6f) +
+                         2.f * sqrtf(dpp2) * ddp / den * 2.f;
+      if (fabsf(fl - ak) <= relk * ak + relf * fl) use64 = true;
+      if (fl > ak) {
+        at = fl;
+        relt = relf;
+      }
+    }
+    if (fabsf(at - amin) <= relt * at + 1e-12f) use64 = true;
+    if (at >= 0.99f && fabsf(at - 0.999999f) <= relt * at + 1e-6f) use64 = true;
+    if (VALIDATE && !use64) {
+      Pop64 o;
+      pop_f64(P, id, x, y, o);
+      if (!o.degen && o.a >= 1e-4) {
+        const double ratio = fabs((double)at - o.a) / ((double)relt * at + 1e-30);
+        atomicMax(P.vstat, (unsigned long long)__double_as_longlong(ratio));
+        atomicMax(P.vstat + 1, (unsigned long long)__double_as_longlong(fabs((double)at - o.a)));
+      }
+    }
+  }
+  if (use64) {
+    ++px.n_f64;
+    Pop64 o;
+    pop_f64(P, id, x, y, o);
+    if (o.degen) {
+      px.err = true;
+      return false;
+    }
+    a64 = o.a;
+    rt = (float)o.rt;
+    sgn = o.sgn;
+    relt = 0.f;
+    if (a64 < P.opt.alpha_min) return true;
+    a64 = dmin(a64, 1.0 - 1e-6);
+  } else {
+    if (at < amin) return true;
+    a64 = dmin((double)at, 1.0 - 1e-6);
+  }
+  // ---- blend (raster.cpp:349-361) ----
+  const float* shp = P.sh + (size_t)id * P.terms * 3;
+  float c0 = 0.5f, c1 = 0.5f, c2 = 0.5f;
+  const int ta = P.opt.terms_active;
+  if ((P.terms & 3) == 0 && (ta & 3) == 0) {
+    const float4* q = reinterpret_cast<const float4*>(shp);
+#pragma unroll
+    for (int t = 0; t < 16; t += 4) {
+      if (t < ta) {
+        const float4 a = __ldg(q + 3 * (t / 4)), b = __ldg(q + 3 * (t / 4) + 1), c = __ldg(q + 3 * (t / 4) + 2);
+        const float b0 = s_basis[t * kBatch], b1 = s_basis[(t + 1) * kBatch], b2 = s_basis[(t + 2) * kBatch],
+                    b3 = s_basis[(t + 3) * kBatch];
+        c0 = fmaf(b0, a.x, c0);
+        c1 = fmaf(b0, a.y, c1);
+        c2 = fmaf(b0, a.z, c2);
+        c0 = fmaf(b1, a.w, c0);
+        c1 = fmaf(b1, b.x, c1);
+        c2 = fmaf(b1, b.y, c2);
+        c0 = fmaf(b2, b.z, c0);
+        c1 = fmaf(b2, b.w, c1);
+        c2 = fmaf(b2, c.x, c2);
+        c0 = fmaf(b3, c.y, c0);
+        c1 = fmaf(b3, c.z, c1);
+        c2 = fmaf(b3, c.w, c2);
+      }
+    }
+  } else {
+    for (int t = 0; t < ta; ++t) {
+      const float bt = s_basis[t * kBatch];
+      c0 = fmaf(bt, __ldg(shp + 3 * t), c0);
+      c1 = fmaf(bt, __ldg(shp + 3 * t + 1), c1);
+      c2 = fmaf(bt, __ldg(shp + 3 * t + 2), c2);
+    }
+  }
+  c0 = fmaxf(c0, 0.f);
+  c1 = fmaxf(c1, 0.f);
+  c2 = fmaxf(c2, 0.f);
+  const float w = (float)(px.T * a64);
+  px.C0 = fmaf(w, c0, px.C0);
+  px.C1 = fmaf(w, c1, px.C1);
+  px.C2 = fmaf(w, c2, px.C2);
+  px.D = fmaf(w, rt, px.D);
+  const float ws = w * sgn;
+  px.N0 = fmaf(ws, R.r0.x, px.N0);
+  px.N1 = fmaf(ws, R.r0.y, px.N1);
+  px.N2 = fmaf(ws, R.r0.z, px.N2);
+  px.A += w;
+  px.T = xm(px.T, xs(1.0, a64));
+  ++px.ncomp;
+  if (relt > 0.f) {
+    const float af = (float)a64;
+    px.E += relt * __fdividef(af, 1.0f - af) + 1e-15f;
+  }
+  if (fabs(px.T - P.opt.early_stop) <= px.T * (double)px.E) px.uncertain = true;
+  if (px.T < P.opt.early_stop) {
+    px.stop = px.ncomp;
+    return false;
+  }
+  return true;
+}
+
+template <bool VALIDATE>
+__global__ void __launch_bounds__(256, 2) k_raster_fast(const __grid_constant__ RasterParams P) {
+  extern __shared__ float4 dyn[];
+  Rec* ring = reinterpret_cast<Rec*>(dyn);
+  int* s_id = reinterpret_cast<int*>(ring + kRing);
+  float* s_basis = reinterpret_cast<float*>(s_id + kRing) + threadIdx.x;  // [16][256], this thread's column
+  __shared__ unsigned s_ddmax;
+  __shared__ TileConst tc;
+  const int tile = blockIdx.x;
+  const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
+  const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
+  const bool active = x < P.cam.W && y < P.cam.H;
+  const double tx0 = (double)tx * kTile, ty0 = (double)ty * kTile;
+  // tile reference ray d0 (centre of the tile) and this pixel's offset dd
+  double d0[3], dir[3];
+  pixel_dir(P.cam, tx0 + 8.0, ty0 + 8.0, d0);
+  pixel_dir(P.cam, x + 0.5, y + 0.5, dir);
+  FastPixel px;
+  px.ddx = (float)(dir[0] - d0[0]);
+  px.ddy = (float)(dir[1] - d0[1]);
+  px.ddz = (float)(dir[2] - d0[2]);
+  px.pxr = (float)(x + 0.5 - tx0);
+  px.pyr = (float)(y + 0.5 - ty0);
+  {
+    float b[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) b[t] = 0.f;
+    sh_basis_f((float)dir[0], (float)dir[1], (float)dir[2], P.opt.sh_degree, b);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) s_basis[t * kBatch] = b[t];
+  }
+  if (threadIdx.x == 0) {
+    s_ddmax = 0u;
+    tc.d0[0] = d0[0];
+    tc.d0[1] = d0[1];
+    tc.d0[2] = d0[2];
+    tc.tx0 = tx0;
+    tc.ty0 = ty0;
+  }
+  __syncthreads();
+  {
+    const float m = fmaxf(fabsf(px.ddx), fmaxf(fabsf(px.ddy), fabsf(px.ddz)));
+    const unsigned wm = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_ddmax, wm);
+  }
+  px.T = 1.0;
+  px.C0 = px.C1 = px.C2 = px.D = px.N0 = px.N1 = px.N2 = px.A = px.E = 0.f;
+  px.ncomp = 0;
+  px.stop = INT_MAX;
+  px.n_pop = px.n_rej1 = px.n_rej2 = px.n_f64 = px.n_miss = 0;
+  px.uncertain = px.err = false;
+  unsigned n_str = 0, n_amb = 0;
+  float clo[kCacheCap], chi[kCacheCap];
+  int cj[kCacheCap];
+#pragma unroll
+  for (int q = 0; q < kCacheCap; ++q) {
+    clo[q] = chi[q] = __int_as_float(0x7f800000);
+    cj[q] = 0;
+  }
+  int csz = 0;
+  bool done = !active;
+  const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
+  const float eps = (float)P.opt.grazing_eps;
+  __syncthreads();
+  if (threadIdx.x == 0) tc.ddmax = __uint_as_float(s_ddmax) * 1.0001f + 1e-30f;
+  int ring_lo = 0;
+  for (long long b0 = beg; b0 < end; b0 += kBatch) {
+    const int jb = (int)(b0 - beg);
+    __syncthreads();
+    {
+      const long long j = b0 + threadIdx.x;
+      if (j < end) {
+        const int id = (int)(P.pv[j] & 0xffffffffull);
+        const int slot = (jb + threadIdx.x) & (kRing - 1);
+        stage_record(P, id, tc, ring[slot]);
+        s_id[slot] = id;
+      }
+    }
+    __syncthreads();
+    ring_lo = jb >= kBatch ? jb - kBatch : 0;
+    const int cnt = (int)min((long long)kBatch, end - b0);
+    if (!done) {
+      for (int c = 0; c < cnt; ++c) {
+        const int jr = jb + c;
+        const int slot = jr & (kRing - 1);
+        const float4 r0 = ring[slot].r0;
+        const float2 r3 = *reinterpret_cast<const float2*>(&ring[slot].r3);
+        const float dz = fmaf(r0.x, px.ddx, fmaf(r0.y, px.ddy, fmaf(r0.z, px.ddz, r0.w)));
+        const float adz = fabsf(dz);
+        float lo, hi;
+        if (adz < eps - r3.y) continue;  // certainly grazing
+        const float inv = rcp_approx(dz);
+        const float rel_z = r3.y * fabsf(inv);
+        if (adz > eps + r3.y && r3.x != 0.f && rel_z <= 1e-3f) {
+          const float rt = r3.x * inv;
+          if (rt <= 0.f) continue;
+          const float er = rt * (4.5e-7f + rel_z * 1.01f);
+          lo = rt - er;
+          hi = rt + er;
+        } else {
+          double rx;
+          if (!exact_rt(P, s_id[slot], x, y, &rx)) continue;
+          lo = __double2float_rd(rx);
+          hi = __double2float_ru(rx);
+        }
+        ++n_str;
+        // SortCache::step (raster.cpp:267-303) on exact-containing intervals
+        bool le[kCacheCap];
+        bool amb = false;
+#pragma unroll
+        for (int q = 0; q < kCacheCap; ++q) {
+          le[q] = chi[q] <= lo;
+          amb |= !le[q] && !(clo[q] > hi);
+        }
+        if (amb) {
+          // overlapping intervals: compare the exact fp64 depths
+          ++n_amb;
+          double rin = 0;
+          exact_rt(P, s_id[slot], x, y, &rin);
+          lo = __double2float_rd(rin);
+          hi = __double2float_ru(rin);
+#pragma unroll
+          for (int q = 0; q < kCacheCap; ++q) {
+            if (!le[q]) {
+              if (chi[q] <= lo) {
+                le[q] = true;
+              } else if (!(clo[q] > hi)) {
+                double rq = 0;
+                exact_rt(P, entry_id(P, s_id, beg, cj[q], ring_lo), x, y, &rq);
+                le[q] = rq <= rin;
+                clo[q] = __double2float_rd(rq);
+                chi[q] = __double2float_ru(rq);
+              }
+            }
+          }
+        }
+        if (csz < kCacheCap) {
+#pragma unroll
+          for (int q = kCacheCap - 1; q >= 0; --q) {
+            const bool prev = q == 0 ? true : le[q - 1];
+            if (!le[q]) {
+              clo[q] = prev ? lo : clo[q - 1];
+              chi[q] = prev ? hi : chi[q - 1];
+              cj[q] = prev ? jr : cj[q - 1];
+            }
+          }
+          ++csz;
+          continue;
+        }
+        int pj;
+        if (!le[0]) {  // incoming strictly shallower than the head: pops through
+          pj = jr;
+        } else {
+          pj = cj[0];
+#pragma unroll
+          for (int q = 0; q < kCacheCap; ++q) {
+            const bool nxt = q + 1 < kCacheCap ? le[q + 1] : false;
+            if (nxt) {
+              clo[q] = clo[q + 1];
+              chi[q] = chi[q + 1];
+              cj[q] = cj[q + 1];
+            } else if (le[q]) {
+              clo[q] = lo;
+              chi[q] = hi;
+              cj[q] = jr;
+            }
+          }
+        }
+        if (!pop_eval<VALIDATE>(P, px, s_basis, ring, s_id, tc, beg, ring_lo, pj, x, y)) {
+          done = true;
+          break;
+        }
+      }
+    }
+    if (__syncthreads_count(!done) == 0) break;
+  }
+  // end marker: drain the cache head first (raster.cpp:410-414)
+  while (!done && csz > 0) {
+    const int pj = cj[0];
+#pragma unroll
+    for (int q = 0; q < kCacheCap - 1; ++q) {
+      clo[q] = clo[q + 1];
+      chi[q] = chi[q + 1];
+      cj[q] = cj[q + 1];
+    }
+    --csz;
+    if (!pop_eval<VALIDATE>(P, px, s_basis, ring, s_id, tc, beg, ring_lo, pj, x, y))
+      done = true;
+  }
+  // counters: one atomic per warp and counter
+  {
+    unsigned long long v[8] = {n_str, px.n_pop, (unsigned long long)px.ncomp, px.n_rej1, px.n_rej2, px.n_f64,
+                               n_amb, px.n_miss};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      unsigned long long s = v[k];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      v[k] = s;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      const int slots[8] = {C_STREAMED, C_POPPED, C_COMPOSITED, C_REJECT_RADIUS, C_REJECT_BRACKET, C_FP64_EVALS,
+                            C_AMBIGUOUS, C_RING_MISS};
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (v[k]) atomicAdd(&P.counters[slots[k]], v[k]);
+    }
+  }
+  if (!active) return;
+  if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
+  const size_t p = (size_t)y * P.cam.W + x;
+  const double c0 = (double)px.C0 + px.T * P.opt.bg[0];
+  const double c1 = (double)px.C1 + px.T * P.opt.bg[1];
+  const double c2 = (double)px.C2 + px.T * P.opt.bg[2];
+  if (P.color) {
+    P.color[3 * p] = (float)c0;
+    P.color[3 * p + 1] = (float)c1;
+    P.color[3 * p + 2] = (float)c2;
+  }
+  if (P.normal) {
+    P.normal[3 * p] = px.N0;
+    P.normal[3 * p + 1] = px.N1;
+    P.normal[3 * p + 2] = px.N2;
+  }
+  if (P.depth) P.depth[p] = px.D;
+  if (P.alpha) P.alpha[p] = px.A;
+  if (P.pxstate) {
+    double* st = P.pxstate + 8 * p;
+    st[0] = c0;
+    st[1] = c1;
+    st[2] = c2;
+    st[3] = px.D;
+    st[4] = px.N0;
+    st[5] = px.N1;
+    st[6] = px.N2;
+    st[7] = px.A;
+  }
+  if (P.pxstop) P.pxstop[p] = px.stop;
+  if (P.pxflag) {
+    P.pxflag[p] = px.uncertain ? 1 : 0;
+    if (px.uncertain) P.redo_list[atomicAdd(P.redo_count, 1u)] = (int)p;
+  }
+}
+
+size_t raster_fast_smem() { return (size_t)kRing * (sizeof(Rec) + sizeof(int)) + 16 * kBatch * sizeof(float); }
+
+bool raster_fast_eligible(const RasterParams& P) {
+  return P.S.K == 8 && P.shrec != nullptr && P.opt.use_cache && !P.opt.exact_sort && !P.opt.fp64_alpha &&
+         P.replay_cap == 0;
+}
+
+void launch_raster_fast(const RasterParams& P, int n_tiles, bool validate, cudaStream_t s) {
+  const size_t smem = raster_fast_smem();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_raster_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_raster_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  if (validate) k_raster_fast<true><<<n_tiles, 256, smem, s>>>(P);
+  else k_raster_fast<false><<<n_tiles, 256, smem, s>>>(P);
+}
+
+}  // namespace drk

@@ -7,6 +7,8 @@ from paper_2412_11752_b200.api import Rasterizer, RenderOptions, FrameGrad
 
 r = Rasterizer(0)
 r.set_timing(True)
+VALIDATE = '--validate' in sys.argv
+sys.argv = [a for a in sys.argv if a != '--validate']
 for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:
     sc = scenes.config_scene(cfg)
     cam = scenes.config_cameras(cfg)[0]
@@ -21,8 +23,10 @@ for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:
     torch.cuda.synchronize(); dt = (time.time() - t) / N
     st = r.stats()
     mp = cam.width * cam.height / 1e6
+    if VALIDATE:
+        r.set_validation(True); r.render(raw, cam, opt); print('validation (max err/bound, max abs err):', r.validation()); r.set_validation(False)
     print(f"cfg{cfg} fwd {dt*1e3:.2f} ms  {mp/dt:.1f} MP/s", {k: round(v, 3) for k, v in st['stage_ms'].items()},
-          {k: st[k] for k in ('pairs', 'streamed', 'popped', 'composited', 'reject_radius', 'reject_bracket', 'fp64_evals', 'fp64_pixels', 'launches')}, flush=True)
+          {k: st[k] for k in ('pairs', 'streamed', 'popped', 'composited', 'reject_radius', 'reject_bracket', 'fp64_evals', 'fp64_pixels', 'ambiguous', 'ring_miss', 'launches')}, flush=True)
     if scenes.CONFIGS[cfg]['backward']:
         tgt = torch.from_numpy(scenes.config_target(cfg, cam).astype(np.float32)).cuda()
         for _ in range(2):

@@ -1,0 +1,89 @@
+"""The fp32 interval forward kernel (drk_raster_fast.cu) against the legacy fp64-depth
+kernel and against its own fp64 re-evaluation.
+
+- Every fp32 alpha of a frame is re-evaluated in fp64 (drk_set_validation): the
+  observed error must stay inside the bound that gates the fp64 fallbacks.
+- Full BASELINE frames (configs 1 and 2, where the CPU oracle is too slow): both
+  kernels make the reference's discrete decisions, so their framebuffers agree
+  within the parity tolerance and their work counters agree.
+- Backward after the fast forward: gradients match the oracle (termination is
+  taken from the forward's per-pixel composite count).
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import port
+from paper_2412_11752_b200 import scenes
+from tests.helpers import api_options, opt_for, rel_l2, small_scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _render(rast, sc, cam, opt, kernel):
+    fb = rast.render(sc.f32(), cam, dataclasses.replace(opt, raster_kernel=kernel))
+    return fb, rast.stats()
+
+
+@pytest.mark.parametrize("cfg,crop", [(0, None), (1, 256), (2, 192)])
+def test_fast_alpha_bound_in_situ(rast, cfg, crop):
+    sc = scenes.config_scene(cfg)
+    cam = scenes.config_cameras(cfg)[0]
+    if crop:
+        cam = cam.crop((cam.width // 2 - crop // 2) // 16 * 16, (cam.height // 2 - crop // 2) // 16 * 16, crop, crop)
+    opt = api_options(opt_for(scenes.CONFIGS[cfg]["sh_degree"]))
+    rast.set_validation(True)
+    try:
+        rast.render(sc.f32(), cam, opt)
+        ratio, max_abs = rast.validation()
+    finally:
+        rast.set_validation(False)
+    st = rast.stats()
+    assert st["popped"] > 0
+    assert ratio < 1.0, (ratio, max_abs)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_fast_matches_legacy_full_frame(rast, cfg):
+    sc = scenes.config_scene(cfg)
+    cam = scenes.config_cameras(cfg)[0]
+    opt = api_options(opt_for(3))
+    fb_l, st_l = _render(rast, sc, cam, opt, 1)
+    legacy = {f: getattr(fb_l, f).clone() for f in ("color", "depth", "normal", "alpha")}
+    fb_f, st_f = _render(rast, sc, cam, opt, 0)
+    for f, v in legacy.items():
+        err = float((getattr(fb_f, f) - v).abs().max())
+        assert err <= 1e-4, (f, err)
+    # identical decisions: the same entries stream, pop and composite (up to the
+    # pixels either kernel hands to the fp64 re-render)
+    for k in ("streamed", "popped", "composited"):
+        assert abs(st_f[k] - st_l[k]) <= 1e-4 * st_l[k], (k, st_f[k], st_l[k])
+    assert st_f["fp64_pixels"] <= 0.02 * cam.width * cam.height
+
+
+def test_fast_small_scenes_vs_oracle(rast):
+    for seed in range(4):
+        sc, cam = small_scene(seed=20 + seed, n=120, sh_degree=3, clusters=3)
+        o = opt_for(3, background=(0.1, 0.7, 0.3))
+        fb = rast.render(sc.f32(), cam, api_options(o))
+        orc = port.render(sc, cam, o)
+        for f in ("color", "depth", "normal", "alpha"):
+            err = float(np.abs(getattr(fb, f).cpu().numpy().astype(np.float64) - orc[f]).max())
+            assert err <= 1e-4, (seed, f, err)
+
+
+def test_fast_backward_termination_from_forward(rast):
+    from paper_2412_11752_b200.api import FrameGrad
+    sc, cam = small_scene(seed=31, n=150, sh_degree=3, clusters=2)
+    o = opt_for(3)
+    rast.render(sc.f32(), cam, api_options(o))
+    rng = np.random.default_rng(3)
+    dc = rng.uniform(-1, 1, (cam.height, cam.width, 3)).astype(np.float32)
+    g = rast.backward_render(sc.f32(), FrameGrad(d_color=torch.from_numpy(dc)))
+    og = port.backward(sc, cam, o, dc, None, None, None)
+    assert rel_l2(g.raw.cpu().numpy(), og["raw"]) <= 1e-3
+    np.testing.assert_array_equal(g.touched.cpu().numpy(), og["touched"])
