@@ -145,6 +145,8 @@ int drk_set_timing(drk_ctx* ctx, int enabled);
  * (must stay below 1) and max |a32 - a64| since validation was enabled. */
 int drk_set_validation(drk_ctx* ctx, int enabled);
 int drk_get_validation(drk_ctx* ctx, double* out2);
+/* First pop whose error exceeded its bound (flag, then 21 diagnostic values). */
+int drk_get_validation_detail(drk_ctx* ctx, double* out22);
 /* Measured FP32 FFMA throughput of this device (TFLOP/s), for rooflines. */
 int drk_measure_fp32_peak(drk_ctx* ctx, double* tflops);
 

@@ -98,6 +98,7 @@ SIGNATURES = {
     "drk_measure_fp32_peak": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "drk_set_validation": (C.c_int, [_P, C.c_int]),
     "drk_get_validation": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "drk_get_validation_detail": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "drk_activate": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(Prims_)]),
     "drk_forward": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(Camera_), C.POINTER(Options_),
                               _P, _P, _P, _P]),

@@ -352,6 +352,11 @@ class Rasterizer:
         self._check(_lib.lib().drk_get_validation(self._h, v))
         return float(v[0]), float(v[1])
 
+    def validation_detail(self) -> list[float]:
+        v = (C.c_double * 22)()
+        self._check(_lib.lib().drk_get_validation_detail(self._h, v))
+        return list(v)
+
     def fp32_peak_tflops(self) -> float:
         v = C.c_double(0)
         self._check(_lib.lib().drk_measure_fp32_peak(self._h, C.byref(v)))

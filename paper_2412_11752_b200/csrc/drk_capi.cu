@@ -279,7 +279,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   P.pxflag = pxflag;
   P.pxstop = pxstop;
   if (c->validate_fast) {
-    P.vstat = ensure<unsigned long long>(c->vstat, 2);
+    P.vstat = ensure<unsigned long long>(c->vstat, 32);
     if (!P.vstat) return set_error(c, DRK_ERR_OOM, "validation buffer");
   }
   P.color = color;
@@ -452,9 +452,9 @@ int drk_set_validation(drk_ctx* c, int enabled) {
   c->validate_fast = enabled != 0;
   if (c->validate_fast) {
     cudaSetDevice(c->device);
-    unsigned long long* v = ensure<unsigned long long>(c->vstat, 2);
+    unsigned long long* v = ensure<unsigned long long>(c->vstat, 32);
     if (!v) return set_error(c, DRK_ERR_OOM, "validation buffer");
-    cudaMemsetAsync(v, 0, 2 * sizeof(unsigned long long), c->stream);
+    cudaMemsetAsync(v, 0, 32 * sizeof(unsigned long long), c->stream);
   }
   return cuda_check(c, cudaGetLastError(), "validation");
 }
@@ -463,11 +463,22 @@ int drk_get_validation(drk_ctx* c, double* out) {
   if (!c || !out) return DRK_ERR_INVALID_ARG;
   out[0] = out[1] = 0;
   if (!c->vstat.p) return DRK_OK;
-  unsigned long long h[2];
+  unsigned long long h[32];
   cudaMemcpyAsync(h, c->vstat.p, sizeof h, cudaMemcpyDeviceToHost, c->stream);
   if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "validation")) return st;
   std::memcpy(&out[0], &h[0], 8);
   std::memcpy(&out[1], &h[1], 8);
+  return DRK_OK;
+}
+
+int drk_get_validation_detail(drk_ctx* c, double* out) {
+  if (!c || !out) return DRK_ERR_INVALID_ARG;
+  for (int i = 0; i < 22; ++i) out[i] = 0;
+  if (!c->vstat.p) return DRK_OK;
+  unsigned long long h[32];
+  cudaMemcpyAsync(h, c->vstat.p, sizeof h, cudaMemcpyDeviceToHost, c->stream);
+  if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "validation")) return st;
+  std::memcpy(out, &h[2], 8 * 22);
   return DRK_OK;
 }
 

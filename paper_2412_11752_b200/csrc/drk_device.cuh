@@ -305,7 +305,7 @@ __device__ __forceinline__ float sharpen_f(float g, float tau) {
 // tests/test_gpu_alpha_bound.py); r2 == 0 gives the exact centre value.
 // Psi(g) in point-slope form from fp64-derived per-primitive constants, with
 // the condition number A g / Psi that maps the relative error of g onto alpha.
-__device__ __forceinline__ float sharpen_ps(const float4 c0, const float4 c1, float g, float* cond,
+__device__ __forceinline__ float sharpen_ps(const float4 c0, const float4 c1, float g, float relg, float* relP,
                                             float* slope = nullptr, int* branch = nullptr) {
   // c0 = (g1, g2, A0, A1), c1 = (A2, Psi(g1), Psi(g2), o)
   float A, P;
@@ -323,7 +323,16 @@ __device__ __forceinline__ float sharpen_ps(const float4 c0, const float4 c1, fl
     P = c1.z + c1.x * (g - c0.y);
     br = 2;
   }
-  *cond = P > 0.f ? A * g / P : 1.0f;
+  // Relative error of P for a relative error relg of g: the largest slope
+  // over [g - dg, g + dg] (a breakpoint inside the interval brings the
+  // neighbouring branch's slope: for tau -> 0.99 the middle branch is ~200x
+  // steeper), the fp32 breakpoint in the point-slope form (<= 2^-25 absolute,
+  // times the branch slope), and the roundings of the constants and the FMA.
+  const float dg = g * relg + 3.5e-8f;
+  float Am = A;
+  if (fabsf(g - c0.x) <= dg) Am = fmaxf(Am, fmaxf(c0.z, c0.w));
+  if (fabsf(g - c0.y) <= dg) Am = fmaxf(Am, fmaxf(c0.w, c1.x));
+  *relP = P > 0.f ? (Am * (g * relg) + (br > 0 ? A * 3.5e-8f : 0.f)) / P + 1.8e-7f : 1.0f;
   if (slope) *slope = A;
   if (branch) *branch = br;
   return P;
@@ -353,16 +362,16 @@ __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const 
   const float4* pc = reinterpret_cast<const float4*>(S.psif) + 3 * (size_t)i;
   const float4 c0 = __ldg(pc), c1 = __ldg(pc + 1);
   if (r2 == 0) {
-    float cond;
+    float relP;
     *rel = 5e-7f;
     if (kf) {
       kf->center = true;
       kf->clamped = false;
       kf->g = 1.0f;
-      kf->P = sharpen_ps(c0, c1, 1.0f, &cond, &kf->A, &kf->br);
+      kf->P = sharpen_ps(c0, c1, 1.0f, 0.f, &relP, &kf->A, &kf->br);
       return c1.w * kf->P;
     }
-    return c1.w * sharpen_ps(c0, c1, 1.0f, &cond);
+    return c1.w * sharpen_ps(c0, c1, 1.0f, 0.f, &relP);
   }
   const int K = S.K;
   const float* thf = S.thf + (size_t)i * K;
@@ -412,8 +421,20 @@ __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const 
   const float Q = eta * r1 * r1 + (1.0f - eta) * (float)r2 * inv;
   const float e = fmaxf(-0.5f * Q, -30.0f);
   const float g = expf(e);
-  float cond;
-  const float P = kf ? sharpen_ps(c0, c1, g, &cond, &kf->A, &kf->br) : sharpen_ps(c0, c1, g, &cond);
+  // Relative error bound.  Q: fp32 formation of r1 and the products (~4
+  // ulp) plus the cosine blend's sensitivity to delta, |d inv| <=
+  // |sin(delta)| |h_lo - h_hi| / 2 * |d delta| with |d delta| <= 8e-7 (1 + delta)
+  // (atan2f of the in-bracket angle times pi/gap).  g = exp(-Q/2) adds
+  // Q/2 * rel(Q) and expf's ~2 ulp; Psi maps it through its largest slope
+  // over g's uncertainty interval (sharpen_ps); the constants add ~4 ulp.
+  // Checked against the fp64 path on the GPU
+  // (tests/test_gpu_parity.py::test_fp32_alpha_error_bound).
+  const float sd = 2.0f * sh * ch;  // sin(delta)
+  const float dinv = 0.5f * fabsf(sd) * fabsf(hlo - hhi) * 8e-7f * (1.0f + fabsf(delta));
+  const float rel_q = 5e-7f + (1.0f - eta) * (float)r2 * dinv / fmaxf(Q, 1e-30f);
+  const float relg = 0.5f * fminf(Q, 60.0f) * 2.0f * rel_q + 4e-7f;
+  float relP;
+  const float P = kf ? sharpen_ps(c0, c1, g, relg, &relP, &kf->A, &kf->br) : sharpen_ps(c0, c1, g, relg, &relP);
   if (kf) {
     kf->center = false;
     kf->clamped = -0.5f * Q < -30.0f;
@@ -429,18 +450,7 @@ __device__ __forceinline__ float alpha_f32(double u, double v, double r2, const 
     kf->lo = lo;
     kf->hi = hi;
   }
-  // Relative error bound.  Q: fp32 formation of r1 and the products (~4
-  // ulp) plus the cosine blend's sensitivity to delta, |d inv| <=
-  // |sin(delta)| |h_lo - h_hi| / 2 * |d delta| with |d delta| <= 8e-7 (1 + delta)
-  // (atan2f of the in-bracket angle times pi/gap).  g = exp(-Q/2) adds
-  // Q/2 * rel(Q) and expf's ~2 ulp; Psi maps it through its condition
-  // number; the constants add ~4 ulp.  Checked against the fp64 path on the
-  // GPU (tests/test_gpu_parity.py::test_fp32_alpha_error_bound) and by an fp32
-  // emulation (max observed error below half the bound).
-  const float sd = 2.0f * sh * ch;  // sin(delta)
-  const float dinv = 0.5f * fabsf(sd) * fabsf(hlo - hhi) * 8e-7f * (1.0f + fabsf(delta));
-  const float rel_q = 5e-7f + (1.0f - eta) * (float)r2 * dinv / fmaxf(Q, 1e-30f);
-  *rel = cond * (0.5f * fminf(Q, 60.0f) * 2.0f * rel_q + 4e-7f) + 6e-7f;
+  *rel = relP + 6e-7f;
   return c1.w * P;
 }
 

@@ -98,6 +98,31 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
+// hi + (lo + c . dd): float-float constant plus a small linear term
+__device__ __forceinline__ float lin3(float4 c, float lo, float dx, float dy, float dz) {
+  return c.w + fmaf(c.x, dx, fmaf(c.y, dy, fmaf(c.z, dz, lo)));
+}
+
+// 1/x with one Newton step: relative error <= 2^-23 (one rounding of the
+// refined value on top of a ~1e-14 refinement error)
+__device__ __forceinline__ float rcp_nr(float x) {
+  const float r = rcp_approx(x);
+  return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
+
+// cos(d) for d in [0, pi] as -sin(d - pi/2) (odd minimax polynomial);
+// |error| <= 1.3e-7 measured in fp32 Horner form.
+__device__ __forceinline__ float cos_0pi(float d) {
+  const float y = d - 1.57079637f, s = y * y;
+  float r = -2.384675390e-08f;
+  r = fmaf(r, s, 2.752262162e-06f);
+  r = fmaf(r, s, -1.984080445e-04f);
+  r = fmaf(r, s, 8.333330043e-03f);
+  r = fmaf(r, s, -1.666666716e-01f);
+  r = r * s;
+  return -fmaf(r, y, y);
+}
+
 // atan2 in (-pi, pi]; |error| <= 2.5e-7 |result| + 1.5e-7 (minimax polynomial
 // for atan on [0, 1]: relative error 8.8e-8 measured in fp32 Horner form).
 __device__ __forceinline__ float atan2_fast(float y, float x) {
@@ -124,7 +149,7 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
 // Staging (fp64, once per (entry, tile))
 // ---------------------------------------------------------------------------
 struct Rec {
-  float4 r0, r1, r2, r3, r4;
+  float4 r0, r1, r2, r3, r4, r5;  // r5 = low parts (dz0, N_u(d0), N_v(d0)) of the float-float constants
 };
 
 // Per-tile constants shared by the CTA: reference ray d0 (tile centre), tile
@@ -156,13 +181,19 @@ __device__ __forceinline__ void stage_record(const RasterParams& P, int id, cons
   const double rz1 = fabs(g.rz[0]) + fabs(g.rz[1]) + fabs(g.rz[2]);
   const double gu1 = fabs(gu[0]) + fabs(gu[1]) + fabs(gu[2]);
   const double gv1 = fabs(gv[0]) + fabs(gv[1]) + fabs(gv[2]);
-  // absolute error bounds of the per-pixel fp32 evaluations (3-FMA chains
-  // from fp32-rounded operands; see the header)
-  const double ez = 4e-7 * (fabs(dz0) + rz1 * ddmax) + 1e-12;
-  const double eN = 2.5e-7 * fmax(fabs(nu0), fabs(nv0)) + 3.2e-7 * fmax(gu1, gv1) * ddmax + 1e-30;
-  R.r0 = make_float4((float)g.rz[0], (float)g.rz[1], (float)g.rz[2], (float)dz0);
-  R.r1 = make_float4((float)gu[0], (float)gu[1], (float)gu[2], (float)nu0);
-  R.r2 = make_float4((float)gv[0], (float)gv[1], (float)gv[2], (float)nv0);
+  // Absolute error bounds of the per-pixel fp32 evaluations
+  // x = hi + (lo + sum_k c_k dd_k) (lin3): the constant enters as a float-float
+  // pair, so only the final rounding (2^-24 of |x| <= |x0| + |c|_1 |dd|) and the
+  // small linear term (fp32 c, dd and three roundings: <= 3.6e-7 |c|_1 |dd|)
+  // contribute.
+  const double ez = 6.5e-8 * fabs(dz0) + 4.3e-7 * rz1 * ddmax + 1e-12;
+  const double g1 = fmax(gu1, gv1);
+  const double eN = 6.5e-8 * fmax(fabs(nu0), fabs(nv0)) + 4.3e-7 * g1 * ddmax + 1e-30;
+  const float dz0h = (float)dz0, nu0h = (float)nu0, nv0h = (float)nv0;
+  R.r0 = make_float4((float)g.rz[0], (float)g.rz[1], (float)g.rz[2], dz0h);
+  R.r1 = make_float4((float)gu[0], (float)gu[1], (float)gu[2], nu0h);
+  R.r2 = make_float4((float)gv[0], (float)gv[1], (float)gv[2], nv0h);
+  R.r5 = make_float4((float)(dz0 - (double)dz0h), (float)(nu0 - (double)nu0h), (float)(nv0 - (double)nv0h), 0.f);
   R.r3 = make_float4((float)g.num, (float)ez, (float)eN, (float)g.r2max);
   const float fvis2 = P.S.psif[12 * (size_t)id + 8];
   R.r4 = g.has_proj ? make_float4((float)(g.ppx - tx0), (float)(g.ppy - ty0), (float)g.dp2max, fvis2)
@@ -185,7 +216,7 @@ __device__ __noinline__ bool exact_rt(const RasterParams& P, int id, int x, int 
 // fp64 composite_candidate values (raster.cpp:327-350) for one popped entry:
 // alpha (before the skip test / clamp), low-pass flag, r_t and the normal sign.
 struct Pop64 {
-  double a, rt;
+  double a, ak, rt;  // alpha, its kernel part o Psi(g)
   float sgn;
   bool lp, degen;
 };
@@ -208,11 +239,12 @@ __device__ __noinline__ void pop_f64(const RasterParams& P, int id, int x, int y
   o.sgn = denom < 0 ? 1.f : -1.f;
   o.lp = false;
   if (ev.degenerate) {
-    o.a = 0;
+    o.a = o.ak = 0;
     return;
   }
   const double ak = P.S.o[id] * sharpen(ev.g, P.S.tau[id]);
   o.a = ak;
+  o.ak = ak;
   if (g.has_proj) {
     const double f = low_pass_filter_term(xs(px, g.ppx), xs(py, g.ppy), fabs(denom), P.S.o[id], P.opt.lowpass_radius);
     if (f > ak) {
@@ -254,10 +286,10 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
     stage_record(P, id, tc, R);
     ++px.n_miss;
   }
-  const float dz = fmaf(R.r0.x, px.ddx, fmaf(R.r0.y, px.ddy, fmaf(R.r0.z, px.ddz, R.r0.w)));
-  const float nu = fmaf(R.r1.x, px.ddx, fmaf(R.r1.y, px.ddy, fmaf(R.r1.z, px.ddz, R.r1.w)));
-  const float nv = fmaf(R.r2.x, px.ddx, fmaf(R.r2.y, px.ddy, fmaf(R.r2.z, px.ddz, R.r2.w)));
-  const float inv = rcp_approx(dz);
+  const float dz = lin3(R.r0, R.r5.x, px.ddx, px.ddy, px.ddz);
+  const float nu = lin3(R.r1, R.r5.y, px.ddx, px.ddy, px.ddz);
+  const float nv = lin3(R.r2, R.r5.z, px.ddx, px.ddy, px.ddz);
+  const float inv = rcp_nr(dz);
   const float ainv = fabsf(inv);
   const float rel_z = R.r3.y * ainv;
   const float u = nu * inv, v = nv * inv;
@@ -268,9 +300,10 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
   bool use64 = rel_z > 1e-3f;
   double a64 = 0;
   if (!use64) {
-    // absolute error bound of u and v
-    const float du = ainv * R.r3.z + fabsf(u) * (rel_z + 3e-7f);
-    const float dv = ainv * R.r3.z + fabsf(v) * (rel_z + 3e-7f);
+    // absolute error bound of u and v (N error / |dz|, relative errors of dz,
+    // 1/dz and the product)
+    const float du = ainv * R.r3.z + fabsf(u) * (rel_z + 1.85e-7f);
+    const float dv = ainv * R.r3.z + fabsf(v) * (rel_z + 1.85e-7f);
     const float dp = fmaxf(du, dv);
     const float r2 = fmaf(u, u, v * v);
     const float au_ = fabsf(u), av_ = fabsf(v);
@@ -325,15 +358,15 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
     const float4 c0 = __ldg(reinterpret_cast<const float4*>(hd) + 2), c1 = __ldg(reinterpret_cast<const float4*>(hd) + 3);
     float ak, relk;
     if (r2 == 0.f) {
-      float cond;
-      ak = c1.w * sharpen_ps(c0, c1, 1.0f, &cond);
-      relk = 6e-7f + cond * 1e-6f;
+      float relP;
+      ak = c1.w * sharpen_ps(c0, c1, 1.0f, 1e-6f, &relP);
+      relk = relP + 2e-7f;
     } else {
       // angle from e_lo inside the bracket, delta = that * pi / gap
       const float cr = e.x * v - e.y * u, dt = e.x * u + e.y * v;
       const float dth = atan2_fast(cr, dt);
       const float delta = fmaxf(dth, 0.f) * f.y;
-      const float cd = __cosf(delta);
+      const float cd = cos_0pi(fminf(delta, 3.14159274f));
       const float hs = 0.5f * (f.z + f.w), hdiff = 0.5f * (f.z - f.w);
       const float inv_s = fmaf(hdiff, cd, hs);
       const float Q = fmaf(eta * r1, r1, (1.f - eta) * r2 * inv_s);
@@ -342,14 +375,14 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
       // absolute), rounding
       const float pabs = sqrtf(r2);
       const float dth_err = 2.5e-7f * dth + 2.5e-7f + 1.5f * dp / pabs;
-      const float dinv = fabsf(hdiff) * (dth_err * f.y + 2.4e-7f * delta + 6e-7f) + 2e-7f * (hs + fabsf(hdiff));
-      const float dQ = eta * (2.f * r1 * dr1 + dr1 * dr1) + (1.f - eta) * (r2 * dinv + inv_s * dr2) + 6e-7f * Q;
+      const float dinv = fabsf(hdiff) * (dth_err * f.y + 2.4e-7f * delta + 2e-7f) + 2e-7f * (hs + fabsf(hdiff));
+      const float dQ = eta * (2.f * r1 * dr1 + dr1 * dr1) + (1.f - eta) * (r2 * dinv + inv_s * dr2) + 3.6e-7f * Q;
       const float ex = fmaxf(-0.5f * Q, -30.0f);
       const float g = __expf(ex);
-      float cond;
-      const float Pv = sharpen_ps(c0, c1, g, &cond);
+      float relP;
+      const float Pv = sharpen_ps(c0, c1, g, 0.5f * dQ + 2.5e-7f + 7e-8f * fabsf(ex), &relP);
       ak = c1.w * Pv;
-      relk = cond * (0.5f * dQ + 2.5e-7f + 1.2e-7f * fabsf(ex)) + 6e-7f;
+      relk = relP + 2e-7f;
     }
     at = ak;
     relt = relk;
@@ -372,10 +405,19 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
     if (VALIDATE && !use64) {
       Pop64 o;
       pop_f64(P, id, x, y, o);
-      if (!o.degen && o.a >= 1e-4) {
-        const double ratio = fabs((double)at - o.a) / ((double)relt * at + 1e-30);
+      // where the floor is certainly out of reach (lp_possible false) the fp32
+      // path evaluates the kernel term alone: compare like with like
+      const double ref = lp_possible ? o.a : o.ak;
+      if (!o.degen && ref >= 1e-4) {
+        const double ratio = fabs((double)at - ref) / ((double)relt * at + 1e-30);
         atomicMax(P.vstat, (unsigned long long)__double_as_longlong(ratio));
-        atomicMax(P.vstat + 1, (unsigned long long)__double_as_longlong(fabs((double)at - o.a)));
+        atomicMax(P.vstat + 1, (unsigned long long)__double_as_longlong(fabs((double)at - ref)));
+        if (ratio > 1.0 && atomicCAS(P.vstat + 2, 0ull, 1ull) == 0ull) {
+          double* d = reinterpret_cast<double*>(P.vstat + 3);
+          d[0] = x; d[1] = y; d[2] = id; d[3] = u; d[4] = v; d[5] = at; d[6] = ref; d[7] = relt;
+          d[8] = lp_possible; d[9] = rel_z; d[10] = dp; d[11] = r1; d[12] = dr1; d[13] = lo;
+          d[14] = th; d[15] = ak; d[16] = relk; d[17] = o.a; d[18] = o.ak; d[19] = o.lp; d[20] = dz;
+        }
       }
     }
   }
@@ -545,16 +587,17 @@ __global__ void __launch_bounds__(256, 2) k_raster_fast(const __grid_constant__ 
         const int slot = jr & (kRing - 1);
         const float4 r0 = ring[slot].r0;
         const float2 r3 = *reinterpret_cast<const float2*>(&ring[slot].r3);
-        const float dz = fmaf(r0.x, px.ddx, fmaf(r0.y, px.ddy, fmaf(r0.z, px.ddz, r0.w)));
+        const float dz = lin3(r0, ring[slot].r5.x, px.ddx, px.ddy, px.ddz);
         const float adz = fabsf(dz);
         float lo, hi;
         if (adz < eps - r3.y) continue;  // certainly grazing
-        const float inv = rcp_approx(dz);
+        const float inv = rcp_nr(dz);
         const float rel_z = r3.y * fabsf(inv);
         if (adz > eps + r3.y && r3.x != 0.f && rel_z <= 1e-3f) {
           const float rt = r3.x * inv;
           if (rt <= 0.f) continue;
-          const float er = rt * (4.5e-7f + rel_z * 1.01f);
+          // num (2^-24), 1/dz (2^-23), product (2^-24), dz (rel_z), interval ends
+          const float er = rt * (3.3e-7f + rel_z * 1.01f);
           lo = rt - er;
           hi = rt + er;
         } else {
@@ -703,6 +746,7 @@ __global__ void __launch_bounds__(256, 2) k_raster_fast(const __grid_constant__ 
 }
 
 size_t raster_fast_smem() { return (size_t)kRing * (sizeof(Rec) + sizeof(int)) + 16 * kBatch * sizeof(float); }
+static_assert(sizeof(Rec) == 96, "ring record");
 
 bool raster_fast_eligible(const RasterParams& P) {
   return P.S.K == 8 && P.shrec != nullptr && P.opt.use_cache && !P.opt.exact_sort && !P.opt.fp64_alpha &&

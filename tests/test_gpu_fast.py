@@ -29,7 +29,7 @@ def _render(rast, sc, cam, opt, kernel):
     return fb, rast.stats()
 
 
-@pytest.mark.parametrize("cfg,crop", [(0, None), (1, 256), (2, 192)])
+@pytest.mark.parametrize("cfg,crop", [(0, None), (1, 256), (2, 192), (1, None), (2, None)])
 def test_fast_alpha_bound_in_situ(rast, cfg, crop):
     sc = scenes.config_scene(cfg)
     cam = scenes.config_cameras(cfg)[0]
