@@ -13,6 +13,11 @@ namespace drk {
 __global__ void k_prep0(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pool,
                         long long pool_cap, int* rowcnt, unsigned long long* counters, const int* list, int list_n,
                         double2* scratch, int scratch_cap, int* overflow);
+__global__ void k_prep_warp(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pts_pool,
+                            long long pts_cap, int2* ptsref, int* rowcnt, unsigned long long* counters, int* overflow);
+__global__ void k_prep_hull(int n, const int2* ptsref, double2* pts_pool, CamD cam, OptD opt, int4* bbox, int2* hullref,
+                            double2* pool, long long pool_cap, int* rowcnt, unsigned long long* counters);
+size_t prep_warp_smem();
 __global__ void k_prep1(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pool,
                         long long pool_cap, int* rowcnt, unsigned long long* counters, const int* list, int list_n,
                         double2* scratch, int scratch_cap, int* overflow);
@@ -178,20 +183,39 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   long long* rowoff = ensure<long long>(c->rowoff, n + 1);
   if (!ctr || !geo || !bbox || !hullref || !rowcnt || !rowoff) return set_error(c, DRK_ERR_OOM, "prep buffers");
   static_assert(sizeof(Geo) % 8 == 0, "Geo alignment");
-  if (c->hull_cap < (long long)n * 96 + 1024) c->hull_cap = (long long)n * 96 + 1024;
+  if (c->hull_cap < (long long)n * 48 + 1024) c->hull_cap = (long long)n * 48 + 1024;
+  if (c->pts_cap < (long long)n * 200 + 1024) c->pts_cap = (long long)n * 200 + 1024;
+  int2* ptsref = ensure<int2>(c->ptsref, n + 1);
+  if (!ptsref) return set_error(c, DRK_ERR_OOM, "point refs");
   // K1 with retry on hull-pool overflow
   DevBuf& ovf_buf = c->rows;  // reused as overflow list before rows are built
   for (int attempt = 0; attempt < 4; ++attempt) {
     double2* pool = ensure<double2>(c->hull, (size_t)c->hull_cap);
+    double2* ppool = ensure<double2>(c->ptspool, (size_t)c->pts_cap);
     int* ovf = ensure<int>(ovf_buf, n + 1);
-    if (!pool || !ovf) return set_error(c, DRK_ERR_OOM, "hull pool");
+    if (!pool || !ovf || !ppool) return set_error(c, DRK_ERR_OOM, "hull pool");
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT, s);
-    if (n > 0)
-      k_prep0<<<(n + 127) / 128, 128, 0, s>>>(A, cd, od, geo, bbox, hullref, pool, c->hull_cap, rowcnt, ctr,
-                                                nullptr, 0, nullptr, 0, ovf);
-    DRK_COUNT_LAUNCH();
+    if (n > 0) {
+      // warp per primitive; near-clipped / oversized polygons -> overflow list (k_prep1)
+      static bool attr = false;
+      const size_t smem = prep_warp_smem();
+      if (!attr) {
+        cudaFuncSetAttribute(k_prep_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+      }
+      k_prep_warp<<<(n + 7) / 8, 256, smem, s>>>(A, cd, od, geo, bbox, hullref, ppool, c->pts_cap, ptsref, rowcnt,
+                                                   ctr, ovf);
+      k_prep_hull<<<(unsigned)((2LL * n + 255) / 256), 256, 0, s>>>(n, ptsref, ppool, cd, od, bbox, hullref, pool,
+                                                                    c->hull_cap, rowcnt, ctr);
+    }
+    launch_counter() += 2;
     unsigned long long h[C_COUNT];
     if (int st = read_counters(c, h)) return st;
+    if ((long long)h[C_PTS_POOL] > c->pts_cap) {
+      c->pts_cap = (long long)h[C_PTS_POOL] + (long long)h[C_PTS_POOL] / 4 + 1024;
+      if (attempt == 3) return set_error(c, DRK_ERR_OOM, "point pool retries");
+      continue;
+    }
     const long long n_ovf = (long long)h[C_POLY_OVERFLOW];
     if (n_ovf > 0) {
       // large-polygon path: 64k-vertex scratch per primitive, batches of 256
@@ -495,7 +519,7 @@ void drk_ctx_destroy(drk_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
                     &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
-                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->rowcnt,
+                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->pk2, &c->pv2,
                     &c->hist, &c->sortoff, &c->tilecnt, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,

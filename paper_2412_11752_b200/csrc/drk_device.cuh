@@ -57,6 +57,7 @@ enum Counter {
   C_FP64_EVALS,        // pops re-evaluated in fp64 (decision within the fp32 bound)
   C_AMBIGUOUS,         // fast kernel: cache steps with overlapping depth intervals
   C_RING_MISS,         // fast kernel: pops re-staged from HBM (older than the ring)
+  C_PTS_POOL,          // K1: sorted-point pool cursor
   C_COUNT
 };
 

@@ -105,12 +105,13 @@ struct drk_ctx {
   drk::Activated act{};
 
   // per view
-  drk::DevBuf geo, bbox, hullref, hull, rowcnt, rowoff, rows, rowpaircnt, rowpairoff;
+  drk::DevBuf geo, bbox, hullref, hull, ptspool, ptsref, rowcnt, rowoff, rows, rowpaircnt, rowpairoff;
   drk::DevBuf pk, pv, pk2, pv2, hist, sortoff, tilecnt, tileoff, cdirs, tdirs, bits;
   drk::DevBuf pxstate, replay_cnt, replay_rec, replay_ids;
   drk::DevBuf gact, touched;
   drk::DevBuf counters, scan_tmp, loss_tmp;
   int64_t hull_cap = 0;
+  int64_t pts_cap = 0;
 
   // stage timing
   bool timing = false;

@@ -402,6 +402,413 @@ __device__ __forceinline__ void prep_body(Activated A, CamD cam, OptD opt, Geo* 
 }
 
 // ---------------------------------------------------------------------------
+// K1 warp-per-primitive variant (pass 0 of every primitive).  The adaptive
+// wedge tree (raster.cpp:178-207) is expanded breadth-first by the 32 lanes:
+// a leaf's two vertices are pure functions of its endpoint angles and
+// weights, so the vertex SET is the reference's whatever the traversal
+// order.  Without near clipping (every vertex at z >= 1e-6, the common case)
+// the polygon order is irrelevant to the hull: the projected vertices are
+// sorted (x, y) by a warp bitonic sort in shared memory and lane 0 runs the
+// reference's monotone chain, so the hull is bit-identical.  Primitives that
+// need the near clip (vertex order matters for Sutherland-Hodgman) or exceed
+// the per-warp buffers go to the serial k_prep1 path through the overflow list.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kPW = 8;          // warps per block
+constexpr int kWStack = 96;     // wedge work items per warp
+constexpr int kWVerts = 256;    // projected vertices per warp
+struct WItem {
+  double a0, a1, r0, i0, r1, i1, c0, s0, c1, s1;  // endpoint angles, weights, cos / sin
+  int depth, k;
+};
+struct BrP {
+  double alo, gap, slo, shi, elx, ely, ehx, ehy, det;
+  int coarse, first;
+};
+struct WarpScratch {
+  WItem stack[kWStack];
+  double2 verts[kWVerts + 8];
+  BrP br[kMaxK];
+};
+__device__ __forceinline__ PolyParams poly_params(const BrP& b, double eta, double support_c) {
+  PolyParams p;
+  p.alo = b.alo;
+  p.gap = b.gap;
+  p.slo = b.slo;
+  p.shi = b.shi;
+  p.elx = b.elx;
+  p.ely = b.ely;
+  p.ehx = b.ehx;
+  p.ehy = b.ehy;
+  p.det = b.det;
+  p.eta = eta;
+  p.support_c = support_c;
+  return p;
+}
+__device__ __forceinline__ bool lessp2(double2 a, double2 b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
+
+// One monotone chain of raster.cpp:46-56 over pts in forward (dir = 1) or
+// reverse order into h; the two top stack entries live in registers.
+__device__ int mono_chain(const double2* pts, int n, bool reverse, double2* h) {
+  int k = 0;
+  double2 a = make_double2(0, 0), b = a;  // h[k-2], h[k-1]
+  for (int t = 0; t < n; ++t) {
+    const double2 pt = pts[reverse ? n - 1 - t : t];
+    while (k >= 2 && cross2(a, b, pt) <= 0) {
+      --k;
+      b = a;
+      if (k >= 2) a = h[k - 2];
+    }
+    h[k++] = pt;
+    a = b;
+    b = pt;
+  }
+  return k;
+}
+}  // namespace
+
+size_t prep_warp_smem() { return (size_t)kPW * sizeof(WarpScratch); }
+
+// weight_at (raster.cpp:158-168) that also returns cos(a), sin(a) for the
+// wedge vertices at a (raster.cpp:199-201 evaluates the same cos/sin).
+__device__ __forceinline__ W2 weight_cs(const PolyParams& p, double a, double* ca, double* sa) {
+  const double delta = (a - p.alo) * kPi / p.gap;
+  const double c = cos(delta);
+  W2 w;
+  w.inv = (1.0 + c) / (2.0 * p.slo * p.slo) + (1.0 - c) / (2.0 * p.shi * p.shi);
+  double dx, dy;
+  sincos(a, &dy, &dx);
+  *ca = dx;
+  *sa = dy;
+  const double cva = (p.ehy * dx - p.ehx * dy) / p.det;
+  const double cvb = (-p.ely * dx + p.elx * dy) / p.det;
+  w.rho1 = fabs(cva) + fabs(cvb);
+  return w;
+}
+
+// Phase A: vertices -> sorted unique points in the point pool.  ptsref[i] =
+// (offset, count) of the sorted points; the pool slot holds 3 count entries
+// (points, lower chain, upper chain) for k_prep_hull.
+__global__ void __launch_bounds__(kPW * 32) k_prep_warp(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox,
+                                                         int2* hullref, double2* pts_pool, long long pts_cap,
+                                                         int2* ptsref, int* rowcnt, unsigned long long* counters,
+                                                         int* overflow) {
+  extern __shared__ double4 prep_dyn[];
+  const unsigned FULL = 0xffffffffu;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kPW + warp;
+  if (i >= A.n) return;  // warp-uniform
+  WarpScratch& W = reinterpret_cast<WarpScratch*>(prep_dyn)[warp];
+  const int K = A.K;
+  double f = 0, fv = 0;
+  const double o = A.o[i];
+  const bool visible = binning_radius_factor(o, A.tau[i], opt.alpha_min, &f, &fv);
+  if (lane == 0) {
+    // per-view geometry record (as prep_body pass 0)
+    Geo g;
+    const double* R = A.rot + 9 * (size_t)i;
+    for (int a = 0; a < 3; ++a) {
+      g.mu[a] = A.mu[3 * i + a];
+      g.rx[a] = R[3 * a];
+      g.ry[a] = R[3 * a + 1];
+      g.rz[a] = R[3 * a + 2];
+    }
+    const double m0 = g.mu[0] - cam.o[0], m1 = g.mu[1] - cam.o[1], m2 = g.mu[2] - cam.o[2];
+    g.num = m0 * g.rz[0] + m1 * g.rz[1] + m2 * g.rz[2];
+    double pr[3];
+    g.has_proj = try_project(cam, g.mu, pr) ? 1 : 0;
+    g.ppx = g.has_proj ? pr[0] : 0.0;
+    g.ppy = g.has_proj ? pr[1] : 0.0;
+    g.projz = g.has_proj ? pr[2] : __longlong_as_double(0x7ff0000000000000ll);
+    g.visible = visible ? 1 : 0;
+    double smax = 0;
+    for (int j = 0; j < K; ++j) smax = dmax(smax, A.s[(size_t)K * i + j]);
+    g.r2max = visible ? (smax * fv) * (smax * fv) * (1.0 + 1e-9) : 0.0;
+    const_cast<float*>(A.psif)[12 * (size_t)i + 8] = visible ? (float)(fv * fv) : __int_as_float(0x7f800000);
+    g.dp2max = visible ? 2.0 * opt.lowpass_radius * opt.lowpass_radius * log(o / opt.alpha_min) * (1.0 + 1e-9) : 0.0;
+    geo[i] = g;
+    rowcnt[i] = 0;
+    bbox[i] = make_int4(1, 0, 1, 0);
+    hullref[i] = make_int2(0, 0);
+    ptsref[i] = make_int2(0, 0);
+  }
+  if (!visible) return;
+  const double eta = A.eta[i];
+  const double support_c = f * f;
+  const double* s = A.s + (size_t)K * i;
+  const double* th = A.th + (size_t)K * i;
+  // bracket parameters (raster.cpp:146-153) and coarse wedge counts (:202)
+  int coarse = 0;
+  BrP b;
+  if (lane < K) {
+    const int k = lane, hi = (k + 1) % K;
+    b.alo = k + 1 < K ? th[k] : th[k] - 2.0 * kPi;
+    const double ahi = k + 1 < K ? th[hi] : th[0];
+    b.gap = ahi - b.alo;
+    b.slo = s[k];
+    b.shi = s[hi];
+    b.elx = A.ex[(size_t)K * i + k];
+    b.ely = A.ey[(size_t)K * i + k];
+    b.ehx = A.ex[(size_t)K * i + hi];
+    b.ehy = A.ey[(size_t)K * i + hi];
+    b.det = A.det[(size_t)K * i + k];
+    const int ci = (int)ceil(b.gap / (kPi / 8.0));
+    coarse = ci > 1 ? ci : 1;
+    b.coarse = coarse;
+  }
+  int incl = coarse;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(FULL, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane < K) {
+    b.first = incl - coarse;
+    W.br[lane] = b;
+  }
+  const int total = (int)__reduce_add_sync(FULL, (unsigned)coarse);
+  __syncwarp();
+  bool fail = total > kWStack - 16;
+  // coarse wedges with their endpoint weights (and cos / sin of the endpoints)
+  if (!fail) {
+    for (int idx = lane; idx < total; idx += 32) {
+      int k = 0;
+      while (k + 1 < K && W.br[k + 1].first <= idx) ++k;
+      const BrP& bk = W.br[k];
+      const int j = idx - bk.first;
+      const PolyParams p = poly_params(bk, eta, support_c);
+      const double a0 = bk.alo + bk.gap * j / bk.coarse;
+      const double a1 = bk.alo + bk.gap * (j + 1) / bk.coarse;
+      WItem it;
+      const W2 w0 = weight_cs(p, a0, &it.c0, &it.s0), w1 = weight_cs(p, a1, &it.c1, &it.s1);
+      it.a0 = a0;
+      it.a1 = a1;
+      it.r0 = w0.rho1;
+      it.i0 = w0.inv;
+      it.r1 = w1.rho1;
+      it.i1 = w1.inv;
+      it.depth = 0;
+      it.k = k;
+      W.stack[idx] = it;
+    }
+  }
+  __syncwarp();
+  int sp = fail ? 0 : total, nv = 0;
+  const double mu[3] = {A.mu[3 * i], A.mu[3 * i + 1], A.mu[3 * i + 2]};
+  const double* R = A.rot + 9 * (size_t)i;
+  const double rx[3] = {R[0], R[3], R[6]}, ry[3] = {R[1], R[4], R[7]};
+  while (sp > 0 && !fail) {
+    // batch size throttled by the free stack space: with few free slots the
+    // LIFO walk is depth-first and grows the stack by at most one item per
+    // tree level (depth <= 9), so it never overflows
+    const int room = (kWStack - 12 - sp) / 2;
+    int m = sp < 32 ? sp : 32;
+    m = m < room ? m : (room > 1 ? room : 1);
+    const int base = sp - m;
+    WItem it;
+    if (lane < m) it = W.stack[base + lane];
+    __syncwarp();
+    bool split = false, leaf = false;
+    double bound = 0, mid = 0, cm = 0, sm_ = 0;
+    W2 wm;
+    if (lane < m) {
+      const PolyParams p = poly_params(W.br[it.k], eta, support_c);
+      const W2 w0{it.r0, it.i0}, w1{it.r1, it.i1};
+      const double rho1_min = dmin(w0.rho1, w1.rho1);
+      const double inv_min = dmin(w0.inv, w1.inv);
+      const double w_lb = p.eta * rho1_min * rho1_min + (1.0 - p.eta) * inv_min;
+      bound = sqrt(p.support_c / dmax(w_lb, 1e-12)) / cos(0.5 * (it.a1 - it.a0));
+      if (it.depth < 9 && it.a1 - it.a0 > 2e-3 && bound > 1.25 * dmin(radius_true(p, w0), radius_true(p, w1))) {
+        split = true;
+        mid = 0.5 * (it.a0 + it.a1);
+        wm = weight_cs(p, mid, &cm, &sm_);
+      } else {
+        leaf = true;
+      }
+    }
+    const unsigned smk = __ballot_sync(FULL, split), lmk = __ballot_sync(FULL, leaf);
+    const unsigned below = (1u << lane) - 1u;
+    const int n_split = __popc(smk), n_leaf = __popc(lmk);
+    if (base + 2 * n_split > kWStack || nv + 2 * n_leaf > kWVerts) {
+      fail = true;
+      break;
+    }
+    if (split) {
+      const int slot = base + 2 * __popc(smk & below);
+      WItem l = it, r = it;
+      l.a1 = mid;
+      l.r1 = wm.rho1;
+      l.i1 = wm.inv;
+      l.c1 = cm;
+      l.s1 = sm_;
+      r.a0 = mid;
+      r.r0 = wm.rho1;
+      r.i0 = wm.inv;
+      r.c0 = cm;
+      r.s0 = sm_;
+      l.depth = r.depth = it.depth + 1;
+      W.stack[slot] = l;
+      W.stack[slot + 1] = r;
+    }
+    bool clip = false;
+    if (leaf) {
+      const int slot = nv + 2 * __popc(lmk & below);
+      const double cs[2][2] = {{it.c0, it.s0}, {it.c1, it.s1}};
+      for (int e = 0; e < 2; ++e) {
+        double w[3], pc[3];
+        for (int a = 0; a < 3; ++a) w[a] = mu[a] + bound * (cs[e][0] * rx[a] + cs[e][1] * ry[a]);
+        to_camera(cam, w, pc);
+        clip |= !(pc[2] >= kNearClip);
+        W.verts[slot + e] = make_double2(cam.fx * pc[0] / pc[2] + cam.cx, cam.fy * pc[1] / pc[2] + cam.cy);
+      }
+    }
+    if (__any_sync(FULL, clip)) {
+      fail = true;
+      break;
+    }
+    sp = base + 2 * n_split;
+    nv += 2 * n_leaf;
+    __syncwarp();
+  }
+  if (fail) {
+    // serial path with the near clip and large buffers (k_prep1)
+    if (lane == 0) {
+      const unsigned long long slot = atomicAdd(&counters[C_POLY_OVERFLOW], 1ull);
+      overflow[slot] = i;
+    }
+    return;
+  }
+  if (nv == 0) return;
+  // bitonic sort of the projected vertices by (x, y) (raster.cpp:35-37)
+  int P2 = 2;
+  while (P2 < nv) P2 <<= 1;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  for (int t = nv + lane; t < P2; t += 32) W.verts[t] = make_double2(inf, inf);
+  __syncwarp();
+  for (int kk = 2; kk <= P2; kk <<= 1) {
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (int t = lane; t < P2; t += 32) {
+        const int u = t ^ jj;
+        if (u > t) {
+          const double2 a = W.verts[t], c = W.verts[u];
+          const bool up = (t & kk) == 0;
+          if (up ? lessp2(c, a) : lessp2(a, c)) {
+            W.verts[t] = c;
+            W.verts[u] = a;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  // unique (raster.cpp:38-40), compacted in place (reads precede writes in
+  // every 32-wide chunk)
+  int n_u = 0;
+  for (int t0 = 0; t0 < nv; t0 += 32) {
+    const int t = t0 + lane;
+    bool keep = false;
+    double2 v;
+    if (t < nv) {
+      v = W.verts[t];
+      keep = t == 0 || !(v.x == W.verts[t - 1].x && v.y == W.verts[t - 1].y);
+    }
+    const unsigned km = __ballot_sync(FULL, keep);
+    if (keep) W.verts[n_u + __popc(km & ((1u << lane) - 1u))] = v;
+    n_u += __popc(km);
+    __syncwarp();
+  }
+  long long off = 0;
+  if (lane == 0) off = (long long)atomicAdd(&counters[C_PTS_POOL], (unsigned long long)(3 * n_u + 2));
+  off = __shfl_sync(FULL, off, 0);
+  if (off + 3 * n_u + 2 > pts_cap) return;  // host detects via the cursor and retries with a larger pool
+  for (int t = lane; t < n_u; t += 32) pts_pool[off + t] = W.verts[t];
+  if (lane == 0) ptsref[i] = make_int2((int)off, n_u);
+}
+
+// Phase B: Andrew's monotone chain (raster.cpp:41-57) with two threads per
+// primitive.  The upper chain only ever pops its own entries (k >= lower),
+// so it is the chain over the reversed points: thread 2p builds the lower
+// chain, thread 2p+1 the upper; hull = lower + upper without its first (the
+// rightmost point) and last (the leftmost).  Then bbox and tile range
+// (raster.cpp:219-231) and the hull into the hull pool.
+__global__ void __launch_bounds__(256) k_prep_hull(int n, const int2* __restrict__ ptsref, double2* pts_pool,
+                                                    CamD cam, OptD opt, int4* bbox, int2* hullref, double2* pool,
+                                                    long long pool_cap, int* rowcnt, unsigned long long* counters) {
+  const unsigned FULL = 0xffffffffu;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int i = (int)(t >> 1);
+  const bool upper = (t & 1) != 0;
+  int2 pr = make_int2(0, 0);
+  if (i < n) pr = ptsref[i];
+  const int n_u = pr.y;
+  const double2* pts = pts_pool + pr.x;
+  int len = 0;
+  if (n_u > 2) len = mono_chain(pts, n_u, upper, pts_pool + pr.x + (upper ? 2 * n_u + 1 : n_u));
+  const int other = __shfl_xor_sync(FULL, len, 1);
+  if (n_u == 0) return;
+  const int L = upper ? other : len, U = upper ? len : other;
+  const int hn = n_u <= 2 ? n_u : L + U - 2;
+  // my part of the hull: lower [0, L) from the even thread, upper [1, U-1) from the odd one
+  const double2* src = n_u <= 2 ? pts : (upper ? pts_pool + pr.x + 2 * n_u + 1 + 1 : pts_pool + pr.x + n_u);
+  const int cnt = n_u <= 2 ? (upper ? 0 : n_u) : (upper ? U - 2 : L);
+  const int dst = upper ? L : 0;
+  double hx0 = 0, hx1 = 0, hy0 = 0, hy1 = 0;
+  bool any = false;
+  for (int j = 0; j < cnt; ++j) {
+    const double2 v = src[j];
+    if (!any) {
+      hx0 = hx1 = v.x;
+      hy0 = hy1 = v.y;
+      any = true;
+    } else {
+      hx0 = dmin(hx0, v.x);
+      hx1 = dmax(hx1, v.x);
+      hy0 = dmin(hy0, v.y);
+      hy1 = dmax(hy1, v.y);
+    }
+  }
+  // combine the two halves (the pair is always in one warp and both reach here)
+  const unsigned pair = 3u << ((threadIdx.x & 31) & ~1);
+  const double ox0 = __shfl_xor_sync(pair, hx0, 1), ox1 = __shfl_xor_sync(pair, hx1, 1);
+  const double oy0 = __shfl_xor_sync(pair, hy0, 1), oy1 = __shfl_xor_sync(pair, hy1, 1);
+  const bool oany = __shfl_xor_sync(pair, any, 1);
+  if (oany) {
+    if (!any) {
+      hx0 = ox0;
+      hx1 = ox1;
+      hy0 = oy0;
+      hy1 = oy1;
+    } else {
+      hx0 = dmin(hx0, ox0);
+      hx1 = dmax(hx1, ox1);
+      hy0 = dmin(hy0, oy0);
+      hy1 = dmax(hy1, oy1);
+    }
+  }
+  const double lp = opt.lp_pad;
+  int tx0 = x86_int(floor((hx0 - lp) / kTile));
+  tx0 = tx0 > 0 ? tx0 : 0;
+  int tx1 = x86_int(floor((hx1 + lp) / kTile));
+  tx1 = tx1 < cam.tiles_x - 1 ? tx1 : cam.tiles_x - 1;
+  int ty0 = x86_int(floor((hy0 - lp) / kTile));
+  ty0 = ty0 > 0 ? ty0 : 0;
+  int ty1 = x86_int(floor((hy1 + lp) / kTile));
+  ty1 = ty1 < cam.tiles_y - 1 ? ty1 : cam.tiles_y - 1;
+  if (tx1 < tx0 || ty1 < ty0) return;
+  long long off = 0;
+  if (!upper) off = (long long)atomicAdd(&counters[C_HULL_POOL], (unsigned long long)hn);
+  off = __shfl_xor_sync(pair, off, 1) + (upper ? 0 : off);
+  if (off + hn > pool_cap) return;  // host detects via the cursor and retries with a larger pool
+  for (int j = 0; j < cnt; ++j) pool[off + dst + j] = src[j];
+  if (!upper) {
+    hullref[i] = make_int2((int)off, hn);
+    bbox[i] = make_int4(tx0, tx1, ty0, ty1);
+    rowcnt[i] = ty1 - ty0 + 1;
+    atomicAdd(&counters[C_VISIBLE], 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2: per-row tile intervals.  For a convex hull H and the dilated row band
 // B = [Y0, Y1], a dilated tile rectangle overlaps H iff its x-range meets the
 // x-extent of H ∩ B.  That is the geometric content of the reference's
