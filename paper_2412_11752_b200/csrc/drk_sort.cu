@@ -141,12 +141,18 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_hist(const unsigned long long
   hist[(size_t)threadIdx.x * nblk + blockIdx.x] = cnt[threadIdx.x];
 }
 
+// One stable LSD pass: per-warp match-based ranks, block-local digit order
+// staged in shared memory, then written out digit run by digit run so that
+// consecutive threads store consecutive addresses of one bucket.
 __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned long long* __restrict__ kin,
                                                            const unsigned long long* __restrict__ vin,
                                                            unsigned long long* kout, unsigned long long* vout,
                                                            long long n, int shift, int digit_from_v,
                                                            const long long* __restrict__ offs, int nblk) {
   __shared__ unsigned whist[kRsWarps][256];
+  __shared__ unsigned bstart[256];
+  __shared__ long long gbase[256];
+  __shared__ unsigned long long sk[kRsChunk], sv[kRsChunk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int d = threadIdx.x; d < kRsWarps * 256; d += kRsThreads) (&whist[0][0])[d] = 0;
   __syncthreads();
@@ -173,6 +179,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned long l
   }
   __syncthreads();
   {
+    // per digit: warp offsets (in warp order) and the block total
     const int d = threadIdx.x;  // kRsThreads == 256 digits
     unsigned run = 0;
     for (int w = 0; w < kRsWarps; ++w) {
@@ -180,14 +187,38 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned long l
       whist[w][d] = run;
       run += t;
     }
+    // block-local digit starts: exclusive scan of the totals over digits
+    unsigned incl = run;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    bstart[d] = incl;  // warp-inclusive for now
+    __syncthreads();
+    unsigned wsum = 0;
+    for (int w = 0; w < warp; ++w) wsum += bstart[w * 32 + 31];
+    __syncthreads();
+    bstart[d] = wsum + incl - run;
+    gbase[d] = offs[(size_t)d * nblk + blockIdx.x];
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRsItems; ++r) {
     if (dig[r] == 256) continue;
-    const long long pos = offs[(size_t)dig[r] * nblk + blockIdx.x] + whist[warp][dig[r]] + rank[r];
-    kout[pos] = kk[r];
-    vout[pos] = vv[r];
+    const unsigned pos = bstart[dig[r]] + whist[warp][dig[r]] + rank[r];
+    sk[pos] = kk[r];
+    sv[pos] = vv[r];
+  }
+  __syncthreads();
+  const long long cnt_ll = n - (long long)blockIdx.x * kRsChunk;
+  const int cnt = cnt_ll < kRsChunk ? (int)cnt_ll : kRsChunk;
+  for (int idx = threadIdx.x; idx < cnt; idx += kRsThreads) {
+    const unsigned long long key = sk[idx], val = sv[idx];
+    const int d = (int)((unsigned)((digit_from_v ? val : key) >> shift) & 255u);
+    const long long pos = gbase[d] + (idx - (long long)bstart[d]);
+    kout[pos] = key;
+    vout[pos] = val;
   }
 }
 
