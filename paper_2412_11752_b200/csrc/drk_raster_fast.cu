@@ -270,22 +270,23 @@ struct FastPixel {
   bool uncertain, err;
 };
 
+// composite_candidate up to the blend (raster.cpp:327-348) for one entry:
+// tangent coordinates from the staged record, cheap rejects, fp32 alpha with
+// its error bound, fp64 re-evaluation of decisions inside the bound.
+struct AlphaOut {
+  double a;     // clamped alpha (valid unless skip / degen)
+  float rel;    // relative error bound of a (0: exact fp64)
+  float rt;     // depth
+  float sgn;    // normal sign (raster.cpp:350-351)
+  bool skip;    // below alpha_min (or rejected): not composited
+  bool degen;   // DegenerateBasisError (core.cpp:191)
+};
+
 template <bool VALIDATE>
-__device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, const float* s_basis, const Rec* ring,
-                                         const int* s_id, const TileConst& tc, long long beg, int ring_lo, int jr,
-                                         int x, int y) {
-  ++px.n_pop;
-  Rec R;
-  int id;
-  if (jr >= ring_lo) {
-    const int slot = jr & (kRing - 1);
-    R = ring[slot];
-    id = s_id[slot];
-  } else {
-    id = (int)(P.pv[beg + jr] & 0xffffffffull);
-    stage_record(P, id, tc, R);
-    ++px.n_miss;
-  }
+__device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px, const Rec& R, int id, int x, int y,
+                                            AlphaOut& out) {
+  out.skip = false;
+  out.degen = false;
   const float dz = lin3(R.r0, R.r5.x, px.ddx, px.ddy, px.ddz);
   const float nu = lin3(R.r1, R.r5.y, px.ddx, px.ddy, px.ddz);
   const float nv = lin3(R.r2, R.r5.z, px.ddx, px.ddy, px.ddz);
@@ -299,6 +300,7 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
   float at = 0.f, relt = 0.f;
   bool use64 = rel_z > 1e-3f;
   double a64 = 0;
+  (void)px;
   if (!use64) {
     // absolute error bound of u and v (N error / |dz|, relative errors of dz,
     // 1/dz and the product)
@@ -319,7 +321,8 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
     }
     if (r2 - dr2 > R.r3.w * 1.000001f && !lp_possible) {
       ++px.n_rej1;
-      return true;
+      out.skip = true;
+      return;
     }
     // ---- alpha = o Psi(g(u, v)) (core.cpp:148-265) ----
     const float* hd = P.shrec + (size_t)kRecStride * id;
@@ -335,8 +338,8 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
     const float4* bp = reinterpret_cast<const float4*>(hd + kRecHdr + 8 * lo);
     const float4 e = __ldg(bp), f = __ldg(bp + 1);  // (elx, ely, ehx, ehy), (1/det, pi/gap, h_lo, h_hi)
     if (isnan(f.x)) {
-      px.err = true;
-      return false;
+      out.degen = true;
+      return;
     }
     const float eta = __ldg(hd + 16);
     const float ka = (e.w * u - e.z * v) * f.x;
@@ -352,7 +355,8 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
       const float qlb = eta * r1l * r1l + (1.f - eta) * fmaxf(r2 - dr2, 0.f) * hmin;
       if (qlb > fvis2 * 1.00002f && !lp_possible) {
         ++px.n_rej2;
-        return true;
+        out.skip = true;
+        return;
       }
     }
     const float4 c0 = __ldg(reinterpret_cast<const float4*>(hd) + 2), c1 = __ldg(reinterpret_cast<const float4*>(hd) + 3);
@@ -426,20 +430,34 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
     Pop64 o;
     pop_f64(P, id, x, y, o);
     if (o.degen) {
-      px.err = true;
-      return false;
+      out.degen = true;
+      return;
     }
     a64 = o.a;
     rt = (float)o.rt;
     sgn = o.sgn;
     relt = 0.f;
-    if (a64 < P.opt.alpha_min) return true;
+    if (a64 < P.opt.alpha_min) {
+      out.skip = true;
+      return;
+    }
     a64 = dmin(a64, 1.0 - 1e-6);
   } else {
-    if (at < amin) return true;
+    if (at < amin) {
+      out.skip = true;
+      return;
+    }
     a64 = dmin((double)at, 1.0 - 1e-6);
   }
-  // ---- blend (raster.cpp:349-361) ----
+  out.a = a64;
+  out.rel = relt;
+  out.rt = rt;
+  out.sgn = sgn;
+}
+// blend (raster.cpp:349-361): colour from SH, accumulation, transmittance
+// and its error bound; returns false once the pixel saturates.
+__device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, const float* s_basis, int id, double a64,
+                                      float relt, float rt, float sgn, float rz0, float rz1, float rz2) {
   const float* shp = P.sh + (size_t)id * P.terms * 3;
   float c0 = 0.5f, c1 = 0.5f, c2 = 0.5f;
   const int ta = P.opt.terms_active;
@@ -482,9 +500,9 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
   px.C2 = fmaf(w, c2, px.C2);
   px.D = fmaf(w, rt, px.D);
   const float ws = w * sgn;
-  px.N0 = fmaf(ws, R.r0.x, px.N0);
-  px.N1 = fmaf(ws, R.r0.y, px.N1);
-  px.N2 = fmaf(ws, R.r0.z, px.N2);
+  px.N0 = fmaf(ws, rz0, px.N0);
+  px.N1 = fmaf(ws, rz1, px.N1);
+  px.N2 = fmaf(ws, rz2, px.N2);
   px.A += w;
   px.T = xm(px.T, xs(1.0, a64));
   ++px.ncomp;
@@ -501,7 +519,33 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
 }
 
 template <bool VALIDATE>
-__global__ void __launch_bounds__(256, 2) k_raster_fast(const __grid_constant__ RasterParams P) {
+__device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, const float* s_basis, const Rec* ring,
+                                         const int* s_id, const TileConst& tc, long long beg, int ring_lo, int jr,
+                                         int x, int y) {
+  ++px.n_pop;
+  Rec R;
+  int id;
+  if (jr >= ring_lo) {
+    const int slot = jr & (kRing - 1);
+    R = ring[slot];
+    id = s_id[slot];
+  } else {
+    id = (int)(P.pv[beg + jr] & 0xffffffffull);
+    stage_record(P, id, tc, R);
+    ++px.n_miss;
+  }
+  AlphaOut o;
+  alpha_entry<VALIDATE>(P, px, R, id, x, y, o);
+  if (o.degen) {
+    px.err = true;
+    return false;
+  }
+  if (o.skip) return true;
+  return blend(P, px, s_basis, id, o.a, o.rel, o.rt, o.sgn, R.r0.x, R.r0.y, R.r0.z);
+}
+
+template <bool VALIDATE, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant__ RasterParams P) {
   extern __shared__ float4 dyn[];
   Rec* ring = reinterpret_cast<Rec*>(dyn);
   int* s_id = reinterpret_cast<int*>(ring + kRing);
@@ -757,12 +801,12 @@ void launch_raster_fast(const RasterParams& P, int n_tiles, bool validate, cudaS
   const size_t smem = raster_fast_smem();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_raster_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_raster_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_raster_fast<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_raster_fast<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  if (validate) k_raster_fast<true><<<n_tiles, 256, smem, s>>>(P);
-  else k_raster_fast<false><<<n_tiles, 256, smem, s>>>(P);
+  if (validate) k_raster_fast<true, 2><<<n_tiles, 256, smem, s>>>(P);
+  else k_raster_fast<false, 2><<<n_tiles, 256, smem, s>>>(P);
 }
 
 }  // namespace drk

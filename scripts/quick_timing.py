@@ -1,5 +1,5 @@
 """Quick per-config forward / backward timing (development aid)."""
-import sys, time
+import os, sys, time
 import numpy as np, torch
 sys.path.insert(0, '.')
 from paper_2412_11752_b200 import scenes
@@ -13,7 +13,7 @@ for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:
     sc = scenes.config_scene(cfg)
     cam = scenes.config_cameras(cfg)[0]
     raw = torch.from_numpy(sc.f32()).cuda()
-    opt = RenderOptions(sh_degree=scenes.CONFIGS[cfg]['sh_degree'])
+    opt = RenderOptions(sh_degree=scenes.CONFIGS[cfg]['sh_degree'], raster_kernel=int(os.environ.get('RK', '0')))
     for _ in range(2):
         fb = r.render(raw, cam, opt)
     torch.cuda.synchronize()
