@@ -234,8 +234,14 @@ def main():
     achieved = flops / (rast_ms * 1e-3) / 1e12
     stage_ms = {k: v / args.steps for k, v in stage_acc.items() if k in ("activate", "preprocess", "rows_emit", "sort",
                                                                          "raster", "raster_fp64")}
-    roofline = {"kernel": "k_raster<0,false,false> (fp32-alpha pass)", "bound": "fp32", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+    traffic = None
+    try:  # DRAM bytes of the dominant kernel from the committed ncu --set full capture (profiles/)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get("k_raster_fast")
+    except (OSError, ValueError):
+        traffic = None
+    roofline = {"kernel": "k_raster_fast (fp32 interval pass)", "bound": "fp32", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": "FFMA microbenchmark (drk_measure_fp32_peak) in this run; MEASURED_PEAKS.json has no "
                                "FP32 CUDA-core figure",
                 "algorithmic_flops_per_launch": flops, "kernel_ms": rast_ms,
@@ -330,7 +336,8 @@ def main():
         line = {"metric": "megapixels/sec rendered (forward; fwd+bwd in fwd_bwd)", "value": value,
                 "unit": "megapixels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f32 (fp64 ray-plane depths, sort keys and accumulators; fp32 alpha with fp64 fallback)",
+                "dtype": "f32 (fp32 tile-linearised intersections and alpha with error bounds; fp64 at ties, sort keys "
+                         "and transmittance)",
                 "data": "synthetic (seeded scenes.py generator; BASELINE.json config 1 distributions)",
                 "config": {"workload": "config1 forward: 100k DRK, K=8, SH degree 3, 1920x1080, 1 view per GPU per step",
                            "primitives": 100000, "K": 8, "sh_degree": 3, "width": 1920, "height": 1080,
