@@ -52,8 +52,9 @@ class RenderOptions:
     exact_sort: bool = False
     presort: PresortMode = PresortMode.NearestDepth
     early_stop_transmittance: float = 1e-4
-    # B200 extension (not in the reference): 0 = fp32 interval kernel where
-    # eligible (SortCache mode, K = 8), 1 = legacy fp64-depth kernel
+    # B200 extension (not in the reference): 0 = fp32 interval forward where
+    # eligible (SortCache mode, K = 8), 1 = legacy fp64-depth forward,
+    # 4 = 0 plus the fp32 interval backward (drk_raster_bwd.cu)
     raster_kernel: int = 0
 
 

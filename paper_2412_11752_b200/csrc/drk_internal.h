@@ -87,6 +87,7 @@ struct RasterParams {
 void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s, cudaEvent_t mid = nullptr);
 bool raster_fast_eligible(const RasterParams& P);
 void launch_raster_fast(const RasterParams& P, int n_tiles, bool validate, cudaStream_t s);
+void launch_raster_bwd_fast(const RasterParams& P, int n_tiles, cudaStream_t s);
 void launch_shape_rec(const ShapeView& S, int n, float* rec, cudaStream_t s);
 double measure_fp32_peak(cudaStream_t s);
 void launch_backward_serial(const RasterParams& P, cudaStream_t s);

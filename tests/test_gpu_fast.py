@@ -87,3 +87,20 @@ def test_fast_backward_termination_from_forward(rast):
     og = port.backward(sc, cam, o, dc, None, None, None)
     assert rel_l2(g.raw.cpu().numpy(), og["raw"]) <= 1e-3
     np.testing.assert_array_equal(g.touched.cpu().numpy(), og["touched"])
+
+
+def test_fast_backward_kernel_parity(rast):
+    """The opt-in fp32 interval backward (raster_kernel=4) against the oracle."""
+    import dataclasses
+    from paper_2412_11752_b200.api import FrameGrad
+    sc, cam = small_scene(seed=41, n=150, sh_degree=3, clusters=2)
+    o = opt_for(3)
+    opt = dataclasses.replace(api_options(o), raster_kernel=4)
+    rast.render(sc.f32(), cam, opt)
+    rng = np.random.default_rng(5)
+    dc = rng.uniform(-1, 1, (cam.height, cam.width, 3)).astype(np.float32)
+    dd = rng.uniform(-0.1, 0.1, (cam.height, cam.width)).astype(np.float32)
+    g = rast.backward_render(sc.f32(), FrameGrad(d_color=torch.from_numpy(dc), d_depth=torch.from_numpy(dd)))
+    og = port.backward(sc, cam, o, dc, dd, None, None)
+    assert rel_l2(g.raw.cpu().numpy(), og["raw"]) <= 1e-3
+    np.testing.assert_array_equal(g.touched.cpu().numpy(), og["touched"])
