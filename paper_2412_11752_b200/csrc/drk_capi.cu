@@ -24,6 +24,9 @@ __global__ void k_prep1(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, i
 __global__ void k_rows(int n, const int4* bbox, const int2* hullref, const double2* pool, const long long* rowoff,
                        CamD cam, OptD opt, int4* rows, int* rowpaircnt, unsigned long long* counters);
 __global__ void k_tile_rays(CamD cam, double* cdirs, double* tdirs);
+__global__ void k_emit_rows(long long n_rows, const int4* rows, const long long* rowpairoff, const Geo* geo,
+                            const double* cdirs, const double* tdirs, CamD cam, OptD opt, unsigned long long* pk,
+                            unsigned long long* pv, int* tilecnt);
 __global__ void k_emit(long long n_rows, const int4* rows, const long long* rowpairoff, const Geo* geo,
                        const double* cdirs, const double* tdirs, CamD cam, OptD opt, unsigned long long* pk,
                        unsigned long long* pv, int* tilecnt);
@@ -280,8 +283,8 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     k_tile_rays<<<(nr + 127) / 128, 128, 0, s>>>(cd, cdirs, tdirs);
   }
   if (n_rows > 0)
-    k_emit<<<(unsigned)((n_rows + 127) / 128), 128, 0, s>>>(n_rows, rows, rowpairoff, geo, cdirs, tdirs, cd, od, pk,
-                                                            pv, tilecnt);
+    k_emit_rows<<<(unsigned)((n_rows * 16 + 255) / 256), 256, 0, s>>>(n_rows, rows, rowpairoff, geo, cdirs, tdirs, cd,
+                                                                      od, pk, pv, tilecnt);
   launch_counter() += 3;
   mark(c, 3);
   if (int st = sort_pairs(c, pk, pv, pk2, pv2, n_pairs)) return st;

@@ -1011,6 +1011,68 @@ __global__ void k_emit(long long n_rows, const int4* __restrict__ rows, const lo
   }
 }
 
+// K3 with 16 lanes per row: lane l owns tile ta + l (chunks of 16), evaluates
+// its left corner rays and its centre ray, and takes the right corners from
+// lane l + 1 (the last lane of a chunk evaluates them itself), so a row of m
+// tiles costs ~3m ray-plane depths instead of 5m.  The key is the minimum of the
+// five depths (raster.cpp:99-115; min is symmetric for the positive depths).
+constexpr int kEmitLanes = 16;
+__global__ void __launch_bounds__(256) k_emit_rows(long long n_rows, const int4* __restrict__ rows,
+                                                   const long long* __restrict__ rowpairoff,
+                                                   const Geo* __restrict__ geo, const double* __restrict__ cdirs,
+                                                   const double* __restrict__ tdirs, CamD cam, OptD opt,
+                                                   unsigned long long* pk, unsigned long long* pv, int* tilecnt) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long r = t / kEmitLanes;
+  const int l = (int)(t % kEmitLanes);
+  const unsigned seg = 0xffffu << (threadIdx.x & 16);  // this lane's 16-lane segment
+  if (r >= n_rows) return;  // whole segments (n_rows * 16 threads, 16 | 32)
+  const int4 rr = rows[r];
+  if (rr.w < rr.z) return;  // segment-uniform
+  const int pid = rr.x, ty = rr.y;
+  const Geo& g = geo[pid];
+  const long long pos0 = rowpairoff[r];
+  const int cw = cam.tiles_x + 1;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const double rz0 = g.rz[0], rz1 = g.rz[1], rz2 = g.rz[2], num = g.num, eps = opt.grazing_eps;
+  auto depth = [&](const double* d) -> double {
+    const double denom = d[0] * rz0 + d[1] * rz1 + d[2] * rz2;
+    if (fabs(denom) < eps) return inf;
+    const double q = num / denom;
+    return q > 0 ? q : inf;
+  };
+  for (int base = rr.z; base <= rr.w; base += kEmitLanes) {
+    const int tx = base + l;
+    const bool valid = tx <= rr.w;
+    const int txc = valid ? tx : rr.w;
+    double key;
+    if (opt.presort == 0) {
+      key = (double)pid;
+    } else if (opt.presort == 1) {
+      key = g.projz;
+    } else {
+      const int c00 = ty * cw + txc;
+      const double top = depth(cdirs + 3 * (size_t)c00), bot = depth(cdirs + 3 * (size_t)(c00 + cw));
+      const double cen = depth(tdirs + 3 * (size_t)(ty * cam.tiles_x + txc));
+      double rtop = __shfl_down_sync(seg, top, 1, kEmitLanes), rbot = __shfl_down_sync(seg, bot, 1, kEmitLanes);
+      if (l == kEmitLanes - 1 || tx >= rr.w) {
+        rtop = depth(cdirs + 3 * (size_t)(c00 + 1));
+        rbot = depth(cdirs + 3 * (size_t)(c00 + cw + 1));
+      }
+      double best = dmin(dmin(dmin(top, rtop), dmin(rbot, bot)), cen);
+      if (isinf(best) && g.has_proj) best = g.projz;
+      key = best;
+    }
+    if (valid) {
+      const int tile = ty * cam.tiles_x + tx;
+      const long long pos = pos0 + (tx - rr.z);
+      pk[pos] = (unsigned long long)__double_as_longlong(key);
+      pv[pos] = ((unsigned long long)(unsigned)tile << 32) | (unsigned)pid;
+      atomicAdd(&tilecnt[tile], 1);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
