@@ -1354,8 +1354,9 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
     Pixel<BWD, true> px;
     px.init(P, x, y);
     if (BWD) px.init_bwd(P);
-    double cd[kCacheCap];
-    int ci[kCacheCap];
+    // SortCache distributed over lanes 0..7 (lane q holds entry q); csz is warp-uniform
+    double cdq = 0;
+    int ciq = -1;
     int csz = 0;
     bool done = false;
     const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
@@ -1380,15 +1381,46 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
           }
         }
         const unsigned hits = __ballot_sync(FULL, hit);
-        for (int k = 0; k < 32; ++k) {
+        unsigned rem = hits;
+        while (rem) {
+          const int k = __ffs(rem) - 1;
+          rem &= rem - 1;
           const double rk = __shfl_sync(FULL, rt, k);
           const int ik = __shfl_sync(FULL, id, k);
-          if (!((hits >> k) & 1u)) continue;
           bool pop = false;
           double prt = rk;
           int pid = ik;
-          if (MODE == 1) pop = true;
-          else pop = cache_step(cd, ci, csz, rk, ik, prt, pid);  // replicated on all lanes
+          if (MODE == 1) {
+            pop = true;
+          } else {
+            // SortCache::step (raster.cpp:267-303): entries <= rk form a prefix
+            const int pos = __popc(__ballot_sync(FULL, lane < csz && cdq <= rk));
+            const double upd = __shfl_up_sync(FULL, cdq, 1), dnd = __shfl_down_sync(FULL, cdq, 1);
+            const int upi = __shfl_up_sync(FULL, ciq, 1), dni = __shfl_down_sync(FULL, ciq, 1);
+            if (csz < kCacheCap) {
+              if (lane > pos && lane <= csz) {
+                cdq = upd;
+                ciq = upi;
+              } else if (lane == pos) {
+                cdq = rk;
+                ciq = ik;
+              }
+              ++csz;
+            } else {
+              pop = true;
+              if (pos > 0) {  // head pops; entries 1..pos-1 move down, incoming at pos-1
+                prt = __shfl_sync(FULL, cdq, 0);
+                pid = __shfl_sync(FULL, ciq, 0);
+                if (lane < pos - 1) {
+                  cdq = dnd;
+                  ciq = dni;
+                } else if (lane == pos - 1) {
+                  cdq = rk;
+                  ciq = ik;
+                }
+              }  // else: the incoming is strictly shallower than the head and pops through
+            }
+          }
           if (pop) {
             if (lane == npop) {
               my_rt = prt;
@@ -1401,14 +1433,17 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
       } else if (MODE == 0) {
         // end marker: drain the head (up to 8 pops)
         while (csz > 0 && npop < 32) {
+          const double h = __shfl_sync(FULL, cdq, 0);
+          const int hi = __shfl_sync(FULL, ciq, 0);
           if (lane == npop) {
-            my_rt = cd[0];
-            my_id = ci[0];
+            my_rt = h;
+            my_id = hi;
           }
-#pragma unroll
-          for (int q = 0; q < kCacheCap - 1; ++q) {
-            cd[q] = cd[q + 1];
-            ci[q] = ci[q + 1];
+          const double dnd = __shfl_down_sync(FULL, cdq, 1);
+          const int dni = __shfl_down_sync(FULL, ciq, 1);
+          if (lane < kCacheCap - 1) {
+            cdq = dnd;
+            ciq = dni;
           }
           --csz;
           ++npop;
