@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--cpu-crop", default="960x544", help="crop of the CPU baseline sample (tile aligned)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fwd-bwd", action="store_true")
+    ap.add_argument("--multiview-views", type=int, default=16,
+                    help="config 3 leg: orbit views per step, split across ranks (0 = skip)")
+    ap.add_argument("--no-train", action="store_true", help="skip the multi-GPU training-step leg")
     return ap.parse_args()
 
 
@@ -323,6 +326,101 @@ def main():
                                              "(raw-parameter gradients), one view per GPU",
                    "stage_ms": bst}
 
+    # ---- config 3: multi-view batch, views sharded across ranks (strong scaling) ----
+    multiview = None
+    if args.multiview_views > 0:
+        from paper_2412_11752_b200.parallel import shard_views
+        sc3 = scenes.config_scene(3)
+        cams3 = scenes.config_cameras(3)[:args.multiview_views]
+        raw3 = torch.from_numpy(sc3.f32()).to(dev)
+        mine = shard_views(len(cams3), world, rank)
+        for v in mine[:1]:
+            r.render(raw3, cams3[v], opt)  # warm-up (allocations)
+        torch.cuda.synchronize(dev)
+        nmv = max(1, min(args.steps, 3))
+        mv_ms = []
+        for _ in range(nmv):
+            barrier()
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for v in mine:
+                r.render(raw3, cams3[v], opt)
+            b.record(stream)
+            b.synchronize()
+            mv_ms.append(a.elapsed_time(b))
+        mv_tot = float(np.mean(mv_ms))
+        if world > 1:
+            t = torch.tensor([mv_tot], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            mv_tot = float(t.item())
+        px3 = cams3[0].width * cams3[0].height
+        multiview = {"value": len(cams3) * px3 / (mv_tot * 1e-3) / 1e6, "unit": "megapixels/s",
+                     "ms_per_step": mv_tot, "steps": nmv, "scaling": "strong", "views_per_step": len(cams3),
+                     "views_on_rank0": len(mine),
+                     "workload": f"config3: 1M DRK, K=8, SH3, {len(cams3)} of the 64 seeded orbit views at 1920x1080 "
+                                 "per step, views split across ranks (replicated primitives, no data-path collective); "
+                                 "max over ranks"}
+        del raw3
+
+    # ---- training step: per-rank views, NCCL all-reduce of the raw gradients, Adam (config 4 structure at
+    #      config 2 scale: 300k DRK, 1280x720, 2 views per GPU) ----
+    train = None
+    if not args.no_train:
+        from paper_2412_11752_b200.api import OptState, TrainConfig
+        from paper_2412_11752_b200.parallel import allreduce_mean_, params_checksum
+        sc4 = scenes.config_scene(2)
+        base_cam = scenes.config_cameras(2)[0]
+        orbit = scenes.orbit_cameras(2 * world, base_cam.width, base_cam.height, seed=4)
+        views = [orbit[2 * rank], orbit[2 * rank + 1]]
+        tg = [torch.from_numpy(scenes.config_target(2, cv, view=2 * rank + i).astype(np.float32)).to(dev)
+              for i, cv in enumerate(views)]
+        p4 = torch.from_numpy(sc4.f32()).to(dev)
+        g4 = torch.zeros_like(p4)
+        st4 = OptState.zeros_like(p4)
+        tcfg = TrainConfig(steps=35000, lr_drk=1e-3, lr_position=1e-3 / 2.0, lr_rotation=1e-3, lr_opacity=1e-3,
+                           lr_sh=1e-3)
+
+        def train_step4():
+            g4.zero_()
+            for cv, tgt in zip(views, tg):
+                fb = r.render(p4, cv, opt2)
+                _, dcol = r.l1_loss(fb.color, tgt)
+                r.backward_render(p4, FrameGrad(d_color=dcol), grad_out=g4, accumulate=True)
+            allreduce_mean_(g4, 2 * world)
+            r.adam_step(p4, g4, st4, tcfg, scene_extent=2.0)
+
+        opt2 = RenderOptions(sh_degree=3)
+        train_step4()
+        torch.cuda.synchronize(dev)
+        ntr = 2
+        tr_ms = []
+        for _ in range(ntr):
+            barrier()
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            train_step4()
+            b.record(stream)
+            b.synchronize()
+            tr_ms.append(a.elapsed_time(b))
+        tr_tot = float(np.mean(tr_ms))
+        csum = params_checksum(p4)
+        in_sync = True
+        if world > 1:
+            t = torch.tensor([tr_tot], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tr_tot = float(t.item())
+            cs = torch.tensor([csum, -csum], device=dev, dtype=torch.float64)
+            dist.all_reduce(cs, op=dist.ReduceOp.MAX)
+            in_sync = bool(abs(float(cs[0].item()) + float(cs[1].item())) == 0.0)
+        px4 = base_cam.width * base_cam.height
+        train = {"value": 2 * world * px4 / (tr_tot * 1e-3) / 1e6, "unit": "megapixels/s", "ms_per_step": tr_tot,
+                 "steps": ntr, "scaling": "weak", "replicas_in_sync": in_sync,
+                 "workload": "training step with config 4's structure at config 2 scale: 300k DRK, K=8, SH3, 2 orbit "
+                             "views of 1280x720 per GPU, forward + L1 + backward per view, NCCL all-reduce (mean over "
+                             "all views) of the raw gradients, Adam (lr 1e-3); replicas checked by parameter checksum"}
+
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -344,7 +442,8 @@ def main():
                            "views_per_gpu": 1, "parallelism": f"views x{world} (replicated primitives)",
                            "l2": "flushed between timed steps (256 MiB write, outside the timed events)"},
                 "stage_ms": stage_ms, "pairs": st["pairs"], "fp64_pixels": st["fp64_pixels"],
-                "roofline": roofline, "e2e": e2e, "fwd_bwd": fwd_bwd, "cpu_baseline": cpu,
+                "roofline": roofline, "e2e": e2e, "fwd_bwd": fwd_bwd, "multiview": multiview, "train": train,
+                "cpu_baseline": cpu,
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
     if world > 1:
