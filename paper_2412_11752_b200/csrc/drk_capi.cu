@@ -187,7 +187,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   if (!ctr || !geo || !bbox || !hullref || !rowcnt || !rowoff) return set_error(c, DRK_ERR_OOM, "prep buffers");
   static_assert(sizeof(Geo) % 8 == 0, "Geo alignment");
   if (c->hull_cap < (long long)n * 96 + 1024) c->hull_cap = (long long)n * 96 + 1024;
-  if (c->pts_cap < (long long)n * 200 + 1024) c->pts_cap = (long long)n * 200 + 1024;
+  if (c->pts_cap < (long long)n * 260 + 1024) c->pts_cap = (long long)n * 260 + 1024;
   int2* ptsref = ensure<int2>(c->ptsref, n + 1);
   if (!ptsref) return set_error(c, DRK_ERR_OOM, "point refs");
   // K1 with retry on hull-pool overflow

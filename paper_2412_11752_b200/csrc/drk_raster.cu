@@ -1354,9 +1354,12 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
     Pixel<BWD, true> px;
     px.init(P, x, y);
     if (BWD) px.init_bwd(P);
-    // SortCache distributed over lanes 0..7 (lane q holds entry q); csz is warp-uniform
+    // forward: SortCache distributed over lanes 0..7 (lane q holds entry q);
+    // backward: replicated on every lane (faster there, measured).  csz is warp-uniform.
     double cdq = 0;
     int ciq = -1;
+    double cd[kCacheCap];
+    int ci[kCacheCap];
     int csz = 0;
     bool done = false;
     const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
@@ -1392,6 +1395,8 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
           int pid = ik;
           if (MODE == 1) {
             pop = true;
+          } else if (BWD) {
+            pop = cache_step(cd, ci, csz, rk, ik, prt, pid);  // replicated on all lanes
           } else {
             // SortCache::step (raster.cpp:267-303): entries <= rk form a prefix
             const int pos = __popc(__ballot_sync(FULL, lane < csz && cdq <= rk));
@@ -1432,7 +1437,20 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
         j += 32;
       } else if (MODE == 0) {
         // end marker: drain the head (up to 8 pops)
-        while (csz > 0 && npop < 32) {
+        while (BWD && csz > 0 && npop < 32) {
+          if (lane == npop) {
+            my_rt = cd[0];
+            my_id = ci[0];
+          }
+#pragma unroll
+          for (int q = 0; q < kCacheCap - 1; ++q) {
+            cd[q] = cd[q + 1];
+            ci[q] = ci[q + 1];
+          }
+          --csz;
+          ++npop;
+        }
+        while (!BWD && csz > 0 && npop < 32) {
           const double h = __shfl_sync(FULL, cdq, 0);
           const int hi = __shfl_sync(FULL, ciq, 0);
           if (lane == npop) {
