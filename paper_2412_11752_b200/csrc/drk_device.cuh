@@ -333,7 +333,7 @@ __device__ __forceinline__ float sharpen_ps(const float4 c0, const float4 c1, fl
   float Am = A;
   if (fabsf(g - c0.x) <= dg) Am = fmaxf(Am, fmaxf(c0.z, c0.w));
   if (fabsf(g - c0.y) <= dg) Am = fmaxf(Am, fmaxf(c0.w, c1.x));
-  *relP = P > 0.f ? (Am * (g * relg) + (br > 0 ? A * 3.5e-8f : 0.f)) / P + 1.8e-7f : 1.0f;
+  *relP = P > 0.f ? 1.001f * __fdividef(Am * (g * relg) + (br > 0 ? A * 3.5e-8f : 0.f), P) + 1.8e-7f : 1.0f;
   if (slope) *slope = A;
   if (branch) *branch = br;
   return P;

@@ -325,8 +325,8 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
       // error of Q: r1 and r2 from the tangent coordinates, the bracket angle
       // (atan2 + coordinate error) through the cosine blend, __cosf (<= 5e-7
       // absolute), rounding
-      const float pabs = sqrtf(r2);
-      const float dth_err = 2.5e-7f * dth + 2.5e-7f + 1.5f * dp / pabs;
+      // (bound arithmetic: approximate reciprocals, inflated by 1e-3)
+      const float dth_err = 2.5e-7f * dth + 2.5e-7f + 1.5015f * dp * rsqrtf(r2);
       const float dinv = fabsf(hdiff) * (dth_err * f.y + 2.4e-7f * delta + 2e-7f) + 2e-7f * (hs + fabsf(hdiff));
       const float dQ = eta * (2.f * r1 * dr1 + dr1 * dr1) + (1.f - eta) * (r2 * dinv + inv_s * dr2) + 3.6e-7f * Q;
       const float ex = fmaxf(-0.5f * Q, -30.0f);
@@ -357,11 +357,11 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
     if (lp_possible) {
       const float sl = (float)P.opt.lowpass_radius;
       const float den = 2.0f * dz * dz * sl * sl;
-      const float exl = fmaxf(-dpp2 / den, -30.0f);
+      const float exl = fmaxf(-__fdividef(dpp2, den), -30.0f);  // 2 ulp: inside relf's 1e-6 |exl|
       const float fl = c1.w * __expf(exl);
       const float ddp = 6e-8f * (fabsf(R.r4.x) + fabsf(R.r4.y) + 32.f);
       const float relf = 4e-7f + 1.2e-7f * fabsf(exl) + fabsf(exl) * (2.f * rel_z + 1e-6f) +
-                         2.f * sqrtf(dpp2) * ddp / den * 2.f;
+                         4.004f * (dpp2 > 0.f ? dpp2 * rsqrtf(dpp2) : 0.f) * __fdividef(ddp, den);
       if (fabsf(fl - ak) <= relk * ak + relf * fl) use64 = true;
       if (fl > ak) {
         at = fl;
