@@ -434,7 +434,7 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
 }
 // blend (raster.cpp:349-361): colour from SH, accumulation, transmittance
 // and its error bound; returns false once the pixel saturates.
-__device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, const float* s_basis, int id, double a64,
+__device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, const float4* s_b4, int id, double a64,
                                       float relt, float rt, float sgn, float rz0, float rz1, float rz2) {
   const float* shp = P.sh + (size_t)id * P.terms * 3;
   float c0 = 0.5f, c1 = 0.5f, c2 = 0.5f;
@@ -445,8 +445,8 @@ __device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, cons
     for (int t = 0; t < 16; t += 4) {
       if (t < ta) {
         const float4 a = __ldg(q + 3 * (t / 4)), b = __ldg(q + 3 * (t / 4) + 1), c = __ldg(q + 3 * (t / 4) + 2);
-        const float b0 = s_basis[t * kBatch], b1 = s_basis[(t + 1) * kBatch], b2 = s_basis[(t + 2) * kBatch],
-                    b3 = s_basis[(t + 3) * kBatch];
+        const float4 bq = s_b4[(t / 4) * kBatch];  // this pixel's basis, terms t..t+3
+        const float b0 = bq.x, b1 = bq.y, b2 = bq.z, b3 = bq.w;
         c0 = fmaf(b0, a.x, c0);
         c1 = fmaf(b0, a.y, c1);
         c2 = fmaf(b0, a.z, c2);
@@ -463,7 +463,9 @@ __device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, cons
     }
   } else {
     for (int t = 0; t < ta; ++t) {
-      const float bt = s_basis[t * kBatch];
+      const float4 bq = s_b4[(t >> 2) * kBatch];
+      const int tq = t & 3;
+      const float bt = tq == 0 ? bq.x : (tq == 1 ? bq.y : (tq == 2 ? bq.z : bq.w));
       c0 = fmaf(bt, __ldg(shp + 3 * t), c0);
       c1 = fmaf(bt, __ldg(shp + 3 * t + 1), c1);
       c2 = fmaf(bt, __ldg(shp + 3 * t + 2), c2);
@@ -488,7 +490,11 @@ __device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, cons
     const float af = (float)a64;
     px.E += relt * __fdividef(af, 1.0f - af) + 1e-15f;
   }
-  if (fabs(px.T - P.opt.early_stop) <= px.T * (double)px.E) px.uncertain = true;
+  {
+    // |T - early_stop| <= T E, in fp32 with the roundings of T and the threshold covered
+    const float tf = (float)px.T, thr = (float)P.opt.early_stop;
+    if (fabsf(tf - thr) <= tf * (px.E * 1.001f + 2.5e-7f)) px.uncertain = true;
+  }
   if (px.T < P.opt.early_stop) {
     px.stop = px.ncomp;
     return false;
@@ -497,7 +503,7 @@ __device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, cons
 }
 
 template <bool VALIDATE>
-__device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, const float* s_basis, const Rec* ring,
+__device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, const float4* s_b4, const Rec* ring,
                                          const int* s_id, const TileConst& tc, long long beg, int ring_lo, int jr,
                                          int x, int y) {
   ++px.n_pop;
@@ -519,7 +525,7 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
     return false;
   }
   if (o.skip) return true;
-  return blend(P, px, s_basis, id, o.a, o.rel, o.rt, o.sgn, R.r0.x, R.r0.y, R.r0.z);
+  return blend(P, px, s_b4, id, o.a, o.rel, o.rt, o.sgn, R.r0.x, R.r0.y, R.r0.z);
 }
 
 }  // namespace drk

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
   extern __shared__ float4 dyn[];
   Rec* ring = reinterpret_cast<Rec*>(dyn);
   int* s_id = reinterpret_cast<int*>(ring + kRing);
-  float* s_basis = reinterpret_cast<float*>(s_id + kRing) + threadIdx.x;  // [16][256], this thread's column
+  float4* s_b4 = reinterpret_cast<float4*>(s_id + kRing) + threadIdx.x;  // [4][256] float4, this thread's column
   __shared__ unsigned s_ddmax;
   __shared__ TileConst tc;
   const int tile = blockIdx.x;
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
     for (int t = 0; t < 16; ++t) b[t] = 0.f;
     sh_basis_f((float)dir[0], (float)dir[1], (float)dir[2], P.opt.sh_degree, b);
 #pragma unroll
-    for (int t = 0; t < 16; ++t) s_basis[t * kBatch] = b[t];
+    for (int q = 0; q < 4; ++q) s_b4[q * kBatch] = make_float4(b[4 * q], b[4 * q + 1], b[4 * q + 2], b[4 * q + 3]);
   }
   if (threadIdx.x == 0) {
     s_ddmax = 0u;
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
             }
           }
         }
-        if (!pop_eval<VALIDATE>(P, px, s_basis, ring, s_id, tc, beg, ring_lo, pj, x, y)) {
+        if (!pop_eval<VALIDATE>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y)) {
           done = true;
           break;
         }
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
       cj[q] = cj[q + 1];
     }
     --csz;
-    if (!pop_eval<VALIDATE>(P, px, s_basis, ring, s_id, tc, beg, ring_lo, pj, x, y))
+    if (!pop_eval<VALIDATE>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y))
       done = true;
   }
   // counters: one atomic per warp and counter
