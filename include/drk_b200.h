@@ -141,6 +141,11 @@ int drk_get_stats(const drk_ctx* ctx, drk_stats* out);
 int drk_set_stream(drk_ctx* ctx, void* cuda_stream);
 /* Enables per-stage CUDA-event timing (drk_stats.stage_ms). */
 int drk_set_timing(drk_ctx* ctx, int enabled);
+/* Banded binning (frames whose tile-pair lists exceed device memory are binned,
+ * sorted and rasterized one band of tile rows at a time; automatic).  Test hook:
+ * force bands above `pairs` pairs per band (0 = memory-based). */
+int drk_set_band_limit(drk_ctx* ctx, int64_t pairs);
+int drk_get_bands(const drk_ctx* ctx, int32_t* n_bands);
 /* Validation of the fast forward kernel: while enabled, every fp32 alpha is
  * also evaluated in fp64; drk_get_validation returns max |a32 - a64| / bound
  * (must stay below 1) and max |a32 - a64| since validation was enabled. */

@@ -343,6 +343,15 @@ class Rasterizer:
     def set_timing(self, enabled: bool = True):
         self._check(_lib.lib().drk_set_timing(self._h, int(enabled)))
 
+    def set_band_limit(self, pairs: int):
+        """Force banded binning above `pairs` tile pairs per band (0 = by free device memory)."""
+        self._check(_lib.lib().drk_set_band_limit(self._h, int(pairs)))
+
+    def bands(self) -> int:
+        v = C.c_int32(0)
+        self._check(_lib.lib().drk_get_bands(self._h, C.byref(v)))
+        return int(v.value)
+
     def set_validation(self, enabled: bool = True):
         """Fast forward kernel: check every fp32 alpha against its fp64 value (slow; tests only)."""
         self._check(_lib.lib().drk_set_validation(self._h, int(enabled)))

@@ -22,7 +22,11 @@ __global__ void k_prep1(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, i
                         long long pool_cap, int* rowcnt, unsigned long long* counters, const int* list, int list_n,
                         double2* scratch, int scratch_cap, int* overflow);
 __global__ void k_rows(int n, const int4* bbox, const int2* hullref, const double2* pool, const long long* rowoff,
-                       CamD cam, OptD opt, int4* rows, int* rowpaircnt, unsigned long long* counters);
+                       CamD cam, OptD opt, int4* rows, int* rowpaircnt, unsigned long long* counters, int ty_lo,
+                       int ty_hi);
+__global__ void k_band_rowcnt(int n, const int4* bbox, int ty_lo, int ty_hi, int* rowcnt);
+__global__ void k_row_pair_bound(int n, const int4* bbox, unsigned long long* rowest);
+__global__ void k_band_flagged(const unsigned char* pxflag, int W, int y0, int y1, int* list, unsigned* count);
 __global__ void k_tile_rays(CamD cam, double* cdirs, double* tdirs);
 __global__ void k_emit_rows(long long n_rows, const int4* rows, const long long* rowpairoff, const Geo* geo,
                             const double* cdirs, const double* tdirs, CamD cam, OptD opt, unsigned long long* pk,
@@ -161,6 +165,102 @@ static float elapsed(drk_ctx* c, int a, int b) {
   return ms;
 }
 
+// Bands of tile rows: one band unless the frame's pairs (upper bound from the
+// bounding boxes) would not fit in device memory; then greedy bands whose
+// bound fits (SURVEY.md §7 hard part 5: banded binning for config 4).
+static int plan_bands(drk_ctx* c) {
+  const CamD& cd = c->camd;
+  const int n = c->act.n;
+  c->bands.assign({0, cd.tiles_y});
+  if (n == 0 || cd.tiles_y <= 1) return DRK_OK;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t held = c->pk.bytes + c->pv.bytes + c->pk2.bytes + c->pv2.bytes + c->hist.bytes + c->sortoff.bytes;
+  const double budget = 0.7 * (double)(free_b + held) / 34.0;
+  const double limit = c->band_pair_limit > 0 ? (double)c->band_pair_limit : budget;
+  // every primitive in every tile: fits without looking closer
+  if ((double)n * cd.tiles_x * cd.tiles_y <= limit) return DRK_OK;
+  unsigned long long* rowest = ensure<unsigned long long>(c->rowest, cd.tiles_y + 1);
+  if (!rowest) return set_error(c, DRK_ERR_OOM, "row estimates");
+  cudaMemsetAsync(rowest, 0, sizeof(unsigned long long) * (cd.tiles_y + 1), c->stream);
+  k_row_pair_bound<<<(n + 255) / 256, 256, 0, c->stream>>>(n, static_cast<const int4*>(c->bbox.p), rowest);
+  DRK_COUNT_LAUNCH();
+  std::vector<unsigned long long> est(cd.tiles_y);
+  cudaMemcpyAsync(est.data(), rowest, sizeof(unsigned long long) * cd.tiles_y, cudaMemcpyDeviceToHost, c->stream);
+  if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "band plan")) return st;
+  unsigned long long total = 0;
+  for (auto e : est) total += e;
+  // bytes per pair: keys + values double-buffered (32 B) + sort histograms / offsets (~1.5 B)
+  if ((double)total <= limit) return DRK_OK;
+  c->bands.assign({0});
+  unsigned long long acc = 0;
+  for (int ty = 0; ty < cd.tiles_y; ++ty) {
+    if (acc > 0 && (double)(acc + est[ty]) > limit) {
+      c->bands.push_back(ty);
+      acc = 0;
+    }
+    acc += est[ty];
+  }
+  c->bands.push_back(cd.tiles_y);
+  return DRK_OK;
+}
+
+// Binning of tile rows [ty_lo, ty_hi): rows, pairs with NearestDepth keys,
+// radix sort, tile offsets (tiles outside the band get empty lists).
+static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
+  const CamD& cd = c->camd;
+  const OptD& od = c->optd;
+  const int n = c->act.n;
+  const int n_tiles = cd.tiles_x * cd.tiles_y;
+  cudaStream_t s = c->stream;
+  const int4* bbox = static_cast<const int4*>(c->bbox.p);
+  int* rowcnt = static_cast<int*>(c->rowcnt.p);
+  long long* rowoff = static_cast<long long*>(c->rowoff.p);
+  unsigned long long* ctr = static_cast<unsigned long long*>(c->counters.p);
+  const bool whole = ty_lo == 0 && ty_hi == cd.tiles_y;
+  if (!whole && n > 0) {
+    k_band_rowcnt<<<(n + 127) / 128, 128, 0, s>>>(n, bbox, ty_lo, ty_hi, rowcnt);
+    DRK_COUNT_LAUNCH();
+  }
+  long long n_rows = 0;
+  if (int st = exclusive_scan<int>(c, rowcnt, n, rowoff, &n_rows)) return st;
+  c->n_rows = n_rows;
+  int4* rows = ensure<int4>(c->rows, n_rows + 1);
+  int* rowpaircnt = ensure<int>(c->rowpaircnt, n_rows + 1);
+  long long* rowpairoff = ensure<long long>(c->rowpairoff, n_rows + 1);
+  if (!rows || !rowpaircnt || !rowpairoff) return set_error(c, DRK_ERR_OOM, "row buffers");
+  if (n > 0)
+    k_rows<<<(n + 127) / 128, 128, 0, s>>>(n, bbox, static_cast<const int2*>(c->hullref.p),
+                                           static_cast<const double2*>(c->hull.p), rowoff, cd, od, rows, rowpaircnt,
+                                           ctr, ty_lo, ty_hi);
+  long long n_pairs = 0;
+  if (int st = exclusive_scan<int>(c, rowpaircnt, n_rows, rowpairoff, &n_pairs)) return st;
+  unsigned long long* pk = ensure<unsigned long long>(c->pk, n_pairs + 1);
+  unsigned long long* pv = ensure<unsigned long long>(c->pv, n_pairs + 1);
+  unsigned long long* pk2 = ensure<unsigned long long>(c->pk2, n_pairs + 1);
+  unsigned long long* pv2 = ensure<unsigned long long>(c->pv2, n_pairs + 1);
+  int* tilecnt = ensure<int>(c->tilecnt, n_tiles + 1);
+  long long* tileoff = ensure<long long>(c->tileoff, n_tiles + 1);
+  if (!pk || !pv || !pk2 || !pv2 || !tilecnt || !tileoff) return set_error(c, DRK_ERR_OOM, "pair buffers");
+  cudaMemsetAsync(tilecnt, 0, sizeof(int) * (n_tiles + 1), s);
+  if (n_rows > 0)
+    k_emit_rows<<<(unsigned)((n_rows * 16 + 255) / 256), 256, 0, s>>>(
+        n_rows, rows, rowpairoff, static_cast<const Geo*>(c->geo.p), static_cast<const double*>(c->cdirs.p),
+        static_cast<const double*>(c->tdirs.p), cd, od, pk, pv, tilecnt);
+  launch_counter() += 2;
+  mark(c, 3);
+  if (int st = sort_pairs(c, pk, pv, pk2, pv2, n_pairs)) return st;
+  if (pk != c->pk.p) {  // keep the sorted arrays in c->pk / c->pv
+    std::swap(c->pk, c->pk2);
+    std::swap(c->pv, c->pv2);
+  }
+  long long tot = 0;
+  if (int st = exclusive_scan<int>(c, tilecnt, n_tiles + 1, tileoff, &tot)) return st;
+  mark(c, 4);
+  *n_pairs_out = n_pairs;
+  return DRK_OK;
+}
+
 int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float* color, float* depth,
                 float* normal, float* alpha) {
   const Activated& A = c->act;
@@ -252,84 +352,79 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     if (attempt == 3) return set_error(c, DRK_ERR_OOM, "hull pool retries");
   }
   mark(c, 2);
-  // rows
-  long long n_rows = 0;
-  if (int st = exclusive_scan<int>(c, rowcnt, n, rowoff, &n_rows)) return st;
-  c->n_rows = n_rows;
-  int4* rows = ensure<int4>(c->rows, n_rows + 1);
-  int* rowpaircnt = ensure<int>(c->rowpaircnt, n_rows + 1);
-  long long* rowpairoff = ensure<long long>(c->rowpairoff, n_rows + 1);
-  if (!rows || !rowpaircnt || !rowpairoff) return set_error(c, DRK_ERR_OOM, "row buffers");
-  if (n > 0)
-    k_rows<<<(n + 127) / 128, 128, 0, s>>>(n, bbox, hullref, static_cast<const double2*>(c->hull.p), rowoff, cd,
-                                           od, rows, rowpaircnt, ctr);
-  long long n_pairs = 0;
-  if (int st = exclusive_scan<int>(c, rowpaircnt, n_rows, rowpairoff, &n_pairs)) return st;
-  c->n_pairs = n_pairs;
-  // pairs
-  unsigned long long* pk = ensure<unsigned long long>(c->pk, n_pairs + 1);
-  unsigned long long* pv = ensure<unsigned long long>(c->pv, n_pairs + 1);
-  unsigned long long* pk2 = ensure<unsigned long long>(c->pk2, n_pairs + 1);
-  unsigned long long* pv2 = ensure<unsigned long long>(c->pv2, n_pairs + 1);
-  int* tilecnt = ensure<int>(c->tilecnt, n_tiles + 1);
-  long long* tileoff = ensure<long long>(c->tileoff, n_tiles + 1);
+  float prep_ms[2] = {0, 0};
+  if (c->timing) {
+    cudaEventSynchronize(c->ev[2]);
+    prep_ms[0] = elapsed(c, 0, 1);
+    prep_ms[1] = elapsed(c, 1, 2);
+  }
   double* cdirs = ensure<double>(c->cdirs, 3 * (size_t)(cd.tiles_x + 1) * (cd.tiles_y + 1));
   double* tdirs = ensure<double>(c->tdirs, 3 * (size_t)n_tiles);
-  if (!pk || !pv || !pk2 || !pv2 || !tilecnt || !tileoff || !cdirs || !tdirs)
-    return set_error(c, DRK_ERR_OOM, "pair buffers");
-  cudaMemsetAsync(tilecnt, 0, sizeof(int) * (n_tiles + 1), s);
+  if (!cdirs || !tdirs) return set_error(c, DRK_ERR_OOM, "tile rays");
   {
     const int nr = (cd.tiles_x + 1) * (cd.tiles_y + 1) + n_tiles;
     k_tile_rays<<<(nr + 127) / 128, 128, 0, s>>>(cd, cdirs, tdirs);
+    DRK_COUNT_LAUNCH();
   }
-  if (n_rows > 0)
-    k_emit_rows<<<(unsigned)((n_rows * 16 + 255) / 256), 256, 0, s>>>(n_rows, rows, rowpairoff, geo, cdirs, tdirs, cd,
-                                                                      od, pk, pv, tilecnt);
-  launch_counter() += 3;
-  mark(c, 3);
-  if (int st = sort_pairs(c, pk, pv, pk2, pv2, n_pairs)) return st;
-  // keep the sorted arrays in c->pk / c->pv
-  if (pk != c->pk.p) {
-    std::swap(c->pk, c->pk2);
-    std::swap(c->pv, c->pv2);
-  }
-  long long tot = 0;
-  if (int st = exclusive_scan<int>(c, tilecnt, n_tiles + 1, tileoff, &tot)) return st;
-  mark(c, 4);
+  if (int st = plan_bands(c)) return st;
   // per-pixel state / replay
   double* pxstate = ensure<double>(c->pxstate, 8 * (size_t)n_pix);
   unsigned char* pxflag = ensure<unsigned char>(c->pxflag, (size_t)n_pix);
   int* pxstop = ensure<int>(c->pxstop, (size_t)n_pix);
   int* redo = ensure<int>(c->redo, (size_t)n_pix + 1);
   if (!pxstate || !pxflag || !redo || !pxstop) return set_error(c, DRK_ERR_OOM, "pixel state");
-  RasterParams P = raster_params(c);
-  P.pxflag = pxflag;
-  P.pxstop = pxstop;
-  if (c->validate_fast) {
-    P.vstat = ensure<unsigned long long>(c->vstat, 32);
-    if (!P.vstat) return set_error(c, DRK_ERR_OOM, "validation buffer");
-  }
-  P.color = color;
-  P.depth = depth;
-  P.normal = normal;
-  P.alpha = alpha;
-  P.pxstate = pxstate;
   if (opt->record_replay > 0) {
-    P.replay_cap = opt->record_replay;
-    P.replay_cnt = ensure<int>(c->replay_cnt, n_pix);
-    P.replay_ids = ensure<int>(c->replay_ids, (size_t)n_pix * P.replay_cap);
-    P.replay_rec = ensure<double>(c->replay_rec, 5 * (size_t)n_pix * P.replay_cap);
-    if (!P.replay_cnt || !P.replay_ids || !P.replay_rec) return set_error(c, DRK_ERR_OOM, "replay buffers");
+    ensure<int>(c->replay_cnt, n_pix);
+    ensure<int>(c->replay_ids, (size_t)n_pix * opt->record_replay);
+    ensure<double>(c->replay_rec, 5 * (size_t)n_pix * opt->record_replay);
+    if (!c->replay_cnt.p || !c->replay_ids.p || !c->replay_rec.p) return set_error(c, DRK_ERR_OOM, "replay buffers");
   }
-  launch_raster(P, n_tiles, false, s, c->timing ? c->ev[5] : nullptr);
-  mark(c, 6);
-  if (int st = cuda_check(c, cudaGetLastError(), "raster")) return st;
+  // bands of tile rows (one band unless the pairs of the frame would not fit)
+  long long n_pairs_total = 0;
+  float band_ms[4] = {0, 0, 0, 0};
+  const int nb = (int)c->bands.size() - 1;
+  for (int b = 0; b < nb; ++b) {
+    const int ty_lo = c->bands[b], ty_hi = c->bands[b + 1];
+    mark(c, 2);
+    long long n_pairs = 0;
+    if (int st = bin_band(c, ty_lo, ty_hi, &n_pairs)) return st;
+    n_pairs_total += n_pairs;
+    RasterParams P = raster_params(c);
+    P.pxflag = pxflag;
+    P.pxstop = pxstop;
+    if (c->validate_fast) {
+      P.vstat = ensure<unsigned long long>(c->vstat, 32);
+      if (!P.vstat) return set_error(c, DRK_ERR_OOM, "validation buffer");
+    }
+    P.color = color;
+    P.depth = depth;
+    P.normal = normal;
+    P.alpha = alpha;
+    P.pxstate = pxstate;
+    if (opt->record_replay > 0) {
+      P.replay_cap = opt->record_replay;
+      P.replay_cnt = static_cast<int*>(c->replay_cnt.p);
+      P.replay_ids = static_cast<int*>(c->replay_ids.p);
+      P.replay_rec = static_cast<double*>(c->replay_rec.p);
+    }
+    P.tile_base = ty_lo * cd.tiles_x;
+    launch_raster(P, (ty_hi - ty_lo) * cd.tiles_x, false, s, c->timing ? c->ev[5] : nullptr);
+    mark(c, 6);
+    if (int st = cuda_check(c, cudaGetLastError(), "raster")) return st;
+    if (c->timing) {
+      cudaEventSynchronize(c->ev[6]);
+      for (int k = 0; k < 4; ++k) band_ms[k] += elapsed(c, 2 + k, 3 + k);
+    }
+  }
+  c->n_pairs = n_pairs_total;
   unsigned long long h[C_COUNT];
   if (int st = read_counters(c, h)) return st;
-  if (c->timing)
-    for (int i = 0; i < 6; ++i) c->stats.stage_ms[i] = elapsed(c, i, i + 1);
+  if (c->timing) {
+    for (int i = 0; i < 2; ++i) c->stats.stage_ms[i] = prep_ms[i];
+    for (int k = 0; k < 4; ++k) c->stats.stage_ms[2 + k] = band_ms[k];
+  }
   c->stats.launches = launch_counter() - c->launch_base;
-  c->stats.pairs = n_pairs;
+  c->stats.pairs = n_pairs_total;
   c->stats.streamed = (int64_t)h[C_STREAMED];
   c->stats.popped = (int64_t)h[C_POPPED];
   c->stats.composited = (int64_t)h[C_COMPOSITED];
@@ -375,8 +470,40 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   P.touched = tch;
   const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
   mark(c, 7);
-  if (deterministic) launch_backward_serial(P, s);  // fixed accumulation order, small images
-  else launch_raster(P, n_tiles, true, s);
+  const int nb = (int)c->bands.size() - 1;
+  if (deterministic) {
+    if (nb > 1) return set_error(c, DRK_ERR_UNSUPPORTED, "deterministic backward of a banded frame");
+    launch_backward_serial(P, s);  // fixed accumulation order, small images
+  } else if (nb <= 1) {
+    launch_raster(P, n_tiles, true, s);
+  } else {
+    // banded frame: re-bin each band, then its backward raster and the fp64
+    // backward of its flagged pixels
+    for (int b = 0; b < nb; ++b) {
+      const int ty_lo = c->bands[b], ty_hi = c->bands[b + 1];
+      long long np = 0;
+      if (int st = bin_band(c, ty_lo, ty_hi, &np)) return st;
+      RasterParams Q = raster_params(c);
+      Q.pxstate = P.pxstate;
+      Q.pxflag = P.pxflag;
+      Q.pxstop = P.pxstop;
+      Q.dC = P.dC;
+      Q.dD = P.dD;
+      Q.dN = P.dN;
+      Q.dA = P.dA;
+      Q.gact = P.gact;
+      Q.G = P.G;
+      Q.touched = P.touched;
+      Q.tile_base = ty_lo * c->camd.tiles_x;
+      const int y0 = ty_lo * kTile, y1 = std::min(ty_hi * kTile, c->camd.H);
+      cudaMemsetAsync(Q.redo_count, 0, sizeof(unsigned), s);
+      const long long npx = (long long)(y1 - y0) * c->camd.W;
+      if (npx > 0)
+        k_band_flagged<<<(unsigned)((npx + 255) / 256), 256, 0, s>>>(Q.pxflag, c->camd.W, y0, y1, Q.redo_list,
+                                                                     Q.redo_count);
+      launch_raster(Q, (ty_hi - ty_lo) * c->camd.tiles_x, true, s);
+    }
+  }
   mark(c, 8);
   if (int st = cuda_check(c, cudaGetLastError(), "raster bwd")) return st;
   launch_act_bwd(n, K, A.terms, raw, gact, G, tch, static_cast<const Geo*>(c->geo.p), c->camd, grad_raw,
@@ -610,8 +737,21 @@ int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_ter
   return cuda_check(c, cudaStreamSynchronize(c->stream), "forward_host");
 }
 
+int drk_set_band_limit(drk_ctx* c, int64_t pairs) {
+  if (!c || pairs < 0) return DRK_ERR_INVALID_ARG;
+  c->band_pair_limit = pairs;
+  return DRK_OK;
+}
+
+int drk_get_bands(const drk_ctx* c, int32_t* n_bands) {
+  if (!c || !n_bands) return DRK_ERR_INVALID_ARG;
+  *n_bands = c->bands.empty() ? 0 : (int32_t)c->bands.size() - 1;
+  return DRK_OK;
+}
+
 int drk_get_tile_lists(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* ids, double* keys) {
   if (!c || !c->has_fwd) return c ? set_error(c, DRK_ERR_INVALID_ARG, "no forward on this context") : DRK_ERR_INVALID_ARG;
+  if (c->bands.size() > 2) return set_error(c, DRK_ERR_UNSUPPORTED, "tile lists of a banded frame are not kept");
   cudaSetDevice(c->device);
   if (total) *total = c->n_pairs;
   const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;

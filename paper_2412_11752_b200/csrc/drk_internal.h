@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "drk_b200.h"
 #include "drk_device.cuh"
@@ -79,6 +80,7 @@ struct RasterParams {
   unsigned char* pxflag;  // 1 = pixel needs the fp64 re-render (uncertain termination)
   int* redo_list;         // flagged pixel indices (forward fp32 pass appends)
   unsigned int* redo_count;
+  int tile_base;          // first tile of this launch (banded frames: tile rows processed band by band)
   const float* shrec;     // fast kernel: per-primitive fp32 shape records (K == 8)
   int* pxstop;            // composites until saturation per pixel (INT_MAX: never), written by the forward
   unsigned long long* vstat;  // fast kernel validation: max |a32 - a64| / bound, max |a32 - a64| (double bits)
@@ -112,6 +114,9 @@ struct drk_ctx {
   drk::DevBuf gact, touched;
   drk::DevBuf counters, scan_tmp, loss_tmp;
   int64_t hull_cap = 0;
+  drk::DevBuf rowest;
+  std::vector<int> bands;         // tile-row band boundaries of the last forward
+  long long band_pair_limit = 0;  // test hook: force bands above this many pairs (0 = memory-based)
   int64_t pts_cap = 0;
 
   // stage timing

@@ -849,10 +849,37 @@ __device__ bool hull_overlaps_rect(const double2* h, int n, double x0, double y0
   return true;
 }
 
+// Banded frames: rows of primitive i inside tile rows [ty_lo, ty_hi).
+__global__ void k_band_rowcnt(int n, const int4* __restrict__ bbox, int ty_lo, int ty_hi, int* rowcnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int4 bb = bbox[i];
+  const int a = max(bb.z, ty_lo), b = min(bb.w, ty_hi - 1);
+  rowcnt[i] = (bb.y >= bb.x && b >= a) ? b - a + 1 : 0;
+}
+
+// Upper bound of the pairs per tile row (bbox width per covered row), for
+// choosing the bands.
+__global__ void k_row_pair_bound(int n, const int4* __restrict__ bbox, unsigned long long* rowest) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int4 bb = bbox[i];
+  if (bb.y < bb.x || bb.w < bb.z) return;
+  for (int ty = bb.z; ty <= bb.w; ++ty) atomicAdd(&rowest[ty], (unsigned long long)(bb.y - bb.x + 1));
+}
+
+// Backward of a banded frame: the band's flagged pixels (fp64 re-render list).
+__global__ void k_band_flagged(const unsigned char* __restrict__ pxflag, int W, int y0, int y1, int* list,
+                               unsigned* count) {
+  const long long p = (long long)y0 * W + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= (long long)y1 * W) return;
+  if (pxflag[p]) list[atomicAdd(count, 1u)] = (int)p;
+}
+
 // Row record: prim id, tile row, first and last tile column (ta > tb: empty).
 __global__ void k_rows(int n, const int4* __restrict__ bbox, const int2* __restrict__ hullref,
                        const double2* __restrict__ pool, const long long* __restrict__ rowoff, CamD cam, OptD opt,
-                       int4* rows, int* rowpaircnt, unsigned long long* counters) {
+                       int4* rows, int* rowpaircnt, unsigned long long* counters, int ty_lo, int ty_hi) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int4 bb = bbox[i];
@@ -870,7 +897,7 @@ __global__ void k_rows(int n, const int4* __restrict__ bbox, const int2* __restr
   const double delta = 1e-9 * amax + 1e-9;
   long long ro = rowoff[i];
   unsigned long long ties = 0;
-  for (int ty = bb.z; ty <= bb.w; ++ty, ++ro) {
+  for (int ty = max(bb.z, ty_lo); ty <= min(bb.w, ty_hi - 1); ++ty, ++ro) {
     const double y0 = ty * kTile, y1 = y0 + kTile;
     const double Y0 = y0 - lp, Y1 = y1 + lp;
     // x-extent of H ∩ [Y0, Y1]

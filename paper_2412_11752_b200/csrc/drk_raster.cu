@@ -891,7 +891,7 @@ template <int MODE, bool BWD, bool F64>
 __global__ void __launch_bounds__(256, DRK_RASTER_MIN_BLOCKS) k_raster(RasterParams P) {
   __shared__ int s_id[256];
   __shared__ double s_num[256], s_r0[256], s_r1[256], s_r2[256];
-  const int tile = blockIdx.x;
+  const int tile = P.tile_base + blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
   bool active = x < P.cam.W && y < P.cam.H;
@@ -1029,7 +1029,7 @@ __global__ void __launch_bounds__(256, DRK_BWD_MIN_BLOCKS) k_raster_bwd(RasterPa
   __shared__ int s_id[256];
   __shared__ double s_num[256], s_r0[256], s_r1[256], s_r2[256];
   const unsigned FULL = 0xffffffffu;
-  const int tile = blockIdx.x;
+  const int tile = P.tile_base + blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
   bool active = x < P.cam.W && y < P.cam.H;
@@ -1591,7 +1591,7 @@ void launch_backward_serial(const RasterParams& P, cudaStream_t s) {
 // (depth, list index).
 template <bool BWD>
 __global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
-  const int tile = blockIdx.y;
+  const int tile = P.tile_base + blockIdx.y;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= 256) return;

@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
   float* s_w = s_w_all + 4 * threadIdx.x;
   __shared__ unsigned s_ddmax;
   __shared__ TileConst tc;
-  const int tile = blockIdx.x;
+  const int tile = P.tile_base + blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
   bool active = x < P.cam.W && y < P.cam.H;

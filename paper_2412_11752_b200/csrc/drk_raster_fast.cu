@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
   float4* s_b4 = reinterpret_cast<float4*>(s_id + kRing) + threadIdx.x;  // [4][256] float4, this thread's column
   __shared__ unsigned s_ddmax;
   __shared__ TileConst tc;
-  const int tile = blockIdx.x;
+  const int tile = P.tile_base + blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
   const bool active = x < P.cam.W && y < P.cam.H;

@@ -104,3 +104,30 @@ def test_fast_backward_kernel_parity(rast):
     og = port.backward(sc, cam, o, dc, dd, None, None)
     assert rel_l2(g.raw.cpu().numpy(), og["raw"]) <= 1e-3
     np.testing.assert_array_equal(g.touched.cpu().numpy(), og["touched"])
+
+
+def test_banded_binning_matches_single_band(rast):
+    """Bands of tile rows (config 4's memory path) give the same frame as one band,
+    and the banded backward the same gradients (up to atomic summation order)."""
+    from paper_2412_11752_b200.api import FrameGrad
+    sc = scenes.config_scene(2, n=30000)
+    cam = scenes.config_cameras(2)[0].crop(0, 0, 320, 256)
+    opt = api_options(opt_for(3))
+    rng = np.random.default_rng(9)
+    dc = torch.from_numpy(rng.uniform(-1, 1, (cam.height, cam.width, 3)).astype(np.float32))
+    fb1 = rast.render(sc.f32(), cam, opt)
+    ref = {f: getattr(fb1, f).clone() for f in ("color", "depth", "normal", "alpha")}
+    g1 = rast.backward_render(sc.f32(), FrameGrad(d_color=dc)).raw.clone()
+    pairs = rast.stats()["pairs"]
+    assert rast.bands() == 1
+    try:
+        rast.set_band_limit(max(1, pairs // 4))
+        fb4 = rast.render(sc.f32(), cam, opt)
+        assert rast.bands() >= 3
+        for f, v in ref.items():
+            assert torch.equal(getattr(fb4, f), v), f
+        assert rast.stats()["pairs"] == pairs
+        g4 = rast.backward_render(sc.f32(), FrameGrad(d_color=dc)).raw
+        assert rel_l2(g4.cpu().numpy(), g1.cpu().numpy()) <= 1e-5
+    finally:
+        rast.set_band_limit(0)
