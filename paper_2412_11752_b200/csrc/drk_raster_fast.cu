@@ -92,7 +92,10 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
   __shared__ TileConst tc;
   const int tile = P.tile_base + blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
-  const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
+  // warp w covers an 8 x 4 pixel block (spatially compact: coherent saturation
+  // depth and popped primitives across the lanes)
+  const int wv = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const int x = tx * kTile + (wv & 1) * 8 + (ln & 7), y = ty * kTile + (wv >> 1) * 4 + (ln >> 3);
   const bool active = x < P.cam.W && y < P.cam.H;
   const double tx0 = (double)tx * kTile, ty0 = (double)ty * kTile;
   // tile reference ray d0 (centre of the tile) and this pixel's offset dd
