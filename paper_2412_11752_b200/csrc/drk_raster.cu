@@ -893,7 +893,8 @@ __global__ void __launch_bounds__(256, DRK_RASTER_MIN_BLOCKS) k_raster(RasterPar
   __shared__ double s_num[256], s_r0[256], s_r1[256], s_r2[256];
   const int tile = P.tile_base + blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
-  const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
+  const int x = tx * kTile + ((threadIdx.x >> 5) & 1) * 8 + (threadIdx.x & 7),
+            y = ty * kTile + (threadIdx.x >> 6) * 4 + ((threadIdx.x & 31) >> 3);  // 8 x 4 per warp
   bool active = x < P.cam.W && y < P.cam.H;
   if (P.pxflag && (F64 || BWD) && active) {
     const bool flagged = P.pxflag[(size_t)y * P.cam.W + x] != 0;
@@ -1031,7 +1032,8 @@ __global__ void __launch_bounds__(256, DRK_BWD_MIN_BLOCKS) k_raster_bwd(RasterPa
   const unsigned FULL = 0xffffffffu;
   const int tile = P.tile_base + blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
-  const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
+  const int x = tx * kTile + ((threadIdx.x >> 5) & 1) * 8 + (threadIdx.x & 7),
+            y = ty * kTile + (threadIdx.x >> 6) * 4 + ((threadIdx.x & 31) >> 3);  // 8 x 4 per warp
   bool active = x < P.cam.W && y < P.cam.H;
   if (P.pxflag && active) {
     const bool flagged = P.pxflag[(size_t)y * P.cam.W + x] != 0;

@@ -326,7 +326,8 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
   __shared__ TileConst tc;
   const int tile = P.tile_base + blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
-  const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
+  const int x = tx * kTile + ((threadIdx.x >> 5) & 1) * 8 + (threadIdx.x & 7),
+            y = ty * kTile + (threadIdx.x >> 6) * 4 + ((threadIdx.x & 31) >> 3);  // 8 x 4 per warp
   bool active = x < P.cam.W && y < P.cam.H;
   if (active && P.pxflag && P.pxflag[(size_t)y * P.cam.W + x]) active = false;  // fp64 backward owns flagged pixels
   if (__syncthreads_count(active) == 0) return;
