@@ -173,12 +173,22 @@ static int plan_bands(drk_ctx* c) {
   const int n = c->act.n;
   c->bands.assign({0, cd.tiles_y});
   if (n == 0 || cd.tiles_y <= 1) return DRK_OK;
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
-  const size_t held = c->pk.bytes + c->pv.bytes + c->pk2.bytes + c->pv2.bytes + c->hist.bytes + c->sortoff.bytes;
-  const double budget = 0.7 * (double)(free_b + held) / 34.0;
-  const double limit = c->band_pair_limit > 0 ? (double)c->band_pair_limit : budget;
-  // every primitive in every tile: fits without looking closer
+  // cudaMemGetInfo is slow (tens of ms): the device size is queried once per
+  // context and free memory only when a trivial bound does not fit
+  if (c->device_bytes == 0) {
+    size_t f0 = 0, t0 = 0;
+    cudaMemGetInfo(&f0, &t0);
+    c->device_bytes = t0;
+  }
+  if (c->band_pair_limit == 0 && (double)n * cd.tiles_x * cd.tiles_y <= 0.25 * (double)c->device_bytes / 34.0)
+    return DRK_OK;  // every primitive in every tile would still fit in a quarter of the device
+  double limit = (double)c->band_pair_limit;
+  if (limit <= 0) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t held = c->pk.bytes + c->pv.bytes + c->pk2.bytes + c->pv2.bytes + c->hist.bytes + c->sortoff.bytes;
+    limit = 0.7 * (double)(free_b + held) / 34.0;
+  }
   if ((double)n * cd.tiles_x * cd.tiles_y <= limit) return DRK_OK;
   unsigned long long* rowest = ensure<unsigned long long>(c->rowest, cd.tiles_y + 1);
   if (!rowest) return set_error(c, DRK_ERR_OOM, "row estimates");

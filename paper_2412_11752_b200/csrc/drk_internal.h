@@ -117,6 +117,7 @@ struct drk_ctx {
   drk::DevBuf rowest;
   std::vector<int> bands;         // tile-row band boundaries of the last forward
   long long band_pair_limit = 0;  // test hook: force bands above this many pairs (0 = memory-based)
+  size_t device_bytes = 0;        // cudaMemGetInfo total, queried once
   int64_t pts_cap = 0;
 
   // stage timing
