@@ -76,8 +76,8 @@ typedef struct drk_options {
   int32_t record_replay;            /* default 0 */
   int32_t fp64_alpha;               /* default 0; 1 = every alpha in fp64 (reference-precision mode:
                                        identical arithmetic across cache / list / exact-sort modes) */
-  int32_t raster_kernel;            /* 0 = auto (fp32 interval forward where eligible, warp-reduced backward),
-                                       1 = legacy fp64-depth forward, 4 = auto + fp32 interval backward */
+  int32_t raster_kernel;            /* 0 = auto (fp32 interval forward and backward where eligible),
+                                       1 = legacy fp64-depth forward and backward, 5 = legacy backward only */
 } drk_options;
 
 /* Activated primitives (drk::DrkPrimitive, reference types.hpp:77-98), all

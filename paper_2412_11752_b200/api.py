@@ -52,9 +52,9 @@ class RenderOptions:
     exact_sort: bool = False
     presort: PresortMode = PresortMode.NearestDepth
     early_stop_transmittance: float = 1e-4
-    # B200 extension (not in the reference): 0 = fp32 interval forward where
-    # eligible (SortCache mode, K = 8), 1 = legacy fp64-depth forward,
-    # 4 = 0 plus the fp32 interval backward (drk_raster_bwd.cu)
+    # B200 extension (not in the reference): 0 = fp32 interval forward and
+    # backward where eligible (SortCache mode, K = 8), 1 = legacy fp64-depth
+    # kernels, 5 = legacy backward only
     raster_kernel: int = 0
 
 

@@ -14,7 +14,8 @@ __global__ void k_prep0(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, i
                         long long pool_cap, int* rowcnt, unsigned long long* counters, const int* list, int list_n,
                         double2* scratch, int scratch_cap, int* overflow);
 __global__ void k_prep_warp(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pts_pool,
-                            long long pts_cap, int2* ptsref, int* rowcnt, unsigned long long* counters, int* overflow);
+                            long long pts_cap, int2* ptsref, int* rowcnt, unsigned long long* counters, int* overflow,
+                            float4* frame32);
 __global__ void k_prep_hull(int n, const int2* ptsref, double2* pts_pool, CamD cam, OptD opt, int4* bbox, int2* hullref,
                             double2* pool, long long pool_cap, int* rowcnt, unsigned long long* counters);
 size_t prep_warp_smem();
@@ -144,6 +145,7 @@ static RasterParams raster_params(drk_ctx* c) {
   P.redo_list = static_cast<int*>(c->redo.p);
   P.redo_count = reinterpret_cast<unsigned int*>(ensure<unsigned long long>(c->redo_cnt, 1));
   P.shrec = A.rec;
+  P.frame32 = static_cast<const float4*>(c->frame32.p);
   return P;
 }
 
@@ -290,6 +292,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   const long long n_pix = (long long)cam->width * cam->height;
   unsigned long long* ctr = ensure<unsigned long long>(c->counters, C_COUNT);
   Geo* geo = ensure<Geo>(c->geo, n);
+  if (!ensure<float4>(c->frame32, 3 * (size_t)n)) return set_error(c, DRK_ERR_OOM, "frame buffer");
   int4* bbox = ensure<int4>(c->bbox, n);
   int2* hullref = ensure<int2>(c->hullref, n);
   int* rowcnt = ensure<int>(c->rowcnt, n + 1);
@@ -317,7 +320,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
         attr = true;
       }
       k_prep_warp<<<(n + 7) / 8, 256, smem, s>>>(A, cd, od, geo, bbox, hullref, ppool, c->pts_cap, ptsref, rowcnt,
-                                                   ctr, ovf);
+                                                   ctr, ovf, static_cast<float4*>(c->frame32.p));
       k_prep_hull<<<(unsigned)((2LL * n + 255) / 256), 256, 0, s>>>(n, ptsref, ppool, cd, od, bbox, hullref, pool,
                                                                     c->hull_cap, rowcnt, ctr);
     }
@@ -659,7 +662,7 @@ void drk_ctx_destroy(drk_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
                     &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
-                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->geo, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
+                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->geo, &c->frame32, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->pk2, &c->pv2,
                     &c->hist, &c->sortoff, &c->tilecnt, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,

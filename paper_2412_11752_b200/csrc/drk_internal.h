@@ -80,6 +80,7 @@ struct RasterParams {
   unsigned char* pxflag;  // 1 = pixel needs the fp64 re-render (uncertain termination)
   int* redo_list;         // flagged pixel indices (forward fp32 pass appends)
   unsigned int* redo_count;
+  const float4* frame32;  // per prim: (R_x, a_x), (R_y, a_y), (R_z, a_z) with a = o - mu, fp32 (backward)
   int tile_base;          // first tile of this launch (banded frames: tile rows processed band by band)
   const float* shrec;     // fast kernel: per-primitive fp32 shape records (K == 8)
   int* pxstop;            // composites until saturation per pixel (INT_MAX: never), written by the forward
@@ -108,7 +109,7 @@ struct drk_ctx {
   drk::Activated act{};
 
   // per view
-  drk::DevBuf geo, bbox, hullref, hull, ptspool, ptsref, rowcnt, rowoff, rows, rowpaircnt, rowpairoff;
+  drk::DevBuf geo, frame32, bbox, hullref, hull, ptspool, ptsref, rowcnt, rowoff, rows, rowpaircnt, rowpairoff;
   drk::DevBuf pk, pv, pk2, pv2, hist, sortoff, tilecnt, tileoff, cdirs, tdirs, bits;
   drk::DevBuf pxstate, replay_cnt, replay_rec, replay_ids;
   drk::DevBuf gact, touched;

@@ -492,7 +492,7 @@ __device__ __forceinline__ W2 weight_cs(const PolyParams& p, double a, double* c
 __global__ void __launch_bounds__(kPW * 32) k_prep_warp(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox,
                                                          int2* hullref, double2* pts_pool, long long pts_cap,
                                                          int2* ptsref, int* rowcnt, unsigned long long* counters,
-                                                         int* overflow) {
+                                                         int* overflow, float4* frame32) {
   extern __shared__ double4 prep_dyn[];
   const unsigned FULL = 0xffffffffu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -527,6 +527,12 @@ __global__ void __launch_bounds__(kPW * 32) k_prep_warp(Activated A, CamD cam, O
     const_cast<float*>(A.psif)[12 * (size_t)i + 8] = visible ? (float)(fv * fv) : __int_as_float(0x7f800000);
     g.dp2max = visible ? 2.0 * opt.lowpass_radius * opt.lowpass_radius * log(o / opt.alpha_min) * (1.0 + 1e-9) : 0.0;
     geo[i] = g;
+    if (frame32) {
+      const double a0 = cam.o[0] - g.mu[0], a1 = cam.o[1] - g.mu[1], a2 = cam.o[2] - g.mu[2];
+      frame32[3 * (size_t)i] = make_float4((float)g.rx[0], (float)g.rx[1], (float)g.rx[2], (float)a0);
+      frame32[3 * (size_t)i + 1] = make_float4((float)g.ry[0], (float)g.ry[1], (float)g.ry[2], (float)a1);
+      frame32[3 * (size_t)i + 2] = make_float4((float)g.rz[0], (float)g.rz[1], (float)g.rz[2], (float)a2);
+    }
     rowcnt[i] = 0;
     bbox[i] = make_int4(1, 0, 1, 0);
     hullref[i] = make_int2(0, 0);

@@ -1668,8 +1668,10 @@ void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s,
   }
   if (!bwd) cudaMemsetAsync(P.redo_count, 0, sizeof(unsigned), s);
   if (P.opt.use_cache) {
-    // fast backward (drk_raster_bwd.cu) on request: at parity with the legacy kernel so far (config 2: 66.8 vs 65 ms)
-    if (bwd && P.opt.raster_kernel == 4 && raster_fast_eligible(P)) launch_raster_bwd_fast(P, n_tiles, s);
+    // fp32 interval backward (drk_raster_bwd.cu) where eligible (config 2: 56.1 ms vs 63.9 ms legacy);
+    // raster_kernel 1 / 5 select the legacy warp-reduced kernel
+    if (bwd && P.opt.raster_kernel != 1 && P.opt.raster_kernel != 5 && raster_fast_eligible(P))
+      launch_raster_bwd_fast(P, n_tiles, s);
     else if (bwd) k_raster_bwd<0, false><<<n_tiles, 256, 0, s>>>(P);
     else if (P.opt.raster_kernel != 1 && raster_fast_eligible(P)) launch_raster_fast(P, n_tiles, P.vstat != nullptr, s);
     else k_raster<0, false, false><<<n_tiles, 256, 0, s>>>(P);

@@ -88,10 +88,10 @@ __device__ __forceinline__ void record_grad_fast(const RasterParams& P, const Bw
   float deta = 0, dtau = 0, dop = 0, ds_lo = 0, ds_hi = 0, da_lo = 0, da_hi = 0;
   int lo = 0, hi = 1;
   const float denf = gf.dz, af = (float)a;
-  const float rzf[3] = {(float)g.rz[0], (float)g.rz[1], (float)g.rz[2]};
-  float hv[3];
-#pragma unroll
-  for (int q = 0; q < 3; ++q) hv[q] = (float)(P.cam.o[q] - g.mu[q]) + rt * df[q];
+  const float4* fr = P.frame32 + 3 * (size_t)id;
+  const float4 fx = __ldg(fr), fy = __ldg(fr + 1), fz = __ldg(fr + 2);
+  const float rzf[3] = {fz.x, fz.y, fz.z};
+  float hv[3] = {fx.w + rt * df[0], fy.w + rt * df[1], fz.w + rt * df[2]};
   if (bp.has_dN) {
     drot[2] += wbf * sgn * bp.dN0;
     drot[5] += wbf * sgn * bp.dN1;
@@ -164,8 +164,8 @@ __device__ __forceinline__ void record_grad_fast(const RasterParams& P, const Bw
           da_lo += d_r1 * invd * (sa * k.a * cross - sb * k.a * slo * slo);
           da_hi += d_r1 * invd * (sa * k.b * shi * shi - sb * k.b * cross);
           // (u, v) and r_t chain to centre and rotation columns (grad.cpp:290-300)
-          const float rxf[3] = {(float)g.rx[0], (float)g.rx[1], (float)g.rx[2]};
-          const float ryf[3] = {(float)g.ry[0], (float)g.ry[1], (float)g.ry[2]};
+          const float rxf[3] = {fx.x, fx.y, fx.z};
+          const float ryf[3] = {fy.x, fy.y, fy.z};
           const float drx = df[0] * rxf[0] + df[1] * rxf[1] + df[2] * rxf[2];
           const float dry = df[0] * ryf[0] + df[1] * ryf[1] + df[2] * ryf[2];
           const float fq = -(du * drx + dv * dry) / denf;
@@ -504,21 +504,30 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
         }
         if (lane < kGCols && xv[0] != 0.f) atomicAdd(pg + gcol_global(lane), xv[0]);
       }
-      // SH: component k = 3 t + ch, lane k and lane k + 32
+      // SH: component k = 3 t + ch (t < 16), value w_ch basis_t(pixel), two
+      // 32-wide transposes (k = 0..31, 32..47)
 #pragma unroll
-      for (int rnd = 0; rnd < 2; ++rnd) {
-        const int k = lane + 32 * rnd;
-        const int t = k / 3, ch = k - 3 * t;
-        if (k < 48 && t < ta) {
-          float acc = 0.f;
-          unsigned m = gm;
-          while (m) {
-            const int l = __ffs(m) - 1;
-            m &= m - 1;
-            acc = fmaf(s_w_all[4 * (warp * 32 + l) + ch], s_basis_all[t * kBatch + warp * 32 + l], acc);
-          }
-          if (acc != 0.f) atomicAdd(pg + kGOffSh + k, acc);
+      for (int chunk = 0; chunk < 2; ++chunk) {
+        float xv[32];
+#pragma unroll
+        for (int i2 = 0; i2 < 32; ++i2) {
+          const int k = 32 * chunk + i2;
+          const int t = k / 3, ch = k - 3 * (k / 3);
+          const float wch = ch == 0 ? w0 : (ch == 1 ? w1 : w2);
+          xv[i2] = (k < 48 && t < ta && ((gm >> lane) & 1u)) ? wch * s_basis[t * kBatch] : 0.f;
         }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+          const bool up = (lane & off) != 0;
+#pragma unroll
+          for (int i2 = 0; i2 < off; ++i2) {
+            const float send = up ? xv[i2] : xv[i2 + off];
+            const float keep = up ? xv[i2 + off] : xv[i2];
+            xv[i2] = keep + __shfl_xor_sync(FULL, send, off);
+          }
+        }
+        const int k = 32 * chunk + lane;
+        if (k < 48 && xv[0] != 0.f) atomicAdd(pg + kGOffSh + k, xv[0]);
       }
     }
     __syncwarp();

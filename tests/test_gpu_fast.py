@@ -89,13 +89,13 @@ def test_fast_backward_termination_from_forward(rast):
     np.testing.assert_array_equal(g.touched.cpu().numpy(), og["touched"])
 
 
-def test_fast_backward_kernel_parity(rast):
-    """The opt-in fp32 interval backward (raster_kernel=4) against the oracle."""
+def test_legacy_backward_kernel_parity(rast):
+    """The legacy warp-reduced backward (raster_kernel=5) against the oracle."""
     import dataclasses
     from paper_2412_11752_b200.api import FrameGrad
     sc, cam = small_scene(seed=41, n=150, sh_degree=3, clusters=2)
     o = opt_for(3)
-    opt = dataclasses.replace(api_options(o), raster_kernel=4)
+    opt = dataclasses.replace(api_options(o), raster_kernel=5)
     rast.render(sc.f32(), cam, opt)
     rng = np.random.default_rng(5)
     dc = rng.uniform(-1, 1, (cam.height, cam.width, 3)).astype(np.float32)
