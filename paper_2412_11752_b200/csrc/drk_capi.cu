@@ -10,9 +10,6 @@
 namespace drk {
 
 // kernels defined in the other translation units
-__global__ void k_prep0(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pool,
-                        long long pool_cap, int* rowcnt, unsigned long long* counters, const int* list, int list_n,
-                        double2* scratch, int scratch_cap, int* overflow);
 __global__ void k_prep_warp(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pts_pool,
                             long long pts_cap, int2* ptsref, int* rowcnt, unsigned long long* counters, int* overflow,
                             float4* frame32);

@@ -1198,6 +1198,5 @@ namespace drk {
       int scratch_cap, int *overflow
 #define DRK_PREP_PASS \
   A, cam, opt, geo, bbox, hullref, pool, pool_cap, rowcnt, counters, list, list_n, scratch, scratch_cap, overflow
-__global__ void __launch_bounds__(128) k_prep0(DRK_PREP_ARGS) { prep_body<0>(DRK_PREP_PASS); }
 __global__ void __launch_bounds__(128) k_prep1(DRK_PREP_ARGS) { prep_body<1>(DRK_PREP_PASS); }
 }  // namespace drk

@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned long l
   __shared__ unsigned whist[kRsWarps][256];
   __shared__ unsigned bstart[256];
   __shared__ long long gbase[256];
-  __shared__ unsigned long long sk[kRsChunk], sv[kRsChunk];
+  extern __shared__ unsigned long long rs_dyn[];  // staging: keys then values, kRsChunk each
+  unsigned long long* sk = rs_dyn;
+  unsigned long long* sv = rs_dyn + kRsChunk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int d = threadIdx.x; d < kRsWarps * 256; d += kRsThreads) (&whist[0][0])[d] = 0;
   __syncthreads();
@@ -241,6 +243,12 @@ int sort_pairs(drk_ctx* c, unsigned long long*& k, unsigned long long*& v, unsig
   cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, s);
   if (int st = cuda_check(c, cudaStreamSynchronize(s), "sort bits")) return st;
   const unsigned long long vary_k = h[0] ^ h[1], vary_v = h[2] ^ h[3];
+  const size_t rs_smem = 2 * sizeof(unsigned long long) * kRsChunk;
+  static bool rs_attr = false;
+  if (!rs_attr) {
+    cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem);
+    rs_attr = true;
+  }
   struct Pass {
     int shift, from_v;
   };
@@ -254,7 +262,7 @@ int sort_pairs(drk_ctx* c, unsigned long long*& k, unsigned long long*& v, unsig
     const unsigned long long* src = passes[p].from_v ? v : k;
     k_rs_hist<<<nblk, kRsThreads, 0, s>>>(src, n, passes[p].shift, hist, nblk);
     if (int st = exclusive_scan<unsigned>(c, hist, (long long)256 * nblk, off, nullptr)) return st;
-    k_rs_scatter<<<nblk, kRsThreads, 0, s>>>(k, v, k2, v2, n, passes[p].shift, passes[p].from_v, off, nblk);
+    k_rs_scatter<<<nblk, kRsThreads, rs_smem, s>>>(k, v, k2, v2, n, passes[p].shift, passes[p].from_v, off, nblk);
     launch_counter() += 2;
     std::swap(k, k2);
     std::swap(v, v2);
