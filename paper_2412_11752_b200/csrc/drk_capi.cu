@@ -239,7 +239,7 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
   long long* rowpairoff = ensure<long long>(c->rowpairoff, n_rows + 1);
   if (!rows || !rowpaircnt || !rowpairoff) return set_error(c, DRK_ERR_OOM, "row buffers");
   if (n > 0)
-    k_rows<<<(n + 127) / 128, 128, 0, s>>>(n, bbox, static_cast<const int2*>(c->hullref.p),
+    k_rows<<<(unsigned)((32LL * n + 127) / 128), 128, 0, s>>>(n, bbox, static_cast<const int2*>(c->hullref.p),
                                            static_cast<const double2*>(c->hull.p), rowoff, cd, od, rows, rowpaircnt,
                                            ctr, ty_lo, ty_hi);
   long long n_pairs = 0;

@@ -886,8 +886,10 @@ __global__ void k_band_flagged(const unsigned char* __restrict__ pxflag, int W, 
 __global__ void k_rows(int n, const int4* __restrict__ bbox, const int2* __restrict__ hullref,
                        const double2* __restrict__ pool, const long long* __restrict__ rowoff, CamD cam, OptD opt,
                        int4* rows, int* rowpaircnt, unsigned long long* counters, int ty_lo, int ty_hi) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  // one warp per primitive, lanes over its tile rows
+  const int i = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;  // warp-uniform
   const int4 bb = bbox[i];
   if (bb.y < bb.x || bb.w < bb.z) return;
   const int2 hr = hullref[i];
@@ -901,9 +903,10 @@ __global__ void k_rows(int n, const int4* __restrict__ bbox, const int2* __restr
     amax = dmax(amax, dmax(fabs(h[j].x), fabs(h[j].y)));
   }
   const double delta = 1e-9 * amax + 1e-9;
-  long long ro = rowoff[i];
   unsigned long long ties = 0;
-  for (int ty = max(bb.z, ty_lo); ty <= min(bb.w, ty_hi - 1); ++ty, ++ro) {
+  const int tyA = max(bb.z, ty_lo);
+  for (int ty = tyA + lane; ty <= min(bb.w, ty_hi - 1); ty += 32) {
+    const long long ro = rowoff[i] + (ty - tyA);
     const double y0 = ty * kTile, y1 = y0 + kTile;
     const double Y0 = y0 - lp, Y1 = y1 + lp;
     // x-extent of H ∩ [Y0, Y1]
