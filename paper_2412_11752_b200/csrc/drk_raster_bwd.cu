@@ -318,8 +318,9 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
   int* s_id = reinterpret_cast<int*>(ring + kRing);
   float* s_basis_all = reinterpret_cast<float*>(s_id + kRing);  // [16][256]
   float* s_w_all = s_basis_all + 16 * kBatch;                   // [256][4]: SH weights per lane
+  float* s_row = s_w_all + 4 * kBatch;                           // [256][kGCols]: gradient rows (odd stride: no bank conflicts)
   const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   float* s_basis = s_basis_all + threadIdx.x;
   float* s_w = s_w_all + 4 * threadIdx.x;
   __shared__ unsigned s_ddmax;
@@ -415,9 +416,7 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
     bool rec = false;
     int id = -1;
     float w0 = 0.f, w1 = 0.f, w2 = 0.f;
-    float row[kGCols];
-#pragma unroll
-    for (int i = 0; i < kGCols; ++i) row[i] = 0.f;
+    float* row = s_row + kGCols * threadIdx.x;
     if (want) {
       Rec R;
       if (pj >= ring_lo) {
@@ -490,7 +489,7 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
         const bool in_g = (gm >> lane) & 1u;
         float xv[32];
 #pragma unroll
-        for (int i = 0; i < kGCols; ++i) xv[i] = in_g ? row[i] : 0.f;
+        for (int i = 0; i < kGCols; ++i) xv[i] = in_g ? row[i] : 0.f;  // row written this step by in_g lanes
         xv[31] = 0.f;
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) {
@@ -672,7 +671,9 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
   }
 }
 
-size_t raster_bwd_fast_smem() { return (size_t)kRing * (sizeof(Rec) + sizeof(int)) + (16 + 4) * kBatch * sizeof(float); }
+size_t raster_bwd_fast_smem() {
+  return (size_t)kRing * (sizeof(Rec) + sizeof(int)) + (16 + 4 + kGCols) * kBatch * sizeof(float);
+}
 
 void launch_raster_bwd_fast(const RasterParams& P, int n_tiles, cudaStream_t s) {
   const size_t smem = raster_bwd_fast_smem();
