@@ -23,19 +23,25 @@ __global__ void k_rows(int n, const int4* bbox, const int2* hullref, const doubl
                        CamD cam, OptD opt, int4* rows, int* rowpaircnt, unsigned long long* counters, int ty_lo,
                        int ty_hi);
 __global__ void k_band_rowcnt(int n, const int4* bbox, int ty_lo, int ty_hi, int* rowcnt);
-__global__ void k_row_pair_bound(int n, const int4* bbox, unsigned long long* rowest);
+__global__ void k_row_pair_bound(int n, int tiles_y, const int4* bbox, unsigned long long* rowest);
 __global__ void k_band_flagged(const unsigned char* pxflag, int W, int y0, int y1, int* list, unsigned* count);
 __global__ void k_tile_rays(CamD cam, double* cdirs, double* tdirs);
 __global__ void k_emit_rows(long long n_rows, const int4* rows, const long long* rowpairoff, const Geo* geo,
                             const double* cdirs, const double* tdirs, CamD cam, OptD opt, unsigned long long* pk,
-                            unsigned long long* pv, int* tilecnt);
-__global__ void k_emit(long long n_rows, const int4* rows, const long long* rowpairoff, const Geo* geo,
-                       const double* cdirs, const double* tdirs, CamD cam, OptD opt, unsigned long long* pk,
-                       unsigned long long* pv, int* tilecnt);
+                            unsigned* pv, unsigned* krange);
+__global__ void k_tile_bounds(long long n, const unsigned* sk, int dbits, int n_tiles, long long* tileoff);
+__global__ void k_key_hist(long long n, const unsigned long long* pk, const unsigned* krange, unsigned* hist);
+__global__ void k_key_map(const unsigned* hist, const unsigned* krange, int dbits, unsigned* map);
+__global__ void k_pack_keys(long long n, const unsigned long long* pk, const unsigned* krange, const unsigned* map,
+                            int dbits, unsigned* sk);
+__global__ void k_tie_keys(long long n, const unsigned* sk, const unsigned* sv, int dbits, const Geo* geo,
+                           const double* cdirs, const double* tdirs, CamD cam, OptD opt, unsigned long long* fk);
+__global__ void k_tie_fix(long long n, const unsigned* sk, unsigned* sv, unsigned long long* fk);
+__global__ void k_full_keys(long long n, const unsigned* sk, const unsigned* sv, int dbits, const Geo* geo,
+                            const double* cdirs, const double* tdirs, CamD cam, OptD opt, double* out);
 template <typename T>
 int exclusive_scan(drk_ctx* c, const T* in, long long n, long long* out, long long* total);
-int sort_pairs(drk_ctx* c, unsigned long long*& k, unsigned long long*& v, unsigned long long*& k2,
-               unsigned long long*& v2, long long n);
+int sort_pairs(drk_ctx* c, unsigned* k, unsigned* v, unsigned* k2, unsigned* v2, long long n);
 void launch_act_bwd(int n, int K, int terms, const float* raw, const float* gact, int G,
                     const unsigned char* touched_dev, const Geo* geo, const CamD& cam, float* grad_raw,
                     float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
@@ -131,7 +137,7 @@ static RasterParams raster_params(drk_ctx* c) {
   P.cam = c->camd;
   P.opt = c->optd;
   P.tileoff = static_cast<const long long*>(c->tileoff.p);
-  P.pv = static_cast<const unsigned long long*>(c->pv.p);
+  P.lid = static_cast<const int*>(c->pv.p);
   P.geo = static_cast<const Geo*>(c->geo.p);
   const Activated& A = c->act;
   P.S = ShapeView{A.s, A.th, A.ex, A.ey, A.det, A.eta, A.tau, A.o, A.thf, A.invdetf, A.piogf, A.hf, A.psif, A.K};
@@ -167,6 +173,10 @@ static float elapsed(drk_ctx* c, int a, int b) {
 // Bands of tile rows: one band unless the frame's pairs (upper bound from the
 // bounding boxes) would not fit in device memory; then greedy bands whose
 // bound fits (SURVEY.md §7 hard part 5: banded binning for config 4).
+// device bytes per (tile, primitive) pair: emitted 64-bit keys (reused as the
+// sort's second buffer), sorted keys and ids (8 + 4 + 4), plus row / tile scratch
+constexpr double kPairBytes = 18.0;
+
 static int plan_bands(drk_ctx* c) {
   const CamD& cd = c->camd;
   const int n = c->act.n;
@@ -179,27 +189,28 @@ static int plan_bands(drk_ctx* c) {
     cudaMemGetInfo(&f0, &t0);
     c->device_bytes = t0;
   }
-  if (c->band_pair_limit == 0 && (double)n * cd.tiles_x * cd.tiles_y <= 0.25 * (double)c->device_bytes / 34.0)
+  if (c->band_pair_limit == 0 && (double)n * cd.tiles_x * cd.tiles_y <= 0.25 * (double)c->device_bytes / kPairBytes)
     return DRK_OK;  // every primitive in every tile would still fit in a quarter of the device
   double limit = (double)c->band_pair_limit;
   if (limit <= 0) {
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    const size_t held = c->pk.bytes + c->pv.bytes + c->pk2.bytes + c->pv2.bytes + c->hist.bytes + c->sortoff.bytes;
-    limit = 0.7 * (double)(free_b + held) / 34.0;
+    const size_t held = c->pk.bytes + c->pv.bytes + c->sk.bytes + c->hist.bytes + c->sortoff.bytes;
+    limit = 0.7 * (double)(free_b + held) / kPairBytes;
   }
   if ((double)n * cd.tiles_x * cd.tiles_y <= limit) return DRK_OK;
   unsigned long long* rowest = ensure<unsigned long long>(c->rowest, cd.tiles_y + 1);
   if (!rowest) return set_error(c, DRK_ERR_OOM, "row estimates");
   cudaMemsetAsync(rowest, 0, sizeof(unsigned long long) * (cd.tiles_y + 1), c->stream);
-  k_row_pair_bound<<<(n + 255) / 256, 256, 0, c->stream>>>(n, static_cast<const int4*>(c->bbox.p), rowest);
+  if (cd.tiles_y > 6000) return set_error(c, DRK_ERR_UNSUPPORTED, "more than 6000 tile rows");
+  k_row_pair_bound<<<std::min((n + 255) / 256, 148 * 4), 256, sizeof(unsigned long long) * cd.tiles_y, c->stream>>>(
+      n, cd.tiles_y, static_cast<const int4*>(c->bbox.p), rowest);
   DRK_COUNT_LAUNCH();
   std::vector<unsigned long long> est(cd.tiles_y);
   cudaMemcpyAsync(est.data(), rowest, sizeof(unsigned long long) * cd.tiles_y, cudaMemcpyDeviceToHost, c->stream);
   if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "band plan")) return st;
   unsigned long long total = 0;
   for (auto e : est) total += e;
-  // bytes per pair: keys + values double-buffered (32 B) + sort histograms / offsets (~1.5 B)
   if ((double)total <= limit) return DRK_OK;
   c->bands.assign({0});
   unsigned long long acc = 0;
@@ -245,26 +256,49 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
   long long n_pairs = 0;
   if (int st = exclusive_scan<int>(c, rowpaircnt, n_rows, rowpairoff, &n_pairs)) return st;
   unsigned long long* pk = ensure<unsigned long long>(c->pk, n_pairs + 1);
-  unsigned long long* pv = ensure<unsigned long long>(c->pv, n_pairs + 1);
-  unsigned long long* pk2 = ensure<unsigned long long>(c->pk2, n_pairs + 1);
-  unsigned long long* pv2 = ensure<unsigned long long>(c->pv2, n_pairs + 1);
-  int* tilecnt = ensure<int>(c->tilecnt, n_tiles + 1);
+  unsigned* pv = ensure<unsigned>(c->pv, n_pairs + 1);
+  unsigned* sk = ensure<unsigned>(c->sk, n_pairs + 1);
+  unsigned* krange = ensure<unsigned>(c->bits, 2 + 2 * 4096);  // range, sampled histogram, q map
   long long* tileoff = ensure<long long>(c->tileoff, n_tiles + 1);
-  if (!pk || !pv || !pk2 || !pv2 || !tilecnt || !tileoff) return set_error(c, DRK_ERR_OOM, "pair buffers");
-  cudaMemsetAsync(tilecnt, 0, sizeof(int) * (n_tiles + 1), s);
+  if (!pk || !pv || !sk || !krange || !tileoff) return set_error(c, DRK_ERR_OOM, "pair buffers");
+  const unsigned kr0[2] = {0xffffffffu, 0u};
+  cudaMemcpyAsync(krange, kr0, sizeof kr0, cudaMemcpyHostToDevice, s);
   if (n_rows > 0)
     k_emit_rows<<<(unsigned)((n_rows * 16 + 255) / 256), 256, 0, s>>>(
         n_rows, rows, rowpairoff, static_cast<const Geo*>(c->geo.p), static_cast<const double*>(c->cdirs.p),
-        static_cast<const double*>(c->tdirs.p), cd, od, pk, pv, tilecnt);
+        static_cast<const double*>(c->tdirs.p), cd, od, pk, pv, krange);
   launch_counter() += 2;
   mark(c, 3);
-  if (int st = sort_pairs(c, pk, pv, pk2, pv2, n_pairs)) return st;
-  if (pk != c->pk.p) {  // keep the sorted arrays in c->pk / c->pv
-    std::swap(c->pk, c->pk2);
-    std::swap(c->pv, c->pv2);
+  // sort key: tile in the high bits, the quantised depth key in the rest
+  int tbits = 1;
+  while ((1ll << tbits) < n_tiles) ++tbits;
+  c->key_dbits = std::min(26, 32 - tbits);  // k_key_map packs base << 5 in 32 bits
+  if (n_pairs > 0) {
+    unsigned* khist = krange + 2;
+    unsigned* kmap = khist + 4096;
+    cudaMemsetAsync(khist, 0, sizeof(unsigned) * 4096, s);
+    const unsigned nb = (unsigned)std::min<long long>((n_pairs + 256 * 8 * 4 - 1) / (256 * 8 * 4), 148 * 8);
+    k_key_hist<<<nb, 256, 0, s>>>(n_pairs, pk, krange, khist);
+    k_key_map<<<1, 1024, 0, s>>>(khist, krange, c->key_dbits, kmap);
+    k_pack_keys<<<(unsigned)std::min<long long>((n_pairs + 1023) / 1024, 148 * 16), 256, 0, s>>>(n_pairs, pk, krange, kmap,
+                                                                                             c->key_dbits, sk);
+    launch_counter() += 3;
   }
-  long long tot = 0;
-  if (int st = exclusive_scan<int>(c, tilecnt, n_tiles + 1, tileoff, &tot)) return st;
+  // the emitted 64-bit keys are dead after packing: their buffer is the sort's
+  // ping-pong space (four passes end back in sk / pv)
+  unsigned* tmp = reinterpret_cast<unsigned*>(pk);
+  if (int st = sort_pairs(c, sk, pv, tmp, tmp + n_pairs + 1, n_pairs)) return st;
+  if (n_pairs > 1) {
+    // runs of equal sort keys: full keys (into the dead emission buffer), then order
+    const unsigned nb = (unsigned)((n_pairs + 255) / 256);
+    k_tie_keys<<<nb, 256, 0, s>>>(n_pairs, sk, pv, c->key_dbits, static_cast<const Geo*>(c->geo.p),
+                                  static_cast<const double*>(c->cdirs.p), static_cast<const double*>(c->tdirs.p), cd,
+                                  od, pk);
+    k_tie_fix<<<nb, 256, 0, s>>>(n_pairs, sk, pv, pk);
+    launch_counter() += 2;
+  }
+  k_tile_bounds<<<(unsigned)((n_pairs + 256) / 256), 256, 0, s>>>(n_pairs, sk, c->key_dbits, n_tiles, tileoff);
+  DRK_COUNT_LAUNCH();
   mark(c, 4);
   *n_pairs_out = n_pairs;
   return DRK_OK;
@@ -660,8 +694,8 @@ void drk_ctx_destroy(drk_ctx* c) {
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
                     &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
                     &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->geo, &c->frame32, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
-                    &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->pk2, &c->pv2,
-                    &c->hist, &c->sortoff, &c->tilecnt, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
+                    &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->sk,
+                    &c->hist, &c->sortoff, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
                     &c->counters, &c->scan_tmp, &c->loss_tmp};
   for (DevBuf* b : bufs) release(*b);
@@ -767,18 +801,27 @@ int drk_get_tile_lists(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* id
   const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
   if (offsets)
     cudaMemcpyAsync(offsets, c->tileoff.p, sizeof(int64_t) * (n_tiles + 1), cudaMemcpyDeviceToHost, c->stream);
-  std::vector<unsigned long long> v, k;
+  std::vector<unsigned> v;
   if (ids) {
     v.resize(c->n_pairs);
-    cudaMemcpyAsync(v.data(), c->pv.p, sizeof(unsigned long long) * c->n_pairs, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(v.data(), c->pv.p, sizeof(unsigned) * c->n_pairs, cudaMemcpyDeviceToHost, c->stream);
   }
-  if (keys) {
-    k.resize(c->n_pairs);
-    cudaMemcpyAsync(k.data(), c->pk.p, sizeof(unsigned long long) * c->n_pairs, cudaMemcpyDeviceToHost, c->stream);
+  if (keys && c->n_pairs > 0) {
+    // the sort carries truncated keys; the full fp64 keys are recomputed
+    DevBuf tmp;
+    double* kd = ensure<double>(tmp, c->n_pairs);
+    if (!kd) return set_error(c, DRK_ERR_OOM, "key buffer");
+    k_full_keys<<<(unsigned)((c->n_pairs + 255) / 256), 256, 0, c->stream>>>(
+        c->n_pairs, static_cast<const unsigned*>(c->sk.p), static_cast<const unsigned*>(c->pv.p), c->key_dbits,
+        static_cast<const Geo*>(c->geo.p), static_cast<const double*>(c->cdirs.p),
+        static_cast<const double*>(c->tdirs.p), c->camd, c->optd, kd);
+    cudaMemcpyAsync(keys, kd, sizeof(double) * c->n_pairs, cudaMemcpyDeviceToHost, c->stream);
+    const int st = cuda_check(c, cudaStreamSynchronize(c->stream), "tile keys");
+    release(tmp);
+    if (st) return st;
   }
   if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "tile lists")) return st;
-  for (int64_t i = 0; ids && i < c->n_pairs; ++i) ids[i] = (int32_t)(v[i] & 0xffffffffull);
-  for (int64_t i = 0; keys && i < c->n_pairs; ++i) std::memcpy(&keys[i], &k[i], sizeof(double));
+  for (int64_t i = 0; ids && i < c->n_pairs; ++i) ids[i] = (int32_t)v[i];
   return DRK_OK;
 }
 

@@ -187,7 +187,7 @@ static __device__ __noinline__ void pop_f64(const RasterParams& P, int id, int x
 }
 
 __device__ __forceinline__ int entry_id(const RasterParams& P, const int* s_id, long long beg, int jr, int ring_lo) {
-  return jr >= ring_lo ? s_id[jr & (kRing - 1)] : (int)(P.pv[beg + jr] & 0xffffffffull);
+  return jr >= ring_lo ? s_id[jr & (kRing - 1)] : P.lid[beg + jr];
 }
 
 // ---------------------------------------------------------------------------
@@ -514,7 +514,7 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
     R = ring[slot];
     id = s_id[slot];
   } else {
-    id = (int)(P.pv[beg + jr] & 0xffffffffull);
+    id = P.lid[beg + jr];
     stage_record(P, id, tc, R);
     ++px.n_miss;
   }

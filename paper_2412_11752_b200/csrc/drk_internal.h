@@ -60,7 +60,7 @@ struct RasterParams {
   CamD cam;
   OptD opt;
   const long long* tileoff;
-  const unsigned long long* pv;  // sorted (tile << 32 | pid)
+  const int* lid;  // sorted tile lists: primitive ids (offsets in tileoff)
   const Geo* geo;
   ShapeView S;
   const float* sh;
@@ -110,7 +110,8 @@ struct drk_ctx {
 
   // per view
   drk::DevBuf geo, frame32, bbox, hullref, hull, ptspool, ptsref, rowcnt, rowoff, rows, rowpaircnt, rowpairoff;
-  drk::DevBuf pk, pv, pk2, pv2, hist, sortoff, tilecnt, tileoff, cdirs, tdirs, bits;
+  drk::DevBuf pk, pv, sk, hist, sortoff, tileoff, cdirs, tdirs, bits;
+  int key_dbits = 19;  // depth bits of the packed 32-bit sort keys (32 - tile bits)
   drk::DevBuf pxstate, replay_cnt, replay_rec, replay_ids;
   drk::DevBuf gact, touched;
   drk::DevBuf counters, scan_tmp, loss_tmp;

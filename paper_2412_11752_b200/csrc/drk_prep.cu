@@ -866,12 +866,20 @@ __global__ void k_band_rowcnt(int n, const int4* __restrict__ bbox, int ty_lo, i
 
 // Upper bound of the pairs per tile row (bbox width per covered row), for
 // choosing the bands.
-__global__ void k_row_pair_bound(int n, const int4* __restrict__ bbox, unsigned long long* rowest) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int4 bb = bbox[i];
-  if (bb.y < bb.x || bb.w < bb.z) return;
-  for (int ty = bb.z; ty <= bb.w; ++ty) atomicAdd(&rowest[ty], (unsigned long long)(bb.y - bb.x + 1));
+__global__ void k_row_pair_bound(int n, int tiles_y, const int4* __restrict__ bbox, unsigned long long* rowest) {
+  // per-block tile-row sums in shared memory (tiles_y <= kRowEstSmem), one
+  // global atomic per row and block
+  extern __shared__ unsigned long long s_est[];
+  for (int t = threadIdx.x; t < tiles_y; t += blockDim.x) s_est[t] = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int4 bb = bbox[i];
+    if (bb.y < bb.x || bb.w < bb.z) continue;
+    for (int ty = bb.z; ty <= bb.w; ++ty) atomicAdd(&s_est[ty], (unsigned long long)(bb.y - bb.x + 1));
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < tiles_y; t += blockDim.x)
+    if (s_est[t]) atomicAdd(&rowest[t], s_est[t]);
 }
 
 // Backward of a banded frame: the band's flagged pixels (fp64 re-render list).
@@ -997,55 +1005,42 @@ __global__ void k_tile_rays(CamD cam, double* cdirs, double* tdirs) {
 }
 
 // classify_intersect depth only (geometry.cpp:40-48).
-__device__ __forceinline__ bool hit_depth(const double* d, const Geo& g, double eps, double* rt) {
-  const double denom = d[0] * g.rz[0] + d[1] * g.rz[1] + d[2] * g.rz[2];
-  if (fabs(denom) < eps) return false;
-  const double r = g.num / denom;
-  if (r <= 0) return false;
-  *rt = r;
-  return true;
+// Ray-plane depth of one corner / centre ray: +inf when grazing or behind
+// (raster.cpp:99-115 nearest_depth_key).  One expression for every caller so
+// the emitted keys, the tie fix and drk_get_tile_lists agree bit for bit.
+__device__ __forceinline__ double ray_depth(const double* d, double rz0, double rz1, double rz2, double num,
+                                            double eps) {
+  const double denom = d[0] * rz0 + d[1] * rz1 + d[2] * rz2;
+  if (fabs(denom) < eps) return __longlong_as_double(0x7ff0000000000000ll);
+  const double q = num / denom;
+  return q > 0 ? q : __longlong_as_double(0x7ff0000000000000ll);
 }
 
-// K3: emit (key, tile|pid) pairs row by row (raster.cpp:233-257).
-__global__ void k_emit(long long n_rows, const int4* __restrict__ rows, const long long* __restrict__ rowpairoff,
-                       const Geo* __restrict__ geo, const double* __restrict__ cdirs,
-                       const double* __restrict__ tdirs, CamD cam, OptD opt, unsigned long long* pk,
-                       unsigned long long* pv, int* tilecnt) {
-  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (r >= n_rows) return;
-  const int4 rr = rows[r];
-  if (rr.w < rr.z) return;
-  const int pid = rr.x, ty = rr.y;
-  const Geo g = geo[pid];
-  long long pos = rowpairoff[r];
-  const int cw = cam.tiles_x + 1;
-  for (int tx = rr.z; tx <= rr.w; ++tx, ++pos) {
-    double key;
-    if (opt.presort == 0) {
-      key = (double)pid;
-    } else if (opt.presort == 1) {
-      key = g.projz;
-    } else {
-      // nearest_depth_key (raster.cpp:99-115): corners (x0,y0) (x1,y0) (x1,y1) (x0,y1), centre
-      const int c00 = ty * cw + tx;
-      const double* dirs[5] = {cdirs + 3 * (size_t)c00, cdirs + 3 * (size_t)(c00 + 1),
-                               cdirs + 3 * (size_t)(c00 + cw + 1), cdirs + 3 * (size_t)(c00 + cw),
-                               tdirs + 3 * (size_t)(ty * cam.tiles_x + tx)};
-      double best = __longlong_as_double(0x7ff0000000000000ll);
-      for (int q = 0; q < 5; ++q) {
-        const double d[3] = {dirs[q][0], dirs[q][1], dirs[q][2]};
-        double rt;
-        if (hit_depth(d, g, opt.grazing_eps, &rt)) best = dmin(best, rt);
-      }
-      if (isinf(best) && g.has_proj) best = g.projz;
-      key = best;
-    }
-    const int tile = ty * cam.tiles_x + tx;
-    pk[pos] = (unsigned long long)__double_as_longlong(key);
-    pv[pos] = ((unsigned long long)(unsigned)tile << 32) | (unsigned)pid;
-    atomicAdd(&tilecnt[tile], 1);
-  }
+// Full fp64 presort key of (tile, primitive) (raster.cpp:99-115, 233-257).
+__device__ double pair_key(const Geo& g, int pid, int tile, const CamD& cam, const OptD& opt,
+                           const double* __restrict__ cdirs, const double* __restrict__ tdirs) {
+  if (opt.presort == 0) return (double)pid;
+  if (opt.presort == 1) return g.projz;
+  const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x, cw = cam.tiles_x + 1;
+  const int c00 = ty * cw + tx;
+  const double rz0 = g.rz[0], rz1 = g.rz[1], rz2 = g.rz[2], num = g.num, eps = opt.grazing_eps;
+  const double top = ray_depth(cdirs + 3 * (size_t)c00, rz0, rz1, rz2, num, eps);
+  const double rtop = ray_depth(cdirs + 3 * (size_t)(c00 + 1), rz0, rz1, rz2, num, eps);
+  const double rbot = ray_depth(cdirs + 3 * (size_t)(c00 + cw + 1), rz0, rz1, rz2, num, eps);
+  const double bot = ray_depth(cdirs + 3 * (size_t)(c00 + cw), rz0, rz1, rz2, num, eps);
+  const double cen = ray_depth(tdirs + 3 * (size_t)tile, rz0, rz1, rz2, num, eps);
+  double best = dmin(dmin(dmin(top, rtop), dmin(rbot, bot)), cen);
+  if (isinf(best) && g.has_proj) best = g.projz;
+  return best;
 }
+
+// Total order of the fp64 keys as unsigned integers (numeric order; the
+// reference compares the doubles with <).
+__device__ __forceinline__ unsigned long long key_order(double key) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(key);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+constexpr unsigned kInfKey32 = 0xfff00000u;  // key_order(+inf) >> 32: keys at or above are not finite
 
 // K3 with 16 lanes per row: lane l owns tile ta + l (chunks of 16), evaluates
 // its left corner rays and its centre ray, and takes the right corners from
@@ -1057,26 +1052,27 @@ __global__ void __launch_bounds__(256) k_emit_rows(long long n_rows, const int4*
                                                    const long long* __restrict__ rowpairoff,
                                                    const Geo* __restrict__ geo, const double* __restrict__ cdirs,
                                                    const double* __restrict__ tdirs, CamD cam, OptD opt,
-                                                   unsigned long long* pk, unsigned long long* pv, int* tilecnt) {
+                                                   unsigned long long* pk, unsigned* pv,
+                                                   unsigned* krange /* min, max finite key32 */) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long r = t / kEmitLanes;
   const int l = (int)(t % kEmitLanes);
   const unsigned seg = 0xffffu << (threadIdx.x & 16);  // this lane's 16-lane segment
-  if (r >= n_rows) return;  // whole segments (n_rows * 16 threads, 16 | 32)
-  const int4 rr = rows[r];
-  if (rr.w < rr.z) return;  // segment-uniform
+  __shared__ unsigned s_kr[2];
+  if (threadIdx.x == 0) {
+    s_kr[0] = 0xffffffffu;
+    s_kr[1] = 0u;
+  }
+  __syncthreads();
+  int4 rr = make_int4(0, 0, 0, -1);  // rows past the end: empty (every thread reaches the block reduction)
+  if (r < n_rows) rr = rows[r];
   const int pid = rr.x, ty = rr.y;
   const Geo& g = geo[pid];
-  const long long pos0 = rowpairoff[r];
+  const long long pos0 = r < n_rows ? rowpairoff[r] : 0;
   const int cw = cam.tiles_x + 1;
-  const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const double rz0 = g.rz[0], rz1 = g.rz[1], rz2 = g.rz[2], num = g.num, eps = opt.grazing_eps;
-  auto depth = [&](const double* d) -> double {
-    const double denom = d[0] * rz0 + d[1] * rz1 + d[2] * rz2;
-    if (fabs(denom) < eps) return inf;
-    const double q = num / denom;
-    return q > 0 ? q : inf;
-  };
+  auto depth = [&](const double* d) -> double { return ray_depth(d, rz0, rz1, rz2, num, eps); };
+  unsigned kmin = 0xffffffffu, kmax = 0u;
   for (int base = rr.z; base <= rr.w; base += kEmitLanes) {
     const int tx = base + l;
     const bool valid = tx <= rr.w;
@@ -1099,14 +1095,203 @@ __global__ void __launch_bounds__(256) k_emit_rows(long long n_rows, const int4*
       if (isinf(best) && g.has_proj) best = g.projz;
       key = best;
     }
+    // top 32 bits of the key's numeric order; k_pack_keys quantises them
+    // against the frame's finite key range
+    const unsigned k32 = (unsigned)(key_order(key) >> 32);
     if (valid) {
       const int tile = ty * cam.tiles_x + tx;
       const long long pos = pos0 + (tx - rr.z);
-      pk[pos] = (unsigned long long)__double_as_longlong(key);
-      pv[pos] = ((unsigned long long)(unsigned)tile << 32) | (unsigned)pid;
-      atomicAdd(&tilecnt[tile], 1);
+      pk[pos] = ((unsigned long long)(unsigned)tile << 32) | k32;
+      pv[pos] = (unsigned)pid;
     }
+    kmin = min(kmin, valid && k32 < kInfKey32 ? k32 : 0xffffffffu);
+    kmax = max(kmax, valid && k32 < kInfKey32 ? k32 : 0u);
   }
+  // block reduction of the finite key range, one atomic pair per block
+  kmin = __reduce_min_sync(seg, kmin);
+  kmax = __reduce_max_sync(seg, kmax);
+  if ((threadIdx.x & 15) == 0) {
+    atomicMin(&s_kr[0], kmin);
+    atomicMax(&s_kr[1], kmax);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_kr[0] != 0xffffffffu) atomicMin(&krange[0], s_kr[0]);
+    if (s_kr[1] != 0u) atomicMax(&krange[1], s_kr[1]);
+  }
+}
+
+// Sort key of each emitted pair: tile << dbits | q, q a monotone map of the
+// key32 (key_order >> 32) to dbits bits.  The map equalises the depth density
+// so that few pairs of one tile share a q (each such run costs k_tie_fix an
+// insertion sort on full keys): the finite key range [lo, hi] is cut into
+// kQBins bins of 2^shift0 key32 units, a sample of the pairs is histogrammed,
+// and bin j gets a power-of-two share a_j of the q space (proportional to its
+// count, at least 1), q = base_j + ((k32 - start_j) >> s_j).  Non-finite keys
+// take the top q.  Any monotone map gives the same final order (ties are
+// resolved on the full key); this one only keeps the runs short.
+constexpr int kQBins = 4096, kQSample = 8;
+
+__device__ __forceinline__ int qbin_shift(unsigned lo, unsigned hi) {
+  const unsigned span = hi > lo ? hi - lo : 0u;
+  const int len = 32 - __clz(span);  // bits of the span
+  return len > 12 ? len - 12 : 0;    // span >> shift0 < kQBins
+}
+
+__global__ void __launch_bounds__(256) k_key_hist(long long n, const unsigned long long* __restrict__ pk,
+                                                  const unsigned* __restrict__ krange, unsigned* hist) {
+  __shared__ unsigned h[kQBins];
+  for (int j = threadIdx.x; j < kQBins; j += blockDim.x) h[j] = 0;
+  __syncthreads();
+  const unsigned lo = krange[0], hi = krange[1];
+  const int sh = qbin_shift(lo, hi);
+  const long long stride = (long long)gridDim.x * blockDim.x * kQSample;
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * kQSample; i < n; i += stride) {
+    const unsigned k32 = (unsigned)pk[i];
+    if (k32 >= lo && k32 <= hi) atomicAdd(&h[min((k32 - lo) >> sh, (unsigned)kQBins - 1u)], 1u);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < kQBins; j += blockDim.x)
+    if (h[j]) atomicAdd(&hist[j], h[j]);
+}
+
+// One block: per-bin share exponents and bases (map[j] = base << 5 | s_j).
+__global__ void __launch_bounds__(1024) k_key_map(const unsigned* __restrict__ hist, const unsigned* __restrict__ krange,
+                                                  int dbits, unsigned* map) {
+  __shared__ unsigned long long tot_s;
+  __shared__ unsigned wsum[32];
+  if (threadIdx.x == 0) tot_s = 0;
+  __syncthreads();
+  constexpr int kPer = kQBins / 1024;
+  unsigned c[kPer];
+  unsigned long long t = 0;
+  for (int q = 0; q < kPer; ++q) {
+    c[q] = hist[threadIdx.x * kPer + q];
+    t += c[q];
+  }
+  atomicAdd(&tot_s, t);
+  __syncthreads();
+  const double tot = (double)(tot_s ? tot_s : 1ull);
+  const int sh = qbin_shift(krange[0], krange[1]);
+  const double budget = (double)((1u << dbits) - 1u - kQBins);  // the +1 minimum of every bin on top
+  unsigned a[kPer], run = 0;
+  int sj[kPer];
+  for (int q = 0; q < kPer; ++q) {
+    const double want = budget * (double)c[q] / tot;
+    int e = want >= 1.0 ? (int)floor(log2(want)) : 0;  // a_j = 2^e <= want (at least 1)
+    e = min(e, sh);                                    // never finer than one key32 unit
+    a[q] = 1u << e;
+    sj[q] = sh - e;
+    run += a[q];
+  }
+  // block exclusive scan of the per-thread totals
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned incl = run;
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    unsigned v = wsum[lane], x = v;
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    wsum[lane] = x - v;
+  }
+  __syncthreads();
+  unsigned base = wsum[w] + incl - run;
+  for (int q = 0; q < kPer; ++q) {
+    map[threadIdx.x * kPer + q] = base << 5 | (unsigned)sj[q];
+    base += a[q];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_pack_keys(long long n, const unsigned long long* __restrict__ pk,
+                                                   const unsigned* __restrict__ krange,
+                                                   const unsigned* __restrict__ map, int dbits, unsigned* sk) {
+  __shared__ unsigned m[kQBins];
+  for (int j = threadIdx.x; j < kQBins; j += blockDim.x) m[j] = map[j];
+  __syncthreads();
+  const unsigned lo = krange[0], hi = krange[1];
+  const int sh = qbin_shift(lo, hi);
+  const unsigned qmax = (1u << dbits) - 1u;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = pk[i];
+    const unsigned k32 = (unsigned)k;
+    unsigned q = qmax;
+    if (k32 >= lo && k32 <= hi) {
+      const unsigned off = k32 - lo;
+      const unsigned j = min(off >> sh, (unsigned)kQBins - 1u);
+      const unsigned e = m[j];
+      q = (e >> 5) + ((off - (j << sh)) >> (e & 31u));
+    }
+    sk[i] = ((unsigned)(k >> 32) << dbits) | q;
+  }
+}
+
+// After the sort: runs of equal sort keys are put in (full fp64 key, pid)
+// order, the reference's order (raster.cpp:260-263: each tile list sorted by
+// key, ties by primitive id).  Two passes: every entry inside a run computes
+// its full key (one thread each), then each run's first entry insertion-sorts
+// the run on those keys.
+__device__ __forceinline__ bool in_run(long long n, const unsigned* sk, long long i, unsigned k) {
+  return (i + 1 < n && sk[i + 1] == k) || (i > 0 && sk[i - 1] == k);
+}
+
+__global__ void k_tie_keys(long long n, const unsigned* __restrict__ sk, const unsigned* __restrict__ sv, int dbits,
+                           const Geo* __restrict__ geo, const double* __restrict__ cdirs,
+                           const double* __restrict__ tdirs, CamD cam, OptD opt, unsigned long long* fk) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned k = sk[i];
+  if (!in_run(n, sk, i, k)) return;
+  const unsigned pid = sv[i];
+  fk[i] = key_order(pair_key(geo[pid], (int)pid, (int)(k >> dbits), cam, opt, cdirs, tdirs));
+}
+
+__global__ void k_tie_fix(long long n, const unsigned* __restrict__ sk, unsigned* sv, unsigned long long* fk) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i + 1 >= n) return;
+  const unsigned k = sk[i];
+  if (sk[i + 1] != k || (i > 0 && sk[i - 1] == k)) return;
+  long long e = i + 2;
+  while (e < n && sk[e] == k) ++e;
+  for (long long a = i + 1; a < e; ++a) {
+    const unsigned pa = sv[a];
+    const unsigned long long ka = fk[a];
+    long long b = a - 1;
+    while (b >= i && (fk[b] > ka || (fk[b] == ka && sv[b] > pa))) {
+      sv[b + 1] = sv[b];
+      fk[b + 1] = fk[b];
+      --b;
+    }
+    sv[b + 1] = pa;
+    fk[b + 1] = ka;
+  }
+}
+
+// Tile offsets from the sorted keys (tile = key >> dbits): thread i writes
+// the starts of the tiles in (tile(i-1), tile(i)]; thread n closes the rest.
+__global__ void k_tile_bounds(long long n, const unsigned* __restrict__ sk, int dbits, int n_tiles,
+                              long long* tileoff) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const int t = i < n ? (int)(sk[i] >> dbits) : n_tiles;
+  const int tp = i > 0 ? (int)(sk[i - 1] >> dbits) : -1;
+  for (int tt = tp + 1; tt <= t; ++tt) tileoff[tt] = i;
+}
+
+// Full fp64 keys of the sorted lists (drk_get_tile_lists).
+__global__ void k_full_keys(long long n, const unsigned* __restrict__ sk, const unsigned* __restrict__ sv, int dbits,
+                            const Geo* __restrict__ geo, const double* __restrict__ cdirs,
+                            const double* __restrict__ tdirs, CamD cam, OptD opt, double* out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned pid = sv[i];
+  out[i] = pair_key(geo[pid], (int)pid, (int)(sk[i] >> dbits), cam, opt, cdirs, tdirs);
 }
 
 // ---------------------------------------------------------------------------

@@ -915,7 +915,7 @@ __global__ void __launch_bounds__(256, DRK_RASTER_MIN_BLOCKS) k_raster(RasterPar
     __syncthreads();
     const long long j = b0 + threadIdx.x;
     if (j < end) {
-      const int id = (int)(P.pv[j] & 0xffffffffull);
+      const int id = P.lid[j];
       const Geo& g = P.geo[id];
       s_id[threadIdx.x] = id;
       s_num[threadIdx.x] = g.num;
@@ -1064,7 +1064,7 @@ __global__ void __launch_bounds__(256, DRK_BWD_MIN_BLOCKS) k_raster_bwd(RasterPa
       __syncthreads();
       const long long j = b0 + threadIdx.x;
       if (j < end) {
-        const int id = (int)(P.pv[j] & 0xffffffffull);
+        const int id = P.lid[j];
         const Geo& g = P.geo[id];
         s_id[threadIdx.x] = id;
         s_num[threadIdx.x] = g.num;
@@ -1229,7 +1229,7 @@ __device__ void process_pixel(const RasterParams& P, int pix) {
       double best_d = 0;
       long long best_j = -1;
       for (long long j = beg; j < end; ++j) {
-        const Geo& g = P.geo[(int)(P.pv[j] & 0xffffffffull)];
+        const Geo& g = P.geo[P.lid[j]];
         const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.rz[0], g.rz[1], g.rz[2]);
         if (fabs(denom) < P.opt.grazing_eps) continue;
         const double rt = g.num / denom;
@@ -1243,11 +1243,11 @@ __device__ void process_pixel(const RasterParams& P, int pix) {
       if (best_j < 0) break;
       last_d = best_d;
       last_j = best_j;
-      done = !px.composite(P, best_d, (int)(P.pv[best_j] & 0xffffffffull));
+      done = !px.composite(P, best_d, P.lid[best_j]);
     }
   } else {
     for (long long j = beg; j < end && !done; ++j) {
-      const int id = (int)(P.pv[j] & 0xffffffffull);
+      const int id = P.lid[j];
       const Geo& g = P.geo[id];
       const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.rz[0], g.rz[1], g.rz[2]);
       if (fabs(denom) < P.opt.grazing_eps) continue;
@@ -1377,7 +1377,7 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
         int id = -1;
         bool hit = false;
         if (jj < end) {
-          id = (int)(P.pv[jj] & 0xffffffffull);
+          id = P.lid[jj];
           const Geo& g = P.geo[id];
           const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.rz[0], g.rz[1], g.rz[2]);
           if (fabs(denom) >= P.opt.grazing_eps) {
@@ -1609,7 +1609,7 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
     double best_d = 0;
     long long best_j = -1;
     for (long long j = beg; j < end; ++j) {
-      const int id = (int)(P.pv[j] & 0xffffffffull);
+      const int id = P.lid[j];
       const Geo& g = P.geo[id];
       const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.rz[0], g.rz[1], g.rz[2]);
       if (fabs(denom) < P.opt.grazing_eps) continue;
@@ -1625,7 +1625,7 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
     if (best_j < 0) break;
     last_d = best_d;
     last_j = best_j;
-    if (!px.composite(P, best_d, (int)(P.pv[best_j] & 0xffffffffull))) break;
+    if (!px.composite(P, best_d, P.lid[best_j])) break;
   }
   if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
   if (!BWD) px.finish_forward(P);

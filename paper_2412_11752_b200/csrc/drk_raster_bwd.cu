@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
         R = ring[slot];
         id = s_id[slot];
       } else {
-        id = (int)(P.pv[beg + pj] & 0xffffffffull);
+        id = P.lid[beg + pj];
         stage_record(P, id, tc, R);
       }
       AlphaOut o;
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
     {
       const long long j = b0 + threadIdx.x;
       if (j < end) {
-        const int id = (int)(P.pv[j] & 0xffffffffull);
+        const int id = P.lid[j];
         const int slot = (jb + threadIdx.x) & (kRing - 1);
         stage_record(P, id, tc, ring[slot]);
         s_id[slot] = id;

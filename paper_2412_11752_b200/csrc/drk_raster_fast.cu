@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
     {
       const long long j = b0 + threadIdx.x;
       if (j < end) {
-        const int id = (int)(P.pv[j] & 0xffffffffull);
+        const int id = P.lid[j];
         const int slot = (jb + threadIdx.x) & (kRing - 1);
         stage_record(P, id, tc, ring[slot]);
         s_id[slot] = id;

@@ -4,8 +4,10 @@
 // Per pass: k_rs_hist (per-CTA digit histogram, digit-major layout) ->
 // exclusive scan of the 256 x nblk histogram -> k_rs_scatter (stable ranks via
 // warp match_any + per-warp running counts, then warp prefix per digit).
-// Pairs are (key u64, value u64); the digit comes from either word.  Passes
-// whose digit is constant over all elements are skipped (OR/AND reduction).
+// Pairs are (key u32, value u32): key = tile << b | b-bit monotone quantisation
+// of the fp64 depth key (k_pack_keys, drk_prep.cu), value = primitive id; four
+// 8-bit passes.  Runs of equal keys are ordered afterwards on the full fp64 key
+// (k_tie_fix, drk_prep.cu), so the sort itself need not be stable.
 #include "drk_internal.h"
 
 namespace drk {
@@ -104,30 +106,7 @@ template int exclusive_scan<unsigned>(drk_ctx*, const unsigned*, long long, long
 #endif
 constexpr int kRsWarps = 8, kRsItems = DRK_RS_ITEMS, kRsThreads = kRsWarps * 32, kRsChunk = kRsThreads * kRsItems;
 
-__global__ void k_bits(const unsigned long long* __restrict__ k, const unsigned long long* __restrict__ v, long long n,
-                       unsigned long long* acc /* or_k, and_k, or_v, and_v */) {
-  unsigned long long ok = 0, ak = ~0ull, ov = 0, av = ~0ull;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    ok |= k[i];
-    ak &= k[i];
-    ov |= v[i];
-    av &= v[i];
-  }
-  for (int off = 16; off > 0; off >>= 1) {
-    ok |= __shfl_down_sync(0xffffffffu, ok, off);
-    ak &= __shfl_down_sync(0xffffffffu, ak, off);
-    ov |= __shfl_down_sync(0xffffffffu, ov, off);
-    av &= __shfl_down_sync(0xffffffffu, av, off);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicOr(&acc[0], ok);
-    atomicAnd(&acc[1], ak);
-    atomicOr(&acc[2], ov);
-    atomicAnd(&acc[3], av);
-  }
-}
-
-__global__ void __launch_bounds__(kRsThreads) k_rs_hist(const unsigned long long* __restrict__ src, long long n,
+__global__ void __launch_bounds__(kRsThreads) k_rs_hist(const unsigned* __restrict__ src, long long n,
                                                         int shift, unsigned* hist, int nblk) {
   __shared__ unsigned cnt[256];
   cnt[threadIdx.x] = 0;
@@ -135,7 +114,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_hist(const unsigned long long
   const long long base = (long long)blockIdx.x * kRsChunk;
   for (int k = 0; k < kRsItems; ++k) {
     const long long i = base + k * kRsThreads + threadIdx.x;
-    if (i < n) atomicAdd(&cnt[(unsigned)(src[i] >> shift) & 255u], 1u);
+    if (i < n) atomicAdd(&cnt[(src[i] >> shift) & 255u], 1u);
   }
   __syncthreads();
   hist[(size_t)threadIdx.x * nblk + blockIdx.x] = cnt[threadIdx.x];
@@ -144,23 +123,23 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_hist(const unsigned long long
 // One stable LSD pass: per-warp match-based ranks, block-local digit order
 // staged in shared memory, then written out digit run by digit run so that
 // consecutive threads store consecutive addresses of one bucket.
-__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned long long* __restrict__ kin,
-                                                           const unsigned long long* __restrict__ vin,
-                                                           unsigned long long* kout, unsigned long long* vout,
-                                                           long long n, int shift, int digit_from_v,
+__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned* __restrict__ kin,
+                                                           const unsigned* __restrict__ vin,
+                                                           unsigned* kout, unsigned* vout,
+                                                           long long n, int shift,
                                                            const long long* __restrict__ offs, int nblk) {
   __shared__ unsigned whist[kRsWarps][256];
   __shared__ unsigned bstart[256];
   __shared__ long long gbase[256];
-  extern __shared__ unsigned long long rs_dyn[];  // staging: keys then values, kRsChunk each
-  unsigned long long* sk = rs_dyn;
-  unsigned long long* sv = rs_dyn + kRsChunk;
+  extern __shared__ unsigned rs_dyn[];  // staging: keys then values, kRsChunk each
+  unsigned* sk = rs_dyn;
+  unsigned* sv = rs_dyn + kRsChunk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int d = threadIdx.x; d < kRsWarps * 256; d += kRsThreads) (&whist[0][0])[d] = 0;
   __syncthreads();
   const long long base = (long long)blockIdx.x * kRsChunk + (long long)warp * 32 * kRsItems;
   const unsigned lt = (1u << lane) - 1u;
-  unsigned long long kk[kRsItems], vv[kRsItems];
+  unsigned kk[kRsItems], vv[kRsItems];
   int dig[kRsItems];
   unsigned rank[kRsItems];
 #pragma unroll
@@ -169,7 +148,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned long l
     const bool valid = i < n;
     kk[r] = valid ? kin[i] : 0;
     vv[r] = valid ? vin[i] : 0;
-    const int d = valid ? (int)((unsigned)((digit_from_v ? vv[r] : kk[r]) >> shift) & 255u) : 256;
+    const int d = valid ? (int)((kk[r] >> shift) & 255u) : 256;
     dig[r] = d;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const unsigned cur = valid ? whist[warp][d] : 0;
@@ -216,53 +195,28 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned long l
   const long long cnt_ll = n - (long long)blockIdx.x * kRsChunk;
   const int cnt = cnt_ll < kRsChunk ? (int)cnt_ll : kRsChunk;
   for (int idx = threadIdx.x; idx < cnt; idx += kRsThreads) {
-    const unsigned long long key = sk[idx], val = sv[idx];
-    const int d = (int)((unsigned)((digit_from_v ? val : key) >> shift) & 255u);
+    const unsigned key = sk[idx], val = sv[idx];
+    const int d = (int)((key >> shift) & 255u);
     const long long pos = gbase[d] + (idx - (long long)bstart[d]);
     kout[pos] = key;
     vout[pos] = val;
   }
 }
 
-// Stable sort of (k, v) pairs, first by the 64-bit key, then by bits [32, 48)
-// of v (the tile id).  Result ends in (k, v) (buffers swapped as needed).
-int sort_pairs(drk_ctx* c, unsigned long long*& k, unsigned long long*& v, unsigned long long*& k2,
-               unsigned long long*& v2, long long n) {
+// LSD sort of (k, v) pairs by the 32-bit key (stable; four passes, so the
+// result ends in the input buffers).
+int sort_pairs(drk_ctx* c, unsigned* k, unsigned* v, unsigned* k2, unsigned* v2, long long n) {
   if (n <= 1) return DRK_OK;
   cudaStream_t s = c->stream;
-  unsigned long long* acc = ensure<unsigned long long>(c->bits, 4);
   const int nblk = (int)((n + kRsChunk - 1) / kRsChunk);
   unsigned* hist = ensure<unsigned>(c->hist, (size_t)256 * nblk);
   long long* off = ensure<long long>(c->sortoff, (size_t)256 * nblk);
-  if (!acc || !hist || !off) return set_error(c, DRK_ERR_OOM, "sort scratch");
-  const unsigned long long init[4] = {0ull, ~0ull, 0ull, ~0ull};
-  cudaMemcpyAsync(acc, init, sizeof init, cudaMemcpyHostToDevice, s);
-  k_bits<<<min(nblk * 8, 148 * 8), 256, 0, s>>>(k, v, n, acc);
-  DRK_COUNT_LAUNCH();
-  unsigned long long h[4];
-  cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, s);
-  if (int st = cuda_check(c, cudaStreamSynchronize(s), "sort bits")) return st;
-  const unsigned long long vary_k = h[0] ^ h[1], vary_v = h[2] ^ h[3];
-  const size_t rs_smem = 2 * sizeof(unsigned long long) * kRsChunk;
-  static bool rs_attr = false;
-  if (!rs_attr) {
-    cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem);
-    rs_attr = true;
-  }
-  struct Pass {
-    int shift, from_v;
-  };
-  Pass passes[10];
-  int np = 0;
-  for (int d = 0; d < 8; ++d)
-    if ((vary_k >> (8 * d)) & 255ull) passes[np++] = {8 * d, 0};
-  for (int d = 4; d < 6; ++d)
-    if ((vary_v >> (8 * d)) & 255ull) passes[np++] = {8 * d, 1};
-  for (int p = 0; p < np; ++p) {
-    const unsigned long long* src = passes[p].from_v ? v : k;
-    k_rs_hist<<<nblk, kRsThreads, 0, s>>>(src, n, passes[p].shift, hist, nblk);
+  if (!hist || !off) return set_error(c, DRK_ERR_OOM, "sort scratch");
+  const size_t rs_smem = 2 * sizeof(unsigned) * kRsChunk;
+  for (int d = 0; d < 4; ++d) {
+    k_rs_hist<<<nblk, kRsThreads, 0, s>>>(k, n, 8 * d, hist, nblk);
     if (int st = exclusive_scan<unsigned>(c, hist, (long long)256 * nblk, off, nullptr)) return st;
-    k_rs_scatter<<<nblk, kRsThreads, rs_smem, s>>>(k, v, k2, v2, n, passes[p].shift, passes[p].from_v, off, nblk);
+    k_rs_scatter<<<nblk, kRsThreads, rs_smem, s>>>(k, v, k2, v2, n, 8 * d, off, nblk);
     launch_counter() += 2;
     std::swap(k, k2);
     std::swap(v, v2);

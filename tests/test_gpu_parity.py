@@ -59,6 +59,32 @@ def test_small_scene_modes(rast, presort, mode):
     _fb_close(fb, port.render(sc, cam, o))
 
 
+@pytest.mark.parametrize("presort", [1, 2])
+def test_sort_key_ties(rast, presort):
+    """Primitives whose presort keys agree in the sort's 32 truncated key bits
+    (centres a few f32 ulps apart, emitted in descending depth) and exact
+    duplicates: the lists must still follow the reference's (fp64 key, id) order."""
+    base, cam = small_scene(seed=5, n=30)
+    cols = []
+    for i in range(base.n):
+        for m in (3, 2, 1, 0, 0):
+            c = base.raw[:, i].copy()
+            z = np.float32(c[2])
+            for _ in range(m):
+                z = np.nextafter(z, np.float32(np.inf))
+            c[2] = float(z)
+            cols.append(c)
+    sc = scenes.Scene(raw=np.stack(cols, axis=1), k=base.k, sh_degree=base.sh_degree)
+    o = opt_for(0, presort=presort)
+    fb = rast.render(sc.f32(), cam, api_options(o))
+    bins = rast.tile_binning()
+    orc = port.bin_primitives(sc, cam, o)
+    _bins_equal(bins, orc)
+    keys = orc[2].view(np.uint64)
+    assert len(keys) > 100 and np.any(keys[1:] == keys[:-1])  # exact ties present
+    _fb_close(fb, port.render(sc, cam, o))
+
+
 def test_sh_degree3_and_k4(rast):
     sc = scenes.random_scene(120, seed=11, k=4, sh_degree=3)
     cam = scenes.look_at_camera(80, 64, (0.0, 0.5, -3.0))
