@@ -691,17 +691,17 @@ __global__ void __launch_bounds__(kPW * 32) k_prep_warp(Activated A, CamD cam, O
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   for (int t = nv + lane; t < P2; t += 32) W.verts[t] = make_double2(inf, inf);
   __syncwarp();
+  // each lane takes compare pairs (t, t + jj) directly: no idle lanes
   for (int kk = 2; kk <= P2; kk <<= 1) {
     for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-      for (int t = lane; t < P2; t += 32) {
-        const int u = t ^ jj;
-        if (u > t) {
-          const double2 a = W.verts[t], c = W.verts[u];
-          const bool up = (t & kk) == 0;
-          if (up ? lessp2(c, a) : lessp2(a, c)) {
-            W.verts[t] = c;
-            W.verts[u] = a;
-          }
+      for (int q = lane; q < (P2 >> 1); q += 32) {
+        const int t = ((q & ~(jj - 1)) << 1) | (q & (jj - 1));
+        const int u = t + jj;
+        const double2 a = W.verts[t], c = W.verts[u];
+        const bool up = (t & kk) == 0;
+        if (up ? lessp2(c, a) : lessp2(a, c)) {
+          W.verts[t] = c;
+          W.verts[u] = a;
         }
       }
       __syncwarp();
