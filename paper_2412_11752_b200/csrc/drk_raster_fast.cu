@@ -82,13 +82,15 @@ void launch_shape_rec(const ShapeView& S, int n, float* rec, cudaStream_t s) {
   }
 }
 
+__device__ __forceinline__ void write_pixel(const RasterParams& P, const FastPixel& px, int x, int y);
+
 template <bool VALIDATE, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant__ RasterParams P) {
   extern __shared__ float4 dyn[];
   Rec* ring = reinterpret_cast<Rec*>(dyn);
   int* s_id = reinterpret_cast<int*>(ring + kRing);
   float4* s_b4 = reinterpret_cast<float4*>(s_id + kRing) + threadIdx.x;  // [4][256] float4, this thread's column
-  __shared__ unsigned s_ddmax;
+  __shared__ unsigned s_ddmax, s_done;
   __shared__ TileConst tc;
   const int tile = P.tile_base + blockIdx.x;
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
   }
   if (threadIdx.x == 0) {
     s_ddmax = 0u;
+    s_done = 0u;
     tc.d0[0] = d0[0];
     tc.d0[1] = d0[1];
     tc.d0[2] = d0[2];
@@ -294,7 +297,16 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
         if (v[k]) atomicAdd(&P.counters[slots[k]], v[k]);
     }
   }
-  if (!active) return;
+  if (active) write_pixel(P, px, x, y);
+  if (P.progress) {
+    // the CTA's last thread to finish marks the tile done for the copy-out
+    // (drk_forward_host waits on the band counter with a stream memory op)
+    __threadfence();
+    if (atomicAdd(&s_done, 1u) == blockDim.x - 1u) atomicAdd(&P.progress[(tile / P.cam.tiles_x) / P.prog_rows], 1u);
+  }
+}
+
+__device__ __forceinline__ void write_pixel(const RasterParams& P, const FastPixel& px, int x, int y) {
   if (px.err) atomicAdd(&P.counters[C_ERR_DEGEN_BASIS], 1ull);
   const size_t p = (size_t)y * P.cam.W + x;
   const double c0 = (double)px.C0 + px.T * P.opt.bg[0];

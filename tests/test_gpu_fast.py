@@ -131,3 +131,29 @@ def test_banded_binning_matches_single_band(rast):
         assert rel_l2(g4.cpu().numpy(), g1.cpu().numpy()) <= 1e-5
     finally:
         rast.set_band_limit(0)
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_forward_host_copy_out_matches_device(rast, cfg):
+    """drk_forward_host copies framebuffer bands out while the raster runs and patches
+    the fp64-re-rendered pixels afterwards: bitwise the device forward's frame."""
+    sc = scenes.config_scene(cfg)
+    cam = scenes.config_cameras(cfg)[0]
+    opt = api_options(opt_for(scenes.CONFIGS[cfg]["sh_degree"]))
+    fb = rast.render(sc.f32(), cam, opt)
+    dev = {f: getattr(fb, f).cpu().numpy().copy() for f in ("color", "depth", "normal", "alpha")}
+    flagged = rast.stats()["fp64_pixels"]
+    if cfg == 1:
+        assert flagged > 0  # the patch path is exercised
+    for pinned in (False, True):
+        if pinned:
+            outs = {f: torch.empty(v.shape, dtype=torch.float32).pin_memory() for f, v in dev.items()}
+            raw = torch.from_numpy(sc.f32()).pin_memory()
+            rast.render_host_ptrs(raw, outs, cam, opt)
+            torch.cuda.synchronize()
+            out = {f: t.numpy() for f, t in outs.items()}
+        else:
+            out = rast.render_host(sc.f32(), cam, opt)
+        assert rast.stats()["fp64_pixels"] == flagged
+        for f, v in dev.items():
+            np.testing.assert_array_equal(out[f], v, err_msg=f"{f} pinned={pinned}")
