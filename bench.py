@@ -334,8 +334,8 @@ def main():
         cams3 = scenes.config_cameras(3)[:args.multiview_views]
         raw3 = torch.from_numpy(sc3.f32()).to(dev)
         mine = shard_views(len(cams3), world, rank)
-        for v in mine[:1]:
-            r.render(raw3, cams3[v], opt)  # warm-up (allocations)
+        for v in mine:
+            r.render(raw3, cams3[v], opt)  # warm-up pass over this rank's views (buffers reach their peak sizes)
         torch.cuda.synchronize(dev)
         nmv = max(1, min(args.steps, 3))
         mv_ms = []
