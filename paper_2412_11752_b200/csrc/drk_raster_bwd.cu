@@ -351,6 +351,12 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
 #pragma unroll
     for (int t = 0; t < 16; ++t) s_basis[t * kBatch] = b[t];
   }
+  float bas[16];  // this pixel's SH basis, zero beyond the active terms (SH gradient columns)
+  {
+    const int ta = P.opt.terms_active;
+#pragma unroll
+    for (int t = 0; t < 16; ++t) bas[t] = t < ta ? s_basis[t * kBatch] : 0.f;
+  }
   if (threadIdx.x == 0) {
     s_ddmax = 0u;
     tc.d0[0] = d0[0];
@@ -475,7 +481,6 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
     ++n_steps;
     __syncwarp();
     unsigned remaining = recmask;
-    const int ta = P.opt.terms_active;
     while (remaining) {
       const int lead = __ffs(remaining) - 1;
       const int gid = __shfl_sync(FULL, id, lead);
@@ -503,30 +508,51 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
         }
         if (lane < kGCols && xv[0] != 0.f) atomicAdd(pg + gcol_global(lane), xv[0]);
       }
-      // SH: component k = 3 t + ch (t < 16), value w_ch basis_t(pixel), two
-      // 32-wide transposes (k = 0..31, 32..47)
+      // SH: component k = 3 t + ch (t < 16), value w_ch basis_t(pixel):
+      // k = 0..31 by a 32-wide transpose, k = 32..47 by a 16-value halving
+      // transpose (16 shuffles) that leaves value v in lanes 2v and 2v + 1
+      {
+        const bool ing = (gm >> lane) & 1u;
+        const float m0 = ing ? w0 : 0.f, m1 = ing ? w1 : 0.f, m2 = ing ? w2 : 0.f;
+        {
+          float xv[32];
 #pragma unroll
-      for (int chunk = 0; chunk < 2; ++chunk) {
-        float xv[32];
-#pragma unroll
-        for (int i2 = 0; i2 < 32; ++i2) {
-          const int k = 32 * chunk + i2;
-          const int t = k / 3, ch = k - 3 * (k / 3);
-          const float wch = ch == 0 ? w0 : (ch == 1 ? w1 : w2);
-          xv[i2] = (k < 48 && t < ta && ((gm >> lane) & 1u)) ? wch * s_basis[t * kBatch] : 0.f;
-        }
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-          const bool up = (lane & off) != 0;
-#pragma unroll
-          for (int i2 = 0; i2 < off; ++i2) {
-            const float send = up ? xv[i2] : xv[i2 + off];
-            const float keep = up ? xv[i2 + off] : xv[i2];
-            xv[i2] = keep + __shfl_xor_sync(FULL, send, off);
+          for (int i2 = 0; i2 < 32; ++i2) {
+            const int ch = i2 % 3;
+            xv[i2] = (ch == 0 ? m0 : (ch == 1 ? m1 : m2)) * bas[i2 / 3];
           }
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) {
+            const bool up = (lane & off) != 0;
+#pragma unroll
+            for (int i2 = 0; i2 < off; ++i2) {
+              const float send = up ? xv[i2] : xv[i2 + off];
+              const float keep = up ? xv[i2 + off] : xv[i2];
+              xv[i2] = keep + __shfl_xor_sync(FULL, send, off);
+            }
+          }
+          if (xv[0] != 0.f) atomicAdd(pg + kGOffSh + lane, xv[0]);
         }
-        const int k = 32 * chunk + lane;
-        if (k < 48 && xv[0] != 0.f) atomicAdd(pg + kGOffSh + k, xv[0]);
+        {
+          float xv[16];
+#pragma unroll
+          for (int i2 = 0; i2 < 16; ++i2) {
+            const int k = 32 + i2, ch = k % 3;
+            xv[i2] = (ch == 0 ? m0 : (ch == 1 ? m1 : m2)) * bas[k / 3];
+          }
+#pragma unroll
+          for (int off = 16, h = 8; off >= 2; off >>= 1, h >>= 1) {
+            const bool up = (lane & off) != 0;
+#pragma unroll
+            for (int i2 = 0; i2 < h; ++i2) {
+              const float send = up ? xv[i2] : xv[i2 + h];
+              const float keep = up ? xv[i2 + h] : xv[i2];
+              xv[i2] = keep + __shfl_xor_sync(FULL, send, off);
+            }
+          }
+          xv[0] += __shfl_xor_sync(FULL, xv[0], 1);
+          if (!(lane & 1) && xv[0] != 0.f) atomicAdd(pg + kGOffSh + 32 + (lane >> 1), xv[0]);
+        }
       }
     }
     __syncwarp();
