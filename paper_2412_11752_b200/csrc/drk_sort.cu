@@ -150,7 +150,15 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned* __res
     vv[r] = valid ? vin[i] : 0;
     const int d = valid ? (int)((kk[r] >> shift) & 255u) : 256;
     dig[r] = d;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    // lanes with the same digit: intersection of per-bit ballots (bit 8 marks
+    // invalid items)
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+      const bool bit = (d >> b) & 1;
+      const unsigned bal = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? bal : ~bal;
+    }
     const unsigned cur = valid ? whist[warp][d] : 0;
     rank[r] = cur + __popc(peers & lt);
     __syncwarp();
