@@ -45,7 +45,10 @@ typedef enum drk_status {
   DRK_ERR_INVALID_ARG = 7,
   DRK_ERR_CUDA = 8,
   DRK_ERR_OOM = 9,
-  DRK_ERR_UNSUPPORTED = 10
+  DRK_ERR_UNSUPPORTED = 10,
+  DRK_ERR_IO = 11,                /* drk::IoError (io.cpp:51,60) */
+  DRK_ERR_CORRUPT_FILE = 12,      /* drk::CorruptFileError (io.cpp:63,68,72,80) */
+  DRK_ERR_VERSION = 13            /* drk::VersionMismatchError (io.cpp:70,74) */
 } drk_status;
 
 /* drk::Camera (reference geometry.hpp:9-19). */
@@ -234,6 +237,27 @@ typedef struct drk_adam_config {
  * OptState::step (host value, incremented). */
 int drk_adam_step(drk_ctx* ctx, float* params, const float* grads, float* m, float* v, int n,
                   int k, int sh_terms, int64_t* step, const drk_adam_config* cfg);
+
+/* --- scene files (DRKSCENE v1, reference io.hpp:20-25, io.cpp:40-97) ------ */
+typedef struct drk_scene_header {
+  int32_t version;      /* 1 */
+  int32_t basis_count;  /* K */
+  int32_t sh_degree;    /* 0..3 */
+  int32_t scalar_count; /* scalar_count(K, (sh_degree+1)^2): floats per primitive */
+  int64_t count;        /* primitives */
+} drk_scene_header;
+/* Header checks of drk::load_scene (io.cpp:58-80): DRK_ERR_IO (cannot open),
+ * DRK_ERR_CORRUPT_FILE (missing / malformed / implausible header, payload size
+ * not count records), DRK_ERR_VERSION (version != 1, K != expected_basis_count
+ * when that is > 0).  No device work. */
+int drk_scene_read_header(const char* path, int expected_basis_count, drk_scene_header* out);
+/* drk::load_scene (io.cpp:58-97) straight to the device: raw_dev (device,
+ * capacity primitives) receives the scene in the C-ABI raw layout, f32
+ * [scalar_count][count] (record-major file -> scalar-major device, bit-exact). */
+int drk_scene_load(drk_ctx* ctx, const char* path, int expected_basis_count, float* raw_dev, int64_t capacity,
+                   drk_scene_header* out);
+/* drk::save_scene (io.cpp:40-56) from device raw parameters f32 [S][n]. */
+int drk_scene_save(drk_ctx* ctx, const char* path, const float* raw_dev, int n, int k, int sh_degree);
 
 /* --- validation hook ----------------------------------------------------- */
 /* Samples the fp32 alpha fast path against the fp64 path on the activated

@@ -38,8 +38,21 @@ class DimensionMismatchError(DrkError):
     status = 6
 
 
+class IoError(DrkError):
+    status = 11
+
+
+class CorruptFileError(DrkError):
+    status = 12
+
+
+class VersionMismatchError(DrkError):
+    status = 13
+
+
 _ERRORS = {e.status: e for e in (NonFiniteError, DegenerateQuaternionError, DegenerateBasisError,
-                                 ReplayMismatchError, DimensionMismatchError)}
+                                 ReplayMismatchError, DimensionMismatchError, IoError, CorruptFileError,
+                                 VersionMismatchError)}
 
 
 class Camera_(C.Structure):
@@ -73,6 +86,11 @@ class Stats_(C.Structure):
         [("stage_ms", C.c_double * 8), ("bwd_warp_steps", C.c_int64), ("bwd_lead_records", C.c_int64),
          ("reject_radius", C.c_int64), ("reject_bracket", C.c_int64), ("fp64_evals", C.c_int64),
          ("ambiguous", C.c_int64), ("ring_miss", C.c_int64)]
+
+
+class SceneHeader_(C.Structure):
+    _fields_ = [("version", C.c_int32), ("basis_count", C.c_int32), ("sh_degree", C.c_int32),
+                ("scalar_count", C.c_int32), ("count", C.c_int64)]
 
 
 class AdamConfig_(C.Structure):
@@ -114,6 +132,9 @@ SIGNATURES = {
     "drk_backward": (C.c_int, [_P, _P, C.POINTER(FrameGrad_), _P, _P, _P, _P, C.c_int, C.c_int]),
     "drk_get_prim_grads": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int)]),
     "drk_l1_loss": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, _P]),
+    "drk_scene_read_header": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(SceneHeader_)]),
+    "drk_scene_load": (C.c_int, [_P, C.c_char_p, C.c_int, _P, C.c_int64, C.POINTER(SceneHeader_)]),
+    "drk_scene_save": (C.c_int, [_P, C.c_char_p, _P, C.c_int, C.c_int, C.c_int]),
     "drk_debug_alpha_bound": (C.c_int, [_P, C.c_int64, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "drk_adam_step": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                 C.POINTER(AdamConfig_)]),

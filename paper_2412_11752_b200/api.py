@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -18,7 +19,8 @@ import torch
 
 from . import _lib
 from ._lib import (DegenerateBasisError, DegenerateQuaternionError, DimensionMismatchError,  # noqa: F401
-                   DrkError, NonFiniteError, ReplayMismatchError)
+                   CorruptFileError, DrkError, IoError, NonFiniteError, ReplayMismatchError,
+                   VersionMismatchError)
 from .scenes import Camera, scalar_count, sh_terms  # noqa: F401
 
 
@@ -415,6 +417,29 @@ class Rasterizer:
         self._check(_lib.lib().drk_l1_loss(self._h, _ptr(r), _ptr(t), W, H, _ptr(value), _ptr(d)))
         return value, d
 
+    # --- scene files (DRKSCENE v1) -------------------------------------------
+    def load_scene(self, path: str, expected_basis_count: int = -1) -> "DeviceScene":
+        """drk::load_scene (reference io.cpp:58-97) straight to a device tensor in the
+        C-ABI raw layout f32 [scalar_count, n]; raises IoError / CorruptFileError /
+        VersionMismatchError like the reference."""
+        h = read_scene_header(path, expected_basis_count)
+        params = torch.empty(h.scalar_count, h.count, device=self.device, dtype=torch.float32)
+        out = _lib.SceneHeader_()
+        self._sync_stream()
+        self._check(_lib.lib().drk_scene_load(self._h, os.fsencode(path), int(expected_basis_count), _ptr(params),
+                                              h.count, C.byref(out)))
+        return DeviceScene(out.basis_count, out.sh_degree, params)
+
+    def save_scene(self, scene: "DeviceScene", path: str):
+        """drk::save_scene (reference io.cpp:40-56) from device raw parameters."""
+        raw = self._raw(scene.params)
+        S, n = raw.shape
+        if S != scalar_count(scene.basis_count, sh_terms(scene.sh_degree)):
+            raise DimensionMismatchError("primitive layout differs from the scene header")
+        self._sync_stream()
+        self._check(_lib.lib().drk_scene_save(self._h, os.fsencode(path), _ptr(raw), n, scene.basis_count,
+                                              scene.sh_degree))
+
     def adam_step(self, params: torch.Tensor, grads: torch.Tensor, state: OptState, cfg: TrainConfig,
                   scene_extent: float, k: int = 8, grad_scale: float = 1.0):
         """drk::adam_step (reference optimize.cpp:259-307), in place on device tensors."""
@@ -430,6 +455,30 @@ class Rasterizer:
         self._check(_lib.lib().drk_adam_step(self._h, _ptr(params), _ptr(grads), _ptr(state.m), _ptr(state.v), n, k,
                                              terms, C.byref(step), C.byref(a)))
         state.step = step.value
+
+
+@dataclass
+class DeviceScene:
+    """drk::Scene (reference io.hpp:14-18) with the records on the device, C-ABI raw layout."""
+
+    basis_count: int
+    sh_degree: int
+    params: torch.Tensor  # f32 [scalar_count(K, terms), n]
+
+
+def read_scene_header(path: str, expected_basis_count: int = -1) -> _lib.SceneHeader_:
+    """Header checks of drk::load_scene (io.cpp:58-80) through the C-ABI; no device work."""
+    h = _lib.SceneHeader_()
+    _lib.check(_lib.lib().drk_scene_read_header(os.fsencode(path), int(expected_basis_count), C.byref(h)))
+    return h
+
+
+def load_scene(path: str, expected_basis_count: int = -1) -> DeviceScene:
+    return default_rasterizer().load_scene(path, expected_basis_count)
+
+
+def save_scene(scene: DeviceScene, path: str):
+    default_rasterizer().save_scene(scene, path)
 
 
 _default: dict[int, Rasterizer] = {}

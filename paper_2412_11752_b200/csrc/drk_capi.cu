@@ -726,6 +726,9 @@ const char* drk_status_string(int s) {
     case DRK_ERR_CUDA: return "CUDA error";
     case DRK_ERR_OOM: return "out of device memory";
     case DRK_ERR_UNSUPPORTED: return "unsupported";
+    case DRK_ERR_IO: return "i/o error";
+    case DRK_ERR_CORRUPT_FILE: return "corrupt file";
+    case DRK_ERR_VERSION: return "version mismatch";
   }
   return "unknown status";
 }
@@ -808,7 +811,7 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->sk,
                     &c->hist, &c->sortoff, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
-                    &c->counters, &c->scan_tmp, &c->loss_tmp, &c->progress, &c->patch};
+                    &c->counters, &c->scan_tmp, &c->loss_tmp, &c->progress, &c->patch, &c->scene_aos};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : c->ev)
     if (e) cudaEventDestroy(e);
