@@ -224,6 +224,19 @@ int drk_get_prim_grads(drk_ctx* ctx, const float** grads, int* stride);
 int drk_l1_loss(drk_ctx* ctx, const float* rendered, const float* target, int width, int height,
                 double* loss_out, float* d_color);
 
+/* drk::loss (optimize.cpp:171-204), channels-interleaved f32 images
+ * (H x W x channels, device): value = (1-w) mean|r-t| + w (1 - mean SSIM),
+ * w = dssim_weight when > 0 and both sides >= 11 (else 0).  out3 (device,
+ * 3 doubles) = {value, L1, mean SSIM}; d_color (device, may be NULL) = dvalue/dr.
+ * SSIM: 11-tap Gaussian (sigma 1.5), valid region, C1 = 1e-4, C2 = 9e-4. */
+int drk_loss(drk_ctx* ctx, const float* rendered, const float* target, int width, int height, int channels,
+             double dssim_weight, double* out3, float* d_color);
+/* drk::ssim (optimize.cpp:157-166): out1 (device) = mean over channels of the
+ * valid-region SSIM; DRK_ERR_DIMENSION if a side is < 11. */
+int drk_ssim(drk_ctx* ctx, const float* a, const float* b, int width, int height, int channels, double* out1);
+/* drk::psnr (optimize.cpp:145-155): out2 (device) = {psnr (100 if mse < 1e-10), mse}. */
+int drk_psnr(drk_ctx* ctx, const float* a, const float* b, int width, int height, int channels, double* out2);
+
 /* drk::TrainConfig learning-rate fields used by adam_step. */
 typedef struct drk_adam_config {
   double lr_drk, lr_position, lr_rotation, lr_opacity, lr_sh;

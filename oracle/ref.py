@@ -200,6 +200,35 @@ def loss_l1(rendered, target):
     return v.value, d
 
 
+def loss(rendered, target, dssim_weight):
+    """Full drk::loss (optimize.cpp:171-204) -> (value, d_color f64 like rendered)."""
+    H, W, Cc = rendered.shape
+    d = np.zeros((H, W, Cc))
+    v = C.c_double(0)
+    _check(lib().ref_loss(_p(np.ascontiguousarray(rendered, dtype=np.float64)),
+                          _p(np.ascontiguousarray(target, dtype=np.float64)), W, H, Cc,
+                          C.c_double(dssim_weight), C.byref(v), _p(d)))
+    return v.value, d
+
+
+def ssim(a, b):
+    """drk::ssim (optimize.cpp:157-166)."""
+    H, W, Cc = a.shape
+    v = C.c_double(0)
+    _check(lib().ref_ssim(_p(np.ascontiguousarray(a, dtype=np.float64)), _p(np.ascontiguousarray(b, dtype=np.float64)),
+                          W, H, Cc, C.byref(v)))
+    return v.value
+
+
+def psnr(a, b):
+    """drk::psnr (optimize.cpp:145-155)."""
+    H, W, Cc = a.shape
+    v = C.c_double(0)
+    _check(lib().ref_psnr(_p(np.ascontiguousarray(a, dtype=np.float64)), _p(np.ascontiguousarray(b, dtype=np.float64)),
+                          W, H, Cc, C.byref(v)))
+    return v.value
+
+
 def adam_step(params, grads, m, v, k, terms, step, lrs, steps_total, extent,
               freeze_eta_tau=False, freeze_angles=False):
     """In-place reference adam_step on float64 SoA arrays; returns the new step."""

@@ -337,6 +337,40 @@ int ref_loss_l1(const double* rendered, const double* target, int w, int h, doub
   }
 }
 
+// Full drk::loss (optimize.cpp:171-204) on interleaved H x W x c images.
+int ref_loss(const double* rendered, const double* target, int w, int h, int c, double dssim_weight,
+             double* value, double* d_color) {
+  try {
+    const drk::LossResult lr = drk::loss(image_from(rendered, w, h, c), image_from(target, w, h, c), dssim_weight);
+    *value = lr.value;
+    copy_image(lr.d_color, d_color);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
+// drk::ssim (optimize.cpp:157-166) and drk::psnr (:145-155).
+int ref_ssim(const double* a, const double* b, int w, int h, int c, double* out) {
+  try {
+    *out = drk::ssim(image_from(a, w, h, c), image_from(b, w, h, c));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+int ref_psnr(const double* a, const double* b, int w, int h, int c, double* out) {
+  try {
+    *out = drk::psnr(image_from(a, w, h, c), image_from(b, w, h, c));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
 // drk::adam_step (optimize.cpp:248-307) on SoA raws; m/v are SoA moment
 // buffers updated in place; *step is OptState::step (incremented).
 // lrs: lr_drk, lr_position, lr_rotation, lr_opacity, lr_sh; steps_total.

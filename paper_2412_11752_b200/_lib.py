@@ -132,6 +132,9 @@ SIGNATURES = {
     "drk_backward": (C.c_int, [_P, _P, C.POINTER(FrameGrad_), _P, _P, _P, _P, C.c_int, C.c_int]),
     "drk_get_prim_grads": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int)]),
     "drk_l1_loss": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, _P]),
+    "drk_loss": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_double, _P, _P]),
+    "drk_ssim": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
+    "drk_psnr": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
     "drk_scene_read_header": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(SceneHeader_)]),
     "drk_scene_load": (C.c_int, [_P, C.c_char_p, C.c_int, _P, C.c_int64, C.POINTER(SceneHeader_)]),
     "drk_scene_save": (C.c_int, [_P, C.c_char_p, _P, C.c_int, C.c_int, C.c_int]),

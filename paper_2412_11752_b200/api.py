@@ -417,6 +417,41 @@ class Rasterizer:
         self._check(_lib.lib().drk_l1_loss(self._h, _ptr(r), _ptr(t), W, H, _ptr(value), _ptr(d)))
         return value, d
 
+    def loss(self, rendered: torch.Tensor, target: torch.Tensor, dssim_weight: float = 0.2):
+        """drk::loss (reference optimize.cpp:171-204): (1 - w) L1 + w (1 - mean SSIM) on
+        H x W x C images; returns (device f64 [value, l1, mean_ssim], d_color)."""
+        if rendered.shape != target.shape:
+            raise DimensionMismatchError("image dimensions differ")
+        H, W = rendered.shape[:2]
+        Cc = rendered.shape[2] if rendered.dim() == 3 else 1
+        r = rendered.to(self.device, torch.float32).contiguous()
+        t = target.to(self.device, torch.float32).contiguous()
+        out = torch.empty(3, device=self.device, dtype=torch.float64)
+        d = torch.empty_like(r)
+        self._sync_stream()
+        self._check(_lib.lib().drk_loss(self._h, _ptr(r), _ptr(t), W, H, Cc, float(dssim_weight), _ptr(out), _ptr(d)))
+        return out, d
+
+    def ssim(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+        """drk::ssim (reference optimize.cpp:157-166): device f64 scalar tensor."""
+        return self._metric(a, b, "drk_ssim", 1)[0]
+
+    def psnr(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+        """drk::psnr (reference optimize.cpp:145-155): device f64 scalar tensor."""
+        return self._metric(a, b, "drk_psnr", 2)[0]
+
+    def _metric(self, a, b, fn, n_out):
+        if a.shape != b.shape:
+            raise DimensionMismatchError("image dimensions differ")
+        H, W = a.shape[:2]
+        Cc = a.shape[2] if a.dim() == 3 else 1
+        a = a.to(self.device, torch.float32).contiguous()
+        b = b.to(self.device, torch.float32).contiguous()
+        out = torch.empty(n_out, device=self.device, dtype=torch.float64)
+        self._sync_stream()
+        self._check(getattr(_lib.lib(), fn)(self._h, _ptr(a), _ptr(b), W, H, Cc, _ptr(out)))
+        return out
+
     # --- scene files (DRKSCENE v1) -------------------------------------------
     def load_scene(self, path: str, expected_basis_count: int = -1) -> "DeviceScene":
         """drk::load_scene (reference io.cpp:58-97) straight to a device tensor in the
