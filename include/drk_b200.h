@@ -236,6 +236,9 @@ int drk_loss(drk_ctx* ctx, const float* rendered, const float* target, int width
 int drk_ssim(drk_ctx* ctx, const float* a, const float* b, int width, int height, int channels, double* out1);
 /* drk::psnr (optimize.cpp:145-155): out2 (device) = {psnr (100 if mse < 1e-10), mse}. */
 int drk_psnr(drk_ctx* ctx, const float* a, const float* b, int width, int height, int channels, double* out2);
+/* psnr(quantize_8bit(a), b) (image.cpp:7-14; train's evaluation, optimize.cpp:432,460). */
+int drk_psnr_quantized(drk_ctx* ctx, const float* a, const float* b, int width, int height, int channels,
+                       double* out2);
 
 /* drk::TrainConfig learning-rate fields used by adam_step. */
 typedef struct drk_adam_config {
@@ -250,6 +253,32 @@ typedef struct drk_adam_config {
  * OptState::step (host value, incremented). */
 int drk_adam_step(drk_ctx* ctx, float* params, const float* grads, float* m, float* v, int n,
                   int k, int sh_terms, int64_t* step, const drk_adam_config* cfg);
+
+/* --- density control (reference optimize.cpp:309-383) ----------------------- */
+/* TrainConfig fields used by densify_and_prune (optimize.hpp:30-61). */
+typedef struct drk_densify_config {
+  double densify_grad_threshold;  /* default 5e-4 */
+  double prune_opacity_threshold; /* default 5e-2 */
+  double percent_dense;           /* default 0.01 */
+} drk_densify_config;
+/* DensifyStats::accumulate (optimize.cpp:309-318): for touched primitives,
+ * accum[i] += screen_grad[i], count[i] += 1 (device buffers; screen_grad and
+ * touched as written by drk_backward). */
+int drk_densify_accumulate(drk_ctx* ctx, const float* screen_grad, const uint8_t* touched, int n, double* accum,
+                           int32_t* count);
+/* densify_and_prune (optimize.cpp:320-373) on raw parameters and Adam moments
+ * f32 [S][n] (device): prune sigmoid(opacity_raw) < prune threshold; primitives
+ * whose mean screen gradient exceeds the threshold are cloned (largest scale
+ * <= percent_dense * extent; the copy gets zero moments) or split in two
+ * (scales / 2, centres +- 0.25 s_max along the longest basis, zero moments).
+ * Output f32 [S][cap] in source order; *n_out = new count (raw_out may be NULL
+ * to query it). */
+int drk_densify_and_prune(drk_ctx* ctx, const float* raw, const float* m, const float* v, int n, int k, int sh_terms,
+                          const double* accum, const int32_t* count, const drk_densify_config* cfg, double extent,
+                          float* raw_out, float* m_out, float* v_out, int64_t cap, int64_t* n_out);
+/* scene_extent (optimize.cpp:375-383): out (device) = max(1e-6, |hi - lo| / 2)
+ * of the raw centres. */
+int drk_scene_extent(drk_ctx* ctx, const float* raw, int n, double* out);
 
 /* --- scene files (DRKSCENE v1, reference io.hpp:20-25, io.cpp:40-97) ------ */
 typedef struct drk_scene_header {

@@ -229,6 +229,46 @@ def psnr(a, b):
     return v.value
 
 
+def densify_and_prune(raw, m, v, k, terms, accum, count, thr, extent):
+    """drk::densify_and_prune (optimize.cpp:320-373) on f64 SoA -> (raw, m, v) of the new set."""
+    S, n = raw.shape
+    cap = 2 * n + 1
+    outs = [np.zeros((S, cap)) for _ in range(3)]
+    n_out = C.c_longlong(0)
+    _check(lib().ref_densify_and_prune(
+        _p(np.ascontiguousarray(raw, dtype=np.float64)), _p(np.ascontiguousarray(m, dtype=np.float64)),
+        _p(np.ascontiguousarray(v, dtype=np.float64)), n, k, terms, _p(np.ascontiguousarray(accum, dtype=np.float64)),
+        _p(np.ascontiguousarray(count, dtype=np.int32)), _p(np.asarray(thr, dtype=np.float64)), C.c_double(extent),
+        *[_p(o) for o in outs], C.c_longlong(cap), C.byref(n_out)))
+    return tuple(np.ascontiguousarray(o[:, :n_out.value]) for o in outs)
+
+
+def scene_extent(raw, k, terms):
+    """drk::scene_extent (optimize.cpp:375-383)."""
+    lib().ref_scene_extent.restype = C.c_double
+    return lib().ref_scene_extent(_p(np.ascontiguousarray(raw, dtype=np.float64)), raw.shape[1], k, terms)
+
+
+def train(raw, k, terms, cams, images, icfg, dcfg):
+    """drk::train (optimize.cpp:390-470): icfg = (steps, densify_interval, densify_start,
+    densify_stop, sh_warmup, max_sh, eval_interval, seed); dcfg = (lr_drk, lr_position,
+    lr_rotation, lr_opacity, lr_sh, densify_grad, prune_opacity, dssim_weight, percent_dense).
+    Returns (log [steps, 3] = loss, psnr, count; final_psnr; params f64 [S, n'])."""
+    S, n = raw.shape
+    steps = int(icfg[0])
+    cams_arr = (RefCamera * len(cams))(*[_cam(c) for c in cams])
+    imgs = np.concatenate([np.ascontiguousarray(im, dtype=np.float64).ravel() for im in images])
+    log = np.zeros((max(steps, 1), 3))
+    fin = C.c_double(0)
+    cap = n * (2 ** 8) + 16
+    out = np.zeros((S, cap))
+    n_out = C.c_longlong(0)
+    _check(lib().ref_train(_p(np.ascontiguousarray(raw, dtype=np.float64)), n, k, terms, len(cams), cams_arr,
+                           _p(imgs), _p(np.asarray(icfg, dtype=np.int32)), _p(np.asarray(dcfg, dtype=np.float64)),
+                           _p(log), C.byref(fin), _p(out), C.c_longlong(cap), C.byref(n_out)))
+    return log[:steps], fin.value, np.ascontiguousarray(out[:, :n_out.value])
+
+
 def adam_step(params, grads, m, v, k, terms, step, lrs, steps_total, extent,
               freeze_eta_tau=False, freeze_angles=False):
     """In-place reference adam_step on float64 SoA arrays; returns the new step."""

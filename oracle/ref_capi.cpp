@@ -371,6 +371,111 @@ int ref_psnr(const double* a, const double* b, int w, int h, int c, double* out)
   }
 }
 
+// densify_and_prune (optimize.cpp:320-373) on SoA raws / moments; outputs
+// (capacity cap, SoA with row stride cap) and *n_out.  thr = {densify_grad,
+// prune_opacity, percent_dense}.
+int ref_densify_and_prune(const double* raw, const double* m, const double* v, int n, int k, int terms,
+                          const double* accum, const int* count, const double* thr, double extent, double* raw_out,
+                          double* m_out, double* v_out, long long cap, long long* n_out) {
+  try {
+    std::vector<drk::RawDrkParams> params = to_raws(raw, n, k, terms);
+    drk::OptState st;
+    st.m = to_raws(m, n, k, terms);
+    st.v = to_raws(v, n, k, terms);
+    drk::DensifyStats stats;
+    stats.resize(n);
+    for (int i = 0; i < n; ++i) {
+      stats.screen_grad_accum[i] = accum[i];
+      stats.touch_count[i] = count[i];
+    }
+    drk::TrainConfig cfg;
+    cfg.densify_grad_threshold = thr[0];
+    cfg.prune_opacity_threshold = thr[1];
+    cfg.percent_dense = thr[2];
+    drk::densify_and_prune(params, st, stats, cfg, extent);
+    *n_out = (long long)params.size();
+    if ((long long)params.size() > cap) return 0;
+    const int no = (int)params.size();
+    std::vector<double> tmp((size_t)drk::scalar_count(k, terms) * no);
+    auto put = [&](const std::vector<drk::RawDrkParams>& src, double* dst) {
+      from_raws(src, tmp.data());
+      for (int sc = 0; sc < drk::scalar_count(k, terms); ++sc)
+        for (int i = 0; i < no; ++i) dst[(size_t)sc * cap + i] = tmp[(size_t)sc * no + i];
+    };
+    put(params, raw_out);
+    put(st.m, m_out);
+    put(st.v, v_out);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
+double ref_scene_extent(const double* raw, int n, int k, int terms) {
+  return drk::scene_extent(to_raws(raw, n, k, terms));
+}
+
+// drk::train (optimize.cpp:390-470) over nv views (images H x W x 3 doubles,
+// one camera each) from SoA raws.  icfg = {steps, densify_interval,
+// densify_start, densify_stop, sh_warmup, max_sh, eval_interval, seed};
+// dcfg = {lr_drk, lr_position, lr_rotation, lr_opacity, lr_sh, densify_grad,
+// prune_opacity, dssim_weight, percent_dense}.  Outputs: log rows
+// (loss, psnr, count) per step, final psnr, final params (cap primitives).
+int ref_train(const double* raw, int n, int k, int terms, int nv, const ref_camera* cams, const double* images,
+              const int* icfg, const double* dcfg, double* log_out, double* final_psnr, double* raw_out,
+              long long cap, long long* n_out) {
+  try {
+    std::vector<drk::TrainView> views(nv);
+    size_t off = 0;
+    for (int v = 0; v < nv; ++v) {
+      views[v].camera = to_cam(&cams[v]);
+      const int w = cams[v].width, h = cams[v].height;
+      views[v].image = drk::Image(w, h, 3);
+      std::memcpy(views[v].image.data.data(), images + off, sizeof(double) * 3 * w * h);
+      off += (size_t)3 * w * h;
+    }
+    drk::TrainConfig cfg;
+    cfg.steps = icfg[0];
+    cfg.densify_interval = icfg[1];
+    cfg.densify_start_step = icfg[2];
+    cfg.densify_stop_step = icfg[3];
+    cfg.sh_degree_warmup_interval = icfg[4];
+    cfg.max_sh_degree = icfg[5];
+    cfg.eval_interval = icfg[6];
+    cfg.seed = (unsigned)icfg[7];
+    cfg.lr_drk = dcfg[0];
+    cfg.lr_position = dcfg[1];
+    cfg.lr_rotation = dcfg[2];
+    cfg.lr_opacity = dcfg[3];
+    cfg.lr_sh = dcfg[4];
+    cfg.densify_grad_threshold = dcfg[5];
+    cfg.prune_opacity_threshold = dcfg[6];
+    cfg.dssim_weight = dcfg[7];
+    cfg.percent_dense = dcfg[8];
+    cfg.kernel.basis_count = k;
+    const drk::TrainResult r = drk::train(views, to_raws(raw, n, k, terms), cfg);
+    for (size_t i = 0; i < r.log.size(); ++i) {
+      log_out[3 * i] = r.log[i].loss;
+      log_out[3 * i + 1] = r.log[i].psnr;
+      log_out[3 * i + 2] = (double)r.log[i].count;
+    }
+    *final_psnr = r.final_psnr;
+    *n_out = (long long)r.params.size();
+    if ((long long)r.params.size() <= cap) {
+      const int no = (int)r.params.size();
+      std::vector<double> tmp((size_t)drk::scalar_count(k, terms) * no);
+      from_raws(r.params, tmp.data());
+      for (int sc = 0; sc < drk::scalar_count(k, terms); ++sc)
+        for (int i = 0; i < no; ++i) raw_out[(size_t)sc * cap + i] = tmp[(size_t)sc * no + i];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
 // drk::adam_step (optimize.cpp:248-307) on SoA raws; m/v are SoA moment
 // buffers updated in place; *step is OptState::step (incremented).
 // lrs: lr_drk, lr_position, lr_rotation, lr_opacity, lr_sh; steps_total.

@@ -88,6 +88,11 @@ class Stats_(C.Structure):
          ("ambiguous", C.c_int64), ("ring_miss", C.c_int64)]
 
 
+class DensifyConfig_(C.Structure):
+    _fields_ = [("densify_grad_threshold", C.c_double), ("prune_opacity_threshold", C.c_double),
+                ("percent_dense", C.c_double)]
+
+
 class SceneHeader_(C.Structure):
     _fields_ = [("version", C.c_int32), ("basis_count", C.c_int32), ("sh_degree", C.c_int32),
                 ("scalar_count", C.c_int32), ("count", C.c_int64)]
@@ -132,9 +137,14 @@ SIGNATURES = {
     "drk_backward": (C.c_int, [_P, _P, C.POINTER(FrameGrad_), _P, _P, _P, _P, C.c_int, C.c_int]),
     "drk_get_prim_grads": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int)]),
     "drk_l1_loss": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, _P]),
+    "drk_densify_accumulate": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
+    "drk_densify_and_prune": (C.c_int, [_P, _P, _P, _P, C.c_int, C.c_int, C.c_int, _P, _P, C.POINTER(DensifyConfig_),
+                                        C.c_double, _P, _P, _P, C.c_int64, C.POINTER(C.c_int64)]),
+    "drk_scene_extent": (C.c_int, [_P, _P, C.c_int, _P]),
     "drk_loss": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_double, _P, _P]),
     "drk_ssim": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
     "drk_psnr": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
+    "drk_psnr_quantized": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
     "drk_scene_read_header": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(SceneHeader_)]),
     "drk_scene_load": (C.c_int, [_P, C.c_char_p, C.c_int, _P, C.c_int64, C.POINTER(SceneHeader_)]),
     "drk_scene_save": (C.c_int, [_P, C.c_char_p, _P, C.c_int, C.c_int, C.c_int]),

@@ -127,7 +127,7 @@ class ParamGrads:
 
 @dataclass
 class TrainConfig:
-    """Learning-rate fields of reference optimize.hpp:30-61 used by adam_step."""
+    """drk::TrainConfig (reference optimize.hpp:30-61), same fields and defaults."""
 
     steps: int = 35000
     lr_drk: float = 5e-3
@@ -135,8 +135,24 @@ class TrainConfig:
     lr_rotation: float = 1e-3
     lr_opacity: float = 5e-2
     lr_sh: float = 2.5e-3
+    densify_grad_threshold: float = 5e-4
+    prune_opacity_threshold: float = 5e-2
+    densify_interval: int = 100
+    densify_start_step: int = 500
+    densify_stop_step: int = 15000
+    dssim_weight: float = 0.2
+    sh_degree_warmup_interval: int = 1000
+    max_sh_degree: int = 3
+    percent_dense: float = 0.01
     freeze_eta_tau: bool = False
     freeze_angles: bool = False
+    seed: int = 0
+    threads: int = 1
+    background: tuple = (1.0, 1.0, 1.0)
+    kernel: "KernelConfig" = None
+    eval_interval: int = 250
+    checkpoint_interval: int = 0
+    checkpoint_path: str = ""
 
 
 @dataclass
@@ -452,6 +468,43 @@ class Rasterizer:
         self._check(getattr(_lib.lib(), fn)(self._h, _ptr(a), _ptr(b), W, H, Cc, _ptr(out)))
         return out
 
+    def psnr_quantized(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+        """psnr(quantize_8bit(a), b) (reference image.cpp:7-14, optimize.cpp:432)."""
+        return self._metric(a, b, "drk_psnr_quantized", 2)[0]
+
+    # --- density control (reference optimize.cpp:309-383) ----------------------
+    def scene_extent(self, params: torch.Tensor) -> float:
+        out = torch.empty(1, device=self.device, dtype=torch.float64)
+        self._sync_stream()
+        self._check(_lib.lib().drk_scene_extent(self._h, _ptr(params), params.shape[1], _ptr(out)))
+        return float(out)
+
+    def densify_accumulate(self, grads: "ParamGrads", stats: "DensifyStats"):
+        """DensifyStats::accumulate (optimize.cpp:309-318) on the device."""
+        n = grads.screen_grad.numel()
+        if stats.screen_grad_accum.numel() != n:
+            raise DimensionMismatchError("densify stats out of sync with the primitive set")
+        self._sync_stream()
+        self._check(_lib.lib().drk_densify_accumulate(self._h, _ptr(grads.screen_grad), _ptr(grads.touched), n,
+                                                      _ptr(stats.screen_grad_accum), _ptr(stats.touch_count)))
+
+    def densify_and_prune(self, params: torch.Tensor, state: "OptState", stats: "DensifyStats", cfg: TrainConfig,
+                          extent: float, k: int = 8):
+        """densify_and_prune (optimize.cpp:320-373): returns the new params; state's moments follow."""
+        S, n = params.shape
+        terms = (S - (3 + 4 + 2 * k + 3)) // 3
+        dc = _lib.DensifyConfig_(cfg.densify_grad_threshold, cfg.prune_opacity_threshold, cfg.percent_dense)
+        cap = 2 * n
+        outs = [torch.empty(S, max(cap, 1), device=self.device, dtype=torch.float32) for _ in range(3)]
+        n_out = C.c_int64(0)
+        self._sync_stream()
+        self._check(_lib.lib().drk_densify_and_prune(
+            self._h, _ptr(params), _ptr(state.m), _ptr(state.v), n, k, terms, _ptr(stats.screen_grad_accum),
+            _ptr(stats.touch_count), C.byref(dc), float(extent), *[_ptr(o) for o in outs], cap, C.byref(n_out)))
+        m = n_out.value
+        p, state.m, state.v = (o[:, :m].contiguous() for o in outs)
+        return p
+
     # --- scene files (DRKSCENE v1) -------------------------------------------
     def load_scene(self, path: str, expected_basis_count: int = -1) -> "DeviceScene":
         """drk::load_scene (reference io.cpp:58-97) straight to a device tensor in the
@@ -490,6 +543,19 @@ class Rasterizer:
         self._check(_lib.lib().drk_adam_step(self._h, _ptr(params), _ptr(grads), _ptr(state.m), _ptr(state.v), n, k,
                                              terms, C.byref(step), C.byref(a)))
         state.step = step.value
+
+
+@dataclass
+class DensifyStats:
+    """drk::DensifyStats (reference optimize.hpp:78-88) on the device."""
+
+    screen_grad_accum: torch.Tensor  # f64 [n]
+    touch_count: torch.Tensor        # i32 [n]
+
+    @staticmethod
+    def zeros(n: int, device) -> "DensifyStats":
+        return DensifyStats(torch.zeros(n, device=device, dtype=torch.float64),
+                            torch.zeros(n, device=device, dtype=torch.int32))
 
 
 @dataclass

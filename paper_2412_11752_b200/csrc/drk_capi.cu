@@ -812,7 +812,7 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->hist, &c->sortoff, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
                     &c->counters, &c->scan_tmp, &c->loss_tmp, &c->progress, &c->patch, &c->scene_aos,
-                    &c->loss_part, &c->ssim_f};
+                    &c->loss_part, &c->ssim_f, &c->dens_code, &c->dens_pos};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : c->ev)
     if (e) cudaEventDestroy(e);

@@ -118,7 +118,8 @@ struct drk_ctx {
   drk::DevBuf gact, touched;
   drk::DevBuf counters, scan_tmp, loss_tmp;
   drk::DevBuf scene_aos;
-  drk::DevBuf loss_part, ssim_f;  // drk_loss / drk_ssim / drk_psnr: partial sums, SSIM adjoint fields  // record-major staging of scene files (drk_scene_load / drk_scene_save)
+  drk::DevBuf loss_part, ssim_f;
+  drk::DevBuf dens_code, dens_pos;  // drk_densify_and_prune: per-primitive decision / output count, scanned positions  // drk_loss / drk_ssim / drk_psnr: partial sums, SSIM adjoint fields  // record-major staging of scene files (drk_scene_load / drk_scene_save)
   int64_t hull_cap = 0;
   drk::DevBuf rowest;
   std::vector<int> bands;         // tile-row band boundaries of the last forward

@@ -229,13 +229,17 @@ __global__ void __launch_bounds__(kThreads) k_loss_l1(long long n, const float* 
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// sum of squared differences (psnr, optimize.cpp:147-151)
+// sum of squared differences (psnr, optimize.cpp:147-151); QUANT: the first
+// image through quantize_8bit first (image.cpp:7-14, train's eval metric)
+template <bool QUANT>
 __global__ void __launch_bounds__(kThreads) k_sq_diff(long long n, const float* __restrict__ a,
                                                       const float* __restrict__ b, double* part) {
   __shared__ double red[kThreads / 32];
   double acc = 0;
   for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kThreads) {
-    const double d = (double)a[i] - (double)b[i];
+    double av = (double)a[i];
+    if (QUANT) av = round(dmin(1.0, dmax(0.0, av)) * 255.0) / 255.0;
+    const double d = av - (double)b[i];
     acc += d * d;
   }
   const double s = block_sum(acc, red);
@@ -251,7 +255,7 @@ __global__ void k_loss_final(int mode, const double* l1p, int nl1, const double*
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double l1 = 0;
   for (int b = 0; b < nl1; ++b) l1 += l1p[b];
-  if (mode == 2) {
+  if (mode >= 2) {
     const double mse = l1 * inv_n_img;
     out[0] = mse < 1e-10 ? 100.0 : -10.0 * log10(mse);
     out[1] = mse;
@@ -292,7 +296,7 @@ void set_smem_attrs() {
 
 }  // namespace
 
-// mode 0: loss, 1: ssim, 2: psnr
+// mode 0: loss, 1: ssim, 2: psnr, 3: psnr of quantize_8bit(first image)
 int run_image_loss(drk_ctx* c, int mode, const float* r, const float* t, int W, int H, int C, double dssim_weight,
                    double* out, float* dcol) {
   if (W < 0 || H < 0 || C <= 0 || !r || !t || !out) return set_error(c, DRK_ERR_INVALID_ARG, "loss arguments");
@@ -319,8 +323,9 @@ int run_image_loss(drk_ctx* c, int mode, const float* r, const float* t, int W, 
   if (!l1p) return set_error(c, DRK_ERR_OOM, "loss partials");
   cudaMemsetAsync(l1p, 0, sizeof(double) * nl1, s);
   const Gauss G = ssim_gauss();
-  if (mode == 2) {
-    if (n > 0) k_sq_diff<<<nl1, kThreads, 0, s>>>(n, r, t, l1p);
+  if (mode >= 2) {
+    if (n > 0 && mode == 2) k_sq_diff<false><<<nl1, kThreads, 0, s>>>(n, r, t, l1p);
+    if (n > 0 && mode == 3) k_sq_diff<true><<<nl1, kThreads, 0, s>>>(n, r, t, l1p);
   } else if (mode == 0 && n > 0) {
     k_loss_l1<<<nl1, kThreads, 0, s>>>(n, r, t, (1.0 - w) * inv_n_img, use_ssim ? nullptr : dcol, l1p);
   }
@@ -360,4 +365,11 @@ extern "C" int drk_psnr(drk_ctx* c, const float* a, const float* b, int width, i
   if (!c) return DRK_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
   return run_image_loss(c, 2, a, b, width, height, channels, 0.0, out2, nullptr);
+}
+
+extern "C" int drk_psnr_quantized(drk_ctx* c, const float* a, const float* b, int width, int height, int channels,
+                                  double* out2) {
+  if (!c) return DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  return run_image_loss(c, 3, a, b, width, height, channels, 0.0, out2, nullptr);
 }
