@@ -236,6 +236,11 @@ int drk_loss(drk_ctx* ctx, const float* rendered, const float* target, int width
 int drk_ssim(drk_ctx* ctx, const float* a, const float* b, int width, int height, int channels, double* out1);
 /* drk::psnr (optimize.cpp:145-155): out2 (device) = {psnr (100 if mse < 1e-10), mse}. */
 int drk_psnr(drk_ctx* ctx, const float* a, const float* b, int width, int height, int channels, double* out2);
+/* The same three on double images (drk::Image, the drop-in adapter's types). */
+int drk_loss_f64(drk_ctx* ctx, const double* rendered, const double* target, int width, int height, int channels,
+                 double dssim_weight, double* out3, double* d_color);
+int drk_ssim_f64(drk_ctx* ctx, const double* a, const double* b, int width, int height, int channels, double* out1);
+int drk_psnr_f64(drk_ctx* ctx, const double* a, const double* b, int width, int height, int channels, double* out2);
 /* psnr(quantize_8bit(a), b) (image.cpp:7-14; train's evaluation, optimize.cpp:432,460). */
 int drk_psnr_quantized(drk_ctx* ctx, const float* a, const float* b, int width, int height, int channels,
                        double* out2);

@@ -144,6 +144,9 @@ SIGNATURES = {
     "drk_loss": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_double, _P, _P]),
     "drk_ssim": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
     "drk_psnr": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
+    "drk_loss_f64": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_double, _P, _P]),
+    "drk_ssim_f64": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
+    "drk_psnr_f64": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
     "drk_psnr_quantized": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, _P]),
     "drk_scene_read_header": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(SceneHeader_)]),
     "drk_scene_load": (C.c_int, [_P, C.c_char_p, C.c_int, _P, C.c_int64, C.POINTER(SceneHeader_)]),

@@ -6,6 +6,9 @@
 //   drk::bin_primitives   (reference raster.hpp:30-31, raster.cpp:119-265)
 //   drk::render           (reference raster.hpp:92-93, raster.cpp:440-485)
 //   drk::backward_render  (reference grad.hpp:58-61, grad.cpp:307-384)
+// and the image losses of the training step:
+//   drk::loss / drk::ssim / drk::psnr (reference optimize.hpp:6-18,
+//   optimize.cpp:145-204) on the device (double images: drk_loss_f64 ...)
 // Everything else (SortCache, eval_sorting, backward_alpha,
 // finite_diff_check, ...) stays the reference's and calls into these.
 //
@@ -25,6 +28,7 @@
 
 #include "drk/errors.hpp"
 #include "drk/grad.hpp"
+#include "drk/optimize.hpp"
 #include "drk/raster.hpp"
 #include "drk_b200.h"
 
@@ -288,6 +292,44 @@ ParamGrads backward_render(const std::vector<RawDrkParams>& raws, const std::vec
     out.touched[i] = (char)th[i];
   }
   return out;
+}
+
+// --- image losses (optimize.cpp:145-204) ------------------------------------
+namespace {
+void same_shape(const Image& a, const Image& b) {
+  if (!a.same_shape(b)) throw DimensionMismatchError("image dimensions differ");  // optimize.cpp:19-21
+}
+// the loss kernels run asynchronously on the context's stream
+void done(int st) {
+  check(st);
+  if (cudaDeviceSynchronize() != cudaSuccess) throw Error("drk_b200: CUDA error in the loss kernels");
+}
+}  // namespace
+
+double psnr(const Image& a, const Image& b) {
+  same_shape(a, b);
+  Dev<double> da(a.data), db(b.data), out(2);
+  done(drk_psnr_f64(ctx(), da.p, db.p, a.width, a.height, a.channels, out.p));
+  return out.get()[0];
+}
+
+double ssim(const Image& a, const Image& b) {
+  same_shape(a, b);
+  Dev<double> da(a.data), db(b.data), out(1);
+  done(drk_ssim_f64(ctx(), da.p, db.p, a.width, a.height, a.channels, out.p));
+  return out.get()[0];
+}
+
+LossResult loss(const Image& rendered, const Image& target, double dssim_weight) {
+  same_shape(rendered, target);
+  Dev<double> dr(rendered.data), dt(target.data), out(3), dcol(rendered.data.size());
+  done(drk_loss_f64(ctx(), dr.p, dt.p, rendered.width, rendered.height, rendered.channels, dssim_weight, out.p,
+                     dcol.p));
+  LossResult res;
+  res.value = out.get()[0];
+  res.d_color = Image(rendered.width, rendered.height, rendered.channels);
+  res.d_color.data = dcol.get();
+  return res;
 }
 
 }  // namespace drk

@@ -70,8 +70,8 @@ __device__ double block_sum(double v, double* red) {
 
 // Valid-region SSIM map of one tile, all channels.  f (GRAD): 3 planes per
 // channel, [c][k][vh][vw].  part: per-CTA sums of s, [c][nblocks].
-template <bool GRAD>
-__global__ void __launch_bounds__(kThreads) k_ssim_map(const float* __restrict__ xr, const float* __restrict__ yr,
+template <bool GRAD, typename T>
+__global__ void __launch_bounds__(kThreads) k_ssim_map(const T* __restrict__ xr, const T* __restrict__ yr,
                                                        int W, int H, int C, const Gauss G, double* f,
                                                        double* part) {
   extern __shared__ double sm[];
@@ -154,10 +154,11 @@ __global__ void __launch_bounds__(kThreads) k_ssim_map(const float* __restrict__
 
 // d_color of loss() (optimize.cpp:184-200) for one image tile, all channels:
 // L1 sign term, then + (-w / C) d_x with d_x from the adjoint taps of f1..f3.
-__global__ void __launch_bounds__(kThreads) k_ssim_grad(const float* __restrict__ xr, const float* __restrict__ yr,
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_ssim_grad(const T* __restrict__ xr, const T* __restrict__ yr,
                                                         int W, int H, int C, const Gauss G, const double* __restrict__ f,
                                                         double w, double inv_n_img, double inv_n_ssim,
-                                                        float* __restrict__ dcol) {
+                                                        T* __restrict__ dcol) {
   extern __shared__ double sm[];
   double* fs = sm;                 // [3][kIH][kIW]: f rows y0-10.., cols x0-10..
   double* hp = fs + 3 * kIH * kIW; // [3][kIH][kTW]
@@ -208,22 +209,23 @@ __global__ void __launch_bounds__(kThreads) k_ssim_grad(const float* __restrict_
       const double d = x - y;
       double g = (1.0 - w) * inv_n_img * (d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0));  // optimize.cpp:184
       g += scale * dx;                                                         // optimize.cpp:196
-      dcol[p] = (float)g;
+      dcol[p] = (T)g;
     }
   }
 }
 
 // L1 part of loss() (optimize.cpp:180-186): per-CTA sums of |r - t|; the sign
 // gradient is written when SSIM is off (otherwise k_ssim_grad writes d_color).
-__global__ void __launch_bounds__(kThreads) k_loss_l1(long long n, const float* __restrict__ r,
-                                                      const float* __restrict__ t, double gscale, float* dcol,
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_loss_l1(long long n, const T* __restrict__ r,
+                                                      const T* __restrict__ t, double gscale, T* dcol,
                                                       double* part) {
   __shared__ double red[kThreads / 32];
   double acc = 0;
   for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kThreads) {
     const double d = (double)r[i] - (double)t[i];
     acc += fabs(d);
-    if (dcol) dcol[i] = (float)(gscale * (d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0)));
+    if (dcol) dcol[i] = (T)(gscale * (d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0)));
   }
   const double s = block_sum(acc, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -231,9 +233,9 @@ __global__ void __launch_bounds__(kThreads) k_loss_l1(long long n, const float* 
 
 // sum of squared differences (psnr, optimize.cpp:147-151); QUANT: the first
 // image through quantize_8bit first (image.cpp:7-14, train's eval metric)
-template <bool QUANT>
-__global__ void __launch_bounds__(kThreads) k_sq_diff(long long n, const float* __restrict__ a,
-                                                      const float* __restrict__ b, double* part) {
+template <bool QUANT, typename T>
+__global__ void __launch_bounds__(kThreads) k_sq_diff(long long n, const T* __restrict__ a,
+                                                      const T* __restrict__ b, double* part) {
   __shared__ double red[kThreads / 32];
   double acc = 0;
   for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kThreads) {
@@ -285,27 +287,31 @@ __global__ void k_loss_final(int mode, const double* l1p, int nl1, const double*
 size_t map_smem() { return sizeof(double) * (2 * kIH * kIW + 5 * kIH * kTW); }
 size_t grad_smem() { return sizeof(double) * (3 * kIH * kIW + 3 * kIH * kTW); }
 
+template <typename T>
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
-  cudaFuncSetAttribute(k_ssim_map<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_smem());
-  cudaFuncSetAttribute(k_ssim_map<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_smem());
-  cudaFuncSetAttribute(k_ssim_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem());
+  cudaFuncSetAttribute(k_ssim_map<true, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_smem());
+  cudaFuncSetAttribute(k_ssim_map<false, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_smem());
+  cudaFuncSetAttribute(k_ssim_grad<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem());
   done = true;
 }
 
 }  // namespace
 
 // mode 0: loss, 1: ssim, 2: psnr, 3: psnr of quantize_8bit(first image)
-int run_image_loss(drk_ctx* c, int mode, const float* r, const float* t, int W, int H, int C, double dssim_weight,
-                   double* out, float* dcol) {
+// T = float (framebuffers of this library) or double (the reference's Image,
+// drop-in adapter)
+template <typename T>
+int run_image_loss(drk_ctx* c, int mode, const T* r, const T* t, int W, int H, int C, double dssim_weight,
+                   double* out, T* dcol) {
   if (W < 0 || H < 0 || C <= 0 || !r || !t || !out) return set_error(c, DRK_ERR_INVALID_ARG, "loss arguments");
   const bool window_fits = W >= kWin && H >= kWin;
   if (mode == 1 && !window_fits) return set_error(c, DRK_ERR_DIMENSION, "image smaller than the SSIM window");
   const bool use_ssim = mode == 1 || (mode == 0 && dssim_weight > 0 && window_fits);  // optimize.cpp:173-175
   const double w = (mode == 0 && use_ssim) ? dssim_weight : 0.0;
   cudaStream_t s = c->stream;
-  set_smem_attrs();
+  set_smem_attrs<T>();
   const long long n = (long long)W * H * C;
   const double inv_n_img = n > 0 ? 1.0 / (double)n : 0.0;
   const int vw = W - kHalo, vh = H - kHalo;
@@ -324,17 +330,17 @@ int run_image_loss(drk_ctx* c, int mode, const float* r, const float* t, int W, 
   cudaMemsetAsync(l1p, 0, sizeof(double) * nl1, s);
   const Gauss G = ssim_gauss();
   if (mode >= 2) {
-    if (n > 0 && mode == 2) k_sq_diff<false><<<nl1, kThreads, 0, s>>>(n, r, t, l1p);
-    if (n > 0 && mode == 3) k_sq_diff<true><<<nl1, kThreads, 0, s>>>(n, r, t, l1p);
+    if (n > 0 && mode == 2) k_sq_diff<false, T><<<nl1, kThreads, 0, s>>>(n, r, t, l1p);
+    if (n > 0 && mode == 3) k_sq_diff<true, T><<<nl1, kThreads, 0, s>>>(n, r, t, l1p);
   } else if (mode == 0 && n > 0) {
-    k_loss_l1<<<nl1, kThreads, 0, s>>>(n, r, t, (1.0 - w) * inv_n_img, use_ssim ? nullptr : dcol, l1p);
+    k_loss_l1<T><<<nl1, kThreads, 0, s>>>(n, r, t, (1.0 - w) * inv_n_img, use_ssim ? nullptr : dcol, l1p);
   }
   if (use_ssim) {
-    if (f) k_ssim_map<true><<<grid, kThreads, map_smem(), s>>>(r, t, W, H, C, G, f, sp);
-    else k_ssim_map<false><<<grid, kThreads, map_smem(), s>>>(r, t, W, H, C, G, nullptr, sp);
+    if (f) k_ssim_map<true, T><<<grid, kThreads, map_smem(), s>>>(r, t, W, H, C, G, f, sp);
+    else k_ssim_map<false, T><<<grid, kThreads, map_smem(), s>>>(r, t, W, H, C, G, nullptr, sp);
     if (f && dcol) {
       const dim3 ig((W + kTW - 1) / kTW, (H + kTH - 1) / kTH);
-      k_ssim_grad<<<ig, kThreads, grad_smem(), s>>>(r, t, W, H, C, G, f, w, inv_n_img, inv_n_ssim, dcol);
+      k_ssim_grad<T><<<ig, kThreads, grad_smem(), s>>>(r, t, W, H, C, G, f, w, inv_n_img, inv_n_ssim, dcol);
     }
   }
   k_loss_final<<<1, 32, 0, s>>>(mode, l1p, nl1, sp, nblk, C, inv_n_img, inv_n_ssim, w, use_ssim, out);
@@ -350,26 +356,48 @@ extern "C" int drk_loss(drk_ctx* c, const float* rendered, const float* target, 
                         double dssim_weight, double* out3, float* d_color) {
   if (!c) return DRK_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
-  return run_image_loss(c, 0, rendered, target, width, height, channels, dssim_weight, out3, d_color);
+  return run_image_loss<float>(c, 0, rendered, target, width, height, channels, dssim_weight, out3, d_color);
 }
 
 extern "C" int drk_ssim(drk_ctx* c, const float* a, const float* b, int width, int height, int channels,
                         double* out1) {
   if (!c) return DRK_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
-  return run_image_loss(c, 1, a, b, width, height, channels, 0.0, out1, nullptr);
+  return run_image_loss<float>(c, 1, a, b, width, height, channels, 0.0, out1, nullptr);
 }
 
 extern "C" int drk_psnr(drk_ctx* c, const float* a, const float* b, int width, int height, int channels,
                         double* out2) {
   if (!c) return DRK_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
-  return run_image_loss(c, 2, a, b, width, height, channels, 0.0, out2, nullptr);
+  return run_image_loss<float>(c, 2, a, b, width, height, channels, 0.0, out2, nullptr);
 }
 
 extern "C" int drk_psnr_quantized(drk_ctx* c, const float* a, const float* b, int width, int height, int channels,
                                   double* out2) {
   if (!c) return DRK_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
-  return run_image_loss(c, 3, a, b, width, height, channels, 0.0, out2, nullptr);
+  return run_image_loss<float>(c, 3, a, b, width, height, channels, 0.0, out2, nullptr);
+}
+
+// double-image variants (drk::Image of the reference; the drop-in adapter)
+extern "C" int drk_loss_f64(drk_ctx* c, const double* rendered, const double* target, int width, int height,
+                            int channels, double dssim_weight, double* out3, double* d_color) {
+  if (!c) return DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  return run_image_loss<double>(c, 0, rendered, target, width, height, channels, dssim_weight, out3, d_color);
+}
+
+extern "C" int drk_ssim_f64(drk_ctx* c, const double* a, const double* b, int width, int height, int channels,
+                            double* out1) {
+  if (!c) return DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  return run_image_loss<double>(c, 1, a, b, width, height, channels, 0.0, out1, nullptr);
+}
+
+extern "C" int drk_psnr_f64(drk_ctx* c, const double* a, const double* b, int width, int height, int channels,
+                            double* out2) {
+  if (!c) return DRK_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  return run_image_loss<double>(c, 2, a, b, width, height, channels, 0.0, out2, nullptr);
 }
