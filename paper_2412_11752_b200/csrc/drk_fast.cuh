@@ -9,6 +9,16 @@
 namespace drk {
 
 
+// DRK_STATS=0 compiles the per-pixel work counters out of the fast kernels
+// (development A/B; the product keeps them for the roofline's counts)
+#ifndef DRK_STATS
+#define DRK_STATS 1
+#endif
+#define DRK_STAT(x) \
+  do {              \
+    if (DRK_STATS) ++(x); \
+  } while (0)
+
 constexpr int kRing = 512;
 constexpr int kBatch = 256;
 constexpr int kRecHdr = 24;
@@ -261,7 +271,7 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
       lp_possible = dpp2 <= dz * dz * R.r4.z * (1.0001f + 4.f * rel_z) + 1e-6f;
     }
     if (r2 - dr2 > R.r3.w * 1.000001f && !lp_possible) {
-      ++px.n_rej1;
+      DRK_STAT(px.n_rej1);
       out.skip = true;
       return;
     }
@@ -295,7 +305,7 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
       const float r1l = fmaxf(r1 - dr1, 0.f);
       const float qlb = eta * r1l * r1l + (1.f - eta) * fmaxf(r2 - dr2, 0.f) * hmin;
       if (qlb > fvis2 * 1.00002f && !lp_possible) {
-        ++px.n_rej2;
+        DRK_STAT(px.n_rej2);
         out.skip = true;
         return;
       }
@@ -402,7 +412,7 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
     }
   }
   if (use64) {
-    ++px.n_f64;
+    DRK_STAT(px.n_f64);
     Pop64 o_local;
     Pop64& o = GRAD ? *o64 : o_local;
     pop_f64(P, id, x, y, o);
@@ -506,7 +516,7 @@ template <bool VALIDATE>
 __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, const float4* s_b4, const Rec* ring,
                                          const int* s_id, const TileConst& tc, long long beg, int ring_lo, int jr,
                                          int x, int y) {
-  ++px.n_pop;
+  DRK_STAT(px.n_pop);
   Rec R;
   int id;
   if (jr >= ring_lo) {
@@ -516,7 +526,7 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
   } else {
     id = P.lid[beg + jr];
     stage_record(P, id, tc, R);
-    ++px.n_miss;
+    DRK_STAT(px.n_miss);
   }
   AlphaOut o;
   alpha_entry<VALIDATE>(P, px, R, id, x, y, o);

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
           lo = __double2float_rd(rx);
           hi = __double2float_ru(rx);
         }
-        ++n_str;
+        DRK_STAT(n_str);
         // SortCache::step (raster.cpp:267-303) on exact-containing intervals
         bool le[kCacheCap];
         bool amb = false;
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(256, MINB) k_raster_fast(const __grid_constant
         }
         if (amb) {
           // overlapping intervals: compare the exact fp64 depths
-          ++n_amb;
+          DRK_STAT(n_amb);
           double rin = 0;
           exact_rt(P, s_id[slot], x, y, &rin);
           lo = __double2float_rd(rin);
