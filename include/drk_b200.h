@@ -259,6 +259,12 @@ typedef struct drk_adam_config {
 int drk_adam_step(drk_ctx* ctx, float* params, const float* grads, float* m, float* v, int n,
                   int k, int sh_terms, int64_t* step, const drk_adam_config* cfg);
 
+/* drk::eval_sorting (raster.cpp:487-560) of the last forward on this context
+ * (its camera, presort and use_cache): out4 (host) = {accuracy, kendall_tau,
+ * mae, pixels}.  Per-pixel values are the reference's exactly and are summed
+ * in its order.  DRK_ERR_UNSUPPORTED for banded frames. */
+int drk_eval_sorting(drk_ctx* ctx, double* out4);
+
 /* --- density control (reference optimize.cpp:309-383) ----------------------- */
 /* TrainConfig fields used by densify_and_prune (optimize.hpp:30-61). */
 typedef struct drk_densify_config {

@@ -128,6 +128,14 @@ def activate(scene):
     return out
 
 
+def eval_sorting(scene, cam, opt: Options = Options()):
+    """drk::eval_sorting (raster.cpp:487-560) -> (accuracy, kendall_tau, mae, pixels)."""
+    out = np.zeros(4)
+    _check(lib().ref_eval_sorting(_p(_raw(scene)), scene.n, scene.k, scene.terms, C.byref(_cam(cam)),
+                                  C.byref(_opt(opt)), _p(out)))
+    return float(out[0]), float(out[1]), float(out[2]), int(out[3])
+
+
 def bin_primitives(scene, cam, opt: Options = Options()):
     """Returns (offsets[T+1], prim_ids[P], keys[P]) of the reference TileBinning."""
     total = C.c_int64(0)

@@ -210,6 +210,28 @@ int ref_bin(const double* raw_soa, int n, int k, int terms, const ref_camera* c,
   }
 }
 
+// drk::eval_sorting (raster.cpp:487-560) over activated raws: out4 = {accuracy,
+// kendall_tau, mae, pixels}; presort / use_cache from the options.
+int ref_eval_sorting(const double* raw_soa, int n, int k, int terms, const ref_camera* c, const ref_options* o,
+                     double* out4) {
+  try {
+    const auto raws = to_raws(raw_soa, n, k, terms);
+    std::vector<drk::DrkPrimitive> prims;
+    prims.reserve(n);
+    for (const auto& r : raws) prims.push_back(drk::activate(r));
+    const drk::RenderOptions opt = to_opt(o, k);
+    const drk::SortingMetrics m = drk::eval_sorting(prims, to_cam(c), opt.kernel, opt.presort, opt.use_cache);
+    out4[0] = m.accuracy;
+    out4[1] = m.kendall_tau;
+    out4[2] = m.mae;
+    out4[3] = (double)m.pixels;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
 void ref_bins_copy(int64_t* offsets, int32_t* ids, double* keys) {
   std::memcpy(offsets, g_bins.offsets.data(), g_bins.offsets.size() * sizeof(int64_t));
   std::memcpy(ids, g_bins.ids.data(), g_bins.ids.size() * sizeof(int32_t));

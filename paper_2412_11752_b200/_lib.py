@@ -137,6 +137,7 @@ SIGNATURES = {
     "drk_backward": (C.c_int, [_P, _P, C.POINTER(FrameGrad_), _P, _P, _P, _P, C.c_int, C.c_int]),
     "drk_get_prim_grads": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int)]),
     "drk_l1_loss": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, _P]),
+    "drk_eval_sorting": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "drk_densify_accumulate": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     "drk_densify_and_prune": (C.c_int, [_P, _P, _P, _P, C.c_int, C.c_int, C.c_int, _P, _P, C.POINTER(DensifyConfig_),
                                         C.c_double, _P, _P, _P, C.c_int64, C.POINTER(C.c_int64)]),

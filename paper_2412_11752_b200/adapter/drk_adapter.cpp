@@ -6,6 +6,7 @@
 //   drk::bin_primitives   (reference raster.hpp:30-31, raster.cpp:119-265)
 //   drk::render           (reference raster.hpp:92-93, raster.cpp:440-485)
 //   drk::backward_render  (reference grad.hpp:58-61, grad.cpp:307-384)
+//   drk::eval_sorting     (reference raster.hpp:105-106, raster.cpp:487-560)
 // and the image losses of the training step:
 //   drk::loss / drk::ssim / drk::psnr (reference optimize.hpp:6-18,
 //   optimize.cpp:145-204) on the device (double images: drk_loss_f64 ...)
@@ -196,6 +197,25 @@ TileBinning bin_primitives(const std::vector<DrkPrimitive>& prims, const Camera&
   for (size_t t = 0; t < b.tiles.size(); ++t)
     for (int64_t j = off[t]; j < off[t + 1]; ++j) b.tiles[t].push_back({ids[j], keys[j]});
   return b;
+}
+
+// drk::eval_sorting (raster.hpp:105-106): GPU binning + per-pixel order metrics
+SortingMetrics eval_sorting(const std::vector<DrkPrimitive>& prims, const Camera& cam, const KernelConfig& cfg,
+                            PresortMode presort, bool use_cache) {
+  DevPrims dp(prims, cfg.basis_count);
+  RenderOptions opt;
+  opt.kernel = cfg;
+  opt.presort = presort;
+  opt.use_cache = use_cache;
+  forward(prims, cam, opt, 0, nullptr, nullptr, nullptr, nullptr, dp);
+  double out[4];
+  check(drk_eval_sorting(ctx(), out));
+  SortingMetrics m;
+  m.accuracy = out[0];
+  m.kendall_tau = out[1];
+  m.mae = out[2];
+  m.pixels = (long)out[3];
+  return m;
 }
 
 FrameBuffers render(const std::vector<DrkPrimitive>& prims, const Camera& cam, const RenderOptions& opt,

@@ -106,6 +106,16 @@ class ReplayBuffer:
 
 
 @dataclass
+class SortingMetrics:
+    """reference raster.hpp:98-103"""
+
+    accuracy: float = 0.0
+    kendall_tau: float = 0.0
+    mae: float = 0.0
+    pixels: int = 0
+
+
+@dataclass
 class FrameGrad:
     """reference grad.hpp:39-45; None = empty image."""
 
@@ -333,6 +343,17 @@ class Rasterizer:
         opt = RenderOptions(kernel=cfg, presort=presort)
         self.render(raw, cam, opt, k=k, outputs=())
         return self.tile_binning()
+
+    def eval_sorting(self, raw, cam: Camera, cfg: KernelConfig = None, presort=PresortMode.NearestDepth,
+                     use_cache: bool = True, k: int = 8) -> "SortingMetrics":
+        """drk::eval_sorting (reference raster.cpp:487-560): bins with ``presort`` and
+        measures the depth order each pixel would process (SortCache or list order)."""
+        cfg = cfg or KernelConfig(basis_count=k)
+        opt = RenderOptions(kernel=cfg, presort=presort, use_cache=use_cache, sh_degree=0)
+        self.render(raw, cam, opt, k=k)
+        out = (C.c_double * 4)()
+        self._check(_lib.lib().drk_eval_sorting(self._h, out))
+        return SortingMetrics(out[0], out[1], out[2], int(out[3]))
 
     def replay_buffer(self) -> ReplayBuffer:
         total = C.c_int64(0)

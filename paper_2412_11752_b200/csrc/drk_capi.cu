@@ -812,7 +812,8 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->hist, &c->sortoff, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
                     &c->counters, &c->scan_tmp, &c->loss_tmp, &c->progress, &c->patch, &c->scene_aos,
-                    &c->loss_part, &c->ssim_f, &c->dens_code, &c->dens_pos};
+                    &c->loss_part, &c->ssim_f, &c->dens_code, &c->dens_pos,
+                    &c->eval_scr, &c->eval_px, &c->eval_off};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -941,6 +942,56 @@ int drk_get_bands(const drk_ctx* c, int32_t* n_bands) {
   if (!c || !n_bands) return DRK_ERR_INVALID_ARG;
   *n_bands = c->bands.empty() ? 0 : (int32_t)c->bands.size() - 1;
   return DRK_OK;
+}
+
+int drk_eval_sorting(drk_ctx* c, double* out4) {
+  if (!c || !out4) return DRK_ERR_INVALID_ARG;
+  if (!c->has_fwd) return set_error(c, DRK_ERR_INVALID_ARG, "no forward on this context");
+  if (c->bands.size() > 2) return set_error(c, DRK_ERR_UNSUPPORTED, "tile lists of a banded frame are not kept");
+  cudaSetDevice(c->device);
+  cudaStream_t s = c->stream;
+  const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
+  std::vector<long long> off(n_tiles + 1);
+  cudaMemcpyAsync(off.data(), c->tileoff.p, sizeof(long long) * (n_tiles + 1), cudaMemcpyDeviceToHost, s);
+  if (int st = cuda_check(c, cudaStreamSynchronize(s), "eval_sorting offsets")) return st;
+  const size_t n_pix = (size_t)c->cam.width * c->cam.height;
+  double* tau = ensure<double>(c->eval_px, 2 * n_pix + n_pix / 8 + 8);
+  if (!tau) return set_error(c, DRK_ERR_OOM, "eval_sorting pixel buffers");
+  double* mae = tau + n_pix;
+  unsigned char* flag = reinterpret_cast<unsigned char*>(mae + n_pix);
+  cudaMemsetAsync(flag, 0, n_pix, s);
+  // tile chunks whose scratch (256 pixels x 3 L doubles per tile) fits the budget
+  const long long budget = 1LL << 27;  // doubles (1 GiB)
+  long long maxL = 0;
+  for (int t = 0; t < n_tiles; ++t) maxL = std::max(maxL, off[t + 1] - off[t]);
+  double* scr = ensure<double>(c->eval_scr, (size_t)std::max(budget, 768 * maxL));
+  long long* doff = ensure<long long>(c->eval_off, (size_t)n_tiles + 1);
+  if (!scr || !doff) return set_error(c, DRK_ERR_OOM, "eval_sorting scratch");
+  RasterParams P = raster_params(c);
+  std::vector<long long> chunk_off;
+  int t0 = 0;
+  while (t0 < n_tiles) {
+    chunk_off.clear();
+    long long used = 0;
+    int t1 = t0;
+    while (t1 < n_tiles) {
+      const long long need = 768 * (off[t1 + 1] - off[t1]);
+      if (t1 > t0 && used + need > std::max(budget, 768 * maxL)) break;
+      chunk_off.push_back(used);
+      used += need;
+      ++t1;
+    }
+    cudaMemcpyAsync(doff, chunk_off.data(), sizeof(long long) * chunk_off.size(), cudaMemcpyHostToDevice, s);
+    launch_eval_sorting(P, t0, t1, doff, scr, c->opt.use_cache, tau, mae, flag, s);
+    DRK_COUNT_LAUNCH();
+    if (int st = cuda_check(c, cudaStreamSynchronize(s), "eval_sorting")) return st;  // chunk_off reused
+    t0 = t1;
+  }
+  double* dout = reinterpret_cast<double*>(doff);
+  launch_eval_sorting_reduce(c->camd, static_cast<const long long*>(c->tileoff.p), tau, mae, flag, dout, s);
+  DRK_COUNT_LAUNCH();
+  cudaMemcpyAsync(out4, dout, sizeof(double) * 4, cudaMemcpyDeviceToHost, s);
+  return cuda_check(c, cudaStreamSynchronize(s), "eval_sorting");
 }
 
 int drk_get_tile_lists(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* ids, double* keys) {

@@ -96,6 +96,10 @@ void launch_raster_bwd_fast(const RasterParams& P, int n_tiles, cudaStream_t s);
 void launch_shape_rec(const ShapeView& S, int n, float* rec, cudaStream_t s);
 double measure_fp32_peak(cudaStream_t s);
 void launch_backward_serial(const RasterParams& P, cudaStream_t s);
+void launch_eval_sorting(const RasterParams& P, int tile0, int tile1, const long long* scr_off, double* scratch,
+                         int use_cache, double* tau, double* mae, unsigned char* flag, cudaStream_t s);
+void launch_eval_sorting_reduce(const CamD& cam, const long long* tileoff, const double* tau, const double* mae,
+                                const unsigned char* flag, double* out, cudaStream_t s);
 
 }  // namespace drk
 
@@ -119,7 +123,8 @@ struct drk_ctx {
   drk::DevBuf counters, scan_tmp, loss_tmp;
   drk::DevBuf scene_aos;
   drk::DevBuf loss_part, ssim_f;
-  drk::DevBuf dens_code, dens_pos;  // drk_densify_and_prune: per-primitive decision / output count, scanned positions  // drk_loss / drk_ssim / drk_psnr: partial sums, SSIM adjoint fields  // record-major staging of scene files (drk_scene_load / drk_scene_save)
+  drk::DevBuf dens_code, dens_pos;
+  drk::DevBuf eval_scr, eval_px, eval_off;  // drk_eval_sorting: sequence scratch, per-pixel metrics, chunk offsets  // drk_densify_and_prune: per-primitive decision / output count, scanned positions  // drk_loss / drk_ssim / drk_psnr: partial sums, SSIM adjoint fields  // record-major staging of scene files (drk_scene_load / drk_scene_save)
   int64_t hull_cap = 0;
   drk::DevBuf rowest;
   std::vector<int> bands;         // tile-row band boundaries of the last forward

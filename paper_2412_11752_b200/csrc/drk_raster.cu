@@ -1946,4 +1946,141 @@ int run_adam(drk_ctx* c, float* params, const float* grads, float* m, float* v, 
   return cuda_check(c, cudaGetLastError(), "adam");
 }
 
+// ---------------------------------------------------------------------------
+// eval_sorting (reference raster.cpp:487-560): per pixel, the depth sequence
+// the renderer would process (SortCache pops, or list order), compared with its
+// sorted order: Kendall tau, MAE, fully-ordered flag.  One thread per pixel of
+// a chunk of tiles; the sequence lives in a per-pixel scratch row of the tile's
+// list length.  Hits and depths are the reference's exact fp64 values
+// (classify_intersect op order), concordant / discordant pairs are counted by
+// a bottom-up merge sort (O(n log n); strict inequalities only, like the
+// reference's O(n^2) loop), so every per-pixel value is the reference's.
+// ---------------------------------------------------------------------------
+__global__ void k_eval_sorting(const RasterParams P, int tile0, int tile1, const long long* __restrict__ scr_off,
+                               double* scratch, int use_cache, double* tau_out, double* mae_out,
+                               unsigned char* flag_out) {
+  const int t = tile0 + blockIdx.x;
+  if (t >= tile1) return;
+  const int tx = t % P.cam.tiles_x, ty = t / P.cam.tiles_x;
+  const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+  const int x = tx * kTile + lx, y = ty * kTile + ly;
+  if (x >= P.cam.W || y >= P.cam.H) return;
+  const size_t pix = (size_t)y * P.cam.W + x;
+  flag_out[pix] = 0;
+  const long long beg = P.tileoff[t], end = P.tileoff[t + 1];
+  const long long L = end - beg;
+  if (L == 0) return;
+  double* seq = scratch + scr_off[blockIdx.x] + (long long)threadIdx.x * 3 * L;
+  double* tmp = seq + L;
+  double dir[3];
+  pixel_dir(P.cam, x + 0.5, y + 0.5, dir);
+  int n = 0;
+  double cd[kCacheCap];
+  int ci[kCacheCap];
+  int csz = 0;
+  for (long long j = beg; j < end; ++j) {
+    const int id = P.lid[j];
+    const Geo& g = P.geo[id];
+    const double denom = xdot3(dir[0], dir[1], dir[2], g.rz[0], g.rz[1], g.rz[2]);
+    if (fabs(denom) < P.opt.grazing_eps) continue;  // geometry.cpp:40-47
+    const double rt = g.num / denom;
+    if (!(rt > 0)) continue;
+    if (!use_cache) {
+      seq[n++] = rt;
+      continue;
+    }
+    double prt;
+    int pid;
+    if (cache_step(cd, ci, csz, rt, id, prt, pid)) seq[n++] = prt;
+  }
+  if (use_cache)
+    for (int q = 0; q < csz; ++q) seq[n++] = cd[q];  // end marker: drain in order
+  if (n < 2) return;
+  // discordant pairs (i < j, p_i > p_j) by bottom-up merge sort of a copy
+  for (int i = 0; i < n; ++i) tmp[i] = seq[i];
+  // the processed order stays in seq; the merge ping-pongs between the row's
+  // second and third thirds (scratch row = 3 L doubles)
+  double* a = tmp;
+  double* c2 = seq + 2 * L;
+  long long disc = 0;
+  for (int w = 1; w < n; w *= 2) {
+    for (int lo = 0; lo < n; lo += 2 * w) {
+      const int mid = min(lo + w, n), hi = min(lo + 2 * w, n);
+      int i = lo, j = mid, k = lo;
+      while (i < mid && j < hi) {
+        if (a[j] < a[i]) {
+          disc += mid - i;
+          c2[k++] = a[j++];
+        } else {
+          c2[k++] = a[i++];
+        }
+      }
+      while (i < mid) c2[k++] = a[i++];
+      while (j < hi) c2[k++] = a[j++];
+    }
+    double* sw = a;
+    a = c2;
+    c2 = sw;
+  }
+  // a = sorted; ties: pairs of equal values are neither concordant nor discordant
+  long long ties = 0, run = 1;
+  for (int i = 1; i < n; ++i) {
+    if (a[i] == a[i - 1]) {
+      ++run;
+    } else {
+      ties += run * (run - 1) / 2;
+      run = 1;
+    }
+  }
+  ties += run * (run - 1) / 2;
+  const long long total = (long long)n * (n - 1) / 2;
+  const long long conc = total - disc - ties;
+  const double pairs = 0.5 * n * (n - 1);
+  tau_out[pix] = (conc - disc) / pairs;
+  double mae = 0;
+  for (int i = 0; i < n; ++i) mae += fabs(seq[i] - a[i]);
+  mae_out[pix] = mae / n;
+  flag_out[pix] = disc == 0 ? 2 : 1;
+}
+
+// the reference's accumulation order: tiles row-major, pixels row-major inside
+__global__ void k_eval_sorting_reduce(CamD cam, const long long* __restrict__ tileoff, const double* __restrict__ tau,
+                                      const double* __restrict__ mae, const unsigned char* __restrict__ flag,
+                                      double* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  double tau_sum = 0, mae_sum = 0;
+  long long ordered = 0, counted = 0;
+  for (int ty = 0; ty < cam.tiles_y; ++ty)
+    for (int tx = 0; tx < cam.tiles_x; ++tx) {
+      const int t = ty * cam.tiles_x + tx;
+      if (tileoff[t + 1] == tileoff[t]) continue;
+      const int x0 = tx * kTile, y0 = ty * kTile;
+      const int x1 = min(cam.W, x0 + kTile), y1 = min(cam.H, y0 + kTile);
+      for (int y = y0; y < y1; ++y)
+        for (int x = x0; x < x1; ++x) {
+          const size_t p = (size_t)y * cam.W + x;
+          if (!flag[p]) continue;
+          tau_sum += tau[p];
+          mae_sum += mae[p];
+          if (flag[p] == 2) ++ordered;
+          ++counted;
+        }
+    }
+  out[0] = counted > 0 ? (double)ordered / counted : 0.0;
+  out[1] = counted > 0 ? tau_sum / counted : 0.0;
+  out[2] = counted > 0 ? mae_sum / counted : 0.0;
+  out[3] = (double)counted;
+}
+
+void launch_eval_sorting(const RasterParams& P, int tile0, int tile1, const long long* scr_off, double* scratch,
+                         int use_cache, double* tau, double* mae, unsigned char* flag, cudaStream_t s) {
+  if (tile1 > tile0) k_eval_sorting<<<tile1 - tile0, 256, 0, s>>>(P, tile0, tile1, scr_off, scratch, use_cache, tau,
+                                                                   mae, flag);
+}
+
+void launch_eval_sorting_reduce(const CamD& cam, const long long* tileoff, const double* tau, const double* mae,
+                                const unsigned char* flag, double* out, cudaStream_t s) {
+  k_eval_sorting_reduce<<<1, 32, 0, s>>>(cam, tileoff, tau, mae, flag, out);
+}
+
 }  // namespace drk
