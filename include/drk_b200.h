@@ -48,7 +48,11 @@ typedef enum drk_status {
   DRK_ERR_UNSUPPORTED = 10,
   DRK_ERR_IO = 11,                /* drk::IoError (io.cpp:51,60) */
   DRK_ERR_CORRUPT_FILE = 12,      /* drk::CorruptFileError (io.cpp:63,68,72,80) */
-  DRK_ERR_VERSION = 13            /* drk::VersionMismatchError (io.cpp:70,74) */
+  DRK_ERR_VERSION = 13,           /* drk::VersionMismatchError (io.cpp:70,74) */
+  DRK_ERR_DEGENERATE_FACE = 14,   /* drk::DegenerateFaceError (mesh.cpp:222-258) */
+  DRK_ERR_TOO_MANY_VERTICES = 15, /* drk::TooManyVerticesError (mesh.cpp:223-225) */
+  DRK_ERR_PARSE = 16,             /* drk::ParseError (mesh.cpp:153-185) */
+  DRK_ERR_EMPTY_MESH = 17         /* drk::EmptyMeshError (mesh.cpp:197) */
 } drk_status;
 
 /* drk::Camera (reference geometry.hpp:9-19). */
@@ -311,6 +315,30 @@ int drk_scene_load(drk_ctx* ctx, const char* path, int expected_basis_count, flo
                    drk_scene_header* out);
 /* drk::save_scene (io.cpp:40-56) from device raw parameters f32 [S][n]. */
 int drk_scene_save(drk_ctx* ctx, const char* path, const float* raw_dev, int n, int k, int sh_degree);
+
+/* --- Mesh2DRK (reference mesh.hpp, mesh.cpp) ------------------------------- */
+typedef struct drk_mesh drk_mesh;
+/* load_mesh (mesh.cpp:134-217): OBJ subset (v, f, usemtl / mtllib diffuse
+ * colour); non-planar or concave polygons fan-triangulated.  Host only.  *out
+ * is always set (free it with drk_mesh_free; drk_mesh_error has the message);
+ * DRK_ERR_IO / DRK_ERR_PARSE / DRK_ERR_EMPTY_MESH like the reference. */
+int drk_mesh_load(const char* path, drk_mesh** out);
+int drk_mesh_info(const drk_mesh* mesh, int64_t* n_vertices, int64_t* n_faces, int64_t* n_indices,
+                  int32_t* n_warnings);
+const char* drk_mesh_error(const drk_mesh* mesh);
+/* Host arrays: vertices [nv][3], face_offsets [nf+1] (CSR), indices, colors [nf][3]. */
+int drk_mesh_arrays(const drk_mesh* mesh, double* vertices, int32_t* face_offsets, int32_t* indices, double* colors);
+void drk_mesh_free(drk_mesh* mesh);
+/* convert (mesh.cpp:326-343) on the device: one DRK per face (face_to_drk_raw,
+ * mesh.cpp:219-319), degenerate faces skipped in order (*n_skipped), a face
+ * with more than k vertices -> DRK_ERR_TOO_MANY_VERTICES.  Inputs are device
+ * arrays as drk_mesh_arrays lays them out; raw_out (device, may be NULL to
+ * query *n_out) = f32 [scalar_count(k, 1)][cap], SH degree 0. */
+int drk_mesh_convert(drk_ctx* ctx, const double* vertices, int64_t n_vertices, const int32_t* face_offsets,
+                     const int32_t* indices, const double* colors, int n_faces, int k, float* raw_out, int64_t cap,
+                     int64_t* n_out, int64_t* n_skipped);
+/* shade_lambert (mesh.cpp:345-357) in place on device raw f32 [S][n]. */
+int drk_shade_lambert(drk_ctx* ctx, float* raw, int n, int k, const double* light_dir, double ambient);
 
 /* --- validation hook ----------------------------------------------------- */
 /* Samples the fp32 alpha fast path against the fp64 path on the activated

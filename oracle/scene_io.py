@@ -137,3 +137,51 @@ def ref_load_scene(path: str, expected_basis_count: int = -1):
     raw = np.zeros((scalar_count(k, deg), n), np.float64)
     st = _lib().refio_load_scene(os.fsencode(path), expected_basis_count, hdr.ctypes.data, raw.ctypes.data, n)
     return st, k, deg, raw
+
+
+# --- Mesh2DRK of the reference build (mesh.cpp in oracle/_ref/libdrk_refio.so) --------
+def ref_load_mesh(path: str):
+    """load_mesh (mesh.cpp:134-217) -> (status, dict of arrays or None)."""
+    h = _lib()
+    h.refmesh_load.argtypes = [C.c_char_p, C.c_void_p]
+    sizes = np.zeros(4, np.int64)
+    st = h.refmesh_load(os.fsencode(path), sizes.ctypes.data)
+    if st:
+        return st, None
+    nv, nf, ni, nw = (int(x) for x in sizes)
+    out = dict(vertices=np.zeros((nv, 3)), face_offsets=np.zeros(nf + 1, np.int32), indices=np.zeros(ni, np.int32),
+               colors=np.zeros((nf, 3)), warnings=nw)
+    h.refmesh_arrays.argtypes = [C.c_void_p] * 4
+    h.refmesh_arrays(out["vertices"].ctypes.data, out["face_offsets"].ctypes.data, out["indices"].ctypes.data,
+                     out["colors"].ctypes.data)
+    return 0, out
+
+
+def ref_convert(mesh: dict, k: int):
+    """convert (mesh.cpp:326-343) -> (status, raw f64 [S, n], n_skipped)."""
+    h = _lib()
+    h.refmesh_convert.argtypes = [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                  C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p]
+    nf = len(mesh["face_offsets"]) - 1
+    S = scalar_count(k, 0)
+    raw = np.zeros((S, max(nf, 1)))
+    n_out, n_skip = C.c_longlong(0), C.c_longlong(0)
+    v = np.ascontiguousarray(mesh["vertices"], np.float64)
+    o = np.ascontiguousarray(mesh["face_offsets"], np.int32)
+    i = np.ascontiguousarray(mesh["indices"], np.int32)
+    c = np.ascontiguousarray(mesh["colors"], np.float64)
+    st = h.refmesh_convert(v.ctypes.data, len(v), o.ctypes.data, i.ctypes.data, c.ctypes.data, nf, k, raw.ctypes.data,
+                           raw.shape[1], C.byref(n_out), C.byref(n_skip))
+    if st:
+        return st, None, None
+    return 0, np.ascontiguousarray(raw[:, :n_out.value]), n_skip.value
+
+
+def ref_shade_lambert(raw: np.ndarray, k: int, light, ambient: float) -> np.ndarray:
+    """shade_lambert (mesh.cpp:345-357) on a copy of raw f64 [S, n] (SH degree 0)."""
+    h = _lib()
+    h.refmesh_shade.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_double]
+    r = np.ascontiguousarray(raw, np.float64).copy()
+    lt = np.asarray(light, np.float64)
+    assert h.refmesh_shade(r.ctypes.data, r.shape[1], k, lt.ctypes.data, float(ambient)) == 0
+    return r

@@ -50,9 +50,26 @@ class VersionMismatchError(DrkError):
     status = 13
 
 
+class DegenerateFaceError(DrkError):
+    status = 14
+
+
+class TooManyVerticesError(DrkError):
+    status = 15
+
+
+class ParseError(DrkError):
+    status = 16
+
+
+class EmptyMeshError(DrkError):
+    status = 17
+
+
 _ERRORS = {e.status: e for e in (NonFiniteError, DegenerateQuaternionError, DegenerateBasisError,
                                  ReplayMismatchError, DimensionMismatchError, IoError, CorruptFileError,
-                                 VersionMismatchError)}
+                                 VersionMismatchError, DegenerateFaceError, TooManyVerticesError, ParseError,
+                                 EmptyMeshError)}
 
 
 class Camera_(C.Structure):
@@ -152,6 +169,15 @@ SIGNATURES = {
     "drk_scene_read_header": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(SceneHeader_)]),
     "drk_scene_load": (C.c_int, [_P, C.c_char_p, C.c_int, _P, C.c_int64, C.POINTER(SceneHeader_)]),
     "drk_scene_save": (C.c_int, [_P, C.c_char_p, _P, C.c_int, C.c_int, C.c_int]),
+    "drk_mesh_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "drk_mesh_info": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                C.POINTER(C.c_int32)]),
+    "drk_mesh_error": (C.c_char_p, [_P]),
+    "drk_mesh_arrays": (C.c_int, [_P, _P, _P, _P, _P]),
+    "drk_mesh_free": (None, [_P]),
+    "drk_mesh_convert": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P, C.c_int, C.c_int, _P, C.c_int64,
+                                   C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "drk_shade_lambert": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, C.c_double]),
     "drk_debug_alpha_bound": (C.c_int, [_P, C.c_int64, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "drk_adam_step": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                 C.POINTER(AdamConfig_)]),

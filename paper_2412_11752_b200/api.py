@@ -526,6 +526,30 @@ class Rasterizer:
         p, state.m, state.v = (o[:, :m].contiguous() for o in outs)
         return p
 
+    # --- Mesh2DRK (reference mesh.cpp) ------------------------------------------
+    def mesh_convert(self, mesh: "MeshData", basis_count: int = 8):
+        """convert (reference mesh.cpp:326-343) on the device -> (raw f32 [S, n], n_skipped):
+        one DRK per face, degenerate faces skipped in order, SH degree 0."""
+        dev = self.device
+        v = torch.from_numpy(np.ascontiguousarray(mesh.vertices, np.float64)).to(dev)
+        o = torch.from_numpy(np.ascontiguousarray(mesh.face_offsets, np.int32)).to(dev)
+        i = torch.from_numpy(np.ascontiguousarray(mesh.indices, np.int32)).to(dev)
+        c = torch.from_numpy(np.ascontiguousarray(mesh.colors, np.float64)).to(dev)
+        nf = len(mesh.face_offsets) - 1
+        raw = torch.empty(scalar_count(basis_count, 1), max(nf, 1), device=dev, dtype=torch.float32)
+        n_out, n_skip = C.c_int64(0), C.c_int64(0)
+        self._sync_stream()
+        self._check(_lib.lib().drk_mesh_convert(self._h, _ptr(v), len(mesh.vertices), _ptr(o), _ptr(i), _ptr(c), nf,
+                                                basis_count, _ptr(raw), raw.shape[1], C.byref(n_out),
+                                                C.byref(n_skip)))
+        return raw[:, :n_out.value].contiguous(), n_skip.value
+
+    def shade_lambert(self, raw: torch.Tensor, light_dir, ambient: float, basis_count: int = 8):
+        """shade_lambert (reference mesh.cpp:345-357), in place on device raw parameters."""
+        lt = (C.c_double * 3)(*[float(x) for x in light_dir])
+        self._sync_stream()
+        self._check(_lib.lib().drk_shade_lambert(self._h, _ptr(raw), raw.shape[1], basis_count, lt, float(ambient)))
+
     # --- scene files (DRKSCENE v1) -------------------------------------------
     def load_scene(self, path: str, expected_basis_count: int = -1) -> "DeviceScene":
         """drk::load_scene (reference io.cpp:58-97) straight to a device tensor in the
@@ -577,6 +601,36 @@ class DensifyStats:
     def zeros(n: int, device) -> "DensifyStats":
         return DensifyStats(torch.zeros(n, device=device, dtype=torch.float64),
                             torch.zeros(n, device=device, dtype=torch.int32))
+
+
+@dataclass
+class MeshData:
+    """drk::Mesh (reference mesh.hpp:10-18) as host arrays: faces in CSR form."""
+
+    vertices: np.ndarray      # f64 [nv, 3]
+    face_offsets: np.ndarray  # i32 [nf + 1]
+    indices: np.ndarray       # i32 (0-based)
+    colors: np.ndarray        # f64 [nf, 3]
+    warnings: int = 0
+
+
+def load_mesh(path: str) -> MeshData:
+    """load_mesh (reference mesh.cpp:134-217) through the C-ABI (host code)."""
+    h = C.c_void_p()
+    L = _lib.lib()
+    st = L.drk_mesh_load(os.fsencode(path), C.byref(h))
+    try:
+        if st:
+            raise _lib._ERRORS.get(st, DrkError)(L.drk_mesh_error(h).decode())
+        nv, nf, ni, nw = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+        L.drk_mesh_info(h, C.byref(nv), C.byref(nf), C.byref(ni), C.byref(nw))
+        m = MeshData(np.zeros((nv.value, 3)), np.zeros(nf.value + 1, np.int32), np.zeros(ni.value, np.int32),
+                     np.zeros((nf.value, 3)), nw.value)
+        L.drk_mesh_arrays(h, m.vertices.ctypes.data, m.face_offsets.ctypes.data, m.indices.ctypes.data,
+                          m.colors.ctypes.data)
+        return m
+    finally:
+        L.drk_mesh_free(h)
 
 
 @dataclass

@@ -729,6 +729,10 @@ const char* drk_status_string(int s) {
     case DRK_ERR_IO: return "i/o error";
     case DRK_ERR_CORRUPT_FILE: return "corrupt file";
     case DRK_ERR_VERSION: return "version mismatch";
+    case DRK_ERR_DEGENERATE_FACE: return "degenerate face";
+    case DRK_ERR_TOO_MANY_VERTICES: return "too many vertices";
+    case DRK_ERR_PARSE: return "parse error";
+    case DRK_ERR_EMPTY_MESH: return "empty mesh";
   }
   return "unknown status";
 }
