@@ -3,6 +3,10 @@
 // tile offsets -> K4 raster; backward: K5 raster-bwd -> K6 activation bwd.
 #include <cuda.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -408,8 +412,30 @@ static int finish_copy_out(drk_ctx* c, const float* color, const float* depth, c
   return DRK_OK;
 }
 
+// DRK_HOST_TRACE=1: host wall-clock checkpoints of run_forward on stderr
+// (development aid for host-side gaps between the device stages)
+struct HostTrace {
+  bool on = getenv("DRK_HOST_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  std::string line;
+  void at(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    char b[64];
+    snprintf(b, sizeof b, " %s %.2f", what, std::chrono::duration<double, std::milli>(now - last).count());
+    line += b;
+    last = now;
+  }
+  ~HostTrace() {
+    if (on)
+      fprintf(stderr, "[drk host] %s | total %.2f ms\n", line.c_str(),
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float* color, float* depth,
                 float* normal, float* alpha) {
+  HostTrace ht;
   const Activated& A = c->act;
   if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0) || !(cam->fy > 0))
     return set_error(c, DRK_ERR_INVALID_ARG, "invalid camera");
@@ -500,6 +526,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     if (attempt == 3) return set_error(c, DRK_ERR_OOM, "hull pool retries");
   }
   mark(c, 2);
+  ht.at("k1");
   float prep_ms[2] = {0, 0};
   if (c->timing) {
     cudaEventSynchronize(c->ev[2]);
@@ -515,6 +542,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     DRK_COUNT_LAUNCH();
   }
   if (int st = plan_bands(c)) return st;
+  ht.at("plan");
   // per-pixel state / replay
   double* pxstate = ensure<double>(c->pxstate, 8 * (size_t)n_pix);
   unsigned char* pxflag = ensure<unsigned char>(c->pxflag, (size_t)n_pix);
@@ -536,6 +564,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     mark(c, 2);
     long long n_pairs = 0;
     if (int st = bin_band(c, ty_lo, ty_hi, &n_pairs)) return st;
+    ht.at("bin");
     n_pairs_total += n_pairs;
     RasterParams P = raster_params(c);
     P.pxflag = pxflag;
@@ -572,8 +601,10 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     }
   }
   c->n_pairs = n_pairs_total;
+  ht.at("launch");
   unsigned long long h[C_COUNT];
   if (int st = read_counters(c, h)) return st;
+  ht.at("raster");
   if (c->timing) {
     for (int i = 0; i < 2; ++i) c->stats.stage_ms[i] = prep_ms[i];
     for (int k = 0; k < 4; ++k) c->stats.stage_ms[2 + k] = band_ms[k];

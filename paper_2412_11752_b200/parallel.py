@@ -53,3 +53,66 @@ def params_checksum(params) -> float:
     p = params.detach().to(torch.float64)
     return float((p * torch.arange(1, p.numel() + 1, dtype=torch.float64, device=p.device).reshape(p.shape)
                   .remainder(7.0).add(1.0)).sum())
+
+
+class MultiViewRenderer:
+    """Renders a batch of views on one GPU with ``inflight`` rasterizer contexts,
+    each on its own CUDA stream driven by its own host thread (the C-ABI calls
+    release the GIL).  A view's host-side sizing points (the scans that return
+    row / pair counts) and its FP64-heavy binning then overlap another view's
+    FP32 rasterization, instead of leaving the GPU idle between views.
+    Views are handed out dynamically (next view to the first free context), and
+    every view's framebuffers are identical to a single-context render."""
+
+    def __init__(self, device=None, inflight: int = 2):
+        import torch
+
+        from .api import Rasterizer
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.rasts = [Rasterizer(self.device.index) for _ in range(inflight)]
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(inflight)]
+
+    def render(self, raw, cams, opt, k: int = 8):
+        """Framebuffers of every camera (list, camera order); ordered after the
+        caller's current stream and before it again on return."""
+        import threading
+
+        import torch
+        start = torch.cuda.Event()
+        start.record(torch.cuda.current_stream(self.device))
+        results = [None] * len(cams)
+        errors = []
+        nxt = [0]
+        lock = threading.Lock()
+
+        def work(w):
+            try:
+                torch.cuda.set_device(self.device)
+                s = self.streams[w]
+                s.wait_event(start)
+                with torch.cuda.stream(s):
+                    while True:
+                        with lock:
+                            i = nxt[0]
+                            nxt[0] += 1
+                        if i >= len(cams):
+                            return
+                        results[i] = self.rasts[w].render(raw, cams[i], opt, k=k)
+            except Exception as e:  # surfaced on the caller's thread
+                errors.append(e)
+
+        threads = [threading.Thread(target=work, args=(w,)) for w in range(len(self.rasts))]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
+        main = torch.cuda.current_stream(self.device)
+        for s in self.streams:
+            main.wait_stream(s)
+        return results
+
+    def close(self):
+        for r in self.rasts:
+            r.close()
