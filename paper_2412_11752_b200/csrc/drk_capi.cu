@@ -197,14 +197,6 @@ static int plan_bands(drk_ctx* c) {
   }
   if (c->band_pair_limit == 0 && (double)n * cd.tiles_x * cd.tiles_y <= 0.25 * (double)c->device_bytes / kPairBytes)
     return DRK_OK;  // every primitive in every tile would still fit in a quarter of the device
-  double limit = (double)c->band_pair_limit;
-  if (limit <= 0) {
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const size_t held = c->pk.bytes + c->pv.bytes + c->sk.bytes + c->hist.bytes + c->sortoff.bytes;
-    limit = 0.7 * (double)(free_b + held) / kPairBytes;
-  }
-  if ((double)n * cd.tiles_x * cd.tiles_y <= limit) return DRK_OK;
   unsigned long long* rowest = ensure<unsigned long long>(c->rowest, cd.tiles_y + 1);
   if (!rowest) return set_error(c, DRK_ERR_OOM, "row estimates");
   cudaMemsetAsync(rowest, 0, sizeof(unsigned long long) * (cd.tiles_y + 1), c->stream);
@@ -217,6 +209,16 @@ static int plan_bands(drk_ctx* c) {
   if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "band plan")) return st;
   unsigned long long total = 0;
   for (auto e : est) total += e;
+  double limit = (double)c->band_pair_limit;
+  if (limit <= 0) {
+    // the bound fits a quarter of the device: no free-memory query (cudaMemGetInfo
+    // costs milliseconds to tens of milliseconds per call)
+    if ((double)total <= 0.25 * (double)c->device_bytes / kPairBytes) return DRK_OK;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t held = c->pk.bytes + c->pv.bytes + c->sk.bytes + c->hist.bytes + c->sortoff.bytes;
+    limit = 0.7 * (double)(free_b + held) / kPairBytes;
+  }
   if ((double)total <= limit) return DRK_OK;
   c->bands.assign({0});
   unsigned long long acc = 0;
@@ -500,10 +502,11 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
       std::vector<int> list(n_ovf);
       cudaMemcpyAsync(list.data(), ovf, sizeof(int) * n_ovf, cudaMemcpyDeviceToHost, s);
       if (int st = cuda_check(c, cudaStreamSynchronize(s), "overflow list")) return st;
-      DevBuf scratch, dlist;
+      // grow-only context buffers: a per-call cudaMalloc / cudaFree of the
+      // 0.5 GB scratch stalled views with near-clipped primitives by 10-500 ms
       const int batch = 256;
-      double2* scr = ensure<double2>(scratch, (size_t)batch * 2 * (cap + 2));
-      int* dl = ensure<int>(dlist, n_ovf);
+      double2* scr = ensure<double2>(c->ovf_scr, (size_t)batch * 2 * (cap + 2));
+      int* dl = ensure<int>(c->ovf_list, n_ovf);
       if (!scr || !dl) return set_error(c, DRK_ERR_OOM, "large polygon scratch");
       cudaMemcpyAsync(dl, list.data(), sizeof(int) * n_ovf, cudaMemcpyHostToDevice, s);
       for (long long b = 0; b < n_ovf; b += batch) {
@@ -511,9 +514,6 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
         k_prep1<<<(cnt + 127) / 128, 128, 0, s>>>(A, cd, od, geo, bbox, hullref, pool, c->hull_cap, rowcnt, ctr,
                                                     dl + b, cnt, scr, cap, ovf);
       }
-      cudaStreamSynchronize(s);
-      release(scratch);
-      release(dlist);
       if (int st = read_counters(c, h)) return st;
       if (h[C_POLY_FAIL]) return set_error(c, DRK_ERR_UNSUPPORTED, "support polygon above 65536 vertices");
     }
@@ -848,7 +848,7 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
                     &c->counters, &c->scan_tmp, &c->loss_tmp, &c->progress, &c->patch, &c->scene_aos,
                     &c->loss_part, &c->ssim_f, &c->dens_code, &c->dens_pos,
-                    &c->eval_scr, &c->eval_px, &c->eval_off};
+                    &c->eval_scr, &c->eval_px, &c->eval_off, &c->ovf_scr, &c->ovf_list};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : c->ev)
     if (e) cudaEventDestroy(e);

@@ -121,10 +121,11 @@ struct drk_ctx {
   drk::DevBuf pxstate, replay_cnt, replay_rec, replay_ids;
   drk::DevBuf gact, touched;
   drk::DevBuf counters, scan_tmp, loss_tmp;
-  drk::DevBuf scene_aos;
-  drk::DevBuf loss_part, ssim_f;
-  drk::DevBuf dens_code, dens_pos;
-  drk::DevBuf eval_scr, eval_px, eval_off;  // drk_eval_sorting: sequence scratch, per-pixel metrics, chunk offsets  // drk_densify_and_prune: per-primitive decision / output count, scanned positions  // drk_loss / drk_ssim / drk_psnr: partial sums, SSIM adjoint fields  // record-major staging of scene files (drk_scene_load / drk_scene_save)
+  drk::DevBuf scene_aos;                  // record-major staging of scene files (drk_scene_load / drk_scene_save)
+  drk::DevBuf loss_part, ssim_f;          // drk_loss / drk_ssim / drk_psnr: partial sums, SSIM adjoint fields
+  drk::DevBuf dens_code, dens_pos;        // drk_densify_and_prune / drk_mesh_convert: per-item code / count, scanned positions
+  drk::DevBuf eval_scr, eval_px, eval_off;  // drk_eval_sorting: sequence scratch, per-pixel metrics, chunk offsets
+  drk::DevBuf ovf_scr, ovf_list;          // K1 large-polygon path: per-primitive vertex scratch, overflow list
   int64_t hull_cap = 0;
   drk::DevBuf rowest;
   std::vector<int> bands;         // tile-row band boundaries of the last forward
