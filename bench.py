@@ -144,11 +144,13 @@ def reference_cpu_sample(crop: str, steps: int = 1):
 
 
 def run_reference(args):
-    """Reference CPU arm: rank 0 alone times the unmodified reference (oracle/_ref); W warm-up
-    steps are skipped (the CPU has no warm-up effects worth the minutes), K bounded steps timed."""
+    """Reference CPU arm: rank 0 alone times the unmodified reference (oracle/_ref): W untimed
+    warm-up samples, then K bounded samples timed (~5 s each on 16 host threads)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    for _ in range(max(0, args.warmup)):
+        reference_cpu_sample(args.cpu_crop, 1)
     vals, cpu = [], None
     for _ in range(max(1, args.steps)):
         cpu, _ = reference_cpu_sample(args.cpu_crop, 1)
@@ -157,7 +159,7 @@ def run_reference(args):
     cpu["value"] = v
     w, h = (int(x) for x in args.cpu_crop.split("x"))
     line = {"impl": "reference", "metric": "megapixels/sec rendered (forward; fwd+bwd in fwd_bwd)", "value": v,
-            "unit": "megapixels/s", "n_gpus": world, "steps": args.steps, "warmup": 0,
+            "unit": "megapixels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * (w * h) / (v * 1e6), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scenes.py generator)",
             "config": {"workload": f"config1 forward (100k DRK, K=8, SH3, 1920x1080 view), {args.cpu_crop} centred "
