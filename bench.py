@@ -56,6 +56,8 @@ def parse():
                     help="config 3 leg: orbit views per step, split across ranks (0 = skip)")
     ap.add_argument("--multiview-inflight", type=int, default=2,
                     help="config 3 leg: rasterizer contexts in flight per GPU (own stream + host thread each)")
+    ap.add_argument("--config4-train", action="store_true",
+                    help="also time one full config-4 training step (4M DRK, 8 views of 3840x2160 per GPU; ~1 min)")
     ap.add_argument("--no-train", action="store_true", help="skip the multi-GPU training-step leg")
     return ap.parse_args()
 
@@ -374,46 +376,50 @@ def main():
     # ---- training step: per-rank views, NCCL all-reduce of the raw gradients, Adam (config 4 structure at
     #      config 2 scale: 300k DRK, 1280x720, 2 views per GPU) ----
     train = None
-    if not args.no_train:
+
+    def train_leg(cfg_id: int, views_per_gpu: int, warm: int, timed: int):
+        """Training step: per-rank views, forward + L1 + backward per view (raw gradients
+        accumulated), NCCL all-reduce (mean over all views), Adam; max over ranks."""
         from paper_2412_11752_b200.api import OptState, TrainConfig
         from paper_2412_11752_b200.parallel import allreduce_mean_, params_checksum
-        sc4 = scenes.config_scene(2)
-        base_cam = scenes.config_cameras(2)[0]
-        orbit = scenes.orbit_cameras(2 * world, base_cam.width, base_cam.height, seed=4)
-        views = [orbit[2 * rank], orbit[2 * rank + 1]]
-        tg = [torch.from_numpy(scenes.config_target(2, cv, view=2 * rank + i).astype(np.float32)).to(dev)
-              for i, cv in enumerate(views)]
-        p4 = torch.from_numpy(sc4.f32()).to(dev)
-        g4 = torch.zeros_like(p4)
-        st4 = OptState.zeros_like(p4)
+        sc_t = scenes.config_scene(cfg_id)
+        base_cam = scenes.config_cameras(cfg_id)[0]
+        orbit = scenes.orbit_cameras(views_per_gpu * world, base_cam.width, base_cam.height, seed=4)
+        views = orbit[views_per_gpu * rank:views_per_gpu * (rank + 1)]
+        tg = [torch.from_numpy(scenes.config_target(cfg_id, cv, view=views_per_gpu * rank + i).astype(np.float32))
+              .to(dev) for i, cv in enumerate(views)]
+        p_t = torch.from_numpy(sc_t.f32()).to(dev)
+        del sc_t
+        g_t = torch.zeros_like(p_t)
+        st_t = OptState.zeros_like(p_t)
         tcfg = TrainConfig(steps=35000, lr_drk=1e-3, lr_position=1e-3 / 2.0, lr_rotation=1e-3, lr_opacity=1e-3,
                            lr_sh=1e-3)
+        opt_t = RenderOptions(sh_degree=3)
 
-        def train_step4():
-            g4.zero_()
+        def step():
+            g_t.zero_()
             for cv, tgt in zip(views, tg):
-                fb = r.render(p4, cv, opt2)
+                fb = r.render(p_t, cv, opt_t)
                 _, dcol = r.l1_loss(fb.color, tgt)
-                r.backward_render(p4, FrameGrad(d_color=dcol), grad_out=g4, accumulate=True)
-            allreduce_mean_(g4, 2 * world)
-            r.adam_step(p4, g4, st4, tcfg, scene_extent=2.0)
+                r.backward_render(p_t, FrameGrad(d_color=dcol), grad_out=g_t, accumulate=True)
+            allreduce_mean_(g_t, views_per_gpu * world)
+            r.adam_step(p_t, g_t, st_t, tcfg, scene_extent=2.0)
 
-        opt2 = RenderOptions(sh_degree=3)
-        train_step4()
+        for _ in range(warm):
+            step()
         torch.cuda.synchronize(dev)
-        ntr = 2
         tr_ms = []
-        for _ in range(ntr):
+        for _ in range(timed):
             barrier()
             torch.cuda.synchronize(dev)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            train_step4()
+            step()
             b.record(stream)
             b.synchronize()
             tr_ms.append(a.elapsed_time(b))
         tr_tot = float(np.mean(tr_ms))
-        csum = params_checksum(p4)
+        csum = params_checksum(p_t)
         in_sync = True
         if world > 1:
             t = torch.tensor([tr_tot], device=dev, dtype=torch.float64)
@@ -422,12 +428,21 @@ def main():
             cs = torch.tensor([csum, -csum], device=dev, dtype=torch.float64)
             dist.all_reduce(cs, op=dist.ReduceOp.MAX)
             in_sync = bool(abs(float(cs[0].item()) + float(cs[1].item())) == 0.0)
-        px4 = base_cam.width * base_cam.height
-        train = {"value": 2 * world * px4 / (tr_tot * 1e-3) / 1e6, "unit": "megapixels/s", "ms_per_step": tr_tot,
-                 "steps": ntr, "scaling": "weak", "replicas_in_sync": in_sync,
-                 "workload": "training step with config 4's structure at config 2 scale: 300k DRK, K=8, SH3, 2 orbit "
+        px = base_cam.width * base_cam.height
+        return {"value": views_per_gpu * world * px / (tr_tot * 1e-3) / 1e6, "unit": "megapixels/s",
+                "ms_per_step": tr_tot, "steps": timed, "warmup": warm, "scaling": "weak", "replicas_in_sync": in_sync}
+
+    if not args.no_train:
+        train = train_leg(2, 2, 1, 2)
+        train["workload"] = ("training step with config 4's structure at config 2 scale: 300k DRK, K=8, SH3, 2 orbit "
                              "views of 1280x720 per GPU, forward + L1 + backward per view, NCCL all-reduce (mean over "
-                             "all views) of the raw gradients, Adam (lr 1e-3); replicas checked by parameter checksum"}
+                             "all views) of the raw gradients, Adam (lr 1e-3); replicas checked by parameter checksum")
+    train_c4 = None
+    if args.config4_train:
+        train_c4 = train_leg(4, 8, 1, 1)
+        train_c4["workload"] = ("config 4 training step: 4M DRK, K=8, SH3, 8 orbit views of 3840x2160 per GPU "
+                                "(banded binning), forward + L1 + backward per view, NCCL all-reduce (mean over all "
+                                "views) of the raw gradients, Adam (lr 1e-3); one warm-up step (buffer growth)")
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
@@ -450,7 +465,7 @@ def main():
                            "views_per_gpu": 1, "parallelism": f"views x{world} (replicated primitives)",
                            "l2": "flushed between timed steps (256 MiB write, outside the timed events)"},
                 "stage_ms": stage_ms, "pairs": st["pairs"], "fp64_pixels": st["fp64_pixels"],
-                "roofline": roofline, "e2e": e2e, "fwd_bwd": fwd_bwd, "multiview": multiview, "train": train,
+                "roofline": roofline, "e2e": e2e, "fwd_bwd": fwd_bwd, "multiview": multiview, "train": train, "train_config4": train_c4,
                 "cpu_baseline": cpu,
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
