@@ -84,7 +84,8 @@ typedef struct drk_options {
   int32_t fp64_alpha;               /* default 0; 1 = every alpha in fp64 (reference-precision mode:
                                        identical arithmetic across cache / list / exact-sort modes) */
   int32_t raster_kernel;            /* 0 = auto (fp32 interval forward and backward where eligible),
-                                       1 = legacy fp64-depth forward and backward, 5 = legacy backward only */
+                                       1 = legacy fp64-depth forward and backward, 5 = legacy backward only,
+                                       6 / 7 = auto with the fast forward forced to half-tile / tile CTAs */
 } drk_options;
 
 /* Activated primitives (drk::DrkPrimitive, reference types.hpp:77-98), all

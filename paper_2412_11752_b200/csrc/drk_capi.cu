@@ -155,6 +155,7 @@ static RasterParams raster_params(drk_ctx* c) {
   P.redo_count = reinterpret_cast<unsigned int*>(ensure<unsigned long long>(c->redo_cnt, 1));
   P.shrec = A.rec;
   P.frame32 = static_cast<const float4*>(c->frame32.p);
+  P.fast_nt = 256;
   return P;
 }
 
@@ -355,7 +356,7 @@ static int start_copy_out(drk_ctx* c, RasterParams& P) {
   const size_t W = (size_t)cd.W;
   for (int b = 0; b < nbands; ++b) {
     const int ty0 = b * kCopyRows, ty1 = std::min(cd.tiles_y, ty0 + kCopyRows);
-    const unsigned need = (unsigned)((ty1 - ty0) * cd.tiles_x);
+    const unsigned need = (unsigned)((ty1 - ty0) * cd.tiles_x * (256 / P.fast_nt));
     if (wait_value32()(c->copy_stream, (CUdeviceptr)(prog + b), need, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
       return set_error(c, DRK_ERR_CUDA, "stream wait value");
     const size_t y0 = (size_t)ty0 * kTile, y1 = std::min((size_t)cd.H, (size_t)ty1 * kTile);
@@ -585,6 +586,9 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
       P.replay_rec = static_cast<double*>(c->replay_rec.p);
     }
     P.tile_base = ty_lo * cd.tiles_x;
+    P.fast_nt = opt->raster_kernel == 6   ? 128
+                : opt->raster_kernel == 7 ? 256
+                                          : raster_fast_nt(n_pairs, (ty_hi - ty_lo) * cd.tiles_x);
     // exactly the launches where launch_raster runs k_raster_fast (the only
     // kernel that advances the band counters)
     const bool copy_out = c->hout.active && nb == 1 && P.opt.use_cache && P.opt.raster_kernel != 1 &&

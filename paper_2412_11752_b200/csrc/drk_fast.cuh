@@ -196,8 +196,9 @@ static __device__ __noinline__ void pop_f64(const RasterParams& P, int id, int x
   }
 }
 
+template <int RING = kRing>
 __device__ __forceinline__ int entry_id(const RasterParams& P, const int* s_id, long long beg, int jr, int ring_lo) {
-  return jr >= ring_lo ? s_id[jr & (kRing - 1)] : P.lid[beg + jr];
+  return jr >= ring_lo ? s_id[jr & (RING - 1)] : P.lid[beg + jr];
 }
 
 // ---------------------------------------------------------------------------
@@ -444,6 +445,7 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
 }
 // blend (raster.cpp:349-361): colour from SH, accumulation, transmittance
 // and its error bound; returns false once the pixel saturates.
+template <int BSTRIDE = kBatch>
 __device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, const float4* s_b4, int id, double a64,
                                       float relt, float rt, float sgn, float rz0, float rz1, float rz2) {
   const float* shp = P.sh + (size_t)id * P.terms * 3;
@@ -455,7 +457,7 @@ __device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, cons
     for (int t = 0; t < 16; t += 4) {
       if (t < ta) {
         const float4 a = __ldg(q + 3 * (t / 4)), b = __ldg(q + 3 * (t / 4) + 1), c = __ldg(q + 3 * (t / 4) + 2);
-        const float4 bq = s_b4[(t / 4) * kBatch];  // this pixel's basis, terms t..t+3
+        const float4 bq = s_b4[(t / 4) * BSTRIDE];  // this pixel's basis, terms t..t+3
         const float b0 = bq.x, b1 = bq.y, b2 = bq.z, b3 = bq.w;
         c0 = fmaf(b0, a.x, c0);
         c1 = fmaf(b0, a.y, c1);
@@ -473,7 +475,7 @@ __device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, cons
     }
   } else {
     for (int t = 0; t < ta; ++t) {
-      const float4 bq = s_b4[(t >> 2) * kBatch];
+      const float4 bq = s_b4[(t >> 2) * BSTRIDE];
       const int tq = t & 3;
       const float bt = tq == 0 ? bq.x : (tq == 1 ? bq.y : (tq == 2 ? bq.z : bq.w));
       c0 = fmaf(bt, __ldg(shp + 3 * t), c0);
@@ -512,7 +514,7 @@ __device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, cons
   return true;
 }
 
-template <bool VALIDATE>
+template <bool VALIDATE, int NT = kBatch>
 __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, const float4* s_b4, const Rec* ring,
                                          const int* s_id, const TileConst& tc, long long beg, int ring_lo, int jr,
                                          int x, int y) {
@@ -520,7 +522,7 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
   Rec R;
   int id;
   if (jr >= ring_lo) {
-    const int slot = jr & (kRing - 1);
+    const int slot = jr & (2 * NT - 1);
     R = ring[slot];
     id = s_id[slot];
   } else {
@@ -535,7 +537,7 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
     return false;
   }
   if (o.skip) return true;
-  return blend(P, px, s_b4, id, o.a, o.rel, o.rt, o.sgn, R.r0.x, R.r0.y, R.r0.z);
+  return blend<NT>(P, px, s_b4, id, o.a, o.rel, o.rt, o.sgn, R.r0.x, R.r0.y, R.r0.z);
 }
 
 }  // namespace drk

@@ -86,12 +86,14 @@ struct RasterParams {
   int prog_rows;
   const float* shrec;     // fast kernel: per-primitive fp32 shape records (K == 8)
   int* pxstop;            // composites until saturation per pixel (INT_MAX: never), written by the forward
+  int fast_nt;            // fast forward: threads per CTA (256: tile, 128: half tile), raster_fast_nt
   unsigned long long* vstat;  // fast kernel validation: max |a32 - a64| / bound, max |a32 - a64| (double bits)
 };
 
 void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s, cudaEvent_t mid = nullptr);
 bool raster_fast_eligible(const RasterParams& P);
 void launch_raster_fast(const RasterParams& P, int n_tiles, bool validate, cudaStream_t s);
+int raster_fast_nt(long long pairs, int n_tiles);
 void launch_raster_bwd_fast(const RasterParams& P, int n_tiles, cudaStream_t s);
 void launch_shape_rec(const ShapeView& S, int n, float* rec, cudaStream_t s);
 double measure_fp32_peak(cudaStream_t s);

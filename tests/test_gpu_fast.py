@@ -179,3 +179,26 @@ def test_multiview_renderer_matches_single_context(rast):
     for g, w in zip(got, want):
         assert torch.equal(g.color, w)
     mv.close()
+
+
+@pytest.mark.gpu
+def test_half_tile_ctas_bit_identical(rast):
+    """The fast forward's half-tile CTAs (8 x 16 pixels, chosen for long tile lists)
+    give the same framebuffers and per-pixel composite counts as whole-tile CTAs,
+    including the host copy-out path that waits on per-band CTA counters."""
+    from paper_2412_11752_b200 import scenes
+    from paper_2412_11752_b200.api import RenderOptions
+    sc = scenes.random_scene(20000, seed=29, sh_degree=3, clusters=12)
+    cam = scenes.look_at_camera(300, 170, (0.3, 0.2, -3.2))
+    raw = torch.from_numpy(sc.f32()).cuda()
+    out = {}
+    for rk in (7, 6):
+        fb = rast.render(raw, cam, RenderOptions(sh_degree=3, raster_kernel=rk))
+        out[rk] = [t.clone() for t in (fb.color, fb.depth, fb.normal, fb.alpha)]
+        st = rast.stats()
+        out[rk].append(st["streamed"]), out[rk].append(st["composited"])
+        host = rast.render_host(sc.f32(), cam, RenderOptions(sh_degree=3, raster_kernel=rk))
+        assert np.array_equal(host["color"], out[rk][0].cpu().numpy())
+    for a, b in zip(out[7][:4], out[6][:4]):
+        assert torch.equal(a, b)
+    assert out[7][4:] == out[6][4:]
