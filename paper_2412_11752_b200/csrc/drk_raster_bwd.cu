@@ -36,6 +36,7 @@ __device__ __forceinline__ int gcol_global(int c) {
 }
 
 // SH colour before the clamp (geometry.cpp:126-138), float4 coefficient loads
+template <int BSTRIDE>
 __device__ __forceinline__ void sh_colour(const RasterParams& P, const float* s_basis, int id, float& c0, float& c1,
                                           float& c2) {
   const float* shp = P.sh + (size_t)id * P.terms * 3;
@@ -47,8 +48,8 @@ __device__ __forceinline__ void sh_colour(const RasterParams& P, const float* s_
     for (int t = 0; t < 16; t += 4) {
       if (t < ta) {
         const float4 a = __ldg(q + 3 * (t / 4)), b = __ldg(q + 3 * (t / 4) + 1), c = __ldg(q + 3 * (t / 4) + 2);
-        const float b0 = s_basis[t * kBatch], b1 = s_basis[(t + 1) * kBatch], b2 = s_basis[(t + 2) * kBatch],
-                    b3 = s_basis[(t + 3) * kBatch];
+        const float b0 = s_basis[t * BSTRIDE], b1 = s_basis[(t + 1) * BSTRIDE], b2 = s_basis[(t + 2) * BSTRIDE],
+                    b3 = s_basis[(t + 3) * BSTRIDE];
         c0 = fmaf(b0, a.x, c0);
         c1 = fmaf(b0, a.y, c1);
         c2 = fmaf(b0, a.z, c2);
@@ -66,7 +67,7 @@ __device__ __forceinline__ void sh_colour(const RasterParams& P, const float* s_
     return;
   }
   for (int t = 0; t < ta; ++t) {
-    const float bt = s_basis[t * kBatch];
+    const float bt = s_basis[t * BSTRIDE];
     c0 = fmaf(bt, __ldg(shp + 3 * t), c0);
     c1 = fmaf(bt, __ldg(shp + 3 * t + 1), c1);
     c2 = fmaf(bt, __ldg(shp + 3 * t + 2), c2);
@@ -312,23 +313,28 @@ __device__ __noinline__ void record_grad_f64(const RasterParams& P, const BwdPix
 }
 }  // namespace
 
-__global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __grid_constant__ RasterParams P) {
+// NT threads per CTA: 256 = a 16x16 tile, 128 = half a tile (8 x 16 pixels;
+// long tile lists), as in the fast forward.
+template <int NT>
+__global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fast(const __grid_constant__ RasterParams P) {
+  constexpr int RING = 2 * NT;
   extern __shared__ float4 dyn[];
   Rec* ring = reinterpret_cast<Rec*>(dyn);
-  int* s_id = reinterpret_cast<int*>(ring + kRing);
-  float* s_basis_all = reinterpret_cast<float*>(s_id + kRing);  // [16][256]
-  float* s_w_all = s_basis_all + 16 * kBatch;                   // [256][4]: SH weights per lane
-  float* s_row = s_w_all + 4 * kBatch;                           // [256][kGCols]: gradient rows (odd stride: no bank conflicts)
+  int* s_id = reinterpret_cast<int*>(ring + RING);
+  float* s_basis_all = reinterpret_cast<float*>(s_id + RING);  // [16][NT]
+  float* s_w_all = s_basis_all + 16 * NT;                     // [NT][4]: SH weights per lane
+  float* s_row = s_w_all + 4 * NT;                            // [NT][kGCols]: gradient rows (odd stride: no bank conflicts)
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   float* s_basis = s_basis_all + threadIdx.x;
   float* s_w = s_w_all + 4 * threadIdx.x;
   __shared__ unsigned s_ddmax;
   __shared__ TileConst tc;
-  const int tile = P.tile_base + blockIdx.x;
+  const int tile = P.tile_base + (NT == 256 ? blockIdx.x : blockIdx.x >> 1);
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
-  const int x = tx * kTile + ((threadIdx.x >> 5) & 1) * 8 + (threadIdx.x & 7),
-            y = ty * kTile + (threadIdx.x >> 6) * 4 + ((threadIdx.x & 31) >> 3);  // 8 x 4 per warp
+  const int half = NT == 256 ? ((threadIdx.x >> 5) & 1) : (int)(blockIdx.x & 1);
+  const int x = tx * kTile + half * 8 + (threadIdx.x & 7),
+            y = ty * kTile + (NT == 256 ? (threadIdx.x >> 6) : (threadIdx.x >> 5)) * 4 + ((threadIdx.x & 31) >> 3);  // 8 x 4 per warp
   bool active = x < P.cam.W && y < P.cam.H;
   if (active && P.pxflag && P.pxflag[(size_t)y * P.cam.W + x]) active = false;  // fp64 backward owns flagged pixels
   if (__syncthreads_count(active) == 0) return;
@@ -349,13 +355,13 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
     for (int t = 0; t < 16; ++t) b[t] = 0.f;
     sh_basis_f(df[0], df[1], df[2], P.opt.sh_degree, b);
 #pragma unroll
-    for (int t = 0; t < 16; ++t) s_basis[t * kBatch] = b[t];
+    for (int t = 0; t < 16; ++t) s_basis[t * NT] = b[t];
   }
   float bas[16];  // this pixel's SH basis, zero beyond the active terms (SH gradient columns)
   {
     const int ta = P.opt.terms_active;
 #pragma unroll
-    for (int t = 0; t < 16; ++t) bas[t] = t < ta ? s_basis[t * kBatch] : 0.f;
+    for (int t = 0; t < 16; ++t) bas[t] = t < ta ? s_basis[t * NT] : 0.f;
   }
   if (threadIdx.x == 0) {
     s_ddmax = 0u;
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
     if (want) {
       Rec R;
       if (pj >= ring_lo) {
-        const int slot = pj & (kRing - 1);
+        const int slot = pj & (RING - 1);
         R = ring[slot];
         id = s_id[slot];
       } else {
@@ -445,7 +451,7 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
         const double a = o.a;
         // colour (geometry.cpp:126-138) with the clamp, upstream scalars (grad.cpp:224-233)
         float c0, c1, c2;
-        sh_colour(P, s_basis, id, c0, c1, c2);
+        sh_colour<NT>(P, s_basis, id, c0, c1, c2);
         const bool cl0 = c0 < 0.f, cl1 = c1 < 0.f, cl2 = c2 < 0.f;
         const float r0 = cl0 ? 0.f : c0, r1 = cl1 ? 0.f : c1, r2 = cl2 ? 0.f : c2;
         const double wb = px.T * a;
@@ -558,28 +564,28 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
     __syncwarp();
   };
 
-  for (long long b0 = beg; b0 < end; b0 += kBatch) {
+  for (long long b0 = beg; b0 < end; b0 += NT) {
     const int jb = (int)(b0 - beg);
     __syncthreads();
     {
       const long long j = b0 + threadIdx.x;
       if (j < end) {
         const int id = P.lid[j];
-        const int slot = (jb + threadIdx.x) & (kRing - 1);
+        const int slot = (jb + threadIdx.x) & (RING - 1);
         stage_record(P, id, tc, ring[slot]);
         s_id[slot] = id;
       }
     }
     __syncthreads();
-    ring_lo = jb >= kBatch ? jb - kBatch : 0;
-    const int cnt = (int)min((long long)kBatch, end - b0);
+    ring_lo = jb >= NT ? jb - NT : 0;
+    const int cnt = (int)min((long long)NT, end - b0);
     if (__any_sync(FULL, !done)) {
       for (int c = 0; c < cnt; ++c) {
         bool want = false;
         int pj = 0;
         if (!done) {
           const int jr = jb + c;
-          const int slot = jr & (kRing - 1);
+          const int slot = jr & (RING - 1);
           const float4 r0 = ring[slot].r0;
           const float2 r3 = *reinterpret_cast<const float2*>(&ring[slot].r3);
           const float dz = lin3(r0, ring[slot].r5.x, px.ddx, px.ddy, px.ddz);
@@ -626,7 +632,7 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
                     le[q] = true;
                   } else if (!(clo[q] > hi)) {
                     double rq = 0;
-                    exact_rt(P, entry_id(P, s_id, beg, cj[q], ring_lo), x, y, &rq);
+                    exact_rt(P, entry_id<RING>(P, s_id, beg, cj[q], ring_lo), x, y, &rq);
                     le[q] = rq <= rin;
                     clo[q] = __double2float_rd(rq);
                     chi[q] = __double2float_ru(rq);
@@ -697,18 +703,24 @@ __global__ void __launch_bounds__(256, DRK_BWDF_MINB) k_raster_bwd_fast(const __
   }
 }
 
-size_t raster_bwd_fast_smem() {
-  return (size_t)kRing * (sizeof(Rec) + sizeof(int)) + (16 + 4 + kGCols) * kBatch * sizeof(float);
+size_t raster_bwd_fast_smem(int nt) {
+  return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + (16 + 4 + kGCols) * nt * sizeof(float);
+}
+
+template <int NT>
+static void launch_bwd_nt(const RasterParams& P, int n_tiles, cudaStream_t s) {
+  const size_t smem = raster_bwd_fast_smem(NT);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_raster_bwd_fast<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_raster_bwd_fast<NT><<<n_tiles * (256 / NT), NT, smem, s>>>(P);
 }
 
 void launch_raster_bwd_fast(const RasterParams& P, int n_tiles, cudaStream_t s) {
-  const size_t smem = raster_bwd_fast_smem();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_raster_bwd_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  k_raster_bwd_fast<<<n_tiles, 256, smem, s>>>(P);
+  if (P.fast_nt == 128) launch_bwd_nt<128>(P, n_tiles, s);
+  else launch_bwd_nt<256>(P, n_tiles, s);
 }
 
 }  // namespace drk

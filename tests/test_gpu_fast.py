@@ -192,13 +192,20 @@ def test_half_tile_ctas_bit_identical(rast):
     cam = scenes.look_at_camera(300, 170, (0.3, 0.2, -3.2))
     raw = torch.from_numpy(sc.f32()).cuda()
     out = {}
+    from paper_2412_11752_b200.api import FrameGrad
+    dcol = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, (cam.height, cam.width, 3)).astype(np.float32))
+    grads = {}
     for rk in (7, 6):
         fb = rast.render(raw, cam, RenderOptions(sh_degree=3, raster_kernel=rk))
         out[rk] = [t.clone() for t in (fb.color, fb.depth, fb.normal, fb.alpha)]
         st = rast.stats()
         out[rk].append(st["streamed"]), out[rk].append(st["composited"])
+        grads[rk] = rast.backward_render(raw, FrameGrad(d_color=dcol.cuda())).raw.clone()
         host = rast.render_host(sc.f32(), cam, RenderOptions(sh_degree=3, raster_kernel=rk))
         assert np.array_equal(host["color"], out[rk][0].cpu().numpy())
     for a, b in zip(out[7][:4], out[6][:4]):
         assert torch.equal(a, b)
     assert out[7][4:] == out[6][4:]
+    # backward with the same CTA shape: equal up to the order of the f32 atomics
+    rel = float((grads[7] - grads[6]).norm() / grads[7].norm())
+    assert rel < 1e-5, rel
