@@ -565,6 +565,14 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   long long n_pairs_total = 0;
   float band_ms[4] = {0, 0, 0, 0};
   const int nb = (int)c->bands.size() - 1;
+  // banded frames keep each band's sorted lists for the backward while free
+  // memory stays above a quarter of the device (the next band's binning reuses
+  // the pair buffers, so this only needs room for the ids and offsets)
+  c->band_cache_valid = nb > 1 && opt->record_replay == 0;
+  if (c->band_cache_valid) {
+    c->band_ids.resize(nb);
+    c->band_off.resize(nb);
+  }
   for (int b = 0; b < nb; ++b) {
     const int ty_lo = c->bands[b], ty_hi = c->bands[b + 1];
     mark(c, 2);
@@ -572,6 +580,26 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     if (int st = bin_band(c, ty_lo, ty_hi, &n_pairs)) return st;
     ht.at("bin");
     n_pairs_total += n_pairs;
+    if (c->band_cache_valid) {
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      const size_t need = sizeof(int) * (size_t)(n_pairs + 1) + sizeof(long long) * (size_t)(n_tiles + 1);
+      const size_t have = c->band_ids[b].bytes + c->band_off[b].bytes;
+      int* ids = nullptr;
+      long long* offs = nullptr;
+      if (free_b + have > need + total_b / 4) {
+        ids = ensure<int>(c->band_ids[b], (size_t)n_pairs + 1);
+        offs = ensure<long long>(c->band_off[b], (size_t)n_tiles + 1);
+      }
+      if (ids && offs) {
+        cudaMemcpyAsync(ids, c->pv.p, sizeof(int) * (size_t)n_pairs, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(offs, c->tileoff.p, sizeof(long long) * (size_t)(n_tiles + 1), cudaMemcpyDeviceToDevice, s);
+      } else {
+        c->band_cache_valid = false;
+        for (auto& d : c->band_ids) release(d);
+        for (auto& d : c->band_off) release(d);
+      }
+    }
     RasterParams P = raster_params(c);
     P.pxflag = pxflag;
     P.pxstop = pxstop;
@@ -678,8 +706,15 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
     for (int b = 0; b < nb; ++b) {
       const int ty_lo = c->bands[b], ty_hi = c->bands[b + 1];
       long long np = 0;
-      if (int st = bin_band(c, ty_lo, ty_hi, &np)) return st;
+      const bool cached = c->band_cache_valid && (int)c->band_ids.size() == nb;
+      if (!cached) {
+        if (int st = bin_band(c, ty_lo, ty_hi, &np)) return st;
+      }
       RasterParams Q = raster_params(c);
+      if (cached) {  // the forward's sorted lists of this band
+        Q.lid = static_cast<const int*>(c->band_ids[b].p);
+        Q.tileoff = static_cast<const long long*>(c->band_off[b].p);
+      }
       Q.pxstate = P.pxstate;
       Q.pxflag = P.pxflag;
       Q.pxstop = P.pxstop;

@@ -131,6 +131,10 @@ struct drk_ctx {
   int64_t hull_cap = 0;
   drk::DevBuf rowest;
   std::vector<int> bands;         // tile-row band boundaries of the last forward
+  // banded frames: each band's sorted tile lists (ids + tile offsets) kept from
+  // the forward so the backward need not re-bin (when device memory allows)
+  std::vector<drk::DevBuf> band_ids, band_off;
+  bool band_cache_valid = false;
   long long band_pair_limit = 0;  // test hook: force bands above this many pairs (0 = memory-based)
   size_t device_bytes = 0;        // cudaMemGetInfo total, queried once
   int64_t pts_cap = 0;
