@@ -1348,8 +1348,15 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const unsigned total = *P.redo_count;
-  const unsigned nwarps = gridDim.x * (blockDim.x / 32);
-  for (unsigned t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); t < total; t += nwarps) {
+  // pixels are fetched dynamically (P.redo_count[1] is the fetch counter, zeroed
+  // at launch): a warp that drew a long tile list does not hold back a fixed
+  // stride of further pixels
+  unsigned* fetch = P.redo_count + 1;
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(fetch, 1u);
+    t = __shfl_sync(FULL, t, 0);
+    if (t >= total) break;
     const int pix = P.redo_list[t];
     const int x = pix % P.cam.W, y = pix / P.cam.W;
     const int tile = (y / kTile) * P.cam.tiles_x + (x / kTile);
@@ -1652,6 +1659,7 @@ void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s,
   // flagged pixels (CTAs without flagged pixels exit immediately).
   // warp per pixel: 148 SMs x 8 CTAs x 4 warps, grid-stride over the list
   const int redo_blocks = 148 * 8;
+  cudaMemsetAsync(P.redo_count + 1, 0, sizeof(unsigned), s);  // k_raster_pixels_warp's fetch counter
   if (P.opt.fp64_alpha) {
     // reference-precision mode: every pixel through the fp64 per-pixel path
     const unsigned npx = (unsigned)P.cam.W * P.cam.H;
