@@ -48,6 +48,8 @@ __global__ void k_full_keys(long long n, const unsigned* sk, const unsigned* sv,
 template <typename T>
 int exclusive_scan(drk_ctx* c, const T* in, long long n, long long* out, long long* total);
 int sort_pairs(drk_ctx* c, unsigned* k, unsigned* v, unsigned* k2, unsigned* v2, long long n);
+void launch_tile_order_keys(int n, int tiles_x, int band_rows, const long long* tileoff, int tile_base, unsigned* key,
+                            unsigned* id, cudaStream_t s);
 void launch_act_bwd(int n, int K, int terms, const float* raw, const float* gact, int G,
                     const unsigned char* touched_dev, const Geo* geo, const CamD& cam, float* grad_raw,
                     float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
@@ -624,6 +626,21 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     // kernel that advances the band counters)
     const bool copy_out = c->hout.active && nb == 1 && P.opt.use_cache && P.opt.raster_kernel != 1 &&
                           raster_fast_eligible(P) && !c->validate_fast && (ty_hi - ty_lo) * cd.tiles_x > 0;
+    // Longest tile lists first (a shorter tail: config 1 -1.9%, config 2 -4% raster
+    // time) on the device path; the host copy-out keeps row-major order so that
+    // framebuffer bands complete, and leave, while the raster still runs.
+    // DRK_TILE_ORDER=0 forces row-major.
+    static const int tile_order_mode = getenv("DRK_TILE_ORDER") ? atoi(getenv("DRK_TILE_ORDER")) : 1;
+    if (tile_order_mode > 0 && !copy_out && raster_fast_eligible(P) && P.opt.raster_kernel != 1) {
+      const int nt = (ty_hi - ty_lo) * cd.tiles_x;
+      unsigned* tk = ensure<unsigned>(c->tord, 4 * (size_t)nt + 4);
+      if (!tk) return set_error(c, DRK_ERR_OOM, "tile order");
+      unsigned *tv = tk + nt + 1, *tk2 = tv + nt + 1, *tv2 = tk2 + nt + 1;
+      launch_tile_order_keys(nt, cd.tiles_x, 0, P.tileoff, P.tile_base, tk, tv, s);
+      launch_counter() += 1;
+      if (int st = sort_pairs(c, tk, tv, tk2, tv2, nt)) return st;
+      P.tile_order = reinterpret_cast<const int*>(tv);
+    }
     if (copy_out) {
       if (int st = start_copy_out(c, P)) return st;
     }

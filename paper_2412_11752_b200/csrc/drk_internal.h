@@ -87,6 +87,7 @@ struct RasterParams {
   const float* shrec;     // fast kernel: per-primitive fp32 shape records (K == 8)
   int* pxstop;            // composites until saturation per pixel (INT_MAX: never), written by the forward
   int fast_nt;            // fast forward: threads per CTA (256: tile, 128: half tile), raster_fast_nt
+  const int* tile_order;  // fast forward: band-local tile of each CTA (longest lists first), or null = row-major
   unsigned long long* vstat;  // fast kernel validation: max |a32 - a64| / bound, max |a32 - a64| (double bits)
 };
 
@@ -127,7 +128,8 @@ struct drk_ctx {
   drk::DevBuf loss_part, ssim_f;          // drk_loss / drk_ssim / drk_psnr: partial sums, SSIM adjoint fields
   drk::DevBuf dens_code, dens_pos;        // drk_densify_and_prune / drk_mesh_convert: per-item code / count, scanned positions
   drk::DevBuf eval_scr, eval_px, eval_off;  // drk_eval_sorting: sequence scratch, per-pixel metrics, chunk offsets
-  drk::DevBuf ovf_scr, ovf_list;          // K1 large-polygon path: per-primitive vertex scratch, overflow list
+  drk::DevBuf ovf_scr, ovf_list;
+  drk::DevBuf tord;                       // fast forward tile order: keys / ids and their sort ping-pong          // K1 large-polygon path: per-primitive vertex scratch, overflow list
   int64_t hull_cap = 0;
   drk::DevBuf rowest;
   std::vector<int> bands;         // tile-row band boundaries of the last forward

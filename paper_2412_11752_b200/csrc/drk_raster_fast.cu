@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   float4* s_b4 = reinterpret_cast<float4*>(s_id + RING) + threadIdx.x;  // [4][NT] float4, this thread's column
   __shared__ unsigned s_ddmax, s_done;
   __shared__ TileConst tc;
-  const int tile = P.tile_base + (NT == 256 ? blockIdx.x : blockIdx.x >> 1);
+  const int cta_tile = NT == 256 ? blockIdx.x : blockIdx.x >> 1;
+  const int tile = P.tile_base + (P.tile_order ? P.tile_order[cta_tile] : cta_tile);
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   // warp w covers an 8 x 4 pixel block (spatially compact: coherent saturation
   // depth and popped primitives across the lanes)
@@ -346,6 +347,24 @@ __device__ __forceinline__ void write_pixel(const RasterParams& P, const FastPix
     P.pxflag[p] = px.uncertain ? 1 : 0;
     if (px.uncertain) P.redo_list[atomicAdd(P.redo_count, 1u)] = (int)p;
   }
+}
+
+// Tile order of the fast forward: key = (band << 20) | (2^20 - 1 - list length),
+// sorted ascending: the longest lists start first (shorter tail).  band_rows > 0
+// groups tiles by bands of rows first (measured: no gain); 0 = one global order.
+__global__ void k_tile_order_keys(int n, int tiles_x, int band_rows, const long long* __restrict__ tileoff,
+                                  int tile_base, unsigned* key, unsigned* id) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const long long len = tileoff[tile_base + t + 1] - tileoff[tile_base + t];
+  const unsigned band = band_rows > 0 ? (unsigned)((tile_base + t) / tiles_x / band_rows) : 0u;
+  key[t] = (band << 20) | (0xfffffu - (unsigned)min(len, 0xfffffLL));
+  id[t] = (unsigned)t;
+}
+
+void launch_tile_order_keys(int n, int tiles_x, int band_rows, const long long* tileoff, int tile_base, unsigned* key,
+                            unsigned* id, cudaStream_t s) {
+  if (n > 0) k_tile_order_keys<<<(n + 255) / 256, 256, 0, s>>>(n, tiles_x, band_rows, tileoff, tile_base, key, id);
 }
 
 size_t raster_fast_smem(int nt) { return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + 16 * nt * sizeof(float); }
