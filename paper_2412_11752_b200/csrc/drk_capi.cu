@@ -716,6 +716,17 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
     if (nb > 1) return set_error(c, DRK_ERR_UNSUPPORTED, "deterministic backward of a banded frame");
     launch_backward_serial(P, s);  // fixed accumulation order, small images
   } else if (nb <= 1) {
+    // longest tile lists first, as in the forward
+    static const int tile_order_mode = getenv("DRK_TILE_ORDER") ? atoi(getenv("DRK_TILE_ORDER")) : 1;
+    if (tile_order_mode > 0 && n_tiles > 0) {
+      unsigned* tk = ensure<unsigned>(c->tord, 4 * (size_t)n_tiles + 4);
+      if (!tk) return set_error(c, DRK_ERR_OOM, "tile order");
+      unsigned *tv = tk + n_tiles + 1, *tk2 = tv + n_tiles + 1, *tv2 = tk2 + n_tiles + 1;
+      launch_tile_order_keys(n_tiles, c->camd.tiles_x, 0, P.tileoff, 0, tk, tv, s);
+      launch_counter() += 1;
+      if (int st = sort_pairs(c, tk, tv, tk2, tv2, n_tiles)) return st;
+      P.tile_order = reinterpret_cast<const int*>(tv);
+    }
     launch_raster(P, n_tiles, true, s);
   } else {
     // banded frame: re-bin each band, then its backward raster and the fp64

@@ -330,7 +330,8 @@ __global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fas
   float* s_w = s_w_all + 4 * threadIdx.x;
   __shared__ unsigned s_ddmax;
   __shared__ TileConst tc;
-  const int tile = P.tile_base + (NT == 256 ? blockIdx.x : blockIdx.x >> 1);
+  const int cta_tile = NT == 256 ? blockIdx.x : blockIdx.x >> 1;
+  const int tile = P.tile_base + (P.tile_order ? P.tile_order[cta_tile] : cta_tile);
   const int tx = tile % P.cam.tiles_x, ty = tile / P.cam.tiles_x;
   const int half = NT == 256 ? ((threadIdx.x >> 5) & 1) : (int)(blockIdx.x & 1);
   const int x = tx * kTile + half * 8 + (threadIdx.x & 7),
