@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--no-fwd-bwd", action="store_true")
     ap.add_argument("--multiview-views", type=int, default=16,
                     help="config 3 leg: orbit views per step, split across ranks (0 = skip)")
-    ap.add_argument("--multiview-inflight", type=int, default=2,
+    ap.add_argument("--multiview-inflight", type=int, default=1,
                     help="config 3 leg: rasterizer contexts in flight per GPU (own stream + host thread each)")
     ap.add_argument("--config4-train", action="store_true",
                     help="also time one full config-4 training step (4M DRK, 8 views of 3840x2160 per GPU; ~1 min)")
@@ -368,8 +368,8 @@ def main():
                      "views_on_rank0": len(mine), "inflight_contexts": args.multiview_inflight,
                      "workload": f"config3: 1M DRK, K=8, SH3, {len(cams3)} of the 64 seeded orbit views at 1920x1080 "
                                  "per step, views split across ranks (replicated primitives, no data-path collective); "
-                                 "on each GPU the views stream through in-flight rasterizer contexts (own CUDA stream "
-                                 "and host thread each); max over ranks"}
+                                 "on each GPU the primitives are activated once per step and the views stream through "
+                                 "MultiViewRenderer (in-flight contexts: --multiview-inflight); max over ranks"}
         mvr.close()
         del raw3
 

@@ -176,6 +176,12 @@ int drk_activate(drk_ctx* ctx, const float* raw, int n, int k, int sh_terms, drk
 int drk_forward(drk_ctx* ctx, const float* raw, int n, int k, int sh_terms,
                 const drk_camera* cam, const drk_options* opt, float* color, float* depth,
                 float* normal, float* alpha);
+/* Renders the primitives of the last drk_forward / drk_forward_prims on this
+ * context (activation and shape constants kept) from another camera / options:
+ * a multi-view batch activates once.  The caller's parameters must not have
+ * changed since (call drk_forward again after an update). */
+int drk_forward_again(drk_ctx* ctx, const drk_camera* cam, const drk_options* opt, float* color, float* depth,
+                      float* normal, float* alpha);
 /* From activated primitives (the reference's std::vector<DrkPrimitive> input). */
 int drk_forward_prims(drk_ctx* ctx, const drk_prims* prims, int n, int k, int sh_terms,
                       const drk_camera* cam, const drk_options* opt, float* color,

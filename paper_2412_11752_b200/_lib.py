@@ -144,6 +144,7 @@ SIGNATURES = {
     "drk_activate": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(Prims_)]),
     "drk_forward": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(Camera_), C.POINTER(Options_),
                               _P, _P, _P, _P]),
+    "drk_forward_again": (C.c_int, [_P, C.POINTER(Camera_), C.POINTER(Options_), _P, _P, _P, _P]),
     "drk_forward_prims": (C.c_int, [_P, C.POINTER(Prims_), C.c_int, C.c_int, C.c_int, C.POINTER(Camera_),
                                     C.POINTER(Options_), _P, _P, _P, _P]),
     "drk_forward_host": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(Camera_), C.POINTER(Options_),

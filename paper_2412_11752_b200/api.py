@@ -271,6 +271,26 @@ class Rasterizer:
         self._shape = (n, k, terms, H, W)
         return fb
 
+    def render_again(self, cam: Camera, opt: RenderOptions = None,
+                     outputs=("color", "depth", "normal", "alpha")) -> FrameBuffers:
+        """drk_forward_again: the primitives of the last render on this rasterizer from another
+        camera, without re-activating them (multi-view batches; the parameters must be unchanged)."""
+        if self._shape is None:
+            raise DrkError("render_again without a previous render on this rasterizer")
+        opt = opt or RenderOptions()
+        n, k, terms, _, _ = self._shape
+        H, W = cam.height, cam.width
+        kw = dict(device=self.device, dtype=torch.float32)
+        fb = FrameBuffers(torch.empty(H, W, 3, **kw) if "color" in outputs else None,
+                          torch.empty(H, W, **kw) if "depth" in outputs else None,
+                          torch.empty(H, W, 3, **kw) if "normal" in outputs else None,
+                          torch.empty(H, W, **kw) if "alpha" in outputs else None, tuple(opt.background))
+        self._sync_stream()
+        self._check(_lib.lib().drk_forward_again(self._h, C.byref(_camera(cam)), C.byref(_options(opt)),
+                                                 _ptr(fb.color), _ptr(fb.depth), _ptr(fb.normal), _ptr(fb.alpha)))
+        self._shape = (n, k, terms, H, W)
+        return fb
+
     def render_prims(self, prims: dict, cam: Camera, opt: RenderOptions = None, replay: bool | int = False):
         """drk::render from activated primitives (dict of device tensors: mu [n,3] f64,
         rot [n,3,3] f64, scales/angles [n,K] f64, eta/tau/opacity [n] f64, sh [n,terms,3] f32)."""

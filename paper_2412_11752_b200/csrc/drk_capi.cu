@@ -967,7 +967,20 @@ int drk_forward(drk_ctx* c, const float* raw, int n, int k, int sh_terms, const 
   c->has_fwd = false;
   c->launch_base = launch_counter();
   mark(c, 0);
+  c->has_act = false;
   if (int st = launch_activate(c, raw, n, k, sh_terms)) return st;
+  c->has_act = true;
+  return run_forward(c, cam, opt, color, depth, normal, alpha);
+}
+
+int drk_forward_again(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float* color, float* depth,
+                      float* normal, float* alpha) {
+  if (!c || !cam || !opt) return DRK_ERR_INVALID_ARG;
+  if (!c->has_act) return set_error(c, DRK_ERR_INVALID_ARG, "no activated primitives on this context");
+  cudaSetDevice(c->device);
+  c->has_fwd = false;
+  c->launch_base = launch_counter();
+  mark(c, 0);
   return run_forward(c, cam, opt, color, depth, normal, alpha);
 }
 
@@ -979,7 +992,9 @@ int drk_forward_prims(drk_ctx* c, const drk_prims* prims, int n, int k, int sh_t
   c->has_fwd = false;
   c->launch_base = launch_counter();
   mark(c, 0);
+  c->has_act = false;
   if (int st = launch_shape(c, prims, n, k, sh_terms)) return st;
+  c->has_act = true;
   return run_forward(c, cam, opt, color, depth, normal, alpha);
 }
 

@@ -158,6 +158,7 @@ struct drk_ctx {
 
   // last forward
   bool has_fwd = false;
+  bool has_act = false;  // activated primitives + shape constants of the last drk_forward / drk_forward_prims
   drk_camera cam{};
   drk_options opt{};
   drk::CamD camd{};
