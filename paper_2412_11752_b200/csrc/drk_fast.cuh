@@ -80,6 +80,29 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
   return copysignf(r, y);
 }
 
+#ifndef DRK_PSEUDO_ANGLE
+#define DRK_PSEUDO_ANGLE 1
+#endif
+
+// Pseudo-angle of (x, y): monotone in the polar angle, 0 < p <= 4 for angles in
+// (0, 2 pi] (the angle 0 maps to 4, like atan2's 0 -> 2 pi; (0, 0) -> 4).
+__device__ __forceinline__ float pseudo_angle(float y, float x) {
+  const float s = fabsf(x) + fabsf(y);
+  if (!(s > 0.f)) return 4.f;
+  float p;
+  if (y >= 0.f) p = x >= 0.f ? __fdividef(y, s) : 1.f - __fdividef(x, s);
+  else p = x < 0.f ? 2.f - __fdividef(y, s) : 3.f + __fdividef(x, s);
+  return p <= 0.f ? 4.f : p;
+}
+__host__ __device__ inline double pseudo_angle_d(double y, double x) {
+  const double s = fabs(x) + fabs(y);
+  if (!(s > 0.0)) return 4.0;
+  double p;
+  if (y >= 0.0) p = x >= 0.0 ? y / s : 1.0 - x / s;
+  else p = x < 0.0 ? 2.0 - y / s : 3.0 + x / s;
+  return p <= 0.0 ? 4.0 : p;
+}
+
 // ---------------------------------------------------------------------------
 // Staging (fp64, once per (entry, tile))
 // ---------------------------------------------------------------------------
@@ -278,6 +301,21 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
     }
     // ---- alpha = o Psi(g(u, v)) (core.cpp:148-265) ----
     const float* hd = P.shrec + (size_t)kRecStride * id;
+#if DRK_PSEUDO_ANGLE
+    // bracket from the pseudo-angle (monotone in the polar angle, (0, 4] for
+    // (0, 2 pi]) against the record's pseudo-angles of theta_0..theta_6
+    // (theta_7 = 2 pi <-> 4); misassignment only within ~5e-7 rad of an
+    // endpoint, where the kernel is continuous across brackets (as with the
+    // fp32 atan2 it replaces)
+    const float4 p0 = __ldg(reinterpret_cast<const float4*>(hd) + 4), p1 = __ldg(reinterpret_cast<const float4*>(hd) + 5);
+    const float th = pseudo_angle(v, u);
+    int lo;
+    if (th <= p0.y) {
+      lo = 7;
+    } else {
+      lo = (p0.z < th) + (p0.w < th) + (p1.x < th) + (p1.y < th) + (p1.z < th) + (p1.w < th);
+    }
+#else
     const float4 t0 = __ldg(reinterpret_cast<const float4*>(hd)), t1 = __ldg(reinterpret_cast<const float4*>(hd) + 1);
     float th = atan2_fast(v, u);
     if (th <= 0.f) th += 6.28318530717958647692f;
@@ -287,6 +325,7 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
     } else {
       lo = (t0.y < th) + (t0.z < th) + (t0.w < th) + (t1.x < th) + (t1.y < th) + (t1.z < th);
     }
+#endif
     const float4* bp = reinterpret_cast<const float4*>(hd + kRecHdr + 8 * lo);
     const float4 e = __ldg(bp), f = __ldg(bp + 1);  // (elx, ely, ehx, ehy), (1/det, pi/gap, h_lo, h_hi)
     if (isnan(f.x)) {

@@ -43,6 +43,7 @@ namespace drk {
 //   [8, 12)  sharpen point-slope constants (g1, g2, A0, A1)
 //   [12, 16) (A2, Psi(g1), Psi(g2), opacity)
 //   [16]     eta
+//   [17, 24) pseudo-angles of theta_0..theta_6 (pseudo_angle)
 //   [24 + 8k, 32 + 8k) bracket (k, k+1 mod K): e_lo (x, y), e_hi (x, y),
 //            1/det (NaN when |det| < 1e-12, core.cpp:191), pi/gap, 1/s_lo^2, 1/s_hi^2
 // ---------------------------------------------------------------------------
@@ -58,8 +59,12 @@ __global__ void k_shape_rec(int n, ShapeView S, float* __restrict__ rec) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) r[8 + k] = q[k];
   r[16] = (float)S.eta[i];
+  // [17, 24): pseudo-angles of theta_0..theta_6 (bracket lookup, DRK_PSEUDO_ANGLE)
 #pragma unroll
-  for (int k = 17; k < kRecHdr; ++k) r[k] = 0.f;
+  for (int k = 0; k < 7; ++k) {
+    const double t = S.th[b + k];
+    r[17 + k] = (float)pseudo_angle_d(sin(t), cos(t));
+  }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int h = (k + 1) & 7;
