@@ -205,7 +205,10 @@ def main():
     for _ in range(args.warmup):
         r.render(raw, cam, opt)
     torch.cuda.synchronize(dev)
+    # the warm-up frames ran with the work counters on: they give the roofline's
+    # counts (the frame is deterministic); the timed frames run without them
     stats0 = r.stats()
+    r.set_counters(False)
 
     # ---- device-resident timed region ----
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -234,7 +237,7 @@ def main():
     ms_per_step = tot_ms / args.steps
     px = cam.width * cam.height
     value = world * px / (ms_per_step * 1e-3) / 1e6
-    st = r.stats()
+    st = stats0
 
     # ---- roofline of the dominant kernel (fp32-pass rasterizer) ----
     flops = (px * F_PIXEL[3] + st["streamed"] * F_ISECT + st["popped"] * F_ALPHA + st["composited"] * F_BLEND[3])
@@ -343,6 +346,8 @@ def main():
         mine = shard_views(len(cams3), world, rank)
         my_cams = [cams3[v] for v in mine]
         mvr = MultiViewRenderer(local, inflight=args.multiview_inflight)
+        for rr in mvr.rasts:
+            rr.set_counters(False)
         for _ in range(2):  # warm-up passes over this rank's views (buffers reach their peak sizes)
             mvr.render(raw3, my_cams, opt)
         torch.cuda.synchronize(dev)

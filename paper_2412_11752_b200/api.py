@@ -402,6 +402,10 @@ class Rasterizer:
     def set_timing(self, enabled: bool = True):
         self._check(_lib.lib().drk_set_timing(self._h, int(enabled)))
 
+    def set_counters(self, enabled: bool = True):
+        """drk_set_counters: the fast forward's work counters on (default) or compiled out."""
+        self._check(_lib.lib().drk_set_counters(self._h, int(enabled)))
+
     def set_band_limit(self, pairs: int):
         """Force banded binning above `pairs` tile pairs per band (0 = by free device memory)."""
         self._check(_lib.lib().drk_set_band_limit(self._h, int(pairs)))

@@ -163,6 +163,7 @@ static RasterParams raster_params(drk_ctx* c) {
   P.shrec = A.rec;
   P.frame32 = static_cast<const float4*>(c->frame32.p);
   P.fast_nt = 256;
+  P.no_counters = c->work_counters ? 0 : 1;
   return P;
 }
 
@@ -1054,6 +1055,12 @@ int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_ter
   if (normal_host) cudaMemcpyAsync(normal_host, dnor, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, c->stream);
   if (alpha_host) cudaMemcpyAsync(alpha_host, dalp, sizeof(float) * npix, cudaMemcpyDeviceToHost, c->stream);
   return cuda_check(c, cudaStreamSynchronize(c->stream), "forward_host");
+}
+
+int drk_set_counters(drk_ctx* c, int enabled) {
+  if (!c) return DRK_ERR_INVALID_ARG;
+  c->work_counters = enabled != 0;
+  return DRK_OK;
 }
 
 int drk_set_band_limit(drk_ctx* c, int64_t pairs) {

@@ -9,14 +9,12 @@
 namespace drk {
 
 
-// DRK_STATS=0 compiles the per-pixel work counters out of the fast kernels
-// (development A/B; the product keeps them for the roofline's counts)
-#ifndef DRK_STATS
-#define DRK_STATS 1
-#endif
+// Per-pixel work counters of the fast kernels: compiled in where the template
+// parameter STATS is true (drk_set_counters; the roofline's counts), out of
+// the timed path otherwise (1.6% of the raster).
 #define DRK_STAT(x) \
   do {              \
-    if (DRK_STATS) ++(x); \
+    if (STATS) ++(x); \
   } while (0)
 
 constexpr int kRing = 512;
@@ -257,7 +255,7 @@ struct GradF {
   KEvalF k;
 };
 
-template <bool VALIDATE, bool GRAD = false>
+template <bool VALIDATE, bool GRAD = false, bool STATS = true>
 __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px, const Rec& R, int id, int x, int y,
                                             AlphaOut& out, GradF* gf = nullptr, Pop64* o64 = nullptr) {
   out.skip = false;
@@ -553,7 +551,7 @@ __device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, cons
   return true;
 }
 
-template <bool VALIDATE, int NT = kBatch>
+template <bool VALIDATE, int NT = kBatch, bool STATS = true>
 __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, const float4* s_b4, const Rec* ring,
                                          const int* s_id, const TileConst& tc, long long beg, int ring_lo, int jr,
                                          int x, int y) {
@@ -570,7 +568,7 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
     DRK_STAT(px.n_miss);
   }
   AlphaOut o;
-  alpha_entry<VALIDATE>(P, px, R, id, x, y, o);
+  alpha_entry<VALIDATE, false, STATS>(P, px, R, id, x, y, o);
   if (o.degen) {
     px.err = true;
     return false;

@@ -87,6 +87,7 @@ struct RasterParams {
   const float* shrec;     // fast kernel: per-primitive fp32 shape records (K == 8)
   int* pxstop;            // composites until saturation per pixel (INT_MAX: never), written by the forward
   int fast_nt;            // fast forward: threads per CTA (256: tile, 128: half tile), raster_fast_nt
+  int no_counters;        // fast forward: work counters compiled out (drk_set_counters(ctx, 0))
   const int* tile_order;  // fast forward: band-local tile of each CTA (longest lists first), or null = row-major
   unsigned long long* vstat;  // fast kernel validation: max |a32 - a64| / bound, max |a32 - a64| (double bits)
 };
@@ -158,7 +159,8 @@ struct drk_ctx {
 
   // last forward
   bool has_fwd = false;
-  bool has_act = false;  // activated primitives + shape constants of the last drk_forward / drk_forward_prims
+  bool has_act = false;
+  bool work_counters = true;  // fast forward work counters (streamed / popped / rejects) on  // activated primitives + shape constants of the last drk_forward / drk_forward_prims
   drk_camera cam{};
   drk_options opt{};
   drk::CamD camd{};

@@ -93,7 +93,7 @@ __device__ __forceinline__ void write_pixel(const RasterParams& P, const FastPix
 // NT threads per CTA: 256 = one 16x16 tile per CTA; 128 = half a tile (8 x 16
 // pixels) per CTA with the tile list staged by both halves — finer-grained
 // release of SM resources when a tile's pixels saturate unevenly (long lists).
-template <bool VALIDATE, int NT>
+template <bool VALIDATE, int NT, bool STATS>
 __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_constant__ RasterParams P) {
   constexpr int RING = 2 * NT;
   extern __shared__ float4 dyn[];
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
             }
           }
         }
-        if (!pop_eval<VALIDATE, NT>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y)) {
+        if (!pop_eval<VALIDATE, NT, STATS>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y)) {
           done = true;
           break;
         }
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
       cj[q] = cj[q + 1];
     }
     --csz;
-    if (!pop_eval<VALIDATE, NT>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y))
+    if (!pop_eval<VALIDATE, NT, STATS>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y))
       done = true;
   }
   // counters: one atomic per warp and counter
@@ -390,13 +390,15 @@ static void launch_nt(const RasterParams& P, int n_tiles, bool validate, cudaStr
   const size_t smem = raster_fast_smem(NT);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_raster_fast<false, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_raster_fast<true, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_raster_fast<false, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_raster_fast<false, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_raster_fast<true, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const int ctas = n_tiles * (256 / NT);
-  if (validate) k_raster_fast<true, NT><<<ctas, NT, smem, s>>>(P);
-  else k_raster_fast<false, NT><<<ctas, NT, smem, s>>>(P);
+  if (validate) k_raster_fast<true, NT, true><<<ctas, NT, smem, s>>>(P);
+  else if (P.no_counters) k_raster_fast<false, NT, false><<<ctas, NT, smem, s>>>(P);
+  else k_raster_fast<false, NT, true><<<ctas, NT, smem, s>>>(P);
 }
 
 // 128 registers per thread either way: 2 CTAs of 256 or 4 CTAs of 128 per SM

@@ -209,3 +209,21 @@ def test_half_tile_ctas_bit_identical(rast):
     # backward with the same CTA shape: equal up to the order of the f32 atomics
     rel = float((grads[7] - grads[6]).norm() / grads[7].norm())
     assert rel < 1e-5, rel
+
+
+@pytest.mark.gpu
+def test_counters_off_same_frame(rast):
+    """drk_set_counters(0) launches the counter-free fast kernel: same frame, zero work counts."""
+    from paper_2412_11752_b200.api import RenderOptions
+    sc = scenes.random_scene(5000, seed=31, sh_degree=3, clusters=6)
+    cam = scenes.look_at_camera(160, 112, (0.2, -0.3, -3.4))
+    raw = torch.from_numpy(sc.f32()).cuda()
+    a = rast.render(raw, cam, RenderOptions(sh_degree=3)).color.clone()
+    assert rast.stats()["popped"] > 0
+    try:
+        rast.set_counters(False)
+        b = rast.render(raw, cam, RenderOptions(sh_degree=3)).color
+        assert rast.stats()["popped"] == 0
+    finally:
+        rast.set_counters(True)
+    assert torch.equal(a, b)
