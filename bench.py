@@ -202,6 +202,7 @@ def main():
         if world > 1:
             dist.barrier()
 
+    r.set_counters(True)
     for _ in range(args.warmup):
         r.render(raw, cam, opt)
     torch.cuda.synchronize(dev)

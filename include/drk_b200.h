@@ -154,8 +154,8 @@ int drk_set_timing(drk_ctx* ctx, int enabled);
  * force bands above `pairs` pairs per band (0 = memory-based). */
 int drk_set_band_limit(drk_ctx* ctx, int64_t pairs);
 /* Work counters of the fast forward (drk_stats streamed / popped / reject
- * counts): on by default; off compiles them out of the kernel launched (about
- * 1.6% of the raster time) and leaves those fields 0. */
+ * counts): off by default (the counter-free kernel is launched, those fields
+ * stay 0); on launches the counting instantiation (about 1.6% slower). */
 int drk_set_counters(drk_ctx* ctx, int enabled);
 int drk_get_bands(const drk_ctx* ctx, int32_t* n_bands);
 /* Validation of the fast forward kernel: while enabled, every fp32 alpha is
@@ -180,8 +180,8 @@ int drk_activate(drk_ctx* ctx, const float* raw, int n, int k, int sh_terms, drk
 int drk_forward(drk_ctx* ctx, const float* raw, int n, int k, int sh_terms,
                 const drk_camera* cam, const drk_options* opt, float* color, float* depth,
                 float* normal, float* alpha);
-/* Renders the primitives of the last drk_forward / drk_forward_prims on this
- * context (activation and shape constants kept) from another camera / options:
+/* Renders the primitives of the last drk_forward / drk_forward_prims /
+ * drk_activate on this context (activation and shape constants kept) from another camera / options:
  * a multi-view batch activates once.  The caller's parameters must not have
  * changed since (call drk_forward again after an update). */
 int drk_forward_again(drk_ctx* ctx, const drk_camera* cam, const drk_options* opt, float* color, float* depth,

@@ -403,7 +403,7 @@ class Rasterizer:
         self._check(_lib.lib().drk_set_timing(self._h, int(enabled)))
 
     def set_counters(self, enabled: bool = True):
-        """drk_set_counters: the fast forward's work counters on (default) or compiled out."""
+        """drk_set_counters: the fast forward's work counters on, or compiled out (the default)."""
         self._check(_lib.lib().drk_set_counters(self._h, int(enabled)))
 
     def set_band_limit(self, pairs: int):

@@ -485,12 +485,9 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT, s);
     if (n > 0) {
       // warp per primitive; near-clipped / oversized polygons -> overflow list (k_prep1)
-      static bool attr = false;
+      static PerDeviceOnce attr;
       const size_t smem = prep_warp_smem();
-      if (!attr) {
-        cudaFuncSetAttribute(k_prep_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-      }
+      attr([&] { cudaFuncSetAttribute(k_prep_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
       k_prep_warp<<<(n + 7) / 8, 256, smem, s>>>(A, cd, od, geo, bbox, hullref, ppool, c->pts_cap, ptsref, rowcnt,
                                                    ctr, ovf, static_cast<float4*>(c->frame32.p));
       k_prep_hull<<<(unsigned)((2LL * n + 255) / 256), 256, 0, s>>>(n, ptsref, ppool, cd, od, bbox, hullref, pool,
@@ -923,8 +920,11 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
                     &c->counters, &c->scan_tmp, &c->loss_tmp, &c->progress, &c->patch, &c->scene_aos,
                     &c->loss_part, &c->ssim_f, &c->dens_code, &c->dens_pos,
-                    &c->eval_scr, &c->eval_px, &c->eval_off, &c->ovf_scr, &c->ovf_list};
+                    &c->eval_scr, &c->eval_px, &c->eval_off, &c->ovf_scr, &c->ovf_list, &c->tord,
+                    &c->rowest, &c->host_raw, &c->host_img};
   for (DevBuf* b : bufs) release(*b);
+  for (DevBuf& b : c->band_ids) release(b);
+  for (DevBuf& b : c->band_off) release(b);
   for (cudaEvent_t e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -952,7 +952,10 @@ int drk_activate(drk_ctx* c, const float* raw, int n, int k, int sh_terms, drk_p
   if (!c || n < 0 || (n > 0 && !raw)) return DRK_ERR_INVALID_ARG;
   if (k < 3 || k > kMaxK) return set_error(c, DRK_ERR_GENERIC, "K must be at least 3 (and at most 16 here)");
   cudaSetDevice(c->device);
+  c->has_act = false;
+  c->has_fwd = false;
   if (int st = launch_activate(c, raw, n, k, sh_terms)) return st;
+  c->has_act = true;  // drk_forward_again now renders this set
   if (out) {
     const Activated& A = c->act;
     *out = drk_prims{A.mu, A.rot, A.s, A.th, A.eta, A.tau, A.o, A.sh};
@@ -1016,9 +1019,8 @@ int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_ter
   cudaSetDevice(c->device);
   const size_t S = (size_t)drk_scalar_count(k, sh_terms);
   const size_t npix = (size_t)cam->width * cam->height;
-  static thread_local DevBuf raw_d, img_d;
-  float* r = ensure<float>(raw_d, S * n + 1);
-  float* img = ensure<float>(img_d, 8 * npix + 1);
+  float* r = ensure<float>(c->host_raw, S * n + 1);
+  float* img = ensure<float>(c->host_img, 8 * npix + 1);
   if (!r || !img) return set_error(c, DRK_ERR_OOM, "host staging");
   cudaMemcpyAsync(r, raw_host, sizeof(float) * S * n, cudaMemcpyHostToDevice, c->stream);
   float* dcol = color_host ? img : nullptr;

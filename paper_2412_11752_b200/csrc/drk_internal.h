@@ -3,7 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -18,10 +20,25 @@ struct DevBuf {
 };
 
 // Process-wide count of kernels this library has launched (drk_stats.launches).
-inline long long& launch_counter() {
-  static long long n = 0;
+// Atomic: MultiViewRenderer drives several contexts from concurrent host threads.
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> n{0};
   return n;
 }
+
+// Runs a function once per (call site, device), thread-safe.  Function attributes
+// such as cudaFuncAttributeMaxDynamicSharedMemorySize are per device, so a
+// process-wide flag would leave a second GPU without them.
+struct PerDeviceOnce {
+  static constexpr int kMaxDevices = 64;
+  std::once_flag flags[kMaxDevices];
+  template <class F>
+  void operator()(F&& f) {
+    int d = 0;
+    cudaGetDevice(&d);
+    std::call_once(flags[d & (kMaxDevices - 1)], std::forward<F>(f));
+  }
+};
 #define DRK_COUNT_LAUNCH() (++::drk::launch_counter())
 
 // Grow-only device allocation; returns nullptr on OOM.
@@ -130,7 +147,8 @@ struct drk_ctx {
   drk::DevBuf dens_code, dens_pos;        // drk_densify_and_prune / drk_mesh_convert: per-item code / count, scanned positions
   drk::DevBuf eval_scr, eval_px, eval_off;  // drk_eval_sorting: sequence scratch, per-pixel metrics, chunk offsets
   drk::DevBuf ovf_scr, ovf_list;
-  drk::DevBuf tord;                       // fast forward tile order: keys / ids and their sort ping-pong          // K1 large-polygon path: per-primitive vertex scratch, overflow list
+  drk::DevBuf tord;                       // fast forward tile order: keys / ids and their sort ping-pong
+  drk::DevBuf host_raw, host_img;         // drk_forward_host: device staging of the host params / framebuffers
   int64_t hull_cap = 0;
   drk::DevBuf rowest;
   std::vector<int> bands;         // tile-row band boundaries of the last forward
@@ -159,8 +177,8 @@ struct drk_ctx {
 
   // last forward
   bool has_fwd = false;
-  bool has_act = false;
-  bool work_counters = true;  // fast forward work counters (streamed / popped / rejects) on  // activated primitives + shape constants of the last drk_forward / drk_forward_prims
+  bool has_act = false;  // activated primitives + shape constants of the last drk_forward / drk_forward_prims / drk_activate
+  bool work_counters = false;  // fast forward work counters (streamed / popped / rejects); off by default
   drk_camera cam{};
   drk_options opt{};
   drk::CamD camd{};

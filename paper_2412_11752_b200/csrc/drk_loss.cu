@@ -289,12 +289,12 @@ size_t grad_smem() { return sizeof(double) * (3 * kIH * kIW + 3 * kIH * kTW); }
 
 template <typename T>
 void set_smem_attrs() {
-  static bool done = false;
-  if (done) return;
-  cudaFuncSetAttribute(k_ssim_map<true, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_smem());
-  cudaFuncSetAttribute(k_ssim_map<false, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_smem());
-  cudaFuncSetAttribute(k_ssim_grad<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem());
-  done = true;
+  static drk::PerDeviceOnce once;
+  once([] {
+    cudaFuncSetAttribute(k_ssim_map<true, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_smem());
+    cudaFuncSetAttribute(k_ssim_map<false, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)map_smem());
+    cudaFuncSetAttribute(k_ssim_grad<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem());
+  });
 }
 
 }  // namespace

@@ -716,11 +716,8 @@ size_t raster_bwd_fast_smem(int nt) {
 template <int NT>
 static void launch_bwd_nt(const RasterParams& P, int n_tiles, cudaStream_t s) {
   const size_t smem = raster_bwd_fast_smem(NT);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_raster_bwd_fast<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  static PerDeviceOnce attr;
+  attr([&] { cudaFuncSetAttribute(k_raster_bwd_fast<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
   k_raster_bwd_fast<NT><<<n_tiles * (256 / NT), NT, smem, s>>>(P);
 }
 

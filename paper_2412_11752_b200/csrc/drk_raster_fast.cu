@@ -388,13 +388,12 @@ bool raster_fast_eligible(const RasterParams& P) {
 template <int NT>
 static void launch_nt(const RasterParams& P, int n_tiles, bool validate, cudaStream_t s) {
   const size_t smem = raster_fast_smem(NT);
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr([&] {
     cudaFuncSetAttribute(k_raster_fast<false, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_raster_fast<false, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_raster_fast<true, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  });
   const int ctas = n_tiles * (256 / NT);
   if (validate) k_raster_fast<true, NT, true><<<ctas, NT, smem, s>>>(P);
   else if (P.no_counters) k_raster_fast<false, NT, false><<<ctas, NT, smem, s>>>(P);

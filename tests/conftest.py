@@ -20,5 +20,6 @@ def rast():
         pytest.skip("no CUDA device")
     from paper_2412_11752_b200.api import Rasterizer
     r = Rasterizer(0)
+    r.set_counters(True)  # the parity tests read the work counters (off by default)
     yield r
     r.close()
