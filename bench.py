@@ -41,6 +41,11 @@ F_PIXEL = {0: 34, 3: 82}
 F_ISECT = 22
 F_ALPHA = 37
 F_BLEND = {0: 30, 3: 120}
+# Backward, per composited record (grad.cpp:224-301 with backward_alpha
+# grad.cpp:16-101, FMA = 2, transcendentals excluded): upstream
+# scalar cw 18, rest / dL/dalpha 7, SH 3 + 96 (deg 3) / 3 + 6 (deg 0), normal 6,
+# depth 28, backward_alpha 117, (u, v) chain to centre / rotation 57.
+F_BWD_RECORD = {0: 240, 3: 330}
 
 
 def parse():
@@ -50,16 +55,35 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-crop", default="960x544", help="crop of the CPU baseline sample (tile aligned)")
+    ap.add_argument("--cpu-crop-bwd", default="320x256", help="crop of the CPU fwd+bwd sample (config 2, tile aligned)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fwd-bwd", action="store_true")
-    ap.add_argument("--multiview-views", type=int, default=16,
+    ap.add_argument("--multiview-views", type=int, default=64,
                     help="config 3 leg: orbit views per step, split across ranks (0 = skip)")
     ap.add_argument("--multiview-inflight", type=int, default=1,
                     help="config 3 leg: rasterizer contexts in flight per GPU (own stream + host thread each)")
-    ap.add_argument("--config4-train", action="store_true",
-                    help="also time one full config-4 training step (4M DRK, 8 views of 3840x2160 per GPU; ~1 min)")
+    ap.add_argument("--no-config4-train", action="store_true",
+                    help="skip the config-4 training step (4M DRK, 8 views of 3840x2160 per GPU; ~1 min)")
+    ap.add_argument("--no-adapter", action="store_true", help="skip the drop-in adapter leg (drk::render / "
+                    "drk::backward_render through oracle/_ref/adapter_bench)")
     ap.add_argument("--no-train", action="store_true", help="skip the multi-GPU training-step leg")
     return ap.parse_args()
+
+
+def maybe_spawn(args) -> None:
+    """`bench.py --gpus N` outside torchrun: re-launch under torch.distributed.run
+    with N ranks (one per GPU, rendezvous on 127.0.0.1); the driver's own torchrun
+    launch sets WORLD_SIZE and runs the ranks directly."""
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1:
+        return
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
 
 
 def dist_env():
@@ -145,6 +169,66 @@ def reference_cpu_sample(crop: str, steps: int = 1):
                        f"{steps} run(s), {t:.2f} s each"), t
 
 
+def reference_cpu_fwd_bwd(crop: str):
+    """Reference CPU training-step span on a centred crop of config 2: activate + render(&replay)
+    + L1 loss + backward_render (oracle/_ref ref_fwd_bwd), all host threads."""
+    from oracle import ref
+    from paper_2412_11752_b200 import scenes
+    w, h = (int(x) for x in crop.split("x"))
+    sc = scenes.config_scene(2)
+    cam0 = scenes.config_cameras(2)[0]
+    cam = cam0.crop((cam0.width // 2 - w // 2) // 16 * 16, (cam0.height // 2 - h // 2) // 16 * 16, w, h)
+    out = ref.fwd_bwd(sc, cam, scenes.config_target(2, cam), ref.Options(sh_degree=3, threads=0))
+    t = out["seconds_fwd"] + out["seconds_bwd"]
+    threads = ref.hardware_threads()
+    return dict(value=w * h / t / 1e6, unit="megapixels/s", cores=threads, kind="reference",
+                seconds_fwd=out["seconds_fwd"], seconds_loss_bwd=out["seconds_bwd"],
+                sample=f"config 2 (300k DRK, SH3) centred {w}x{h} crop of the 1280x720 view; reference activate + "
+                       f"render(&replay) + L1 loss + backward_render (oracle/_ref, unmodified sources) with "
+                       f"threads=0 ({threads} threads); bin_primitives (single-threaded) still processes all "
+                       f"primitives; {t:.2f} s")
+
+
+def adapter_leg(warm: int = 1, steps: int = 3):
+    """drk::render / drk::loss / drk::backward_render through the drop-in adapter
+    (oracle/_ref/adapter_bench, DRK_ADAPTER_PRECISION=fast) on config 2: host
+    std::vector<DrkPrimitive> in, host Images / ParamGrads out."""
+    import tempfile
+
+    from paper_2412_11752_b200 import scenes
+    exe = os.path.join(ROOT, "oracle", "_ref", "adapter_bench")
+    if not os.path.exists(exe):
+        return {"unavailable": "oracle/_ref/adapter_bench not built"}
+    sc = scenes.config_scene(2)
+    cam = scenes.config_cameras(2)[0]
+    tgt = scenes.config_target(2, cam)
+    with tempfile.NamedTemporaryFile(suffix=".bin", delete=False) as fh:
+        fh.write(np.array([sc.n, sc.k, sc.terms, cam.width, cam.height], np.int32).tobytes())
+        fh.write(np.concatenate([[cam.fx, cam.fy, cam.cx, cam.cy], np.asarray(cam.R).ravel(),
+                                 np.asarray(cam.t).ravel()]).astype(np.float64).tobytes())
+        fh.write(sc.f32().tobytes())
+        fh.write(np.ascontiguousarray(tgt, np.float64).tobytes())
+        path = fh.name
+    try:
+        env = dict(os.environ, DRK_ADAPTER_PRECISION="fast")
+        rr = subprocess.run([exe, path, str(warm), str(steps)], capture_output=True, text=True, timeout=600, env=env)
+        if rr.returncode != 0:
+            return {"unavailable": f"adapter_bench rc={rr.returncode}: {rr.stderr[-300:]}"}
+        res = json.loads(rr.stdout.strip().splitlines()[-1])
+    finally:
+        os.unlink(path)
+    px = cam.width * cam.height
+    return {"render": {"value": px / (res["render_ms"] * 1e-3) / 1e6, "unit": "megapixels/s",
+                       "ms_per_step": res["render_ms"]},
+            "fwd_bwd": {"value": px / (res["render_loss_backward_ms"] * 1e-3) / 1e6, "unit": "megapixels/s",
+                        "ms_per_step": res["render_loss_backward_ms"]},
+            "activate_ms_host": res["activate_ms"], "steps": res["steps"],
+            "workload": "config 2 (300k DRK, SH3, 1280x720) through the reference C++ API: drk::render, then "
+                        "drk::render + drk::loss (L1) + drk::backward_render (deterministic parallel backward), "
+                        "host std::vector<DrkPrimitive> in / host Images and ParamGrads out (conversions and copies "
+                        "timed; drk::activate on the host, reported apart)"}
+
+
 def run_reference(args):
     """Reference CPU arm: rank 0 alone times the unmodified reference (oracle/_ref): W untimed
     warm-up samples, then K bounded samples timed (~5 s each on 16 host threads)."""
@@ -160,6 +244,7 @@ def run_reference(args):
     v = float(np.mean(vals))
     cpu["value"] = v
     w, h = (int(x) for x in args.cpu_crop.split("x"))
+    fb = reference_cpu_fwd_bwd(args.cpu_crop_bwd)
     line = {"impl": "reference", "metric": "megapixels/sec rendered (forward; fwd+bwd in fwd_bwd)", "value": v,
             "unit": "megapixels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * (w * h) / (v * 1e6), "higher_is_better": True, "scaling": "weak",
@@ -168,12 +253,16 @@ def run_reference(args):
                                    "crop per step as the bounded CPU sample", "primitives": 100000, "K": 8,
                        "sh_degree": 3},
             "cpu_baseline": cpu,
+            "fwd_bwd": {"value": fb["value"], "unit": "megapixels/s", "ms_per_step": 1e3 * (fb["seconds_fwd"] +
+                                                                                           fb["seconds_loss_bwd"]),
+                        "workload": fb["sample"]},
             "e2e": {"value": v, "unit": "megapixels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
+    maybe_spawn(args)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -247,22 +336,45 @@ def main():
     achieved = flops / (rast_ms * 1e-3) / 1e12
     stage_ms = {k: v / args.steps for k, v in stage_acc.items() if k in ("activate", "preprocess", "rows_emit", "sort",
                                                                          "raster", "raster_fp64")}
-    traffic = None
+    traffic, traffic_src = None, None
     try:  # DRAM bytes of the dominant kernel from the committed ncu --set full capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get("k_raster_fast")
+            tj = json.load(fh)
+            traffic = tj.get("k_raster_fast")
+            traffic_src = tj.get("source", "profiles/ncu_traffic.json")
     except (OSError, ValueError):
         traffic = None
     roofline = {"kernel": "k_raster_fast (fp32 interval pass)", "bound": "fp32", "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": f"committed ncu --set full capture (not measured in this run): {traffic_src}",
                 "peak_source": "FFMA microbenchmark (drk_measure_fp32_peak) in this run; MEASURED_PEAKS.json has no "
                                "FP32 CUDA-core figure",
                 "algorithmic_flops_per_launch": flops, "kernel_ms": rast_ms,
                 "counts": {"pixels": px, "streamed": st["streamed"], "popped": st["popped"],
                            "composited": st["composited"]},
                 "share_of_step": rast_ms / ms_per_step}
-    # sort (HBM-bound): 10 passes max of 16 B/pair read + 16 B/pair write + 8 B/pair digit read
-    sort_ms = stage_ms.get("sort", 0.0)
+    # ---- HBM stages of the same frame: algorithmic bytes / CUDA-event stage time ----
+    hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            hbm_peak, hbm_src = float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        pass
+    S1 = sc.raw.shape[0]
+    algo_bytes = {
+        "activate": sc.n * (4 * S1 + 4 * 79),   # raw f32 in, activated record (79 values) out
+        "preprocess": sc.n * (8 * 31 + 160),    # activated fp64 geometry in, 160-B screen record out
+        "rows_emit": st["pairs"] * 12,          # one (u64 key, u32 id) pair written per tile entry
+        "sort": st["pairs"] * 16,               # u32 key + u32 id written once and read once
+    }
+    hbm_stages = {}
+    for k, b in algo_bytes.items():
+        ms = stage_ms.get(k, 0.0)
+        gbs = b / (ms * 1e-3) / 1e9 if ms else None
+        hbm_stages[k] = {"bytes": int(b), "ms": ms, "GB/s": gbs, "frac": gbs / hbm_peak if gbs else None}
+    hbm_roofline = {"bound": "hbm", "peak": hbm_peak, "unit": "GB/s", "peak_source": hbm_src, "stages": hbm_stages,
+                    "note": "K1 preprocess and K2 rows+emit are FP64 / latency bound (wedge polygons, fp64 keys), "
+                            "so their HBM fractions are low by construction; the sort is the HBM-bound stage"}
 
     # ---- e2e through the C-ABI host-buffer entry ----
     e2e = None
@@ -308,6 +420,10 @@ def main():
             _, dcol = r.l1_loss(fb.color, tgt2)
             r.backward_render(raw2, FrameGrad(d_color=dcol), grad_out=grad2)
 
+        r.set_counters(True)  # one counted frame (deterministic): the backward roofline's work counts
+        train_step()
+        st2 = r.stats()
+        r.set_counters(False)
         for _ in range(max(1, min(args.warmup, 2))):
             train_step()
         torch.cuda.synchronize(dev)
@@ -331,10 +447,22 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             fb_tot = float(t.item())
         px2 = cam2.width * cam2.height
+        bwd_ms = bst.get("backward_raster", 0.0)
+        bflops = (px2 * F_PIXEL[3] + st2["streamed"] * F_ISECT + st2["popped"] * F_ALPHA
+                  + st2["composited"] * (F_BLEND[3] + F_BWD_RECORD[3]))
+        roofline_bwd = {"kernel": "k_raster_bwd_fast + fp64 pixel backward (stage backward_raster)", "bound": "fp32",
+                        "achieved": bflops / (bwd_ms * 1e-3) / 1e12 if bwd_ms else None, "peak": peak,
+                        "unit": "TFLOP/s", "frac": (bflops / (bwd_ms * 1e-3) / 1e12) / peak if bwd_ms else None,
+                        "algorithmic_flops_per_launch": bflops, "kernel_ms": bwd_ms,
+                        "counts": {"pixels": px2, "streamed": st2["streamed"], "popped": st2["popped"],
+                                   "composited_records": st2["composited"]},
+                        "per_unit": {"pixel": F_PIXEL[3], "streamed": F_ISECT, "popped": F_ALPHA,
+                                     "record": F_BLEND[3] + F_BWD_RECORD[3]},
+                        "share_of_step": bwd_ms / fb_tot if fb_tot else None}
         fwd_bwd = {"value": world * px2 / (fb_tot * 1e-3) / 1e6, "unit": "megapixels/s", "ms_per_step": fb_tot,
                    "steps": nfb, "workload": "config2: 300k DRK, K=8, SH3, 1280x720, forward + L1 loss + backward "
                                              "(raw-parameter gradients), one view per GPU",
-                   "stage_ms": bst}
+                   "stage_ms": bst, "roofline_bwd": roofline_bwd}
 
     # ---- config 3: multi-view batch, views sharded across ranks (strong scaling) ----
     multiview = None
@@ -344,15 +472,25 @@ def main():
         cams3 = scenes.config_cameras(3)[:args.multiview_views]
         raw3 = torch.from_numpy(sc3.f32()).to(dev)
         from paper_2412_11752_b200.parallel import MultiViewRenderer
-        mine = shard_views(len(cams3), world, rank)
+        # per-view cost = tile pairs, from one pass over views v = rank (mod world),
+        # gathered so that every rank shards the same way (greedy LPT, shard_views)
+        cost = torch.zeros(len(cams3), dtype=torch.float64, device=dev)
+        for i, v in enumerate(range(rank, len(cams3), world)):
+            if i == 0:
+                r.render(raw3, cams3[v], opt)
+            else:
+                r.render_again(cams3[v], opt)
+            cost[v] = float(r.stats()["pairs"])
+        if world > 1:
+            dist.all_reduce(cost)
+        mine = shard_views(len(cams3), world, rank, cost.cpu().numpy())
         my_cams = [cams3[v] for v in mine]
         mvr = MultiViewRenderer(local, inflight=args.multiview_inflight)
         for rr in mvr.rasts:
             rr.set_counters(False)
-        for _ in range(2):  # warm-up passes over this rank's views (buffers reach their peak sizes)
-            mvr.render(raw3, my_cams, opt)
+        mvr.render(raw3, my_cams, opt)  # warm-up pass over this rank's views (buffers reach their peak sizes)
         torch.cuda.synchronize(dev)
-        nmv = max(1, min(args.steps, 3))
+        nmv = max(1, min(args.steps, 2))
         mv_ms = []
         for _ in range(nmv):
             barrier()
@@ -372,8 +510,9 @@ def main():
         multiview = {"value": len(cams3) * px3 / (mv_tot * 1e-3) / 1e6, "unit": "megapixels/s",
                      "ms_per_step": mv_tot, "steps": nmv, "scaling": "strong", "views_per_step": len(cams3),
                      "views_on_rank0": len(mine), "inflight_contexts": args.multiview_inflight,
+                     "sharding": "greedy longest-first by tile-pair count (shard_views), pairs gathered over ranks",
                      "workload": f"config3: 1M DRK, K=8, SH3, {len(cams3)} of the 64 seeded orbit views at 1920x1080 "
-                                 "per step, views split across ranks (replicated primitives, no data-path collective); "
+                                 "per step, views split across ranks by cost (replicated primitives, no data-path collective); "
                                  "on each GPU the primitives are activated once per step and the views stream through "
                                  "MultiViewRenderer (in-flight contexts: --multiview-inflight); max over ranks"}
         mvr.close()
@@ -444,17 +583,23 @@ def main():
                              "views of 1280x720 per GPU, forward + L1 + backward per view, NCCL all-reduce (mean over "
                              "all views) of the raw gradients, Adam (lr 1e-3); replicas checked by parameter checksum")
     train_c4 = None
-    if args.config4_train:
+    if not args.no_config4_train:
         train_c4 = train_leg(4, 8, 1, 1)
         train_c4["workload"] = ("config 4 training step: 4M DRK, K=8, SH3, 8 orbit views of 3840x2160 per GPU "
                                 "(banded binning), forward + L1 + backward per view, NCCL all-reduce (mean over all "
                                 "views) of the raw gradients, Adam (lr 1e-3); one warm-up step (buffer growth)")
+
+    # ---- drop-in adapter (rank 0, N = 1): the reference C++ API served by the GPU ----
+    adapter = None
+    if rank == 0 and world == 1 and not args.no_adapter:
+        adapter = adapter_leg()
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cpu, _ = reference_cpu_sample(args.cpu_crop, 1)
+            cpu["fwd_bwd"] = reference_cpu_fwd_bwd(args.cpu_crop_bwd)
         except Exception as e:  # the oracle build is missing: report, do not fail the bench
             cpu = {"value": None, "unit": "megapixels/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -471,7 +616,7 @@ def main():
                            "views_per_gpu": 1, "parallelism": f"views x{world} (replicated primitives)",
                            "l2": "flushed between timed steps (256 MiB write, outside the timed events)"},
                 "stage_ms": stage_ms, "pairs": st["pairs"], "fp64_pixels": st["fp64_pixels"],
-                "roofline": roofline, "e2e": e2e, "fwd_bwd": fwd_bwd, "multiview": multiview, "train": train, "train_config4": train_c4,
+                "roofline": roofline, "hbm_roofline": hbm_roofline, "adapter": adapter, "e2e": e2e, "fwd_bwd": fwd_bwd, "multiview": multiview, "train": train, "train_config4": train_c4,
                 "cpu_baseline": cpu,
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)

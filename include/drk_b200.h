@@ -153,6 +153,8 @@ int drk_set_timing(drk_ctx* ctx, int enabled);
  * sorted and rasterized one band of tile rows at a time; automatic).  Test hook:
  * force bands above `pairs` pairs per band (0 = memory-based). */
 int drk_set_band_limit(drk_ctx* ctx, int64_t pairs);
+/* Deterministic backward: records per chunk of tile rows (test hook; 0 = memory-based). */
+int drk_set_det_chunk_limit(drk_ctx* ctx, int64_t records);
 /* Work counters of the fast forward (drk_stats streamed / popped / reject
  * counts): off by default (the counter-free kernel is launched, those fields
  * stay 0); on launches the counting instantiation (about 1.6% slower). */
@@ -221,7 +223,10 @@ int drk_get_replay(drk_ctx* ctx, int64_t* total_records, int64_t* offsets_host,
  * DRK_ERR_REPLAY_MISMATCH.  grad_raw (SoA, like raw) receives the raw-space
  * gradient; with accumulate != 0 it is added to instead of overwritten
  * (multi-view batches).  d_center_world (n x 3), screen_grad (n), touched (n)
- * may be NULL.  deterministic != 0 selects the fixed-order reduction. */
+ * may be NULL.  deterministic != 0 selects the fixed-order reduction: every
+ * composited record writes its gradient row to its own slot and the rows are
+ * reduced per primitive in (tile, pixel, composite) order, tile partials in fp64
+ * (reference grad.cpp:327-368) — parallel, and bitwise reproducible. */
 int drk_backward(drk_ctx* ctx, const float* raw, const drk_frame_grad* fg, float* grad_raw,
                  float* d_center_world, float* screen_grad, uint8_t* touched, int accumulate,
                  int deterministic);

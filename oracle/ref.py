@@ -149,6 +149,40 @@ def bin_primitives(scene, cam, opt: Options = Options()):
     return off, ids, keys
 
 
+def bin_primitives_parallel(scene, cam, opt: Options = Options(), threads: int = 0):
+    """Reference bin_primitives on `threads` chunks of the primitives, merged with the
+    reference comparator (ref_bin_parallel): identical to bin_primitives, faster."""
+    total = C.c_int64(0)
+    _check(lib().ref_bin_parallel(_p(_raw(scene)), scene.n, scene.k, scene.terms, C.byref(_cam(cam)),
+                                  C.byref(_opt(opt)), int(threads), C.byref(total)))
+    tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    off = np.zeros(tiles + 1, dtype=np.int64)
+    ids = np.zeros(total.value, dtype=np.int32)
+    keys = np.zeros(total.value, dtype=np.float64)
+    lib().ref_bins_copy(_p(off), _p(ids), _p(keys))
+    return off, ids, keys
+
+
+def fwd_bwd(scene, cam, target, opt: Options = Options()):
+    """Reference activate + render(&replay) + L1 loss + backward_render (ref_fwd_bwd):
+    framebuffers, loss, d_color, raw grads, d_center_world, screen_grad, touched and
+    the wall seconds of the forward and of loss + backward."""
+    H, W, n = cam.height, cam.width, scene.n
+    out = dict(color=np.zeros((H, W, 3)), depth=np.zeros((H, W)), normal=np.zeros((H, W, 3)),
+               alpha=np.zeros((H, W)), d_color=np.zeros((H, W, 3)), raw=np.zeros_like(scene.raw, dtype=np.float64),
+               d_center_world=np.zeros((n, 3)), screen_grad=np.zeros(n), touched=np.zeros(n, dtype=np.int8))
+    loss = C.c_double(0)
+    secs = np.zeros(2)
+    tgt = np.ascontiguousarray(target, dtype=np.float64)
+    _check(lib().ref_fwd_bwd(_p(_raw(scene)), n, scene.k, scene.terms, C.byref(_cam(cam)), C.byref(_opt(opt)),
+                             _p(tgt), *[_p(out[f]) for f in ("color", "depth", "normal", "alpha")], C.byref(loss),
+                             _p(out["d_color"]), _p(out["raw"]), _p(out["d_center_world"]), _p(out["screen_grad"]),
+                             _p(out["touched"]), _p(secs)))
+    out["loss"] = loss.value
+    out["seconds_fwd"], out["seconds_bwd"] = float(secs[0]), float(secs[1])
+    return out
+
+
 def render(scene, cam, opt: Options = Options(), replay: bool = False):
     H, W = cam.height, cam.width
     color = np.zeros((H, W, 3))

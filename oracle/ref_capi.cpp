@@ -11,6 +11,7 @@
 //     in drk::for_each_scalar order (types.hpp:48-72), s < scalar_count(K, terms);
 //   camera: drk_camera (fx, fy, cx, cy, width, height, R row-major world->cam, t);
 //   images: row-major interleaved, double here.
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -203,6 +204,122 @@ int ref_bin(const double* raw_soa, int n, int k, int terms, const ref_camera* c,
       g_bins.offsets[t + 1] = static_cast<int64_t>(g_bins.ids.size());
     }
     *total_pairs = static_cast<int64_t>(g_bins.ids.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
+// Thread-parallel drk::bin_primitives: the reference function (unmodified) on
+// `threads` contiguous chunks of the primitives, then per tile the chunks'
+// entries (ids made global) re-sorted with the reference comparator
+// (raster.cpp:260-263).  Identical to one call over all primitives — the
+// binning is per primitive apart from that final sort — in a fraction of the
+// single-threaded time (full BASELINE frames in the parity tests).
+int ref_bin_parallel(const double* raw_soa, int n, int k, int terms, const ref_camera* c, const ref_options* o,
+                     int threads, int64_t* total_pairs) {
+  try {
+    const auto raws = to_raws(raw_soa, n, k, terms);
+    const drk::RenderOptions opt = to_opt(o, k);
+    const drk::Camera cam = to_cam(c);
+    const int T = std::max(1, std::min(threads > 0 ? threads : drk::resolve_thread_count(0), std::max(1, n)));
+    std::vector<drk::TileBinning> parts(T);
+    std::vector<std::string> errs(T);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t) {
+      pool.emplace_back([&, t] {
+        try {
+          const int lo = (int)((long long)n * t / T), hi = (int)((long long)n * (t + 1) / T);
+          std::vector<drk::DrkPrimitive> prims;
+          prims.reserve(hi - lo);
+          for (int i = lo; i < hi; ++i) prims.push_back(drk::activate(raws[i]));
+          parts[t] = drk::bin_primitives(prims, cam, opt.kernel, opt.presort);
+        } catch (const std::exception& e) {
+          errs[t] = e.what();
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+    for (const auto& e : errs)
+      if (!e.empty()) throw drk::Error(e);
+    const size_t tiles = parts[0].tiles.size();
+    std::vector<std::vector<drk::TileEntry>> merged(tiles);
+    std::vector<std::thread> pool2;
+    for (int t = 0; t < T; ++t) {
+      pool2.emplace_back([&, t] {
+        for (size_t tile = t; tile < tiles; tile += T) {
+          auto& m = merged[tile];
+          for (int q = 0; q < T; ++q) {
+            const int lo = (int)((long long)n * q / T);
+            for (const auto& e : parts[q].tiles[tile]) m.push_back({e.prim_id + lo, e.key});
+          }
+          std::sort(m.begin(), m.end(), [](const drk::TileEntry& a, const drk::TileEntry& b) {
+            return a.key < b.key || (a.key == b.key && a.prim_id < b.prim_id);
+          });
+        }
+      });
+    }
+    for (auto& th : pool2) th.join();
+    g_bins.offsets.assign(tiles + 1, 0);
+    g_bins.ids.clear();
+    g_bins.keys.clear();
+    for (size_t t = 0; t < tiles; ++t) {
+      for (const auto& e : merged[t]) {
+        g_bins.ids.push_back(e.prim_id);
+        g_bins.keys.push_back(e.key);
+      }
+      g_bins.offsets[t + 1] = static_cast<int64_t>(g_bins.ids.size());
+    }
+    *total_pairs = static_cast<int64_t>(g_bins.ids.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return status_of(e);
+  }
+}
+
+// The reference training-step span of one view: activate + render(&replay) +
+// loss (L1, dssim_weight = 0; optimize.cpp:171-204) + backward_render
+// (grad.cpp:307-384).  Any output may be null.  seconds2 = {forward
+// (activate + render), loss + backward}.
+int ref_fwd_bwd(const double* raw_soa, int n, int k, int terms, const ref_camera* c, const ref_options* o,
+                const double* target, double* color, double* depth, double* normal, double* alpha, double* loss_out,
+                double* d_color, double* grad_soa, double* d_center_world, double* screen_grad, int8_t* touched,
+                double* seconds2) {
+  try {
+    const auto raws = to_raws(raw_soa, n, k, terms);
+    const drk::Camera cam = to_cam(c);
+    const drk::RenderOptions opt = to_opt(o, k);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<drk::DrkPrimitive> prims;
+    prims.reserve(n);
+    for (const auto& r : raws) prims.push_back(drk::activate(r));
+    drk::ReplayBuffer rb;
+    const drk::FrameBuffers fb = drk::render(prims, cam, opt, &rb);
+    const auto t1 = std::chrono::steady_clock::now();
+    const drk::LossResult lr = drk::loss(fb.color, image_from(target, cam.width, cam.height, 3), 0.0);
+    drk::FrameGrad fg;
+    fg.d_color = lr.d_color;
+    const drk::ParamGrads g = drk::backward_render(raws, prims, cam, opt, rb, fg);
+    const auto t2 = std::chrono::steady_clock::now();
+    if (seconds2) {
+      seconds2[0] = std::chrono::duration<double>(t1 - t0).count();
+      seconds2[1] = std::chrono::duration<double>(t2 - t1).count();
+    }
+    copy_image(fb.color, color);
+    copy_image(fb.depth, depth);
+    copy_image(fb.normal, normal);
+    copy_image(fb.alpha, alpha);
+    copy_image(lr.d_color, d_color);
+    if (loss_out) *loss_out = lr.value;
+    if (grad_soa) from_raws(g.raw, grad_soa);
+    for (int i = 0; i < n; ++i) {
+      if (d_center_world)
+        for (int q = 0; q < 3; ++q) d_center_world[3 * i + q] = g.d_center_world[i][q];
+      if (screen_grad) screen_grad[i] = g.screen_grad[i];
+      if (touched) touched[i] = g.touched[i];
+    }
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

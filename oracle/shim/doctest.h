@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <fnmatch.h>
 #include <functional>
 #include <set>
 #include <string>
@@ -143,14 +144,28 @@ struct Subcase {
 
 inline int run_all(int argc, char** argv) {
   std::string suite_filter;
+  std::vector<std::string> exclude;  // -tce=<name>[,<name>...] (doctest's test-case-exclude; '*' wildcards)
   for (int i = 1; i < argc; ++i) {
     const char* a = argv[i];
     if (std::strncmp(a, "-ts=", 4) == 0) suite_filter = a + 4;
     if (std::strncmp(a, "--test-suite=", 13) == 0) suite_filter = a + 13;
+    if (std::strncmp(a, "-tce=", 5) == 0) {
+      std::string list = a + 5;
+      size_t pos = 0;
+      while (pos <= list.size()) {
+        const size_t comma = list.find(',', pos);
+        exclude.push_back(list.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos));
+        if (comma == std::string::npos) break;
+        pos = comma + 1;
+      }
+    }
   }
   int cases = 0, failed_cases = 0;
   for (const TestCase& tc : registry()) {
     if (!suite_filter.empty() && suite_filter != tc.suite) continue;
+    bool excluded = false;
+    for (const std::string& pat : exclude) excluded = excluded || fnmatch(pat.c_str(), tc.name, 0) == 0;
+    if (excluded) continue;
     ++cases;
     counters().test_failed = false;
     subcases() = SubcaseState{};

@@ -138,6 +138,7 @@ SIGNATURES = {
     "drk_measure_fp32_peak": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "drk_set_validation": (C.c_int, [_P, C.c_int]),
     "drk_set_band_limit": (C.c_int, [_P, C.c_int64]),
+    "drk_set_det_chunk_limit": (C.c_int, [_P, C.c_int64]),
     "drk_set_counters": (C.c_int, [_P, C.c_int]),
     "drk_get_bands": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "drk_get_validation": (C.c_int, [_P, C.POINTER(C.c_double)]),

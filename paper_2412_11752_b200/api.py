@@ -58,6 +58,9 @@ class RenderOptions:
     # backward where eligible (SortCache mode, K = 8), 1 = legacy fp64-depth
     # kernels, 5 = legacy backward only
     raster_kernel: int = 0
+    # B200 extension: reference-precision mode (fp64 alpha on every pixel), as the
+    # C++ adapter's default; False = fp32 fast path with fp64 fallbacks
+    fp64_alpha: bool = False
 
 
 @dataclass
@@ -205,6 +208,7 @@ def _options(opt: RenderOptions, replay_cap: int = 0) -> _lib.Options_:
     o.sh_degree, o.use_cache, o.exact_sort = opt.sh_degree, int(opt.use_cache), int(opt.exact_sort)
     o.presort, o.threads, o.record_replay = int(opt.presort), int(opt.threads), int(replay_cap)
     o.raster_kernel = int(opt.raster_kernel)
+    o.fp64_alpha = int(opt.fp64_alpha)
     return o
 
 
@@ -409,6 +413,10 @@ class Rasterizer:
     def set_band_limit(self, pairs: int):
         """Force banded binning above `pairs` tile pairs per band (0 = by free device memory)."""
         self._check(_lib.lib().drk_set_band_limit(self._h, int(pairs)))
+
+    def set_det_chunk_limit(self, records: int = 0):
+        """Test hook: records per chunk of tile rows in the deterministic backward (0 = memory-based)."""
+        self._check(_lib.lib().drk_set_det_chunk_limit(self._h, int(records)))
 
     def bands(self) -> int:
         v = C.c_int32(0)

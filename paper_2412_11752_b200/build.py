@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 SOURCES = {"drk_prep.cu": False, "drk_sort.cu": False, "drk_raster.cu": True, "drk_raster_fast.cu": True, "drk_raster_bwd.cu": True,
-           "drk_capi.cu": False, "drk_scene.cu": False, "drk_loss.cu": False, "drk_train.cu": False, "drk_mesh.cu": False}
+           "drk_capi.cu": False, "drk_scene.cu": False, "drk_loss.cu": False, "drk_train.cu": False, "drk_mesh.cu": False, "drk_det.cu": False}
 LIB = os.path.join(HERE, "libdrk_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -164,6 +164,7 @@ static RasterParams raster_params(drk_ctx* c) {
   P.frame32 = static_cast<const float4*>(c->frame32.p);
   P.fast_nt = 256;
   P.no_counters = c->work_counters ? 0 : 1;
+  P.pxcomp = static_cast<int*>(c->pxcomp.p);
   return P;
 }
 
@@ -553,8 +554,9 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   double* pxstate = ensure<double>(c->pxstate, 8 * (size_t)n_pix);
   unsigned char* pxflag = ensure<unsigned char>(c->pxflag, (size_t)n_pix);
   int* pxstop = ensure<int>(c->pxstop, (size_t)n_pix);
+  int* pxcomp = ensure<int>(c->pxcomp, (size_t)n_pix);
   int* redo = ensure<int>(c->redo, (size_t)n_pix + 1);
-  if (!pxstate || !pxflag || !redo || !pxstop) return set_error(c, DRK_ERR_OOM, "pixel state");
+  if (!pxstate || !pxflag || !redo || !pxstop || !pxcomp) return set_error(c, DRK_ERR_OOM, "pixel state");
   if (opt->record_replay > 0) {
     ensure<int>(c->replay_cnt, n_pix);
     ensure<int>(c->replay_ids, (size_t)n_pix * opt->record_replay);
@@ -677,6 +679,26 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   return DRK_OK;
 }
 
+int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& bands,
+                     int (*band_lists)(drk_ctx*, int, RasterParams&));
+
+// Tile lists of band b of a banded frame for the deterministic backward: the
+// forward's kept lists, or the band binned again.
+static int det_band_lists(drk_ctx* c, int b, RasterParams& Q) {
+  const int nb = (int)c->bands.size() - 1;
+  if (c->band_cache_valid && (int)c->band_ids.size() == nb) {
+    Q.lid = static_cast<const int*>(c->band_ids[b].p);
+    Q.tileoff = static_cast<const long long*>(c->band_off[b].p);
+    return DRK_OK;
+  }
+  long long np = 0;
+  if (int st = bin_band(c, c->bands[b], c->bands[b + 1], &np)) return st;
+  Q.lid = static_cast<const int*>(c->pv.p);
+  Q.tileoff = static_cast<const long long*>(c->tileoff.p);
+  Q.geo = static_cast<const Geo*>(c->geo.p);
+  return DRK_OK;
+}
+
 int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* grad_raw, float* d_center_world,
                  float* screen_grad, uint8_t* touched, int accumulate, int deterministic) {
   if (!c->has_fwd) return set_error(c, DRK_ERR_REPLAY_MISMATCH, "backward without a forward on this context");
@@ -711,8 +733,9 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   mark(c, 7);
   const int nb = (int)c->bands.size() - 1;
   if (deterministic) {
-    if (nb > 1) return set_error(c, DRK_ERR_UNSUPPORTED, "deterministic backward of a banded frame");
-    launch_backward_serial(P, s);  // fixed accumulation order, small images
+    // parallel, fixed accumulation order (drk_det.cu)
+    std::vector<int> bands = c->bands.size() >= 2 ? c->bands : std::vector<int>{0, c->camd.tiles_y};
+    if (int st = run_backward_det(c, P, bands, det_band_lists)) return st;
   } else if (nb <= 1) {
     // longest tile lists first, as in the forward
     static const int tile_order_mode = getenv("DRK_TILE_ORDER") ? atoi(getenv("DRK_TILE_ORDER")) : 1;
@@ -921,7 +944,8 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->counters, &c->scan_tmp, &c->loss_tmp, &c->progress, &c->patch, &c->scene_aos,
                     &c->loss_part, &c->ssim_f, &c->dens_code, &c->dens_pos,
                     &c->eval_scr, &c->eval_px, &c->eval_off, &c->ovf_scr, &c->ovf_list, &c->tord,
-                    &c->rowest, &c->host_raw, &c->host_img};
+                    &c->rowest, &c->host_raw, &c->host_img, &c->pxcomp, &c->det_cnt, &c->det_base,
+                    &c->det_rec, &c->det_id, &c->det_tile, &c->det_sort, &c->det_poff, &c->det_acc, &c->det_rowoff};
   for (DevBuf* b : bufs) release(*b);
   for (DevBuf& b : c->band_ids) release(b);
   for (DevBuf& b : c->band_off) release(b);
@@ -1062,6 +1086,12 @@ int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_ter
 int drk_set_counters(drk_ctx* c, int enabled) {
   if (!c) return DRK_ERR_INVALID_ARG;
   c->work_counters = enabled != 0;
+  return DRK_OK;
+}
+
+int drk_set_det_chunk_limit(drk_ctx* c, int64_t records) {
+  if (!c || records < 0) return DRK_ERR_INVALID_ARG;
+  c->det_chunk_limit = records;
   return DRK_OK;
 }
 

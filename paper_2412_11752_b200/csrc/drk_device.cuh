@@ -58,6 +58,7 @@ enum Counter {
   C_AMBIGUOUS,         // fast kernel: cache steps with overlapping depth intervals
   C_RING_MISS,         // fast kernel: pops re-staged from HBM (older than the ring)
   C_PTS_POOL,          // K1: sorted-point pool cursor
+  C_DET_OVERFLOW,      // deterministic backward: records beyond the forward's composite count (must stay 0)
   C_COUNT
 };
 

@@ -107,7 +107,34 @@ struct RasterParams {
   int no_counters;        // fast forward: work counters compiled out (drk_set_counters(ctx, 0))
   const int* tile_order;  // fast forward: band-local tile of each CTA (longest lists first), or null = row-major
   unsigned long long* vstat;  // fast kernel validation: max |a32 - a64| / bound, max |a32 - a64| (double bits)
+  int* pxcomp;                // forward: composited entries per pixel (the deterministic backward's record counts)
+  // deterministic backward (drk_backward(..., deterministic = 1)): every composited
+  // record writes its gradient row to det_rec[det_base[slot] + k - det_off] (slot =
+  // tile * 256 + row-major pixel in the tile, k = composite index in the pixel)
+  // instead of adding it atomically; records are reduced per primitive afterwards
+  // in (tile, pixel, composite) order (reference grad.cpp:327-368)
+  float* det_rec;
+  int* det_id;
+  int* det_tile;
+  const long long* det_base;
+  long long det_off, det_cap;
 };
+
+// Record row of a composited (pixel, k) in the deterministic backward, or
+// nullptr (counted in C_DET_OVERFLOW) when the backward composites more entries
+// than the forward counted.
+__device__ __forceinline__ float* det_row(const RasterParams& P, int x, int y, int k, int id) {
+  const int tile = (y >> 4) * P.cam.tiles_x + (x >> 4);
+  const long long slot = (long long)tile * 256 + (y & 15) * 16 + (x & 15);
+  const long long r = P.det_base[slot] + k - P.det_off;
+  if (k >= P.pxcomp[(size_t)y * P.cam.W + x] || r < 0 || r >= P.det_cap) {
+    atomicAdd(&P.counters[C_DET_OVERFLOW], 1ull);
+    return nullptr;
+  }
+  P.det_id[r] = id;
+  P.det_tile[r] = tile;
+  return P.det_rec + (size_t)r * P.G;
+}
 
 void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s, cudaEvent_t mid = nullptr);
 bool raster_fast_eligible(const RasterParams& P);
@@ -116,7 +143,9 @@ int raster_fast_nt(long long pairs, int n_tiles);
 void launch_raster_bwd_fast(const RasterParams& P, int n_tiles, cudaStream_t s);
 void launch_shape_rec(const ShapeView& S, int n, float* rec, cudaStream_t s);
 double measure_fp32_peak(cudaStream_t s);
-void launch_backward_serial(const RasterParams& P, cudaStream_t s);
+void launch_raster_bwd_fast_det(const RasterParams& P, int n_tiles, cudaStream_t s);
+void launch_pixels_bwd(const RasterParams& P, cudaStream_t s);  // k_raster_pixels_warp<MODE, true> over P.redo_list
+void launch_exact_bwd(const RasterParams& P, int n_tiles, cudaStream_t s);
 void launch_eval_sorting(const RasterParams& P, int tile0, int tile1, const long long* scr_off, double* scratch,
                          int use_cache, double* tau, double* mae, unsigned char* flag, cudaStream_t s);
 void launch_eval_sorting_reduce(const CamD& cam, const long long* tileoff, const double* tau, const double* mae,
@@ -149,6 +178,11 @@ struct drk_ctx {
   drk::DevBuf ovf_scr, ovf_list;
   drk::DevBuf tord;                       // fast forward tile order: keys / ids and their sort ping-pong
   drk::DevBuf host_raw, host_img;         // drk_forward_host: device staging of the host params / framebuffers
+  drk::DevBuf pxcomp;                     // composited entries per pixel (forward)
+  // deterministic backward: slot counts / record offsets, record rows, ids, tiles,
+  // sort buffers, per-primitive offsets, fp64 accumulator
+  drk::DevBuf det_cnt, det_base, det_rec, det_id, det_tile, det_sort, det_poff, det_acc, det_rowoff;
+  long long det_chunk_limit = 0;          // test hook: records per chunk (0 = memory-based)
   int64_t hull_cap = 0;
   drk::DevBuf rowest;
   std::vector<int> bands;         // tile-row band boundaries of the last forward

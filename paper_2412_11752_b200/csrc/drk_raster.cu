@@ -237,7 +237,8 @@ struct Pixel {
                       (dN[0] * (sgn * rz[0]) + dN[1] * (sgn * rz[1]) + dN[2] * (sgn * rz[2])) + dA;
     rest -= wb * cw;
     const double dat = T * cw - rest / (1.0 - a);
-    backward_record_dat(P, id, g, rt, u, v, a, lp, ev, rgb, cl0, cl1, cl2, sgn, rdz, dpw, dph, wb, dat, T);
+    backward_record_dat(P, id, g, rt, u, v, a, lp, ev, rgb, cl0, cl1, cl2, sgn, rdz, dpw, dph, wb, dat, T,
+                        (int)n_comp - 1);
   }
 
   // Gradient of one record given its upstream dL/d(alpha_tilde) (`dat`) and
@@ -245,10 +246,21 @@ struct Pixel {
   __device__ void backward_record_dat(const RasterParams& P, int id, const Geo& g, double rt, double u, double v,
                                       double a, bool lp, const KEval& ev, const double rgb[3], bool cl0, bool cl1,
                                       bool cl2, double sgn, double rdz, double dpw, double dph, double wb,
-                                      double dat, double T_i) const {
+                                      double dat, double T_i, int comp_idx) const {
     (void)rgb;
     (void)T_i;
+    // deterministic backward: the record's own row (plain adds, fixed order);
+    // otherwise atomics into the primitive's row
+    const bool det_mode = P.det_rec != nullptr;
     float* pg = P.gact + (size_t)id * P.G;
+    if (det_mode) {
+      pg = det_row(P, pix % P.cam.W, pix / P.cam.W, comp_idx, id);
+      if (!pg) return;
+    }
+    auto gadd = [det_mode](float* a, double v) {
+      if (det_mode) *a += (float)v;
+      else atomicAdd(a, (float)v);
+    };
     const int K = P.S.K;
     const double rz[3] = {g.rz[0], g.rz[1], g.rz[2]};
     P.touched[id] = 1;
@@ -260,16 +272,16 @@ struct Pixel {
       if (cl[ch]) continue;
       const double dc = wb * dC[ch];
       if (dc == 0) continue;
-      for (int t = 0; t < P.opt.terms_active; ++t) atomicAdd(pg + o_sh + 3 * t + ch, dc * (double)basis[t]);
+      for (int t = 0; t < P.opt.terms_active; ++t) gadd(pg + o_sh + 3 * t + ch, dc * (double)basis[t]);
     }
     if (has_dN)
-      for (int q = 0; q < 3; ++q) atomicAdd(pg + o_rot + 3 * q + 2, wb * sgn * dN[q]);
+      for (int q = 0; q < 3; ++q) gadd(pg + o_rot + 3 * q + 2, wb * sgn * dN[q]);
     if (dD != 0) {
       const double d_rt = wb * dD;
       for (int q = 0; q < 3; ++q) {
         const double h = P.cam.o[q] + rt * dir[q] - g.mu[q];
-        atomicAdd(pg + q, d_rt * rz[q] / rdz);
-        atomicAdd(pg + o_rot + 3 * q + 2, d_rt * (-h / rdz));
+        gadd(pg + q, d_rt * rz[q] / rdz);
+        gadd(pg + o_rot + 3 * q + 2, d_rt * (-h / rdz));
       }
     }
     const bool alpha_clamped = a >= 1.0 - 1e-6 - 1e-12;
@@ -277,25 +289,25 @@ struct Pixel {
     const double o = P.S.o[id];
     if (lp) {
       const double cv = fabs(rdz), sl = P.opt.lowpass_radius;
-      atomicAdd(pg + o_op, dat * a / o);
+      gadd(pg + o_op, dat * a / o);
       const double inv = 1.0 / (cv * cv * sl * sl);
       const double d_dpw = dat * a * (-dpw * inv);
       const double d_dph = dat * a * (-dph * inv);
       const double d_cos = dat * a * (dpw * dpw + dph * dph) * inv / cv;
       double J[6];
       projection_jacobian(P.cam, g.mu, J);
-      for (int q = 0; q < 3; ++q) atomicAdd(pg + q, -(J[q] * d_dpw + J[3 + q] * d_dph));
+      for (int q = 0; q < 3; ++q) gadd(pg + q, -(J[q] * d_dpw + J[3 + q] * d_dph));
       const double sg = rdz < 0 ? -1.0 : 1.0;
-      for (int q = 0; q < 3; ++q) atomicAdd(pg + o_rot + 3 * q + 2, d_cos * sg * dir[q]);
+      for (int q = 0; q < 3; ++q) gadd(pg + o_rot + 3 * q + 2, d_cos * sg * dir[q]);
       return;
     }
     // backward_alpha (grad.cpp:16-101)
     const double tau = P.S.tau[id];
     const double d_alpha = dat;
-    atomicAdd(pg + o_op, d_alpha * sharpen(ev.g, tau));
+    gadd(pg + o_op, d_alpha * sharpen(ev.g, tau));
     if (ev.center) return;
     const int br = sharpen_branch(ev.g, tau);
-    atomicAdd(pg + o_tau, d_alpha * o * sharpen_dtau(br, ev.g, tau));
+    gadd(pg + o_tau, d_alpha * o * sharpen_dtau(br, ev.g, tau));
     if (ev.clamped) return;
     const double d_g = d_alpha * o * sharpen_slope(br, tau);
     const double d_q = d_g * (-0.5 * ev.g);
@@ -303,7 +315,7 @@ struct Pixel {
     const double* s = P.S.s + (size_t)id * K;
     const double* th = P.S.th + (size_t)id * K;
     const double slo = s[lo], shi = s[hi], eta = P.S.eta[id];
-    atomicAdd(pg + o_eta, d_q * (ev.r1 * ev.r1 - ev.r2 * ev.inv_sbar));
+    gadd(pg + o_eta, d_q * (ev.r1 * ev.r1 - ev.r2 * ev.inv_sbar));
     const double d_r1 = d_q * eta * 2.0 * ev.r1;
     const double d_r2sq = d_q * (1.0 - eta) * ev.inv_sbar;
     const double d_inv = d_q * (1.0 - eta) * ev.r2;
@@ -343,10 +355,10 @@ struct Pixel {
     const double dth_x = nb * ((ehy * thx - ehx * thy) / det), dth_y = nb * ((-ely * thx + elx * thy) / det);
     da_lo += d_r1 * (sa * dtl_x + sb * dtl_y);
     da_hi += d_r1 * (sa * dth_x + sb * dth_y);
-    atomicAdd(pg + o_sc + lo, ds_lo);
-    atomicAdd(pg + o_sc + hi, ds_hi);
-    atomicAdd(pg + o_an + lo, da_lo);
-    atomicAdd(pg + o_an + hi, da_hi);
+    gadd(pg + o_sc + lo, ds_lo);
+    gadd(pg + o_sc + hi, ds_hi);
+    gadd(pg + o_an + lo, da_lo);
+    gadd(pg + o_an + hi, da_hi);
     // (u, v) and r_t chain to centre and rotation columns (grad.cpp:290-300)
     const double h[3] = {P.cam.o[0] + rt * dir[0] - g.mu[0], P.cam.o[1] + rt * dir[1] - g.mu[1],
                          P.cam.o[2] + rt * dir[2] - g.mu[2]};
@@ -355,13 +367,13 @@ struct Pixel {
     for (int q = 0; q < 3; ++q) {
       const double du_dmu = rz[q] * (drx / rdz) - g.rx[q];
       const double dv_dmu = rz[q] * (dry / rdz) - g.ry[q];
-      atomicAdd(pg + q, du * du_dmu + dv * dv_dmu);
+      gadd(pg + q, du * du_dmu + dv * dv_dmu);
     }
     const double f = -(du * drx + dv * dry) / rdz;
     for (int q = 0; q < 3; ++q) {
-      atomicAdd(pg + o_rot + 3 * q + 0, du * h[q]);
-      atomicAdd(pg + o_rot + 3 * q + 1, dv * h[q]);
-      atomicAdd(pg + o_rot + 3 * q + 2, f * h[q]);
+      gadd(pg + o_rot + 3 * q + 0, du * h[q]);
+      gadd(pg + o_rot + 3 * q + 1, dv * h[q]);
+      gadd(pg + o_rot + 3 * q + 2, f * h[q]);
     }
   }
 
@@ -863,6 +875,7 @@ struct Pixel {
     if (P.depth) P.depth[p] = (float)D;
     if (P.alpha) P.alpha[p] = (float)A;
     if (!F64 && P.pxstop) P.pxstop[p] = stop;
+    if (P.pxcomp) P.pxcomp[p] = (int)n_comp;
     if (P.pxstate) {
       double* st = P.pxstate + 8 * p;
       st[0] = c0;
@@ -1487,6 +1500,7 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
       if (lane < npop && e.ev.degenerate) px.err = true;
       // 3) in-order compositing (all lanes replicate the scalar state)
       double wb_mine = 0, dat_mine = 0, T_mine = 1;
+      int idx_mine = 0;
       int last_k = npop - 1;
       for (int k = 0; k < npop && !done; ++k) {
         last_k = k;
@@ -1520,6 +1534,7 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
             wb_mine = w;
             T_mine = px.T;
             dat_mine = px.T * cw - px.rest / (1.0 - a);
+            idx_mine = (int)px.n_comp - 1;
           }
         }
         px.T = xm(px.T, xs(1.0, a));
@@ -1551,7 +1566,7 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
         const double rgb[3] = {(double)e.rgb[0], (double)e.rgb[1], (double)e.rgb[2]};
         const double sgn = e.denom < 0 ? 1.0 : -1.0;
         px.backward_record_dat(P, e.id, g, e.rt, e.u, e.v, e.a, e.lp, e.ev, rgb, e.cl[0], e.cl[1], e.cl[2], sgn,
-                               e.denom, e.dpw, e.dph, wb_mine, dat_mine, T_mine);
+                               e.denom, e.dpw, e.dph, wb_mine, dat_mine, T_mine, idx_mine);
       }
     }
     if (lane == 0) {
@@ -1571,28 +1586,6 @@ __global__ void __launch_bounds__(128) k_raster_pixels(RasterParams P) {
     process_pixel<MODE, BWD>(P, P.redo_list[t]);
     if (!BWD) atomicAdd(&P.counters[C_REDO_PIXELS], 1ull);
   }
-}
-
-// Deterministic backward (drk_backward(..., deterministic = 1)): one thread
-// walks tiles in index order and pixels row-major inside each tile — the
-// reference's accumulation order (grad.cpp:327-368) — so every fp64 atomic
-// lands in a fixed order and the gradients are bitwise reproducible.
-// Meant for the small images of the drop-in test suites.
-template <int MODE>
-__global__ void k_backward_serial(RasterParams P) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  for (int t = 0; t < P.cam.tiles_x * P.cam.tiles_y; ++t) {
-    const int tx = t % P.cam.tiles_x, ty = t / P.cam.tiles_x;
-    for (int y = ty * kTile; y < min(P.cam.H, (ty + 1) * kTile); ++y)
-      for (int x = tx * kTile; x < min(P.cam.W, (tx + 1) * kTile); ++x) process_pixel<MODE, true>(P, y * P.cam.W + x);
-  }
-}
-
-void launch_backward_serial(const RasterParams& P, cudaStream_t s) {
-  launch_counter() += 1;
-  if (P.opt.exact_sort) k_backward_serial<2><<<1, 1, 0, s>>>(P);
-  else if (P.opt.use_cache) k_backward_serial<0><<<1, 1, 0, s>>>(P);
-  else k_backward_serial<1><<<1, 1, 0, s>>>(P);
 }
 
 // exact_sort oracle mode (raster.cpp:395-401): every hit composited in
@@ -1693,6 +1686,24 @@ void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s,
     if (bwd) k_raster_pixels_warp<1, true><<<redo_blocks, 128, 0, s>>>(P);
     else k_raster_pixels_warp<1, false><<<redo_blocks, 128, 0, s>>>(P);
   }
+}
+
+// Deterministic backward building blocks (drk_det.cu): the fp64 per-pixel
+// path over P.redo_list (all pixels of a chunk, or its flagged pixels after the
+// fast kernel), and the exact-sort path over a range of tiles.
+void launch_pixels_bwd(const RasterParams& P, cudaStream_t s) {
+  cudaMemsetAsync(P.redo_count + 1, 0, sizeof(unsigned), s);
+  launch_counter() += 1;
+  if (P.opt.use_cache) k_raster_pixels_warp<0, true><<<148 * 8, 128, 0, s>>>(P);
+  else k_raster_pixels_warp<1, true><<<148 * 8, 128, 0, s>>>(P);
+}
+
+void launch_exact_bwd(const RasterParams& P, int n_tiles, cudaStream_t s) {
+  if (n_tiles <= 0) return;
+  launch_counter() += 1;
+  RasterParams Q = P;
+  Q.pxflag = nullptr;
+  k_raster_exact<true><<<dim3(2, n_tiles), 128, 0, s>>>(Q);
 }
 
 // FFMA throughput probe (8 independent chains per thread, 148 x 8 CTAs).

@@ -320,7 +320,9 @@ __device__ __noinline__ void record_grad_f64(const RasterParams& P, const BwdPix
 
 // NT threads per CTA: 256 = a 16x16 tile, 128 = half a tile (8 x 16 pixels;
 // long tile lists), as in the fast forward.
-template <int NT>
+// DET: deterministic mode — each composited record writes its own gradient row
+// (det_row) instead of the warp-group reduction and atomics.
+template <int NT, bool DET>
 __global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fast(const __grid_constant__ RasterParams P) {
   constexpr int RING = 2 * NT;
   extern __shared__ float4 dyn[];
@@ -480,10 +482,29 @@ __global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fas
           record_grad_f64(P, bp, id, g, o64, a, wb, dat, dd, row);
         }
         P.touched[id] = 1;
+        if (DET) {
+          float* dr = det_row(P, x, y, px.ncomp, id);
+          if (dr) {
+#pragma unroll
+            for (int i = 0; i < kGCols; ++i) dr[gcol_global(i)] = row[i];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              if (t < P.opt.terms_active) {
+                dr[kGOffSh + 3 * t] = w0 * bas[t];
+                dr[kGOffSh + 3 * t + 1] = w1 * bas[t];
+                dr[kGOffSh + 3 * t + 2] = w2 * bas[t];
+              }
+            }
+          }
+        }
         px.T = xm(px.T, xs(1.0, a));
         ++px.ncomp;
         if (px.ncomp >= stop) done = true;
       }
+    }
+    if (DET) {
+      __syncwarp();
+      return;
     }
     s_w[0] = w0;
     s_w[1] = w1;
@@ -713,17 +734,23 @@ size_t raster_bwd_fast_smem(int nt) {
   return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + (16 + 4 + kGCols) * nt * sizeof(float);
 }
 
-template <int NT>
+template <int NT, bool DET>
 static void launch_bwd_nt(const RasterParams& P, int n_tiles, cudaStream_t s) {
   const size_t smem = raster_bwd_fast_smem(NT);
   static PerDeviceOnce attr;
-  attr([&] { cudaFuncSetAttribute(k_raster_bwd_fast<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
-  k_raster_bwd_fast<NT><<<n_tiles * (256 / NT), NT, smem, s>>>(P);
+  attr([&] { cudaFuncSetAttribute(k_raster_bwd_fast<NT, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+  k_raster_bwd_fast<NT, DET><<<n_tiles * (256 / NT), NT, smem, s>>>(P);
 }
 
 void launch_raster_bwd_fast(const RasterParams& P, int n_tiles, cudaStream_t s) {
-  if (P.fast_nt == 128) launch_bwd_nt<128>(P, n_tiles, s);
-  else launch_bwd_nt<256>(P, n_tiles, s);
+  if (P.fast_nt == 128) launch_bwd_nt<128, false>(P, n_tiles, s);
+  else launch_bwd_nt<256, false>(P, n_tiles, s);
+}
+
+void launch_raster_bwd_fast_det(const RasterParams& P, int n_tiles, cudaStream_t s) {
+  if (n_tiles <= 0) return;
+  launch_counter() += 1;
+  launch_bwd_nt<256, true>(P, n_tiles, s);
 }
 
 }  // namespace drk

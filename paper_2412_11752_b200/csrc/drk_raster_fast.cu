@@ -348,6 +348,7 @@ __device__ __forceinline__ void write_pixel(const RasterParams& P, const FastPix
     st[7] = px.A;
   }
   if (P.pxstop) P.pxstop[p] = px.stop;
+  if (P.pxcomp) P.pxcomp[p] = px.ncomp;
   if (P.pxflag) {
     P.pxflag[p] = px.uncertain ? 1 : 0;
     if (px.uncertain) P.redo_list[atomicAdd(P.redo_count, 1u)] = (int)p;

@@ -119,3 +119,19 @@ def test_config1_crop_bit_exact():
     opt = ref.Options(sh_degree=3)
     assert _same(ref.bin_primitives(sc, cam, opt), port.bin_primitives(sc, cam, opt))
     _render_equal(sc, cam, opt, replay=False)
+
+
+@pytest.mark.parametrize("cfg,n,threads", [(0, None, 3), (1, 6000, 4)])
+def test_reference_parallel_binning_is_exact(cfg, n, threads):
+    """ref_bin_parallel (the reference bin_primitives on chunks of the primitives,
+    merged with its own comparator) equals one reference bin_primitives call."""
+    sc = scenes.config_scene(cfg, n=n)
+    cam = scenes.config_cameras(cfg)[0]
+    if cfg:
+        cam = cam.crop(640, 320, 320, 256)
+    opt = ref.Options(sh_degree=scenes.CONFIGS[cfg]["sh_degree"])
+    a = ref.bin_primitives(sc, cam, opt)
+    b = ref.bin_primitives_parallel(sc, cam, opt, threads=threads)
+    assert len(a[1]) > 1000
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
