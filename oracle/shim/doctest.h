@@ -145,16 +145,19 @@ struct Subcase {
 inline int run_all(int argc, char** argv) {
   std::string suite_filter;
   std::vector<std::string> exclude;  // -tce=<name>[,<name>...] (doctest's test-case-exclude; '*' wildcards)
+  std::vector<std::string> include;  // -tc=<name>[,<name>...] (test-case filter)
   for (int i = 1; i < argc; ++i) {
     const char* a = argv[i];
     if (std::strncmp(a, "-ts=", 4) == 0) suite_filter = a + 4;
     if (std::strncmp(a, "--test-suite=", 13) == 0) suite_filter = a + 13;
-    if (std::strncmp(a, "-tce=", 5) == 0) {
-      std::string list = a + 5;
+    const bool inc = std::strncmp(a, "-tc=", 4) == 0;
+    if (inc || std::strncmp(a, "-tce=", 5) == 0) {
+      std::string list = a + (inc ? 4 : 5);
+      std::vector<std::string>& dst = inc ? include : exclude;
       size_t pos = 0;
       while (pos <= list.size()) {
         const size_t comma = list.find(',', pos);
-        exclude.push_back(list.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos));
+        dst.push_back(list.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos));
         if (comma == std::string::npos) break;
         pos = comma + 1;
       }
@@ -165,7 +168,9 @@ inline int run_all(int argc, char** argv) {
     if (!suite_filter.empty() && suite_filter != tc.suite) continue;
     bool excluded = false;
     for (const std::string& pat : exclude) excluded = excluded || fnmatch(pat.c_str(), tc.name, 0) == 0;
-    if (excluded) continue;
+    bool included = include.empty();
+    for (const std::string& pat : include) included = included || fnmatch(pat.c_str(), tc.name, 0) == 0;
+    if (excluded || !included) continue;
     ++cases;
     counters().test_failed = false;
     subcases() = SubcaseState{};

@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -69,17 +71,38 @@ void check(int st) {
   if (st != DRK_OK) raise(st);
 }
 
+// Grow-only device scratch, one slot per argument role: the reference API is
+// called once per training step / finite-difference probe, so per-call
+// cudaMalloc / cudaFree (an implicit device synchronisation each) would dominate
+// small renders.
+void* slot_bytes(int slot, size_t bytes) {
+  struct Slot {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  static Slot slots[32];
+  Slot& s = slots[slot];
+  if (s.bytes < bytes) {
+    if (s.p) cudaFree(s.p);
+    s.p = nullptr;
+    const size_t want = bytes + bytes / 4;
+    if (cudaMalloc(&s.p, want) != cudaSuccess) throw drk::Error("drk_b200: cudaMalloc");
+    s.bytes = want;
+  }
+  return s.p;
+}
+
+enum Slots { kMu, kRot, kS, kTh, kEta, kTau, kO, kSh, kColor, kDepth, kNormal, kAlpha, kRaw, kDC, kDD, kDN, kDA,
+             kG, kDcw, kSg, kTch, kLossA, kLossB, kLossOut, kLossD };
+
 template <class T>
 struct Dev {
   T* p = nullptr;
   size_t n = 0;
-  explicit Dev(size_t count) : n(count) {
-    if (cudaMalloc(&p, sizeof(T) * (count ? count : 1)) != cudaSuccess) throw drk::Error("drk_b200: cudaMalloc");
-  }
-  Dev(const std::vector<T>& h) : Dev(h.size()) {
+  Dev(int slot, size_t count) : p(static_cast<T*>(slot_bytes(slot, sizeof(T) * (count ? count : 1)))), n(count) {}
+  Dev(int slot, const std::vector<T>& h) : Dev(slot, h.size()) {
     if (!h.empty()) cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice);
   }
-  ~Dev() { cudaFree(p); }
   std::vector<T> get() const {
     std::vector<T> h(n);
     if (n) cudaMemcpy(h.data(), p, sizeof(T) * n, cudaMemcpyDeviceToHost);
@@ -87,12 +110,38 @@ struct Dev {
   }
 };
 
+// Fingerprint of the host inputs of a forward (64-bit words, multiply-xorshift): the
+// backward reuses the device state of the last forward when it saw the same
+// primitives, camera and options — the reference's render(&replay) ->
+// backward_render sequence — instead of uploading and rendering again.
+struct Fnv {
+  uint64_t h = 1469598103934665603ull;
+  void mix(uint64_t w) {
+    h = (h ^ w) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 29;
+  }
+  void add(const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+      uint64_t w;
+      std::memcpy(&w, b + i, 8);
+      mix(w);
+    }
+    uint64_t tail = n;
+    for (; i < n; ++i) tail = (tail << 8) | b[i];
+    mix(tail);
+  }
+  template <class T>
+  void vec(const std::vector<T>& v) {
+    add(v.data(), v.size() * sizeof(T));
+  }
+};
+uint64_t g_last_forward = 0;  // fingerprint of the context's last forward (0: none)
+
 // Activated primitives on the device (drk_prims).
 struct DevPrims {
   int n, k, terms;
-  Dev<double> mu, rot, s, th, eta, tau, o;
-  Dev<float> sh;
-  drk_prims view;
   static std::vector<double> field(const std::vector<drk::DrkPrimitive>& P, int per, int which) {
     std::vector<double> v;
     v.reserve(P.size() * per);
@@ -125,22 +174,45 @@ struct DevPrims {
           for (const auto& p : P) t = std::max<int>(t, (int)p.sh.rows());
           return t;
         }()),
-        mu(field(P, 3, 0)),
-        rot(field(P, 9, 1)),
-        s(field(P, k, 2)),
-        th(field(P, k, 3)),
-        eta(field(P, 1, 4)),
-        tau(field(P, 1, 5)),
-        o(field(P, 1, 6)),
-        sh(shf(P, terms)) {
+        hmu(field(P, 3, 0)),
+        hrot(field(P, 9, 1)),
+        hs(field(P, k, 2)),
+        hth(field(P, k, 3)),
+        heta(field(P, 1, 4)),
+        htau(field(P, 1, 5)),
+        ho(field(P, 1, 6)),
+        hsh(shf(P, terms)) {
     for (const auto& p : P)
       if (p.basis_count() != k) throw drk::DimensionMismatchError("drk_b200 adapter: mixed basis counts");
+    Fnv f;
+    f.add(&n, sizeof n);
+    f.add(&k, sizeof k);
+    f.add(&terms, sizeof terms);
+    f.vec(hmu);
+    f.vec(hrot);
+    f.vec(hs);
+    f.vec(hth);
+    f.vec(heta);
+    f.vec(htau);
+    f.vec(ho);
+    f.vec(hsh);
+    hash = f.h;
+  }
+  // device copies (only when a forward must run)
+  void upload() {
+    Dev<double> mu(kMu, hmu), rot(kRot, hrot), s(kS, hs), th(kTh, hth), eta(kEta, heta), tau(kTau, htau), o(kO, ho);
+    Dev<float> sh(kSh, hsh);
     view = drk_prims{mu.p, rot.p, s.p, th.p, eta.p, tau.p, o.p, sh.p};
   }
+  std::vector<double> hmu, hrot, hs, hth, heta, htau, ho;
+  std::vector<float> hsh;
+  drk_prims view{};
+  uint64_t hash = 0;
 };
 
 drk_camera to_cam(const drk::Camera& c) {
   drk_camera d;
+  std::memset(&d, 0, sizeof d);  // padding too: the struct is fingerprinted
   d.fx = c.fx;
   d.fy = c.fy;
   d.cx = c.cx;
@@ -153,6 +225,22 @@ drk_camera to_cam(const drk::Camera& c) {
   return d;
 }
 
+// DRK_ADAPTER_TRACE=1: wall time of every adapter call on stderr.
+struct Trace {
+  const char* what;
+  int w, h, n;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  static bool on() {
+    static const bool e = std::getenv("DRK_ADAPTER_TRACE") != nullptr;
+    return e;
+  }
+  ~Trace() {
+    if (on())
+      std::fprintf(stderr, "[drk adapter] %s %dx%d n=%d: %.3f ms\n", what, w, h, n,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 bool fast_precision() {
   static const bool fast = [] {
     const char* e = std::getenv("DRK_ADAPTER_PRECISION");
@@ -163,6 +251,7 @@ bool fast_precision() {
 
 drk_options to_opt(const drk::RenderOptions& o, int replay_cap) {
   drk_options d;
+  std::memset(&d, 0, sizeof d);
   drk_default_options(&d);
   d.lowpass_radius = o.kernel.lowpass_radius;
   d.alpha_min = o.kernel.alpha_min;
@@ -179,11 +268,25 @@ drk_options to_opt(const drk::RenderOptions& o, int replay_cap) {
   return d;
 }
 
+uint64_t forward_hash(const DevPrims& dp, const drk_camera& c, const drk_options& o) {
+  drk_options oo = o;
+  oo.record_replay = 0;  // the backward does not depend on the replay capacity
+  Fnv f;
+  f.add(&dp.hash, sizeof dp.hash);
+  f.add(&c, sizeof c);
+  f.add(&oo, sizeof oo);
+  return f.h | 1;
+}
+
 void forward(const std::vector<drk::DrkPrimitive>& prims, const drk::Camera& cam, const drk::RenderOptions& opt,
              int replay_cap, float* color, float* depth, float* normal, float* alpha, DevPrims& dp) {
+  (void)prims;
   const drk_camera c = to_cam(cam);
   const drk_options o = to_opt(opt, replay_cap);
+  g_last_forward = 0;
+  dp.upload();
   check(drk_forward_prims(ctx(), &dp.view, dp.n, dp.k, dp.terms, &c, &o, color, depth, normal, alpha));
+  g_last_forward = forward_hash(dp, c, o);
 }
 
 }  // namespace
@@ -233,9 +336,10 @@ SortingMetrics eval_sorting(const std::vector<DrkPrimitive>& prims, const Camera
 
 FrameBuffers render(const std::vector<DrkPrimitive>& prims, const Camera& cam, const RenderOptions& opt,
                     ReplayBuffer* replay) {
+  Trace tr{replay ? "render(replay)" : "render", cam.width, cam.height, (int)prims.size()};
   DevPrims dp(prims, opt.kernel.basis_count);
   const size_t npx = (size_t)cam.width * cam.height;
-  Dev<float> color(3 * npx), depth(npx), normal(3 * npx), alpha(npx);
+  Dev<float> color(kColor, 3 * npx), depth(kDepth, npx), normal(kNormal, 3 * npx), alpha(kAlpha, npx);
   forward(prims, cam, opt, replay ? 1024 : 0, color.p, depth.p, normal.p, alpha.p, dp);
   FrameBuffers fb;
   fb.color = Image(cam.width, cam.height, 3);
@@ -274,12 +378,16 @@ FrameBuffers render(const std::vector<DrkPrimitive>& prims, const Camera& cam, c
 ParamGrads backward_render(const std::vector<RawDrkParams>& raws, const std::vector<DrkPrimitive>& prims,
                            const Camera& cam, const RenderOptions& opt, const ReplayBuffer& replay,
                            const FrameGrad& frame_grad) {
+  Trace tr{"backward_render", cam.width, cam.height, (int)prims.size()};
   if (replay.width != cam.width || replay.height != cam.height)
     throw ReplayMismatchError("replay buffer does not match the camera dimensions");
   if (raws.size() != prims.size()) throw ReplayMismatchError("raw and activated primitive counts differ");
   DevPrims dp(prims, opt.kernel.basis_count);
-  // the device keeps the decisions of this forward in place of the ReplayBuffer
-  forward(prims, cam, opt, 0, nullptr, nullptr, nullptr, nullptr, dp);
+  // the device keeps the decisions of the forward in place of the ReplayBuffer:
+  // the last forward's when it rendered these primitives with this camera and
+  // these options (render(&replay) -> backward_render), else a fresh one
+  if (g_last_forward != forward_hash(dp, to_cam(cam), to_opt(opt, 0)))
+    forward(prims, cam, opt, 0, nullptr, nullptr, nullptr, nullptr, dp);
   const int n = dp.n, k = dp.k, terms = dp.terms;
   const int S = drk_scalar_count(k, terms);
   std::vector<float> raw_soa((size_t)S * n, 0.f);
@@ -290,7 +398,7 @@ ParamGrads backward_render(const std::vector<RawDrkParams>& raws, const std::vec
       ++s;
     });
   }
-  Dev<float> raw_d(raw_soa);
+  Dev<float> raw_d(kRaw, raw_soa);
   auto img = [&](const Image& im, int ch) -> std::vector<float> {
     if (im.empty()) return {};
     if (im.width != cam.width || im.height != cam.height || im.channels != ch)
@@ -299,11 +407,11 @@ ParamGrads backward_render(const std::vector<RawDrkParams>& raws, const std::vec
   };
   const std::vector<float> hc = img(frame_grad.d_color, 3), hd = img(frame_grad.d_depth, 1),
                            hn = img(frame_grad.d_normal, 3), ha = img(frame_grad.d_alpha, 1);
-  Dev<float> dc(hc), dd(hd), dn(hn), da(ha);
+  Dev<float> dc(kDC, hc), dd(kDD, hd), dn(kDN, hn), da(kDA, ha);
   drk_frame_grad fg{hc.empty() ? nullptr : dc.p, hd.empty() ? nullptr : dd.p, hn.empty() ? nullptr : dn.p,
                     ha.empty() ? nullptr : da.p};
-  Dev<float> g((size_t)S * n), dcw(3 * (size_t)n), sg(n);
-  Dev<uint8_t> tch(n);
+  Dev<float> g(kG, (size_t)S * n), dcw(kDcw, 3 * (size_t)n), sg(kSg, n);
+  Dev<uint8_t> tch(kTch, n);
   check(drk_backward(ctx(), raw_d.p, &fg, g.p, dcw.p, sg.p, tch.p, 0, /*deterministic=*/1));
   const std::vector<float> gh = g.get(), dcwh = dcw.get(), sgh = sg.get();
   const std::vector<uint8_t> th = tch.get();
@@ -341,21 +449,21 @@ void done(int st) {
 
 double psnr(const Image& a, const Image& b) {
   same_shape(a, b);
-  Dev<double> da(a.data), db(b.data), out(2);
+  Dev<double> da(kLossA, a.data), db(kLossB, b.data), out(kLossOut, 2);
   done(drk_psnr_f64(ctx(), da.p, db.p, a.width, a.height, a.channels, out.p));
   return out.get()[0];
 }
 
 double ssim(const Image& a, const Image& b) {
   same_shape(a, b);
-  Dev<double> da(a.data), db(b.data), out(1);
+  Dev<double> da(kLossA, a.data), db(kLossB, b.data), out(kLossOut, 1);
   done(drk_ssim_f64(ctx(), da.p, db.p, a.width, a.height, a.channels, out.p));
   return out.get()[0];
 }
 
 LossResult loss(const Image& rendered, const Image& target, double dssim_weight) {
   same_shape(rendered, target);
-  Dev<double> dr(rendered.data), dt(target.data), out(3), dcol(rendered.data.size());
+  Dev<double> dr(kLossA, rendered.data), dt(kLossB, target.data), out(kLossOut, 3), dcol(kLossD, rendered.data.size());
   done(drk_loss_f64(ctx(), dr.p, dt.p, rendered.width, rendered.height, rendered.channels, dssim_weight, out.p,
                      dcol.p));
   LossResult res;

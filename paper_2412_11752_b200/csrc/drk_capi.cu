@@ -45,11 +45,17 @@ __global__ void k_tie_keys(long long n, const unsigned* sk, const unsigned* sv, 
 __global__ void k_tie_fix(long long n, const unsigned* sk, unsigned* sv, unsigned long long* fk);
 __global__ void k_full_keys(long long n, const unsigned* sk, const unsigned* sv, int dbits, const Geo* geo,
                             const double* cdirs, const double* tdirs, CamD cam, OptD opt, double* out);
+__global__ void k_full_keys_off(long long n, const long long* tileoff, int n_tiles, const unsigned* sv, const Geo* geo,
+                                const double* cdirs, const double* tdirs, CamD cam, OptD opt, double* out);
 template <typename T>
 int exclusive_scan(drk_ctx* c, const T* in, long long n, long long* out, long long* total);
 int sort_pairs(drk_ctx* c, unsigned* k, unsigned* v, unsigned* k2, unsigned* v2, long long n);
 void launch_tile_order_keys(int n, int tiles_x, int band_rows, const long long* tileoff, int tile_base, unsigned* key,
                             unsigned* id, cudaStream_t s);
+void launch_act_bwd(int n, int K, int terms, const float* raw, const double* gact, int G,
+                    const unsigned char* touched_dev, const Geo* geo, const CamD& cam, float* grad_raw,
+                    float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
+                    cudaStream_t s);
 void launch_act_bwd(int n, int K, int terms, const float* raw, const float* gact, int G,
                     const unsigned char* touched_dev, const Geo* geo, const CamD& cam, float* grad_raw,
                     float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
@@ -787,8 +793,13 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   }
   mark(c, 8);
   if (int st = cuda_check(c, cudaGetLastError(), "raster bwd")) return st;
-  launch_act_bwd(n, K, A.terms, raw, gact, G, tch, static_cast<const Geo*>(c->geo.p), c->camd, grad_raw,
-                 d_center_world, screen_grad, touched, accumulate, s);
+  if (deterministic)  // the fp64 sums of the fixed-order reduction
+    launch_act_bwd(n, K, A.terms, raw, static_cast<const double*>(c->det_acc.p), G, tch,
+                   static_cast<const Geo*>(c->geo.p), c->camd, grad_raw, d_center_world, screen_grad, touched,
+                   accumulate, s);
+  else
+    launch_act_bwd(n, K, A.terms, raw, gact, G, tch, static_cast<const Geo*>(c->geo.p), c->camd, grad_raw,
+                   d_center_world, screen_grad, touched, accumulate, s);
   DRK_COUNT_LAUNCH();
   mark(c, 9);
   if (int st = cuda_check(c, cudaGetLastError(), "activation bwd")) return st;
@@ -1157,10 +1168,54 @@ int drk_eval_sorting(drk_ctx* c, double* out4) {
   return cuda_check(c, cudaStreamSynchronize(s), "eval_sorting");
 }
 
+// Banded frame: the per-band lists the forward kept (ids + per-tile offsets;
+// bands are tile-row ranges in order, so concatenating them keeps tile order),
+// keys recomputed per band.
+static int banded_tile_lists(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* ids, double* keys) {
+  const int nb = (int)c->bands.size() - 1;
+  if (!(c->band_cache_valid && (int)c->band_ids.size() == nb))
+    return set_error(c, DRK_ERR_UNSUPPORTED, "tile lists of this banded frame were not kept (device memory)");
+  const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
+  std::vector<int64_t> off_b((size_t)n_tiles + 1);
+  int64_t base = 0;
+  if (offsets) offsets[0] = 0;
+  for (int b = 0; b < nb; ++b) {
+    cudaMemcpyAsync(off_b.data(), c->band_off[b].p, sizeof(int64_t) * (n_tiles + 1), cudaMemcpyDeviceToHost,
+                    c->stream);
+    if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "band offsets")) return st;
+    const long long np = off_b[n_tiles];
+    const int t0 = c->bands[b] * c->camd.tiles_x, t1 = c->bands[b + 1] * c->camd.tiles_x;
+    if (offsets)
+      for (int t = t0; t < t1; ++t) offsets[t + 1] = base + off_b[t + 1];
+    if (ids && np > 0) {
+      std::vector<unsigned> v((size_t)np);
+      cudaMemcpyAsync(v.data(), c->band_ids[b].p, sizeof(unsigned) * np, cudaMemcpyDeviceToHost, c->stream);
+      if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "band ids")) return st;
+      for (long long i = 0; i < np; ++i) ids[base + i] = (int32_t)v[i];
+    }
+    if (keys && np > 0) {
+      DevBuf tmp;
+      double* kd = ensure<double>(tmp, (size_t)np);
+      if (!kd) return set_error(c, DRK_ERR_OOM, "key buffer");
+      k_full_keys_off<<<(unsigned)((np + 255) / 256), 256, 0, c->stream>>>(
+          np, static_cast<const long long*>(c->band_off[b].p), n_tiles, static_cast<const unsigned*>(c->band_ids[b].p),
+          static_cast<const Geo*>(c->geo.p), static_cast<const double*>(c->cdirs.p),
+          static_cast<const double*>(c->tdirs.p), c->camd, c->optd, kd);
+      cudaMemcpyAsync(keys + base, kd, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream);
+      const int st = cuda_check(c, cudaStreamSynchronize(c->stream), "band keys");
+      release(tmp);
+      if (st) return st;
+    }
+    base += np;
+  }
+  if (total) *total = base;
+  return DRK_OK;
+}
+
 int drk_get_tile_lists(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* ids, double* keys) {
   if (!c || !c->has_fwd) return c ? set_error(c, DRK_ERR_INVALID_ARG, "no forward on this context") : DRK_ERR_INVALID_ARG;
-  if (c->bands.size() > 2) return set_error(c, DRK_ERR_UNSUPPORTED, "tile lists of a banded frame are not kept");
   cudaSetDevice(c->device);
+  if (c->bands.size() > 2) return banded_tile_lists(c, total, offsets, ids, keys);
   if (total) *total = c->n_pairs;
   const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
   if (offsets)

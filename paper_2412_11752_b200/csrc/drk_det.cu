@@ -18,7 +18,7 @@
 //      then walks its records, forming each tile's partial in fp64 and adding
 //      the partials tile by tile to an fp64 accumulator.
 // The result does not depend on scheduling: two runs are bitwise identical.
-// Record rows take G floats each; frames whose records exceed the memory budget
+// Record rows take G floats (fast-kernel frames) or doubles (reference precision) each; frames whose records exceed the memory budget
 // are processed in chunks of tile rows (in row order, so the accumulation order
 // is unchanged).
 #include <algorithm>
@@ -83,8 +83,9 @@ __global__ void k_det_segments(long long n, const unsigned* __restrict__ k, long
 
 // One warp per primitive: its records in (tile, pixel, composite) order; the
 // fp64 partial of each tile is added to the running total when the tile ends.
+template <typename RT>
 __global__ void k_det_reduce(int n, int G, const long long* __restrict__ seg, const unsigned* __restrict__ rec_of,
-                             const int* __restrict__ tile_of, const float* __restrict__ rows, double* acc) {
+                             const int* __restrict__ tile_of, const RT* __restrict__ rows, double* acc) {
   const int p = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= n) return;
@@ -119,7 +120,8 @@ unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
 // P: the backward's parameters (gact, touched, frame gradients, pixel state);
-// band_lists(b, Q): sets Q's tile lists for band b.  Writes P.gact.
+// band_lists(b, Q): sets Q's tile lists for band b.  Writes P.gact (fp32) and
+// leaves the fp64 sums in ctx->det_acc for the activation backward.
 int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& bands,
                      int (*band_lists)(drk_ctx*, int, RasterParams&)) {
   cudaStream_t s = c->stream;
@@ -147,7 +149,12 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
 
   // records per chunk: the budget covers the row (G floats), id, tile and the
   // sort's four u32 arrays
-  const size_t per_rec = sizeof(float) * G + 2 * sizeof(int) + 4 * sizeof(unsigned);
+  const bool fast = P.opt.use_cache && !P.opt.exact_sort && P.opt.raster_kernel != 1 && P.opt.raster_kernel != 5 &&
+                    raster_fast_eligible(P);
+  // fp32 rows where the fast fp32 kernel computes the records; fp64 rows where
+  // every record comes from the fp64 per-pixel path (reference precision)
+  const size_t row_bytes = fast ? sizeof(float) : sizeof(double);
+  const size_t per_rec = row_bytes * G + 2 * sizeof(int) + 4 * sizeof(unsigned);
   long long limit = c->det_chunk_limit;
   if (limit <= 0) {
     size_t free_b = 0, total_b = 0;
@@ -157,8 +164,6 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
   }
   limit = std::max(1LL, std::min(limit, (long long)0x7fffffff));
 
-  const bool fast = P.opt.use_cache && !P.opt.exact_sort && P.opt.raster_kernel != 1 && P.opt.raster_kernel != 5 &&
-                    raster_fast_eligible(P);
   const int nb = (int)bands.size() - 1;
   for (int b = 0; b < nb; ++b) {
     RasterParams Q = P;
@@ -173,13 +178,14 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
       const int nt = (ty1 - ty0) * cd.tiles_x;
       const int y0 = ty0 * kTile, y1 = std::min(ty1 * kTile, cd.H);
       if (R > 0) {
-        float* rows = ensure<float>(c->det_rec, (size_t)R * G);
+        void* rows = ensure_bytes(c->det_rec, row_bytes * (size_t)R * G);
         int* ids = ensure<int>(c->det_id, (size_t)R);
         int* tiles = ensure<int>(c->det_tile, (size_t)R);
         unsigned* sk = ensure<unsigned>(c->det_sort, 4 * (size_t)R + 4);
         if (!rows || !ids || !tiles || !sk) return set_error(c, DRK_ERR_OOM, "deterministic backward records");
-        cudaMemsetAsync(rows, 0, sizeof(float) * (size_t)R * G, s);
-        Q.det_rec = rows;
+        cudaMemsetAsync(rows, 0, row_bytes * (size_t)R * G, s);
+        Q.det_rec = fast ? nullptr : static_cast<double*>(rows);
+        Q.det_rec32 = fast ? static_cast<float*>(rows) : nullptr;
         Q.det_id = ids;
         Q.det_tile = tiles;
         Q.det_base = base;
@@ -209,7 +215,8 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
         if (int st = sort_pairs(c, kk, vv, k2, v2, R)) return st;
         cudaMemsetAsync(seg, 0, sizeof(long long) * 2 * (size_t)n, s);
         k_det_segments<<<blocks(R, 256), 256, 0, s>>>(R, kk, seg);
-        k_det_reduce<<<blocks(32LL * n, 256), 256, 0, s>>>(n, G, seg, vv, tiles, rows, acc);
+        if (fast) k_det_reduce<float><<<blocks(32LL * n, 256), 256, 0, s>>>(n, G, seg, vv, tiles, Q.det_rec32, acc);
+        else k_det_reduce<double><<<blocks(32LL * n, 256), 256, 0, s>>>(n, G, seg, vv, tiles, Q.det_rec, acc);
         launch_counter() += 2;
         if (int st = cuda_check(c, cudaGetLastError(), "deterministic backward reduce")) return st;
       }

@@ -113,27 +113,28 @@ struct RasterParams {
   // tile * 256 + row-major pixel in the tile, k = composite index in the pixel)
   // instead of adding it atomically; records are reduced per primitive afterwards
   // in (tile, pixel, composite) order (reference grad.cpp:327-368)
-  float* det_rec;
+  double* det_rec;   // fp64 rows (reference-precision frames), or
+  float* det_rec32;  // fp32 rows (fast-kernel frames: their gradients are fp32 already; half the bytes)
   int* det_id;
   int* det_tile;
   const long long* det_base;
   long long det_off, det_cap;
 };
 
-// Record row of a composited (pixel, k) in the deterministic backward, or
-// nullptr (counted in C_DET_OVERFLOW) when the backward composites more entries
-// than the forward counted.
-__device__ __forceinline__ float* det_row(const RasterParams& P, int x, int y, int k, int id) {
+// Record index of a composited (pixel, k) in the deterministic backward, or -1
+// (counted in C_DET_OVERFLOW) when the backward composites more entries than
+// the forward counted.
+__device__ __forceinline__ long long det_row(const RasterParams& P, int x, int y, int k, int id) {
   const int tile = (y >> 4) * P.cam.tiles_x + (x >> 4);
   const long long slot = (long long)tile * 256 + (y & 15) * 16 + (x & 15);
   const long long r = P.det_base[slot] + k - P.det_off;
   if (k >= P.pxcomp[(size_t)y * P.cam.W + x] || r < 0 || r >= P.det_cap) {
     atomicAdd(&P.counters[C_DET_OVERFLOW], 1ull);
-    return nullptr;
+    return -1;
   }
   P.det_id[r] = id;
   P.det_tile[r] = tile;
-  return P.det_rec + (size_t)r * P.G;
+  return r;
 }
 
 void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s, cudaEvent_t mid = nullptr);

@@ -1284,6 +1284,24 @@ __global__ void k_tile_bounds(long long n, const unsigned* __restrict__ sk, int 
   for (int tt = tp + 1; tt <= t; ++tt) tileoff[tt] = i;
 }
 
+// Full fp64 keys of kept per-tile lists (banded frames): the tile of entry i
+// from the offsets (binary search; tiles outside the band are empty ranges).
+__global__ void k_full_keys_off(long long n, const long long* __restrict__ tileoff, int n_tiles,
+                                const unsigned* __restrict__ sv, const Geo* __restrict__ geo,
+                                const double* __restrict__ cdirs, const double* __restrict__ tdirs, CamD cam, OptD opt,
+                                double* out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int lo = 0, hi = n_tiles;  // largest t with tileoff[t] <= i
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (tileoff[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  const unsigned pid = sv[i];
+  out[i] = pair_key(geo[pid], (int)pid, lo, cam, opt, cdirs, tdirs);
+}
+
 // Full fp64 keys of the sorted lists (drk_get_tile_lists).
 __global__ void k_full_keys(long long n, const unsigned* __restrict__ sk, const unsigned* __restrict__ sv, int dbits,
                             const Geo* __restrict__ geo, const double* __restrict__ cdirs,

@@ -249,16 +249,20 @@ struct Pixel {
                                       double dat, double T_i, int comp_idx) const {
     (void)rgb;
     (void)T_i;
-    // deterministic backward: the record's own row (plain adds, fixed order);
-    // otherwise atomics into the primitive's row
-    const bool det_mode = P.det_rec != nullptr;
+    // deterministic mode: the record's own fp64 row (plain adds, fixed order);
+    // otherwise fp32 atomics into the primitive's row
     float* pg = P.gact + (size_t)id * P.G;
-    if (det_mode) {
-      pg = det_row(P, pix % P.cam.W, pix / P.cam.W, comp_idx, id);
-      if (!pg) return;
+    double* dr = nullptr;
+    float* dr32 = nullptr;
+    if (P.det_rec || P.det_rec32) {
+      const long long r = det_row(P, pix % P.cam.W, pix / P.cam.W, comp_idx, id);
+      if (r < 0) return;
+      if (P.det_rec) dr = P.det_rec + (size_t)r * P.G;
+      else dr32 = P.det_rec32 + (size_t)r * P.G;
     }
-    auto gadd = [det_mode](float* a, double v) {
-      if (det_mode) *a += (float)v;
+    auto gadd = [dr, dr32, pg](float* a, double v) {
+      if (dr) dr[a - pg] += v;
+      else if (dr32) dr32[a - pg] += (float)v;
       else atomicAdd(a, (float)v);
     };
     const int K = P.S.K;
@@ -1789,7 +1793,8 @@ void launch_alpha_bound(const ShapeView& S, int n, long long samples, unsigned l
 // ---------------------------------------------------------------------------
 // K6: activation backward (grad.cpp:122-159) + screen_grad (grad.cpp:375-383)
 // ---------------------------------------------------------------------------
-__global__ void k_act_bwd(int n, int K, int terms, const float* __restrict__ raw, const float* __restrict__ gact,
+template <typename GT>
+__global__ void k_act_bwd(int n, int K, int terms, const float* __restrict__ raw, const GT* __restrict__ gact,
                           int G, const unsigned char* __restrict__ touched_dev, const Geo* __restrict__ geo, CamD cam,
                           float* grad_raw, float* d_center_world, float* screen_grad, unsigned char* touched_out,
                           int accumulate) {
@@ -1882,8 +1887,18 @@ void launch_act_bwd(int n, int K, int terms, const float* raw, const float* gact
                     float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
                     cudaStream_t s) {
   if (n == 0) return;
-  k_act_bwd<<<(n + 127) / 128, 128, 0, s>>>(n, K, terms, raw, gact, G, touched_dev, geo, cam, grad_raw,
-                                              d_center_world, screen_grad, touched_out, accumulate);
+  k_act_bwd<float><<<(n + 127) / 128, 128, 0, s>>>(n, K, terms, raw, gact, G, touched_dev, geo, cam, grad_raw,
+                                                     d_center_world, screen_grad, touched_out, accumulate);
+}
+
+// the deterministic backward's fp64 activated-space gradients
+void launch_act_bwd(int n, int K, int terms, const float* raw, const double* gact, int G,
+                    const unsigned char* touched_dev, const Geo* geo, const CamD& cam, float* grad_raw,
+                    float* d_center_world, float* screen_grad, unsigned char* touched_out, int accumulate,
+                    cudaStream_t s) {
+  if (n == 0) return;
+  k_act_bwd<double><<<(n + 127) / 128, 128, 0, s>>>(n, K, terms, raw, gact, G, touched_dev, geo, cam, grad_raw,
+                                                      d_center_world, screen_grad, touched_out, accumulate);
 }
 
 // ---------------------------------------------------------------------------

@@ -28,6 +28,11 @@
 #ifndef DRK_BWDF_MINB
 #define DRK_BWDF_MINB 1
 #endif
+// 1: warp-group sums read the members' rows / SH weights / basis from shared
+// memory (lane = gradient component); 0: register transposes with shuffles
+#ifndef DRK_BWD_SMEM
+#define DRK_BWD_SMEM 1
+#endif
 namespace drk {
 
 namespace {
@@ -328,8 +333,11 @@ __global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fas
   extern __shared__ float4 dyn[];
   Rec* ring = reinterpret_cast<Rec*>(dyn);
   int* s_id = reinterpret_cast<int*>(ring + RING);
-  float* s_basis_all = reinterpret_cast<float*>(s_id + RING);  // [16][NT]
-  float* s_w_all = s_basis_all + 16 * NT;                     // [NT][4]: SH weights per lane
+  // per-pixel SH basis [16][BS]; BS = NT + 1 so that one pixel's 16 terms sit in
+  // distinct banks (the shared-memory group sums read them across lanes)
+  constexpr int BS = DRK_BWD_SMEM ? NT + 1 : NT;
+  float* s_basis_all = reinterpret_cast<float*>(s_id + RING);  // [16][BS]
+  float* s_w_all = s_basis_all + 16 * BS;                     // [NT][4]: SH weights per lane
   float* s_row = s_w_all + 4 * NT;                            // [NT][kGCols]: gradient rows (odd stride: no bank conflicts)
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -363,14 +371,16 @@ __global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fas
     for (int t = 0; t < 16; ++t) b[t] = 0.f;
     sh_basis_f(df[0], df[1], df[2], P.opt.sh_degree, b);
 #pragma unroll
-    for (int t = 0; t < 16; ++t) s_basis[t * NT] = b[t];
+    for (int t = 0; t < 16; ++t) s_basis[t * BS] = b[t];
   }
+#if !DRK_BWD_SMEM
   float bas[16];  // this pixel's SH basis, zero beyond the active terms (SH gradient columns)
   {
     const int ta = P.opt.terms_active;
 #pragma unroll
     for (int t = 0; t < 16; ++t) bas[t] = t < ta ? s_basis[t * NT] : 0.f;
   }
+#endif
   if (threadIdx.x == 0) {
     s_ddmax = 0u;
     tc.d0[0] = d0[0];
@@ -459,7 +469,7 @@ __global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fas
         const double a = o.a;
         // colour (geometry.cpp:126-138) with the clamp, upstream scalars (grad.cpp:224-233)
         float c0, c1, c2;
-        sh_colour<NT>(P, s_basis, id, c0, c1, c2);
+        sh_colour<BS>(P, s_basis, id, c0, c1, c2);
         const bool cl0 = c0 < 0.f, cl1 = c1 < 0.f, cl2 = c2 < 0.f;
         const float r0 = cl0 ? 0.f : c0, r1 = cl1 ? 0.f : c1, r2 = cl2 ? 0.f : c2;
         const double wb = px.T * a;
@@ -483,16 +493,31 @@ __global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fas
         }
         P.touched[id] = 1;
         if (DET) {
-          float* dr = det_row(P, x, y, px.ncomp, id);
-          if (dr) {
+          const long long r = det_row(P, x, y, px.ncomp, id);
+          if (r >= 0 && P.det_rec32) {
+            float* dr = P.det_rec32 + (size_t)r * P.G;
 #pragma unroll
             for (int i = 0; i < kGCols; ++i) dr[gcol_global(i)] = row[i];
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
               if (t < P.opt.terms_active) {
-                dr[kGOffSh + 3 * t] = w0 * bas[t];
-                dr[kGOffSh + 3 * t + 1] = w1 * bas[t];
-                dr[kGOffSh + 3 * t + 2] = w2 * bas[t];
+                const float bt = s_basis[t * BS];
+                dr[kGOffSh + 3 * t] = w0 * bt;
+                dr[kGOffSh + 3 * t + 1] = w1 * bt;
+                dr[kGOffSh + 3 * t + 2] = w2 * bt;
+              }
+            }
+          } else if (r >= 0) {
+            double* dr = P.det_rec + (size_t)r * P.G;
+#pragma unroll
+            for (int i = 0; i < kGCols; ++i) dr[gcol_global(i)] = row[i];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              if (t < P.opt.terms_active) {
+                const float bt = s_basis[t * BS];
+                dr[kGOffSh + 3 * t] = w0 * bt;
+                dr[kGOffSh + 3 * t + 1] = w1 * bt;
+                dr[kGOffSh + 3 * t + 2] = w2 * bt;
               }
             }
           }
@@ -521,6 +546,26 @@ __global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fas
       remaining &= ~gm;
       ++n_groups;
       float* pg = P.gact + (size_t)gid * G;
+#if DRK_BWD_SMEM
+      {
+        // lane = component: non-SH column `lane` (< 31), SH components lane and
+        // 32 + lane (k = 3 t + ch: w_ch basis_t of each member pixel)
+        const int wbase = threadIdx.x & ~31;
+        const int ta = P.opt.terms_active;
+        const int t1 = lane / 3, c1 = lane - 3 * t1, t2 = (32 + lane) / 3, c2 = 32 + lane - 3 * t2;
+        const bool v1 = t1 < ta, v2 = lane < 16 && t2 < ta;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+        for (unsigned mm = gm; mm; mm &= mm - 1u) {
+          const int tm = wbase + __ffs(mm) - 1;
+          if (lane < kGCols) a0 += s_row[kGCols * tm + lane];
+          if (v1) a1 = fmaf(s_w_all[4 * tm + c1], s_basis_all[t1 * BS + tm], a1);
+          if (v2) a2 = fmaf(s_w_all[4 * tm + c2], s_basis_all[t2 * BS + tm], a2);
+        }
+        if (lane < kGCols && a0 != 0.f) atomicAdd(pg + gcol_global(lane), a0);
+        if (v1 && a1 != 0.f) atomicAdd(pg + kGOffSh + lane, a1);
+        if (v2 && a2 != 0.f) atomicAdd(pg + kGOffSh + 32 + lane, a2);
+      }
+#else
       // non-SH columns: transpose-reduce (5 halving steps, 31 shuffles) leaves
       // lane c with the group sum of column c
       {
@@ -587,6 +632,7 @@ __global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fas
           if (!(lane & 1) && xv[0] != 0.f) atomicAdd(pg + kGOffSh + 32 + (lane >> 1), xv[0]);
         }
       }
+#endif
     }
     __syncwarp();
   };
@@ -731,7 +777,7 @@ __global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fas
 }
 
 size_t raster_bwd_fast_smem(int nt) {
-  return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + (16 + 4 + kGCols) * nt * sizeof(float);
+  return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + (16 * (nt + DRK_BWD_SMEM) + (4 + kGCols) * nt) * sizeof(float);
 }
 
 template <int NT, bool DET>

@@ -7,6 +7,7 @@ from paper_2412_11752_b200.api import Rasterizer, RenderOptions, FrameGrad
 
 r = Rasterizer(0)
 r.set_timing(True)
+r.set_counters(True)
 VALIDATE = '--validate' in sys.argv
 sys.argv = [a for a in sys.argv if a != '--validate']
 for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:

@@ -105,17 +105,39 @@ def _crop_parity(rast, sc, cam, o, band_limit_div=0):
     return st, bands, len(orc_bins[1])
 
 
-@pytest.mark.parametrize("view", [0, 1])
-def test_config3_orbit_view_crops(rast, view):
-    """Orbit views of the 1M-primitive scene (camera inside the cluster cloud's
-    reach: near-clipped primitives go through the serial k_prep1 path)."""
+def _centre_crop(cam0, size):
+    return cam0.crop(cam0.width // 2 // 16 * 16 - size // 2, cam0.height // 2 // 16 * 16 - size // 2, size, size)
+
+
+def test_config3_orbit_view_crops(rast):
+    """Two orbit views of the 1M-primitive scene whose binning sends primitives
+    through the large-polygon path (k_prep1: polygons clipped at the near plane,
+    raster.cpp:15-30 / :209, or too many vertices for the warp path): the first
+    two of the 64 views where that counter is nonzero, on a centred 128 x 128
+    crop; at least one of them has such a primitive (centre within 6 largest
+    scales of the camera plane) in the crop's tile lists."""
     sc = scenes.config_scene(3)
-    cam0 = scenes.config_cameras(3)[view]
-    rast.render(sc.f32(), cam0, api_options(ref.Options(sh_degree=3)))
-    assert rast.stats()["poly_overflow"] > 0  # the large-polygon (near-clip) path ran on this view
-    cam = cam0.crop(cam0.width // 2 // 16 * 16 - 64, cam0.height // 2 // 16 * 16 - 64, 128, 128)
-    st, _, pairs = _crop_parity(rast, sc, cam, ref.Options(sh_degree=3, threads=0))
-    assert st["poly_overflow"] > 0 and pairs > 0
+    cams = scenes.config_cameras(3)
+    o = ref.Options(sh_degree=3, threads=0)
+    raw = torch.from_numpy(sc.f32()).cuda()
+    picked = []
+    for v, cam0 in enumerate(cams):
+        rast.render(raw, _centre_crop(cam0, 128), api_options(o))
+        if rast.stats()["poly_overflow"] > 0:
+            picked.append(v)
+        if len(picked) == 2:
+            break
+    assert len(picked) == 2, "no orbit view exercises the large-polygon path"
+    smax = np.exp(sc.raw[7:15].max(axis=0))
+    near_in_lists = 0
+    for v in picked:
+        cam = _centre_crop(cams[v], 128)
+        st, _, pairs = _crop_parity(rast, sc, cam, o)
+        assert st["poly_overflow"] > 0 and pairs > 0
+        z = sc.raw[0:3].T @ np.asarray(cam.R)[2] + np.asarray(cam.t)[2]
+        near = np.nonzero(np.abs(z) < 6 * smax)[0]
+        near_in_lists += int(np.isin(near, rast.tile_binning().prim_ids).any())
+    assert near_in_lists >= 1
 
 
 def test_config4_band(rast):
