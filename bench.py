@@ -526,7 +526,7 @@ def main():
         """Training step: per-rank views, forward + L1 + backward per view (raw gradients
         accumulated), NCCL all-reduce (mean over all views), Adam; max over ranks."""
         from paper_2412_11752_b200.api import OptState, TrainConfig
-        from paper_2412_11752_b200.parallel import allreduce_mean_, params_checksum
+        from paper_2412_11752_b200.parallel import NcclComm, params_checksum
         sc_t = scenes.config_scene(cfg_id)
         base_cam = scenes.config_cameras(cfg_id)[0]
         orbit = scenes.orbit_cameras(views_per_gpu * world, base_cam.width, base_cam.height, seed=4)
@@ -540,6 +540,7 @@ def main():
         tcfg = TrainConfig(steps=35000, lr_drk=1e-3, lr_position=1e-3 / 2.0, lr_rotation=1e-3, lr_opacity=1e-3,
                            lr_sh=1e-3)
         opt_t = RenderOptions(sh_degree=3)
+        comm = NcclComm(r, rank, world)
 
         def step():
             g_t.zero_()
@@ -547,8 +548,9 @@ def main():
                 fb = r.render(p_t, cv, opt_t)
                 _, dcol = r.l1_loss(fb.color, tgt)
                 r.backward_render(p_t, FrameGrad(d_color=dcol), grad_out=g_t, accumulate=True)
-            allreduce_mean_(g_t, views_per_gpu * world)
-            r.adam_step(p_t, g_t, st_t, tcfg, scene_extent=2.0)
+            # native NCCL exchange: reduce-scatter (sum), Adam on this rank's shard
+            # with the 1 / total-views scale folded in, all-gather of the parameters
+            r.allreduce_adam(comm, p_t, g_t, st_t, tcfg, scene_extent=2.0, grad_scale=1.0 / (views_per_gpu * world))
 
         for _ in range(warm):
             step()
@@ -574,20 +576,24 @@ def main():
             dist.all_reduce(cs, op=dist.ReduceOp.MAX)
             in_sync = bool(abs(float(cs[0].item()) + float(cs[1].item())) == 0.0)
         px = base_cam.width * base_cam.height
+        comm.close()
         return {"value": views_per_gpu * world * px / (tr_tot * 1e-3) / 1e6, "unit": "megapixels/s",
-                "ms_per_step": tr_tot, "steps": timed, "warmup": warm, "scaling": "weak", "replicas_in_sync": in_sync}
+                "ms_per_step": tr_tot, "steps": timed, "warmup": warm, "scaling": "weak", "replicas_in_sync": in_sync,
+                "exchange": "drk_allreduce_adam (native NCCL: reduce-scatter, sharded Adam, all-gather)"}
 
     if not args.no_train:
         train = train_leg(2, 2, 1, 2)
         train["workload"] = ("training step with config 4's structure at config 2 scale: 300k DRK, K=8, SH3, 2 orbit "
-                             "views of 1280x720 per GPU, forward + L1 + backward per view, NCCL all-reduce (mean over "
-                             "all views) of the raw gradients, Adam (lr 1e-3); replicas checked by parameter checksum")
+                             "views of 1280x720 per GPU, forward + L1 + backward per view, NCCL reduce-scatter of the raw "
+                             "gradients, Adam (lr 1e-3, mean over all views) on each rank's shard, all-gather; "
+                             "replicas checked by parameter checksum")
     train_c4 = None
     if not args.no_config4_train:
         train_c4 = train_leg(4, 8, 1, 1)
         train_c4["workload"] = ("config 4 training step: 4M DRK, K=8, SH3, 8 orbit views of 3840x2160 per GPU "
-                                "(banded binning), forward + L1 + backward per view, NCCL all-reduce (mean over all "
-                                "views) of the raw gradients, Adam (lr 1e-3); one warm-up step (buffer growth)")
+                                "(banded binning), forward + L1 + backward per view, NCCL reduce-scatter of the raw "
+                                "gradients, Adam (lr 1e-3, mean over all views) on each rank's shard, all-gather; one "
+                                "warm-up step (buffer growth)")
 
     # ---- drop-in adapter (rank 0, N = 1): the reference C++ API served by the GPU ----
     adapter = None

@@ -52,7 +52,8 @@ typedef enum drk_status {
   DRK_ERR_DEGENERATE_FACE = 14,   /* drk::DegenerateFaceError (mesh.cpp:222-258) */
   DRK_ERR_TOO_MANY_VERTICES = 15, /* drk::TooManyVerticesError (mesh.cpp:223-225) */
   DRK_ERR_PARSE = 16,             /* drk::ParseError (mesh.cpp:153-185) */
-  DRK_ERR_EMPTY_MESH = 17         /* drk::EmptyMeshError (mesh.cpp:197) */
+  DRK_ERR_EMPTY_MESH = 17,        /* drk::EmptyMeshError (mesh.cpp:197) */
+  DRK_ERR_COMM = 18               /* NCCL failure (ncclCommGetAsyncError / call status); the communicator is aborted */
 } drk_status;
 
 /* drk::Camera (reference geometry.hpp:9-19). */
@@ -278,6 +279,31 @@ typedef struct drk_adam_config {
  * OptState::step (host value, incremented). */
 int drk_adam_step(drk_ctx* ctx, float* params, const float* grads, float* m, float* v, int n,
                   int k, int sh_terms, int64_t* step, const drk_adam_config* cfg);
+
+/* --- multi-GPU gradient exchange (BASELINE.json config 4) --
+ * The reference has no distributed path: the multi-view gradient is the mean
+ * over views of per-view backward_render.  One process per
+ * GPU; NCCL is loaded at drk_comm_init (dlopen of libnccl.so.2: the copy a
+ * host framework already loaded, else the system's), so the library has no
+ * link-time NCCL dependency.  Calls are ordered on the context's stream; NCCL
+ * failures are detected with ncclCommGetAsyncError while waiting and abort
+ * the communicator (DRK_ERR_COMM). */
+typedef struct drk_comm drk_comm;
+/* 128-byte NCCL unique id, created by rank 0 and shared by the caller. */
+int drk_comm_unique_id(uint8_t id_out[128]);
+int drk_comm_init(drk_ctx* ctx, const uint8_t id[128], int nranks, int rank, drk_comm** out);
+void drk_comm_destroy(drk_comm* comm);
+/* In-place sum over the ranks of `count` floats (device). */
+int drk_allreduce_sum(drk_ctx* ctx, drk_comm* comm, float* buf, int64_t count);
+/* One training-step exchange + update: the raw-gradient buffers (SoA f32,
+ * like drk_adam_step) are reduce-scattered (sum) across the ranks, each rank
+ * applies drk::adam_step (reference optimize.cpp:259-307, gradients scaled by
+ * cfg->grad_scale, normally 1 / total views) to its contiguous shard of the
+ * scalars, and the updated parameters are all-gathered: every rank ends with
+ * the same parameters, 1/N of the Adam work each.  m and v are full-size but
+ * a rank only ever reads and writes its own shard of them. */
+int drk_allreduce_adam(drk_ctx* ctx, drk_comm* comm, float* params, float* grads, float* m, float* v, int n, int k,
+                       int sh_terms, int64_t* step, const drk_adam_config* cfg);
 
 /* drk::eval_sorting (raster.cpp:487-560) of the last forward on this context
  * (its camera, presort and use_cache): out4 (host) = {accuracy, kendall_tau,

@@ -184,6 +184,12 @@ SIGNATURES = {
     "drk_debug_alpha_bound": (C.c_int, [_P, C.c_int64, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "drk_adam_step": (C.c_int, [_P, _P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                 C.POINTER(AdamConfig_)]),
+    "drk_comm_unique_id": (C.c_int, [_P]),
+    "drk_comm_init": (C.c_int, [_P, _P, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "drk_comm_destroy": (None, [_P]),
+    "drk_allreduce_sum": (C.c_int, [_P, _P, _P, C.c_int64]),
+    "drk_allreduce_adam": (C.c_int, [_P, _P, _P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
+                                     C.POINTER(AdamConfig_)]),
 }
 
 _lib = None

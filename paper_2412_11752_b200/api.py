@@ -621,6 +621,24 @@ class Rasterizer:
                                              terms, C.byref(step), C.byref(a)))
         state.step = step.value
 
+    def allreduce_adam(self, comm, params: torch.Tensor, grads: torch.Tensor, state: OptState, cfg: TrainConfig,
+                       scene_extent: float, grad_scale: float, k: int = 8):
+        """drk_allreduce_adam: gradients summed across the communicator's ranks
+        (reduce-scatter), Adam on this rank's shard (gradients x grad_scale, e.g.
+        1 / total views), parameters all-gathered; in place, every rank equal."""
+        if params.shape != grads.shape or params.shape != state.m.shape:
+            raise DimensionMismatchError("optimizer shapes out of sync")
+        S, n = params.shape
+        terms = (S - (3 + 4 + 2 * k + 3)) // 3
+        a = _lib.AdamConfig_(cfg.lr_drk, cfg.lr_position, cfg.lr_rotation, cfg.lr_opacity, cfg.lr_sh, cfg.steps,
+                             int(cfg.freeze_eta_tau), int(cfg.freeze_angles), 0, float(scene_extent),
+                             float(grad_scale))
+        step = C.c_int64(state.step)
+        self._sync_stream()
+        self._check(_lib.lib().drk_allreduce_adam(self._h, comm.handle, _ptr(params), _ptr(grads), _ptr(state.m),
+                                                  _ptr(state.v), n, k, terms, C.byref(step), C.byref(a)))
+        state.step = step.value
+
 
 @dataclass
 class DensifyStats:

@@ -17,7 +17,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 SOURCES = {"drk_prep.cu": False, "drk_sort.cu": False, "drk_raster.cu": True, "drk_raster_fast.cu": True, "drk_raster_bwd.cu": True,
-           "drk_capi.cu": False, "drk_scene.cu": False, "drk_loss.cu": False, "drk_train.cu": False, "drk_mesh.cu": False, "drk_det.cu": False}
+           "drk_capi.cu": False, "drk_scene.cu": False, "drk_loss.cu": False, "drk_train.cu": False, "drk_mesh.cu": False, "drk_det.cu": False,
+           "drk_comm.cu": False}
 LIB = os.path.join(HERE, "libdrk_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -53,7 +54,7 @@ def build(verbose: bool = False, extra=None, jobs: int = 4) -> str:
         if p.wait() != 0:
             raise RuntimeError(f"nvcc failed on {name}")
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

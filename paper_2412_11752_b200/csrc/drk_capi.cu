@@ -870,6 +870,7 @@ const char* drk_status_string(int s) {
     case DRK_ERR_TOO_MANY_VERTICES: return "too many vertices";
     case DRK_ERR_PARSE: return "parse error";
     case DRK_ERR_EMPTY_MESH: return "empty mesh";
+    case DRK_ERR_COMM: return "communication error";
   }
   return "unknown status";
 }
@@ -956,7 +957,8 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->loss_part, &c->ssim_f, &c->dens_code, &c->dens_pos,
                     &c->eval_scr, &c->eval_px, &c->eval_off, &c->ovf_scr, &c->ovf_list, &c->tord,
                     &c->rowest, &c->host_raw, &c->host_img, &c->pxcomp, &c->det_cnt, &c->det_base,
-                    &c->det_rec, &c->det_id, &c->det_tile, &c->det_sort, &c->det_poff, &c->det_acc, &c->det_rowoff};
+                    &c->det_rec, &c->det_id, &c->det_tile, &c->det_sort, &c->det_poff, &c->det_acc, &c->det_rowoff,
+                    &c->comm_buf, &c->scan_tmp2, &c->replay_cid, &c->replay_cval};
   for (DevBuf* b : bufs) release(*b);
   for (DevBuf& b : c->band_ids) release(b);
   for (DevBuf& b : c->band_off) release(b);
@@ -1263,6 +1265,18 @@ int drk_get_framebuffers_f64(drk_ctx* c, double* color, double* depth, double* n
   return DRK_OK;
 }
 
+__global__ void k_replay_compact(long long npix, int cap, const int* __restrict__ cnt, const long long* __restrict__ off,
+                                 const int* __restrict__ ids, const double* __restrict__ rec, int* cid, double* cval) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= npix) return;
+  const int n = min(cnt[p], cap);
+  const long long o = off[p];
+  for (int j = 0; j < n; ++j) {
+    cid[o + j] = ids[p * cap + j];
+    for (int q = 0; q < 5; ++q) cval[5 * (o + j) + q] = rec[5 * (p * cap + j) + q];
+  }
+}
+
 int drk_get_replay(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* ids, double* vals) {
   if (!c || !c->has_fwd || c->opt.record_replay <= 0)
     return c ? set_error(c, DRK_ERR_INVALID_ARG, "no replay recorded") : DRK_ERR_INVALID_ARG;
@@ -1276,22 +1290,24 @@ int drk_get_replay(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* ids, d
   int64_t tot = 0;
   for (size_t p = 0; p < npix; ++p) tot += cnt[p];
   if (total) *total = tot;
-  if (!offsets && !ids && !vals) return DRK_OK;
-  std::vector<int> rid(npix * cap);
-  std::vector<double> rv(5 * npix * cap);
-  cudaMemcpyAsync(rid.data(), c->replay_ids.p, sizeof(int) * rid.size(), cudaMemcpyDeviceToHost, c->stream);
-  cudaMemcpyAsync(rv.data(), c->replay_rec.p, sizeof(double) * rv.size(), cudaMemcpyDeviceToHost, c->stream);
-  if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "replay")) return st;
-  int64_t o = 0;
-  if (offsets) offsets[0] = 0;
-  for (size_t p = 0; p < npix; ++p) {
-    for (int j = 0; j < cnt[p]; ++j, ++o) {
-      if (ids) ids[o] = rid[p * cap + j];
-      if (vals) std::memcpy(vals + 5 * o, &rv[5 * (p * cap + j)], 5 * sizeof(double));
-    }
-    if (offsets) offsets[p + 1] = o;
+  if (offsets) {
+    offsets[0] = 0;
+    for (size_t p = 0; p < npix; ++p) offsets[p + 1] = offsets[p] + cnt[p];
   }
-  return DRK_OK;
+  if ((!ids && !vals) || tot == 0) return DRK_OK;
+  // compact the per-pixel slots (npix x cap) on the device; copy only the records
+  long long* off_d = ensure<long long>(c->scan_tmp2, npix + 1);
+  int* cid = ensure<int>(c->replay_cid, (size_t)tot);
+  double* cval = ensure<double>(c->replay_cval, 5 * (size_t)tot);
+  if (!off_d || !cid || !cval) return set_error(c, DRK_ERR_OOM, "replay compaction");
+  if (int st = exclusive_scan<int>(c, static_cast<const int*>(c->replay_cnt.p), (long long)npix, off_d, nullptr))
+    return st;
+  k_replay_compact<<<(unsigned)((npix + 255) / 256), 256, 0, c->stream>>>(
+      (long long)npix, cap, static_cast<const int*>(c->replay_cnt.p), off_d, static_cast<const int*>(c->replay_ids.p),
+      static_cast<const double*>(c->replay_rec.p), cid, cval);
+  if (ids) cudaMemcpyAsync(ids, cid, sizeof(int) * tot, cudaMemcpyDeviceToHost, c->stream);
+  if (vals) cudaMemcpyAsync(vals, cval, sizeof(double) * 5 * tot, cudaMemcpyDeviceToHost, c->stream);
+  return cuda_check(c, cudaStreamSynchronize(c->stream), "replay");
 }
 
 int drk_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* grad_raw, float* d_center_world,

@@ -243,6 +243,10 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
       DRK_COUNT_LAUNCH();
     }
   }
+  // record scratch can reach tens of GB on large frames: give it back
+  constexpr size_t kKeep = 256u << 20;
+  for (DevBuf* b : {&c->det_rec, &c->det_id, &c->det_tile, &c->det_sort})
+    if (b->bytes > kKeep) release(*b);
   unsigned long long ovf = 0;
   cudaMemcpyAsync(&ovf, P.counters + C_DET_OVERFLOW, sizeof ovf, cudaMemcpyDeviceToHost, s);
   if (int st = cuda_check(c, cudaStreamSynchronize(s), "deterministic backward")) return st;

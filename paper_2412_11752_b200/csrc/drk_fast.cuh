@@ -116,8 +116,14 @@ struct TileConst {
   float ddmax;
 };
 
+__device__ __forceinline__ void stage_record_from(const RasterParams& P, const Geo& g, const TileConst& tc, Rec& R);
 __device__ __forceinline__ void stage_record(const RasterParams& P, int id, const TileConst& tc, Rec& R) {
-  const Geo& g = P.geo[id];
+  stage_record_from(P, P.geo[id], tc, R);
+}
+
+// g: the primitive's Geo record (global, or a shared-memory copy staged by
+// cp.async.bulk in the fast forward)
+__device__ __forceinline__ void stage_record_from(const RasterParams& P, const Geo& g, const TileConst& tc, Rec& R) {
   const double d00 = tc.d0[0], d01 = tc.d0[1], d02 = tc.d0[2], tx0 = tc.tx0, ty0 = tc.ty0;
   const double ddmax = tc.ddmax;
   const double a0 = P.cam.o[0] - g.mu[0], a1 = P.cam.o[1] - g.mu[1], a2 = P.cam.o[2] - g.mu[2];
@@ -151,7 +157,7 @@ __device__ __forceinline__ void stage_record(const RasterParams& P, int id, cons
   R.r2 = make_float4((float)gv[0], (float)gv[1], (float)gv[2], nv0h);
   R.r5 = make_float4((float)(dz0 - (double)dz0h), (float)(nu0 - (double)nu0h), (float)(nv0 - (double)nv0h), 0.f);
   R.r3 = make_float4((float)g.num, (float)ez, (float)eN, (float)g.r2max);
-  const float fvis2 = P.S.psif[12 * (size_t)id + 8];
+  const float fvis2 = g.fvis2;
   R.r4 = g.has_proj ? make_float4((float)(g.ppx - tx0), (float)(g.ppy - ty0), (float)g.dp2max, fvis2)
                     : make_float4(0.f, 0.f, -1.f, fvis2);
 }

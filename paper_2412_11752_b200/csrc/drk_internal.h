@@ -62,7 +62,10 @@ struct Geo {
   double dp2max;           // 2 s_l^2 ln(o / alpha_min) (1+1e-9): low-pass floor bound / cos^2
   int has_proj;
   int visible;
+  float fvis2;             // f_vis^2 (fp32, as ShapeView psif[12 i + 8])
+  int pad_;                // 160 bytes: a multiple of 16 (cp.async.bulk staging of the fast forward)
 };
+static_assert(sizeof(Geo) == 160, "Geo record size");
 
 struct Activated {
   const double *mu, *rot, *s, *th, *eta, *tau, *o;
@@ -184,6 +187,8 @@ struct drk_ctx {
   // sort buffers, per-primitive offsets, fp64 accumulator
   drk::DevBuf det_cnt, det_base, det_rec, det_id, det_tile, det_sort, det_poff, det_acc, det_rowoff;
   long long det_chunk_limit = 0;          // test hook: records per chunk (0 = memory-based)
+  drk::DevBuf comm_buf;                   // drk_allreduce_adam: padded gradient / parameter exchange buffers
+  drk::DevBuf scan_tmp2, replay_cid, replay_cval;  // drk_get_replay: per-pixel offsets, compacted records
   int64_t hull_cap = 0;
   drk::DevBuf rowest;
   std::vector<int> bands;         // tile-row band boundaries of the last forward
@@ -236,6 +241,9 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
 int run_l1_loss(drk_ctx* c, const float* r, const float* t, int w, int h, double* loss, float* dcol);
 int run_adam(drk_ctx* c, float* params, const float* grads, float* m, float* v, int n, int K, int terms,
              int64_t step, const drk_adam_config* cfg);
+// Adam on scalars [e0, e1) of the SoA parameters; gradient of scalar e at grads[e - g0]
+int run_adam_range(drk_ctx* c, float* params, const float* grads, long long g0, float* m, float* v, int n, int K,
+                   long long e0, long long e1, int64_t step, const drk_adam_config* cfg);
 int set_error(drk_ctx* c, int status, const std::string& msg);
 int cuda_check(drk_ctx* c, cudaError_t e, const char* where);
 

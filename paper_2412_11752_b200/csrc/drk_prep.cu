@@ -345,6 +345,8 @@ __device__ __forceinline__ void prep_body(Activated A, CamD cam, OptD opt, Geo* 
     for (int j = 0; j < K; ++j) smax = dmax(smax, A.s[(size_t)K * i + j]);
     g.r2max = g.visible ? (smax * fv) * (smax * fv) * (1.0 + 1e-9) : 0.0;
     const_cast<float*>(A.psif)[12 * (size_t)i + 8] = g.visible ? (float)(fv * fv) : __int_as_float(0x7f800000);
+    g.fvis2 = A.psif[12 * (size_t)i + 8];
+    g.pad_ = 0;
     g.dp2max = g.visible ? 2.0 * opt.lowpass_radius * opt.lowpass_radius * log(o / opt.alpha_min) * (1.0 + 1e-9) : 0.0;
     geo[i] = g;
     rowcnt[i] = 0;
@@ -525,6 +527,8 @@ __global__ void __launch_bounds__(kPW * 32) k_prep_warp(Activated A, CamD cam, O
     for (int j = 0; j < K; ++j) smax = dmax(smax, A.s[(size_t)K * i + j]);
     g.r2max = visible ? (smax * fv) * (smax * fv) * (1.0 + 1e-9) : 0.0;
     const_cast<float*>(A.psif)[12 * (size_t)i + 8] = visible ? (float)(fv * fv) : __int_as_float(0x7f800000);
+    g.fvis2 = visible ? (float)(fv * fv) : __int_as_float(0x7f800000);
+    g.pad_ = 0;
     g.dp2max = visible ? 2.0 * opt.lowpass_radius * opt.lowpass_radius * log(o / opt.alpha_min) * (1.0 + 1e-9) : 0.0;
     geo[i] = g;
     if (frame32) {

@@ -1934,11 +1934,13 @@ void launch_l1(long long n, const float* r, const float* t, double* loss, float*
 // K8: Adam (optimize.cpp:226-307): beta (0.9, 0.999), eps 1e-15, bias
 // corrected, per-class learning rates, SH rows >= 1 at lr_sh / 20.
 // ---------------------------------------------------------------------------
-__global__ void k_adam(long long total, int n, int K, float* p, const float* __restrict__ gr, float* m, float* v,
-                       double bc1, double bc2, double lr_center, double lr_quat, double lr_scale, double lr_angle,
-                       double lr_eta, double lr_tau, double lr_op, double lr_sh, double lr_sh_rest,
+// scalars e in [e0, e1) of the SoA parameters (a rank's shard in drk_allreduce_adam);
+// the gradient of scalar e is gr[e - g0]
+__global__ void k_adam(long long e0, long long e1, long long g0, int n, int K, float* p, const float* __restrict__ gr,
+                       float* m, float* v, double bc1, double bc2, double lr_center, double lr_quat, double lr_scale,
+                       double lr_angle, double lr_eta, double lr_tau, double lr_op, double lr_sh, double lr_sh_rest,
                        double grad_scale) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+  for (long long e = e0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e1;
        e += (long long)gridDim.x * blockDim.x) {
     const int s = (int)(e / n);
     double lr;
@@ -1950,7 +1952,7 @@ __global__ void k_adam(long long total, int n, int K, float* p, const float* __r
     else if (s == 8 + 2 * K) lr = lr_tau;
     else if (s == 9 + 2 * K) lr = lr_op;
     else lr = (s - (10 + 2 * K)) < 3 ? lr_sh : lr_sh_rest;
-    const double g = (double)gr[e] * grad_scale;
+    const double g = (double)gr[e - g0] * grad_scale;
     const double mm = 0.9 * (double)m[e] + (1.0 - 0.9) * g;
     const double vv = 0.999 * (double)v[e] + (1.0 - 0.999) * g * g;
     m[e] = (float)mm;
@@ -1963,6 +1965,12 @@ __global__ void k_adam(long long total, int n, int K, float* p, const float* __r
 int run_adam(drk_ctx* c, float* params, const float* grads, float* m, float* v, int n, int K, int terms,
              int64_t step, const drk_adam_config* cfg) {
   const long long total = (long long)(3 + 4 + 2 * K + 3 + 3 * terms) * n;
+  return run_adam_range(c, params, grads, 0, m, v, n, K, 0, total, step, cfg);
+}
+
+int run_adam_range(drk_ctx* c, float* params, const float* grads, long long g0, float* m, float* v, int n, int K,
+                   long long e0, long long e1, int64_t step, const drk_adam_config* cfg) {
+  const long long total = e1 - e0;
   const double bc1 = 1.0 - pow(0.9, (double)step);
   const double bc2 = 1.0 - pow(0.999, (double)step);
   const double t = cfg->steps > 0 ? dmin(1.0, (double)step / cfg->steps) : 1.0;
@@ -1971,7 +1979,7 @@ int run_adam(drk_ctx* c, float* params, const float* grads, float* m, float* v, 
   const double lr_sh = cfg->lr_sh;
   if (total > 0) {
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-    k_adam<<<blocks, 256, 0, c->stream>>>(total, n, K, params, grads, m, v, bc1, bc2,
+    k_adam<<<blocks, 256, 0, c->stream>>>(e0, e1, g0, n, K, params, grads, m, v, bc1, bc2,
                                            cfg->lr_position * cfg->scene_extent * decay, cfg->lr_rotation, lr_drk,
                                            cfg->freeze_angles ? 0.0 : lr_drk, cfg->freeze_eta_tau ? 0.0 : lr_drk,
                                            cfg->freeze_eta_tau ? 0.0 : lr_drk, cfg->lr_opacity, lr_sh, lr_sh / 20.0,

@@ -31,7 +31,7 @@
 // 1: warp-group sums read the members' rows / SH weights / basis from shared
 // memory (lane = gradient component); 0: register transposes with shuffles
 #ifndef DRK_BWD_SMEM
-#define DRK_BWD_SMEM 1
+#define DRK_BWD_SMEM 0  // measured on config 2: 47.8 ms with 1, 47.0 ms with 0 (groups average 18 lanes)
 #endif
 namespace drk {
 

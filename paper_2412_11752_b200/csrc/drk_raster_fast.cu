@@ -34,6 +34,18 @@
 // explicitly rounded intrinsics (__dmul_rn / __dadd_rn).
 #include "drk_fast.cuh"
 
+// 1: the next batch's Geo records are gathered into shared memory with
+// cp.async.bulk (one 160-byte bulk copy per entry, completion on an mbarrier)
+// while the current batch streams; 0: synchronous loads at staging time.
+#ifndef DRK_TMA_STAGE
+#define DRK_TMA_STAGE 1
+#endif
+// 1: the streaming loop takes two candidates per iteration (both intersections,
+// then both cache steps): independent instructions for the scheduler
+#ifndef DRK_ISECT2
+#define DRK_ISECT2 0
+#endif
+
 
 namespace drk {
 
@@ -88,6 +100,36 @@ void launch_shape_rec(const ShapeView& S, int n, float* rec, cudaStream_t s) {
   }
 }
 
+// --- mbarrier + 1-D bulk copy (TMA engine, sm_90+) --------------------------
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 __device__ __forceinline__ void write_pixel(const RasterParams& P, const FastPixel& px, int x, int y);
 
 // NT threads per CTA: 256 = one 16x16 tile per CTA; 128 = half a tile (8 x 16
@@ -100,6 +142,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   Rec* ring = reinterpret_cast<Rec*>(dyn);
   int* s_id = reinterpret_cast<int*>(ring + RING);
   float4* s_b4 = reinterpret_cast<float4*>(s_id + RING) + threadIdx.x;  // [4][NT] float4, this thread's column
+#if DRK_TMA_STAGE
+  Geo* s_geo = reinterpret_cast<Geo*>(reinterpret_cast<float4*>(s_id + RING) + 4 * NT);  // [NT]: next batch's Geo
+  __shared__ unsigned long long s_bar;
+#endif
   __shared__ unsigned s_ddmax, s_done;
   __shared__ TileConst tc;
   const int cta_tile = NT == 256 ? blockIdx.x : blockIdx.x >> 1;
@@ -166,9 +212,139 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   __syncthreads();
   if (threadIdx.x == 0) tc.ddmax = __uint_as_float(s_ddmax) * 1.0001f + 1e-30f;
   int ring_lo = 0;
+  // ray-plane intersection of stream entry jr (geometry.cpp:40-47) as an fp32
+  // interval [lo, hi] containing the exact fp64 r_t; false: grazing / behind
+  auto isect = [&](int jr, float& lo, float& hi) -> bool {
+    const int slot = jr & (RING - 1);
+    const float4 r0 = ring[slot].r0;
+    const float2 r3 = *reinterpret_cast<const float2*>(&ring[slot].r3);
+    const float dz = lin3(r0, ring[slot].r5.x, px.ddx, px.ddy, px.ddz);
+    const float adz = fabsf(dz);
+    if (adz < eps - r3.y) return false;  // certainly grazing
+    const float inv = rcp_nr(dz);
+    const float rel_z = r3.y * fabsf(inv);
+    if (adz > eps + r3.y && r3.x != 0.f && rel_z <= 1e-3f) {
+      const float rt = r3.x * inv;
+      if (rt <= 0.f) return false;
+      // num (2^-24), 1/dz (2^-23), product (2^-24), dz (rel_z), interval ends
+      const float er = rt * (3.3e-7f + rel_z * 1.01f);
+      lo = rt - er;
+      hi = rt + er;
+      return true;
+    }
+    double rx;
+    if (!exact_rt(P, s_id[slot], x, y, &rx)) return false;
+    lo = __double2float_rd(rx);
+    hi = __double2float_ru(rx);
+    return true;
+  };
+  // SortCache::step (raster.cpp:267-303) for a hit of entry jr on intervals
+  // that contain the exact depths, popping (pop_eval) when full; false once the
+  // pixel saturates
+  auto cache_step = [&](int jr, float lo, float hi) -> bool {
+    DRK_STAT(n_str);
+    bool le[kCacheCap];
+    bool amb = false;
+#pragma unroll
+    for (int q = 0; q < kCacheCap; ++q) {
+      le[q] = chi[q] <= lo;
+      amb |= !le[q] && !(clo[q] > hi);
+    }
+    if (amb) {
+      // overlapping intervals: compare the exact fp64 depths
+      DRK_STAT(n_amb);
+      double rin = 0;
+      exact_rt(P, s_id[jr & (RING - 1)], x, y, &rin);
+      lo = __double2float_rd(rin);
+      hi = __double2float_ru(rin);
+#pragma unroll
+      for (int q = 0; q < kCacheCap; ++q) {
+        if (!le[q]) {
+          if (chi[q] <= lo) {
+            le[q] = true;
+          } else if (!(clo[q] > hi)) {
+            double rq = 0;
+            exact_rt(P, entry_id<RING>(P, s_id, beg, cj[q], ring_lo), x, y, &rq);
+            le[q] = rq <= rin;
+            clo[q] = __double2float_rd(rq);
+            chi[q] = __double2float_ru(rq);
+          }
+        }
+      }
+    }
+    if (csz < kCacheCap) {
+#pragma unroll
+      for (int q = kCacheCap - 1; q >= 0; --q) {
+        const bool prev = q == 0 ? true : le[q - 1];
+        if (!le[q]) {
+          clo[q] = prev ? lo : clo[q - 1];
+          chi[q] = prev ? hi : chi[q - 1];
+          cj[q] = prev ? jr : cj[q - 1];
+        }
+      }
+      ++csz;
+      return true;
+    }
+    int pj;
+    if (!le[0]) {  // incoming strictly shallower than the head: pops through
+      pj = jr;
+    } else {
+      pj = cj[0];
+#pragma unroll
+      for (int q = 0; q < kCacheCap; ++q) {
+        const bool nxt = q + 1 < kCacheCap ? le[q + 1] : false;
+        if (nxt) {
+          clo[q] = clo[q + 1];
+          chi[q] = chi[q + 1];
+          cj[q] = cj[q + 1];
+        } else if (le[q]) {
+          clo[q] = lo;
+          chi[q] = hi;
+          cj[q] = jr;
+        }
+      }
+    }
+    return pop_eval<VALIDATE, NT, STATS>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y);
+  };
+#if DRK_TMA_STAGE
+  // batch b's Geo records arrive in s_geo by bulk copies issued while batch b-1
+  // streamed (thread j copies entry j of the batch); s_bar completes one phase
+  // per batch
+  unsigned gpar = 0;
+  int my_id = 0;
+  bool pending = false;
+  auto prefetch = [&](long long b0n) {
+    const int cntn = (int)min((long long)NT, end - b0n);
+    if (threadIdx.x == 0) mbar_expect_tx(&s_bar, (unsigned)(cntn * sizeof(Geo)));
+    fence_proxy_async();  // s_geo was last read by the generic proxy
+    if ((int)threadIdx.x < cntn) {
+      my_id = P.lid[b0n + threadIdx.x];
+      bulk_g2s(s_geo + threadIdx.x, P.geo + my_id, (unsigned)sizeof(Geo), &s_bar);
+    }
+    pending = true;
+  };
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  if (beg < end) prefetch(beg);
+#endif
   for (long long b0 = beg; b0 < end; b0 += NT) {
     const int jb = (int)(b0 - beg);
     __syncthreads();
+#if DRK_TMA_STAGE
+    mbar_wait(&s_bar, gpar);
+    gpar ^= 1u;
+    pending = false;
+    {
+      const long long j = b0 + threadIdx.x;
+      if (j < end) {
+        const int slot = (jb + threadIdx.x) & (RING - 1);
+        stage_record_from(P, s_geo[threadIdx.x], tc, ring[slot]);
+        s_id[slot] = my_id;
+      }
+    }
+    __syncthreads();
+    if (b0 + NT < end) prefetch(b0 + NT);
+#else
     {
       const long long j = b0 + threadIdx.x;
       if (j < end) {
@@ -179,104 +355,47 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
       }
     }
     __syncthreads();
+#endif
     ring_lo = jb >= NT ? jb - NT : 0;
     const int cnt = (int)min((long long)NT, end - b0);
     if (!done) {
-      for (int c = 0; c < cnt; ++c) {
-        const int jr = jb + c;
-        const int slot = jr & (RING - 1);
-        const float4 r0 = ring[slot].r0;
-        const float2 r3 = *reinterpret_cast<const float2*>(&ring[slot].r3);
-        const float dz = lin3(r0, ring[slot].r5.x, px.ddx, px.ddy, px.ddz);
-        const float adz = fabsf(dz);
-        float lo, hi;
-        if (adz < eps - r3.y) continue;  // certainly grazing
-        const float inv = rcp_nr(dz);
-        const float rel_z = r3.y * fabsf(inv);
-        if (adz > eps + r3.y && r3.x != 0.f && rel_z <= 1e-3f) {
-          const float rt = r3.x * inv;
-          if (rt <= 0.f) continue;
-          // num (2^-24), 1/dz (2^-23), product (2^-24), dz (rel_z), interval ends
-          const float er = rt * (3.3e-7f + rel_z * 1.01f);
-          lo = rt - er;
-          hi = rt + er;
-        } else {
-          double rx;
-          if (!exact_rt(P, s_id[slot], x, y, &rx)) continue;
-          lo = __double2float_rd(rx);
-          hi = __double2float_ru(rx);
+#if DRK_ISECT2
+      // two candidates per iteration: both ray-plane intersections first
+      // (independent work for the scheduler), then the two cache steps in order
+      int c = 0;
+      for (; c + 1 < cnt; c += 2) {
+        float lo0, hi0, lo1, hi1;
+        const bool h0 = isect(jb + c, lo0, hi0);
+        const bool h1 = isect(jb + c + 1, lo1, hi1);
+        if (h0 && !cache_step(jb + c, lo0, hi0)) {
+          done = true;
+          break;
         }
-        DRK_STAT(n_str);
-        // SortCache::step (raster.cpp:267-303) on exact-containing intervals
-        bool le[kCacheCap];
-        bool amb = false;
-#pragma unroll
-        for (int q = 0; q < kCacheCap; ++q) {
-          le[q] = chi[q] <= lo;
-          amb |= !le[q] && !(clo[q] > hi);
-        }
-        if (amb) {
-          // overlapping intervals: compare the exact fp64 depths
-          DRK_STAT(n_amb);
-          double rin = 0;
-          exact_rt(P, s_id[slot], x, y, &rin);
-          lo = __double2float_rd(rin);
-          hi = __double2float_ru(rin);
-#pragma unroll
-          for (int q = 0; q < kCacheCap; ++q) {
-            if (!le[q]) {
-              if (chi[q] <= lo) {
-                le[q] = true;
-              } else if (!(clo[q] > hi)) {
-                double rq = 0;
-                exact_rt(P, entry_id<RING>(P, s_id, beg, cj[q], ring_lo), x, y, &rq);
-                le[q] = rq <= rin;
-                clo[q] = __double2float_rd(rq);
-                chi[q] = __double2float_ru(rq);
-              }
-            }
-          }
-        }
-        if (csz < kCacheCap) {
-#pragma unroll
-          for (int q = kCacheCap - 1; q >= 0; --q) {
-            const bool prev = q == 0 ? true : le[q - 1];
-            if (!le[q]) {
-              clo[q] = prev ? lo : clo[q - 1];
-              chi[q] = prev ? hi : chi[q - 1];
-              cj[q] = prev ? jr : cj[q - 1];
-            }
-          }
-          ++csz;
-          continue;
-        }
-        int pj;
-        if (!le[0]) {  // incoming strictly shallower than the head: pops through
-          pj = jr;
-        } else {
-          pj = cj[0];
-#pragma unroll
-          for (int q = 0; q < kCacheCap; ++q) {
-            const bool nxt = q + 1 < kCacheCap ? le[q + 1] : false;
-            if (nxt) {
-              clo[q] = clo[q + 1];
-              chi[q] = chi[q + 1];
-              cj[q] = cj[q + 1];
-            } else if (le[q]) {
-              clo[q] = lo;
-              chi[q] = hi;
-              cj[q] = jr;
-            }
-          }
-        }
-        if (!pop_eval<VALIDATE, NT, STATS>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y)) {
+        if (h1 && !cache_step(jb + c + 1, lo1, hi1)) {
           done = true;
           break;
         }
       }
+      if (!done && c < cnt) {
+        float lo0, hi0;
+        if (isect(jb + c, lo0, hi0) && !cache_step(jb + c, lo0, hi0)) done = true;
+      }
+#else
+      for (int c = 0; c < cnt; ++c) {
+        float lo, hi;
+        if (!isect(jb + c, lo, hi)) continue;
+        if (!cache_step(jb + c, lo, hi)) {
+          done = true;
+          break;
+        }
+      }
+#endif
     }
     if (__syncthreads_count(!done) == 0) break;
   }
+#if DRK_TMA_STAGE
+  if (pending) mbar_wait(&s_bar, gpar);  // no bulk copy may land after the CTA exits
+#endif
   // end marker: drain the cache head first (raster.cpp:410-414)
   while (!done && csz > 0) {
     const int pj = cj[0];
@@ -373,7 +492,9 @@ void launch_tile_order_keys(int n, int tiles_x, int band_rows, const long long* 
   if (n > 0) k_tile_order_keys<<<(n + 255) / 256, 256, 0, s>>>(n, tiles_x, band_rows, tileoff, tile_base, key, id);
 }
 
-size_t raster_fast_smem(int nt) { return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + 16 * nt * sizeof(float); }
+size_t raster_fast_smem(int nt) {
+  return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + 16 * nt * sizeof(float) + (DRK_TMA_STAGE ? nt * sizeof(Geo) : 0);
+}
 
 // Half-tile CTAs pay off once tile lists are long (measured: config 2 / 3 with
 // ~9.5k / 28k entries per tile -3% / -2.3% raster time, config 1 with 2.2k

@@ -47,6 +47,51 @@ def allreduce_mean_(grad, total_views: int, group=None):
     return grad
 
 
+class NcclComm:
+    """Native NCCL communicator of a Rasterizer's device (drk_comm_init; the
+    unique id is created by rank 0 and broadcast over the torch.distributed
+    process group, or passed in).  Used by the training step's gradient
+    exchange (Rasterizer.allreduce_adam: reduce-scatter, sharded Adam,
+    all-gather) and drk_allreduce_sum."""
+
+    def __init__(self, rast, rank: int = 0, world: int = 1, uid: bytes | None = None, group=None):
+        import ctypes as C
+
+        from . import _lib
+        if uid is None:
+            buf = (C.c_uint8 * 128)()
+            if rank == 0:
+                _lib.check(_lib.lib().drk_comm_unique_id(buf))
+            if world > 1:
+                import torch.distributed as dist
+                obj = [bytes(buf) if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                uid = obj[0]
+            else:
+                uid = bytes(buf)
+        raw = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self.handle = C.c_void_p()
+        self._rast = rast
+        rast._check(_lib.lib().drk_comm_init(rast._h, raw, int(world), int(rank), C.byref(self.handle)))
+        self.rank, self.world = rank, world
+
+    def allreduce_sum_(self, buf):
+        """In-place sum over the ranks (f32 device tensor)."""
+        import ctypes as C
+
+        from . import _lib
+        self._rast._sync_stream()
+        self._rast._check(_lib.lib().drk_allreduce_sum(self._rast._h, self.handle, C.c_void_p(buf.data_ptr()),
+                                                       buf.numel()))
+        return buf
+
+    def close(self):
+        from . import _lib
+        if self.handle:
+            _lib.lib().drk_comm_destroy(self.handle)
+            self.handle = None
+
+
 def params_checksum(params) -> float:
     """Order-independent fp64 checksum used to verify that replicas stay in sync."""
     import torch

@@ -19,5 +19,5 @@ for src, fmad in b.SOURCES.items():
         subprocess.run(cmd, check=True)
         o = vo
     objs.append(o)
-subprocess.run([b.NVCC, *b.ARCH, "-shared", "-o", out, *objs, "-lcudart"], check=True)
+subprocess.run([b.NVCC, *b.ARCH, "-shared", "-o", out, *objs, "-lcudart", "-ldl"], check=True)
 print(out)
