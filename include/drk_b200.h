@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define DRK_ABI_VERSION 1
+#define DRK_ABI_VERSION 2
 
 typedef enum drk_status {
   DRK_OK = 0,
@@ -101,6 +101,9 @@ typedef struct drk_prims {
   const double* tau;     /* n */
   const double* opacity; /* n */
   const float* sh;       /* n x terms x 3 */
+  const double* sh64;    /* optional (may be NULL): the same coefficients in fp64.  When given, the
+                          * fp64 pixel path (reference precision, fp64 re-render) evaluates colours from
+                          * them bit-exactly like the reference (geometry.cpp:101-138) */
 } drk_prims;
 
 /* Frame gradients (drk::FrameGrad, reference grad.hpp:40-45); NULL = empty. */

@@ -86,7 +86,7 @@ class Options_(C.Structure):
 
 
 class Prims_(C.Structure):
-    _fields_ = [(f, C.c_void_p) for f in ("mu", "rot", "scales", "angles", "eta", "tau", "opacity", "sh")]
+    _fields_ = [(f, C.c_void_p) for f in ("mu", "rot", "scales", "angles", "eta", "tau", "opacity", "sh", "sh64")]
 
 
 class FrameGrad_(C.Structure):

@@ -93,7 +93,7 @@ void* slot_bytes(int slot, size_t bytes) {
 }
 
 enum Slots { kMu, kRot, kS, kTh, kEta, kTau, kO, kSh, kColor, kDepth, kNormal, kAlpha, kRaw, kDC, kDD, kDN, kDA,
-             kG, kDcw, kSg, kTch, kLossA, kLossB, kLossOut, kLossD };
+             kG, kDcw, kSg, kTch, kLossA, kLossB, kLossOut, kLossD, kSh64 };
 
 template <class T>
 struct Dev {
@@ -158,6 +158,14 @@ struct DevPrims {
     }
     return v;
   }
+  static std::vector<double> shd(const std::vector<drk::DrkPrimitive>& P, int terms) {
+    std::vector<double> v;
+    v.reserve(P.size() * terms * 3);
+    for (const auto& p : P)
+      for (int t = 0; t < terms; ++t)
+        for (int c = 0; c < 3; ++c) v.push_back(t < p.sh.rows() ? p.sh(t, c) : 0.0);
+    return v;
+  }
   static std::vector<float> shf(const std::vector<drk::DrkPrimitive>& P, int terms) {
     std::vector<float> v;
     v.reserve(P.size() * terms * 3);
@@ -181,7 +189,8 @@ struct DevPrims {
         heta(field(P, 1, 4)),
         htau(field(P, 1, 5)),
         ho(field(P, 1, 6)),
-        hsh(shf(P, terms)) {
+        hsh(shf(P, terms)),
+        hsh64(shd(P, terms)) {
     for (const auto& p : P)
       if (p.basis_count() != k) throw drk::DimensionMismatchError("drk_b200 adapter: mixed basis counts");
     Fnv f;
@@ -195,17 +204,19 @@ struct DevPrims {
     f.vec(heta);
     f.vec(htau);
     f.vec(ho);
-    f.vec(hsh);
+    f.vec(hsh64);
     hash = f.h;
   }
   // device copies (only when a forward must run)
   void upload() {
     Dev<double> mu(kMu, hmu), rot(kRot, hrot), s(kS, hs), th(kTh, hth), eta(kEta, heta), tau(kTau, htau), o(kO, ho);
     Dev<float> sh(kSh, hsh);
-    view = drk_prims{mu.p, rot.p, s.p, th.p, eta.p, tau.p, o.p, sh.p};
+    Dev<double> sh64(kSh64, hsh64);  // the fp64 pixel path's colours use the reference's coefficients exactly
+    view = drk_prims{mu.p, rot.p, s.p, th.p, eta.p, tau.p, o.p, sh.p, sh64.p};
   }
   std::vector<double> hmu, hrot, hs, hth, heta, htau, ho;
   std::vector<float> hsh;
+  std::vector<double> hsh64;
   drk_prims view{};
   uint64_t hash = 0;
 };

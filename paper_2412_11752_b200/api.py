@@ -301,11 +301,14 @@ class Rasterizer:
         opt = opt or RenderOptions()
         n, k = prims["scales"].shape
         sh = prims["sh"].to(self.device, torch.float32).contiguous()
+        # an fp64 SH tensor is also passed as drk_prims.sh64 (fp64 pixel path colours)
+        sh64 = prims["sh"].to(self.device).contiguous() if prims["sh"].dtype == torch.float64 else None
         terms = sh.shape[1] if sh.numel() else 0
         keep = {f: prims[f].to(self.device, torch.float64).contiguous()
                 for f in ("mu", "rot", "scales", "angles", "eta", "tau", "opacity")}
         p = _lib.Prims_(*[C.c_void_p(keep[f].data_ptr()) for f in
-                          ("mu", "rot", "scales", "angles", "eta", "tau", "opacity")], C.c_void_p(sh.data_ptr()))
+                          ("mu", "rot", "scales", "angles", "eta", "tau", "opacity")], C.c_void_p(sh.data_ptr()),
+                        _ptr(sh64))
         H, W = cam.height, cam.width
         kw = dict(device=self.device, dtype=torch.float32)
         fb = FrameBuffers(torch.empty(H, W, 3, **kw), torch.empty(H, W, **kw), torch.empty(H, W, 3, **kw),
@@ -315,7 +318,7 @@ class Rasterizer:
         self._check(_lib.lib().drk_forward_prims(self._h, C.byref(p), n, k, terms, C.byref(_camera(cam)),
                                                  C.byref(_options(opt, cap)), _ptr(fb.color), _ptr(fb.depth),
                                                  _ptr(fb.normal), _ptr(fb.alpha)))
-        self._keep = (keep, sh)
+        self._keep = (keep, sh, sh64)
         self._shape = (n, k, terms, H, W)
         return fb
 

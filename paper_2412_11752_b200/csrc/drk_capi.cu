@@ -161,6 +161,7 @@ static RasterParams raster_params(drk_ctx* c) {
   const Activated& A = c->act;
   P.S = ShapeView{A.s, A.th, A.ex, A.ey, A.det, A.eta, A.tau, A.o, A.thf, A.invdetf, A.piogf, A.hf, A.psif, A.K};
   P.sh = A.sh;
+  P.sh64 = A.sh64;
   P.terms = A.terms;
   P.counters = static_cast<unsigned long long*>(c->counters.p);
   // pixels flagged for the fp64 re-render (list written by the fp32 pass)
@@ -995,7 +996,7 @@ int drk_activate(drk_ctx* c, const float* raw, int n, int k, int sh_terms, drk_p
   c->has_act = true;  // drk_forward_again now renders this set
   if (out) {
     const Activated& A = c->act;
-    *out = drk_prims{A.mu, A.rot, A.s, A.th, A.eta, A.tau, A.o, A.sh};
+    *out = drk_prims{A.mu, A.rot, A.s, A.th, A.eta, A.tau, A.o, A.sh, nullptr};
   }
   return DRK_OK;
 }

@@ -466,6 +466,32 @@ __device__ __forceinline__ double low_pass_filter_term(double dpw, double dph, d
 }
 
 // Real SH basis (geometry.cpp:91-124), fp32.
+// sh_basis (geometry.cpp:101-124) in fp64 with the reference's op order,
+// explicitly rounded: the fp64 pixel path's colours are the reference's bits.
+__device__ __forceinline__ void sh_basis_d(double x, double y, double z, int degree, double* out) {
+  out[0] = 0.28209479177387814;
+  if (degree < 1) return;
+  const double k1 = 0.4886025119029199;
+  out[1] = xm(-k1, y);
+  out[2] = xm(k1, z);
+  out[3] = xm(-k1, x);
+  if (degree < 2) return;
+  const double xx = xm(x, x), yy = xm(y, y), zz = xm(z, z), xy = xm(x, y), yz = xm(y, z), xz = xm(x, z);
+  out[4] = xm(1.0925484305920792, xy);
+  out[5] = xm(-1.0925484305920792, yz);
+  out[6] = xm(0.31539156525252005, xs(xs(xm(2.0, zz), xx), yy));
+  out[7] = xm(-1.0925484305920792, xz);
+  out[8] = xm(0.5462742152960396, xs(xx, yy));
+  if (degree < 3) return;
+  out[9] = xm(xm(-0.5900435899266435, y), xs(xm(3.0, xx), yy));
+  out[10] = xm(xm(2.890611442640554, xy), z);
+  out[11] = xm(xm(-0.4570457994644658, y), xs(xs(xm(4.0, zz), xx), yy));
+  out[12] = xm(xm(0.3731763325901154, z), xs(xs(xm(2.0, zz), xm(3.0, xx)), xm(3.0, yy)));
+  out[13] = xm(xm(-0.4570457994644658, x), xs(xs(xm(4.0, zz), xx), yy));
+  out[14] = xm(xm(1.445305721320277, z), xs(xx, yy));
+  out[15] = xm(xm(-0.5900435899266435, x), xs(xx, xm(3.0, yy)));
+}
+
 __device__ __forceinline__ void sh_basis_f(float x, float y, float z, int degree, float* out) {
   const float kSh0 = 0.28209479177387814f, kSh1 = 0.4886025119029199f;
   out[0] = kSh0;

@@ -70,6 +70,7 @@ static_assert(sizeof(Geo) == 160, "Geo record size");
 struct Activated {
   const double *mu, *rot, *s, *th, *eta, *tau, *o;
   const float* sh;  // n x terms x 3 (AoS)
+  const double* sh64;  // optional fp64 copy (drk_prims.sh64) for the fp64 pixel path, or nullptr
   const double *ex, *ey, *det;
   const float *thf, *invdetf, *piogf, *hf, *psif;
   const float* rec;  // fast-kernel shape records (K == 8), else nullptr
@@ -84,6 +85,7 @@ struct RasterParams {
   const Geo* geo;
   ShapeView S;
   const float* sh;
+  const double* sh64;  // optional fp64 SH (fp64 pixel path colours), or nullptr
   int terms;  // stored SH rows per primitive
   float *color, *depth, *normal, *alpha;
   double* pxstate;  // 8 doubles per pixel: C(3, incl. background), D, N(3), A

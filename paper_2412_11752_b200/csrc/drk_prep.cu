@@ -1363,6 +1363,7 @@ int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms) {
   A.tau = ensure<double>(c->a_tau, n);
   A.o = ensure<double>(c->a_o, n);
   A.sh = ensure<float>(c->a_sh, (size_t)3 * terms * n);
+  A.sh64 = nullptr;  // raw f32 coefficients widen exactly
   unsigned long long* ctr = ensure<unsigned long long>(c->counters, C_COUNT);
   if (!A.mu || !A.rot || !A.s || !A.th || !A.eta || !A.tau || !A.o || !A.sh || !ctr)
     return set_error(c, DRK_ERR_OOM, "activation buffers");
@@ -1396,6 +1397,7 @@ int launch_shape(drk_ctx* c, const drk_prims* p, int n, int K, int terms) {
   A.tau = p->tau;
   A.o = p->opacity;
   A.sh = p->sh;
+  A.sh64 = p->sh64;
   return launch_shape_consts(c, n, K);
 }
 

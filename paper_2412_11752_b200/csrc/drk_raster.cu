@@ -182,10 +182,18 @@ struct Pixel {
     }
     if (a < P.opt.alpha_min) return true;
     a = dmin(a, 1.0 - 1e-6);
-    float r0, r1, r2c;
-    sh_rgb(P, id, r0, r1, r2c);
-    const bool cl0 = r0 < 0, cl1 = r1 < 0, cl2 = r2c < 0;
-    const double rgb[3] = {cl0 ? 0.0 : (double)r0, cl1 ? 0.0 : (double)r1, cl2 ? 0.0 : (double)r2c};
+    double rgb[3];
+    if (F64) {
+      sh_rgb_d(P, id, rgb);
+    } else {
+      float r0, r1, r2c;
+      sh_rgb(P, id, r0, r1, r2c);
+      rgb[0] = r0;
+      rgb[1] = r1;
+      rgb[2] = r2c;
+    }
+    const bool cl0 = rgb[0] < 0, cl1 = rgb[1] < 0, cl2 = rgb[2] < 0;
+    for (int c = 0; c < 3; ++c) rgb[c] = rgb[c] < 0 ? 0.0 : rgb[c];
     const double sgn = denom < 0 ? 1.0 : -1.0;
     const double w = T * a;
     ++n_comp;
@@ -272,11 +280,14 @@ struct Pixel {
               o_sh = kGOffSh;
     // SH (linear, clamped channels gated)
     const bool cl[3] = {cl0, cl1, cl2};
+    double bd[16];
+    if (F64) sh_basis_d(dir[0], dir[1], dir[2], P.opt.sh_degree, bd);
     for (int ch = 0; ch < 3; ++ch) {
       if (cl[ch]) continue;
       const double dc = wb * dC[ch];
       if (dc == 0) continue;
-      for (int t = 0; t < P.opt.terms_active; ++t) gadd(pg + o_sh + 3 * t + ch, dc * (double)basis[t]);
+      for (int t = 0; t < P.opt.terms_active; ++t)
+        gadd(pg + o_sh + 3 * t + ch, dc * (F64 ? bd[t] : (double)basis[t]));
     }
     if (has_dN)
       for (int q = 0; q < 3; ++q) gadd(pg + o_rot + 3 * q + 2, wb * sgn * dN[q]);
@@ -861,6 +872,22 @@ struct Pixel {
     }
   }
 
+  // SH colour in fp64 (geometry.cpp:126-138, reference op order, rounded
+  // explicitly) from the pixel's fp64 ray; coefficients from the fp64 copy when
+  // the caller gave one, else the f32 ones widened.  Before the clamp at zero.
+  __device__ void sh_rgb_d(const RasterParams& P, int id, double rgb[3]) const {
+    double b[16];
+    sh_basis_d(dir[0], dir[1], dir[2], P.opt.sh_degree, b);
+    rgb[0] = rgb[1] = rgb[2] = 0.5;
+    const int ta = P.opt.terms_active;
+    const size_t base = (size_t)id * P.terms * 3;
+    for (int t = 0; t < ta; ++t)
+      for (int c = 0; c < 3; ++c) {
+        const double s = P.sh64 ? P.sh64[base + 3 * t + c] : (double)P.sh[base + 3 * t + c];
+        rgb[c] = xa(rgb[c], xm(b[t], s));
+      }
+  }
+
   __device__ void finish_forward(const RasterParams& P) {
     const size_t p = (size_t)pix;
     const double c0 = C[0] + T * P.opt.bg[0];
@@ -1301,7 +1328,7 @@ __device__ void process_pixel(const RasterParams& P, int pix) {
 // colour, kernel partials for the backward.
 struct PopEval {
   double a, rt, u, v, denom, dpw, dph;
-  float rgb[3];
+  double rgb[3];
   bool valid, lp, cl[3];
   KEval ev;
   int id;
@@ -1344,14 +1371,11 @@ __device__ void eval_pop(const RasterParams& P, const Pixel<BWD, true>& px, doub
   }
   if (a < P.opt.alpha_min) return;
   e.a = dmin(a, 1.0 - 1e-6);
-  float r0, r1, r2c;
-  px.sh_rgb(P, id, r0, r1, r2c);
-  e.cl[0] = r0 < 0;
-  e.cl[1] = r1 < 0;
-  e.cl[2] = r2c < 0;
-  e.rgb[0] = e.cl[0] ? 0.f : r0;
-  e.rgb[1] = e.cl[1] ? 0.f : r1;
-  e.rgb[2] = e.cl[2] ? 0.f : r2c;
+  px.sh_rgb_d(P, id, e.rgb);
+  for (int c = 0; c < 3; ++c) {
+    e.cl[c] = e.rgb[c] < 0;
+    if (e.cl[c]) e.rgb[c] = 0.0;
+  }
   e.valid = true;
 }
 
@@ -1512,8 +1536,8 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
         if (!valid) continue;
         const double a = __shfl_sync(FULL, e.a, k);
         const double rt = __shfl_sync(FULL, e.rt, k);
-        const float r0 = __shfl_sync(FULL, e.rgb[0], k), r1 = __shfl_sync(FULL, e.rgb[1], k),
-                    r2 = __shfl_sync(FULL, e.rgb[2], k);
+        const double r0 = __shfl_sync(FULL, e.rgb[0], k), r1 = __shfl_sync(FULL, e.rgb[1], k),
+                     r2 = __shfl_sync(FULL, e.rgb[2], k);
         const double denom = __shfl_sync(FULL, e.denom, k);
         const int id = __shfl_sync(FULL, e.id, k);
         const Geo& g = P.geo[id];

@@ -99,6 +99,9 @@ __device__ __forceinline__ void record_grad_fast(const RasterParams& P, const Bw
   float deta = 0, dtau = 0, dop = 0, ds_lo = 0, ds_hi = 0, da_lo = 0, da_hi = 0;
   int lo = 0, hi = 1;
   const float denf = gf.dz, af = (float)a;
+  // reciprocals instead of IEEE divisions (2^-23 relative; the backward's
+  // tolerance is 1e-3 relative L2)
+  const float iden = rcp_nr(denf);
   const float4* fr = P.frame32 + 3 * (size_t)id;
   const float4 fx = __ldg(fr), fy = __ldg(fr + 1), fz = __ldg(fr + 2);
   const float rzf[3] = {fz.x, fz.y, fz.z};
@@ -112,8 +115,8 @@ __device__ __forceinline__ void record_grad_fast(const RasterParams& P, const Bw
     const float d_rt = wbf * bp.dD;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      dcen[q] += d_rt * rzf[q] / denf;
-      drot[3 * q + 2] += d_rt * (-hv[q] / denf);
+      dcen[q] += d_rt * rzf[q] * iden;
+      drot[3 * q + 2] += d_rt * (-hv[q] * iden);
     }
   }
   if (a < 1.0 - 1e-6 - 1e-12) {  // alpha not clamped
@@ -121,10 +124,10 @@ __device__ __forceinline__ void record_grad_fast(const RasterParams& P, const Bw
     if (gf.lp) {
       const float cv = fabsf(denf), sl = (float)P.opt.lowpass_radius;
       const float dpwf = gf.dpx, dphf = gf.dpy;  // pixel - projected centre
-      dop += datf * af / o;
-      const float inv = 1.0f / (cv * cv * sl * sl);
+      dop += datf * af * rcp_nr(o);
+      const float inv = rcp_nr(cv * cv * sl * sl);
       const float d_dpw = datf * af * (-dpwf * inv), d_dph = datf * af * (-dphf * inv);
-      const float d_cos = datf * af * (dpwf * dpwf + dphf * dphf) * inv / cv;
+      const float d_cos = datf * af * (dpwf * dpwf + dphf * dphf) * inv * rcp_nr(cv);
       double J[6];
       projection_jacobian(P.cam, g.mu, J);
       const float sg = denf < 0 ? -1.0f : 1.0f;
@@ -138,10 +141,9 @@ __device__ __forceinline__ void record_grad_fast(const RasterParams& P, const Bw
       const float tau = (float)P.S.tau[id];
       dop += datf * k.P;
       if (!k.center) {
+        const float tp = k.br == 1 ? 1.0f - tau : 1.0f + tau;
         dtau += datf * o *
-                (k.br == 0 ? -2.0f * k.g / ((1.0f + tau) * (1.0f + tau))
-                           : (k.br == 1 ? (2.0f * k.g - 1.0f) / ((1.0f - tau) * (1.0f - tau))
-                                        : (2.0f - 2.0f * k.g) / ((1.0f + tau) * (1.0f + tau))));
+                (k.br == 0 ? -2.0f * k.g : (k.br == 1 ? 2.0f * k.g - 1.0f : 2.0f - 2.0f * k.g)) * rcp_nr(tp * tp);
         if (!k.clamped) {
           lo = k.lo;
           hi = k.hi;
@@ -150,6 +152,7 @@ __device__ __forceinline__ void record_grad_fast(const RasterParams& P, const Bw
           const float4 f = __ldg(reinterpret_cast<const float4*>(br) + 1);  // 1/det, pi/gap, h_lo, h_hi
           const float elx = e.x, ely = e.y, ehx = e.z, ehy = e.w, invd = f.x, piog = f.y, hlo = f.z, hhi = f.w;
           const float slo = rsqrtf(hlo), shi = rsqrtf(hhi);
+          const float islo = hlo * slo, ishi = hhi * shi;  // 1 / s_lo, 1 / s_hi
           const float eta = __ldg(P.shrec + (size_t)kRecStride * id + 16);
           const float r2f = gf.r2;
           const float d_q = datf * o * k.A * (-0.5f * k.g);
@@ -157,20 +160,20 @@ __device__ __forceinline__ void record_grad_fast(const RasterParams& P, const Bw
           const float d_r1 = d_q * eta * 2.0f * k.r1;
           const float d_r2sq = d_q * (1.0f - eta) * k.inv;
           const float d_inv = d_q * (1.0f - eta) * r2f;
-          ds_lo = d_inv * (-2.0f * k.ch * k.ch * hlo / slo);
-          ds_hi = d_inv * (-2.0f * k.sh * k.sh * hhi / shi);
+          ds_lo = d_inv * (-2.0f * k.ch * k.ch * hlo * islo);
+          ds_hi = d_inv * (-2.0f * k.sh * k.sh * hhi * ishi);
           const float d_delta = -(d_inv * 0.5f * (hlo - hhi)) * (2.0f * k.sh * k.ch);
           const float d_tfd = d_delta * piog;
           const float dl = k.delta * (float)(1.0 / kPi);
           da_lo = d_tfd * (dl - 1.0f);
           da_hi = -d_tfd * dl;
-          const float uf = gf.u, vf = gf.v, r2s = fmaxf(r2f, 1e-24f);
+          const float uf = gf.u, vf = gf.v, ir2s = rcp_nr(fmaxf(r2f, 1e-24f));
           const float sa = k.a > 0.f ? 1.f : (k.a < 0.f ? -1.f : 0.f);
           const float sb = k.b > 0.f ? 1.f : (k.b < 0.f ? -1.f : 0.f);
-          const float du = d_tfd * (-vf / r2s) + 2.0f * d_r2sq * uf + d_r1 * (sa * ehy - sb * ely) * invd;
-          const float dv = d_tfd * (uf / r2s) + 2.0f * d_r2sq * vf + d_r1 * (sb * elx - sa * ehx) * invd;
-          ds_lo += d_r1 * (-sa * k.a / slo);
-          ds_hi += d_r1 * (-sb * k.b / shi);
+          const float du = d_tfd * (-vf * ir2s) + 2.0f * d_r2sq * uf + d_r1 * (sa * ehy - sb * ely) * invd;
+          const float dv = d_tfd * (uf * ir2s) + 2.0f * d_r2sq * vf + d_r1 * (sb * elx - sa * ehx) * invd;
+          ds_lo += d_r1 * (-sa * k.a * islo);
+          ds_hi += d_r1 * (-sb * k.b * ishi);
           const float cross = ehy * ely + ehx * elx;
           da_lo += d_r1 * invd * (sa * k.a * cross - sb * k.a * slo * slo);
           da_hi += d_r1 * invd * (sa * k.b * shi * shi - sb * k.b * cross);
@@ -179,10 +182,11 @@ __device__ __forceinline__ void record_grad_fast(const RasterParams& P, const Bw
           const float ryf[3] = {fy.x, fy.y, fy.z};
           const float drx = df[0] * rxf[0] + df[1] * rxf[1] + df[2] * rxf[2];
           const float dry = df[0] * ryf[0] + df[1] * ryf[1] + df[2] * ryf[2];
-          const float fq = -(du * drx + dv * dry) / denf;
+          const float fq = -(du * drx + dv * dry) * iden;
+          const float drxd = drx * iden, dryd = dry * iden;
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
-            dcen[q] += du * (rzf[q] * (drx / denf) - rxf[q]) + dv * (rzf[q] * (dry / denf) - ryf[q]);
+            dcen[q] += du * (rzf[q] * drxd - rxf[q]) + dv * (rzf[q] * dryd - ryf[q]);
             drot[3 * q + 0] += du * hv[q];
             drot[3 * q + 1] += dv * hv[q];
             drot[3 * q + 2] += fq * hv[q];

@@ -39,7 +39,7 @@ def test_binding_covers_header_and_loads():
     from paper_2412_11752_b200 import _lib
     assert set(declared()) == set(_lib.SIGNATURES)
     h = _lib.lib()  # dlopen + argtypes for every symbol (libcudart resolves without a GPU)
-    assert h.drk_abi_version() == 1
+    assert h.drk_abi_version() == 2
     assert h.drk_scalar_count(8, 16) == 74 and h.drk_scalar_count(8, 1) == 29
     assert h.drk_status_string(5) == b"replay mismatch"
 
