@@ -137,6 +137,9 @@ typedef struct drk_stats {
   int64_t fp64_evals;        /* pops re-evaluated in fp64 (decision inside the fp32 error bound) */
   int64_t ambiguous;         /* cache steps whose fp32 depth intervals overlapped (resolved in fp64) */
   int64_t ring_miss;         /* pops of entries older than the shared-memory ring (re-staged from HBM) */
+  int64_t tie_runs;          /* sort: runs of equal packed 32-bit keys (ordered on the fp64 key afterwards) */
+  int64_t tie_members;       /* sort: entries in those runs */
+  int64_t tie_max_run;       /* sort: longest run */
 } drk_stats;
 
 typedef struct drk_ctx drk_ctx;

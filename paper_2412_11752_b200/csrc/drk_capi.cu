@@ -42,7 +42,8 @@ __global__ void k_pack_keys(long long n, const unsigned long long* pk, const uns
                             int dbits, unsigned* sk);
 __global__ void k_tie_keys(long long n, const unsigned* sk, const unsigned* sv, int dbits, const Geo* geo,
                            const double* cdirs, const double* tdirs, CamD cam, OptD opt, unsigned long long* fk);
-__global__ void k_tie_fix(long long n, const unsigned* sk, unsigned* sv, unsigned long long* fk);
+__global__ void k_tie_fix(long long n, const unsigned* sk, unsigned* sv, unsigned long long* fk,
+                          unsigned long long* counters);
 __global__ void k_full_keys(long long n, const unsigned* sk, const unsigned* sv, int dbits, const Geo* geo,
                             const double* cdirs, const double* tdirs, CamD cam, OptD opt, double* out);
 __global__ void k_full_keys_off(long long n, const long long* tileoff, int n_tiles, const unsigned* sv, const Geo* geo,
@@ -319,7 +320,7 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
     k_tie_keys<<<nb, 256, 0, s>>>(n_pairs, sk, pv, c->key_dbits, static_cast<const Geo*>(c->geo.p),
                                   static_cast<const double*>(c->cdirs.p), static_cast<const double*>(c->tdirs.p), cd,
                                   od, pk);
-    k_tie_fix<<<nb, 256, 0, s>>>(n_pairs, sk, pv, pk);
+    k_tie_fix<<<nb, 256, 0, s>>>(n_pairs, sk, pv, pk, static_cast<unsigned long long*>(c->counters.p));
     launch_counter() += 2;
   }
   k_tile_bounds<<<(unsigned)((n_pairs + 256) / 256), 256, 0, s>>>(n_pairs, sk, c->key_dbits, n_tiles, tileoff);
@@ -681,6 +682,9 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   c->stats.fp64_evals = (int64_t)h[C_FP64_EVALS];
   c->stats.ambiguous = (int64_t)h[C_AMBIGUOUS];
   c->stats.ring_miss = (int64_t)h[C_RING_MISS];
+  c->stats.tie_runs = (int64_t)h[C_TIE_RUNS];
+  c->stats.tie_members = (int64_t)h[C_TIE_MEMBERS];
+  c->stats.tie_max_run = (int64_t)h[C_TIE_MAXRUN];
   if (h[C_ERR_DEGEN_BASIS]) return set_error(c, DRK_ERR_DEGENERATE_BASIS, "adjacent endpoints nearly collinear");
   c->has_fwd = true;
   return DRK_OK;
@@ -736,7 +740,8 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
   // the backward keeps whole-tile CTAs (half tiles measured +1.7% on config 2)
   // unless raster_kernel 6 forces them
-  P.fast_nt = c->opt.raster_kernel == 6 ? 128 : 256;
+  static const int bwd_nt = getenv("DRK_BWD_NT") ? atoi(getenv("DRK_BWD_NT")) : 256;
+  P.fast_nt = (c->opt.raster_kernel == 6 || bwd_nt == 128) ? 128 : 256;
   mark(c, 7);
   const int nb = (int)c->bands.size() - 1;
   if (deterministic) {

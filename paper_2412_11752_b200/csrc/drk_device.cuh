@@ -59,6 +59,9 @@ enum Counter {
   C_RING_MISS,         // fast kernel: pops re-staged from HBM (older than the ring)
   C_PTS_POOL,          // K1: sorted-point pool cursor
   C_DET_OVERFLOW,      // deterministic backward: records beyond the forward's composite count (must stay 0)
+  C_TIE_RUNS,          // sort: runs of equal packed keys (ordered on the full fp64 key afterwards)
+  C_TIE_MEMBERS,       // sort: entries in such runs
+  C_TIE_MAXRUN,        // sort: longest run
   C_COUNT
 };
 

@@ -1256,13 +1256,17 @@ __global__ void k_tie_keys(long long n, const unsigned* __restrict__ sk, const u
   fk[i] = key_order(pair_key(geo[pid], (int)pid, (int)(k >> dbits), cam, opt, cdirs, tdirs));
 }
 
-__global__ void k_tie_fix(long long n, const unsigned* __restrict__ sk, unsigned* sv, unsigned long long* fk) {
+__global__ void k_tie_fix(long long n, const unsigned* __restrict__ sk, unsigned* sv, unsigned long long* fk,
+                          unsigned long long* counters) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i + 1 >= n) return;
   const unsigned k = sk[i];
   if (sk[i + 1] != k || (i > 0 && sk[i - 1] == k)) return;
   long long e = i + 2;
   while (e < n && sk[e] == k) ++e;
+  atomicAdd(&counters[C_TIE_RUNS], 1ull);
+  atomicAdd(&counters[C_TIE_MEMBERS], (unsigned long long)(e - i));
+  atomicMax(&counters[C_TIE_MAXRUN], (unsigned long long)(e - i));
   for (long long a = i + 1; a < e; ++a) {
     const unsigned pa = sv[a];
     const unsigned long long ka = fk[a];

@@ -195,17 +195,19 @@ struct Pixel {
     const bool cl0 = rgb[0] < 0, cl1 = rgb[1] < 0, cl2 = rgb[2] < 0;
     for (int c = 0; c < 3; ++c) rgb[c] = rgb[c] < 0 ? 0.0 : rgb[c];
     const double sgn = denom < 0 ? 1.0 : -1.0;
-    const double w = T * a;
+    const double w = xm(T, a);
     ++n_comp;
     if (!BWD) {
-      C[0] += w * rgb[0];
-      C[1] += w * rgb[1];
-      C[2] += w * rgb[2];
-      D += w * rt;
-      N[0] += w * (sgn * rz0);
-      N[1] += w * (sgn * rz1);
-      N[2] += w * (sgn * rz2);
-      A += w;
+      // raster.cpp:353-357, each op rounded (no contraction): the cache, list
+      // and exact-sort paths accumulate bit-identically
+      C[0] = xa(C[0], xm(w, rgb[0]));
+      C[1] = xa(C[1], xm(w, rgb[1]));
+      C[2] = xa(C[2], xm(w, rgb[2]));
+      D = xa(D, xm(w, rt));
+      N[0] = xa(N[0], xm(w, xm(sgn, rz0)));
+      N[1] = xa(N[1], xm(w, xm(sgn, rz1)));
+      N[2] = xa(N[2], xm(w, xm(sgn, rz2)));
+      A = xa(A, w);
       if (P.replay_cap > 0) {
         if (n_rec < P.replay_cap) {
           const size_t r = (size_t)pix * P.replay_cap + n_rec;
@@ -890,9 +892,9 @@ struct Pixel {
 
   __device__ void finish_forward(const RasterParams& P) {
     const size_t p = (size_t)pix;
-    const double c0 = C[0] + T * P.opt.bg[0];
-    const double c1 = C[1] + T * P.opt.bg[1];
-    const double c2 = C[2] + T * P.opt.bg[2];
+    const double c0 = xa(C[0], xm(T, P.opt.bg[0]));  // raster.cpp:420
+    const double c1 = xa(C[1], xm(T, P.opt.bg[1]));
+    const double c2 = xa(C[2], xm(T, P.opt.bg[2]));
     if (P.color) {
       P.color[3 * p] = (float)c0;
       P.color[3 * p + 1] = (float)c1;
@@ -1542,17 +1544,17 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
         const int id = __shfl_sync(FULL, e.id, k);
         const Geo& g = P.geo[id];
         const double sgn = denom < 0 ? 1.0 : -1.0;
-        const double w = px.T * a;
+        const double w = xm(px.T, a);
         ++px.n_comp;
         if (!BWD) {
-          px.C[0] += w * r0;
-          px.C[1] += w * r1;
-          px.C[2] += w * r2;
-          px.D += w * rt;
-          px.N[0] += w * (sgn * g.rz[0]);
-          px.N[1] += w * (sgn * g.rz[1]);
-          px.N[2] += w * (sgn * g.rz[2]);
-          px.A += w;
+          px.C[0] = xa(px.C[0], xm(w, r0));
+          px.C[1] = xa(px.C[1], xm(w, r1));
+          px.C[2] = xa(px.C[2], xm(w, r2));
+          px.D = xa(px.D, xm(w, rt));
+          px.N[0] = xa(px.N[0], xm(w, xm(sgn, g.rz[0])));
+          px.N[1] = xa(px.N[1], xm(w, xm(sgn, g.rz[1])));
+          px.N[2] = xa(px.N[2], xm(w, xm(sgn, g.rz[2])));
+          px.A = xa(px.A, w);
         } else {
           const double cw = (px.dC[0] * r0 + px.dC[1] * r1 + px.dC[2] * r2) + px.dD * rt +
                             (px.dN[0] * (sgn * g.rz[0]) + px.dN[1] * (sgn * g.rz[1]) + px.dN[2] * (sgn * g.rz[2])) +

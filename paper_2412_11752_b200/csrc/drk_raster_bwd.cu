@@ -28,6 +28,10 @@
 #ifndef DRK_BWDF_MINB
 #define DRK_BWDF_MINB 1
 #endif
+// half-tile CTAs (128 threads): resident CTAs per SM the register budget is set for
+#ifndef DRK_BWD_MINB128
+#define DRK_BWD_MINB128 2
+#endif
 // 1: warp-group sums read the members' rows / SH weights / basis from shared
 // memory (lane = gradient component); 0: register transposes with shuffles
 #ifndef DRK_BWD_SMEM
@@ -332,7 +336,8 @@ __device__ __noinline__ void record_grad_f64(const RasterParams& P, const BwdPix
 // DET: deterministic mode — each composited record writes its own gradient row
 // (det_row) instead of the warp-group reduction and atomics.
 template <int NT, bool DET>
-__global__ void __launch_bounds__(NT, DRK_BWDF_MINB * 256 / NT) k_raster_bwd_fast(const __grid_constant__ RasterParams P) {
+__global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MINB) k_raster_bwd_fast(
+    const __grid_constant__ RasterParams P) {
   constexpr int RING = 2 * NT;
   extern __shared__ float4 dyn[];
   Rec* ring = reinterpret_cast<Rec*>(dyn);

@@ -18,7 +18,9 @@ for v in range(int(sys.argv[1]) if len(sys.argv) > 1 else 1):
     torch.cuda.synchronize(); dt = time.time() - t
     st = r.stats()
     free, total = torch.cuda.mem_get_info()
-    print(f'view {v}: {dt*1e3:.0f} ms pairs {st["pairs"]} fp64px {st["fp64_pixels"]}', {k: round(x, 1) for k, x in st['stage_ms'].items()},
+    print(f'view {v}: {dt*1e3:.0f} ms pairs {st["pairs"]} fp64px {st["fp64_pixels"]} bands {r.bands()} '
+          f'tie runs {st["tie_runs"]} members {st["tie_members"]} max run {st["tie_max_run"]}',
+          {k: round(x, 1) for k, x in st['stage_ms'].items()},
           'device mem used GB', round((total - free) / 1e9, 1), flush=True)
     if len(sys.argv) > 2 and sys.argv[2] == 'bwd':
         tgt = torch.from_numpy(scenes.config_target(4, cams[v], view=v).astype(np.float32)).cuda()
