@@ -66,10 +66,15 @@ class EmptyMeshError(DrkError):
     status = 17
 
 
+class CommError(DrkError):
+    """NCCL failure in the gradient exchange (drk_comm; the communicator is aborted)."""
+    status = 18
+
+
 _ERRORS = {e.status: e for e in (NonFiniteError, DegenerateQuaternionError, DegenerateBasisError,
                                  ReplayMismatchError, DimensionMismatchError, IoError, CorruptFileError,
                                  VersionMismatchError, DegenerateFaceError, TooManyVerticesError, ParseError,
-                                 EmptyMeshError)}
+                                 EmptyMeshError, CommError)}
 
 
 class Camera_(C.Structure):

@@ -738,10 +738,11 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
   P.G = G;
   P.touched = tch;
   const int n_tiles = c->camd.tiles_x * c->camd.tiles_y;
-  // the backward keeps whole-tile CTAs (half tiles measured +1.7% on config 2)
-  // unless raster_kernel 6 forces them
-  static const int bwd_nt = getenv("DRK_BWD_NT") ? atoi(getenv("DRK_BWD_NT")) : 256;
-  P.fast_nt = (c->opt.raster_kernel == 6 || bwd_nt == 128) ? 128 : 256;
+  // half-tile CTAs of 128 threads at 3 per SM (168 registers): 12 warps / SM
+  // instead of 8 (config 2 backward 41.8 ms vs 43.4 ms); raster_kernel 7 or
+  // DRK_BWD_NT=256 keep whole tiles
+  static const int bwd_nt = getenv("DRK_BWD_NT") ? atoi(getenv("DRK_BWD_NT")) : 128;
+  P.fast_nt = (c->opt.raster_kernel == 7 || (bwd_nt == 256 && c->opt.raster_kernel != 6)) ? 256 : 128;
   mark(c, 7);
   const int nb = (int)c->bands.size() - 1;
   if (deterministic) {

@@ -81,6 +81,10 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
 #ifndef DRK_PSEUDO_ANGLE
 #define DRK_PSEUDO_ANGLE 1
 #endif
+// 1: alpha_entry loads the shape record's bracket-lookup angles and eta first
+#ifndef DRK_EARLY_LOADS
+#define DRK_EARLY_LOADS 0
+#endif
 
 // Pseudo-angle of (x, y): monotone in the polar angle, 0 < p <= 4 for angles in
 // (0, 2 pi] (the angle 0 maps to 4, like atan2's 0 -> 2 pi; (0, 0) -> 4).
@@ -266,6 +270,14 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
                                             AlphaOut& out, GradF* gf = nullptr, Pop64* o64 = nullptr) {
   out.skip = false;
   out.degen = false;
+#if DRK_EARLY_LOADS
+  // the bracket-lookup angles and eta of the shape record, issued before the
+  // tangent-coordinate math so that their load latency overlaps it
+  const float* hd_e = P.shrec + (size_t)kRecStride * id;
+  const float4 ela = __ldg(reinterpret_cast<const float4*>(hd_e) + (DRK_PSEUDO_ANGLE ? 4 : 0));
+  const float4 elb = __ldg(reinterpret_cast<const float4*>(hd_e) + (DRK_PSEUDO_ANGLE ? 5 : 1));
+  const float eeta = __ldg(hd_e + 16);
+#endif
   const float dz = lin3(R.r0, R.r5.x, px.ddx, px.ddy, px.ddz);
   const float nu = lin3(R.r1, R.r5.y, px.ddx, px.ddy, px.ddz);
   const float nv = lin3(R.r2, R.r5.z, px.ddx, px.ddy, px.ddz);
@@ -311,7 +323,11 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
     // (theta_7 = 2 pi <-> 4); misassignment only within ~5e-7 rad of an
     // endpoint, where the kernel is continuous across brackets (as with the
     // fp32 atan2 it replaces)
+#if DRK_EARLY_LOADS
+    const float4 p0 = ela, p1 = elb;
+#else
     const float4 p0 = __ldg(reinterpret_cast<const float4*>(hd) + 4), p1 = __ldg(reinterpret_cast<const float4*>(hd) + 5);
+#endif
     const float th = pseudo_angle(v, u);
     int lo;
     if (th <= p0.y) {
@@ -320,7 +336,11 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
       lo = (p0.z < th) + (p0.w < th) + (p1.x < th) + (p1.y < th) + (p1.z < th) + (p1.w < th);
     }
 #else
+#if DRK_EARLY_LOADS
+    const float4 t0 = ela, t1 = elb;
+#else
     const float4 t0 = __ldg(reinterpret_cast<const float4*>(hd)), t1 = __ldg(reinterpret_cast<const float4*>(hd) + 1);
+#endif
     float th = atan2_fast(v, u);
     if (th <= 0.f) th += 6.28318530717958647692f;
     int lo;
@@ -336,7 +356,11 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
       out.degen = true;
       return;
     }
+#if DRK_EARLY_LOADS
+    const float eta = eeta;
+#else
     const float eta = __ldg(hd + 16);
+#endif
     const float ka = (e.w * u - e.z * v) * f.x;
     const float kb = (e.x * v - e.y * u) * f.x;
     const float r1 = fabsf(ka) + fabsf(kb);

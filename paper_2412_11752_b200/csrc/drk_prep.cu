@@ -1259,14 +1259,24 @@ __global__ void k_tie_keys(long long n, const unsigned* __restrict__ sk, const u
 __global__ void k_tie_fix(long long n, const unsigned* __restrict__ sk, unsigned* sv, unsigned long long* fk,
                           unsigned long long* counters) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i + 1 >= n) return;
-  const unsigned k = sk[i];
-  if (sk[i + 1] != k || (i > 0 && sk[i - 1] == k)) return;
+  const unsigned k = i < n ? sk[i] : 0u;
+  const bool start = i + 1 < n && sk[i + 1] == k && !(i > 0 && sk[i - 1] == k);
   long long e = i + 2;
-  while (e < n && sk[e] == k) ++e;
-  atomicAdd(&counters[C_TIE_RUNS], 1ull);
-  atomicAdd(&counters[C_TIE_MEMBERS], (unsigned long long)(e - i));
-  atomicMax(&counters[C_TIE_MAXRUN], (unsigned long long)(e - i));
+  if (start)
+    while (e < n && sk[e] == k) ++e;
+  {
+    // run statistics, aggregated per warp (one atomic per warp and counter)
+    const unsigned len = start ? (unsigned)(e - i) : 0u;
+    const unsigned runs = __reduce_add_sync(0xffffffffu, start ? 1u : 0u);
+    const unsigned mem = __reduce_add_sync(0xffffffffu, len);
+    const unsigned mx = __reduce_max_sync(0xffffffffu, len);
+    if ((threadIdx.x & 31) == 0 && runs) {
+      atomicAdd(&counters[C_TIE_RUNS], (unsigned long long)runs);
+      atomicAdd(&counters[C_TIE_MEMBERS], (unsigned long long)mem);
+      atomicMax(&counters[C_TIE_MAXRUN], (unsigned long long)mx);
+    }
+  }
+  if (!start) return;
   for (long long a = i + 1; a < e; ++a) {
     const unsigned pa = sv[a];
     const unsigned long long ka = fk[a];

@@ -30,7 +30,7 @@
 #endif
 // half-tile CTAs (128 threads): resident CTAs per SM the register budget is set for
 #ifndef DRK_BWD_MINB128
-#define DRK_BWD_MINB128 2
+#define DRK_BWD_MINB128 3  // 168 registers, 12 warps / SM (config 2: 41.8 ms vs 43.4 ms with whole-tile CTAs)
 #endif
 // 1: warp-group sums read the members' rows / SH weights / basis from shared
 // memory (lane = gradient component); 0: register transposes with shuffles
