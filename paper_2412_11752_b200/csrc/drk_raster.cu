@@ -39,6 +39,29 @@ static_assert(kGOffSh + 48 <= kGradSlotStride, "gradient row layout");
 #define DRK_BWD_MIN_BLOCKS 2
 #endif
 
+// alpha_tilde in fp64 (composite_candidate, raster.cpp:333-345: kernel alpha,
+// low-pass floor when the centre projects).  One compiled instance serves the
+// cache, list and exact-sort paths, so equal inputs give equal bits in all of
+// them (FMA contraction cannot differ between inlined copies).
+static __device__ __noinline__ double alpha64(const ShapeView& S, int id, double u, double v, bool has_proj,
+                                               double dpw, double dph, double cos_view, double lowpass_radius,
+                                               KEval& ev, bool& lp) {
+  eval_kernel(u, v, S, id, ev);
+  lp = false;
+  if (ev.degenerate) return 0.0;
+  const double o = S.o[id];
+  const double a_kernel = o * sharpen(ev.g, S.tau[id]);
+  double a = a_kernel;
+  if (has_proj) {
+    const double f = low_pass_filter_term(dpw, dph, cos_view, o, lowpass_radius);
+    if (f > a_kernel) {
+      a = f;
+      lp = true;
+    }
+  }
+  return a;
+}
+
 template <bool BWD, bool F64>
 struct Pixel {
   double dir[3];
@@ -159,24 +182,12 @@ struct Pixel {
       a = (double)at;
       rel = relt;
     }
-    const double o = P.S.o[id];
     if (use64) {
       ++n_f64;
-      const double tau = P.S.tau[id];
-      eval_kernel(u, v, P.S, id, ev);
+      a = alpha64(P.S, id, u, v, g.has_proj, dpw, dph, cos_view, P.opt.lowpass_radius, ev, lp);
       if (ev.degenerate) {
         err = true;
         return false;
-      }
-      const double a_kernel = o * sharpen(ev.g, tau);
-      a = a_kernel;
-      lp = false;
-      if (g.has_proj) {
-        const double f = low_pass_filter_term(dpw, dph, cos_view, o, P.opt.lowpass_radius);
-        if (f > a_kernel) {
-          a = f;
-          lp = true;
-        }
       }
       rel = 0.f;
     }
@@ -1359,18 +1370,8 @@ __device__ void eval_pop(const RasterParams& P, const Pixel<BWD, true>& px, doub
   const bool lp_possible = g.has_proj && e.dpw * e.dpw + e.dph * e.dph <= cos_view * cos_view * g.dp2max;
   e.ev.center = e.ev.clamped = e.ev.degenerate = false;
   if (r2 > g.r2max && !lp_possible) return;
-  eval_kernel(e.u, e.v, P.S, id, e.ev);
+  const double a = alpha64(P.S, id, e.u, e.v, g.has_proj, e.dpw, e.dph, cos_view, P.opt.lowpass_radius, e.ev, e.lp);
   if (e.ev.degenerate) return;
-  const double o = P.S.o[id];
-  const double a_kernel = o * sharpen(e.ev.g, P.S.tau[id]);
-  double a = a_kernel;
-  if (g.has_proj) {
-    const double f = low_pass_filter_term(e.dpw, e.dph, cos_view, o, P.opt.lowpass_radius);
-    if (f > a_kernel) {
-      a = f;
-      e.lp = true;
-    }
-  }
   if (a < P.opt.alpha_min) return;
   e.a = dmin(a, 1.0 - 1e-6);
   px.sh_rgb_d(P, id, e.rgb);

@@ -45,6 +45,11 @@
 #ifndef DRK_ISECT2
 #define DRK_ISECT2 0
 #endif
+// 1: SortCache steps whose incoming entry is certainly deeper than the whole
+// (full) cache take a branch-free shift (no per-entry compares / selects)
+#ifndef DRK_CACHE_FAST
+#define DRK_CACHE_FAST 0
+#endif
 
 
 namespace drk {
@@ -206,6 +211,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
     cj[q] = 0;
   }
   int csz = 0;
+  float maxhi = __int_as_float(0x7f800000);  // max of chi[] (+inf while the cache has free slots)
   bool done = !active;
   const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
   const float eps = (float)P.opt.grazing_eps;
@@ -243,6 +249,24 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   // pixel saturates
   auto cache_step = [&](int jr, float lo, float hi) -> bool {
     DRK_STAT(n_str);
+#if DRK_CACHE_FAST
+    if (maxhi <= lo) {
+      // full cache and the incoming entry certainly deeper than every cached one
+      // (the common case: lists are presorted by depth): pop the head, append
+      const int pj = cj[0];
+#pragma unroll
+      for (int q = 0; q < kCacheCap - 1; ++q) {
+        clo[q] = clo[q + 1];
+        chi[q] = chi[q + 1];
+        cj[q] = cj[q + 1];
+      }
+      clo[kCacheCap - 1] = lo;
+      chi[kCacheCap - 1] = hi;
+      cj[kCacheCap - 1] = jr;
+      maxhi = hi;
+      return pop_eval<VALIDATE, NT, STATS>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y);
+    }
+#endif
     bool le[kCacheCap];
     bool amb = false;
 #pragma unroll
@@ -283,6 +307,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
         }
       }
       ++csz;
+#if DRK_CACHE_FAST
+      if (csz == kCacheCap) {
+        maxhi = chi[0];
+#pragma unroll
+        for (int q = 1; q < kCacheCap; ++q) maxhi = fmaxf(maxhi, chi[q]);
+      }
+#endif
       return true;
     }
     int pj;
@@ -304,6 +335,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
         }
       }
     }
+#if DRK_CACHE_FAST
+    // the cache changed (shift + insert, or intervals tightened to exact depths)
+    maxhi = chi[0];
+#pragma unroll
+    for (int q = 1; q < kCacheCap; ++q) maxhi = fmaxf(maxhi, chi[q]);
+#endif
     return pop_eval<VALIDATE, NT, STATS>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y);
   };
 #if DRK_TMA_STAGE
