@@ -83,7 +83,7 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
 #endif
 // 1: alpha_entry loads the shape record's bracket-lookup angles and eta first
 #ifndef DRK_EARLY_LOADS
-#define DRK_EARLY_LOADS 0
+#define DRK_EARLY_LOADS 1  // measured: config-1 raster 20.32 -> 20.22 ms, config-2 backward 41.9 -> 41.0 ms
 #endif
 
 // Pseudo-angle of (x, y): monotone in the polar angle, 0 < p <= 4 for angles in

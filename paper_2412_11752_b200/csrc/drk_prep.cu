@@ -1264,7 +1264,7 @@ __global__ void k_tie_fix(long long n, const unsigned* __restrict__ sk, unsigned
   long long e = i + 2;
   if (start)
     while (e < n && sk[e] == k) ++e;
-  {
+  if (__ballot_sync(0xffffffffu, start)) {
     // run statistics, aggregated per warp (one atomic per warp and counter)
     const unsigned len = start ? (unsigned)(e - i) : 0u;
     const unsigned runs = __reduce_add_sync(0xffffffffu, start ? 1u : 0u);

@@ -66,6 +66,7 @@ template <bool BWD, bool F64>
 struct Pixel {
   double dir[3];
   float basis[16];
+  double basis64[F64 ? 16 : 1];  // fp64 SH basis of the pixel's ray (sh_basis_d), fp64 paths only
   double px, py;
   double T, C[3], D, N[3], A;
   float E;  // relative error bound of T (fp32 alphas)
@@ -86,6 +87,7 @@ struct Pixel {
 #pragma unroll
     for (int t = 0; t < 16; ++t) basis[t] = 0.f;
     sh_basis_f((float)dir[0], (float)dir[1], (float)dir[2], P.opt.sh_degree, basis);
+    if (F64) sh_basis_d(dir[0], dir[1], dir[2], P.opt.sh_degree, basis64);
     T = 1.0;
     C[0] = C[1] = C[2] = D = N[0] = N[1] = N[2] = A = 0;
     E = 0.f;
@@ -293,14 +295,12 @@ struct Pixel {
               o_sh = kGOffSh;
     // SH (linear, clamped channels gated)
     const bool cl[3] = {cl0, cl1, cl2};
-    double bd[16];
-    if (F64) sh_basis_d(dir[0], dir[1], dir[2], P.opt.sh_degree, bd);
     for (int ch = 0; ch < 3; ++ch) {
       if (cl[ch]) continue;
       const double dc = wb * dC[ch];
       if (dc == 0) continue;
       for (int t = 0; t < P.opt.terms_active; ++t)
-        gadd(pg + o_sh + 3 * t + ch, dc * (F64 ? bd[t] : (double)basis[t]));
+        gadd(pg + o_sh + 3 * t + ch, dc * (F64 ? basis64[t < 16 && F64 ? t : 0] : (double)basis[t]));
     }
     if (has_dN)
       for (int q = 0; q < 3; ++q) gadd(pg + o_rot + 3 * q + 2, wb * sgn * dN[q]);
@@ -889,8 +889,7 @@ struct Pixel {
   // explicitly) from the pixel's fp64 ray; coefficients from the fp64 copy when
   // the caller gave one, else the f32 ones widened.  Before the clamp at zero.
   __device__ void sh_rgb_d(const RasterParams& P, int id, double rgb[3]) const {
-    double b[16];
-    sh_basis_d(dir[0], dir[1], dir[2], P.opt.sh_degree, b);
+    const double* b = basis64;
     rgb[0] = rgb[1] = rgb[2] = 0.5;
     const int ta = P.opt.terms_active;
     const size_t base = (size_t)id * P.terms * 3;
