@@ -140,6 +140,8 @@ typedef struct drk_stats {
   int64_t tie_runs;          /* sort: runs of equal packed 32-bit keys (ordered on the fp64 key afterwards) */
   int64_t tie_members;       /* sort: entries in those runs */
   int64_t tie_max_run;       /* sort: longest run */
+  int64_t cache_appends;     /* fast forward: full-cache steps whose incoming entry is certainly deeper than
+                              * every cached one (work counters on) */
 } drk_stats;
 
 typedef struct drk_ctx drk_ctx;

@@ -108,7 +108,7 @@ class Stats_(C.Structure):
         [("stage_ms", C.c_double * 8), ("bwd_warp_steps", C.c_int64), ("bwd_lead_records", C.c_int64),
          ("reject_radius", C.c_int64), ("reject_bracket", C.c_int64), ("fp64_evals", C.c_int64),
          ("ambiguous", C.c_int64), ("ring_miss", C.c_int64), ("tie_runs", C.c_int64), ("tie_members", C.c_int64),
-         ("tie_max_run", C.c_int64)]
+         ("tie_max_run", C.c_int64), ("cache_appends", C.c_int64)]
 
 
 class DensifyConfig_(C.Structure):

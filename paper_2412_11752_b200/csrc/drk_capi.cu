@@ -42,8 +42,9 @@ __global__ void k_pack_keys(long long n, const unsigned long long* pk, const uns
                             int dbits, unsigned* sk);
 __global__ void k_tie_keys(long long n, const unsigned* sk, const unsigned* sv, int dbits, const Geo* geo,
                            const double* cdirs, const double* tdirs, CamD cam, OptD opt, unsigned long long* fk);
-__global__ void k_tie_fix(long long n, const unsigned* sk, unsigned* sv, unsigned long long* fk,
-                          unsigned long long* counters);
+__global__ void k_tie_rank(long long n, const unsigned* sk, const unsigned* sv, const unsigned long long* fk,
+                           unsigned* out, unsigned long long* counters);
+__global__ void k_tie_long(long long n, const unsigned* sk, unsigned long long* fk, unsigned* out);
 __global__ void k_full_keys(long long n, const unsigned* sk, const unsigned* sv, int dbits, const Geo* geo,
                             const double* cdirs, const double* tdirs, CamD cam, OptD opt, double* out);
 __global__ void k_full_keys_off(long long n, const long long* tileoff, int n_tiles, const unsigned* sv, const Geo* geo,
@@ -198,8 +199,9 @@ static float elapsed(drk_ctx* c, int a, int b) {
 // bounding boxes) would not fit in device memory; then greedy bands whose
 // bound fits (SURVEY.md §7 hard part 5: banded binning for config 4).
 // device bytes per (tile, primitive) pair: emitted 64-bit keys (reused as the
-// sort's second buffer), sorted keys and ids (8 + 4 + 4), plus row / tile scratch
-constexpr double kPairBytes = 18.0;
+// sort's second buffer and for the full keys of tied entries), sorted keys and
+// two id lists (8 + 4 + 4 + 4), plus row / tile scratch
+constexpr double kPairBytes = 22.0;
 
 static int plan_bands(drk_ctx* c) {
   const CamD& cd = c->camd;
@@ -234,7 +236,7 @@ static int plan_bands(drk_ctx* c) {
     if ((double)total <= 0.25 * (double)c->device_bytes / kPairBytes) return DRK_OK;
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    const size_t held = c->pk.bytes + c->pv.bytes + c->sk.bytes + c->hist.bytes + c->sortoff.bytes;
+    const size_t held = c->pk.bytes + c->pv.bytes + c->sk.bytes + c->pidx.bytes + c->hist.bytes + c->sortoff.bytes;
     limit = 0.7 * (double)(free_b + held) / kPairBytes;
   }
   if ((double)total <= limit) return DRK_OK;
@@ -284,9 +286,10 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
   unsigned long long* pk = ensure<unsigned long long>(c->pk, n_pairs + 1);
   unsigned* pv = ensure<unsigned>(c->pv, n_pairs + 1);
   unsigned* sk = ensure<unsigned>(c->sk, n_pairs + 1);
+  unsigned* ids2 = ensure<unsigned>(c->pidx, n_pairs + 1);  // the tie ordering's output id list
   unsigned* krange = ensure<unsigned>(c->bits, 2 + 2 * 4096);  // range, sampled histogram, q map
   long long* tileoff = ensure<long long>(c->tileoff, n_tiles + 1);
-  if (!pk || !pv || !sk || !krange || !tileoff) return set_error(c, DRK_ERR_OOM, "pair buffers");
+  if (!pk || !pv || !sk || !ids2 || !krange || !tileoff) return set_error(c, DRK_ERR_OOM, "pair buffers");
   const unsigned kr0[2] = {0xffffffffu, 0u};
   cudaMemcpyAsync(krange, kr0, sizeof kr0, cudaMemcpyHostToDevice, s);
   if (n_rows > 0)
@@ -314,14 +317,18 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
   // ping-pong space (four passes end back in sk / pv)
   unsigned* tmp = reinterpret_cast<unsigned*>(pk);
   if (int st = sort_pairs(c, sk, pv, tmp, tmp + n_pairs + 1, n_pairs)) return st;
-  if (n_pairs > 1) {
-    // runs of equal sort keys: full keys (into the dead emission buffer), then order
+  if (n_pairs > 0) {
+    // runs of equal sort keys: full keys (into the dead emission buffer), then
+    // the ids in (key, id) order into the second id buffer, which becomes the list
     const unsigned nb = (unsigned)((n_pairs + 255) / 256);
+    unsigned long long* fk = pk;
     k_tie_keys<<<nb, 256, 0, s>>>(n_pairs, sk, pv, c->key_dbits, static_cast<const Geo*>(c->geo.p),
                                   static_cast<const double*>(c->cdirs.p), static_cast<const double*>(c->tdirs.p), cd,
-                                  od, pk);
-    k_tie_fix<<<nb, 256, 0, s>>>(n_pairs, sk, pv, pk, static_cast<unsigned long long*>(c->counters.p));
-    launch_counter() += 2;
+                                  od, fk);
+    k_tie_rank<<<nb, 256, 0, s>>>(n_pairs, sk, pv, fk, ids2, static_cast<unsigned long long*>(c->counters.p));
+    k_tie_long<<<nb, 256, 0, s>>>(n_pairs, sk, fk, ids2);
+    launch_counter() += 3;
+    std::swap(c->pv, c->pidx);
   }
   k_tile_bounds<<<(unsigned)((n_pairs + 256) / 256), 256, 0, s>>>(n_pairs, sk, c->key_dbits, n_tiles, tileoff);
   DRK_COUNT_LAUNCH();
@@ -685,6 +692,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   c->stats.tie_runs = (int64_t)h[C_TIE_RUNS];
   c->stats.tie_members = (int64_t)h[C_TIE_MEMBERS];
   c->stats.tie_max_run = (int64_t)h[C_TIE_MAXRUN];
+  c->stats.cache_appends = (int64_t)h[C_CACHE_APPEND];
   if (h[C_ERR_DEGEN_BASIS]) return set_error(c, DRK_ERR_DEGENERATE_BASIS, "adjacent endpoints nearly collinear");
   c->has_fwd = true;
   return DRK_OK;
@@ -965,7 +973,7 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->eval_scr, &c->eval_px, &c->eval_off, &c->ovf_scr, &c->ovf_list, &c->tord,
                     &c->rowest, &c->host_raw, &c->host_img, &c->pxcomp, &c->det_cnt, &c->det_base,
                     &c->det_rec, &c->det_id, &c->det_tile, &c->det_sort, &c->det_poff, &c->det_acc, &c->det_rowoff,
-                    &c->comm_buf, &c->scan_tmp2, &c->replay_cid, &c->replay_cval};
+                    &c->comm_buf, &c->scan_tmp2, &c->replay_cid, &c->replay_cval, &c->pidx};
   for (DevBuf* b : bufs) release(*b);
   for (DevBuf& b : c->band_ids) release(b);
   for (DevBuf& b : c->band_off) release(b);

@@ -62,6 +62,7 @@ enum Counter {
   C_TIE_RUNS,          // sort: runs of equal packed keys (ordered on the full fp64 key afterwards)
   C_TIE_MEMBERS,       // sort: entries in such runs
   C_TIE_MAXRUN,        // sort: longest run
+  C_CACHE_APPEND,      // fast kernel: full-cache steps whose incoming entry is certainly deeper than every cached one
   C_COUNT
 };
 

@@ -1127,8 +1127,8 @@ __global__ void __launch_bounds__(256) k_emit_rows(long long n_rows, const int4*
 
 // Sort key of each emitted pair: tile << dbits | q, q a monotone map of the
 // key32 (key_order >> 32) to dbits bits.  The map equalises the depth density
-// so that few pairs of one tile share a q (each such run costs k_tie_fix an
-// insertion sort on full keys): the finite key range [lo, hi] is cut into
+// so that few pairs of one tile share a q (each such run is ordered on the full
+// keys afterwards, k_tie_rank): the finite key range [lo, hi] is cut into
 // kQBins bins of 2^shift0 key32 units, a sample of the pairs is histogrammed,
 // and bin j gets a power-of-two share a_j of the q space (proportional to its
 // count, at least 1), q = base_j + ((k32 - start_j) >> s_j).  Non-finite keys
@@ -1236,11 +1236,15 @@ __global__ void __launch_bounds__(256) k_pack_keys(long long n, const unsigned l
   }
 }
 
-// After the sort: runs of equal sort keys are put in (full fp64 key, pid)
-// order, the reference's order (raster.cpp:260-263: each tile list sorted by
-// key, ties by primitive id).  Two passes: every entry inside a run computes
-// its full key (one thread each), then each run's first entry insertion-sorts
-// the run on those keys.
+// After the sort: runs of equal packed sort keys are put in (full fp64 key,
+// pid) order — the reference's order (raster.cpp:260-263: each tile list
+// sorted by key, ties by primitive id).  Every run member computes its full key
+// (k_tie_keys, into the dead emission buffer); runs of up to kRankMax entries
+// are then ordered in parallel — each member counts the members that precede
+// it and writes its id at run start + rank into a second id buffer — and
+// longer runs by one thread (k_tie_long, insertion sort).
+constexpr int kRankMax = 1024;
+
 __device__ __forceinline__ bool in_run(long long n, const unsigned* sk, long long i, unsigned k) {
   return (i + 1 < n && sk[i + 1] == k) || (i > 0 && sk[i - 1] == k);
 }
@@ -1256,14 +1260,21 @@ __global__ void k_tie_keys(long long n, const unsigned* __restrict__ sk, const u
   fk[i] = key_order(pair_key(geo[pid], (int)pid, (int)(k >> dbits), cam, opt, cdirs, tdirs));
 }
 
-__global__ void k_tie_fix(long long n, const unsigned* __restrict__ sk, unsigned* sv, unsigned long long* fk,
-                          unsigned long long* counters) {
+__device__ __forceinline__ bool pair_less(unsigned long long ka, unsigned pa, unsigned long long kb, unsigned pb) {
+  return ka < kb || (ka == kb && pa < pb);
+}
+
+__global__ void k_tie_rank(long long n, const unsigned* __restrict__ sk, const unsigned* __restrict__ sv,
+                           const unsigned long long* __restrict__ fk, unsigned* out, unsigned long long* counters) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const unsigned k = i < n ? sk[i] : 0u;
-  const bool start = i + 1 < n && sk[i + 1] == k && !(i > 0 && sk[i - 1] == k);
-  long long e = i + 2;
-  if (start)
-    while (e < n && sk[e] == k) ++e;
+  const bool member = i < n && in_run(n, sk, i, k);
+  const bool start = member && !(i > 0 && sk[i - 1] == k);
+  long long s = i, e = i + 1;
+  if (member) {
+    while (s > 0 && sk[s - 1] == k && i - s <= kRankMax) --s;
+    while (e < n && sk[e] == k && e - s <= kRankMax) ++e;
+  }
   if (__ballot_sync(0xffffffffu, start)) {
     // run statistics, aggregated per warp (one atomic per warp and counter)
     const unsigned len = start ? (unsigned)(e - i) : 0u;
@@ -1276,17 +1287,38 @@ __global__ void k_tie_fix(long long n, const unsigned* __restrict__ sk, unsigned
       atomicMax(&counters[C_TIE_MAXRUN], (unsigned long long)mx);
     }
   }
-  if (!start) return;
+  if (i >= n) return;
+  const unsigned pid = sv[i];
+  if (!member || e - s > kRankMax) {  // not in a run, or a long run (k_tie_long)
+    out[i] = pid;
+    return;
+  }
+  const unsigned long long ki = fk[i];
+  long long rank = 0;
+  for (long long j = s; j < e; ++j) rank += pair_less(fk[j], sv[j], ki, pid) ? 1 : 0;
+  out[s + rank] = pid;
+}
+
+// Runs longer than kRankMax: the run's first entry insertion-sorts it (keys in
+// fk, ids in out) on (full key, pid).
+__global__ void k_tie_long(long long n, const unsigned* __restrict__ sk, unsigned long long* fk, unsigned* out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i + 1 >= n) return;
+  const unsigned k = sk[i];
+  if (sk[i + 1] != k || (i > 0 && sk[i - 1] == k)) return;
+  long long e = i + 2;
+  while (e < n && sk[e] == k) ++e;
+  if (e - i <= kRankMax) return;
   for (long long a = i + 1; a < e; ++a) {
-    const unsigned pa = sv[a];
+    const unsigned pa = out[a];
     const unsigned long long ka = fk[a];
     long long b = a - 1;
-    while (b >= i && (fk[b] > ka || (fk[b] == ka && sv[b] > pa))) {
-      sv[b + 1] = sv[b];
+    while (b >= i && pair_less(ka, pa, fk[b], out[b])) {
+      out[b + 1] = out[b];
       fk[b + 1] = fk[b];
       --b;
     }
-    sv[b + 1] = pa;
+    out[b + 1] = pa;
     fk[b + 1] = ka;
   }
 }

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   px.stop = INT_MAX;
   px.n_pop = px.n_rej1 = px.n_rej2 = px.n_f64 = px.n_miss = 0;
   px.uncertain = px.err = false;
-  unsigned n_str = 0, n_amb = 0;
+  unsigned n_str = 0, n_amb = 0, n_app = 0;
   float clo[kCacheCap], chi[kCacheCap];
   int cj[kCacheCap];
 #pragma unroll
@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
         }
       }
     }
+    if (STATS && csz == kCacheCap && le[kCacheCap - 1]) ++n_app;  // le is a prefix: all entries <= incoming
     if (csz < kCacheCap) {
 #pragma unroll
       for (int q = kCacheCap - 1; q >= 0; --q) {
@@ -448,20 +449,20 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   }
   // counters: one atomic per warp and counter
   {
-    unsigned long long v[8] = {n_str, px.n_pop, (unsigned long long)px.ncomp, px.n_rej1, px.n_rej2, px.n_f64,
-                               n_amb, px.n_miss};
+    unsigned long long v[9] = {n_str, px.n_pop, (unsigned long long)px.ncomp, px.n_rej1, px.n_rej2, px.n_f64,
+                               n_amb, px.n_miss, n_app};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 9; ++k) {
       unsigned long long s = v[k];
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       v[k] = s;
     }
     if ((threadIdx.x & 31) == 0) {
-      const int slots[8] = {C_STREAMED, C_POPPED, C_COMPOSITED, C_REJECT_RADIUS, C_REJECT_BRACKET, C_FP64_EVALS,
-                            C_AMBIGUOUS, C_RING_MISS};
+      const int slots[9] = {C_STREAMED, C_POPPED, C_COMPOSITED, C_REJECT_RADIUS, C_REJECT_BRACKET, C_FP64_EVALS,
+                            C_AMBIGUOUS, C_RING_MISS, C_CACHE_APPEND};
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < 9; ++k)
         if (v[k]) atomicAdd(&P.counters[slots[k]], v[k]);
     }
   }

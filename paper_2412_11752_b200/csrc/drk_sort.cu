@@ -7,7 +7,7 @@
 // Pairs are (key u32, value u32): key = tile << b | b-bit monotone quantisation
 // of the fp64 depth key (k_pack_keys, drk_prep.cu), value = primitive id; four
 // 8-bit passes.  Runs of equal keys are ordered afterwards on the full fp64 key
-// (k_tie_fix, drk_prep.cu), so the sort itself need not be stable.
+// (k_tie_rank, drk_prep.cu), so the sort itself need not be stable.
 #include "drk_internal.h"
 
 namespace drk {

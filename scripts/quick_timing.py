@@ -27,7 +27,7 @@ for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:
     if VALIDATE:
         r.set_validation(True); r.render(raw, cam, opt); print('validation (max err/bound, max abs err):', r.validation(), r.validation_detail()); r.set_validation(False)
     print(f"cfg{cfg} fwd {dt*1e3:.2f} ms  {mp/dt:.1f} MP/s", {k: round(v, 3) for k, v in st['stage_ms'].items()},
-          {k: st[k] for k in ('pairs', 'streamed', 'popped', 'composited', 'reject_radius', 'reject_bracket', 'fp64_evals', 'fp64_pixels', 'ambiguous', 'ring_miss', 'poly_overflow', 'launches')}, flush=True)
+          {k: st[k] for k in ('pairs', 'streamed', 'popped', 'composited', 'reject_radius', 'reject_bracket', 'fp64_evals', 'fp64_pixels', 'ambiguous', 'ring_miss', 'poly_overflow', 'launches', 'cache_appends', 'tie_runs', 'tie_members', 'tie_max_run')}, flush=True)
     if scenes.CONFIGS[cfg]['backward']:
         tgt = torch.from_numpy(scenes.config_target(cfg, cam).astype(np.float32)).cuda()
         for _ in range(2):
