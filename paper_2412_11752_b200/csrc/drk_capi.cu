@@ -325,7 +325,10 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
     k_tie_keys<<<nb, 256, 0, s>>>(n_pairs, sk, pv, c->key_dbits, static_cast<const Geo*>(c->geo.p),
                                   static_cast<const double*>(c->cdirs.p), static_cast<const double*>(c->tdirs.p), cd,
                                   od, fk);
-    k_tie_rank<<<nb, 256, 0, s>>>(n_pairs, sk, pv, fk, ids2, static_cast<unsigned long long*>(c->counters.p));
+    // run statistics only with the work counters on (same-address atomics from
+    // billions of entries would serialise on config 4)
+    k_tie_rank<<<nb, 256, 0, s>>>(n_pairs, sk, pv, fk, ids2,
+                                  c->work_counters ? static_cast<unsigned long long*>(c->counters.p) : nullptr);
     k_tie_long<<<nb, 256, 0, s>>>(n_pairs, sk, fk, ids2);
     launch_counter() += 3;
     std::swap(c->pv, c->pidx);

@@ -1275,8 +1275,8 @@ __global__ void k_tie_rank(long long n, const unsigned* __restrict__ sk, const u
     while (s > 0 && sk[s - 1] == k && i - s <= kRankMax) --s;
     while (e < n && sk[e] == k && e - s <= kRankMax) ++e;
   }
-  if (__ballot_sync(0xffffffffu, start)) {
-    // run statistics, aggregated per warp (one atomic per warp and counter)
+  if (counters && __ballot_sync(0xffffffffu, start)) {
+    // run statistics (work counters on), aggregated per warp
     const unsigned len = start ? (unsigned)(e - i) : 0u;
     const unsigned runs = __reduce_add_sync(0xffffffffu, start ? 1u : 0u);
     const unsigned mem = __reduce_add_sync(0xffffffffu, len);

@@ -67,6 +67,7 @@ struct Pixel {
   double dir[3];
   float basis[16];
   double basis64[F64 ? 16 : 1];  // fp64 SH basis of the pixel's ray (sh_basis_d), fp64 paths only
+  bool col64;                    // colours in fp64 (reference precision, or fp64 coefficients given)
   double px, py;
   double T, C[3], D, N[3], A;
   float E;  // relative error bound of T (fp32 alphas)
@@ -87,7 +88,8 @@ struct Pixel {
 #pragma unroll
     for (int t = 0; t < 16; ++t) basis[t] = 0.f;
     sh_basis_f((float)dir[0], (float)dir[1], (float)dir[2], P.opt.sh_degree, basis);
-    if (F64) sh_basis_d(dir[0], dir[1], dir[2], P.opt.sh_degree, basis64);
+    col64 = F64 && (P.opt.fp64_alpha || P.sh64 != nullptr);
+    if (col64) sh_basis_d(dir[0], dir[1], dir[2], P.opt.sh_degree, basis64);
     T = 1.0;
     C[0] = C[1] = C[2] = D = N[0] = N[1] = N[2] = A = 0;
     E = 0.f;
@@ -196,7 +198,7 @@ struct Pixel {
     if (a < P.opt.alpha_min) return true;
     a = dmin(a, 1.0 - 1e-6);
     double rgb[3];
-    if (F64) {
+    if (F64 && col64) {
       sh_rgb_d(P, id, rgb);
     } else {
       float r0, r1, r2c;
@@ -300,7 +302,7 @@ struct Pixel {
       const double dc = wb * dC[ch];
       if (dc == 0) continue;
       for (int t = 0; t < P.opt.terms_active; ++t)
-        gadd(pg + o_sh + 3 * t + ch, dc * (F64 ? basis64[t < 16 && F64 ? t : 0] : (double)basis[t]));
+        gadd(pg + o_sh + 3 * t + ch, dc * (F64 && col64 ? basis64[t < 16 && F64 ? t : 0] : (double)basis[t]));
     }
     if (has_dN)
       for (int q = 0; q < 3; ++q) gadd(pg + o_rot + 3 * q + 2, wb * sgn * dN[q]);
@@ -1373,7 +1375,15 @@ __device__ void eval_pop(const RasterParams& P, const Pixel<BWD, true>& px, doub
   if (e.ev.degenerate) return;
   if (a < P.opt.alpha_min) return;
   e.a = dmin(a, 1.0 - 1e-6);
-  px.sh_rgb_d(P, id, e.rgb);
+  if (px.col64) {
+    px.sh_rgb_d(P, id, e.rgb);
+  } else {  // fp64 re-render of a fast-path frame: fp32 colours like the fast kernel
+    float r0, r1, r2c;
+    px.sh_rgb(P, id, r0, r1, r2c);
+    e.rgb[0] = r0;
+    e.rgb[1] = r1;
+    e.rgb[2] = r2c;
+  }
   for (int c = 0; c < 3; ++c) {
     e.cl[c] = e.rgb[c] < 0;
     if (e.cl[c]) e.rgb[c] = 0.0;

@@ -40,3 +40,16 @@ for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2]:
         print(f"cfg{cfg} fwd+bwd {dt*1e3:.2f} ms  {mp/dt:.1f} MP/s loss {float(v):.4f}",
               {k: round(v, 3) for k, v in st['stage_ms'].items()}, 'warpsteps', st['bwd_warp_steps'],
               'lead_records', st['bwd_lead_records'], 'composited', st['composited'], flush=True)
+if os.environ.get('DET'):
+    # deterministic backward (drk_det.cu) on the last config with a backward
+    for cfg in [2]:
+        sc = scenes.config_scene(cfg); cam = scenes.config_cameras(cfg)[0]
+        raw = torch.from_numpy(sc.f32()).cuda()
+        opt = RenderOptions(sh_degree=3)
+        tgt = torch.from_numpy(scenes.config_target(cfg, cam).astype(np.float32)).cuda()
+        fb = r.render(raw, cam, opt); v, d = r.l1_loss(fb.color, tgt)
+        for det in (False, True, True):
+            torch.cuda.synchronize(); t = time.time()
+            g = r.backward_render(raw, FrameGrad(d_color=d), deterministic=det)
+            torch.cuda.synchronize()
+            print(f"cfg{cfg} backward deterministic={det}: {1e3 * (time.time() - t):.1f} ms", flush=True)
