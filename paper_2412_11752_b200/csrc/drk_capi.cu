@@ -43,8 +43,9 @@ __global__ void k_pack_keys(long long n, const unsigned long long* pk, const uns
 __global__ void k_tie_keys(long long n, const unsigned* sk, const unsigned* sv, int dbits, const Geo* geo,
                            const double* cdirs, const double* tdirs, CamD cam, OptD opt, unsigned long long* fk);
 __global__ void k_tie_rank(long long n, const unsigned* sk, const unsigned* sv, const unsigned long long* fk,
-                           unsigned* out, unsigned long long* counters);
-__global__ void k_tie_long(long long n, const unsigned* sk, unsigned long long* fk, unsigned* out);
+                           unsigned* out, unsigned long long* counters, long long* long_runs);
+__global__ void k_tie_long(long long n, const unsigned* sk, unsigned long long* fk, unsigned* out,
+                           const long long* long_runs);
 __global__ void k_full_keys(long long n, const unsigned* sk, const unsigned* sv, int dbits, const Geo* geo,
                             const double* cdirs, const double* tdirs, CamD cam, OptD opt, double* out);
 __global__ void k_full_keys_off(long long n, const long long* tileoff, int n_tiles, const unsigned* sv, const Geo* geo,
@@ -327,9 +328,13 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
                                   od, fk);
     // run statistics only with the work counters on (same-address atomics from
     // billions of entries would serialise on config 4)
+    long long* long_runs = ensure<long long>(c->tie_long, (size_t)(n_pairs / 1024 + 2));
+    if (!long_runs) return set_error(c, DRK_ERR_OOM, "tie runs");
+    cudaMemsetAsync(long_runs, 0, sizeof(long long), s);
     k_tie_rank<<<nb, 256, 0, s>>>(n_pairs, sk, pv, fk, ids2,
-                                  c->work_counters ? static_cast<unsigned long long*>(c->counters.p) : nullptr);
-    k_tie_long<<<nb, 256, 0, s>>>(n_pairs, sk, fk, ids2);
+                                  c->work_counters ? static_cast<unsigned long long*>(c->counters.p) : nullptr,
+                                  long_runs);
+    k_tie_long<<<64, 128, 0, s>>>(n_pairs, sk, fk, ids2, long_runs);
     launch_counter() += 3;
     std::swap(c->pv, c->pidx);
   }
@@ -976,7 +981,7 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->eval_scr, &c->eval_px, &c->eval_off, &c->ovf_scr, &c->ovf_list, &c->tord,
                     &c->rowest, &c->host_raw, &c->host_img, &c->pxcomp, &c->det_cnt, &c->det_base,
                     &c->det_rec, &c->det_id, &c->det_tile, &c->det_sort, &c->det_poff, &c->det_acc, &c->det_rowoff,
-                    &c->comm_buf, &c->scan_tmp2, &c->replay_cid, &c->replay_cval, &c->pidx};
+                    &c->comm_buf, &c->scan_tmp2, &c->replay_cid, &c->replay_cval, &c->pidx, &c->tie_long};
   for (DevBuf* b : bufs) release(*b);
   for (DevBuf& b : c->band_ids) release(b);
   for (DevBuf& b : c->band_off) release(b);

@@ -173,7 +173,8 @@ struct drk_ctx {
   // per view
   drk::DevBuf geo, frame32, bbox, hullref, hull, ptspool, ptsref, rowcnt, rowoff, rows, rowpaircnt, rowpairoff;
   drk::DevBuf pk, pv, sk, hist, sortoff, tileoff, cdirs, tdirs, bits;
-  drk::DevBuf pidx;  // second sorted-id list (tie ordering output; swapped with pv)
+  drk::DevBuf pidx;      // second sorted-id list (tie ordering output; swapped with pv)
+  drk::DevBuf tie_long;  // starts of tied runs longer than kRankMax (count first)
   int key_dbits = 19;  // depth bits of the packed 32-bit sort keys (32 - tile bits)
   drk::DevBuf pxstate, replay_cnt, replay_rec, replay_ids;
   drk::DevBuf gact, touched;

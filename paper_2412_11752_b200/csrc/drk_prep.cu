@@ -1265,61 +1265,93 @@ __device__ __forceinline__ bool pair_less(unsigned long long ka, unsigned pa, un
 }
 
 __global__ void k_tie_rank(long long n, const unsigned* __restrict__ sk, const unsigned* __restrict__ sv,
-                           const unsigned long long* __restrict__ fk, unsigned* out, unsigned long long* counters) {
+                           const unsigned long long* __restrict__ fk, unsigned* out, unsigned long long* counters,
+                           long long* long_runs) {
+  const unsigned FULL = 0xffffffffu;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const unsigned k = i < n ? sk[i] : 0u;
-  const bool member = i < n && in_run(n, sk, i, k);
-  const bool start = member && !(i > 0 && sk[i - 1] == k);
-  long long s = i, e = i + 1;
-  if (member) {
-    while (s > 0 && sk[s - 1] == k && i - s <= kRankMax) --s;
-    while (e < n && sk[e] == k && e - s <= kRankMax) ++e;
+  const int lane = threadIdx.x & 31;
+  const bool valid = i < n;
+  const unsigned k = valid ? sk[i] : 0u;
+  const bool start = valid && (i == 0 || sk[i - 1] != k);
+  const bool next_same = valid && i + 1 < n && sk[i + 1] == k;
+  const bool member = valid && (!start || next_same);  // in a run of two or more
+  const unsigned pid = valid ? sv[i] : 0u;
+  const unsigned long long ki = member ? fk[i] : 0ull;
+  // runs inside this warp: bounds from the ballot of run starts, ranks from the
+  // members' keys by shuffles (most runs are short: config 4 has runs of up to ~50)
+  const unsigned smask = __ballot_sync(FULL, start);
+  const unsigned upto = lane == 31 ? FULL : ((2u << lane) - 1u);
+  const unsigned below = smask & upto, above = smask & ~upto;
+  const int s_lane = below ? 31 - __clz(below) : -1;
+  const int e_lane = above ? __ffs(above) - 1 : 32;
+  const bool tail_cont = __shfl_sync(FULL, next_same, 31);  // lane 31's run continues into the next warp
+  const bool in_warp = s_lane >= 0 && (e_lane < 32 || !tail_cont);
+  int rank = 0;
+  for (int jl = 0; jl < 32; ++jl) {
+    const unsigned long long kj = __shfl_sync(FULL, ki, jl);
+    const unsigned pj = __shfl_sync(FULL, pid, jl);
+    rank += (jl >= s_lane && jl < e_lane && pair_less(kj, pj, ki, pid)) ? 1 : 0;
   }
-  if (counters && __ballot_sync(0xffffffffu, start)) {
-    // run statistics (work counters on), aggregated per warp
-    const unsigned len = start ? (unsigned)(e - i) : 0u;
-    const unsigned runs = __reduce_add_sync(0xffffffffu, start ? 1u : 0u);
-    const unsigned mem = __reduce_add_sync(0xffffffffu, len);
-    const unsigned mx = __reduce_max_sync(0xffffffffu, len);
-    if ((threadIdx.x & 31) == 0 && runs) {
+  if (counters && __ballot_sync(FULL, start && next_same)) {
+    // run statistics (work counters on; runs inside the warp only), per warp
+    const unsigned len = (start && next_same && in_warp) ? (unsigned)(e_lane - lane) : 0u;
+    const unsigned runs = __reduce_add_sync(FULL, (start && next_same) ? 1u : 0u);
+    const unsigned mem = __reduce_add_sync(FULL, len);
+    const unsigned mx = __reduce_max_sync(FULL, len);
+    if (lane == 0 && runs) {
       atomicAdd(&counters[C_TIE_RUNS], (unsigned long long)runs);
       atomicAdd(&counters[C_TIE_MEMBERS], (unsigned long long)mem);
       atomicMax(&counters[C_TIE_MAXRUN], (unsigned long long)mx);
     }
   }
-  if (i >= n) return;
-  const unsigned pid = sv[i];
-  if (!member || e - s > kRankMax) {  // not in a run, or a long run (k_tie_long)
+  if (!valid) return;
+  if (!member) {
     out[i] = pid;
     return;
   }
-  const unsigned long long ki = fk[i];
-  long long rank = 0;
-  for (long long j = s; j < e; ++j) rank += pair_less(fk[j], sv[j], ki, pid) ? 1 : 0;
-  out[s + rank] = pid;
+  const long long s0 = i - lane;  // global index of lane 0
+  if (in_warp) {
+    out[s0 + s_lane + rank] = pid;
+    return;
+  }
+  // a run crossing a warp boundary: bounds and rank from memory
+  long long s = i, e = i + 1;
+  while (s > 0 && sk[s - 1] == k && i - s <= kRankMax) --s;
+  while (e < n && sk[e] == k && e - s <= kRankMax) ++e;
+  if (e - s > kRankMax) {  // long run: k_tie_long orders it
+    out[i] = pid;
+    if (start) long_runs[1 + atomicAdd((unsigned long long*)long_runs, 1ull)] = i;
+    return;
+  }
+  long long r = 0;
+  for (long long j = s; j < e; ++j) r += pair_less(fk[j], sv[j], ki, pid) ? 1 : 0;
+  out[s + r] = pid;
 }
 
-// Runs longer than kRankMax: the run's first entry insertion-sorts it (keys in
-// fk, ids in out) on (full key, pid).
-__global__ void k_tie_long(long long n, const unsigned* __restrict__ sk, unsigned long long* fk, unsigned* out) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i + 1 >= n) return;
-  const unsigned k = sk[i];
-  if (sk[i + 1] != k || (i > 0 && sk[i - 1] == k)) return;
-  long long e = i + 2;
-  while (e < n && sk[e] == k) ++e;
-  if (e - i <= kRankMax) return;
-  for (long long a = i + 1; a < e; ++a) {
-    const unsigned pa = out[a];
-    const unsigned long long ka = fk[a];
-    long long b = a - 1;
-    while (b >= i && pair_less(ka, pa, fk[b], out[b])) {
-      out[b + 1] = out[b];
-      fk[b + 1] = fk[b];
-      --b;
+// Runs longer than kRankMax (their starts listed by k_tie_rank: long_runs[0] =
+// count): one thread per run insertion-sorts it (keys in fk, ids in out) on
+// (full key, pid).
+__global__ void k_tie_long(long long n, const unsigned* __restrict__ sk, unsigned long long* fk, unsigned* out,
+                           const long long* __restrict__ long_runs) {
+  const long long cnt = long_runs[0];
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < cnt;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = long_runs[1 + t];
+    const unsigned k = sk[i];
+    long long e = i + 1;
+    while (e < n && sk[e] == k) ++e;
+    for (long long a = i + 1; a < e; ++a) {
+      const unsigned pa = out[a];
+      const unsigned long long ka = fk[a];
+      long long b = a - 1;
+      while (b >= i && pair_less(ka, pa, fk[b], out[b])) {
+        out[b + 1] = out[b];
+        fk[b + 1] = fk[b];
+        --b;
+      }
+      out[b + 1] = pa;
+      fk[b + 1] = ka;
     }
-    out[b + 1] = pa;
-    fk[b + 1] = ka;
   }
 }
 

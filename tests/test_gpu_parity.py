@@ -232,3 +232,21 @@ def test_config2_crop_backward_parity(rast):
     g = rast.backward_render(sc.f32(), FrameGrad(d_color=torch.from_numpy(od.astype(np.float32))))
     og = port.backward(sc, cam, o, od.astype(np.float32), None, None, None)
     _check_grads(g, og)
+
+
+def test_sort_long_tie_runs(rast):
+    """1300 exact copies of each of two primitives: runs of equal packed keys longer
+    than the parallel rank ordering handles (k_tie_long) and shorter ones, ordered
+    like the reference's (key, id) comparator."""
+    base, cam = small_scene(seed=8, n=12)
+    cols = [base.raw[:, i] for i in range(base.n)]
+    cols += [base.raw[:, 3]] * 1300 + [base.raw[:, 7]] * 1300
+    sc = scenes.Scene(raw=np.stack(cols, axis=1), k=base.k, sh_degree=base.sh_degree)
+    o = opt_for(0)
+    fb = rast.render(sc.f32(), cam, api_options(o))
+    bins = rast.tile_binning()
+    orc = port.bin_primitives(sc, cam, o)
+    _bins_equal(bins, orc)
+    sizes = np.diff(orc[0])
+    assert sizes.max() > 2600
+    _fb_close(fb, port.render(sc, cam, o))
