@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-crop", default="960x544", help="crop of the CPU baseline sample (tile aligned)")
     ap.add_argument("--cpu-crop-bwd", default="320x256", help="crop of the CPU fwd+bwd sample (config 2, tile aligned)")
+    ap.add_argument("--cpu-crop-c3", default="128x128", help="crop of the CPU config-3 view sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fwd-bwd", action="store_true")
     ap.add_argument("--multiview-views", type=int, default=64,
@@ -187,6 +188,22 @@ def reference_cpu_fwd_bwd(crop: str):
                        f"render(&replay) + L1 loss + backward_render (oracle/_ref, unmodified sources) with "
                        f"threads=0 ({threads} threads); bin_primitives (single-threaded) still processes all "
                        f"primitives; {t:.2f} s")
+
+
+def reference_cpu_config3(crop: str):
+    """Reference CPU forward of one config-3 orbit view (1M DRK) on a centred crop, all host threads."""
+    from oracle import ref
+    from paper_2412_11752_b200 import scenes
+    w, h = (int(x) for x in crop.split("x"))
+    sc = scenes.config_scene(3)
+    cam0 = scenes.config_cameras(3)[0]
+    cam = cam0.crop((cam0.width // 2 - w // 2) // 16 * 16, (cam0.height // 2 - h // 2) // 16 * 16, w, h)
+    t = ref.render(sc, cam, ref.Options(sh_degree=3, threads=0))["seconds"]
+    threads = ref.hardware_threads()
+    return dict(value=w * h / t / 1e6, unit="megapixels/s", cores=threads, kind="reference", seconds=t,
+                sample=f"config 3 (1M DRK, SH3) view 0, centred {w}x{h} crop of the 1920x1080 view; reference "
+                       f"activate + render with threads=0 ({threads} threads); bin_primitives (single-threaded) "
+                       f"still processes all 1M primitives, which dominates a crop this small; {t:.2f} s")
 
 
 def adapter_leg(warm: int = 1, steps: int = 3):
@@ -606,6 +623,7 @@ def main():
         try:
             cpu, _ = reference_cpu_sample(args.cpu_crop, 1)
             cpu["fwd_bwd"] = reference_cpu_fwd_bwd(args.cpu_crop_bwd)
+            cpu["config3_view"] = reference_cpu_config3(args.cpu_crop_c3)
         except Exception as e:  # the oracle build is missing: report, do not fail the bench
             cpu = {"value": None, "unit": "megapixels/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}

@@ -22,6 +22,10 @@
 // are processed in chunks of tile rows (in row order, so the accumulation order
 // is unchanged).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "drk_internal.h"
@@ -127,6 +131,19 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
   cudaStream_t s = c->stream;
   const CamD& cd = c->camd;
   const int n = c->act.n, G = P.G;
+  // DRK_HOST_TRACE=1: phase times (stream synchronised at each checkpoint) on stderr
+  static const bool trace = getenv("DRK_HOST_TRACE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  std::string tline;
+  auto tr = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    char b[64];
+    snprintf(b, sizeof b, " %s %.2f", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+    tline += b;
+    t_last = now;
+  };
   const long long slots = (long long)cd.tiles_x * cd.tiles_y * 256;
   if (!P.pxcomp) return set_error(c, DRK_ERR_GENERIC, "deterministic backward: no composite counts");
   int* cnt = ensure<int>(c->det_cnt, (size_t)slots + 1);
@@ -143,6 +160,7 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
     k_det_row_offsets<<<blocks(cd.tiles_y + 1, 128), 128, 0, s>>>(base, cnt, cd.tiles_x, cd.tiles_y, rowoff_d);
     DRK_COUNT_LAUNCH();
   }
+  tr("offsets");
   std::vector<long long> rowoff((size_t)cd.tiles_y + 1, 0);
   if (slots > 0) cudaMemcpyAsync(rowoff.data(), rowoff_d, sizeof(long long) * rowoff.size(), cudaMemcpyDeviceToHost, s);
   if (int st = cuda_check(c, cudaStreamSynchronize(s), "deterministic backward offsets")) return st;
@@ -183,7 +201,9 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
         int* tiles = ensure<int>(c->det_tile, (size_t)R);
         unsigned* sk = ensure<unsigned>(c->det_sort, 4 * (size_t)R + 4);
         if (!rows || !ids || !tiles || !sk) return set_error(c, DRK_ERR_OOM, "deterministic backward records");
+        tr("alloc");
         cudaMemsetAsync(rows, 0, row_bytes * (size_t)R * G, s);
+        tr("memset");
         Q.det_rec = fast ? nullptr : static_cast<double*>(rows);
         Q.det_rec32 = fast ? static_cast<float*>(rows) : nullptr;
         Q.det_id = ids;
@@ -208,17 +228,20 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
           launch_pixels_bwd(Q, s);
         }
         if (int st = cuda_check(c, cudaGetLastError(), "deterministic backward raster")) return st;
+        tr("raster");
         // group the records by primitive, keeping their order, and reduce
         unsigned *kk = sk, *vv = sk + R + 1, *k2 = vv + R + 1, *v2 = k2 + R;
         k_det_keys<<<blocks(R, 256), 256, 0, s>>>(R, ids, kk, vv);
         DRK_COUNT_LAUNCH();
         if (int st = sort_pairs(c, kk, vv, k2, v2, R)) return st;
+        tr("sort");
         cudaMemsetAsync(seg, 0, sizeof(long long) * 2 * (size_t)n, s);
         k_det_segments<<<blocks(R, 256), 256, 0, s>>>(R, kk, seg);
         if (fast) k_det_reduce<float><<<blocks(32LL * n, 256), 256, 0, s>>>(n, G, seg, vv, tiles, Q.det_rec32, acc);
         else k_det_reduce<double><<<blocks(32LL * n, 256), 256, 0, s>>>(n, G, seg, vv, tiles, Q.det_rec, acc);
         launch_counter() += 2;
         if (int st = cuda_check(c, cudaGetLastError(), "deterministic backward reduce")) return st;
+        tr("reduce");
       }
       ty0 = ty1;
     }
@@ -247,6 +270,8 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
   constexpr size_t kKeep = 256u << 20;
   for (DevBuf* b : {&c->det_rec, &c->det_id, &c->det_tile, &c->det_sort})
     if (b->bytes > kKeep) release(*b);
+  tr("release");
+  if (trace) fprintf(stderr, "[drk det]%s\n", tline.c_str());
   unsigned long long ovf = 0;
   cudaMemcpyAsync(&ovf, P.counters + C_DET_OVERFLOW, sizeof ovf, cudaMemcpyDeviceToHost, s);
   if (int st = cuda_check(c, cudaStreamSynchronize(s), "deterministic backward")) return st;

@@ -1267,65 +1267,42 @@ __device__ __forceinline__ bool pair_less(unsigned long long ka, unsigned pa, un
 __global__ void k_tie_rank(long long n, const unsigned* __restrict__ sk, const unsigned* __restrict__ sv,
                            const unsigned long long* __restrict__ fk, unsigned* out, unsigned long long* counters,
                            long long* long_runs) {
-  const unsigned FULL = 0xffffffffu;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const bool valid = i < n;
-  const unsigned k = valid ? sk[i] : 0u;
-  const bool start = valid && (i == 0 || sk[i - 1] != k);
-  const bool next_same = valid && i + 1 < n && sk[i + 1] == k;
-  const bool member = valid && (!start || next_same);  // in a run of two or more
-  const unsigned pid = valid ? sv[i] : 0u;
-  const unsigned long long ki = member ? fk[i] : 0ull;
-  // runs inside this warp: bounds from the ballot of run starts, ranks from the
-  // members' keys by shuffles (most runs are short: config 4 has runs of up to ~50)
-  const unsigned smask = __ballot_sync(FULL, start);
-  const unsigned upto = lane == 31 ? FULL : ((2u << lane) - 1u);
-  const unsigned below = smask & upto, above = smask & ~upto;
-  const int s_lane = below ? 31 - __clz(below) : -1;
-  const int e_lane = above ? __ffs(above) - 1 : 32;
-  const bool tail_cont = __shfl_sync(FULL, next_same, 31);  // lane 31's run continues into the next warp
-  const bool in_warp = s_lane >= 0 && (e_lane < 32 || !tail_cont);
-  int rank = 0;
-  for (int jl = 0; jl < 32; ++jl) {
-    const unsigned long long kj = __shfl_sync(FULL, ki, jl);
-    const unsigned pj = __shfl_sync(FULL, pid, jl);
-    rank += (jl >= s_lane && jl < e_lane && pair_less(kj, pj, ki, pid)) ? 1 : 0;
+  const unsigned k = i < n ? sk[i] : 0u;
+  const bool member = i < n && in_run(n, sk, i, k);
+  const bool start = member && !(i > 0 && sk[i - 1] == k);
+  long long s = i, e = i + 1;
+  if (member) {
+    while (s > 0 && sk[s - 1] == k && i - s <= kRankMax) --s;
+    while (e < n && sk[e] == k && e - s <= kRankMax) ++e;
   }
-  if (counters && __ballot_sync(FULL, start && next_same)) {
-    // run statistics (work counters on; runs inside the warp only), per warp
-    const unsigned len = (start && next_same && in_warp) ? (unsigned)(e_lane - lane) : 0u;
-    const unsigned runs = __reduce_add_sync(FULL, (start && next_same) ? 1u : 0u);
-    const unsigned mem = __reduce_add_sync(FULL, len);
-    const unsigned mx = __reduce_max_sync(FULL, len);
-    if (lane == 0 && runs) {
+  if (counters && __ballot_sync(0xffffffffu, start)) {
+    // run statistics (work counters on), aggregated per warp
+    const unsigned len = start ? (unsigned)(e - i) : 0u;
+    const unsigned runs = __reduce_add_sync(0xffffffffu, start ? 1u : 0u);
+    const unsigned mem = __reduce_add_sync(0xffffffffu, len);
+    const unsigned mx = __reduce_max_sync(0xffffffffu, len);
+    if ((threadIdx.x & 31) == 0 && runs) {
       atomicAdd(&counters[C_TIE_RUNS], (unsigned long long)runs);
       atomicAdd(&counters[C_TIE_MEMBERS], (unsigned long long)mem);
       atomicMax(&counters[C_TIE_MAXRUN], (unsigned long long)mx);
     }
   }
-  if (!valid) return;
+  if (i >= n) return;
+  const unsigned pid = sv[i];
   if (!member) {
     out[i] = pid;
     return;
   }
-  const long long s0 = i - lane;  // global index of lane 0
-  if (in_warp) {
-    out[s0 + s_lane + rank] = pid;
-    return;
-  }
-  // a run crossing a warp boundary: bounds and rank from memory
-  long long s = i, e = i + 1;
-  while (s > 0 && sk[s - 1] == k && i - s <= kRankMax) --s;
-  while (e < n && sk[e] == k && e - s <= kRankMax) ++e;
-  if (e - s > kRankMax) {  // long run: k_tie_long orders it
+  if (e - s > kRankMax) {  // long run: its start is listed for k_tie_long
     out[i] = pid;
-    if (start) long_runs[1 + atomicAdd((unsigned long long*)long_runs, 1ull)] = i;
+    if (start) long_runs[1 + atomicAdd(reinterpret_cast<unsigned long long*>(long_runs), 1ull)] = i;
     return;
   }
-  long long r = 0;
-  for (long long j = s; j < e; ++j) r += pair_less(fk[j], sv[j], ki, pid) ? 1 : 0;
-  out[s + r] = pid;
+  const unsigned long long ki = fk[i];
+  long long rank = 0;
+  for (long long j = s; j < e; ++j) rank += pair_less(fk[j], sv[j], ki, pid) ? 1 : 0;
+  out[s + rank] = pid;
 }
 
 // Runs longer than kRankMax (their starts listed by k_tie_rank: long_runs[0] =
