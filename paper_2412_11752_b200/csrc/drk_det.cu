@@ -87,30 +87,59 @@ __global__ void k_det_segments(long long n, const unsigned* __restrict__ k, long
 
 // One warp per primitive: its records in (tile, pixel, composite) order; the
 // fp64 partial of each tile is added to the running total when the tile ends.
+// Lanes are gradient columns (three 32-column chunks per record, G <= 96); the
+// record indices, tiles and rows of 8 records are loaded ahead of the
+// (sequential, fixed-order) accumulation, so the loads overlap.
 template <typename RT>
 __global__ void k_det_reduce(int n, int G, const long long* __restrict__ seg, const unsigned* __restrict__ rec_of,
                              const int* __restrict__ tile_of, const RT* __restrict__ rows, double* acc) {
+  constexpr int kB = 8;
   const int p = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= n) return;
   const long long b = seg[2 * (size_t)p], e = seg[2 * (size_t)p + 1];
   if (e <= b) return;
-  for (int c0 = 0; c0 < G; c0 += 32) {
-    const int c = c0 + lane;
-    double total = c < G ? acc[(size_t)p * G + c] : 0.0, part = 0.0;
-    int cur = -1;
-    for (long long r = b; r < e; ++r) {
-      const unsigned rec = rec_of[r];
-      const int t = tile_of[rec];
-      if (t != cur) {
-        total += part;
-        part = 0.0;
-        cur = t;
+  double total[3], part[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int c = 32 * q + lane;
+    total[q] = c < G ? acc[(size_t)p * G + c] : 0.0;
+  }
+  int cur = -1;
+  for (long long r0 = b; r0 < e; r0 += kB) {
+    unsigned rec[kB];
+    int tl[kB];
+    double v[kB][3];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) rec[u] = r0 + u < e ? rec_of[r0 + u] : 0u;
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      tl[u] = r0 + u < e ? tile_of[rec[u]] : -1;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int c = 32 * q + lane;
+        v[u][q] = (r0 + u < e && c < G) ? (double)rows[(size_t)rec[u] * G + c] : 0.0;
       }
-      if (c < G) part += (double)rows[(size_t)rec * G + c];
     }
-    total += part;
-    if (c < G) acc[(size_t)p * G + c] = total;
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      if (r0 + u >= e) break;
+      if (tl[u] != cur) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          total[q] += part[q];
+          part[q] = 0.0;
+        }
+        cur = tl[u];
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) part[q] += v[u][q];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int c = 32 * q + lane;
+    if (c < G) acc[(size_t)p * G + c] = total[q] + part[q];
   }
 }
 
@@ -201,9 +230,7 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
         int* tiles = ensure<int>(c->det_tile, (size_t)R);
         unsigned* sk = ensure<unsigned>(c->det_sort, 4 * (size_t)R + 4);
         if (!rows || !ids || !tiles || !sk) return set_error(c, DRK_ERR_OOM, "deterministic backward records");
-        tr("alloc");
-        cudaMemsetAsync(rows, 0, row_bytes * (size_t)R * G, s);
-        tr("memset");
+        tr("alloc");  // no clearing: every record's writer stores its whole row
         Q.det_rec = fast ? nullptr : static_cast<double*>(rows);
         Q.det_rec32 = fast ? static_cast<float*>(rows) : nullptr;
         Q.det_id = ids;

@@ -282,8 +282,14 @@ struct Pixel {
     if (P.det_rec || P.det_rec32) {
       const long long r = det_row(P, pix % P.cam.W, pix / P.cam.W, comp_idx, id);
       if (r < 0) return;
-      if (P.det_rec) dr = P.det_rec + (size_t)r * P.G;
-      else dr32 = P.det_rec32 + (size_t)r * P.G;
+      // the row belongs to this record alone: clear it, then accumulate
+      if (P.det_rec) {
+        dr = P.det_rec + (size_t)r * P.G;
+        for (int c = 0; c < P.G; ++c) dr[c] = 0.0;
+      } else {
+        dr32 = P.det_rec32 + (size_t)r * P.G;
+        for (int c = 0; c < P.G; ++c) dr32[c] = 0.f;
+      }
     }
     auto gadd = [dr, dr32, pg](float* a, double v) {
       if (dr) dr[a - pg] += v;

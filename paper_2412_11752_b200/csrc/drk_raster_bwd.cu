@@ -455,6 +455,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
     bool rec = false;
     int id = -1;
     float w0 = 0.f, w1 = 0.f, w2 = 0.f;
+    long long det_r = -1;
     float* row = s_row + kGCols * threadIdx.x;
     if (want) {
       Rec R;
@@ -501,48 +502,47 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
           record_grad_f64(P, bp, id, g, o64, a, wb, dat, dd, row);
         }
         P.touched[id] = 1;
-        if (DET) {
-          const long long r = det_row(P, x, y, px.ncomp, id);
-          if (r >= 0 && P.det_rec32) {
-            float* dr = P.det_rec32 + (size_t)r * P.G;
-#pragma unroll
-            for (int i = 0; i < kGCols; ++i) dr[gcol_global(i)] = row[i];
-#pragma unroll
-            for (int t = 0; t < 16; ++t) {
-              if (t < P.opt.terms_active) {
-                const float bt = s_basis[t * BS];
-                dr[kGOffSh + 3 * t] = w0 * bt;
-                dr[kGOffSh + 3 * t + 1] = w1 * bt;
-                dr[kGOffSh + 3 * t + 2] = w2 * bt;
-              }
-            }
-          } else if (r >= 0) {
-            double* dr = P.det_rec + (size_t)r * P.G;
-#pragma unroll
-            for (int i = 0; i < kGCols; ++i) dr[gcol_global(i)] = row[i];
-#pragma unroll
-            for (int t = 0; t < 16; ++t) {
-              if (t < P.opt.terms_active) {
-                const float bt = s_basis[t * BS];
-                dr[kGOffSh + 3 * t] = w0 * bt;
-                dr[kGOffSh + 3 * t + 1] = w1 * bt;
-                dr[kGOffSh + 3 * t + 2] = w2 * bt;
-              }
-            }
-          }
-        }
+        if (DET) det_r = det_row(P, x, y, px.ncomp, id);  // the row is written by the warp below
         px.T = xm(px.T, xs(1.0, a));
         ++px.ncomp;
         if (px.ncomp >= stop) done = true;
       }
     }
-    if (DET) {
-      __syncwarp();
-      return;
-    }
     s_w[0] = w0;
     s_w[1] = w1;
     s_w[2] = w2;
+    if (DET) {
+      // deterministic mode: each record's whole row (zeros included) to its slot,
+      // written by the warp 32 columns per store (coalesced)
+      const unsigned wm = __ballot_sync(FULL, rec && det_r >= 0);
+      __syncwarp();
+      const int wbase = threadIdx.x & ~31;
+      const int ta = P.opt.terms_active;
+      for (unsigned mm = wm; mm; mm &= mm - 1u) {
+        const int m = __ffs(mm) - 1;
+        const long long r = __shfl_sync(FULL, det_r, m);
+        const int tm = wbase + m;
+        const float* rw = s_row + kGCols * tm;
+        float* dst = P.det_rec32 + (size_t)r * G;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int c = 32 * q + lane;
+          if (c >= G) continue;
+          float val = 0.f;
+          if (c < 12) val = rw[c];
+          else if (c < kGOffAn) val = c - kGOffSc < 8 ? rw[12 + c - kGOffSc] : 0.f;
+          else if (c < kGOffEta) val = c - kGOffAn < 8 ? rw[20 + c - kGOffAn] : 0.f;
+          else if (c < kGOffSh) val = rw[28 + c - kGOffEta];
+          else {
+            const int k = c - kGOffSh, t = k / 3, ch = k - 3 * t;
+            if (t < ta) val = s_w_all[4 * tm + ch] * s_basis_all[t * BS + tm];
+          }
+          dst[c] = val;
+        }
+      }
+      __syncwarp();
+      return;
+    }
     const unsigned recmask = __ballot_sync(FULL, rec);
     if (!recmask) return;
     ++n_steps;
