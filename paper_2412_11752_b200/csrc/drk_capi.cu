@@ -591,7 +591,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   float band_ms[4] = {0, 0, 0, 0};
   const int nb = (int)c->bands.size() - 1;
   // banded frames keep each band's sorted lists for the backward while free
-  // memory stays above a quarter of the device (the next band's binning reuses
+  // memory stays above an eighth of the device (the next band's binning reuses
   // the pair buffers, so this only needs room for the ids and offsets)
   c->band_cache_valid = nb > 1 && opt->record_replay == 0;
   if (c->band_cache_valid) {
@@ -612,7 +612,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
       const size_t have = c->band_ids[b].bytes + c->band_off[b].bytes;
       int* ids = nullptr;
       long long* offs = nullptr;
-      if (free_b + have > need + total_b / 4) {
+      if (free_b + have > need + total_b / 8) {
         ids = ensure<int>(c->band_ids[b], (size_t)n_pairs + 1);
         offs = ensure<long long>(c->band_off[b], (size_t)n_tiles + 1);
       }
@@ -981,7 +981,8 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->eval_scr, &c->eval_px, &c->eval_off, &c->ovf_scr, &c->ovf_list, &c->tord,
                     &c->rowest, &c->host_raw, &c->host_img, &c->pxcomp, &c->det_cnt, &c->det_base,
                     &c->det_rec, &c->det_id, &c->det_tile, &c->det_sort, &c->det_poff, &c->det_acc, &c->det_rowoff,
-                    &c->comm_buf, &c->scan_tmp2, &c->replay_cid, &c->replay_cval, &c->pidx, &c->tie_long};
+                    &c->comm_buf, &c->scan_tmp2, &c->replay_cid, &c->replay_cval, &c->pidx, &c->tie_long,
+                    &c->det_tflag, &c->det_tpos, &c->det_tstart, &c->det_tprim};
   for (DevBuf* b : bufs) release(*b);
   for (DevBuf& b : c->band_ids) release(b);
   for (DevBuf& b : c->band_off) release(b);

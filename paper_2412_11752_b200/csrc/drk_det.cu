@@ -14,9 +14,10 @@
 //      per-pixel path for the pixels the forward re-rendered in fp64 (or for
 //      every pixel in the list / exact-sort / fp64-alpha modes);
 //   3. a stable radix sort of the record slots by primitive id keeps, within a
-//      primitive, the (tile, pixel, composite) order; one warp per primitive
-//      then walks its records, forming each tile's partial in fp64 and adding
-//      the partials tile by tile to an fp64 accumulator.
+//      primitive, the (tile, pixel, composite) order; the records of each
+//      (primitive, tile) pair — a tile segment — are summed in order by one warp
+//      (fp64, in parallel over the segments), then one warp per primitive adds
+//      its tile partials in tile order to an fp64 accumulator.
 // The result does not depend on scheduling: two runs are bitwise identical.
 // Record rows take G floats (fast-kernel frames) or doubles (reference precision) each; frames whose records exceed the memory budget
 // are processed in chunks of tile rows (in row order, so the accumulation order
@@ -85,61 +86,97 @@ __global__ void k_det_segments(long long n, const unsigned* __restrict__ k, long
   if (i == n - 1 || k[i + 1] != key) seg[2 * (size_t)key + 1] = i + 1;
 }
 
-// One warp per primitive: its records in (tile, pixel, composite) order; the
-// fp64 partial of each tile is added to the running total when the tile ends.
-// Lanes are gradient columns (three 32-column chunks per record, G <= 96); the
-// record indices, tiles and rows of 8 records are loaded ahead of the
-// (sequential, fixed-order) accumulation, so the loads overlap.
+// Tile segments of the sorted records: a segment = the records of one
+// (primitive, tile) pair, consecutive after the stable sort by primitive.
+__global__ void k_det_tseg_flags(long long n, const unsigned* __restrict__ k, const unsigned* __restrict__ rec_of,
+                                 const int* __restrict__ tile_of, int* flag) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  flag[i] = (i == 0 || k[i] != k[i - 1] || tile_of[rec_of[i]] != tile_of[rec_of[i - 1]]) ? 1 : 0;
+}
+
+__global__ void k_det_tseg_starts(long long n, const int* __restrict__ flag, const long long* __restrict__ pos,
+                                  const unsigned* __restrict__ k, long long* starts, unsigned* seg_prim) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (flag[i]) {
+    starts[pos[i]] = i;
+    seg_prim[pos[i]] = k[i];
+  }
+}
+
+// Phase 1: one warp per tile segment sums its records' rows in order (fp64)
+// and stores the tile partial in the segment's first row.
 template <typename RT>
-__global__ void k_det_reduce(int n, int G, const long long* __restrict__ seg, const unsigned* __restrict__ rec_of,
-                             const int* __restrict__ tile_of, const RT* __restrict__ rows, double* acc) {
+__global__ void k_det_tseg_sum(long long nseg, long long nrec, int G, const long long* __restrict__ starts,
+                               const unsigned* __restrict__ rec_of, RT* rows) {
+  constexpr int kB = 8;
+  const long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= nseg) return;
+  const long long b = starts[t], e = t + 1 < nseg ? starts[t + 1] : nrec;
+  double part[3] = {0.0, 0.0, 0.0};
+  for (long long r0 = b; r0 < e; r0 += kB) {
+    double v[kB][3];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const unsigned rec = r0 + u < e ? rec_of[r0 + u] : 0u;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int c = 32 * q + lane;
+        v[u][q] = (r0 + u < e && c < G) ? (double)rows[(size_t)rec * G + c] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) part[q] += v[u][q];
+  }
+  const unsigned first = rec_of[b];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int c = 32 * q + lane;
+    if (c < G) rows[(size_t)first * G + c] = (RT)part[q];
+  }
+}
+
+// Phase 2: one warp per primitive adds its tile partials in tile order to the
+// fp64 accumulator (the reference's tile-then-id reduction, grad.cpp:352-368).
+template <typename RT>
+__global__ void k_det_prim_sum(int n, int G, const long long* __restrict__ pseg, const long long* __restrict__ starts,
+                               const unsigned* __restrict__ rec_of, const RT* __restrict__ rows, double* acc) {
   constexpr int kB = 8;
   const int p = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= n) return;
-  const long long b = seg[2 * (size_t)p], e = seg[2 * (size_t)p + 1];
+  const long long b = pseg[2 * (size_t)p], e = pseg[2 * (size_t)p + 1];
   if (e <= b) return;
-  double total[3], part[3] = {0.0, 0.0, 0.0};
+  double total[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     const int c = 32 * q + lane;
     total[q] = c < G ? acc[(size_t)p * G + c] : 0.0;
   }
-  int cur = -1;
-  for (long long r0 = b; r0 < e; r0 += kB) {
-    unsigned rec[kB];
-    int tl[kB];
+  for (long long t0 = b; t0 < e; t0 += kB) {
     double v[kB][3];
 #pragma unroll
-    for (int u = 0; u < kB; ++u) rec[u] = r0 + u < e ? rec_of[r0 + u] : 0u;
-#pragma unroll
     for (int u = 0; u < kB; ++u) {
-      tl[u] = r0 + u < e ? tile_of[rec[u]] : -1;
+      const unsigned rec = t0 + u < e ? rec_of[starts[t0 + u]] : 0u;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const int c = 32 * q + lane;
-        v[u][q] = (r0 + u < e && c < G) ? (double)rows[(size_t)rec[u] * G + c] : 0.0;
+        v[u][q] = (t0 + u < e && c < G) ? (double)rows[(size_t)rec * G + c] : 0.0;
       }
     }
 #pragma unroll
-    for (int u = 0; u < kB; ++u) {
-      if (r0 + u >= e) break;
-      if (tl[u] != cur) {
+    for (int u = 0; u < kB; ++u)
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          total[q] += part[q];
-          part[q] = 0.0;
-        }
-        cur = tl[u];
-      }
-#pragma unroll
-      for (int q = 0; q < 3; ++q) part[q] += v[u][q];
-    }
+      for (int q = 0; q < 3; ++q) total[q] += v[u][q];
   }
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     const int c = 32 * q + lane;
-    if (c < G) acc[(size_t)p * G + c] = total[q] + part[q];
+    if (c < G) acc[(size_t)p * G + c] = total[q];
   }
 }
 
@@ -201,7 +238,7 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
   // fp32 rows where the fast fp32 kernel computes the records; fp64 rows where
   // every record comes from the fp64 per-pixel path (reference precision)
   const size_t row_bytes = fast ? sizeof(float) : sizeof(double);
-  const size_t per_rec = row_bytes * G + 2 * sizeof(int) + 4 * sizeof(unsigned);
+  const size_t per_rec = row_bytes * G + 2 * sizeof(int) + 4 * sizeof(unsigned) + 28;  // + tile-segment scratch
   long long limit = c->det_chunk_limit;
   if (limit <= 0) {
     size_t free_b = 0, total_b = 0;
@@ -262,11 +299,24 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
         DRK_COUNT_LAUNCH();
         if (int st = sort_pairs(c, kk, vv, k2, v2, R)) return st;
         tr("sort");
+        // tile segments (one per (primitive, tile)): partials in parallel, then
+        // each primitive's partials in tile order
+        int* tflag = ensure<int>(c->det_tflag, (size_t)R + 1);
+        long long* tpos = ensure<long long>(c->det_tpos, (size_t)R + 1);
+        long long* tstart = ensure<long long>(c->det_tstart, (size_t)R + 1);
+        unsigned* tprim = ensure<unsigned>(c->det_tprim, (size_t)R + 1);
+        if (!tflag || !tpos || !tstart || !tprim) return set_error(c, DRK_ERR_OOM, "deterministic backward segments");
+        k_det_tseg_flags<<<blocks(R, 256), 256, 0, s>>>(R, kk, vv, tiles, tflag);
+        long long nseg = 0;
+        if (int st = exclusive_scan<int>(c, tflag, R, tpos, &nseg)) return st;
+        k_det_tseg_starts<<<blocks(R, 256), 256, 0, s>>>(R, tflag, tpos, kk, tstart, tprim);
+        if (fast) k_det_tseg_sum<float><<<blocks(32LL * nseg, 256), 256, 0, s>>>(nseg, R, G, tstart, vv, Q.det_rec32);
+        else k_det_tseg_sum<double><<<blocks(32LL * nseg, 256), 256, 0, s>>>(nseg, R, G, tstart, vv, Q.det_rec);
         cudaMemsetAsync(seg, 0, sizeof(long long) * 2 * (size_t)n, s);
-        k_det_segments<<<blocks(R, 256), 256, 0, s>>>(R, kk, seg);
-        if (fast) k_det_reduce<float><<<blocks(32LL * n, 256), 256, 0, s>>>(n, G, seg, vv, tiles, Q.det_rec32, acc);
-        else k_det_reduce<double><<<blocks(32LL * n, 256), 256, 0, s>>>(n, G, seg, vv, tiles, Q.det_rec, acc);
-        launch_counter() += 2;
+        k_det_segments<<<blocks(nseg, 256), 256, 0, s>>>(nseg, tprim, seg);
+        if (fast) k_det_prim_sum<float><<<blocks(32LL * n, 256), 256, 0, s>>>(n, G, seg, tstart, vv, Q.det_rec32, acc);
+        else k_det_prim_sum<double><<<blocks(32LL * n, 256), 256, 0, s>>>(n, G, seg, tstart, vv, Q.det_rec, acc);
+        launch_counter() += 5;
         if (int st = cuda_check(c, cudaGetLastError(), "deterministic backward reduce")) return st;
         tr("reduce");
       }
@@ -295,7 +345,8 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
   }
   // record scratch can reach tens of GB on large frames: give it back
   constexpr size_t kKeep = 256u << 20;
-  for (DevBuf* b : {&c->det_rec, &c->det_id, &c->det_tile, &c->det_sort})
+  for (DevBuf* b : {&c->det_rec, &c->det_id, &c->det_tile, &c->det_sort, &c->det_tflag, &c->det_tpos, &c->det_tstart,
+                    &c->det_tprim})
     if (b->bytes > kKeep) release(*b);
   tr("release");
   if (trace) fprintf(stderr, "[drk det]%s\n", tline.c_str());

@@ -190,6 +190,7 @@ struct drk_ctx {
   // deterministic backward: slot counts / record offsets, record rows, ids, tiles,
   // sort buffers, per-primitive offsets, fp64 accumulator
   drk::DevBuf det_cnt, det_base, det_rec, det_id, det_tile, det_sort, det_poff, det_acc, det_rowoff;
+  drk::DevBuf det_tflag, det_tpos, det_tstart, det_tprim;  // tile segments of the sorted records
   long long det_chunk_limit = 0;          // test hook: records per chunk (0 = memory-based)
   drk::DevBuf comm_buf;                   // drk_allreduce_adam: padded gradient / parameter exchange buffers
   drk::DevBuf scan_tmp2, replay_cid, replay_cval;  // drk_get_replay: per-pixel offsets, compacted records
