@@ -241,10 +241,14 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
   const size_t per_rec = row_bytes * G + 2 * sizeof(int) + 4 * sizeof(unsigned) + 28;  // + tile-segment scratch
   long long limit = c->det_chunk_limit;
   if (limit <= 0) {
+    // at most 16 GB of record scratch (kept by the context between calls: no
+    // multi-second allocation of a frame-sized buffer per backward), and at most
+    // half of the free memory
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    const size_t have = c->det_rec.bytes + c->det_id.bytes + c->det_tile.bytes + c->det_sort.bytes;
-    limit = (long long)((free_b + have) / 2 / per_rec);
+    const size_t have = c->det_rec.bytes + c->det_id.bytes + c->det_tile.bytes + c->det_sort.bytes +
+                        c->det_tflag.bytes + c->det_tpos.bytes + c->det_tstart.bytes + c->det_tprim.bytes;
+    limit = (long long)(std::min<size_t>((free_b + have) / 2, (size_t)16 << 30) / per_rec);
   }
   limit = std::max(1LL, std::min(limit, (long long)0x7fffffff));
 
@@ -343,11 +347,6 @@ int run_backward_det(drk_ctx* c, const RasterParams& P, const std::vector<int>& 
       DRK_COUNT_LAUNCH();
     }
   }
-  // record scratch can reach tens of GB on large frames: give it back
-  constexpr size_t kKeep = 256u << 20;
-  for (DevBuf* b : {&c->det_rec, &c->det_id, &c->det_tile, &c->det_sort, &c->det_tflag, &c->det_tpos, &c->det_tstart,
-                    &c->det_tprim})
-    if (b->bytes > kKeep) release(*b);
   tr("release");
   if (trace) fprintf(stderr, "[drk det]%s\n", tline.c_str());
   unsigned long long ovf = 0;
