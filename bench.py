@@ -87,6 +87,27 @@ def maybe_spawn(args) -> None:
     sys.exit(subprocess.call(cmd))
 
 
+_JSON_FD = None
+
+
+def claim_stdout() -> None:
+    """Keep stdout for the one JSON line: anything else written to file
+    descriptor 1 (NCCL's version banner, library prints) goes to stderr."""
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -274,12 +295,13 @@ def run_reference(args):
                                                                                            fb["seconds_loss_bwd"]),
                         "workload": fb["sample"]},
             "e2e": {"value": v, "unit": "megapixels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
     args = parse()
     maybe_spawn(args)
+    claim_stdout()
     if args.impl == "reference":
         run_reference(args)
         return
@@ -420,7 +442,8 @@ def main():
         e_tot = float(t.item())
     e2e = {"value": world * px / (e_tot / args.steps * 1e-3) / 1e6, "unit": "megapixels/s",
            "h2d_bytes_per_step": int(host_raw.numel() * 4), "d2h_bytes_per_step": int(px * 8 * 4),
-           "path": "drk_forward_host (C-ABI): pinned host raw params -> device -> 4 framebuffers -> pinned host"}
+           "path": "drk_forward_host (C-ABI): pinned host raw params -> device (H2D copy) -> render; the raster "
+                   "kernels store the 4 framebuffers into the pinned host buffers (zero-copy D2H)"}
 
     # ---- forward + backward (config 2) ----
     fwd_bwd = None
@@ -643,7 +666,7 @@ def main():
                 "roofline": roofline, "hbm_roofline": hbm_roofline, "adapter": adapter, "e2e": e2e, "fwd_bwd": fwd_bwd, "multiview": multiview, "train": train, "train_config4": train_c4,
                 "cpu_baseline": cpu,
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 

@@ -201,8 +201,10 @@ int drk_forward_again(drk_ctx* ctx, const drk_camera* cam, const drk_options* op
 int drk_forward_prims(drk_ctx* ctx, const drk_prims* prims, int n, int k, int sh_terms,
                       const drk_camera* cam, const drk_options* opt, float* color,
                       float* depth, float* normal, float* alpha);
-/* Host-buffer variant of drk_forward: copies raw in, renders, copies images
- * out (any output may be NULL); synchronous. */
+/* Host-buffer variant of drk_forward: copies raw in and renders; page-locked
+ * outputs (mapped under unified addressing) are written in place by the
+ * kernels as tiles finish (zero-copy), other outputs are copied out after the
+ * forward.  Any output may be NULL; synchronous. */
 int drk_forward_host(drk_ctx* ctx, const float* raw_host, int n, int k, int sh_terms,
                      const drk_camera* cam, const drk_options* opt, float* color_host,
                      float* depth_host, float* normal_host, float* alpha_host);

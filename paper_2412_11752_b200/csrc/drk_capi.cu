@@ -345,108 +345,6 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
   return DRK_OK;
 }
 
-// Host-buffer forward: the fast kernel counts finished tiles per band of
-// kCopyRows tile rows; copy_stream waits on each band's counter
-// (cuStreamWaitValue32) and copies that band's framebuffer rows to the host
-// while later bands still rasterize.  Pixels the fp64 pass rewrites are
-// patched afterwards (finish_copy_out).
-constexpr int kCopyRows = 8;
-
-// Driver stream memory ops through the runtime's entry-point query (the
-// library does not link libcuda directly).
-using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-static WaitValueFn driver_fn(const char* name) {
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
-    return nullptr;
-  return reinterpret_cast<WaitValueFn>(fn);
-}
-static WaitValueFn wait_value32() {
-  static WaitValueFn f = driver_fn("cuStreamWaitValue32");
-  return f;
-}
-static WaitValueFn write_value32() {
-  static WaitValueFn f = driver_fn("cuStreamWriteValue32");
-  return f;
-}
-
-static int start_copy_out(drk_ctx* c, RasterParams& P) {
-  const CamD& cd = c->camd;
-  const int nbands = (cd.tiles_y + kCopyRows - 1) / kCopyRows;
-  if (!wait_value32() || !write_value32()) return DRK_OK;  // no stream memory ops: copies after the forward
-  unsigned* prog = ensure<unsigned>(c->progress, nbands);
-  if (!prog) return set_error(c, DRK_ERR_OOM, "copy-out counters");
-  if (!c->copy_stream && cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
-    return set_error(c, DRK_ERR_CUDA, "copy stream");
-  cudaMemsetAsync(prog, 0, sizeof(unsigned) * nbands, c->stream);
-  if (!c->ev[9]) cudaEventCreateWithFlags(&c->ev[9], cudaEventDisableTiming);
-  cudaEventRecord(c->ev[9], c->stream);
-  cudaStreamWaitEvent(c->copy_stream, c->ev[9], 0);
-  P.progress = prog;
-  P.prog_rows = kCopyRows;
-  const size_t W = (size_t)cd.W;
-  for (int b = 0; b < nbands; ++b) {
-    const int ty0 = b * kCopyRows, ty1 = std::min(cd.tiles_y, ty0 + kCopyRows);
-    const unsigned need = (unsigned)((ty1 - ty0) * cd.tiles_x * (256 / P.fast_nt));
-    if (wait_value32()(c->copy_stream, (CUdeviceptr)(prog + b), need, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-      return set_error(c, DRK_ERR_CUDA, "stream wait value");
-    const size_t y0 = (size_t)ty0 * kTile, y1 = std::min((size_t)cd.H, (size_t)ty1 * kTile);
-    const size_t p0 = y0 * W, np = (y1 - y0) * W;
-    if (c->hout.color) cudaMemcpyAsync(c->hout.color + 3 * p0, P.color + 3 * p0, 12 * np, cudaMemcpyDeviceToHost, c->copy_stream);
-    if (c->hout.depth) cudaMemcpyAsync(c->hout.depth + p0, P.depth + p0, 4 * np, cudaMemcpyDeviceToHost, c->copy_stream);
-    if (c->hout.normal) cudaMemcpyAsync(c->hout.normal + 3 * p0, P.normal + 3 * p0, 12 * np, cudaMemcpyDeviceToHost, c->copy_stream);
-    if (c->hout.alpha) cudaMemcpyAsync(c->hout.alpha + p0, P.alpha + p0, 4 * np, cudaMemcpyDeviceToHost, c->copy_stream);
-  }
-  c->hout.used = true;
-  return DRK_OK;
-}
-
-__global__ void k_gather_patch(const int* __restrict__ list, int count, const float* color, const float* depth,
-                               const float* normal, const float* alpha, float* out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= count) return;
-  const size_t p = (size_t)list[t];
-  float* o = out + 8 * (size_t)t;
-  for (int k = 0; k < 3; ++k) {
-    o[k] = color ? color[3 * p + k] : 0.f;
-    o[4 + k] = normal ? normal[3 * p + k] : 0.f;
-  }
-  o[3] = depth ? depth[p] : 0.f;
-  o[7] = alpha ? alpha[p] : 0.f;
-}
-
-// After the forward: the fp64-re-rendered pixels (redo list) overwrite what
-// the band copies took.
-static int finish_copy_out(drk_ctx* c, const float* color, const float* depth, const float* normal,
-                           const float* alpha) {
-  const int count = (int)c->stats.fp64_pixels;
-  std::vector<float> h(8 * (size_t)count);
-  if (count > 0) {
-    float* d = ensure<float>(c->patch, 8 * (size_t)count);
-    if (!d) return set_error(c, DRK_ERR_OOM, "patch buffer");
-    k_gather_patch<<<(count + 255) / 256, 256, 0, c->stream>>>(static_cast<const int*>(c->redo.p), count, color, depth,
-                                                              normal, alpha, d);
-    DRK_COUNT_LAUNCH();
-    cudaMemcpyAsync(h.data(), d, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream);
-  }
-  std::vector<int> ids(count);
-  if (count > 0) cudaMemcpyAsync(ids.data(), c->redo.p, sizeof(int) * count, cudaMemcpyDeviceToHost, c->stream);
-  if (int st = cuda_check(c, cudaStreamSynchronize(c->stream), "patch")) return st;
-  if (int st = cuda_check(c, cudaStreamSynchronize(c->copy_stream), "copy-out")) return st;
-  for (int t = 0; t < count; ++t) {
-    const size_t p = (size_t)ids[t];
-    const float* o = h.data() + 8 * (size_t)t;
-    for (int k = 0; k < 3; ++k) {
-      if (c->hout.color) c->hout.color[3 * p + k] = o[k];
-      if (c->hout.normal) c->hout.normal[3 * p + k] = o[4 + k];
-    }
-    if (c->hout.depth) c->hout.depth[p] = o[3];
-    if (c->hout.alpha) c->hout.alpha[p] = o[7];
-  }
-  return DRK_OK;
-}
-
 // DRK_HOST_TRACE=1: host wall-clock checkpoints of run_forward on stderr
 // (development aid for host-side gaps between the device stages)
 struct HostTrace {
@@ -645,16 +543,10 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     }
     P.tile_base = ty_lo * cd.tiles_x;
     P.fast_nt = choose_nt(c, n_pairs, (ty_hi - ty_lo) * cd.tiles_x);
-    // exactly the launches where launch_raster runs k_raster_fast (the only
-    // kernel that advances the band counters)
-    const bool copy_out = c->hout.active && nb == 1 && P.opt.use_cache && P.opt.raster_kernel != 1 &&
-                          raster_fast_eligible(P) && !c->validate_fast && (ty_hi - ty_lo) * cd.tiles_x > 0;
     // Longest tile lists first (a shorter tail: config 1 -1.9%, config 2 -4% raster
-    // time) on the device path; the host copy-out keeps row-major order so that
-    // framebuffer bands complete, and leave, while the raster still runs.
-    // DRK_TILE_ORDER=0 forces row-major.
+    // time).  DRK_TILE_ORDER=0 forces row-major.
     static const int tile_order_mode = getenv("DRK_TILE_ORDER") ? atoi(getenv("DRK_TILE_ORDER")) : 1;
-    if (tile_order_mode > 0 && !copy_out && raster_fast_eligible(P) && P.opt.raster_kernel != 1) {
+    if (tile_order_mode > 0 && raster_fast_eligible(P) && P.opt.raster_kernel != 1) {
       const int nt = (ty_hi - ty_lo) * cd.tiles_x;
       unsigned* tk = ensure<unsigned>(c->tord, 4 * (size_t)nt + 4);
       if (!tk) return set_error(c, DRK_ERR_OOM, "tile order");
@@ -663,9 +555,6 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
       launch_counter() += 1;
       if (int st = sort_pairs(c, tk, tv, tk2, tv2, nt)) return st;
       P.tile_order = reinterpret_cast<const int*>(tv);
-    }
-    if (copy_out) {
-      if (int st = start_copy_out(c, P)) return st;
     }
     launch_raster(P, (ty_hi - ty_lo) * cd.tiles_x, false, s, c->timing ? c->ev[5] : nullptr);
     mark(c, 6);
@@ -976,7 +865,7 @@ void drk_ctx_destroy(drk_ctx* c) {
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->sk,
                     &c->hist, &c->sortoff, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
-                    &c->counters, &c->scan_tmp, &c->loss_tmp, &c->progress, &c->patch, &c->scene_aos,
+                    &c->counters, &c->scan_tmp, &c->loss_tmp, &c->scene_aos,
                     &c->loss_part, &c->ssim_f, &c->dens_code, &c->dens_pos,
                     &c->eval_scr, &c->eval_px, &c->eval_off, &c->ovf_scr, &c->ovf_list, &c->tord,
                     &c->rowest, &c->host_raw, &c->host_img, &c->pxcomp, &c->det_cnt, &c->det_base,
@@ -988,7 +877,6 @@ void drk_ctx_destroy(drk_ctx* c) {
   for (DevBuf& b : c->band_off) release(b);
   for (cudaEvent_t e : c->ev)
     if (e) cudaEventDestroy(e);
-  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1073,6 +961,20 @@ static bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// Device address of a page-locked host buffer (mapped under unified
+// addressing), or null: the kernels then write the framebuffer straight into
+// host memory (zero-copy) as tiles finish.
+static float* mapped(float* p, bool* ok) {
+  if (!p) return nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess || a.type != cudaMemoryTypeHost || !a.devicePointer) {
+    cudaGetLastError();
+    *ok = false;
+    return nullptr;
+  }
+  return static_cast<float*>(a.devicePointer);
+}
+
 int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_terms, const drk_camera* cam,
                      const drk_options* opt, float* color_host, float* depth_host, float* normal_host,
                      float* alpha_host) {
@@ -1084,35 +986,28 @@ int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_ter
   float* img = ensure<float>(c->host_img, 8 * npix + 1);
   if (!r || !img) return set_error(c, DRK_ERR_OOM, "host staging");
   cudaMemcpyAsync(r, raw_host, sizeof(float) * S * n, cudaMemcpyHostToDevice, c->stream);
+  // Page-locked outputs: the raster kernels store the pixels straight into
+  // them as tiles finish (zero-copy; config 1 e2e 25.9 ms vs 26.8 ms with a
+  // band-wise staging copy).  DRK_HOST_OUT=copy forces device framebuffers.
+  static const bool zero_copy = !getenv("DRK_HOST_OUT") || std::string(getenv("DRK_HOST_OUT")) != "copy";
+  if (zero_copy) {
+    bool ok = true;
+    float* mc = mapped(color_host, &ok);
+    float* md = mapped(depth_host, &ok);
+    float* mn = mapped(normal_host, &ok);
+    float* ma = mapped(alpha_host, &ok);
+    if (ok) {
+      const int st = drk_forward(c, r, n, k, sh_terms, cam, opt, mc, md, mn, ma);
+      if (st) return st;
+      return cuda_check(c, cudaStreamSynchronize(c->stream), "forward_host");
+    }
+  }
+  // not page-locked (or not mapped): device framebuffers, copied out afterwards
   float* dcol = color_host ? img : nullptr;
   float* ddep = depth_host ? img + 3 * npix : nullptr;
   float* dnor = normal_host ? img + 4 * npix : nullptr;
   float* dalp = alpha_host ? img + 7 * npix : nullptr;
-  c->hout.color = color_host;
-  c->hout.depth = depth_host;
-  c->hout.normal = normal_host;
-  c->hout.alpha = alpha_host;
-  // band copies only into page-locked buffers: a copy into pageable memory
-  // blocks the calling thread, which has not launched the raster yet
-  c->hout.active = is_pinned(color_host) && is_pinned(depth_host) && is_pinned(normal_host) && is_pinned(alpha_host);
-  c->hout.used = false;
-  const int st = drk_forward(c, r, n, k, sh_terms, cam, opt, dcol, ddep, dnor, dalp);
-  c->hout.active = false;
-  if (c->hout.used) {
-    c->hout.used = false;
-    if (st) {
-      // release the copy stream's waits before reporting the error
-      const int nbands = (c->camd.tiles_y + kCopyRows - 1) / kCopyRows;
-      for (int b = 0; b < nbands; ++b)
-        write_value32()(c->stream, (CUdeviceptr)(static_cast<unsigned*>(c->progress.p) + b), 0x7fffffffu, 0);
-      cudaStreamSynchronize(c->stream);
-      cudaStreamSynchronize(c->copy_stream);
-      return st;
-    }
-    // framebuffer rows went out during the raster; patch the fp64-re-rendered pixels
-    return finish_copy_out(c, dcol, ddep, dnor, dalp);
-  }
-  if (st) return st;
+  if (int st = drk_forward(c, r, n, k, sh_terms, cam, opt, dcol, ddep, dnor, dalp)) return st;
   if (color_host) cudaMemcpyAsync(color_host, dcol, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, c->stream);
   if (depth_host) cudaMemcpyAsync(depth_host, ddep, sizeof(float) * npix, cudaMemcpyDeviceToHost, c->stream);
   if (normal_host) cudaMemcpyAsync(normal_host, dnor, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, c->stream);

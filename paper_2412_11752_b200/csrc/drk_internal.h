@@ -104,8 +104,6 @@ struct RasterParams {
   unsigned int* redo_count;
   const float4* frame32;  // per prim: (R_x, a_x), (R_y, a_y), (R_z, a_z) with a = o - mu, fp32 (backward)
   int tile_base;          // first tile of this launch (banded frames: tile rows processed band by band)
-  unsigned* progress;     // fast forward: finished CTAs per band of prog_rows tile rows (host-buffer copy-out), or null
-  int prog_rows;
   const float* shrec;     // fast kernel: per-primitive fp32 shape records (K == 8)
   int* pxstop;            // composites until saturation per pixel (INT_MAX: never), written by the forward
   int fast_nt;            // fast forward: threads per CTA (256: tile, 128: half tile), raster_fast_nt
@@ -204,15 +202,6 @@ struct drk_ctx {
   long long band_pair_limit = 0;  // test hook: force bands above this many pairs (0 = memory-based)
   size_t device_bytes = 0;        // cudaMemGetInfo total, queried once
   int64_t pts_cap = 0;
-
-  // host-buffer forward (drk_forward_host): framebuffer rows are copied out
-  // band by band on copy_stream while the raster still runs
-  struct HostOut {
-    float *color = nullptr, *depth = nullptr, *normal = nullptr, *alpha = nullptr;
-    bool active = false, used = false;
-  } hout;
-  cudaStream_t copy_stream = nullptr;
-  drk::DevBuf progress, patch;
 
   // stage timing
   bool timing = false;

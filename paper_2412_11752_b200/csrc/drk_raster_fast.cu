@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   Geo* s_geo = reinterpret_cast<Geo*>(reinterpret_cast<float4*>(s_id + RING) + 4 * NT);  // [NT]: next batch's Geo
   __shared__ unsigned long long s_bar;
 #endif
-  __shared__ unsigned s_ddmax, s_done;
+  __shared__ unsigned s_ddmax;
   __shared__ TileConst tc;
   const int cta_tile = NT == 256 ? blockIdx.x : blockIdx.x >> 1;
   const int tile = P.tile_base + (P.tile_order ? P.tile_order[cta_tile] : cta_tile);
@@ -183,7 +183,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   }
   if (threadIdx.x == 0) {
     s_ddmax = 0u;
-    s_done = 0u;
     tc.d0[0] = d0[0];
     tc.d0[1] = d0[1];
     tc.d0[2] = d0[2];
@@ -467,12 +466,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
     }
   }
   if (active) write_pixel(P, px, x, y);
-  if (P.progress) {
-    // the CTA's last thread to finish marks the tile done for the copy-out
-    // (drk_forward_host waits on the band counter with a stream memory op)
-    __threadfence();
-    if (atomicAdd(&s_done, 1u) == blockDim.x - 1u) atomicAdd(&P.progress[(tile / P.cam.tiles_x) / P.prog_rows], 1u);
-  }
 }
 
 __device__ __forceinline__ void write_pixel(const RasterParams& P, const FastPixel& px, int x, int y) {
