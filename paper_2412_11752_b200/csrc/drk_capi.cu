@@ -22,6 +22,7 @@ __global__ void k_prep_warp(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbo
 __global__ void k_prep_hull(int n, const int2* ptsref, double2* pts_pool, CamD cam, OptD opt, int4* bbox, int2* hullref,
                             double2* pool, long long pool_cap, int* rowcnt, unsigned long long* counters);
 size_t prep_warp_smem();
+int prep_warp_warps();
 __global__ void k_prep1(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pool,
                         long long pool_cap, int* rowcnt, unsigned long long* counters, const int* list, int list_n,
                         double2* scratch, int scratch_cap, int* overflow);
@@ -410,7 +411,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
       static PerDeviceOnce attr;
       const size_t smem = prep_warp_smem();
       attr([&] { cudaFuncSetAttribute(k_prep_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
-      k_prep_warp<<<(n + 7) / 8, 256, smem, s>>>(A, cd, od, geo, bbox, hullref, ppool, c->pts_cap, ptsref, rowcnt,
+      k_prep_warp<<<(n + prep_warp_warps() - 1) / prep_warp_warps(), 32 * prep_warp_warps(), smem, s>>>(A, cd, od, geo, bbox, hullref, ppool, c->pts_cap, ptsref, rowcnt,
                                                    ctr, ovf, static_cast<float4*>(c->frame32.p));
       k_prep_hull<<<(unsigned)((2LL * n + 255) / 256), 256, 0, s>>>(n, ptsref, ppool, cd, od, bbox, hullref, pool,
                                                                     c->hull_cap, rowcnt, ctr);
