@@ -1406,6 +1406,8 @@ template <int MODE, bool BWD>
 __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  constexpr int kPopVals = BWD ? 3 : 9;
+  __shared__ double s_pop[4 * 32 * kPopVals];  // per warp: 32 pops x kPopVals (step 3)
   const unsigned total = *P.redo_count;
   // pixels are fetched dynamically (P.redo_count[1] is the fetch counter, zeroed
   // at launch): a warp that drew a long tile list does not hold back a fixed
@@ -1432,6 +1434,19 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
     bool done = false;
     const long long beg = P.tileoff[tile], end = P.tileoff[tile + 1];
     long long j = beg;
+    // software pipeline over 32-entry chunks: the ray-plane constants (num, R_z:
+    // the first 32 bytes of Geo) of the next chunk and the ids of the one after
+    // are in flight while the current chunk is sorted, evaluated and composited
+    // (a long tile list is walked by one warp: load latency is its critical path)
+    auto ld_ray = [&](int id) -> double4 {
+      if (id < 0) return make_double4(0, 0, 0, 0);
+      const double2* q = reinterpret_cast<const double2*>(P.geo + id);
+      const double2 a = __ldg(q), b = __ldg(q + 1);
+      return make_double4(a.x, a.y, b.x, b.y);  // num, rz0, rz1, rz2
+    };
+    int id_a = beg + lane < end ? P.lid[beg + lane] : -1;
+    int id_b = beg + 32 + lane < end ? P.lid[beg + 32 + lane] : -1;
+    double4 g_a = ld_ray(id_a);
     while (!done) {
       // 1) up to 32 pops: parallel intersections, in-order SortCache on lane 0
       double my_rt = 0;
@@ -1440,14 +1455,16 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
       if (!list_end) {
         const long long jj = j + lane;
         double rt = 0;
-        int id = -1;
+        const int id = id_a;
+        const double4 g = g_a;
+        id_a = id_b;
+        g_a = ld_ray(id_b);
+        id_b = j + 64 + lane < end ? P.lid[j + 64 + lane] : -1;
         bool hit = false;
         if (jj < end) {
-          id = P.lid[jj];
-          const Geo& g = P.geo[id];
-          const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.rz[0], g.rz[1], g.rz[2]);
+          const double denom = xdot3(px.dir[0], px.dir[1], px.dir[2], g.y, g.z, g.w);
           if (fabs(denom) >= P.opt.grazing_eps) {
-            rt = g.num / denom;
+            rt = g.x / denom;
             hit = rt > 0;
           }
         }
@@ -1544,37 +1561,57 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
       e.valid = false;
       if (lane < npop) eval_pop<BWD>(P, px, my_rt, my_id, e);
       if (lane < npop && e.ev.degenerate) px.err = true;
-      // 3) in-order compositing (all lanes replicate the scalar state)
+      // 3) in-order compositing (all lanes replicate the scalar state).  Lane k
+      // first lays out what pop k contributes (alpha, 1 - alpha, and the colour /
+      // depth / normal factors, or the upstream dot product) in the warp's shared
+      // slots; the sequential loop then reads them as broadcasts: its critical path
+      // is the transmittance product alone (same explicitly rounded operations,
+      // same order as a per-pop loop).
+      double* slot = s_pop + (threadIdx.x >> 5) * 32 * kPopVals;
+      if (lane < npop) {
+        double* row = slot + lane * kPopVals;
+        row[0] = e.valid ? e.a : -1.0;  // -1: not composited
+        if (e.valid) {
+          row[1] = xs(1.0, e.a);
+          const Geo& g = P.geo[e.id];
+          const double sgn = e.denom < 0 ? 1.0 : -1.0;
+          const double n0 = sgn * g.rz[0], n1 = sgn * g.rz[1], n2 = sgn * g.rz[2];
+          if (!BWD) {
+            row[2] = e.rgb[0];
+            row[3] = e.rgb[1];
+            row[4] = e.rgb[2];
+            row[5] = e.rt;
+            row[6] = xm(sgn, g.rz[0]);
+            row[7] = xm(sgn, g.rz[1]);
+            row[8] = xm(sgn, g.rz[2]);
+          } else {
+            row[2] = (px.dC[0] * e.rgb[0] + px.dC[1] * e.rgb[1] + px.dC[2] * e.rgb[2]) + px.dD * e.rt +
+                     (px.dN[0] * n0 + px.dN[1] * n1 + px.dN[2] * n2) + px.dA;
+          }
+        }
+      }
+      __syncwarp();
       double wb_mine = 0, dat_mine = 0, T_mine = 1;
       int idx_mine = 0;
       int last_k = npop - 1;
       for (int k = 0; k < npop && !done; ++k) {
         last_k = k;
-        const bool valid = __shfl_sync(FULL, e.valid, k);
-        if (!valid) continue;
-        const double a = __shfl_sync(FULL, e.a, k);
-        const double rt = __shfl_sync(FULL, e.rt, k);
-        const double r0 = __shfl_sync(FULL, e.rgb[0], k), r1 = __shfl_sync(FULL, e.rgb[1], k),
-                     r2 = __shfl_sync(FULL, e.rgb[2], k);
-        const double denom = __shfl_sync(FULL, e.denom, k);
-        const int id = __shfl_sync(FULL, e.id, k);
-        const Geo& g = P.geo[id];
-        const double sgn = denom < 0 ? 1.0 : -1.0;
+        const double* row = slot + k * kPopVals;
+        const double a = row[0];
+        if (a < 0) continue;
         const double w = xm(px.T, a);
         ++px.n_comp;
         if (!BWD) {
-          px.C[0] = xa(px.C[0], xm(w, r0));
-          px.C[1] = xa(px.C[1], xm(w, r1));
-          px.C[2] = xa(px.C[2], xm(w, r2));
-          px.D = xa(px.D, xm(w, rt));
-          px.N[0] = xa(px.N[0], xm(w, xm(sgn, g.rz[0])));
-          px.N[1] = xa(px.N[1], xm(w, xm(sgn, g.rz[1])));
-          px.N[2] = xa(px.N[2], xm(w, xm(sgn, g.rz[2])));
+          px.C[0] = xa(px.C[0], xm(w, row[2]));
+          px.C[1] = xa(px.C[1], xm(w, row[3]));
+          px.C[2] = xa(px.C[2], xm(w, row[4]));
+          px.D = xa(px.D, xm(w, row[5]));
+          px.N[0] = xa(px.N[0], xm(w, row[6]));
+          px.N[1] = xa(px.N[1], xm(w, row[7]));
+          px.N[2] = xa(px.N[2], xm(w, row[8]));
           px.A = xa(px.A, w);
         } else {
-          const double cw = (px.dC[0] * r0 + px.dC[1] * r1 + px.dC[2] * r2) + px.dD * rt +
-                            (px.dN[0] * (sgn * g.rz[0]) + px.dN[1] * (sgn * g.rz[1]) + px.dN[2] * (sgn * g.rz[2])) +
-                            px.dA;
+          const double cw = row[2];
           px.rest -= w * cw;
           if (lane == k) {
             wb_mine = w;
@@ -1583,9 +1620,10 @@ __global__ void __launch_bounds__(128) k_raster_pixels_warp(RasterParams P) {
             idx_mine = (int)px.n_comp - 1;
           }
         }
-        px.T = xm(px.T, xs(1.0, a));
+        px.T = xm(px.T, row[1]);
         if (px.T < P.opt.early_stop) done = true;
       }
+      __syncwarp();
       if (!BWD && P.replay_cap > 0) {
         // replay records in order (lane k writes its own entry)
         int rec_idx = px.n_rec;

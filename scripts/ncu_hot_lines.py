@@ -1,18 +1,24 @@
 """Source lines of an ncu --set full report (--import-source, -lineinfo) ranked by
 warp-stall samples: share of executed instructions and of samples per line.
-usage: python scripts/ncu_hot_lines.py REPORT.ncu-rep [N]"""
+usage: python scripts/ncu_hot_lines.py REPORT.ncu-rep [N] [FUNCTION-SUBSTRING]"""
 import csv
 import subprocess
 import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+fsel = sys.argv[3] if len(sys.argv) > 3 else None
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
                      capture_output=True, text=True).stdout
-cur, hdr, agg = None, None, []
+cur, hdr, agg, fn = None, None, [], ""
 for r in csv.reader(txt.splitlines()):
     if len(r) >= 2 and r[0] == "File Path":
         cur = r[1].split("/")[-1]
+        continue
+    if len(r) >= 2 and r[0] == "Function Name":
+        fn = r[1]
+        continue
+    if fsel and fsel not in fn:
         continue
     if len(r) > 2 and r[0] == "Line No":
         hdr = r
