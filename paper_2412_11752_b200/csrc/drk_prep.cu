@@ -1015,16 +1015,51 @@ __global__ void k_tile_rays(CamD cam, double* cdirs, double* tdirs) {
   }
 }
 
-// classify_intersect depth only (geometry.cpp:40-48).
-// Ray-plane depth of one corner / centre ray: +inf when grazing or behind
-// (raster.cpp:99-115 nearest_depth_key).  One expression for every caller so
-// the emitted keys, the tie fix and drk_get_tile_lists agree bit for bit.
-__device__ __forceinline__ double ray_depth(const double* d, double rz0, double rz1, double rz2, double num,
-                                            double eps) {
-  const double denom = d[0] * rz0 + d[1] * rz1 + d[2] * rz2;
-  if (fabs(denom) < eps) return __longlong_as_double(0x7ff0000000000000ll);
-  const double q = num / denom;
-  return q > 0 ? q : __longlong_as_double(0x7ff0000000000000ll);
+// classify_intersect depth only (geometry.cpp:40-48) of one corner / centre
+// ray is num / den, +inf when |den| < eps or the quotient is not positive
+// (raster.cpp:99-115 nearest_depth_key).  One expression (ray_denom +
+// nearest_depth5) for every caller so the emitted keys, the tie fix and
+// drk_get_tile_lists agree bit for bit.
+__device__ __forceinline__ double ray_denom(const double* d, double rz0, double rz1, double rz2) {
+  return d[0] * rz0 + d[1] * rz1 + d[2] * rz2;
+}
+
+// NearestDepth key of the five tile rays (raster.cpp:99-115) from their
+// denominators (top, right-top, right-bottom, bottom, centre):
+// min over the rays of ray_depth.  One division instead of five: a ray is
+// valid iff |den| >= eps and den has num's sign (then num / den > 0 exactly),
+// division by a larger |den| gives a smaller exact quotient and rounding is
+// monotone, so the minimum of the rounded quotients is the rounded quotient of
+// the valid denominator of largest magnitude.  A quotient that underflows to 0
+// or overflows (the reference then drops that ray or keeps +inf) takes the
+// per-ray path.  Returns +inf when no ray is valid.
+__device__ __forceinline__ double nearest_depth5(const double den[5], double num, double eps) {
+  double best_den = 0;
+  bool any = false;
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const double d = den[r];
+    const bool valid = fabs(d) >= eps && ((num > 0 && d > 0) || (num < 0 && d < 0));
+    if (valid && (!any || fabs(d) > fabs(best_den))) {
+      best_den = d;
+      any = true;
+    }
+  }
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  if (!any) return inf;
+  const double q = num / best_den;
+  if (q > 0 && q < inf) return q;
+  double best = inf;  // per-ray path (raster.cpp:99-115 as written)
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    double qr = inf;
+    if (!(fabs(den[r]) < eps)) {
+      const double t = num / den[r];
+      if (t > 0) qr = t;
+    }
+    best = dmin(best, qr);
+  }
+  return best;
 }
 
 // Full fp64 presort key of (tile, primitive) (raster.cpp:99-115, 233-257).
@@ -1034,13 +1069,13 @@ __device__ double pair_key(const Geo& g, int pid, int tile, const CamD& cam, con
   if (opt.presort == 1) return g.projz;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x, cw = cam.tiles_x + 1;
   const int c00 = ty * cw + tx;
-  const double rz0 = g.rz[0], rz1 = g.rz[1], rz2 = g.rz[2], num = g.num, eps = opt.grazing_eps;
-  const double top = ray_depth(cdirs + 3 * (size_t)c00, rz0, rz1, rz2, num, eps);
-  const double rtop = ray_depth(cdirs + 3 * (size_t)(c00 + 1), rz0, rz1, rz2, num, eps);
-  const double rbot = ray_depth(cdirs + 3 * (size_t)(c00 + cw + 1), rz0, rz1, rz2, num, eps);
-  const double bot = ray_depth(cdirs + 3 * (size_t)(c00 + cw), rz0, rz1, rz2, num, eps);
-  const double cen = ray_depth(tdirs + 3 * (size_t)tile, rz0, rz1, rz2, num, eps);
-  double best = dmin(dmin(dmin(top, rtop), dmin(rbot, bot)), cen);
+  const double rz0 = g.rz[0], rz1 = g.rz[1], rz2 = g.rz[2];
+  const double den[5] = {ray_denom(cdirs + 3 * (size_t)c00, rz0, rz1, rz2),
+                         ray_denom(cdirs + 3 * (size_t)(c00 + 1), rz0, rz1, rz2),
+                         ray_denom(cdirs + 3 * (size_t)(c00 + cw + 1), rz0, rz1, rz2),
+                         ray_denom(cdirs + 3 * (size_t)(c00 + cw), rz0, rz1, rz2),
+                         ray_denom(tdirs + 3 * (size_t)tile, rz0, rz1, rz2)};
+  double best = nearest_depth5(den, g.num, opt.grazing_eps);
   if (isinf(best) && g.has_proj) best = g.projz;
   return best;
 }
@@ -1082,7 +1117,7 @@ __global__ void __launch_bounds__(256) k_emit_rows(long long n_rows, const int4*
   const long long pos0 = r < n_rows ? rowpairoff[r] : 0;
   const int cw = cam.tiles_x + 1;
   const double rz0 = g.rz[0], rz1 = g.rz[1], rz2 = g.rz[2], num = g.num, eps = opt.grazing_eps;
-  auto depth = [&](const double* d) -> double { return ray_depth(d, rz0, rz1, rz2, num, eps); };
+  auto dnm = [&](const double* d) -> double { return ray_denom(d, rz0, rz1, rz2); };
   unsigned kmin = 0xffffffffu, kmax = 0u;
   for (int base = rr.z; base <= rr.w; base += kEmitLanes) {
     const int tx = base + l;
@@ -1095,14 +1130,17 @@ __global__ void __launch_bounds__(256) k_emit_rows(long long n_rows, const int4*
       key = g.projz;
     } else {
       const int c00 = ty * cw + txc;
-      const double top = depth(cdirs + 3 * (size_t)c00), bot = depth(cdirs + 3 * (size_t)(c00 + cw));
-      const double cen = depth(tdirs + 3 * (size_t)(ty * cam.tiles_x + txc));
-      double rtop = __shfl_down_sync(seg, top, 1, kEmitLanes), rbot = __shfl_down_sync(seg, bot, 1, kEmitLanes);
+      double den[5];
+      den[0] = dnm(cdirs + 3 * (size_t)c00);
+      den[3] = dnm(cdirs + 3 * (size_t)(c00 + cw));
+      den[4] = dnm(tdirs + 3 * (size_t)(ty * cam.tiles_x + txc));
+      den[1] = __shfl_down_sync(seg, den[0], 1, kEmitLanes);
+      den[2] = __shfl_down_sync(seg, den[3], 1, kEmitLanes);
       if (l == kEmitLanes - 1 || tx >= rr.w) {
-        rtop = depth(cdirs + 3 * (size_t)(c00 + 1));
-        rbot = depth(cdirs + 3 * (size_t)(c00 + cw + 1));
+        den[1] = dnm(cdirs + 3 * (size_t)(c00 + 1));
+        den[2] = dnm(cdirs + 3 * (size_t)(c00 + cw + 1));
       }
-      double best = dmin(dmin(dmin(top, rtop), dmin(rbot, bot)), cen);
+      double best = nearest_depth5(den, num, eps);
       if (isinf(best) && g.has_proj) best = g.projz;
       key = best;
     }
