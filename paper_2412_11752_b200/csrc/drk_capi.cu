@@ -952,16 +952,6 @@ int drk_forward_prims(drk_ctx* c, const drk_prims* prims, int n, int k, int sh_t
   return run_forward(c, cam, opt, color, depth, normal, alpha);
 }
 
-static bool is_pinned(const void* p) {
-  if (!p) return true;
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
-}
-
 // Device address of a page-locked host buffer (mapped under unified
 // addressing), or null: the kernels then write the framebuffer straight into
 // host memory (zero-copy) as tiles finish.
