@@ -170,6 +170,8 @@ static RasterParams raster_params(drk_ctx* c) {
   P.counters = static_cast<unsigned long long*>(c->counters.p);
   // pixels flagged for the fp64 re-render (list written by the fp32 pass)
   P.redo_list = static_cast<int*>(c->redo.p);
+  P.redo_tmp = c->redo.p && c->redo_half > 0 ? P.redo_list + c->redo_half : nullptr;
+  P.redo_hist = P.redo_tmp ? reinterpret_cast<unsigned*>(P.redo_tmp + c->redo_half) : nullptr;
   P.redo_count = reinterpret_cast<unsigned int*>(ensure<unsigned long long>(c->redo_cnt, 1));
   P.shrec = A.rec;
   P.frame32 = static_cast<const float4*>(c->frame32.p);
@@ -477,7 +479,8 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   unsigned char* pxflag = ensure<unsigned char>(c->pxflag, (size_t)n_pix);
   int* pxstop = ensure<int>(c->pxstop, (size_t)n_pix);
   int* pxcomp = ensure<int>(c->pxcomp, (size_t)n_pix);
-  int* redo = ensure<int>(c->redo, (size_t)n_pix + 1);
+  int* redo = ensure<int>(c->redo, 2 * ((size_t)n_pix + 1) + 128);  // list + ordering scratch + counters
+  c->redo_half = n_pix + 1;
   if (!pxstate || !pxflag || !redo || !pxstop || !pxcomp) return set_error(c, DRK_ERR_OOM, "pixel state");
   if (opt->record_replay > 0) {
     ensure<int>(c->replay_cnt, n_pix);

@@ -101,6 +101,8 @@ struct RasterParams {
   unsigned long long* counters;
   unsigned char* pxflag;  // 1 = pixel needs the fp64 re-render (uncertain termination)
   int* redo_list;         // flagged pixel indices (forward fp32 pass appends)
+  int* redo_tmp;          // scratch of the same size (order_redo_list), or null
+  unsigned* redo_hist;    // 128 counters of order_redo_list
   unsigned int* redo_count;
   const float4* frame32;  // per prim: (R_x, a_x), (R_y, a_y), (R_z, a_z) with a = o - mu, fp32 (backward)
   int tile_base;          // first tile of this launch (banded frames: tile rows processed band by band)
@@ -202,6 +204,7 @@ struct drk_ctx {
   long long band_pair_limit = 0;  // test hook: force bands above this many pairs (0 = memory-based)
   size_t device_bytes = 0;        // cudaMemGetInfo total, queried once
   int64_t pts_cap = 0;
+  long long redo_half = 0;  // offset of the redo list's ordering scratch (pixels of the last forward + 1)
 
   // stage timing
   bool timing = false;

@@ -1715,6 +1715,61 @@ __global__ void __launch_bounds__(128) k_raster_exact(RasterParams P) {
   if (!BWD) px.finish_forward(P);
 }
 
+// Flagged pixels in decreasing order of their composite count (pxcomp, in
+// quarter-octave buckets): the fp64 pass fetches pixels dynamically, so the
+// longest walks start first and the short ones fill in behind them instead of
+// a few long walks trailing the grid.
+__device__ __forceinline__ int redo_bucket(int ncomp) {
+  return 63 - min(63, (int)(4.f * __log2f((float)max(ncomp, 0) + 1.f)));
+}
+
+__global__ void k_redo_hist(const int* __restrict__ list, const unsigned* count, const int* __restrict__ pxcomp,
+                            unsigned* hist) {
+  __shared__ unsigned sh[64];
+  if (threadIdx.x < 64) sh[threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned n = *count;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    atomicAdd(&sh[redo_bucket(pxcomp[list[t]])], 1u);
+  __syncthreads();
+  if (threadIdx.x < 64 && sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
+}
+
+__global__ void k_redo_scatter(const int* __restrict__ list, const unsigned* count, const int* __restrict__ pxcomp,
+                               const unsigned* hist, unsigned* cursor, int* out) {
+  __shared__ unsigned start[64];
+  if (threadIdx.x == 0) {
+    unsigned a = 0;
+    for (int b = 0; b < 64; ++b) {
+      start[b] = a;
+      a += hist[b];
+    }
+  }
+  __syncthreads();
+  const unsigned n = *count;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int p = list[t];
+    const int b = redo_bucket(pxcomp[p]);
+    out[start[b] + atomicAdd(&cursor[b], 1u)] = p;
+  }
+}
+
+__global__ void k_redo_copy(const int* __restrict__ src, const unsigned* count, int* dst) {
+  const unsigned n = *count;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) dst[t] = src[t];
+}
+
+static void order_redo_list(const RasterParams& P, cudaStream_t s) {
+  static const bool on = !getenv("DRK_REDO_ORDER") || atoi(getenv("DRK_REDO_ORDER")) != 0;
+  if (!on || !P.redo_tmp || !P.redo_hist || !P.pxcomp) return;
+  cudaMemsetAsync(P.redo_hist, 0, 128 * sizeof(unsigned), s);
+  k_redo_hist<<<148 * 2, 256, 0, s>>>(P.redo_list, P.redo_count, P.pxcomp, P.redo_hist);
+  k_redo_scatter<<<148 * 2, 256, 0, s>>>(P.redo_list, P.redo_count, P.pxcomp, P.redo_hist, P.redo_hist + 64,
+                                         P.redo_tmp);
+  k_redo_copy<<<148 * 2, 256, 0, s>>>(P.redo_tmp, P.redo_count, P.redo_list);
+  launch_counter() += 3;
+}
+
 __global__ void k_fill_pixels(int* list, unsigned* count, unsigned n) {
   const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) list[i] = (int)i;
@@ -1761,6 +1816,7 @@ void launch_raster(const RasterParams& P, int n_tiles, bool bwd, cudaStream_t s,
     else if (P.opt.raster_kernel != 1 && raster_fast_eligible(P)) launch_raster_fast(P, n_tiles, P.vstat != nullptr, s);
     else k_raster<0, false, false><<<n_tiles, 256, 0, s>>>(P);
     if (mid) cudaEventRecord(mid, s);
+    order_redo_list(P, s);
     if (bwd) k_raster_pixels_warp<0, true><<<redo_blocks, 128, 0, s>>>(P);
     else k_raster_pixels_warp<0, false><<<redo_blocks, 128, 0, s>>>(P);
   } else {
