@@ -54,6 +54,7 @@ __global__ void k_full_keys_off(long long n, const long long* tileoff, int n_til
 template <typename T>
 int exclusive_scan(drk_ctx* c, const T* in, long long n, long long* out, long long* total);
 int sort_pairs(drk_ctx* c, unsigned* k, unsigned* v, unsigned* k2, unsigned* v2, long long n);
+void launch_tile_cost_keys(int n, const unsigned* cost, unsigned* key, unsigned* id, cudaStream_t s);
 void launch_tile_order_keys(int n, int tiles_x, int band_rows, const long long* tileoff, int tile_base, unsigned* key,
                             unsigned* id, cudaStream_t s);
 void launch_act_bwd(int n, int K, int terms, const float* raw, const double* gact, int G,
@@ -500,6 +501,11 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     c->band_ids.resize(nb);
     c->band_off.resize(nb);
   }
+  // per-tile streamed lengths of the fast forward (the backward's dispatch order)
+  unsigned* tcost = ensure<unsigned>(c->tile_cost, (size_t)n_tiles + 1);
+  if (!tcost) return set_error(c, DRK_ERR_OOM, "tile costs");
+  cudaMemsetAsync(tcost, 0, sizeof(unsigned) * n_tiles, s);
+  c->tile_cost_valid = false;
   for (int b = 0; b < nb; ++b) {
     const int ty_lo = c->bands[b], ty_hi = c->bands[b + 1];
     mark(c, 2);
@@ -546,6 +552,8 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
       P.replay_rec = static_cast<double*>(c->replay_rec.p);
     }
     P.tile_base = ty_lo * cd.tiles_x;
+    P.tile_cost = tcost;
+    c->tile_cost_valid = nb == 1 && raster_fast_eligible(P) && P.opt.raster_kernel != 1;
     P.fast_nt = choose_nt(c, n_pairs, (ty_hi - ty_lo) * cd.tiles_x);
     // Longest tile lists first (a shorter tail: config 1 -1.9%, config 2 -4% raster
     // time).  DRK_TILE_ORDER=0 forces row-major.
@@ -665,7 +673,11 @@ int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* 
       unsigned* tk = ensure<unsigned>(c->tord, 4 * (size_t)n_tiles + 4);
       if (!tk) return set_error(c, DRK_ERR_OOM, "tile order");
       unsigned *tv = tk + n_tiles + 1, *tk2 = tv + n_tiles + 1, *tv2 = tk2 + n_tiles + 1;
-      launch_tile_order_keys(n_tiles, c->camd.tiles_x, 0, P.tileoff, 0, tk, tv, s);
+      static const bool by_cost = !getenv("DRK_BWD_ORDER") || atoi(getenv("DRK_BWD_ORDER")) != 0;
+      if (by_cost && c->tile_cost_valid && c->tile_cost.p)
+        launch_tile_cost_keys(n_tiles, static_cast<const unsigned*>(c->tile_cost.p), tk, tv, s);
+      else
+        launch_tile_order_keys(n_tiles, c->camd.tiles_x, 0, P.tileoff, 0, tk, tv, s);
       launch_counter() += 1;
       if (int st = sort_pairs(c, tk, tv, tk2, tv2, n_tiles)) return st;
       P.tile_order = reinterpret_cast<const int*>(tv);
@@ -865,7 +877,7 @@ void drk_ctx_destroy(drk_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
                     &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
-                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->geo, &c->frame32, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
+                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->tile_cost, &c->geo, &c->frame32, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->sk,
                     &c->hist, &c->sortoff, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,

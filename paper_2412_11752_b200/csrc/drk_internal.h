@@ -103,6 +103,7 @@ struct RasterParams {
   int* redo_list;         // flagged pixel indices (forward fp32 pass appends)
   int* redo_tmp;          // scratch of the same size (order_redo_list), or null
   unsigned* redo_hist;    // 128 counters of order_redo_list
+  unsigned* tile_cost;    // fast forward: list entries each tile streamed before its pixels saturated (backward tile order), or null
   unsigned int* redo_count;
   const float4* frame32;  // per prim: (R_x, a_x), (R_y, a_y), (R_z, a_z) with a = o - mu, fp32 (backward)
   int tile_base;          // first tile of this launch (banded frames: tile rows processed band by band)
@@ -204,6 +205,8 @@ struct drk_ctx {
   long long band_pair_limit = 0;  // test hook: force bands above this many pairs (0 = memory-based)
   size_t device_bytes = 0;        // cudaMemGetInfo total, queried once
   int64_t pts_cap = 0;
+  drk::DevBuf tile_cost;       // per tile: entries the fast forward streamed (the backward's dispatch order)
+  bool tile_cost_valid = false;
   long long redo_half = 0;  // offset of the redo list's ordering scratch (pixels of the last forward + 1)
 
   // stage timing

@@ -364,8 +364,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   __syncthreads();
   if (beg < end) prefetch(beg);
 #endif
+  long long streamed = 0;
   for (long long b0 = beg; b0 < end; b0 += NT) {
     const int jb = (int)(b0 - beg);
+    streamed = min(end, b0 + NT) - beg;
     __syncthreads();
 #if DRK_TMA_STAGE
     mbar_wait(&s_bar, gpar);
@@ -433,6 +435,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
 #if DRK_TMA_STAGE
   if (pending) mbar_wait(&s_bar, gpar);  // no bulk copy may land after the CTA exits
 #endif
+  if (P.tile_cost && threadIdx.x == 0) atomicMax(P.tile_cost + tile, (unsigned)streamed);
   // end marker: drain the cache head first (raster.cpp:410-414)
   while (!done && csz > 0) {
     const int pj = cj[0];
@@ -516,6 +519,19 @@ __global__ void k_tile_order_keys(int n, int tiles_x, int band_rows, const long 
   const unsigned band = band_rows > 0 ? (unsigned)((tile_base + t) / tiles_x / band_rows) : 0u;
   key[t] = (band << 20) | (0xfffffu - (unsigned)min(len, 0xfffffLL));
   id[t] = (unsigned)t;
+}
+
+// Backward dispatch order: the tiles that streamed the most list entries in
+// the forward (their CTAs run longest) first.
+__global__ void k_tile_cost_keys(int n, const unsigned* __restrict__ cost, unsigned* key, unsigned* id) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  key[t] = ~cost[t];
+  id[t] = (unsigned)t;
+}
+
+void launch_tile_cost_keys(int n, const unsigned* cost, unsigned* key, unsigned* id, cudaStream_t s) {
+  if (n > 0) k_tile_cost_keys<<<(n + 255) / 256, 256, 0, s>>>(n, cost, key, id);
 }
 
 void launch_tile_order_keys(int n, int tiles_x, int band_rows, const long long* tileoff, int tile_base, unsigned* key,
