@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "drk/errors.hpp"
@@ -95,17 +96,46 @@ void* slot_bytes(int slot, size_t bytes) {
 enum Slots { kMu, kRot, kS, kTh, kEta, kTau, kO, kSh, kColor, kDepth, kNormal, kAlpha, kRaw, kDC, kDD, kDN, kDA,
              kG, kDcw, kSg, kTch, kLossA, kLossB, kLossOut, kLossD, kSh64 };
 
+// Grow-only page-locked host staging, one slot per role: the conversions write
+// into memory that is already mapped (no first-touch page faults per call) and
+// the copies run at full link speed.
+enum HostSlots { kHMu, kHRot, kHS, kHTh, kHEta, kHTau, kHO, kHSh, kHSh64, kHRaw, kHG, kHDcw, kHSg, kHTch, kHostSlots };
+template <class T>
+T* pinned(int slot, size_t count) {
+  struct Slot {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  static Slot slots[kHostSlots];
+  Slot& s = slots[slot];
+  const size_t bytes = sizeof(T) * (count ? count : 1);
+  if (s.bytes < bytes) {
+    if (s.p) cudaFreeHost(s.p);
+    s.p = nullptr;
+    const size_t want = bytes + bytes / 4;
+    if (cudaHostAlloc(&s.p, want, cudaHostAllocDefault) != cudaSuccess) throw drk::Error("drk_b200: cudaHostAlloc");
+    s.bytes = want;
+  }
+  return static_cast<T*>(s.p);
+}
+
 template <class T>
 struct Dev {
   T* p = nullptr;
   size_t n = 0;
   Dev(int slot, size_t count) : p(static_cast<T*>(slot_bytes(slot, sizeof(T) * (count ? count : 1)))), n(count) {}
-  Dev(int slot, const std::vector<T>& h) : Dev(slot, h.size()) {
-    if (!h.empty()) cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice);
+  Dev(int slot, const T* h, size_t count) : Dev(slot, count) {
+    if (count) cudaMemcpy(p, h, sizeof(T) * count, cudaMemcpyHostToDevice);
   }
+  Dev(int slot, const std::vector<T>& h) : Dev(slot, h.data(), h.size()) {}
   std::vector<T> get() const {
     std::vector<T> h(n);
     if (n) cudaMemcpy(h.data(), p, sizeof(T) * n, cudaMemcpyDeviceToHost);
+    return h;
+  }
+  const T* get_pinned(int host_slot) const {  // into page-locked staging
+    T* h = pinned<T>(host_slot, n);
+    if (n) cudaMemcpy(h, p, sizeof(T) * n, cudaMemcpyDeviceToHost);
     return h;
   }
 };
@@ -139,84 +169,110 @@ struct Fnv {
 };
 uint64_t g_last_forward = 0;  // fingerprint of the context's last forward (0: none)
 
-// Activated primitives on the device (drk_prims).
+// Host loops over the primitives / pixels on all cores (the reference API hands
+// over host std::vectors; their conversion would otherwise dominate a call).
+template <class F>
+void parallel_for(size_t n, F f, size_t serial_below = 8192) {
+  static const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const unsigned T = n < serial_below ? 1u : (unsigned)std::min<size_t>(hw, n);
+  if (T == 1) {
+    f(size_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(T);
+  const size_t chunk = (n + T - 1) / T;
+  for (unsigned t = 0; t < T; ++t) {
+    const size_t b = t * chunk, e = std::min(n, b + chunk);
+    if (b < e) th.emplace_back([=, &f] { f(b, e); });
+  }
+  for (auto& x : th) x.join();
+}
+
+// Activated primitives on the device (drk_prims).  One parallel pass fills the
+// SoA fields and fingerprints them in blocks of kHashBlock primitives (the block
+// hashes combined in order: independent of the thread count).
 struct DevPrims {
+  static constexpr size_t kHashBlock = 4096;
   int n, k, terms;
-  static std::vector<double> field(const std::vector<drk::DrkPrimitive>& P, int per, int which) {
-    std::vector<double> v;
-    v.reserve(P.size() * per);
-    for (const auto& p : P) {
-      switch (which) {
-        case 0: for (int a = 0; a < 3; ++a) v.push_back(p.center[a]); break;
-        case 1: for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) v.push_back(p.rot(r, c)); break;
-        case 2: for (int j = 0; j < per; ++j) v.push_back(p.scales[j]); break;
-        case 3: for (int j = 0; j < per; ++j) v.push_back(p.angles[j]); break;
-        case 4: v.push_back(p.eta); break;
-        case 5: v.push_back(p.tau); break;
-        default: v.push_back(p.opacity); break;
-      }
-    }
-    return v;
-  }
-  static std::vector<double> shd(const std::vector<drk::DrkPrimitive>& P, int terms) {
-    std::vector<double> v;
-    v.reserve(P.size() * terms * 3);
-    for (const auto& p : P)
-      for (int t = 0; t < terms; ++t)
-        for (int c = 0; c < 3; ++c) v.push_back(t < p.sh.rows() ? p.sh(t, c) : 0.0);
-    return v;
-  }
-  static std::vector<float> shf(const std::vector<drk::DrkPrimitive>& P, int terms) {
-    std::vector<float> v;
-    v.reserve(P.size() * terms * 3);
-    for (const auto& p : P)
-      for (int t = 0; t < terms; ++t)
-        for (int c = 0; c < 3; ++c) v.push_back(t < p.sh.rows() ? (float)p.sh(t, c) : 0.f);
-    return v;
-  }
   DevPrims(const std::vector<drk::DrkPrimitive>& P, int k_default)
-      : n((int)P.size()),
-        k(P.empty() ? k_default : P[0].basis_count()),
-        terms([&] {
-          int t = 0;
-          for (const auto& p : P) t = std::max<int>(t, (int)p.sh.rows());
-          return t;
-        }()),
-        hmu(field(P, 3, 0)),
-        hrot(field(P, 9, 1)),
-        hs(field(P, k, 2)),
-        hth(field(P, k, 3)),
-        heta(field(P, 1, 4)),
-        htau(field(P, 1, 5)),
-        ho(field(P, 1, 6)),
-        hsh(shf(P, terms)),
-        hsh64(shd(P, terms)) {
-    for (const auto& p : P)
+      : n((int)P.size()), k(P.empty() ? k_default : P[0].basis_count()), terms(0) {
+    for (const auto& p : P) {
+      terms = std::max<int>(terms, (int)p.sh.rows());
       if (p.basis_count() != k) throw drk::DimensionMismatchError("drk_b200 adapter: mixed basis counts");
+    }
+    const size_t N = P.size(), T3 = 3 * (size_t)terms;
+    nmu = 3 * N;
+    nrot = 9 * N;
+    nk = (size_t)k * N;
+    nsh = T3 * N;
+    hmu = pinned<double>(kHMu, nmu);
+    hrot = pinned<double>(kHRot, nrot);
+    hs = pinned<double>(kHS, nk);
+    hth = pinned<double>(kHTh, nk);
+    heta = pinned<double>(kHEta, N);
+    htau = pinned<double>(kHTau, N);
+    ho = pinned<double>(kHO, N);
+    hsh = pinned<float>(kHSh, nsh);
+    hsh64 = pinned<double>(kHSh64, nsh);
+    const size_t nblk = (N + kHashBlock - 1) / kHashBlock;
+    std::vector<uint64_t> bh(nblk);
+    parallel_for(nblk, [&](size_t b0, size_t b1) {
+      for (size_t blk = b0; blk < b1; ++blk) {
+        const size_t i0 = blk * kHashBlock, i1 = std::min(N, i0 + kHashBlock);
+        for (size_t i = i0; i < i1; ++i) {
+          const auto& p = P[i];
+          for (int a = 0; a < 3; ++a) hmu[3 * i + a] = p.center[a];
+          for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) hrot[9 * i + 3 * r + c] = p.rot(r, c);
+          for (int j = 0; j < k; ++j) {
+            hs[(size_t)k * i + j] = p.scales[j];
+            hth[(size_t)k * i + j] = p.angles[j];
+          }
+          heta[i] = p.eta;
+          htau[i] = p.tau;
+          ho[i] = p.opacity;
+          for (int t = 0; t < terms; ++t)
+            for (int c = 0; c < 3; ++c) {
+              const double v = t < p.sh.rows() ? p.sh(t, c) : 0.0;
+              hsh64[T3 * i + 3 * t + c] = v;
+              hsh[T3 * i + 3 * t + c] = (float)v;
+            }
+        }
+        Fnv f;
+        const size_t m = i1 - i0;
+        f.add(hmu + 3 * i0, 8 * 3 * m);
+        f.add(hrot + 9 * i0, 8 * 9 * m);
+        f.add(hs + (size_t)k * i0, 8 * (size_t)k * m);
+        f.add(hth + (size_t)k * i0, 8 * (size_t)k * m);
+        f.add(heta + i0, 8 * m);
+        f.add(htau + i0, 8 * m);
+        f.add(ho + i0, 8 * m);
+        f.add(hsh64 + T3 * i0, 8 * T3 * m);
+        bh[blk] = f.h;
+      }
+    }, 2);
     Fnv f;
     f.add(&n, sizeof n);
     f.add(&k, sizeof k);
     f.add(&terms, sizeof terms);
-    f.vec(hmu);
-    f.vec(hrot);
-    f.vec(hs);
-    f.vec(hth);
-    f.vec(heta);
-    f.vec(htau);
-    f.vec(ho);
-    f.vec(hsh64);
+    f.vec(bh);
     hash = f.h;
   }
   // device copies (only when a forward must run)
   void upload() {
-    Dev<double> mu(kMu, hmu), rot(kRot, hrot), s(kS, hs), th(kTh, hth), eta(kEta, heta), tau(kTau, htau), o(kO, ho);
-    Dev<float> sh(kSh, hsh);
-    Dev<double> sh64(kSh64, hsh64);  // the fp64 pixel path's colours use the reference's coefficients exactly
+    const size_t N = (size_t)n;
+    Dev<double> mu(kMu, hmu, nmu), rot(kRot, hrot, nrot), s(kS, hs, nk), th(kTh, hth, nk), eta(kEta, heta, N),
+        tau(kTau, htau, N), o(kO, ho, N);
+    Dev<float> sh(kSh, hsh, nsh);
+    Dev<double> sh64(kSh64, hsh64, nsh);  // the fp64 pixel path's colours use the reference's coefficients exactly
     view = drk_prims{mu.p, rot.p, s.p, th.p, eta.p, tau.p, o.p, sh.p, sh64.p};
   }
-  std::vector<double> hmu, hrot, hs, hth, heta, htau, ho;
-  std::vector<float> hsh;
-  std::vector<double> hsh64;
+  // page-locked host copies (adapter staging slots: valid until the next conversion)
+  double *hmu, *hrot, *hs, *hth, *heta, *htau, *ho;
+  float* hsh;
+  double* hsh64;
+  size_t nmu, nrot, nk, nsh;
   drk_prims view{};
   uint64_t hash = 0;
 };
@@ -240,15 +296,26 @@ drk_camera to_cam(const drk::Camera& c) {
 struct Trace {
   const char* what;
   int w, h, n;
-  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  std::string phases;
+  Trace(const char* what_, int w_, int h_, int n_) : what(what_), w(w_), h(h_), n(n_) {}
   static bool on() {
     static const bool e = std::getenv("DRK_ADAPTER_TRACE") != nullptr;
     return e;
   }
+  void at(const char* phase) {  // checkpoint: time since the previous one
+    if (!on()) return;
+    const auto now = std::chrono::steady_clock::now();
+    char b[64];
+    std::snprintf(b, sizeof b, " %s %.2f", phase, std::chrono::duration<double, std::milli>(now - last).count());
+    phases += b;
+    last = now;
+  }
   ~Trace() {
     if (on())
-      std::fprintf(stderr, "[drk adapter] %s %dx%d n=%d: %.3f ms\n", what, w, h, n,
-                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      std::fprintf(stderr, "[drk adapter] %s %dx%d n=%d: %.3f ms |%s\n", what, w, h, n,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+                   phases.c_str());
   }
 };
 
@@ -349,17 +416,21 @@ FrameBuffers render(const std::vector<DrkPrimitive>& prims, const Camera& cam, c
                     ReplayBuffer* replay) {
   Trace tr{replay ? "render(replay)" : "render", cam.width, cam.height, (int)prims.size()};
   DevPrims dp(prims, opt.kernel.basis_count);
+  tr.at("convert+hash");
   const size_t npx = (size_t)cam.width * cam.height;
   Dev<float> color(kColor, 3 * npx), depth(kDepth, npx), normal(kNormal, 3 * npx), alpha(kAlpha, npx);
   forward(prims, cam, opt, replay ? 1024 : 0, color.p, depth.p, normal.p, alpha.p, dp);
+  tr.at("upload+forward");
   FrameBuffers fb;
   fb.color = Image(cam.width, cam.height, 3);
   fb.depth = Image(cam.width, cam.height, 1);
   fb.normal = Image(cam.width, cam.height, 3);
   fb.alpha = Image(cam.width, cam.height, 1);
+  tr.at("images");
   // the rasterizer's fp64 accumulators (the f32 planes above are their rounding)
   check(drk_get_framebuffers_f64(ctx(), fb.color.data.data(), fb.depth.data.data(), fb.normal.data.data(),
                                  fb.alpha.data.data()));
+  tr.at("framebuffers_f64");
   fb.background = opt.background;
   if (replay) {
     replay->width = cam.width;
@@ -394,22 +465,28 @@ ParamGrads backward_render(const std::vector<RawDrkParams>& raws, const std::vec
     throw ReplayMismatchError("replay buffer does not match the camera dimensions");
   if (raws.size() != prims.size()) throw ReplayMismatchError("raw and activated primitive counts differ");
   DevPrims dp(prims, opt.kernel.basis_count);
+  tr.at("convert+hash");
   // the device keeps the decisions of the forward in place of the ReplayBuffer:
   // the last forward's when it rendered these primitives with this camera and
   // these options (render(&replay) -> backward_render), else a fresh one
   if (g_last_forward != forward_hash(dp, to_cam(cam), to_opt(opt, 0)))
     forward(prims, cam, opt, 0, nullptr, nullptr, nullptr, nullptr, dp);
+  tr.at("reforward?");
   const int n = dp.n, k = dp.k, terms = dp.terms;
   const int S = drk_scalar_count(k, terms);
-  std::vector<float> raw_soa((size_t)S * n, 0.f);
-  for (int i = 0; i < n; ++i) {
-    int s = 0;
-    for_each_scalar(raws[i], [&](const double& x, ParamClass) {
-      if (s < S) raw_soa[(size_t)s * n + i] = (float)x;
-      ++s;
-    });
-  }
-  Dev<float> raw_d(kRaw, raw_soa);
+  float* raw_soa = pinned<float>(kHRaw, (size_t)S * n);
+  parallel_for((size_t)n, [&](size_t i0, size_t i1) {
+    for (int q = 0; q < S; ++q) std::memset(raw_soa + (size_t)q * n + i0, 0, sizeof(float) * (i1 - i0));
+    for (size_t i = i0; i < i1; ++i) {
+      int s = 0;
+      for_each_scalar(raws[i], [&](const double& x, ParamClass) {
+        if (s < S) raw_soa[(size_t)s * n + i] = (float)x;
+        ++s;
+      });
+    }
+  });
+  tr.at("raw_soa");
+  Dev<float> raw_d(kRaw, raw_soa, (size_t)S * n);
   auto img = [&](const Image& im, int ch) -> std::vector<float> {
     if (im.empty()) return {};
     if (im.width != cam.width || im.height != cam.height || im.channels != ch)
@@ -423,26 +500,32 @@ ParamGrads backward_render(const std::vector<RawDrkParams>& raws, const std::vec
                     ha.empty() ? nullptr : da.p};
   Dev<float> g(kG, (size_t)S * n), dcw(kDcw, 3 * (size_t)n), sg(kSg, n);
   Dev<uint8_t> tch(kTch, n);
+  tr.at("uploads");
   check(drk_backward(ctx(), raw_d.p, &fg, g.p, dcw.p, sg.p, tch.p, 0, /*deterministic=*/1));
-  const std::vector<float> gh = g.get(), dcwh = dcw.get(), sgh = sg.get();
-  const std::vector<uint8_t> th = tch.get();
+  tr.at("backward");
+  const float *gh = g.get_pinned(kHG), *dcwh = dcw.get_pinned(kHDcw), *sgh = sg.get_pinned(kHSg);
+  const uint8_t* th = tch.get_pinned(kHTch);
+  tr.at("downloads");
   ParamGrads out;
   out.raw.resize(n);
   out.d_center_world.resize(n);
   out.screen_grad.assign(n, 0.0);
   out.touched.assign(n, 0);
-  for (int i = 0; i < n; ++i) {
-    RawDrkParams r = RawDrkParams::zeros_like(raws[i]);
-    int s = 0;
-    for_each_scalar(r, [&](double& x, ParamClass) {
-      if (s < S) x = gh[(size_t)s * n + i];
-      ++s;
-    });
-    out.raw[i] = r;
-    out.d_center_world[i] = Vec3(dcwh[3 * i], dcwh[3 * i + 1], dcwh[3 * i + 2]);
-    out.screen_grad[i] = sgh[i];
-    out.touched[i] = (char)th[i];
-  }
+  parallel_for((size_t)n, [&](size_t i0, size_t i1) {
+    for (size_t i = i0; i < i1; ++i) {
+      RawDrkParams r = RawDrkParams::zeros_like(raws[i]);
+      int s = 0;
+      for_each_scalar(r, [&](double& x, ParamClass) {
+        if (s < S) x = gh[(size_t)s * n + i];
+        ++s;
+      });
+      out.raw[i] = std::move(r);
+      out.d_center_world[i] = Vec3(dcwh[3 * i], dcwh[3 * i + 1], dcwh[3 * i + 2]);
+      out.screen_grad[i] = sgh[i];
+      out.touched[i] = (char)th[i];
+    }
+  });
+  tr.at("param_grads");
   return out;
 }
 
@@ -473,6 +556,7 @@ double ssim(const Image& a, const Image& b) {
 }
 
 LossResult loss(const Image& rendered, const Image& target, double dssim_weight) {
+  Trace tr{"loss", rendered.width, rendered.height, 0};
   same_shape(rendered, target);
   Dev<double> dr(kLossA, rendered.data), dt(kLossB, target.data), out(kLossOut, 3), dcol(kLossD, rendered.data.size());
   done(drk_loss_f64(ctx(), dr.p, dt.p, rendered.width, rendered.height, rendered.channels, dssim_weight, out.p,

@@ -877,7 +877,7 @@ void drk_ctx_destroy(drk_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
                     &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
-                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->tile_cost, &c->geo, &c->frame32, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
+                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->tile_cost, &c->planes64, &c->geo, &c->frame32, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->sk,
                     &c->hist, &c->sortoff, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,
@@ -1171,23 +1171,36 @@ int drk_get_tile_lists(drk_ctx* c, int64_t* total, int64_t* offsets, int32_t* id
   return DRK_OK;
 }
 
+// pixel state (8 doubles per pixel) -> colour, depth, normal, alpha planes
+__global__ void k_split_state(long long npix, const double* __restrict__ st, double* color, double* depth,
+                              double* normal, double* alpha) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= npix) return;
+  const double* q = st + 8 * p;
+  for (int k = 0; k < 3; ++k) {
+    color[3 * p + k] = q[k];
+    normal[3 * p + k] = q[4 + k];
+  }
+  depth[p] = q[3];
+  alpha[p] = q[7];
+}
+
 int drk_get_framebuffers_f64(drk_ctx* c, double* color, double* depth, double* normal, double* alpha) {
   if (!c || !c->has_fwd) return c ? set_error(c, DRK_ERR_INVALID_ARG, "no forward on this context") : DRK_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
   const size_t npix = (size_t)c->cam.width * c->cam.height;
-  std::vector<double> st(8 * npix);
-  cudaMemcpyAsync(st.data(), c->pxstate.p, sizeof(double) * st.size(), cudaMemcpyDeviceToHost, c->stream);
-  if (int s = cuda_check(c, cudaStreamSynchronize(c->stream), "framebuffers")) return s;
-  for (size_t p = 0; p < npix; ++p) {
-    const double* q = st.data() + 8 * p;
-    if (color)
-      for (int k = 0; k < 3; ++k) color[3 * p + k] = q[k];
-    if (depth) depth[p] = q[3];
-    if (normal)
-      for (int k = 0; k < 3; ++k) normal[3 * p + k] = q[4 + k];
-    if (alpha) alpha[p] = q[7];
-  }
-  return DRK_OK;
+  if (npix == 0) return DRK_OK;
+  double* d = ensure<double>(c->planes64, 8 * npix);
+  if (!d) return set_error(c, DRK_ERR_OOM, "framebuffer planes");
+  k_split_state<<<(unsigned)((npix + 255) / 256), 256, 0, c->stream>>>((long long)npix,
+                                                                       static_cast<const double*>(c->pxstate.p), d,
+                                                                       d + 3 * npix, d + 4 * npix, d + 7 * npix);
+  DRK_COUNT_LAUNCH();
+  if (color) cudaMemcpyAsync(color, d, sizeof(double) * 3 * npix, cudaMemcpyDeviceToHost, c->stream);
+  if (depth) cudaMemcpyAsync(depth, d + 3 * npix, sizeof(double) * npix, cudaMemcpyDeviceToHost, c->stream);
+  if (normal) cudaMemcpyAsync(normal, d + 4 * npix, sizeof(double) * 3 * npix, cudaMemcpyDeviceToHost, c->stream);
+  if (alpha) cudaMemcpyAsync(alpha, d + 7 * npix, sizeof(double) * npix, cudaMemcpyDeviceToHost, c->stream);
+  return cuda_check(c, cudaStreamSynchronize(c->stream), "framebuffers");
 }
 
 __global__ void k_replay_compact(long long npix, int cap, const int* __restrict__ cnt, const long long* __restrict__ off,

@@ -205,6 +205,7 @@ struct drk_ctx {
   long long band_pair_limit = 0;  // test hook: force bands above this many pairs (0 = memory-based)
   size_t device_bytes = 0;        // cudaMemGetInfo total, queried once
   int64_t pts_cap = 0;
+  drk::DevBuf planes64;  // drk_get_framebuffers_f64 staging
   drk::DevBuf tile_cost;       // per tile: entries the fast forward streamed (the backward's dispatch order)
   bool tile_cost_valid = false;
   long long redo_half = 0;  // offset of the redo list's ordering scratch (pixels of the last forward + 1)
