@@ -805,7 +805,10 @@ void launch_raster_bwd_fast(const RasterParams& P, int n_tiles, cudaStream_t s) 
 void launch_raster_bwd_fast_det(const RasterParams& P, int n_tiles, cudaStream_t s) {
   if (n_tiles <= 0) return;
   launch_counter() += 1;
-  launch_bwd_nt<256, true>(P, n_tiles, s);
+  // half-tile CTAs as in the atomic backward (config 2 record raster -11%); DRK_DET_NT=256: whole tiles
+  static const int det_nt = getenv("DRK_DET_NT") ? atoi(getenv("DRK_DET_NT")) : 128;
+  if (det_nt == 128) launch_bwd_nt<128, true>(P, n_tiles, s);
+  else launch_bwd_nt<256, true>(P, n_tiles, s);
 }
 
 }  // namespace drk
