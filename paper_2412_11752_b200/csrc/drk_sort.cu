@@ -142,20 +142,31 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const unsigned* __res
   unsigned kk[kRsItems], vv[kRsItems];
   int dig[kRsItems];
   unsigned rank[kRsItems];
+  // a warp whose items are all valid needs only the 8 digit-bit ballots
+  const bool full = base + 32 * kRsItems <= n;
 #pragma unroll
   for (int r = 0; r < kRsItems; ++r) {
     const long long i = base + r * 32 + lane;
     const bool valid = i < n;
     kk[r] = valid ? kin[i] : 0;
     vv[r] = valid ? vin[i] : 0;
+  }
+#pragma unroll
+  for (int r = 0; r < kRsItems; ++r) {
+    const bool valid = base + r * 32 + lane < n;
     const int d = valid ? (int)((kk[r] >> shift) & 255u) : 256;
     dig[r] = d;
     // lanes with the same digit: intersection of per-bit ballots (bit 8 marks
     // invalid items)
     unsigned peers = 0xffffffffu;
 #pragma unroll
-    for (int b = 0; b < 9; ++b) {
+    for (int b = 0; b < 8; ++b) {
       const bool bit = (d >> b) & 1;
+      const unsigned bal = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? bal : ~bal;
+    }
+    if (!full) {
+      const bool bit = (d >> 8) & 1;
       const unsigned bal = __ballot_sync(0xffffffffu, bit);
       peers &= bit ? bal : ~bal;
     }

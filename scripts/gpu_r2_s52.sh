@@ -1,0 +1,7 @@
+#!/bin/bash
+# round 2 session 52: radix scatter — loads hoisted, 8 ballots for full warps
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out
+O=gpurun_out/r2s52
+for i in 1 2; do timeout 300 python scripts/quick_timing.py 1 3 > $O.t_$i.log 2>&1; done
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_scale.py -m gpu -q -x > $O.tests.log 2>&1
