@@ -34,6 +34,9 @@
 #endif
 // 1: warp-group sums read the members' rows / SH weights / basis from shared
 // memory (lane = gradient component); 0: register transposes with shuffles
+#ifndef DRK_BWD_THRU
+#define DRK_BWD_THRU 1  // pop-through fast path (config 2 backward -1%)
+#endif
 #ifndef DRK_BWD_SMEM
 #define DRK_BWD_SMEM 0  // measured on config 2: 47.8 ms with 1, 47.0 ms with 0 (groups average 18 lanes)
 #endif
@@ -694,7 +697,11 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
               }
             }
           }
-          if (hit) {
+          if (hit && DRK_BWD_THRU && csz == kCacheCap && hi < clo[0]) {
+            // certainly shallower than the head: pops through, cache unchanged
+            want = true;
+            pj = jr;
+          } else if (hit) {
             bool le[kCacheCap];
             bool amb = false;
 #pragma unroll
