@@ -18,7 +18,7 @@ namespace drk {
 // kernels defined in the other translation units
 __global__ void k_prep_warp(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pts_pool,
                             long long pts_cap, int2* ptsref, int* rowcnt, unsigned long long* counters, int* overflow,
-                            float4* frame32);
+                            float4* frame32, int i0, int i1);
 __global__ void k_prep_hull(int n, const int2* ptsref, double2* pts_pool, CamD cam, OptD opt, int4* bbox, int2* hullref,
                             double2* pool, long long pool_cap, int* rowcnt, unsigned long long* counters);
 size_t prep_warp_smem();
@@ -371,7 +371,7 @@ struct HostTrace {
 };
 
 int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float* color, float* depth,
-                float* normal, float* alpha) {
+                float* normal, float* alpha, const H2DPipe* pipe) {
   HostTrace ht;
   const Activated& A = c->act;
   if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0) || !(cam->fy > 0))
@@ -408,20 +408,40 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     double2* ppool = ensure<double2>(c->ptspool, (size_t)c->pts_cap);
     int* ovf = ensure<int>(ovf_buf, n + 1);
     if (!pool || !ovf || !ppool) return set_error(c, DRK_ERR_OOM, "hull pool");
-    cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT, s);
+    // the pipelined host-buffer forward zeroed the counters before its
+    // activation (whose error counts they carry) on the first attempt
+    const bool piped = pipe && attempt == 0;
+    if (!piped) cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT, s);
     if (n > 0) {
       // warp per primitive; near-clipped / oversized polygons -> overflow list (k_prep1)
       static PerDeviceOnce attr;
       const size_t smem = prep_warp_smem();
       attr([&] { cudaFuncSetAttribute(k_prep_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
-      k_prep_warp<<<(n + prep_warp_warps() - 1) / prep_warp_warps(), 32 * prep_warp_warps(), smem, s>>>(A, cd, od, geo, bbox, hullref, ppool, c->pts_cap, ptsref, rowcnt,
-                                                   ctr, ovf, static_cast<float4*>(c->frame32.p));
+      const int pw = prep_warp_warps();
+      // pipelined: activation + K1 of each chunk of primitives as soon as its
+      // parameters have crossed the link (the copies of later chunks overlap)
+      const int nchunk = piped ? pipe->nchunk : 1;
+      for (int q = 0; q < nchunk; ++q) {
+        const int i0 = piped ? pipe->bounds[q] : 0, i1 = piped ? pipe->bounds[q + 1] : n;
+        if (piped) {
+          cudaStreamWaitEvent(s, pipe->ready[q], 0);
+          activate_range(c, pipe->raw, i0, i1);
+        }
+        if (i1 > i0)
+          k_prep_warp<<<(i1 - i0 + pw - 1) / pw, 32 * pw, smem, s>>>(A, cd, od, geo, bbox, hullref, ppool, c->pts_cap,
+                                                                  ptsref, rowcnt, ctr, ovf,
+                                                                  static_cast<float4*>(c->frame32.p), i0, i1);
+      }
       k_prep_hull<<<(unsigned)((2LL * n + 255) / 256), 256, 0, s>>>(n, ptsref, ppool, cd, od, bbox, hullref, pool,
                                                                     c->hull_cap, rowcnt, ctr);
     }
     launch_counter() += 2;
     unsigned long long h[C_COUNT];
     if (int st = read_counters(c, h)) return st;
+    if (piped) {  // the activation's checks, deferred to the first read of the counters
+      if (h[C_ERR_NONFINITE]) return set_error(c, DRK_ERR_NONFINITE, "raw parameters contain NaN/Inf");
+      if (h[C_ERR_DEGEN_QUAT]) return set_error(c, DRK_ERR_DEGENERATE_QUAT, "quaternion norm below 1e-12");
+    }
     if ((long long)h[C_PTS_POOL] > c->pts_cap) {
       c->pts_cap = (long long)h[C_PTS_POOL] + (long long)h[C_PTS_POOL] / 4 + 1024;
       if (attempt == 3) return set_error(c, DRK_ERR_OOM, "point pool retries");
@@ -875,6 +895,12 @@ void drk_ctx_destroy(drk_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  if (c->h2d_stream) {
+    cudaStreamSynchronize(c->h2d_stream);
+    cudaStreamDestroy(c->h2d_stream);
+  }
+  for (cudaEvent_t e : c->h2d_ev)
+    if (e) cudaEventDestroy(e);
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
                     &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
                     &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->tile_cost, &c->planes64, &c->geo, &c->frame32, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
@@ -991,7 +1017,61 @@ int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_ter
   float* r = ensure<float>(c->host_raw, S * n + 1);
   float* img = ensure<float>(c->host_img, 8 * npix + 1);
   if (!r || !img) return set_error(c, DRK_ERR_OOM, "host staging");
-  cudaMemcpyAsync(r, raw_host, sizeof(float) * S * n, cudaMemcpyHostToDevice, c->stream);
+  // Page-locked parameters of a large scene: copied in chunks of primitives on
+  // a second stream, each chunk's activation and K1 (per-primitive polygons,
+  // the longest prep stage) launched as soon as it has landed, so the copy
+  // overlaps them (config 1: the 29.6 MB upload hides behind K1).
+  // DRK_H2D_CHUNKS=1 turns the pipeline off.
+  static const int env_chunks = getenv("DRK_H2D_CHUNKS") ? atoi(getenv("DRK_H2D_CHUNKS")) : 4;
+  const int nchunk = std::max(1, std::min(8, n >= 65536 ? env_chunks : 1));
+  bool piped = nchunk > 1 && k >= 3 && k <= kMaxK;
+  if (piped) {
+    cudaPointerAttributes pa;
+    piped = cudaPointerGetAttributes(&pa, raw_host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+  }
+  if (piped && !c->h2d_stream) {
+    bool ok = cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking) == cudaSuccess;
+    for (int q = 0; q < 9 && ok; ++q) ok = cudaEventCreateWithFlags(&c->h2d_ev[q], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+      cudaGetLastError();
+      piped = false;
+    }
+  }
+  H2DPipe pipe;
+  if (piped) {
+    pipe.raw = r;
+    pipe.nchunk = nchunk;
+    // the copies may start once the context's stream is past earlier work on r
+    cudaEventRecord(c->h2d_ev[8], c->stream);
+    cudaStreamWaitEvent(c->h2d_stream, c->h2d_ev[8], 0);
+    for (int q = 0; q <= nchunk; ++q) pipe.bounds[q] = (int)((long long)n * q / nchunk);
+    for (int q = 0; q < nchunk; ++q) {
+      const size_t i0 = pipe.bounds[q], w = pipe.bounds[q + 1] - pipe.bounds[q];
+      cudaMemcpy2DAsync(r + i0, sizeof(float) * n, raw_host + i0, sizeof(float) * n, sizeof(float) * w, S,
+                        cudaMemcpyHostToDevice, c->h2d_stream);
+      cudaEventRecord(c->h2d_ev[q], c->h2d_stream);
+      pipe.ready[q] = c->h2d_ev[q];
+    }
+  } else {
+    cudaMemcpyAsync(r, raw_host, sizeof(float) * S * n, cudaMemcpyHostToDevice, c->stream);
+  }
+  // forward on device parameters: the whole activation up front, or (piped)
+  // the counters zeroed here and the activation issued chunk by chunk from K1
+  auto forward = [&](float* col, float* dep, float* nor, float* alp) -> int {
+    if (!piped) return drk_forward(c, r, n, k, sh_terms, cam, opt, col, dep, nor, alp);
+    if (!c || !cam || !opt || n < 0) return DRK_ERR_INVALID_ARG;
+    c->has_fwd = false;
+    c->launch_base = launch_counter();
+    mark(c, 0);
+    c->has_act = false;
+    if (int st = activate_setup(c, n, k, sh_terms)) return st;
+    cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * C_COUNT, c->stream);
+    c->has_act = true;
+    const int st = run_forward(c, cam, opt, col, dep, nor, alp, &pipe);
+    if (st) c->has_act = false;
+    return st;
+  };
   // Page-locked outputs: the raster kernels store the pixels straight into
   // them as tiles finish (zero-copy; config 1 e2e 25.9 ms vs 26.8 ms with a
   // band-wise staging copy).  DRK_HOST_OUT=copy forces device framebuffers.
@@ -1003,7 +1083,7 @@ int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_ter
     float* mn = mapped(normal_host, &ok);
     float* ma = mapped(alpha_host, &ok);
     if (ok) {
-      const int st = drk_forward(c, r, n, k, sh_terms, cam, opt, mc, md, mn, ma);
+      const int st = forward(mc, md, mn, ma);
       if (st) return st;
       return cuda_check(c, cudaStreamSynchronize(c->stream), "forward_host");
     }
@@ -1013,7 +1093,7 @@ int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_ter
   float* ddep = depth_host ? img + 3 * npix : nullptr;
   float* dnor = normal_host ? img + 4 * npix : nullptr;
   float* dalp = alpha_host ? img + 7 * npix : nullptr;
-  if (int st = drk_forward(c, r, n, k, sh_terms, cam, opt, dcol, ddep, dnor, dalp)) return st;
+  if (int st = forward(dcol, ddep, dnor, dalp)) return st;
   if (color_host) cudaMemcpyAsync(color_host, dcol, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, c->stream);
   if (depth_host) cudaMemcpyAsync(depth_host, ddep, sizeof(float) * npix, cudaMemcpyDeviceToHost, c->stream);
   if (normal_host) cudaMemcpyAsync(normal_host, dnor, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, c->stream);

@@ -148,7 +148,12 @@ bool raster_fast_eligible(const RasterParams& P);
 void launch_raster_fast(const RasterParams& P, int n_tiles, bool validate, cudaStream_t s);
 int raster_fast_nt(long long pairs, int n_tiles);
 void launch_raster_bwd_fast(const RasterParams& P, int n_tiles, cudaStream_t s);
-void launch_shape_rec(const ShapeView& S, int n, float* rec, cudaStream_t s);
+void launch_shape_rec(const ShapeView& S, int i0, int i1, float* rec, cudaStream_t s);
+// Activation split for the host-buffer pipeline (drk_forward_host): buffers and
+// the Activated view first, then kernels over primitive ranges as their
+// parameters arrive.
+int activate_setup(drk_ctx* c, int n, int K, int terms);
+void activate_range(drk_ctx* c, const float* raw, int i0, int i1);
 double measure_fp32_peak(cudaStream_t s);
 void launch_raster_bwd_fast_det(const RasterParams& P, int n_tiles, cudaStream_t s);
 void launch_pixels_bwd(const RasterParams& P, cudaStream_t s);  // k_raster_pixels_warp<MODE, true> over P.redo_list
@@ -163,6 +168,9 @@ void launch_eval_sorting_reduce(const CamD& cam, const long long* tileoff, const
 struct drk_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // drk_forward_host pipeline: parameter chunks copied on h2d_stream, h2d_ev[q] = chunk q landed
+  cudaStream_t h2d_stream = nullptr;
+  cudaEvent_t h2d_ev[9] = {};
   bool own_stream = false;
   std::string err;
 
@@ -234,8 +242,17 @@ namespace drk {
 // Launchers (drk_kernels.cu).  All return a drk_status.
 int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms);
 int launch_shape(drk_ctx* c, const drk_prims* p, int n, int K, int terms);
+// Host-buffer pipeline (drk_forward_host): the raw parameters arrive in nchunk
+// primitive ranges [bounds[q], bounds[q+1]), chunk q complete when ready[q] fires.
+struct H2DPipe {
+  const float* raw = nullptr;  // device copy of the [S][n] parameters
+  int nchunk = 0;
+  int bounds[9] = {};
+  cudaEvent_t ready[8] = {};
+};
 int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float* color, float* depth,
-                float* normal, float* alpha);
+                float* normal, float* alpha,
+                const H2DPipe* pipe = nullptr);
 int run_backward(drk_ctx* c, const float* raw, const drk_frame_grad* fg, float* grad_raw,
                  float* d_center_world, float* screen_grad, uint8_t* touched, int accumulate,
                  int deterministic);

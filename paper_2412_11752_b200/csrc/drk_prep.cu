@@ -20,9 +20,9 @@ namespace drk {
 // ---------------------------------------------------------------------------
 __global__ void k_activate(const float* __restrict__ raw, int n, int K, int terms, double* mu, double* rot,
                            double* s, double* th, double* eta, double* tau, double* o, float* sh,
-                           unsigned long long* counters) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+                           unsigned long long* counters, int i0, int i1) {
+  const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= i1) return;
   const int S = 3 + 4 + 2 * K + 3 + 3 * terms;
   bool finite = true;
   for (int j = 0; j < S; ++j) finite &= isfinite(raw[(size_t)j * n + i]);
@@ -61,11 +61,11 @@ __global__ void k_activate(const float* __restrict__ raw, int n, int K, int term
 
 // Endpoints and bracket determinants (types.hpp:93-95, core.cpp:188-190) and
 // the fp32 fast-path constants of ShapeView.
-__global__ void k_shape(int n, int K, const double* s, const double* th, double* ex, double* ey, double* det,
+__global__ void k_shape(int i0, int i1, int K, const double* s, const double* th, double* ex, double* ey, double* det,
                         float* thf, float* invdetf, float* piogf, float* hf, const double* tau, const double* o,
                         float* psif) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= i1) return;
   {
     // sharpen (core.cpp:229-237) in point-slope form
     const double t = tau[i];
@@ -501,12 +501,12 @@ __device__ __forceinline__ W2 weight_cs(const PolyParams& p, double a, double* c
 __global__ void __launch_bounds__(kPW * 32) k_prep_warp(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox,
                                                          int2* hullref, double2* pts_pool, long long pts_cap,
                                                          int2* ptsref, int* rowcnt, unsigned long long* counters,
-                                                         int* overflow, float4* frame32) {
+                                                         int* overflow, float4* frame32, int i0, int i1) {
   extern __shared__ double4 prep_dyn[];
   const unsigned FULL = 0xffffffffu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * kPW + warp;
-  if (i >= A.n) return;  // warp-uniform
+  const int i = i0 + blockIdx.x * kPW + warp;
+  if (i >= i1) return;  // warp-uniform
   WarpScratch& W = reinterpret_cast<WarpScratch*>(prep_dyn)[warp];
   const int K = A.K;
   double f = 0, fv = 0;
@@ -1449,7 +1449,7 @@ __global__ void k_full_keys(long long n, const unsigned* __restrict__ sk, const 
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-static int launch_shape_consts(drk_ctx* c, int n, int K) {
+static int shape_setup(drk_ctx* c, int n, int K) {
   Activated& A = c->act;
   A.ex = ensure<double>(c->a_ex, (size_t)K * n);
   A.ey = ensure<double>(c->a_ey, (size_t)K * n);
@@ -1461,26 +1461,37 @@ static int launch_shape_consts(drk_ctx* c, int n, int K) {
   A.psif = ensure<float>(c->a_psif, 12 * (size_t)n);
   if (!A.ex || !A.ey || !A.det || !A.thf || !A.invdetf || !A.piogf || !A.hf || !A.psif)
     return set_error(c, DRK_ERR_OOM, "shape buffers");
-  if (n > 0) {
-    k_shape<<<(n + 127) / 128, 128, 0, c->stream>>>(n, K, A.s, A.th, const_cast<double*>(A.ex),
-                                                   const_cast<double*>(A.ey), const_cast<double*>(A.det),
-                                                   const_cast<float*>(A.thf), const_cast<float*>(A.invdetf),
-                                                   const_cast<float*>(A.piogf), const_cast<float*>(A.hf), A.tau, A.o,
-                                                   const_cast<float*>(A.psif));
-    DRK_COUNT_LAUNCH();
-  }
   A.rec = nullptr;
   if (K == 8) {
     // AoS fp32 records of the fast forward kernel (drk_raster_fast.cu)
     A.rec = ensure<float>(c->a_rec, (size_t)88 * n);
     if (!A.rec) return set_error(c, DRK_ERR_OOM, "shape records");
-    const ShapeView S{A.s, A.th, A.ex, A.ey, A.det, A.eta, A.tau, A.o, A.thf, A.invdetf, A.piogf, A.hf, A.psif, K};
-    launch_shape_rec(S, n, const_cast<float*>(A.rec), c->stream);
   }
+  return DRK_OK;
+}
+
+static void shape_range(drk_ctx* c, int i0, int i1) {
+  const Activated& A = c->act;
+  if (i1 <= i0) return;
+  k_shape<<<(i1 - i0 + 127) / 128, 128, 0, c->stream>>>(i0, i1, A.K, A.s, A.th, const_cast<double*>(A.ex),
+                                                        const_cast<double*>(A.ey), const_cast<double*>(A.det),
+                                                        const_cast<float*>(A.thf), const_cast<float*>(A.invdetf),
+                                                        const_cast<float*>(A.piogf), const_cast<float*>(A.hf), A.tau,
+                                                        A.o, const_cast<float*>(A.psif));
+  DRK_COUNT_LAUNCH();
+  if (A.rec) {
+    const ShapeView S{A.s, A.th, A.ex, A.ey, A.det, A.eta, A.tau, A.o, A.thf, A.invdetf, A.piogf, A.hf, A.psif, A.K};
+    launch_shape_rec(S, i0, i1, const_cast<float*>(A.rec), c->stream);
+  }
+}
+
+static int launch_shape_consts(drk_ctx* c, int n, int K) {
+  if (int st = shape_setup(c, n, K)) return st;
+  shape_range(c, 0, n);
   return cuda_check(c, cudaGetLastError(), "shape");
 }
 
-int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms) {
+int activate_setup(drk_ctx* c, int n, int K, int terms) {
   Activated& A = c->act;
   A.n = n;
   A.K = K;
@@ -1497,14 +1508,27 @@ int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms) {
   unsigned long long* ctr = ensure<unsigned long long>(c->counters, C_COUNT);
   if (!A.mu || !A.rot || !A.s || !A.th || !A.eta || !A.tau || !A.o || !A.sh || !ctr)
     return set_error(c, DRK_ERR_OOM, "activation buffers");
+  return shape_setup(c, n, K);
+}
+
+// activation + shape constants of primitives [i0, i1) (raw: the whole [S][n] array)
+void activate_range(drk_ctx* c, const float* raw, int i0, int i1) {
+  const Activated& A = c->act;
+  if (i1 <= i0) return;
+  k_activate<<<(i1 - i0 + 127) / 128, 128, 0, c->stream>>>(
+      raw, A.n, A.K, A.terms, const_cast<double*>(A.mu), const_cast<double*>(A.rot), const_cast<double*>(A.s),
+      const_cast<double*>(A.th), const_cast<double*>(A.eta), const_cast<double*>(A.tau), const_cast<double*>(A.o),
+      const_cast<float*>(A.sh), static_cast<unsigned long long*>(c->counters.p), i0, i1);
+  DRK_COUNT_LAUNCH();
+  shape_range(c, i0, i1);
+}
+
+int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms) {
+  if (int st = activate_setup(c, n, K, terms)) return st;
+  unsigned long long* ctr = static_cast<unsigned long long*>(c->counters.p);
   cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT, c->stream);
-  if (n > 0)
-    k_activate<<<(n + 127) / 128, 128, 0, c->stream>>>(
-        raw, n, K, terms, const_cast<double*>(A.mu), const_cast<double*>(A.rot), const_cast<double*>(A.s),
-        const_cast<double*>(A.th), const_cast<double*>(A.eta), const_cast<double*>(A.tau),
-        const_cast<double*>(A.o), const_cast<float*>(A.sh), ctr);
-  if (n > 0) DRK_COUNT_LAUNCH();
-  if (int st = launch_shape_consts(c, n, K)) return st;
+  activate_range(c, raw, 0, n);
+  if (int st = cuda_check(c, cudaGetLastError(), "activate")) return st;
   unsigned long long h[C_COUNT];
   if (int st = cuda_check(c, cudaMemcpyAsync(h, ctr, sizeof h, cudaMemcpyDeviceToHost, c->stream), "activate"))
     return st;

@@ -70,9 +70,9 @@ namespace drk {
 //   [24 + 8k, 32 + 8k) bracket (k, k+1 mod K): e_lo (x, y), e_hi (x, y),
 //            1/det (NaN when |det| < 1e-12, core.cpp:191), pi/gap, 1/s_lo^2, 1/s_hi^2
 // ---------------------------------------------------------------------------
-__global__ void k_shape_rec(int n, ShapeView S, float* __restrict__ rec) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+__global__ void k_shape_rec(int i0, int i1, ShapeView S, float* __restrict__ rec) {
+  const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= i1) return;
   const int K = 8;
   float* r = rec + (size_t)kRecStride * i;
   const size_t b = (size_t)K * i;
@@ -104,9 +104,9 @@ __global__ void k_shape_rec(int n, ShapeView S, float* __restrict__ rec) {
   }
 }
 
-void launch_shape_rec(const ShapeView& S, int n, float* rec, cudaStream_t s) {
-  if (n > 0 && S.K == 8) {
-    k_shape_rec<<<(n + 127) / 128, 128, 0, s>>>(n, S, rec);
+void launch_shape_rec(const ShapeView& S, int i0, int i1, float* rec, cudaStream_t s) {
+  if (i1 > i0 && S.K == 8) {
+    k_shape_rec<<<(i1 - i0 + 127) / 128, 128, 0, s>>>(i0, i1, S, rec);
     DRK_COUNT_LAUNCH();
   }
 }
