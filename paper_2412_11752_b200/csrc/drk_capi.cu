@@ -1065,11 +1065,17 @@ int drk_forward_host(drk_ctx* c, const float* raw_host, int n, int k, int sh_ter
     c->launch_base = launch_counter();
     mark(c, 0);
     c->has_act = false;
-    if (int st = activate_setup(c, n, k, sh_terms)) return st;
-    cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * C_COUNT, c->stream);
-    c->has_act = true;
-    const int st = run_forward(c, cam, opt, col, dep, nor, alp, &pipe);
-    if (st) c->has_act = false;
+    int st = activate_setup(c, n, k, sh_terms);
+    if (!st) {
+      cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * C_COUNT, c->stream);
+      c->has_act = true;
+      st = run_forward(c, cam, opt, col, dep, nor, alp, &pipe);
+    }
+    if (st) {
+      // an early error may leave chunk copies in flight: none may outlive the call
+      c->has_act = false;
+      cudaStreamSynchronize(c->h2d_stream);
+    }
     return st;
   };
   // Page-locked outputs: the raster kernels store the pixels straight into
