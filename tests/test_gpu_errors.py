@@ -79,3 +79,34 @@ def test_replay_mismatch():
         assert st == _lib.ReplayMismatchError.status
     finally:
         r.close()
+
+
+@pytest.mark.parametrize("bad", ["nonfinite", "quaternion"])
+def test_host_pipeline_errors(bad):
+    """drk_forward_host on page-locked parameters of a large scene (the chunked
+    upload that overlaps activation and K1) reports the activation's errors
+    after the fact, like the device path, and leaves the context usable."""
+    sc = scenes.random_scene(70000, seed=5, sh_degree=0)
+    raw = sc.f32().copy()
+    if bad == "nonfinite":
+        raw[9, 65000] = np.nan  # a primitive in the last chunk
+    else:
+        raw[3:7, 12345] = 0.0
+    cam = scenes.look_at_camera(96, 64, (0.0, 0.0, -3.0))
+    host = torch.from_numpy(raw).pin_memory()
+    outs = {"color": torch.empty(cam.height, cam.width, 3, pin_memory=True),
+            "depth": torch.empty(cam.height, cam.width, pin_memory=True),
+            "normal": torch.empty(cam.height, cam.width, 3, pin_memory=True),
+            "alpha": torch.empty(cam.height, cam.width, pin_memory=True)}
+    exc = _lib.NonFiniteError if bad == "nonfinite" else _lib.DegenerateQuaternionError
+    r = Rasterizer(0)
+    try:
+        with pytest.raises(exc):
+            r.render_host_ptrs(host, outs, cam, RenderOptions(sh_degree=0))
+        good = torch.from_numpy(sc.f32()).pin_memory()
+        r.render_host_ptrs(good, outs, cam, RenderOptions(sh_degree=0))
+        torch.cuda.synchronize()
+        fb = r.render(sc.f32(), cam, RenderOptions(sh_degree=0))
+        assert torch.equal(fb.color.cpu(), outs["color"])
+    finally:
+        r.close()
