@@ -106,18 +106,30 @@ template int exclusive_scan<unsigned>(drk_ctx*, const unsigned*, long long, long
 #endif
 constexpr int kRsWarps = 8, kRsItems = DRK_RS_ITEMS, kRsThreads = kRsWarps * 32, kRsChunk = kRsThreads * kRsItems;
 
+// per-warp sub-histograms: after the first pass the keys arrive grouped by
+// digit, and a single block-wide histogram would serialise on same-address
+// shared-memory atomics
 __global__ void __launch_bounds__(kRsThreads) k_rs_hist(const unsigned* __restrict__ src, long long n,
                                                         int shift, unsigned* hist, int nblk) {
-  __shared__ unsigned cnt[256];
-  cnt[threadIdx.x] = 0;
+  __shared__ unsigned cnt[kRsWarps][256];
+  for (int d = threadIdx.x; d < kRsWarps * 256; d += kRsThreads) (&cnt[0][0])[d] = 0;
   __syncthreads();
+  const int warp = threadIdx.x >> 5;
   const long long base = (long long)blockIdx.x * kRsChunk;
+  unsigned kk[kRsItems];
+#pragma unroll
   for (int k = 0; k < kRsItems; ++k) {
     const long long i = base + k * kRsThreads + threadIdx.x;
-    if (i < n) atomicAdd(&cnt[(src[i] >> shift) & 255u], 1u);
+    kk[k] = i < n ? ((src[i] >> shift) & 255u) : 256u;
   }
+#pragma unroll
+  for (int k = 0; k < kRsItems; ++k)
+    if (kk[k] < 256u) atomicAdd(&cnt[warp][kk[k]], 1u);
   __syncthreads();
-  hist[(size_t)threadIdx.x * nblk + blockIdx.x] = cnt[threadIdx.x];
+  unsigned t = 0;
+#pragma unroll
+  for (int w = 0; w < kRsWarps; ++w) t += cnt[w][threadIdx.x];
+  hist[(size_t)threadIdx.x * nblk + blockIdx.x] = t;
 }
 
 // One stable LSD pass: per-warp match-based ranks, block-local digit order
