@@ -375,20 +375,22 @@ def main():
     achieved = flops / (rast_ms * 1e-3) / 1e12
     stage_ms = {k: v / args.steps for k, v in stage_acc.items() if k in ("activate", "preprocess", "rows_emit", "sort",
                                                                          "raster", "raster_fp64")}
-    traffic, traffic_src = None, None
+    traffic, traffic_src, pipes = None, None, None
     try:  # DRAM bytes of the dominant kernel from the committed ncu --set full capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tj = json.load(fh)
             traffic = tj.get("k_raster_fast")
             traffic_src = tj.get("source", "profiles/ncu_traffic.json")
+            pipes = tj.get("k_raster_fast_pipes")
     except (OSError, ValueError):
-        traffic = None
+        traffic, pipes = None, None
     roofline = {"kernel": "k_raster_fast (fp32 interval pass)", "bound": "fp32", "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                 "traffic_source": f"committed ncu --set full capture (not measured in this run): {traffic_src}",
                 "peak_source": "FFMA microbenchmark (drk_measure_fp32_peak) in this run; MEASURED_PEAKS.json has no "
                                "FP32 CUDA-core figure",
                 "algorithmic_flops_per_launch": flops, "kernel_ms": rast_ms,
+                "pipe_utilisation": pipes,
                 "counts": {"pixels": px, "streamed": st["streamed"], "popped": st["popped"],
                            "composited": st["composited"]},
                 "share_of_step": rast_ms / ms_per_step}
