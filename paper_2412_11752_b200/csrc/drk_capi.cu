@@ -16,13 +16,8 @@
 namespace drk {
 
 // kernels defined in the other translation units
-__global__ void k_prep_warp(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pts_pool,
-                            long long pts_cap, int2* ptsref, int* rowcnt, unsigned long long* counters, int* overflow,
-                            float4* frame32, int i0, int i1);
 __global__ void k_prep_hull(int n, const int2* ptsref, double2* pts_pool, CamD cam, OptD opt, int4* bbox, int2* hullref,
                             double2* pool, long long pool_cap, int* rowcnt, unsigned long long* counters);
-size_t prep_warp_smem();
-int prep_warp_warps();
 __global__ void k_prep1(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox, int2* hullref, double2* pool,
                         long long pool_cap, int* rowcnt, unsigned long long* counters, const int* list, int list_n,
                         double2* scratch, int scratch_cap, int* overflow);
@@ -401,6 +396,40 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   if (c->pts_cap < (long long)n * 260 + 1024) c->pts_cap = (long long)n * 260 + 1024;
   int2* ptsref = ensure<int2>(c->ptsref, n + 1);
   if (!ptsref) return set_error(c, DRK_ERR_OOM, "point refs");
+  // K1 vertex cache: off for the first forward of an activation (the usual
+  // single view), built on the second, used from the third (views of one
+  // activation: multi-view batches, training views).  DRK_VCACHE=0: off.
+  static const bool vc_on = !getenv("DRK_VCACHE") || atoi(getenv("DRK_VCACHE")) != 0;
+  int k1_mode = 0;
+  VertexCache vc;
+  if (vc_on && n >= 4096 && !pipe) {
+    const bool ready = c->vc_gen == c->act_gen && c->vc_alpha_min == opt->alpha_min && c->vc_ref.p;
+    if (ready) {
+      k1_mode = 2;
+    } else if (c->act_renders >= 1) {
+      // room for ~96 vertices per primitive, within an eighth of the free memory
+      const long long cap = (long long)n * 96;
+      const size_t bytes = sizeof(double) * 3 * (size_t)cap + sizeof(int2) * (size_t)n + 64;
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      const size_t have = c->vc_pool.bytes + c->vc_ref.bytes;
+      if (bytes <= (free_b + have) / 8) {
+        double* pool = ensure<double>(c->vc_pool, 3 * (size_t)cap);
+        int2* ref = ensure<int2>(c->vc_ref, (size_t)n);
+        unsigned long long* cur = ensure<unsigned long long>(c->vc_cursor, 1);
+        if (pool && ref && cur) {
+          k1_mode = 1;
+          cudaMemsetAsync(cur, 0, sizeof(unsigned long long), s);
+        }
+      }
+    }
+    if (k1_mode) {
+      vc.pool = static_cast<double*>(c->vc_pool.p);
+      vc.cap = (long long)(c->vc_pool.bytes / (3 * sizeof(double)));
+      vc.ref = static_cast<int2*>(c->vc_ref.p);
+      vc.cursor = static_cast<unsigned long long*>(c->vc_cursor.p);
+    }
+  }
   // K1 with retry on hull-pool overflow
   DevBuf& ovf_buf = c->rows;  // reused as overflow list before rows are built
   for (int attempt = 0; attempt < 4; ++attempt) {
@@ -414,10 +443,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     if (!piped) cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * C_COUNT, s);
     if (n > 0) {
       // warp per primitive; near-clipped / oversized polygons -> overflow list (k_prep1)
-      static PerDeviceOnce attr;
-      const size_t smem = prep_warp_smem();
-      attr([&] { cudaFuncSetAttribute(k_prep_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
-      const int pw = prep_warp_warps();
+      const int mode = attempt == 0 ? k1_mode : (k1_mode ? 2 : 0);  // a retry reuses the cache built
       // pipelined: activation + K1 of each chunk of primitives as soon as its
       // parameters have crossed the link (the copies of later chunks overlap)
       const int nchunk = piped ? pipe->nchunk : 1;
@@ -427,10 +453,8 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
           cudaStreamWaitEvent(s, pipe->ready[q], 0);
           activate_range(c, pipe->raw, i0, i1);
         }
-        if (i1 > i0)
-          k_prep_warp<<<(i1 - i0 + pw - 1) / pw, 32 * pw, smem, s>>>(A, cd, od, geo, bbox, hullref, ppool, c->pts_cap,
-                                                                  ptsref, rowcnt, ctr, ovf,
-                                                                  static_cast<float4*>(c->frame32.p), i0, i1);
+        launch_prep_warp(mode, A, cd, od, geo, bbox, hullref, ppool, c->pts_cap, ptsref, rowcnt, ctr, ovf,
+                         static_cast<float4*>(c->frame32.p), i0, i1, vc, s);
       }
       k_prep_hull<<<(unsigned)((2LL * n + 255) / 256), 256, 0, s>>>(n, ptsref, ppool, cd, od, bbox, hullref, pool,
                                                                     c->hull_cap, rowcnt, ctr);
@@ -472,6 +496,10 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
     if ((long long)h[C_HULL_POOL] <= c->hull_cap) {
       c->stats.poly_overflow = n_ovf;
       c->stats.primitives = (int64_t)h[C_VISIBLE];
+      if (k1_mode == 1) {
+        c->vc_gen = c->act_gen;
+        c->vc_alpha_min = opt->alpha_min;
+      }
       break;
     }
     c->hull_cap = (long long)h[C_HULL_POOL] + (long long)h[C_HULL_POOL] / 4 + 1024;
@@ -624,6 +652,7 @@ int run_forward(drk_ctx* c, const drk_camera* cam, const drk_options* opt, float
   c->stats.cache_appends = (int64_t)h[C_CACHE_APPEND];
   if (h[C_ERR_DEGEN_BASIS]) return set_error(c, DRK_ERR_DEGENERATE_BASIS, "adjacent endpoints nearly collinear");
   c->has_fwd = true;
+  ++c->act_renders;
   return DRK_OK;
 }
 
@@ -903,7 +932,7 @@ void drk_ctx_destroy(drk_ctx* c) {
     if (e) cudaEventDestroy(e);
   DevBuf* bufs[] = {&c->a_mu, &c->a_rot, &c->a_s, &c->a_th, &c->a_eta, &c->a_tau, &c->a_o, &c->a_sh,
                     &c->a_ex, &c->a_ey, &c->a_det, &c->a_thf, &c->a_invdetf, &c->a_piogf, &c->a_hf,
-                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->tile_cost, &c->planes64, &c->geo, &c->frame32, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
+                    &c->a_psif, &c->a_rec, &c->pxflag, &c->pxstop, &c->vstat, &c->redo, &c->redo_cnt, &c->tile_cost, &c->planes64, &c->vc_pool, &c->vc_ref, &c->vc_cursor, &c->geo, &c->frame32, &c->bbox, &c->hullref, &c->hull, &c->ptspool, &c->ptsref, &c->rowcnt,
                     &c->rowoff, &c->rows, &c->rowpaircnt, &c->rowpairoff, &c->pk, &c->pv, &c->sk,
                     &c->hist, &c->sortoff, &c->tileoff, &c->cdirs, &c->tdirs, &c->bits,
                     &c->pxstate, &c->replay_cnt, &c->replay_rec, &c->replay_ids, &c->gact, &c->touched,

@@ -153,6 +153,19 @@ void launch_shape_rec(const ShapeView& S, int i0, int i1, float* rec, cudaStream
 // the Activated view first, then kernels over primitive ranges as their
 // parameters arrive.
 int activate_setup(drk_ctx* c, int n, int K, int terms);
+// K1 vertex cache (several views of one activation): world-space vertices of
+// the wedge-tree leaves, vref[i] = (offset, count) (drk_prep.cu k_prep_warp)
+struct VertexCache {
+  double* pool = nullptr;
+  long long cap = 0;  // vertices
+  int2* ref = nullptr;
+  unsigned long long* cursor = nullptr;
+};
+// mode 0: plain K1; 1: build the cache; 2: use it
+void launch_prep_warp(int mode, const Activated& A, const CamD& cam, const OptD& opt, Geo* geo, int4* bbox,
+                      int2* hullref, double2* ppool, long long pts_cap, int2* ptsref, int* rowcnt,
+                      unsigned long long* ctr, int* ovf, float4* frame32, int i0, int i1, const VertexCache& vc,
+                      cudaStream_t s);
 void activate_range(drk_ctx* c, const float* raw, int i0, int i1);
 double measure_fp32_peak(cudaStream_t s);
 void launch_raster_bwd_fast_det(const RasterParams& P, int n_tiles, cudaStream_t s);
@@ -216,6 +229,12 @@ struct drk_ctx {
   drk::DevBuf planes64;  // drk_get_framebuffers_f64 staging
   drk::DevBuf tile_cost;       // per tile: entries the fast forward streamed (the backward's dispatch order)
   bool tile_cost_valid = false;
+  // K1 vertex cache: built on the second forward of one activation, used from the third
+  drk::DevBuf vc_pool, vc_ref, vc_cursor;
+  uint64_t act_gen = 0;       // bumped by every new activation
+  int act_renders = 0;        // forwards of the current activation
+  uint64_t vc_gen = ~0ull;    // activation the cache holds
+  double vc_alpha_min = -1;   // ... and the alpha_min its support radii used
   long long redo_half = 0;  // offset of the redo list's ordering scratch (pixels of the last forward + 1)
 
   // stage timing

@@ -438,6 +438,11 @@ struct WarpScratch {
   double2 verts[kWVerts + 8];
   BrP br[kMaxK];
 };
+// build mode of the vertex cache: the leaves' world-space vertices beside
+struct WarpScratchB {
+  WarpScratch w;
+  double world[3 * kWVerts];
+};
 __device__ __forceinline__ PolyParams poly_params(const BrP& b, double eta, double support_c) {
   PolyParams p;
   p.alo = b.alo;
@@ -475,8 +480,9 @@ __device__ int mono_chain(const double2* pts, int n, bool reverse, double2* h) {
 }
 }  // namespace
 
-size_t prep_warp_smem() { return (size_t)kPW * sizeof(WarpScratch); }
-int prep_warp_warps() { return kPW; }
+static size_t prep_warp_smem(int mode) {
+  return (size_t)kPW * (mode == 1 ? sizeof(WarpScratchB) : sizeof(WarpScratch));
+}
 
 // weight_at (raster.cpp:158-168) that also returns cos(a), sin(a) for the
 // wedge vertices at a (raster.cpp:199-201 evaluates the same cos/sin).
@@ -498,16 +504,28 @@ __device__ __forceinline__ W2 weight_cs(const PolyParams& p, double a, double* c
 // Phase A: vertices -> sorted unique points in the point pool.  ptsref[i] =
 // (offset, count) of the sorted points; the pool slot holds 3 count entries
 // (points, lower chain, upper chain) for k_prep_hull.
+// MODE 0: plain.  Vertex cache (camera-independent leaves of the wedge tree, for
+// several views of one activation): MODE 1 builds it (the tree runs to the end
+// even when a vertex is near-clipped in this view, and its world-space
+// vertices go to vpool; vref[i] = (offset, count), count -1: the tree overflows
+// the warp buffers, -2: not cached), MODE 2 projects the cached vertices
+// instead of expanding the tree (uncached primitives expand it as in MODE 0).
+// The vertex set, hence the hull, is the same bits in every mode.
+template <int MODE>
 __global__ void __launch_bounds__(kPW * 32) k_prep_warp(Activated A, CamD cam, OptD opt, Geo* geo, int4* bbox,
                                                          int2* hullref, double2* pts_pool, long long pts_cap,
                                                          int2* ptsref, int* rowcnt, unsigned long long* counters,
-                                                         int* overflow, float4* frame32, int i0, int i1) {
+                                                         int* overflow, float4* frame32, int i0, int i1,
+                                                         double* vpool, long long vcap, int2* vref,
+                                                         unsigned long long* vcursor) {
   extern __shared__ double4 prep_dyn[];
   const unsigned FULL = 0xffffffffu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = i0 + blockIdx.x * kPW + warp;
   if (i >= i1) return;  // warp-uniform
-  WarpScratch& W = reinterpret_cast<WarpScratch*>(prep_dyn)[warp];
+  WarpScratch& W = MODE == 1 ? reinterpret_cast<WarpScratchB*>(prep_dyn)[warp].w
+                             : reinterpret_cast<WarpScratch*>(prep_dyn)[warp];
+  double* Wworld = MODE == 1 ? reinterpret_cast<WarpScratchB*>(prep_dyn)[warp].world : nullptr;
   const int K = A.K;
   double f = 0, fv = 0;
   const double o = A.o[i];
@@ -548,145 +566,198 @@ __global__ void __launch_bounds__(kPW * 32) k_prep_warp(Activated A, CamD cam, O
     bbox[i] = make_int4(1, 0, 1, 0);
     hullref[i] = make_int2(0, 0);
     ptsref[i] = make_int2(0, 0);
+    if (MODE == 1) vref[i] = make_int2(0, 0);
   }
   if (!visible) return;
-  const double eta = A.eta[i];
-  const double support_c = f * f;
-  const double* s = A.s + (size_t)K * i;
-  const double* th = A.th + (size_t)K * i;
-  // bracket parameters (raster.cpp:146-153) and coarse wedge counts (:202)
-  int coarse = 0;
-  BrP b;
-  if (lane < K) {
-    const int k = lane, hi = (k + 1) % K;
-    b.alo = k + 1 < K ? th[k] : th[k] - 2.0 * kPi;
-    const double ahi = k + 1 < K ? th[hi] : th[0];
-    b.gap = ahi - b.alo;
-    b.slo = s[k];
-    b.shi = s[hi];
-    b.elx = A.ex[(size_t)K * i + k];
-    b.ely = A.ey[(size_t)K * i + k];
-    b.ehx = A.ex[(size_t)K * i + hi];
-    b.ehy = A.ey[(size_t)K * i + hi];
-    b.det = A.det[(size_t)K * i + k];
-    const int ci = (int)ceil(b.gap / (kPi / 8.0));
-    coarse = ci > 1 ? ci : 1;
-    b.coarse = coarse;
-  }
-  int incl = coarse;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int v = __shfl_up_sync(FULL, incl, off);
-    if (lane >= off) incl += v;
-  }
-  if (lane < K) {
-    b.first = incl - coarse;
-    W.br[lane] = b;
-  }
-  const int total = (int)__reduce_add_sync(FULL, (unsigned)coarse);
-  __syncwarp();
-  bool fail = total > kWStack - 16;
-  // coarse wedges with their endpoint weights (and cos / sin of the endpoints)
-  if (!fail) {
-    for (int idx = lane; idx < total; idx += 32) {
-      int k = 0;
-      while (k + 1 < K && W.br[k + 1].first <= idx) ++k;
-      const BrP& bk = W.br[k];
-      const int j = idx - bk.first;
-      const PolyParams p = poly_params(bk, eta, support_c);
-      const double a0 = bk.alo + bk.gap * j / bk.coarse;
-      const double a1 = bk.alo + bk.gap * (j + 1) / bk.coarse;
-      WItem it;
-      const W2 w0 = weight_cs(p, a0, &it.c0, &it.s0), w1 = weight_cs(p, a1, &it.c1, &it.s1);
-      it.a0 = a0;
-      it.a1 = a1;
-      it.r0 = w0.rho1;
-      it.i0 = w0.inv;
-      it.r1 = w1.rho1;
-      it.i1 = w1.inv;
-      it.depth = 0;
-      it.k = k;
-      W.stack[idx] = it;
-    }
-  }
-  __syncwarp();
-  int sp = fail ? 0 : total, nv = 0;
-  const double mu[3] = {A.mu[3 * i], A.mu[3 * i + 1], A.mu[3 * i + 2]};
-  const double* R = A.rot + 9 * (size_t)i;
-  const double rx[3] = {R[0], R[3], R[6]}, ry[3] = {R[1], R[4], R[7]};
-  while (sp > 0 && !fail) {
-    // batch size throttled by the free stack space: with few free slots the
-    // LIFO walk is depth-first and grows the stack by at most one item per
-    // tree level (depth <= 9), so it never overflows
-    const int room = (kWStack - 12 - sp) / 2;
-    int m = sp < 32 ? sp : 32;
-    m = m < room ? m : (room > 1 ? room : 1);
-    const int base = sp - m;
-    WItem it;
-    if (lane < m) it = W.stack[base + lane];
-    __syncwarp();
-    bool split = false, leaf = false;
-    double bound = 0, mid = 0, cm = 0, sm_ = 0;
-    W2 wm;
-    if (lane < m) {
-      const PolyParams p = poly_params(W.br[it.k], eta, support_c);
-      const W2 w0{it.r0, it.i0}, w1{it.r1, it.i1};
-      const double rho1_min = dmin(w0.rho1, w1.rho1);
-      const double inv_min = dmin(w0.inv, w1.inv);
-      const double w_lb = p.eta * rho1_min * rho1_min + (1.0 - p.eta) * inv_min;
-      bound = sqrt(p.support_c / dmax(w_lb, 1e-12)) / cos(0.5 * (it.a1 - it.a0));
-      if (it.depth < 9 && it.a1 - it.a0 > 2e-3 && bound > 1.25 * dmin(radius_true(p, w0), radius_true(p, w1))) {
-        split = true;
-        mid = 0.5 * (it.a0 + it.a1);
-        wm = weight_cs(p, mid, &cm, &sm_);
-      } else {
-        leaf = true;
-      }
-    }
-    const unsigned smk = __ballot_sync(FULL, split), lmk = __ballot_sync(FULL, leaf);
-    const unsigned below = (1u << lane) - 1u;
-    const int n_split = __popc(smk), n_leaf = __popc(lmk);
-    if (base + 2 * n_split > kWStack || nv + 2 * n_leaf > kWVerts) {
+  bool fail = false;
+  int nv = 0;
+  bool cached = false;
+  if (MODE == 2) {
+    const int2 vr = vref[i];
+    if (vr.y == -1) {
       fail = true;
-      break;
-    }
-    if (split) {
-      const int slot = base + 2 * __popc(smk & below);
-      WItem l = it, r = it;
-      l.a1 = mid;
-      l.r1 = wm.rho1;
-      l.i1 = wm.inv;
-      l.c1 = cm;
-      l.s1 = sm_;
-      r.a0 = mid;
-      r.r0 = wm.rho1;
-      r.i0 = wm.inv;
-      r.c0 = cm;
-      r.s0 = sm_;
-      l.depth = r.depth = it.depth + 1;
-      W.stack[slot] = l;
-      W.stack[slot + 1] = r;
-    }
-    bool clip = false;
-    if (leaf) {
-      const int slot = nv + 2 * __popc(lmk & below);
-      const double cs[2][2] = {{it.c0, it.s0}, {it.c1, it.s1}};
-      for (int e = 0; e < 2; ++e) {
-        double w[3], pc[3];
-        for (int a = 0; a < 3; ++a) w[a] = mu[a] + bound * (cs[e][0] * rx[a] + cs[e][1] * ry[a]);
+      cached = true;
+    } else if (vr.y >= 0) {
+      // project the cached world-space vertices (the leaves' order)
+      cached = true;
+      nv = vr.y;
+      bool clip = false;
+      for (int t = lane; t < nv; t += 32) {
+        const double* wv = vpool + 3 * ((size_t)vr.x + t);
+        const double w[3] = {wv[0], wv[1], wv[2]};
+        double pc[3];
         to_camera(cam, w, pc);
         clip |= !(pc[2] >= kNearClip);
-        W.verts[slot + e] = make_double2(cam.fx * pc[0] / pc[2] + cam.cx, cam.fy * pc[1] / pc[2] + cam.cy);
+        W.verts[t] = make_double2(cam.fx * pc[0] / pc[2] + cam.cx, cam.fy * pc[1] / pc[2] + cam.cy);
+      }
+      if (__any_sync(FULL, clip)) fail = true;
+      __syncwarp();
+    }
+  }
+  if (!cached) {
+    const double eta = A.eta[i];
+    const double support_c = f * f;
+    const double* s = A.s + (size_t)K * i;
+    const double* th = A.th + (size_t)K * i;
+    // bracket parameters (raster.cpp:146-153) and coarse wedge counts (:202)
+    int coarse = 0;
+    BrP b;
+    if (lane < K) {
+      const int k = lane, hi = (k + 1) % K;
+      b.alo = k + 1 < K ? th[k] : th[k] - 2.0 * kPi;
+      const double ahi = k + 1 < K ? th[hi] : th[0];
+      b.gap = ahi - b.alo;
+      b.slo = s[k];
+      b.shi = s[hi];
+      b.elx = A.ex[(size_t)K * i + k];
+      b.ely = A.ey[(size_t)K * i + k];
+      b.ehx = A.ex[(size_t)K * i + hi];
+      b.ehy = A.ey[(size_t)K * i + hi];
+      b.det = A.det[(size_t)K * i + k];
+      const int ci = (int)ceil(b.gap / (kPi / 8.0));
+      coarse = ci > 1 ? ci : 1;
+      b.coarse = coarse;
+    }
+    int incl = coarse;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(FULL, incl, off);
+      if (lane >= off) incl += v;
+    }
+    if (lane < K) {
+      b.first = incl - coarse;
+      W.br[lane] = b;
+    }
+    const int total = (int)__reduce_add_sync(FULL, (unsigned)coarse);
+    __syncwarp();
+    fail = total > kWStack - 16;
+    // coarse wedges with their endpoint weights (and cos / sin of the endpoints)
+    if (!fail) {
+      for (int idx = lane; idx < total; idx += 32) {
+        int k = 0;
+        while (k + 1 < K && W.br[k + 1].first <= idx) ++k;
+        const BrP& bk = W.br[k];
+        const int j = idx - bk.first;
+        const PolyParams p = poly_params(bk, eta, support_c);
+        const double a0 = bk.alo + bk.gap * j / bk.coarse;
+        const double a1 = bk.alo + bk.gap * (j + 1) / bk.coarse;
+        WItem it;
+        const W2 w0 = weight_cs(p, a0, &it.c0, &it.s0), w1 = weight_cs(p, a1, &it.c1, &it.s1);
+        it.a0 = a0;
+        it.a1 = a1;
+        it.r0 = w0.rho1;
+        it.i0 = w0.inv;
+        it.r1 = w1.rho1;
+        it.i1 = w1.inv;
+        it.depth = 0;
+        it.k = k;
+        W.stack[idx] = it;
       }
     }
-    if (__any_sync(FULL, clip)) {
-      fail = true;
-      break;
-    }
-    sp = base + 2 * n_split;
-    nv += 2 * n_leaf;
     __syncwarp();
-  }
+    int sp = fail ? 0 : total;
+    bool clip_any = false;
+    const double mu[3] = {A.mu[3 * i], A.mu[3 * i + 1], A.mu[3 * i + 2]};
+    const double* R = A.rot + 9 * (size_t)i;
+    const double rx[3] = {R[0], R[3], R[6]}, ry[3] = {R[1], R[4], R[7]};
+    while (sp > 0 && !fail) {
+      // batch size throttled by the free stack space: with few free slots the
+      // LIFO walk is depth-first and grows the stack by at most one item per
+      // tree level (depth <= 9), so it never overflows
+      const int room = (kWStack - 12 - sp) / 2;
+      int m = sp < 32 ? sp : 32;
+      m = m < room ? m : (room > 1 ? room : 1);
+      const int base = sp - m;
+      WItem it;
+      if (lane < m) it = W.stack[base + lane];
+      __syncwarp();
+      bool split = false, leaf = false;
+      double bound = 0, mid = 0, cm = 0, sm_ = 0;
+      W2 wm;
+      if (lane < m) {
+        const PolyParams p = poly_params(W.br[it.k], eta, support_c);
+        const W2 w0{it.r0, it.i0}, w1{it.r1, it.i1};
+        const double rho1_min = dmin(w0.rho1, w1.rho1);
+        const double inv_min = dmin(w0.inv, w1.inv);
+        const double w_lb = p.eta * rho1_min * rho1_min + (1.0 - p.eta) * inv_min;
+        bound = sqrt(p.support_c / dmax(w_lb, 1e-12)) / cos(0.5 * (it.a1 - it.a0));
+        if (it.depth < 9 && it.a1 - it.a0 > 2e-3 && bound > 1.25 * dmin(radius_true(p, w0), radius_true(p, w1))) {
+          split = true;
+          mid = 0.5 * (it.a0 + it.a1);
+          wm = weight_cs(p, mid, &cm, &sm_);
+        } else {
+          leaf = true;
+        }
+      }
+      const unsigned smk = __ballot_sync(FULL, split), lmk = __ballot_sync(FULL, leaf);
+      const unsigned below = (1u << lane) - 1u;
+      const int n_split = __popc(smk), n_leaf = __popc(lmk);
+      if (base + 2 * n_split > kWStack || nv + 2 * n_leaf > kWVerts) {
+        fail = true;
+        break;
+      }
+      if (split) {
+        const int slot = base + 2 * __popc(smk & below);
+        WItem l = it, r = it;
+        l.a1 = mid;
+        l.r1 = wm.rho1;
+        l.i1 = wm.inv;
+        l.c1 = cm;
+        l.s1 = sm_;
+        r.a0 = mid;
+        r.r0 = wm.rho1;
+        r.i0 = wm.inv;
+        r.c0 = cm;
+        r.s0 = sm_;
+        l.depth = r.depth = it.depth + 1;
+        W.stack[slot] = l;
+        W.stack[slot + 1] = r;
+      }
+      bool clip = false;
+      if (leaf) {
+        const int slot = nv + 2 * __popc(lmk & below);
+        const double cs[2][2] = {{it.c0, it.s0}, {it.c1, it.s1}};
+        for (int e = 0; e < 2; ++e) {
+          double w[3], pc[3];
+          for (int a = 0; a < 3; ++a) w[a] = mu[a] + bound * (cs[e][0] * rx[a] + cs[e][1] * ry[a]);
+          if (MODE == 1)
+            for (int a = 0; a < 3; ++a) Wworld[3 * (slot + e) + a] = w[a];
+          to_camera(cam, w, pc);
+          clip |= !(pc[2] >= kNearClip);
+          W.verts[slot + e] = make_double2(cam.fx * pc[0] / pc[2] + cam.cx, cam.fy * pc[1] / pc[2] + cam.cy);
+        }
+      }
+      if (__any_sync(FULL, clip)) {
+        if (MODE == 1) {
+          clip_any = true;  // this view takes the serial path, the cache still needs every vertex
+        } else {
+          fail = true;
+          break;
+        }
+      }
+      sp = base + 2 * n_split;
+      nv += 2 * n_leaf;
+      __syncwarp();
+    }
+    if (MODE == 1) {
+      // publish the leaves' world-space vertices (count -1: the tree overflowed)
+      int2 r = make_int2(0, -1);
+      if (!fail) {
+        unsigned long long off = 0;
+        if (lane == 0) off = atomicAdd(vcursor, (unsigned long long)nv);
+        off = __shfl_sync(FULL, off, 0);
+        if ((long long)off + nv <= vcap) {
+          __syncwarp();
+          for (int t = lane; t < 3 * nv; t += 32) vpool[3 * off + t] = Wworld[t];
+          r = make_int2((int)off, nv);
+        } else {
+          r = make_int2(0, -2);
+        }
+      }
+      if (lane == 0) vref[i] = r;
+      if (clip_any) fail = true;
+    }
+  }  // !cached
   if (fail) {
     // serial path with the near clip and large buffers (k_prep1)
     if (lane == 0) {
@@ -770,6 +841,32 @@ __global__ void __launch_bounds__(kPW * 32) k_prep_warp(Activated A, CamD cam, O
   if (off + 3 * n_u + 2 > pts_cap) return;  // host detects via the cursor and retries with a larger pool
   for (int t = lane; t < n_u; t += 32) pts_pool[off + t] = W.verts[t];
   if (lane == 0) ptsref[i] = make_int2((int)off, n_u);
+}
+
+template <int MODE>
+static void launch_prep_warp_mode(const Activated& A, const CamD& cam, const OptD& opt, Geo* geo, int4* bbox,
+                                  int2* hullref, double2* ppool, long long pts_cap, int2* ptsref, int* rowcnt,
+                                  unsigned long long* ctr, int* ovf, float4* frame32, int i0, int i1,
+                                  const VertexCache& vc, cudaStream_t s) {
+  static PerDeviceOnce attr;
+  const size_t smem = prep_warp_smem(MODE);
+  attr([&] { cudaFuncSetAttribute(k_prep_warp<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+  k_prep_warp<MODE><<<(i1 - i0 + kPW - 1) / kPW, 32 * kPW, smem, s>>>(A, cam, opt, geo, bbox, hullref, ppool, pts_cap,
+                                                                   ptsref, rowcnt, ctr, ovf, frame32, i0, i1, vc.pool,
+                                                                   vc.cap, vc.ref, vc.cursor);
+}
+
+void launch_prep_warp(int mode, const Activated& A, const CamD& cam, const OptD& opt, Geo* geo, int4* bbox,
+                      int2* hullref, double2* ppool, long long pts_cap, int2* ptsref, int* rowcnt,
+                      unsigned long long* ctr, int* ovf, float4* frame32, int i0, int i1, const VertexCache& vc,
+                      cudaStream_t s) {
+  if (i1 <= i0) return;
+  if (mode == 1)
+    launch_prep_warp_mode<1>(A, cam, opt, geo, bbox, hullref, ppool, pts_cap, ptsref, rowcnt, ctr, ovf, frame32, i0, i1, vc, s);
+  else if (mode == 2)
+    launch_prep_warp_mode<2>(A, cam, opt, geo, bbox, hullref, ppool, pts_cap, ptsref, rowcnt, ctr, ovf, frame32, i0, i1, vc, s);
+  else
+    launch_prep_warp_mode<0>(A, cam, opt, geo, bbox, hullref, ppool, pts_cap, ptsref, rowcnt, ctr, ovf, frame32, i0, i1, vc, s);
 }
 
 // Phase B: Andrew's monotone chain (raster.cpp:41-57) with two threads per
@@ -1492,6 +1589,8 @@ static int launch_shape_consts(drk_ctx* c, int n, int K) {
 }
 
 int activate_setup(drk_ctx* c, int n, int K, int terms) {
+  ++c->act_gen;  // a new activation: the K1 vertex cache is stale
+  c->act_renders = 0;
   Activated& A = c->act;
   A.n = n;
   A.K = K;
@@ -1539,6 +1638,8 @@ int launch_activate(drk_ctx* c, const float* raw, int n, int K, int terms) {
 }
 
 int launch_shape(drk_ctx* c, const drk_prims* p, int n, int K, int terms) {
+  ++c->act_gen;
+  c->act_renders = 0;
   Activated& A = c->act;
   A.n = n;
   A.K = K;
