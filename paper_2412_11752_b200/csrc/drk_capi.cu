@@ -298,6 +298,7 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
         static_cast<const double*>(c->tdirs.p), cd, od, pk, pv, krange);
   launch_counter() += 2;
   mark(c, 3);
+  sort_trace("start", s);
   // sort key: tile in the high bits, the quantised depth key in the rest
   int tbits = 1;
   while ((1ll << tbits) < n_tiles) ++tbits;
@@ -313,10 +314,12 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
                                                                                              c->key_dbits, sk);
     launch_counter() += 3;
   }
+  sort_trace("pack", s);
   // the emitted 64-bit keys are dead after packing: their buffer is the sort's
   // ping-pong space (four passes end back in sk / pv)
   unsigned* tmp = reinterpret_cast<unsigned*>(pk);
   if (int st = sort_pairs(c, sk, pv, tmp, tmp + n_pairs + 1, n_pairs)) return st;
+  sort_trace("radix", s);
   if (n_pairs > 0) {
     // runs of equal sort keys: full keys (into the dead emission buffer), then
     // the ids in (key, id) order into the second id buffer, which becomes the list
@@ -330,16 +333,20 @@ static int bin_band(drk_ctx* c, int ty_lo, int ty_hi, long long* n_pairs_out) {
     long long* long_runs = ensure<long long>(c->tie_long, (size_t)(n_pairs / 1024 + 2));
     if (!long_runs) return set_error(c, DRK_ERR_OOM, "tie runs");
     cudaMemsetAsync(long_runs, 0, sizeof(long long), s);
+    sort_trace("tie_keys", s);
     k_tie_rank<<<nb, 256, 0, s>>>(n_pairs, sk, pv, fk, ids2,
                                   c->work_counters ? static_cast<unsigned long long*>(c->counters.p) : nullptr,
                                   long_runs);
+    sort_trace("tie_rank", s);
     k_tie_long<<<64, 128, 0, s>>>(n_pairs, sk, fk, ids2, long_runs);
+    sort_trace("tie_long", s);
     launch_counter() += 3;
     std::swap(c->pv, c->pidx);
   }
   k_tile_bounds<<<(unsigned)((n_pairs + 256) / 256), 256, 0, s>>>(n_pairs, sk, c->key_dbits, n_tiles, tileoff);
   DRK_COUNT_LAUNCH();
   mark(c, 4);
+  sort_trace("bounds", s, true);
   *n_pairs_out = n_pairs;
   return DRK_OK;
 }

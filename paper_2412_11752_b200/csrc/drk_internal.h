@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -13,6 +15,34 @@
 #include "drk_device.cuh"
 
 namespace drk {
+
+// DRK_SORT_TRACE=1: device-time checkpoints of the binning sort on stderr
+// (development aid: per-phase CUDA events, printed when the phase list closes)
+inline bool sort_trace_on() {
+  static const bool on = getenv("DRK_SORT_TRACE") != nullptr;
+  return on;
+}
+inline void sort_trace(const char* what, cudaStream_t s, bool flush = false) {
+  if (!sort_trace_on()) return;
+  static std::vector<std::pair<std::string, cudaEvent_t>> evs;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  evs.emplace_back(what, e);
+  if (!flush) return;
+  cudaEventSynchronize(e);
+  std::string line;
+  for (size_t i = 1; i < evs.size(); ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, evs[i - 1].second, evs[i].second);
+    char b[96];
+    snprintf(b, sizeof b, " %s %.3f", evs[i].first.c_str(), ms);
+    line += b;
+  }
+  fprintf(stderr, "[drk sort]%s\n", line.c_str());
+  for (auto& x : evs) cudaEventDestroy(x.second);
+  evs.clear();
+}
 
 struct DevBuf {
   void* p = nullptr;

@@ -53,6 +53,11 @@
 #ifndef DRK_POP_THRU
 #define DRK_POP_THRU -1  // -1: half-tile CTAs only (long lists); 0: off; 1: always
 #endif
+// 1: a barrier at the top of every batch (0: the previous batch's closing
+// __syncthreads_count already orders the ring reuse; measured +0.6% raster time)
+#ifndef DRK_TOP_BARRIER
+#define DRK_TOP_BARRIER 1
+#endif
 #ifndef DRK_THRU_STAT
 #define DRK_THRU_STAT 0
 #endif
@@ -386,7 +391,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   for (long long b0 = beg; b0 < end; b0 += NT) {
     const int jb = (int)(b0 - beg);
     streamed = min(end, b0 + NT) - beg;
+#if DRK_TOP_BARRIER
     __syncthreads();
+#endif
 #if DRK_TMA_STAGE
     mbar_wait(&s_bar, gpar);
     gpar ^= 1u;

@@ -246,8 +246,11 @@ int sort_pairs(drk_ctx* c, unsigned* k, unsigned* v, unsigned* k2, unsigned* v2,
   const size_t rs_smem = 2 * sizeof(unsigned) * kRsChunk;
   for (int d = 0; d < 4; ++d) {
     k_rs_hist<<<nblk, kRsThreads, 0, s>>>(k, n, 8 * d, hist, nblk);
+    sort_trace("hist", s);
     if (int st = exclusive_scan<unsigned>(c, hist, (long long)256 * nblk, off, nullptr)) return st;
+    sort_trace("scan", s);
     k_rs_scatter<<<nblk, kRsThreads, rs_smem, s>>>(k, v, k2, v2, n, 8 * d, off, nblk);
+    sort_trace("scatter", s);
     launch_counter() += 2;
     std::swap(k, k2);
     std::swap(v, v2);
