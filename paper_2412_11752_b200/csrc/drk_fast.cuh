@@ -82,7 +82,11 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
 #define DRK_PSEUDO_ANGLE 1
 #endif
 // 1: alpha_entry loads the shape record's bracket-lookup angles and eta first
-// 1: the bracket lookup and its loads move ahead of the radius reject (forward)
+// 1: L1 prefetch of the SH coefficients once an entry passes the bracket bound
+#ifndef DRK_SH_PREFETCH
+#define DRK_SH_PREFETCH 0
+#endif
+// 1: the bracket lookup and its loads move ahead of the radius reject
 #ifndef DRK_EARLY_BRACKET
 #define DRK_EARLY_BRACKET 1  // measured: config-1 raster 20.09 -> 19.72 ms, config 2 11.10 -> 11.04 ms
 #endif
@@ -411,6 +415,17 @@ __device__ __forceinline__ void alpha_entry(const RasterParams& P, FastPixel& px
         return;
       }
     }
+#if DRK_SH_PREFETCH
+    if (!GRAD) {
+      // most entries past the bracket bound composite: pull their SH
+      // coefficients into L1 while the kernel value is evaluated
+      const char* shp = reinterpret_cast<const char*>(P.sh + (size_t)id * P.terms * 3);
+      const size_t bytes = (size_t)P.terms * 12;
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(shp));
+      if (bytes > 64) asm volatile("prefetch.global.L1 [%0];" ::"l"(shp + bytes - 4));
+      if (bytes > 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(shp + 128));
+    }
+#endif
     const float4 c0 = __ldg(reinterpret_cast<const float4*>(hd) + 2), c1 = __ldg(reinterpret_cast<const float4*>(hd) + 3);
     float ak, relk;
     KEvalF kf;
