@@ -83,6 +83,7 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
 #endif
 // 1: alpha_entry loads the shape record's bracket-lookup angles and eta first
 // 1: L1 prefetch of the SH coefficients once an entry passes the bracket bound
+// (measured: config-1 raster 19.73 -> 20.36 ms; off)
 #ifndef DRK_SH_PREFETCH
 #define DRK_SH_PREFETCH 0
 #endif
