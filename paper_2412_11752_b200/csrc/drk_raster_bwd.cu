@@ -40,10 +40,36 @@
 #ifndef DRK_BWD_SMEM
 #define DRK_BWD_SMEM 0  // measured on config 2: 47.8 ms with 1, 47.0 ms with 0 (groups average 18 lanes)
 #endif
+// 1: the SH-gradient group sums on the tensor cores (mma.sync tf32, 3 products
+// on hi / lo splits; parity green); 0: register transposes with shuffles.
+// Measured on config 2 fwd+bwd: 63.3 ms with 1 (padded basis rows, four
+// accumulator chains; 63.6 ms with one chain) vs 60.9 ms with 0 — the splits,
+// fragment loads and MMA latency cost more than the 47 shuffles they replace.
+#ifndef DRK_BWD_MMA
+#define DRK_BWD_MMA 0
+#endif
 namespace drk {
 
 namespace {
 constexpr int kGCols = 31;       // non-SH gradient columns
+// row stride padding of the per-pixel SH basis [16][NT + pad]: the MMA's A
+// fragments read 8 terms x 4 pixels per load (pad 4: 32 distinct banks)
+constexpr int kBasisPad = DRK_BWD_SMEM ? 1 : (DRK_BWD_MMA ? 4 : 0);
+
+__device__ __forceinline__ unsigned f32_to_tf32(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+// D += A B, m16n8k8, A row-major tf32 (4 regs), B col-major tf32 (2 regs), fp32 accumulators
+__device__ __forceinline__ void mma_tf32(float& d0, float& d1, float& d2, float& d3, const unsigned a[4],
+                                         const unsigned b[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d0), "+f"(d1), "+f"(d2), "+f"(d3)
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
 
 __device__ __forceinline__ int gcol_global(int c) {
   if (c < 12) return c;                   // centre 0..2, rotation 3..11 (row-major)
@@ -347,7 +373,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
   int* s_id = reinterpret_cast<int*>(ring + RING);
   // per-pixel SH basis [16][BS]; BS = NT + 1 so that one pixel's 16 terms sit in
   // distinct banks (the shared-memory group sums read them across lanes)
-  constexpr int BS = DRK_BWD_SMEM ? NT + 1 : NT;
+  constexpr int BS = NT + kBasisPad;
   float* s_basis_all = reinterpret_cast<float*>(s_id + RING);  // [16][BS]
   float* s_w_all = s_basis_all + 16 * BS;                     // [NT][4]: SH weights per lane
   float* s_row = s_w_all + 4 * NT;                            // [NT][kGCols]: gradient rows (odd stride: no bank conflicts)
@@ -390,7 +416,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
   {
     const int ta = P.opt.terms_active;
 #pragma unroll
-    for (int t = 0; t < 16; ++t) bas[t] = t < ta ? s_basis[t * NT] : 0.f;
+    for (int t = 0; t < 16; ++t) bas[t] = t < ta ? s_basis[t * BS] : 0.f;
   }
 #endif
   if (threadIdx.x == 0) {
@@ -598,6 +624,59 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
         }
         if (lane < kGCols && xv[0] != 0.f) atomicAdd(pg + gcol_global(lane), xv[0]);
       }
+#if DRK_BWD_MMA
+      // SH: d sh[t][c] = sum over the group's lanes k of basis_t(k) w_c(k), a
+      // [16 x 32] x [32 x 3] product on the tensor cores (mma.sync m16n8k8
+      // tf32, four k-chunks of 8 lanes; three products per chunk on hi / lo
+      // tf32 splits for fp32-level accuracy).  A = the pixels' basis (shared
+      // memory), B = the members' SH weights (s_w, zero outside the group);
+      // lane (g, tig) ends with D[g (+8)][2 tig (+1)].
+      {
+        const int wbase = threadIdx.x & ~31;
+        const int ta = P.opt.terms_active;
+        const int g = lane >> 2, tig = lane & 3;
+        // one accumulator set per k-chunk: four independent MMA chains of three
+        float dk[4][4];
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) dk[kc][0] = dk[kc][1] = dk[kc][2] = dk[kc][3] = 0.f;
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+          const int k0 = kc * 8 + tig, k1 = k0 + 4;
+          float a[4] = {s_basis_all[g * BS + wbase + k0], s_basis_all[(g + 8) * BS + wbase + k0],
+                        s_basis_all[g * BS + wbase + k1], s_basis_all[(g + 8) * BS + wbase + k1]};
+          float b[2] = {g < 3 && ((gm >> k0) & 1u) ? s_w_all[4 * (wbase + k0) + g] : 0.f,
+                        g < 3 && ((gm >> k1) & 1u) ? s_w_all[4 * (wbase + k1) + g] : 0.f};
+          unsigned ah[4], al[4], bh[2], bl[2];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            ah[i] = f32_to_tf32(a[i]);
+            al[i] = f32_to_tf32(a[i] - __uint_as_float(ah[i]));
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            bh[i] = f32_to_tf32(b[i]);
+            bl[i] = f32_to_tf32(b[i] - __uint_as_float(bh[i]));
+          }
+          mma_tf32(dk[kc][0], dk[kc][1], dk[kc][2], dk[kc][3], al, bh);
+          mma_tf32(dk[kc][0], dk[kc][1], dk[kc][2], dk[kc][3], ah, bl);
+          mma_tf32(dk[kc][0], dk[kc][1], dk[kc][2], dk[kc][3], ah, bh);
+        }
+        const float d0 = (dk[0][0] + dk[1][0]) + (dk[2][0] + dk[3][0]);
+        const float d1 = (dk[0][1] + dk[1][1]) + (dk[2][1] + dk[3][1]);
+        const float d2 = (dk[0][2] + dk[1][2]) + (dk[2][2] + dk[3][2]);
+        const float d3 = (dk[0][3] + dk[1][3]) + (dk[2][3] + dk[3][3]);
+        float* psh = pg + kGOffSh;
+        const int c0 = 2 * tig;
+        if (c0 < 3) {
+          if (g < ta && d0 != 0.f) atomicAdd(psh + 3 * g + c0, d0);
+          if (g + 8 < ta && d2 != 0.f) atomicAdd(psh + 3 * (g + 8) + c0, d2);
+        }
+        if (c0 + 1 < 3) {
+          if (g < ta && d1 != 0.f) atomicAdd(psh + 3 * g + c0 + 1, d1);
+          if (g + 8 < ta && d3 != 0.f) atomicAdd(psh + 3 * (g + 8) + c0 + 1, d3);
+        }
+      }
+#else
       // SH: component k = 3 t + ch (t < 16), value w_ch basis_t(pixel):
       // k = 0..31 by a 32-wide transpose, k = 32..47 by a 16-value halving
       // transpose (16 shuffles) that leaves value v in lanes 2v and 2v + 1
@@ -644,6 +723,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
           if (!(lane & 1) && xv[0] != 0.f) atomicAdd(pg + kGOffSh + 32 + (lane >> 1), xv[0]);
         }
       }
+#endif  // DRK_BWD_MMA
 #endif
     }
     __syncwarp();
@@ -793,7 +873,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
 }
 
 size_t raster_bwd_fast_smem(int nt) {
-  return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + (16 * (nt + DRK_BWD_SMEM) + (4 + kGCols) * nt) * sizeof(float);
+  return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + (16 * (nt + kBasisPad) + (4 + kGCols) * nt) * sizeof(float);
 }
 
 template <int NT, bool DET>
