@@ -630,7 +630,7 @@ __device__ __forceinline__ bool blend(const RasterParams& P, FastPixel& px, cons
   return true;
 }
 
-template <bool VALIDATE, int NT = kBatch, bool STATS = true>
+template <bool VALIDATE, int NT = kBatch, bool STATS = true, int RINGN = 2 * NT>
 __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, const float4* s_b4, const Rec* ring,
                                          const int* s_id, const TileConst& tc, long long beg, int ring_lo, int jr,
                                          int x, int y) {
@@ -638,7 +638,7 @@ __device__ __forceinline__ bool pop_eval(const RasterParams& P, FastPixel& px, c
   Rec R;
   int id;
   if (jr >= ring_lo) {
-    const int slot = jr & (2 * NT - 1);
+    const int slot = jr & (RINGN - 1);
     R = ring[slot];
     id = s_id[slot];
   } else {

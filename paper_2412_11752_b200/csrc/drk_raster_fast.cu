@@ -58,6 +58,16 @@
 #ifndef DRK_TOP_BARRIER
 #define DRK_TOP_BARRIER 1
 #endif
+// list entries per staged batch (the ring holds two) of the whole-tile and the
+// half-tile kernel: one per thread, or fewer for less shared memory (more L1
+// for the shape and SH records) at more batch barriers.  Measured, config-1
+// raster: 256 -> 128 entries 19.73 -> 19.60 ms.
+#ifndef DRK_BATCH256
+#define DRK_BATCH256 128
+#endif
+#ifndef DRK_BATCH128
+#define DRK_BATCH128 128
+#endif
 #ifndef DRK_THRU_STAT
 #define DRK_THRU_STAT 0
 #endif
@@ -153,13 +163,14 @@ __device__ __forceinline__ void write_pixel(const RasterParams& P, const FastPix
 // release of SM resources when a tile's pixels saturate unevenly (long lists).
 template <bool VALIDATE, int NT, bool STATS>
 __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_constant__ RasterParams P) {
-  constexpr int RING = 2 * NT;
+  constexpr int BATCH = NT == 256 ? DRK_BATCH256 : DRK_BATCH128;  // list entries staged per batch
+  constexpr int RING = 2 * BATCH;
   extern __shared__ float4 dyn[];
   Rec* ring = reinterpret_cast<Rec*>(dyn);
   int* s_id = reinterpret_cast<int*>(ring + RING);
   float4* s_b4 = reinterpret_cast<float4*>(s_id + RING) + threadIdx.x;  // [4][NT] float4, this thread's column
 #if DRK_TMA_STAGE
-  Geo* s_geo = reinterpret_cast<Geo*>(reinterpret_cast<float4*>(s_id + RING) + 4 * NT);  // [NT]: next batch's Geo
+  Geo* s_geo = reinterpret_cast<Geo*>(reinterpret_cast<float4*>(s_id + RING) + 4 * NT);  // [BATCH]: next batch's Geo
   __shared__ unsigned long long s_bar;
 #endif
   __shared__ unsigned s_ddmax;
@@ -286,7 +297,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
         chi[kCacheCap - 1] = hi;
         cj[kCacheCap - 1] = jr;
         maxhi = hi;
-        return pop_eval<VALIDATE, NT, STATS>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y);
+        return pop_eval<VALIDATE, NT, STATS, RING>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y);
       }
 #endif
       bool le[kCacheCap];
@@ -364,7 +375,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
       for (int q = 1; q < kCacheCap; ++q) maxhi = fmaxf(maxhi, chi[q]);
 #endif
     }
-    return pop_eval<VALIDATE, NT, STATS>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y);
+    return pop_eval<VALIDATE, NT, STATS, RING>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y);
   };
 #if DRK_TMA_STAGE
   // batch b's Geo records arrive in s_geo by bulk copies issued while batch b-1
@@ -374,7 +385,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   int my_id = 0;
   bool pending = false;
   auto prefetch = [&](long long b0n) {
-    const int cntn = (int)min((long long)NT, end - b0n);
+    const int cntn = (int)min((long long)BATCH, end - b0n);
     if (threadIdx.x == 0) mbar_expect_tx(&s_bar, (unsigned)(cntn * sizeof(Geo)));
     fence_proxy_async();  // s_geo was last read by the generic proxy
     if ((int)threadIdx.x < cntn) {
@@ -388,9 +399,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
   if (beg < end) prefetch(beg);
 #endif
   long long streamed = 0;
-  for (long long b0 = beg; b0 < end; b0 += NT) {
+  for (long long b0 = beg; b0 < end; b0 += BATCH) {
     const int jb = (int)(b0 - beg);
-    streamed = min(end, b0 + NT) - beg;
+    streamed = min(end, b0 + BATCH) - beg;
 #if DRK_TOP_BARRIER
     __syncthreads();
 #endif
@@ -400,18 +411,18 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
     pending = false;
     {
       const long long j = b0 + threadIdx.x;
-      if (j < end) {
+      if ((int)threadIdx.x < BATCH && j < end) {
         const int slot = (jb + threadIdx.x) & (RING - 1);
         stage_record_from(P, s_geo[threadIdx.x], tc, ring[slot]);
         s_id[slot] = my_id;
       }
     }
     __syncthreads();
-    if (b0 + NT < end) prefetch(b0 + NT);
+    if (b0 + BATCH < end) prefetch(b0 + BATCH);
 #else
     {
       const long long j = b0 + threadIdx.x;
-      if (j < end) {
+      if ((int)threadIdx.x < BATCH && j < end) {
         const int id = P.lid[j];
         const int slot = (jb + threadIdx.x) & (RING - 1);
         stage_record(P, id, tc, ring[slot]);
@@ -420,8 +431,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
     }
     __syncthreads();
 #endif
-    ring_lo = jb >= NT ? jb - NT : 0;
-    const int cnt = (int)min((long long)NT, end - b0);
+    ring_lo = jb >= BATCH ? jb - BATCH : 0;
+    const int cnt = (int)min((long long)BATCH, end - b0);
     if (!done) {
 #if DRK_ISECT2
       // two candidates per iteration: both ray-plane intersections first
@@ -471,7 +482,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_raster_fast(const __grid_const
       cj[q] = cj[q + 1];
     }
     --csz;
-    if (!pop_eval<VALIDATE, NT, STATS>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y))
+    if (!pop_eval<VALIDATE, NT, STATS, RING>(P, px, s_b4, ring, s_id, tc, beg, ring_lo, pj, x, y))
       done = true;
   }
   // counters: one atomic per warp and counter
@@ -565,7 +576,9 @@ void launch_tile_order_keys(int n, int tiles_x, int band_rows, const long long* 
 }
 
 size_t raster_fast_smem(int nt) {
-  return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + 16 * nt * sizeof(float) + (DRK_TMA_STAGE ? nt * sizeof(Geo) : 0);
+  const int batch = nt == 256 ? DRK_BATCH256 : DRK_BATCH128;
+  return (size_t)2 * batch * (sizeof(Rec) + sizeof(int)) + 16 * nt * sizeof(float) +
+         (DRK_TMA_STAGE ? batch * sizeof(Geo) : 0);
 }
 
 // Half-tile CTAs pay off once tile lists are long (measured: config 2 / 3 with
