@@ -60,13 +60,15 @@
 #endif
 // list entries per staged batch (the ring holds two) of the whole-tile and the
 // half-tile kernel: one per thread, or fewer for less shared memory (more L1
-// for the shape and SH records) at more batch barriers.  Measured, config-1
-// raster: 256 -> 128 entries 19.73 -> 19.60 ms.
+// for the shape and SH records) at more batch barriers.  Measured: whole-tile
+// 256 -> 128 entries, config-1 raster 19.73 -> 19.60 ms (64: 20.18 ms);
+// half-tile 128 -> 64 entries, config-2 raster 10.96 -> 10.82 ms, config 3
+// 34.4 -> 34.0 ms.
 #ifndef DRK_BATCH256
 #define DRK_BATCH256 128
 #endif
 #ifndef DRK_BATCH128
-#define DRK_BATCH128 128
+#define DRK_BATCH128 64
 #endif
 #ifndef DRK_THRU_STAT
 #define DRK_THRU_STAT 0
