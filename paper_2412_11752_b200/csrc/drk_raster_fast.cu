@@ -2,10 +2,10 @@
 // raster.cpp:267-430) with every per-candidate quantity in fp32 and exact
 // fp64 fallbacks wherever a discrete decision falls inside its error bound.
 //
-// One CTA per 16x16 tile, one thread per pixel.  Tile-list entries are staged
-// 256 at a time into a 512-entry shared-memory ring (the current and the
-// previous batch) as an 84-byte fp32 record computed once per (entry, tile)
-// in fp64 (stage_record):
+// One CTA per 16x16 tile (or per half tile for long lists), one thread per
+// pixel.  Tile-list entries are staged DRK_BATCH256 / DRK_BATCH128 at a time
+// into a two-batch shared-memory ring (the current and the previous batch) as
+// a 96-byte fp32 record computed once per (entry, tile) in fp64 (stage_record):
 //
 //   r0 = (R_z, R_z . d0)                     ray-plane denominator at the tile ray d0
 //   r1 = (G_u, N_u(d0)), r2 = (G_v, N_v(d0)) tangent-coordinate numerators
