@@ -37,6 +37,13 @@
 #ifndef DRK_BWD_THRU
 #define DRK_BWD_THRU 1  // pop-through fast path (config 2 backward -1%)
 #endif
+// list entries per staged batch (0: one per thread); the ring holds two.
+// Measured, config-2 fwd+bwd: 60.7 ms with one per thread (128), 59.3 ms with
+// 64, 59.8 ms with 32 (the smaller ring leaves more L1 to the shape, SH and
+// frame records)
+#ifndef DRK_BWD_BATCH
+#define DRK_BWD_BATCH 64
+#endif
 #ifndef DRK_BWD_SMEM
 #define DRK_BWD_SMEM 0  // measured on config 2: 47.8 ms with 1, 47.0 ms with 0 (groups average 18 lanes)
 #endif
@@ -367,7 +374,8 @@ __device__ __noinline__ void record_grad_f64(const RasterParams& P, const BwdPix
 template <int NT, bool DET>
 __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MINB) k_raster_bwd_fast(
     const __grid_constant__ RasterParams P) {
-  constexpr int RING = 2 * NT;
+  constexpr int BATCH = DRK_BWD_BATCH > 0 && DRK_BWD_BATCH < NT ? DRK_BWD_BATCH : NT;  // entries per staged batch
+  constexpr int RING = 2 * BATCH;
   extern __shared__ float4 dyn[];
   Rec* ring = reinterpret_cast<Rec*>(dyn);
   int* s_id = reinterpret_cast<int*>(ring + RING);
@@ -729,12 +737,12 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
     __syncwarp();
   };
 
-  for (long long b0 = beg; b0 < end; b0 += NT) {
+  for (long long b0 = beg; b0 < end; b0 += BATCH) {
     const int jb = (int)(b0 - beg);
     __syncthreads();
     {
       const long long j = b0 + threadIdx.x;
-      if (j < end) {
+      if ((int)threadIdx.x < BATCH && j < end) {
         const int id = P.lid[j];
         const int slot = (jb + threadIdx.x) & (RING - 1);
         stage_record(P, id, tc, ring[slot]);
@@ -742,8 +750,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
       }
     }
     __syncthreads();
-    ring_lo = jb >= NT ? jb - NT : 0;
-    const int cnt = (int)min((long long)NT, end - b0);
+    ring_lo = jb >= BATCH ? jb - BATCH : 0;
+    const int cnt = (int)min((long long)BATCH, end - b0);
     if (__any_sync(FULL, !done)) {
       for (int c = 0; c < cnt; ++c) {
         bool want = false;
@@ -873,7 +881,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? DRK_BWD_MINB128 : DRK_BWDF_MIN
 }
 
 size_t raster_bwd_fast_smem(int nt) {
-  return (size_t)2 * nt * (sizeof(Rec) + sizeof(int)) + (16 * (nt + kBasisPad) + (4 + kGCols) * nt) * sizeof(float);
+  const int batch = DRK_BWD_BATCH > 0 && DRK_BWD_BATCH < nt ? DRK_BWD_BATCH : nt;
+  return (size_t)2 * batch * (sizeof(Rec) + sizeof(int)) + (16 * (nt + kBasisPad) + (4 + kGCols) * nt) * sizeof(float);
 }
 
 template <int NT, bool DET>
