@@ -63,7 +63,7 @@
 // for the shape and SH records) at more batch barriers.  Measured: whole-tile
 // 256 -> 128 entries, config-1 raster 19.73 -> 19.60 ms (64: 20.18 ms);
 // half-tile 128 -> 64 entries, config-2 raster 10.96 -> 10.82 ms, config 3
-// 34.4 -> 34.0 ms.
+// 34.4 -> 34.0 ms (32: config 2 11.1 ms, config 3 34.7 ms).
 #ifndef DRK_BATCH256
 #define DRK_BATCH256 128
 #endif
